@@ -1,0 +1,275 @@
+/*
+ * dagrt.h -- C ABI of the run-time DAG scheduler (libdagrt.so).
+ *
+ * B200-native re-design of the scheduler of arXiv 2012.09646, "DAG-based
+ * Scheduling with Resource Sharing for Multi-task Applications in a Polyglot
+ * GPU Runtime".  Citations "Lnnn" are lines of the paper text.
+ *
+ * The user registers device arrays, declares kernels whose pointer arguments
+ * are const (read-only) or mutable, launches kernels and touches arrays from
+ * the host, writing host code "as if it were run sequentially, with no
+ * explicit mention of synchronization points or streams" (L528-530).  The
+ * library infers the computation DAG at run time from the read/write argument
+ * sets (L386-430, L490-491), assigns CUDA streams (L570-582, L647-654), wires
+ * cudaEvent / cudaStreamWaitEvent edges (L546-553), keeps the host-sync
+ * frontier of active computations (L553-558) and overlaps host<->device
+ * transfers with compute on side streams (L356-366, L662-664).
+ *
+ * Conventions for every call:
+ *  - returns dagrt_status: 0 = DAGRT_OK, < 0 = error (enum below); no C++
+ *    exception or longjmp ever crosses this boundary;
+ *  - on error, dagrt_last_error(ctx) returns a NUL-terminated message owned by
+ *    the context (valid until the next call on it);
+ *  - a CUDA error makes the context sticky-failed: every later call returns
+ *    DAGRT_ECUDA until dagrt_destroy;
+ *  - a context is bound to one device and is NOT thread-safe (one per host
+ *    thread; independent contexts on different devices run in parallel);
+ *  - all device and pinned host memory is owned by the CALLER; the library
+ *    never allocates or frees user data.  It owns only the streams, events
+ *    and graphs it creates, released by dagrt_destroy.
+ */
+#ifndef DAGRT_H
+#define DAGRT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dagrt_status;
+enum {
+  DAGRT_OK = 0,
+  DAGRT_EINVAL = -1,    /* bad argument (null pointer, bad size, range out of bounds) */
+  DAGRT_ENOTFOUND = -2, /* unknown or stale array / kernel handle or name */
+  DAGRT_EALIAS = -3,    /* device range overlaps a registered array (no aliasing, L400-404) */
+  DAGRT_ESIG = -4,      /* signature parse error or argument kind/count mismatch */
+  DAGRT_ESTATE = -5,    /* call not valid in the current state (e.g. map without mirror) */
+  DAGRT_ECUDA = -6,     /* CUDA runtime error (sticky) */
+  DAGRT_ENOMEM = -7     /* host allocation failure */
+};
+
+typedef struct dagrt_ctx_s* dagrt_ctx;
+/* Array handle: {index:32 | generation:32}; 0 is never a valid handle. */
+typedef uint64_t dagrt_array;
+typedef uint32_t dagrt_kernel;
+
+/* Scheduling policy (L559-569): the original GrCUDA scheduler is serial and
+ * synchronous (the baseline); the paper's scheduler is parallel and async. */
+enum { DAGRT_PARALLEL_ASYNC = 0, DAGRT_SERIAL_SYNC = 1 };
+/* Backend: the CUDA runtime, or a recorder that performs no device work
+ * (for scheduler tests on machines without a GPU). */
+enum { DAGRT_BACKEND_CUDA = 0, DAGRT_BACKEND_RECORD = 1 };
+/* Host access modes for dagrt_host_map. */
+enum { DAGRT_R = 1, DAGRT_W = 2, DAGRT_RW = 3 };
+
+typedef struct {
+  int32_t policy;      /* DAGRT_PARALLEL_ASYNC or DAGRT_SERIAL_SYNC */
+  int32_t prefetch;    /* 1: H2D of host-newer read arguments on an in-order side copy
+                          stream, overlapped with compute (L356-366, L662-664);
+                          0: the copy is issued on the consumer's own stream */
+  int32_t max_streams; /* 0 = unlimited; otherwise cap on compute streams */
+  int32_t record_dag;  /* 1: keep vertices/edges/trace for dagrt_dag_export/dagrt_trace_export */
+  int32_t backend;     /* DAGRT_BACKEND_CUDA or DAGRT_BACKEND_RECORD */
+} dagrt_config;
+
+typedef struct { uint32_t x, y, z; } dagrt_dim3;
+
+/* One kernel argument: an array handle for pointer parameters, else a scalar
+ * passed by value (scalars are "passed by copy, ignored for dependencies",
+ * Fig. 4 note L450-451). */
+typedef union {
+  dagrt_array array;
+  int32_t i32;
+  int64_t i64;
+  float f32;
+  double f64;
+} dagrt_arg;
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on CUDA device `device` (ignored by the RECORD backend).
+ * cfg may be NULL (defaults: parallel-async, prefetch on, unlimited streams,
+ * no DAG recording, CUDA backend).  *out receives the context. */
+dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out);
+/* Drain all work (full barrier), free the library's streams/events/graphs
+ * and the context.  ctx may be NULL.  Use after destroy is undefined. */
+dagrt_status dagrt_destroy(dagrt_ctx ctx);
+/* Message for the last non-OK status of ctx ("" if none). */
+const char* dagrt_last_error(dagrt_ctx ctx);
+
+/* ---------------------------------------------------------------- arrays */
+
+/* Register `bytes` of caller-owned device memory at `dev` as one array
+ * (GrCUDA's managed array, L400-404, L505-507).  `host_pinned` (nullable)
+ * is an optional caller-owned pinned host mirror of the same size used for
+ * host accesses and transfers.  The array starts with the device copy valid
+ * (the mirror is considered stale).  Overlap with a registered array ->
+ * DAGRT_EALIAS.  bytes may be 0.  *out receives the handle. */
+dagrt_status dagrt_array_register(dagrt_ctx ctx, void* dev, void* host_pinned, size_t bytes,
+                                  dagrt_array* out);
+/* Wait for the array's in-flight users, then forget it (the caller frees the
+ * memory afterwards).  The handle becomes stale (DAGRT_ENOTFOUND). */
+dagrt_status dagrt_array_unregister(dagrt_ctx ctx, dagrt_array a);
+/* Device pointer of a registered array (for the caller's own bookkeeping). */
+dagrt_status dagrt_array_device_ptr(dagrt_ctx ctx, dagrt_array a, void** dev);
+
+/* ---------------------------------------------------------------- kernels */
+
+/* Declare a kernel: `global_fn` is a __global__ function symbol compiled for
+ * sm_100a (may be NULL with the RECORD backend), `name` a label, `signature`
+ * one comma-separated token per parameter (L431-433, L668-677):
+ *   "const ptr" | "in ptr"   read-only pointer   (prefetched)
+ *   "ptr" | "inout ptr"      modified pointer    (prefetched)   -- unannotated = modified
+ *   "out ptr"                modified pointer, overwritten entirely (not prefetched)
+ *   "sint32" | "sint64" | "float" | "double"   scalar by value, no dependency
+ * At most 16 parameters.  Parse error -> DAGRT_ESIG. */
+dagrt_status dagrt_kernel_register(dagrt_ctx ctx, const void* global_fn, const char* name,
+                                   const char* signature, dagrt_kernel* out);
+/* Find a kernel by name: user-registered ones, then the built-in sm_100a
+ * benchmark kernels of the library (list: dagrt_builtin_count/_name). */
+dagrt_status dagrt_kernel_lookup(dagrt_ctx ctx, const char* name, dagrt_kernel* out);
+/* Parameter kinds of kernel k: kinds[i] = 0 sint32, 1 sint64, 2 const ptr,
+ * 3 mutable ptr (prefetched), 4 out ptr, 5 float, 6 double.
+ * *n: capacity in, count out. */
+dagrt_status dagrt_kernel_signature(dagrt_ctx ctx, dagrt_kernel k, int32_t* kinds, int32_t* n);
+int32_t dagrt_builtin_count(void);
+const char* dagrt_builtin_name(int32_t i);
+const char* dagrt_builtin_signature(int32_t i);
+
+/* ---------------------------------------------------------------- launch */
+
+/* Launch kernel k with `nargs` arguments (count and kinds must match the
+ * signature, else DAGRT_ESIG).  Never blocks the host under the parallel
+ * policy (L564-569): builds the computational element (L388-396), computes
+ * its parents from the dependency sets of active computations (L408-431,
+ * L490-491), picks a stream (L570-582, L647-650), makes the stream wait on
+ * the events of parents running on other streams (L546-553), prefetches
+ * host-newer read arguments on the copy stream (L356-366), launches, and
+ * records the vertex's event.  Under DAGRT_SERIAL_SYNC the launch and any
+ * copy run on one stream, each followed by a stream synchronize (L560-569). */
+dagrt_status dagrt_launch(dagrt_ctx ctx, dagrt_kernel k, dagrt_dim3 grid, dagrt_dim3 block,
+                          uint32_t smem, const dagrt_arg* args, int32_t nargs);
+
+/* ---------------------------------------------------------------- host access */
+
+/* Host read of bytes [off, off+bytes) of array a into dst (L505-516): if the
+ * access conflicts with active GPU work it becomes a DAG vertex and the host
+ * waits on exactly the conflicting computations' events, retiring them and
+ * their ancestors (L526-528, L553-556); then the range is copied D2H if the
+ * device copy is newer (via the mirror when one is registered).  A
+ * non-conflicting access runs immediately and is not recorded (L512-516). */
+dagrt_status dagrt_host_read(dagrt_ctx ctx, dagrt_array a, size_t off, size_t bytes, void* dst);
+/* Host write of [off, off+bytes) from src: waits on the active readers since
+ * the last writer, else on the last writer (reading D6), then writes the
+ * mirror (marking the host copy newer; the next GPU reader pulls it) or,
+ * without a mirror, copies H2D synchronously.  A partial write of a
+ * device-newer mirrored array first pulls the whole array D2H. */
+dagrt_status dagrt_host_write(dagrt_ctx ctx, dagrt_array a, size_t off, size_t bytes,
+                              const void* src);
+/* Whole-array host access through the pinned mirror (DAGRT_ESTATE without
+ * one): access R syncs like host_read and makes the mirror current; W syncs
+ * like host_write and marks the host copy newer (the caller writes through
+ * *host_ptr until dagrt_host_unmap).  RW does both. */
+dagrt_status dagrt_host_map(dagrt_ctx ctx, dagrt_array a, int32_t access, void** host_ptr);
+dagrt_status dagrt_host_unmap(dagrt_ctx ctx, dagrt_array a);
+/* Full barrier (build-only API, reading D6b): waits for all streams and
+ * retires every active computation.  Records no vertex. */
+dagrt_status dagrt_sync(dagrt_ctx ctx);
+
+/* ---------------------------------------------------------------- introspection */
+
+typedef struct {
+  uint32_t id;     /* vertex id = order of recording */
+  uint32_t kind;   /* 0 kernel, 1 host access */
+  uint32_t kernel; /* kernel handle (kind 0) */
+  int32_t stream;  /* compute stream index (0-based, creation order); -1 for host */
+  dagrt_array array; /* accessed array (kind 1), else 0 */
+} dagrt_vertex_info;
+
+typedef struct {
+  uint32_t parent, child;
+  dagrt_array array; /* the argument causing the dependency (one row per label, L218-220) */
+} dagrt_edge_info;
+
+/* Copy out the DAG recorded since the last dagrt_dag_clear (needs
+ * record_dag=1).  *nv / *ne: capacity in, count out; NULL arrays query the
+ * counts; insufficient capacity -> DAGRT_EINVAL with the counts set.  The
+ * scheduler itself only ever keeps the active frontier (L495-501). */
+dagrt_status dagrt_dag_export(dagrt_ctx ctx, dagrt_vertex_info* v, uint32_t* nv,
+                              dagrt_edge_info* e, uint32_t* ne);
+dagrt_status dagrt_dag_clear(dagrt_ctx ctx);
+
+/* Backend operation trace (record_dag=1), for event-wiring and transfer checks. */
+enum {
+  DAGRT_OP_LAUNCH = 1,      /* a = vertex, b = kernel, stream */
+  DAGRT_OP_RECORD = 2,      /* a = vertex, stream: event of vertex a recorded */
+  DAGRT_OP_WAIT = 3,        /* stream waits on the event of vertex a */
+  DAGRT_OP_H2D = 4,         /* a = array index, bytes, stream (-2 = copy stream) */
+  DAGRT_OP_D2H = 5,         /* a = array index, bytes */
+  DAGRT_OP_EVENT_SYNC = 6,  /* host waits on the event of vertex a */
+  DAGRT_OP_STREAM_SYNC = 7, /* host waits on stream */
+  DAGRT_OP_WAIT_COPY = 8    /* stream waits on the H2D copy event of array a */
+};
+typedef struct {
+  int32_t op;
+  int32_t stream; /* compute stream index, -2 copy stream, -1 none */
+  int64_t a, b;
+  uint64_t bytes;
+} dagrt_trace_op;
+dagrt_status dagrt_trace_export(dagrt_ctx ctx, dagrt_trace_op* ops, uint32_t* n);
+
+typedef struct {
+  uint64_t launches;           /* kernel launches */
+  uint64_t vertices;           /* recorded vertices (kernels + conflicting host accesses) */
+  uint64_t host_vertices;
+  uint64_t edges;              /* (parent, child) pairs */
+  uint64_t cross_stream_waits; /* cudaStreamWaitEvent on vertex events */
+  uint64_t copy_waits;         /* cudaStreamWaitEvent on copy events */
+  uint64_t streams;            /* compute streams created */
+  uint64_t events_created;
+  uint64_t h2d_bytes, d2h_bytes, h2d_copies, d2h_copies;
+  uint64_t host_syncs;         /* host-blocking waits (event or stream) */
+  uint64_t sched_ns;           /* host ns spent inside dagrt_launch */
+} dagrt_stats_t;
+/* Copy min(size, sizeof(dagrt_stats_t)) bytes of the counters to out. */
+dagrt_status dagrt_stats(dagrt_ctx ctx, void* out, size_t size);
+dagrt_status dagrt_stats_reset(dagrt_ctx ctx);
+/* Number of compute streams the context has created. */
+dagrt_status dagrt_stream_count(dagrt_ctx ctx, int32_t* n);
+/* The cudaStream_t of compute stream i (as void*), e.g. for profiling marks. */
+dagrt_status dagrt_stream_handle(dagrt_ctx ctx, int32_t i, void** stream);
+
+/* ---------------------------------------------------------------- baselines */
+
+/* Direct launch on a caller-given cudaStream_t with no scheduling at all
+ * (arrays resolved to device pointers only).  For the hand-written schedules
+ * the paper compares against (CUDA Graphs, L1057-1070). */
+dagrt_status dagrt_launch_raw(dagrt_ctx ctx, dagrt_kernel k, dagrt_dim3 grid, dagrt_dim3 block,
+                              uint32_t smem, const dagrt_arg* args, int32_t nargs, void* stream);
+
+/* Hand-built CUDA graph with MANUAL dependencies ("Graph API + manual
+ * dependencies", L1062-1067): nodes are added with the explicit list of
+ * earlier node ids they depend on; nothing is inferred. */
+typedef struct dagrt_graph_s* dagrt_graph;
+dagrt_status dagrt_graph_create(dagrt_ctx ctx, dagrt_graph* g);
+/* Kernel node; deps are node ids returned by earlier add calls. */
+dagrt_status dagrt_graph_add_kernel(dagrt_ctx ctx, dagrt_graph g, dagrt_kernel k, dagrt_dim3 grid,
+                                    dagrt_dim3 block, uint32_t smem, const dagrt_arg* args,
+                                    int32_t nargs, const uint32_t* deps, int32_t ndeps,
+                                    uint32_t* node);
+/* Copy node between an array's device memory and its pinned mirror:
+ * dir 0 = H2D, 1 = D2H, bytes [off, off+bytes). */
+dagrt_status dagrt_graph_add_copy(dagrt_ctx ctx, dagrt_graph g, dagrt_array a, int32_t dir,
+                                  size_t off, size_t bytes, const uint32_t* deps, int32_t ndeps,
+                                  uint32_t* node);
+dagrt_status dagrt_graph_instantiate(dagrt_ctx ctx, dagrt_graph g);
+/* Launch the instantiated graph on the context's graph stream and wait for it. */
+dagrt_status dagrt_graph_run(dagrt_ctx ctx, dagrt_graph g, int32_t wait);
+dagrt_status dagrt_graph_destroy(dagrt_ctx ctx, dagrt_graph g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAGRT_H */

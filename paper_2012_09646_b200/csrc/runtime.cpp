@@ -1,0 +1,1113 @@
+// libdagrt -- run-time DAG scheduler core (C++17), behind the C ABI of
+// include/dagrt.h.  B200-native re-design of the scheduler of arXiv
+// 2012.09646 (§IV); readings D1-D8 in DESIGN.md.
+//
+// Per launch (Fig. 5 steps 1-6, L630-639):
+//   1 convert the invocation to a computational element (vertex)    L388-396
+//   2-3 dependency inference from the per-array table:              L408-431, L490-491
+//        read  -> last writer, if active                 (Fig. 3 A, C)
+//        write -> active readers since the last writer, else the last
+//                 writer if active                        (Fig. 3 B; D1)
+//   4 stream: parent's stream if that parent is its tail, else the first
+//     stream with no active vertex (FIFO), else a new stream  L570-582, L647-650
+//   5 cudaStreamWaitEvent on parents living on other streams   L546-553
+//     + prefetch of host-newer read args on the copy stream    L356-366, L662-664
+//   6 launch, record the vertex event; return without blocking L564-569
+// Host accesses (L505-530) wait on exactly the conflicting vertices' events
+// and retire them and their DAG ancestors (L553-556; reading D4/D5).
+//
+// The scheduler keeps only the active frontier: per-array {last writer,
+// readers since it}, per-vertex {active, stream, event, parents} -- parents
+// are kept only to close retirement over ancestors and are dropped whenever
+// the frontier empties.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dagrt.h"
+#include "builtin.h"
+
+namespace dagrt {
+
+// ------------------------------------------------------------ builtin registry
+static std::vector<Builtin>& registry() {
+  static std::vector<Builtin> r;
+  return r;
+}
+int register_builtins(const Builtin* t, int n) {
+  for (int i = 0; i < n; ++i) registry().push_back(t[i]);
+  return n;
+}
+int builtin_count() { return (int)registry().size(); }
+const Builtin* builtin_at(int i) {
+  return (i >= 0 && i < builtin_count()) ? &registry()[i] : nullptr;
+}
+
+// ------------------------------------------------------------ backends
+// The CUDA runtime manager of Fig. 5 (L543-545, L590): the only place that
+// talks to CUDA.  The recorder implements the same interface without a GPU.
+struct Backend {
+  virtual ~Backend() {}
+  virtual cudaError_t stream_create(void** s) = 0;
+  virtual cudaError_t stream_destroy(void* s) = 0;
+  virtual cudaError_t event_create(void** e) = 0;
+  virtual cudaError_t event_destroy(void* e) = 0;
+  virtual cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
+                             bool coop) = 0;
+  virtual cudaError_t record(void* e, void* s) = 0;
+  virtual cudaError_t wait(void* s, void* e) = 0;
+  virtual cudaError_t event_sync(void* e) = 0;
+  virtual cudaError_t stream_sync(void* s) = 0;
+  virtual cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k,
+                                 void* s) = 0;
+  virtual bool real() const = 0;
+};
+
+struct CudaBackend final : Backend {
+  cudaError_t stream_create(void** s) override {
+    return cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(s), cudaStreamNonBlocking);
+  }
+  cudaError_t stream_destroy(void* s) override { return cudaStreamDestroy((cudaStream_t)s); }
+  cudaError_t event_create(void** e) override {
+    return cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(e), cudaEventDisableTiming);
+  }
+  cudaError_t event_destroy(void* e) override { return cudaEventDestroy((cudaEvent_t)e); }
+  cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
+                     bool coop) override {
+    if (coop) return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
+    return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
+  }
+  cudaError_t record(void* e, void* s) override {
+    return cudaEventRecord((cudaEvent_t)e, (cudaStream_t)s);
+  }
+  cudaError_t wait(void* s, void* e) override {
+    return cudaStreamWaitEvent((cudaStream_t)s, (cudaEvent_t)e, 0);
+  }
+  cudaError_t event_sync(void* e) override { return cudaEventSynchronize((cudaEvent_t)e); }
+  cudaError_t stream_sync(void* s) override { return cudaStreamSynchronize((cudaStream_t)s); }
+  cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k,
+                         void* s) override {
+    return cudaMemcpyAsync(dst, src, n, k, (cudaStream_t)s);
+  }
+  bool real() const override { return true; }
+};
+
+struct RecordBackend final : Backend {
+  uintptr_t next = 0x1000;
+  cudaError_t stream_create(void** s) override { *s = (void*)(next += 16); return cudaSuccess; }
+  cudaError_t stream_destroy(void*) override { return cudaSuccess; }
+  cudaError_t event_create(void** e) override { *e = (void*)(next += 16); return cudaSuccess; }
+  cudaError_t event_destroy(void*) override { return cudaSuccess; }
+  cudaError_t launch(const void*, dim3, dim3, void**, size_t, void*, bool) override {
+    return cudaSuccess;
+  }
+  cudaError_t record(void*, void*) override { return cudaSuccess; }
+  cudaError_t wait(void*, void*) override { return cudaSuccess; }
+  cudaError_t event_sync(void*) override { return cudaSuccess; }
+  cudaError_t stream_sync(void*) override { return cudaSuccess; }
+  cudaError_t copy_async(void*, const void*, size_t, cudaMemcpyKind, void*) override {
+    return cudaSuccess;
+  }
+  bool real() const override { return false; }
+};
+
+// ------------------------------------------------------------ context state
+enum : uint8_t { P_I32 = 0, P_I64 = 1, P_CONST = 2, P_INOUT = 3, P_OUT = 4, P_F32 = 5, P_F64 = 6 };
+inline bool is_ptr(uint8_t k) { return k >= P_CONST && k <= P_OUT; }
+enum : uint8_t { COH_DEVICE = 0, COH_HOST = 1, COH_BOTH = 2 };  // which copy is newest
+
+constexpr int kMaxArgs = 16;
+
+struct KernelRec {
+  std::string name;
+  const void* fn;
+  int32_t nparams;
+  uint8_t kind[kMaxArgs];
+  bool coop;
+};
+
+struct ArrayRec {
+  char* dev = nullptr;
+  char* host = nullptr;
+  size_t bytes = 0;
+  uint32_t gen = 0;
+  bool live = false;
+  bool mapped = false;
+  int64_t last_writer = -1;         // vertex id of the last kernel writer, -1 = none/host
+  std::vector<uint32_t> readers;    // readers since the last writer (pruned lazily)
+  uint8_t coh = COH_DEVICE;
+  bool h2d_pending = false;         // an H2D prefetch whose consumer is still active
+  void* h2d_ev = nullptr;
+  int64_t h2d_consumer = -1;
+  int32_t h2d_stream = -1;          // stream of the consumer (already ordered after the copy)
+};
+
+struct VertexRec {
+  uint8_t active;
+  uint8_t kind;   // 0 kernel, 1 host
+  int32_t stream;
+  void* ev;
+  uint32_t pbeg, pcnt;  // parents in parent_pool
+};
+
+struct StreamRec {
+  void* s;
+  int64_t tail;    // last enqueued vertex
+  int32_t nactive; // active vertices on this stream
+};
+
+struct GraphRec {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> nodes;
+};
+
+}  // namespace dagrt
+
+using namespace dagrt;
+
+struct dagrt_graph_s {
+  GraphRec r;
+};
+
+struct dagrt_ctx_s {
+  dagrt_config cfg{};
+  int device = 0;
+  Backend* be = nullptr;
+  std::string err;
+  bool sticky = false;
+
+  std::vector<KernelRec> kernels;
+  std::vector<ArrayRec> arrays;       // index 0 unused (handle 0 invalid)
+  std::vector<VertexRec> vertices;
+  std::vector<uint32_t> parent_pool;
+  std::vector<StreamRec> streams;
+  std::vector<void*> event_pool;      // free events
+  std::vector<void*> all_events;
+  int64_t n_active = 0;
+  void* copy_stream = nullptr;        // in-order H2D side stream
+  void* d2h_stream = nullptr;         // in-order D2H side stream
+  void* graph_stream = nullptr;
+  void* serial_stream = nullptr;
+  std::vector<dagrt_graph_s*> graphs;
+
+  // introspection
+  std::vector<dagrt_vertex_info> rec_v;
+  std::vector<dagrt_edge_info> rec_e;
+  std::vector<dagrt_trace_op> trace;
+  dagrt_stats_t st{};
+
+  // scratch reused across launches (no per-launch heap traffic)
+  std::vector<std::pair<uint32_t, uint32_t>> scratch_edges;  // (parent vid, array idx)
+  std::vector<uint32_t> scratch_parents;
+  std::vector<uint32_t> stack;
+};
+
+namespace {
+
+dagrt_status fail(dagrt_ctx c, dagrt_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  c->err = buf;
+  return s;
+}
+
+dagrt_status cuda_fail(dagrt_ctx c, cudaError_t e, const char* what) {
+  c->sticky = true;
+  return fail(c, DAGRT_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                   \
+  do {                                                   \
+    cudaError_t e__ = (call);                            \
+    if (e__ != cudaSuccess) return cuda_fail(c, e__, what); \
+  } while (0)
+
+#define GUARD(c)                                                   \
+  do {                                                             \
+    if (!(c)) return DAGRT_EINVAL;                                 \
+    if ((c)->sticky) return DAGRT_ECUDA;                           \
+  } while (0)
+
+inline void trace_op(dagrt_ctx c, int32_t op, int32_t stream, int64_t a, int64_t b, uint64_t bytes) {
+  if (c->cfg.record_dag) c->trace.push_back(dagrt_trace_op{op, stream, a, b, bytes});
+}
+
+ArrayRec* get_array(dagrt_ctx c, dagrt_array h) {
+  uint32_t idx = (uint32_t)(h & 0xffffffffu);
+  uint32_t gen = (uint32_t)(h >> 32);
+  if (idx == 0 || idx >= c->arrays.size()) return nullptr;
+  ArrayRec* a = &c->arrays[idx];
+  if (!a->live || a->gen != gen) return nullptr;
+  return a;
+}
+
+inline uint32_t array_index(dagrt_ctx c, const ArrayRec* a) { return (uint32_t)(a - c->arrays.data()); }
+inline dagrt_array array_handle(dagrt_ctx c, const ArrayRec* a) {
+  return ((uint64_t)a->gen << 32) | array_index(c, a);
+}
+
+inline bool is_active(dagrt_ctx c, int64_t v) {
+  return v >= 0 && (size_t)v < c->vertices.size() && c->vertices[v].active;
+}
+
+dagrt_status get_event(dagrt_ctx c, void** ev) {
+  if (!c->event_pool.empty()) {
+    *ev = c->event_pool.back();
+    c->event_pool.pop_back();
+    return DAGRT_OK;
+  }
+  CK(c->be->event_create(ev), "cudaEventCreate");
+  c->all_events.push_back(*ev);
+  c->st.events_created++;
+  return DAGRT_OK;
+}
+
+// Retire vertex v and all its active ancestors (D4/D5: a host sync on v
+// proves v and everything v waited on have completed).
+void retire(dagrt_ctx c, uint32_t v) {
+  auto& stk = c->stack;
+  stk.clear();
+  stk.push_back(v);
+  while (!stk.empty()) {
+    uint32_t k = stk.back();
+    stk.pop_back();
+    VertexRec& vr = c->vertices[k];
+    if (!vr.active) continue;
+    vr.active = 0;
+    c->n_active--;
+    if (vr.stream >= 0) c->streams[vr.stream].nactive--;
+    if (vr.ev) {
+      c->event_pool.push_back(vr.ev);
+      vr.ev = nullptr;
+    }
+    for (uint32_t i = 0; i < vr.pcnt; ++i) {
+      uint32_t p = c->parent_pool[vr.pbeg + i];
+      if (c->vertices[p].active) stk.push_back(p);
+    }
+  }
+  if (c->n_active == 0) c->parent_pool.clear();  // frontier empty: parent links no longer needed
+}
+
+void retire_all(dagrt_ctx c) {
+  for (size_t v = 0; v < c->vertices.size(); ++v)
+    if (c->vertices[v].active) retire(c, (uint32_t)v);
+}
+
+// Dependency inference for one access (array a, write?) against the active
+// frontier; appends (parent, array) pairs to scratch_edges.
+void infer(dagrt_ctx c, ArrayRec* a, bool write) {
+  uint32_t ai = array_index(c, a);
+  if (!write) {
+    if (is_active(c, a->last_writer)) c->scratch_edges.push_back({(uint32_t)a->last_writer, ai});
+    return;
+  }
+  // prune readers that are no longer active
+  auto& rd = a->readers;
+  size_t w = 0;
+  for (size_t i = 0; i < rd.size(); ++i)
+    if (c->vertices[rd[i]].active) rd[w++] = rd[i];
+  rd.resize(w);
+  if (!rd.empty()) {
+    for (uint32_t r : rd) c->scratch_edges.push_back({r, ai});
+  } else if (is_active(c, a->last_writer)) {
+    c->scratch_edges.push_back({(uint32_t)a->last_writer, ai});
+  }
+}
+
+// Sorted unique parent list from scratch_edges; records edge rows.
+void collect_parents(dagrt_ctx c, uint32_t child) {
+  auto& e = c->scratch_edges;
+  std::sort(e.begin(), e.end());
+  e.erase(std::unique(e.begin(), e.end()), e.end());
+  auto& ps = c->scratch_parents;
+  ps.clear();
+  for (auto& pr : e) {
+    if (ps.empty() || ps.back() != pr.first) ps.push_back(pr.first);
+    if (c->cfg.record_dag)
+      c->rec_e.push_back(dagrt_edge_info{pr.first, child, array_handle(c, &c->arrays[pr.second])});
+  }
+  c->st.edges += ps.size();
+}
+
+dagrt_status new_stream(dagrt_ctx c, int32_t* out) {
+  void* s = nullptr;
+  CK(c->be->stream_create(&s), "cudaStreamCreate");
+  c->streams.push_back(StreamRec{s, -1, 0});
+  c->st.streams++;
+  *out = (int32_t)c->streams.size() - 1;
+  return DAGRT_OK;
+}
+
+// Stream manager (L570-582, L647-654; stream oracle in SURVEY §8(c1)).
+dagrt_status pick_stream(dagrt_ctx c, int32_t* out) {
+  for (uint32_t p : c->scratch_parents) {
+    int32_t s = c->vertices[p].stream;
+    if (s >= 0 && c->streams[s].tail == (int64_t)p) { *out = s; return DAGRT_OK; }
+  }
+  for (size_t s = 0; s < c->streams.size(); ++s)
+    if (c->streams[s].nactive == 0) { *out = (int32_t)s; return DAGRT_OK; }
+  if (c->cfg.max_streams <= 0 || (int)c->streams.size() < c->cfg.max_streams)
+    return new_stream(c, out);
+  // capped: the first parent's stream, else the least loaded stream
+  if (!c->scratch_parents.empty() && c->vertices[c->scratch_parents[0]].stream >= 0) {
+    *out = c->vertices[c->scratch_parents[0]].stream;
+    return DAGRT_OK;
+  }
+  int32_t best = 0;
+  for (size_t s = 1; s < c->streams.size(); ++s)
+    if (c->streams[s].nactive < c->streams[best].nactive) best = (int32_t)s;
+  *out = best;
+  return DAGRT_OK;
+}
+
+// Host blocks on exactly the conflicting vertices (L553-555), then retires them.
+dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write) {
+  c->scratch_edges.clear();
+  infer(c, a, write);
+  if (c->scratch_edges.empty()) {
+    if (write) { a->readers.clear(); a->last_writer = -1; }
+    return DAGRT_OK;  // not modelled as a DAG element (L512-516)
+  }
+  uint32_t vid = (uint32_t)c->vertices.size();
+  collect_parents(c, vid);
+  c->vertices.push_back(VertexRec{0, 1, -1, nullptr, 0, 0});
+  c->st.vertices++;
+  c->st.host_vertices++;
+  if (c->cfg.record_dag)
+    c->rec_v.push_back(dagrt_vertex_info{vid, 1, 0, -1, array_handle(c, a)});
+  for (uint32_t p : c->scratch_parents) {
+    trace_op(c, DAGRT_OP_EVENT_SYNC, -1, p, 0, 0);
+    CK(c->be->event_sync(c->vertices[p].ev), "cudaEventSynchronize");
+    c->st.host_syncs++;
+  }
+  for (uint32_t p : c->scratch_parents) retire(c, p);
+  if (write) { a->readers.clear(); a->last_writer = -1; }
+  return DAGRT_OK;
+}
+
+dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
+  if (n == 0) return DAGRT_OK;
+  trace_op(c, DAGRT_OP_D2H, -1, array_index(c, a), (int64_t)off, n);
+  c->st.d2h_bytes += n;
+  c->st.d2h_copies++;
+  if (!c->be->real()) return DAGRT_OK;
+  CK(c->be->copy_async(dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream),
+     "cudaMemcpyAsync D2H");
+  CK(c->be->stream_sync(c->d2h_stream), "cudaStreamSynchronize D2H");
+  c->st.host_syncs++;
+  return DAGRT_OK;
+}
+
+dagrt_status ensure_streams(dagrt_ctx c) {
+  if (!c->copy_stream) {
+    CK(c->be->stream_create(&c->copy_stream), "cudaStreamCreate copy");
+    CK(c->be->stream_create(&c->d2h_stream), "cudaStreamCreate d2h");
+    CK(c->be->stream_create(&c->graph_stream), "cudaStreamCreate graph");
+    CK(c->be->stream_create(&c->serial_stream), "cudaStreamCreate serial");
+  }
+  return DAGRT_OK;
+}
+
+dagrt_status parse_signature(const char* sig, KernelRec* k) {
+  k->nparams = 0;
+  std::string s(sig ? sig : "");
+  size_t pos = 0;
+  if (s.find_first_not_of(" \t") == std::string::npos) return DAGRT_OK;
+  while (pos <= s.size()) {
+    size_t comma = s.find(',', pos);
+    std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+    // normalise whitespace
+    std::string norm;
+    bool sp = false;
+    for (char ch : tok) {
+      if (ch == ' ' || ch == '\t') { sp = !norm.empty(); continue; }
+      if (sp) { norm += ' '; sp = false; }
+      norm += ch;
+    }
+    uint8_t kind;
+    if (norm == "const ptr" || norm == "in ptr" || norm == "const pointer" || norm == "in pointer")
+      kind = P_CONST;
+    else if (norm == "ptr" || norm == "inout ptr" || norm == "pointer" || norm == "inout pointer")
+      kind = P_INOUT;
+    else if (norm == "out ptr" || norm == "out pointer")
+      kind = P_OUT;
+    else if (norm == "sint32" || norm == "uint32" || norm == "int")
+      kind = P_I32;
+    else if (norm == "float")
+      kind = P_F32;
+    else if (norm == "sint64" || norm == "uint64")
+      kind = P_I64;
+    else if (norm == "double")
+      kind = P_F64;
+    else
+      return DAGRT_ESIG;
+    if (k->nparams >= kMaxArgs) return DAGRT_ESIG;
+    k->kind[k->nparams++] = kind;
+    if (comma == std::string::npos) break;
+    pos = comma + 1;
+  }
+  return DAGRT_OK;
+}
+
+// Resolve args to the kernel parameter buffer; validates kinds.
+dagrt_status marshal(dagrt_ctx c, const KernelRec& k, const dagrt_arg* args, int32_t nargs,
+                     uint64_t* vals, void** argv, ArrayRec** arrs) {
+  if (nargs != k.nparams)
+    return fail(c, DAGRT_ESIG, "kernel %s: %d args given, signature has %d", k.name.c_str(), nargs,
+                k.nparams);
+  if (nargs > 0 && !args) return fail(c, DAGRT_EINVAL, "null args");
+  for (int i = 0; i < nargs; ++i) {
+    uint8_t kd = k.kind[i];
+    if (is_ptr(kd)) {
+      ArrayRec* a = get_array(c, args[i].array);
+      if (!a) return fail(c, DAGRT_ENOTFOUND, "kernel %s arg %d: not a live array handle", k.name.c_str(), i);
+      if (a->mapped) return fail(c, DAGRT_ESTATE, "kernel %s arg %d: array is host-mapped", k.name.c_str(), i);
+      arrs[i] = a;
+      vals[i] = (uint64_t)(uintptr_t)a->dev;
+    } else {
+      arrs[i] = nullptr;
+      vals[i] = (uint64_t)args[i].i64;
+      if (kd == P_I32 || kd == P_F32) vals[i] &= 0xffffffffull;
+    }
+    argv[i] = &vals[i];
+  }
+  return DAGRT_OK;
+}
+
+dagrt_status lookup_kernel(dagrt_ctx c, dagrt_kernel k, KernelRec** out) {
+  if (k >= c->kernels.size()) return fail(c, DAGRT_ENOTFOUND, "kernel handle %u", k);
+  *out = &c->kernels[k];
+  return DAGRT_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
+  if (!out) return DAGRT_EINVAL;
+  *out = nullptr;
+  dagrt_ctx c = new (std::nothrow) dagrt_ctx_s();
+  if (!c) return DAGRT_ENOMEM;
+  if (cfg) c->cfg = *cfg;
+  else c->cfg = dagrt_config{DAGRT_PARALLEL_ASYNC, 1, 0, 0, DAGRT_BACKEND_CUDA};
+  c->device = device;
+  if (c->cfg.backend == DAGRT_BACKEND_RECORD) {
+    c->be = new RecordBackend();
+  } else {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+      delete c;
+      return DAGRT_ECUDA;
+    }
+    c->be = new CudaBackend();
+  }
+  c->arrays.resize(1);
+  // built-in kernels are pre-registered (handles 0..n-1)
+  for (int i = 0; i < builtin_count(); ++i) {
+    const Builtin* b = builtin_at(i);
+    KernelRec k;
+    k.name = b->name;
+    k.fn = b->fn;
+    k.coop = (b->flags & KF_COOPERATIVE) != 0;
+    if (parse_signature(b->signature, &k) != DAGRT_OK) {
+      delete c->be;
+      delete c;
+      return DAGRT_ESIG;
+    }
+    c->kernels.push_back(k);
+  }
+  if (ensure_streams(c) != DAGRT_OK) {
+    delete c->be;
+    delete c;
+    return DAGRT_ECUDA;
+  }
+  c->scratch_edges.reserve(64);
+  c->scratch_parents.reserve(64);
+  *out = c;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_destroy(dagrt_ctx c) {
+  if (!c) return DAGRT_OK;
+  if (c->be->real()) {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+  }
+  for (auto* g : c->graphs) {
+    if (g->r.exec) cudaGraphExecDestroy(g->r.exec);
+    if (g->r.g) cudaGraphDestroy(g->r.g);
+    delete g;
+  }
+  for (void* e : c->all_events) c->be->event_destroy(e);
+  for (auto& s : c->streams) c->be->stream_destroy(s.s);
+  for (void* s : {c->copy_stream, c->d2h_stream, c->graph_stream, c->serial_stream})
+    if (s) c->be->stream_destroy(s);
+  for (auto& a : c->arrays)
+    if (a.h2d_ev) c->be->event_destroy(a.h2d_ev);
+  delete c->be;
+  delete c;
+  return DAGRT_OK;
+}
+
+const char* dagrt_last_error(dagrt_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+dagrt_status dagrt_array_register(dagrt_ctx c, void* dev, void* host, size_t bytes,
+                                  dagrt_array* out) {
+  GUARD(c);
+  if (!out) return fail(c, DAGRT_EINVAL, "null out");
+  if (!dev && bytes) return fail(c, DAGRT_EINVAL, "null device pointer");
+  if (bytes) {
+    uintptr_t b0 = (uintptr_t)dev, b1 = b0 + bytes;
+    for (size_t i = 1; i < c->arrays.size(); ++i) {
+      const ArrayRec& a = c->arrays[i];
+      if (!a.live || !a.bytes) continue;
+      uintptr_t a0 = (uintptr_t)a.dev, a1 = a0 + a.bytes;
+      if (b0 < a1 && a0 < b1)
+        return fail(c, DAGRT_EALIAS, "device range [%p,+%zu) overlaps array %zu", dev, bytes, i);
+    }
+  }
+  // reuse a dead slot if any
+  size_t idx = 0;
+  for (size_t i = 1; i < c->arrays.size(); ++i)
+    if (!c->arrays[i].live) { idx = i; break; }
+  if (!idx) {
+    c->arrays.emplace_back();
+    idx = c->arrays.size() - 1;
+  }
+  ArrayRec& a = c->arrays[idx];
+  uint32_t gen = a.gen + 1;
+  void* keep_ev = a.h2d_ev;
+  a = ArrayRec();
+  a.h2d_ev = keep_ev;
+  a.gen = gen;
+  a.dev = (char*)dev;
+  a.host = (char*)host;
+  a.bytes = bytes;
+  a.live = true;
+  *out = array_handle(c, &a);
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_array_unregister(dagrt_ctx c, dagrt_array h) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  // wait for in-flight users: the last writer, active readers, a pending copy
+  if (is_active(c, a->last_writer)) {
+    CK(c->be->event_sync(c->vertices[a->last_writer].ev), "cudaEventSynchronize");
+    c->st.host_syncs++;
+  }
+  for (uint32_t r : a->readers)
+    if (c->vertices[r].active) {
+      CK(c->be->event_sync(c->vertices[r].ev), "cudaEventSynchronize");
+      c->st.host_syncs++;
+    }
+  if (a->h2d_pending) {
+    CK(c->be->event_sync(a->h2d_ev), "cudaEventSynchronize");
+    a->h2d_pending = false;
+  }
+  a->live = false;
+  a->readers.clear();
+  a->readers.shrink_to_fit();
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_array_device_ptr(dagrt_ctx c, dagrt_array h, void** dev) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a || !dev) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  *dev = a->dev;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_kernel_register(dagrt_ctx c, const void* fn, const char* name,
+                                   const char* signature, dagrt_kernel* out) {
+  GUARD(c);
+  if (!name || !out) return fail(c, DAGRT_EINVAL, "null name/out");
+  if (!fn && c->be->real()) return fail(c, DAGRT_EINVAL, "null kernel function");
+  KernelRec k;
+  k.name = name;
+  k.fn = fn;
+  k.coop = false;
+  if (parse_signature(signature, &k) != DAGRT_OK)
+    return fail(c, DAGRT_ESIG, "bad signature '%s'", signature ? signature : "(null)");
+  c->kernels.push_back(k);
+  *out = (dagrt_kernel)(c->kernels.size() - 1);
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_kernel_lookup(dagrt_ctx c, const char* name, dagrt_kernel* out) {
+  GUARD(c);
+  if (!name || !out) return fail(c, DAGRT_EINVAL, "null name/out");
+  // user registrations shadow built-ins: search from the end
+  for (size_t i = c->kernels.size(); i-- > 0;)
+    if (c->kernels[i].name == name) {
+      *out = (dagrt_kernel)i;
+      return DAGRT_OK;
+    }
+  return fail(c, DAGRT_ENOTFOUND, "no kernel named '%s'", name);
+}
+
+dagrt_status dagrt_kernel_signature(dagrt_ctx c, dagrt_kernel k, int32_t* kinds, int32_t* n) {
+  GUARD(c);
+  KernelRec* kr;
+  if (dagrt_status s = lookup_kernel(c, k, &kr)) return s;
+  if (!n) return fail(c, DAGRT_EINVAL, "null n");
+  int32_t cap = *n;
+  *n = kr->nparams;
+  if (!kinds) return DAGRT_OK;
+  if (cap < kr->nparams) return fail(c, DAGRT_EINVAL, "capacity");
+  for (int i = 0; i < kr->nparams; ++i) kinds[i] = kr->kind[i];
+  return DAGRT_OK;
+}
+
+int32_t dagrt_builtin_count(void) { return builtin_count(); }
+const char* dagrt_builtin_name(int32_t i) {
+  const Builtin* b = builtin_at(i);
+  return b ? b->name : nullptr;
+}
+const char* dagrt_builtin_signature(int32_t i) {
+  const Builtin* b = builtin_at(i);
+  return b ? b->signature : nullptr;
+}
+
+dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
+                          uint32_t smem, const dagrt_arg* args, int32_t nargs) {
+  GUARD(c);
+  auto t0 = std::chrono::steady_clock::now();
+  KernelRec* k;
+  if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  uint64_t vals[kMaxArgs];
+  void* argv[kMaxArgs];
+  ArrayRec* arrs[kMaxArgs];
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+
+  // merged access per distinct array (D3): write if any use writes,
+  // needs data if any use reads (const / inout)
+  ArrayRec* acc[kMaxArgs];
+  bool wr[kMaxArgs], need[kMaxArgs];
+  int nacc = 0;
+  for (int i = 0; i < nargs; ++i) {
+    if (!arrs[i]) continue;
+    int j = 0;
+    while (j < nacc && acc[j] != arrs[i]) ++j;
+    if (j == nacc) { acc[nacc] = arrs[i]; wr[nacc] = false; need[nacc] = false; ++nacc; }
+    uint8_t kd = k->kind[i];
+    if (kd != P_CONST) wr[j] = true;
+    if (kd != P_OUT) need[j] = true;
+  }
+  dim3 g(grid.x, grid.y, grid.z), b(block.x, block.y, block.z);
+  uint32_t vid = (uint32_t)c->vertices.size();
+  c->st.launches++;
+  c->st.vertices++;
+
+  if (c->cfg.policy == DAGRT_SERIAL_SYNC) {
+    // L560-569 / L908-909: program order on one stream, no dependency
+    // computation, host waits after every copy and kernel.
+    void* s = c->serial_stream;
+    for (int j = 0; j < nacc; ++j) {
+      ArrayRec* a = acc[j];
+      if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
+        trace_op(c, DAGRT_OP_H2D, -3, array_index(c, a), 0, a->bytes);
+        c->st.h2d_bytes += a->bytes;
+        c->st.h2d_copies++;
+        if (c->be->real()) {
+          CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
+          CK(c->be->stream_sync(s), "cudaStreamSynchronize");
+          c->st.host_syncs++;
+        }
+        a->coh = COH_BOTH;
+      }
+    }
+    trace_op(c, DAGRT_OP_LAUNCH, -3, vid, kh, 0);
+    CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+    CK(c->be->stream_sync(s), "cudaStreamSynchronize");
+    c->st.host_syncs++;
+    c->vertices.push_back(VertexRec{0, 0, -1, nullptr, 0, 0});
+    if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{vid, 0, kh, -1, 0});
+    for (int j = 0; j < nacc; ++j)
+      if (wr[j] && acc[j]->host) acc[j]->coh = COH_DEVICE;
+    c->st.sched_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                          std::chrono::steady_clock::now() - t0).count();
+    return DAGRT_OK;
+  }
+
+  // (2-3) dependencies from the dependency sets of active computations
+  c->scratch_edges.clear();
+  for (int j = 0; j < nacc; ++j) infer(c, acc[j], wr[j]);
+  collect_parents(c, vid);
+
+  // (4) stream
+  int32_t sid;
+  if (dagrt_status s = pick_stream(c, &sid)) return s;
+  void* s = c->streams[sid].s;
+
+  // (5) events: wait on parents running on other streams (one wait each)
+  for (uint32_t p : c->scratch_parents) {
+    const VertexRec& pv = c->vertices[p];
+    if (pv.stream != sid) {
+      trace_op(c, DAGRT_OP_WAIT, sid, p, 0, 0);
+      CK(c->be->wait(s, pv.ev), "cudaStreamWaitEvent");
+      c->st.cross_stream_waits++;
+    }
+  }
+  // transfers: prefetch host-newer inputs; order after pending prefetches
+  for (int j = 0; j < nacc; ++j) {
+    ArrayRec* a = acc[j];
+    if (a->h2d_pending && !is_active(c, a->h2d_consumer)) a->h2d_pending = false;
+    if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
+      void* cs = c->cfg.prefetch ? c->copy_stream : s;
+      trace_op(c, DAGRT_OP_H2D, c->cfg.prefetch ? -2 : sid, array_index(c, a), 0, a->bytes);
+      c->st.h2d_bytes += a->bytes;
+      c->st.h2d_copies++;
+      CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, cs), "cudaMemcpyAsync H2D");
+      a->coh = COH_BOTH;
+      if (c->cfg.prefetch) {
+        if (!a->h2d_ev) CK(c->be->event_create(&a->h2d_ev), "cudaEventCreate");
+        CK(c->be->record(a->h2d_ev, cs), "cudaEventRecord copy");
+        trace_op(c, DAGRT_OP_WAIT_COPY, sid, array_index(c, a), 0, 0);
+        CK(c->be->wait(s, a->h2d_ev), "cudaStreamWaitEvent copy");
+        c->st.copy_waits++;
+        a->h2d_pending = true;
+        a->h2d_consumer = vid;
+        a->h2d_stream = sid;
+      }
+    } else if (a->h2d_pending && a->h2d_stream != sid) {
+      trace_op(c, DAGRT_OP_WAIT_COPY, sid, array_index(c, a), 0, 0);
+      CK(c->be->wait(s, a->h2d_ev), "cudaStreamWaitEvent copy");
+      c->st.copy_waits++;
+    }
+  }
+
+  // (6) launch + event
+  void* ev;
+  if (dagrt_status st = get_event(c, &ev)) return st;
+  trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
+  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+  trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
+  CK(c->be->record(ev, s), "cudaEventRecord");
+
+  // bookkeeping: vertex, frontier, dependency sets
+  uint32_t pbeg = (uint32_t)c->parent_pool.size();
+  c->parent_pool.insert(c->parent_pool.end(), c->scratch_parents.begin(), c->scratch_parents.end());
+  c->vertices.push_back(VertexRec{1, 0, sid, ev, pbeg, (uint32_t)c->scratch_parents.size()});
+  c->n_active++;
+  c->streams[sid].tail = vid;
+  c->streams[sid].nactive++;
+  if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{vid, 0, kh, sid, 0});
+  for (int j = 0; j < nacc; ++j) {
+    ArrayRec* a = acc[j];
+    if (wr[j]) {
+      a->last_writer = vid;
+      a->readers.clear();
+      if (a->host) a->coh = COH_DEVICE;
+    } else {
+      a->readers.push_back(vid);
+    }
+  }
+  c->st.sched_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now() - t0).count();
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes, void* dst) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (off > a->bytes || bytes > a->bytes - off) return fail(c, DAGRT_EINVAL, "range out of bounds");
+  if (bytes && !dst) return fail(c, DAGRT_EINVAL, "null dst");
+  if (c->cfg.policy != DAGRT_SERIAL_SYNC)
+    if (dagrt_status s = host_sync_parents(c, a, false)) return s;
+  if (!a->host) return d2h(c, a, off, bytes, dst);
+  if (a->coh == COH_DEVICE) {
+    if (dagrt_status s = d2h(c, a, off, bytes, a->host + off)) return s;
+    if (off == 0 && bytes == a->bytes) a->coh = COH_BOTH;
+  }
+  if (bytes && dst != a->host + off) memcpy(dst, a->host + off, bytes);
+  return DAGRT_OK;
+}
+
+static dagrt_status host_write_prepare(dagrt_ctx c, ArrayRec* a, bool whole) {
+  if (c->cfg.policy != DAGRT_SERIAL_SYNC) {
+    if (dagrt_status s = host_sync_parents(c, a, true)) return s;
+  }
+  if (a->h2d_pending) {  // the copy engine may still read the mirror
+    CK(c->be->event_sync(a->h2d_ev), "cudaEventSynchronize copy");
+    a->h2d_pending = false;
+  }
+  if (a->host && a->coh == COH_DEVICE && !whole)
+    if (dagrt_status s = d2h(c, a, 0, a->bytes, a->host)) return s;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_host_write(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes,
+                              const void* src) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (off > a->bytes || bytes > a->bytes - off) return fail(c, DAGRT_EINVAL, "range out of bounds");
+  if (bytes && !src) return fail(c, DAGRT_EINVAL, "null src");
+  bool whole = off == 0 && bytes == a->bytes;
+  if (dagrt_status s = host_write_prepare(c, a, whole)) return s;
+  a->last_writer = -1;
+  a->readers.clear();
+  if (!a->host) {
+    if (!bytes) return DAGRT_OK;
+    trace_op(c, DAGRT_OP_H2D, -1, array_index(c, a), (int64_t)off, bytes);
+    c->st.h2d_bytes += bytes;
+    c->st.h2d_copies++;
+    if (c->be->real()) {
+      CK(c->be->copy_async(a->dev + off, src, bytes, cudaMemcpyHostToDevice, c->copy_stream),
+         "cudaMemcpyAsync H2D");
+      CK(c->be->stream_sync(c->copy_stream), "cudaStreamSynchronize");
+      c->st.host_syncs++;
+    }
+    return DAGRT_OK;
+  }
+  if (bytes && src != a->host + off) memcpy(a->host + off, src, bytes);
+  a->coh = COH_HOST;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_host_map(dagrt_ctx c, dagrt_array h, int32_t access, void** host_ptr) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (!host_ptr || access < DAGRT_R || access > DAGRT_RW) return fail(c, DAGRT_EINVAL, "bad access/ptr");
+  if (!a->host) return fail(c, DAGRT_ESTATE, "array has no host mirror");
+  if (access & DAGRT_W) {
+    // a W map is a host write of the whole array; RW keeps the current data
+    if (dagrt_status s = host_write_prepare(c, a, !(access & DAGRT_R))) return s;
+    if ((access & DAGRT_R) && a->coh == COH_DEVICE) {
+      if (dagrt_status s = d2h(c, a, 0, a->bytes, a->host)) return s;
+    }
+    a->last_writer = -1;
+    a->readers.clear();
+    a->coh = COH_HOST;
+  } else {
+    if (c->cfg.policy != DAGRT_SERIAL_SYNC)
+      if (dagrt_status s = host_sync_parents(c, a, false)) return s;
+    if (a->coh == COH_DEVICE) {
+      if (dagrt_status s = d2h(c, a, 0, a->bytes, a->host)) return s;
+      a->coh = COH_BOTH;
+    }
+  }
+  a->mapped = true;
+  *host_ptr = a->host;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_host_unmap(dagrt_ctx c, dagrt_array h) {
+  GUARD(c);
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (!a->mapped) return fail(c, DAGRT_ESTATE, "array not mapped");
+  a->mapped = false;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_sync(dagrt_ctx c) {
+  GUARD(c);
+  for (size_t s = 0; s < c->streams.size(); ++s) {
+    trace_op(c, DAGRT_OP_STREAM_SYNC, (int32_t)s, 0, 0, 0);
+    CK(c->be->stream_sync(c->streams[s].s), "cudaStreamSynchronize");
+  }
+  for (void* s : {c->copy_stream, c->d2h_stream, c->graph_stream, c->serial_stream})
+    CK(c->be->stream_sync(s), "cudaStreamSynchronize");
+  c->st.host_syncs++;
+  retire_all(c);
+  for (size_t i = 1; i < c->arrays.size(); ++i) c->arrays[i].h2d_pending = false;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_dag_export(dagrt_ctx c, dagrt_vertex_info* v, uint32_t* nv, dagrt_edge_info* e,
+                              uint32_t* ne) {
+  GUARD(c);
+  if (!nv || !ne) return fail(c, DAGRT_EINVAL, "null counts");
+  uint32_t cv = *nv, ce = *ne;
+  *nv = (uint32_t)c->rec_v.size();
+  *ne = (uint32_t)c->rec_e.size();
+  if (!v && !e) return DAGRT_OK;
+  if (cv < *nv || ce < *ne) return fail(c, DAGRT_EINVAL, "capacity");
+  if (v) std::copy(c->rec_v.begin(), c->rec_v.end(), v);
+  if (e) std::copy(c->rec_e.begin(), c->rec_e.end(), e);
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_dag_clear(dagrt_ctx c) {
+  GUARD(c);
+  c->rec_v.clear();
+  c->rec_e.clear();
+  c->trace.clear();
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_trace_export(dagrt_ctx c, dagrt_trace_op* ops, uint32_t* n) {
+  GUARD(c);
+  if (!n) return fail(c, DAGRT_EINVAL, "null n");
+  uint32_t cap = *n;
+  *n = (uint32_t)c->trace.size();
+  if (!ops) return DAGRT_OK;
+  if (cap < *n) return fail(c, DAGRT_EINVAL, "capacity");
+  std::copy(c->trace.begin(), c->trace.end(), ops);
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_stats(dagrt_ctx c, void* out, size_t size) {
+  if (!c || !out) return DAGRT_EINVAL;
+  memcpy(out, &c->st, std::min(size, sizeof(dagrt_stats_t)));
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_stats_reset(dagrt_ctx c) {
+  if (!c) return DAGRT_EINVAL;
+  c->st = dagrt_stats_t{};
+  c->st.streams = c->streams.size();
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_stream_count(dagrt_ctx c, int32_t* n) {
+  if (!c || !n) return DAGRT_EINVAL;
+  *n = (int32_t)c->streams.size();
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_stream_handle(dagrt_ctx c, int32_t i, void** s) {
+  if (!c || !s) return DAGRT_EINVAL;
+  if (i == -2) { *s = c->copy_stream; return DAGRT_OK; }
+  if (i == -3) { *s = c->serial_stream; return DAGRT_OK; }
+  if (i == -4) { *s = c->graph_stream; return DAGRT_OK; }
+  if (i < 0 || (size_t)i >= c->streams.size()) return DAGRT_EINVAL;
+  *s = c->streams[i].s;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_launch_raw(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
+                              uint32_t smem, const dagrt_arg* args, int32_t nargs, void* stream) {
+  GUARD(c);
+  KernelRec* k;
+  if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  uint64_t vals[kMaxArgs];
+  void* argv[kMaxArgs];
+  ArrayRec* arrs[kMaxArgs];
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+  CK(c->be->launch(k->fn, dim3(grid.x, grid.y, grid.z), dim3(block.x, block.y, block.z), argv, smem,
+                   stream, k->coop),
+     "cudaLaunchKernel raw");
+  return DAGRT_OK;
+}
+
+// ------------------------------------------------------------ manual CUDA graphs
+dagrt_status dagrt_graph_create(dagrt_ctx c, dagrt_graph* g) {
+  GUARD(c);
+  if (!g) return fail(c, DAGRT_EINVAL, "null graph out");
+  if (!c->be->real()) return fail(c, DAGRT_ESTATE, "graphs need the CUDA backend");
+  auto* gr = new (std::nothrow) dagrt_graph_s();
+  if (!gr) return DAGRT_ENOMEM;
+  CK(cudaGraphCreate(&gr->r.g, 0), "cudaGraphCreate");
+  c->graphs.push_back(gr);
+  *g = gr;
+  return DAGRT_OK;
+}
+
+static dagrt_status graph_deps(dagrt_ctx c, dagrt_graph g, const uint32_t* deps, int32_t ndeps,
+                               std::vector<cudaGraphNode_t>* out) {
+  for (int i = 0; i < ndeps; ++i) {
+    if (deps[i] >= g->r.nodes.size()) return fail(c, DAGRT_EINVAL, "bad dependency node %u", deps[i]);
+    out->push_back(g->r.nodes[deps[i]]);
+  }
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh, dagrt_dim3 grid,
+                                    dagrt_dim3 block, uint32_t smem, const dagrt_arg* args,
+                                    int32_t nargs, const uint32_t* deps, int32_t ndeps,
+                                    uint32_t* node) {
+  GUARD(c);
+  if (!g || !node) return fail(c, DAGRT_EINVAL, "null graph/node");
+  KernelRec* k;
+  if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  if (k->coop) return fail(c, DAGRT_ESTATE, "cooperative kernel %s in a graph", k->name.c_str());
+  uint64_t vals[kMaxArgs];
+  void* argv[kMaxArgs];
+  ArrayRec* arrs[kMaxArgs];
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+  std::vector<cudaGraphNode_t> d;
+  if (dagrt_status s = graph_deps(c, g, deps, ndeps, &d)) return s;
+  cudaKernelNodeParams p{};
+  p.func = const_cast<void*>(k->fn);
+  p.gridDim = dim3(grid.x, grid.y, grid.z);
+  p.blockDim = dim3(block.x, block.y, block.z);
+  p.sharedMemBytes = smem;
+  p.kernelParams = argv;
+  cudaGraphNode_t n;
+  CK(cudaGraphAddKernelNode(&n, g->r.g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+  g->r.nodes.push_back(n);
+  *node = (uint32_t)g->r.nodes.size() - 1;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_add_copy(dagrt_ctx c, dagrt_graph g, dagrt_array h, int32_t dir, size_t off,
+                                  size_t bytes, const uint32_t* deps, int32_t ndeps, uint32_t* node) {
+  GUARD(c);
+  if (!g || !node) return fail(c, DAGRT_EINVAL, "null graph/node");
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (!a->host) return fail(c, DAGRT_ESTATE, "array has no host mirror");
+  if (off > a->bytes || bytes > a->bytes - off) return fail(c, DAGRT_EINVAL, "range");
+  std::vector<cudaGraphNode_t> d;
+  if (dagrt_status s = graph_deps(c, g, deps, ndeps, &d)) return s;
+  cudaGraphNode_t n;
+  if (dir == 0)
+    CK(cudaGraphAddMemcpyNode1D(&n, g->r.g, d.data(), d.size(), a->dev + off, a->host + off, bytes,
+                                cudaMemcpyHostToDevice), "cudaGraphAddMemcpyNode1D");
+  else
+    CK(cudaGraphAddMemcpyNode1D(&n, g->r.g, d.data(), d.size(), a->host + off, a->dev + off, bytes,
+                                cudaMemcpyDeviceToHost), "cudaGraphAddMemcpyNode1D");
+  g->r.nodes.push_back(n);
+  *node = (uint32_t)g->r.nodes.size() - 1;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_instantiate(dagrt_ctx c, dagrt_graph g) {
+  GUARD(c);
+  if (!g) return fail(c, DAGRT_EINVAL, "null graph");
+  if (g->r.exec) { cudaGraphExecDestroy(g->r.exec); g->r.exec = nullptr; }
+  CK(cudaGraphInstantiate(&g->r.exec, g->r.g, 0), "cudaGraphInstantiate");
+  CK(cudaGraphUpload(g->r.exec, (cudaStream_t)c->graph_stream), "cudaGraphUpload");
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_run(dagrt_ctx c, dagrt_graph g, int32_t wait) {
+  GUARD(c);
+  if (!g || !g->r.exec) return fail(c, DAGRT_ESTATE, "graph not instantiated");
+  CK(cudaGraphLaunch(g->r.exec, (cudaStream_t)c->graph_stream), "cudaGraphLaunch");
+  if (wait) CK(cudaStreamSynchronize((cudaStream_t)c->graph_stream), "cudaStreamSynchronize graph");
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_destroy(dagrt_ctx c, dagrt_graph g) {
+  if (!c || !g) return DAGRT_EINVAL;
+  auto it = std::find(c->graphs.begin(), c->graphs.end(), g);
+  if (it == c->graphs.end()) return DAGRT_ENOTFOUND;
+  if (g->r.exec) cudaGraphExecDestroy(g->r.exec);
+  if (g->r.g) cudaGraphDestroy(g->r.g);
+  delete g;
+  c->graphs.erase(it);
+  return DAGRT_OK;
+}
+
+}  // extern "C"

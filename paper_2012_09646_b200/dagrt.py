@@ -1,0 +1,418 @@
+"""Thin ctypes binding of libdagrt.so (include/dagrt.h) -- argument
+marshalling only.  Every step of the hot path (dependency inference, stream
+assignment, event wiring, transfers, kernels) runs in the native library.
+
+PyTorch is used by callers only for device memory, pinned host memory and
+streams; this module never falls back to any Python or CPU computation: if
+the native library is missing it raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIBPATH = os.path.join(HERE, "libdagrt.so")
+
+OK, EINVAL, ENOTFOUND, EALIAS, ESIG, ESTATE, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5, -6, -7
+PARALLEL_ASYNC, SERIAL_SYNC = 0, 1
+BACKEND_CUDA, BACKEND_RECORD = 0, 1
+R, W, RW = 1, 2, 3
+K_I32, K_I64, K_CONST, K_INOUT, K_OUT, K_F32, K_F64 = 0, 1, 2, 3, 4, 5, 6
+OPS = {1: "launch", 2: "record", 3: "wait", 4: "h2d", 5: "d2h", 6: "event_sync",
+       7: "stream_sync", 8: "wait_copy"}
+
+
+class DagrtError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"dagrt error {status}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("prefetch", C.c_int32), ("max_streams", C.c_int32),
+                ("record_dag", C.c_int32), ("backend", C.c_int32)]
+
+
+class Dim3(C.Structure):
+    _fields_ = [("x", C.c_uint32), ("y", C.c_uint32), ("z", C.c_uint32)]
+
+
+class Arg(C.Union):
+    _fields_ = [("array", C.c_uint64), ("i32", C.c_int32), ("i64", C.c_int64),
+                ("f32", C.c_float), ("f64", C.c_double)]
+
+
+class VertexInfo(C.Structure):
+    _fields_ = [("id", C.c_uint32), ("kind", C.c_uint32), ("kernel", C.c_uint32),
+                ("stream", C.c_int32), ("array", C.c_uint64)]
+
+
+class EdgeInfo(C.Structure):
+    _fields_ = [("parent", C.c_uint32), ("child", C.c_uint32), ("array", C.c_uint64)]
+
+
+class TraceOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("stream", C.c_int32), ("a", C.c_int64), ("b", C.c_int64),
+                ("bytes", C.c_uint64)]
+
+
+STAT_FIELDS = ["launches", "vertices", "host_vertices", "edges", "cross_stream_waits",
+               "copy_waits", "streams", "events_created", "h2d_bytes", "d2h_bytes",
+               "h2d_copies", "d2h_copies", "host_syncs", "sched_ns"]
+
+
+class Stats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in STAT_FIELDS]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdagrt.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIBPATH):
+        raise ImportError(f"{LIBPATH} not built: run `python -m paper_2012_09646_b200.build`")
+    L = C.CDLL(LIBPATH)
+    st = C.c_int32
+    ctx = C.c_void_p
+    L.dagrt_create.argtypes = [C.c_int, C.POINTER(Config), C.POINTER(C.c_void_p)]
+    L.dagrt_destroy.argtypes = [ctx]
+    L.dagrt_last_error.argtypes = [ctx]
+    L.dagrt_last_error.restype = C.c_char_p
+    L.dagrt_array_register.argtypes = [ctx, C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
+    L.dagrt_array_unregister.argtypes = [ctx, C.c_uint64]
+    L.dagrt_array_device_ptr.argtypes = [ctx, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.dagrt_kernel_register.argtypes = [ctx, C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_uint32)]
+    L.dagrt_kernel_lookup.argtypes = [ctx, C.c_char_p, C.POINTER(C.c_uint32)]
+    L.dagrt_kernel_signature.argtypes = [ctx, C.c_uint32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.dagrt_builtin_count.restype = C.c_int32
+    L.dagrt_builtin_name.argtypes = [C.c_int32]
+    L.dagrt_builtin_name.restype = C.c_char_p
+    L.dagrt_builtin_signature.argtypes = [C.c_int32]
+    L.dagrt_builtin_signature.restype = C.c_char_p
+    L.dagrt_launch.argtypes = [ctx, C.c_uint32, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32]
+    L.dagrt_launch_raw.argtypes = [ctx, C.c_uint32, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32,
+                                   C.c_void_p]
+    L.dagrt_host_read.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
+    L.dagrt_host_write.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
+    L.dagrt_host_map.argtypes = [ctx, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p)]
+    L.dagrt_host_unmap.argtypes = [ctx, C.c_uint64]
+    L.dagrt_sync.argtypes = [ctx]
+    L.dagrt_dag_export.argtypes = [ctx, C.POINTER(VertexInfo), C.POINTER(C.c_uint32),
+                                   C.POINTER(EdgeInfo), C.POINTER(C.c_uint32)]
+    L.dagrt_dag_clear.argtypes = [ctx]
+    L.dagrt_trace_export.argtypes = [ctx, C.POINTER(TraceOp), C.POINTER(C.c_uint32)]
+    L.dagrt_stats.argtypes = [ctx, C.c_void_p, C.c_size_t]
+    L.dagrt_stats_reset.argtypes = [ctx]
+    L.dagrt_stream_count.argtypes = [ctx, C.POINTER(C.c_int32)]
+    L.dagrt_stream_handle.argtypes = [ctx, C.c_int32, C.POINTER(C.c_void_p)]
+    L.dagrt_graph_create.argtypes = [ctx, C.POINTER(C.c_void_p)]
+    L.dagrt_graph_add_kernel.argtypes = [ctx, C.c_void_p, C.c_uint32, Dim3, Dim3, C.c_uint32,
+                                         C.POINTER(Arg), C.c_int32, C.POINTER(C.c_uint32), C.c_int32,
+                                         C.POINTER(C.c_uint32)]
+    L.dagrt_graph_add_copy.argtypes = [ctx, C.c_void_p, C.c_uint64, C.c_int32, C.c_size_t, C.c_size_t,
+                                       C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_uint32)]
+    L.dagrt_graph_instantiate.argtypes = [ctx, C.c_void_p]
+    L.dagrt_graph_run.argtypes = [ctx, C.c_void_p, C.c_int32]
+    L.dagrt_graph_destroy.argtypes = [ctx, C.c_void_p]
+    for name in dir(L):
+        pass
+    for fn in ("dagrt_create", "dagrt_destroy", "dagrt_array_register", "dagrt_array_unregister",
+               "dagrt_array_device_ptr", "dagrt_kernel_register", "dagrt_kernel_lookup",
+               "dagrt_kernel_signature", "dagrt_launch", "dagrt_launch_raw", "dagrt_host_read",
+               "dagrt_host_write", "dagrt_host_map", "dagrt_host_unmap", "dagrt_sync",
+               "dagrt_dag_export", "dagrt_dag_clear", "dagrt_trace_export", "dagrt_stats",
+               "dagrt_stats_reset", "dagrt_stream_count", "dagrt_stream_handle",
+               "dagrt_graph_create", "dagrt_graph_add_kernel", "dagrt_graph_add_copy",
+               "dagrt_graph_instantiate", "dagrt_graph_run", "dagrt_graph_destroy"):
+        getattr(L, fn).restype = st
+    _lib = L
+    return L
+
+
+def builtins():
+    L = lib()
+    return [(L.dagrt_builtin_name(i).decode(), L.dagrt_builtin_signature(i).decode())
+            for i in range(L.dagrt_builtin_count())]
+
+
+def dim3(v):
+    if isinstance(v, int):
+        return Dim3(v, 1, 1)
+    v = tuple(v) + (1, 1)
+    return Dim3(v[0], v[1], v[2])
+
+
+class Array:
+    """A registered array.  Keeps the caller's tensors alive until unregister."""
+    __slots__ = ("ctx", "handle", "name", "nbytes", "dev_ptr", "host_ptr", "_keep")
+
+    def __init__(self, ctx, handle, name, nbytes, dev_ptr, host_ptr, keep):
+        self.ctx, self.handle, self.name, self.nbytes = ctx, handle, name, nbytes
+        self.dev_ptr, self.host_ptr, self._keep = dev_ptr, host_ptr, keep
+
+    def __repr__(self):
+        return f"Array({self.name}, {self.nbytes} B)"
+
+
+class Kernel:
+    __slots__ = ("handle", "name", "kinds")
+
+    def __init__(self, handle, name, kinds):
+        self.handle, self.name, self.kinds = handle, name, kinds
+
+
+def _set_arg(slot, kind, v):
+    if K_CONST <= kind <= K_OUT:
+        if not isinstance(v, Array):
+            raise TypeError(f"pointer parameter needs an Array, got {type(v)}")
+        slot.array = v.handle
+    elif kind == K_I32:
+        slot.i64 = 0
+        slot.i32 = int(v)
+    elif kind == K_I64:
+        slot.i64 = int(v)
+    elif kind == K_F32:
+        slot.i64 = 0
+        slot.f32 = float(v)
+    elif kind == K_F64:
+        slot.f64 = float(v)
+    else:
+        raise ValueError(kind)
+
+
+class Launch:
+    """A prepared launch (args marshalled once; calling it enqueues it)."""
+    __slots__ = ("ctx", "kernel", "grid", "block", "smem", "args", "n", "_fn", "_c")
+
+    def __init__(self, ctx, kernel, grid, block, args, smem=0):
+        if len(args) != len(kernel.kinds):
+            raise DagrtError(ESIG, f"{kernel.name}: {len(args)} args, signature has {len(kernel.kinds)}")
+        self.ctx, self.kernel, self.smem = ctx, kernel, smem
+        self.grid, self.block = dim3(grid), dim3(block)
+        self.n = len(args)
+        self.args = (Arg * max(1, self.n))()
+        for i, (k, v) in enumerate(zip(kernel.kinds, args)):
+            _set_arg(self.args[i], k, v)
+        self._fn = lib().dagrt_launch
+        self._c = ctx._c
+
+    def __call__(self):
+        s = self._fn(self._c, self.kernel.handle, self.grid, self.block, self.smem, self.args, self.n)
+        if s:
+            self.ctx._raise(s)
+
+    def raw(self, stream_ptr):
+        s = lib().dagrt_launch_raw(self._c, self.kernel.handle, self.grid, self.block, self.smem,
+                                   self.args, self.n, C.c_void_p(stream_ptr))
+        if s:
+            self.ctx._raise(s)
+
+
+class Graph:
+    """Hand-built CUDA graph with manual dependencies (baseline, L1062-1067)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        h = C.c_void_p()
+        ctx._check(lib().dagrt_graph_create(ctx._c, C.byref(h)))
+        self._h = h
+
+    def _deps(self, deps):
+        deps = list(deps or [])
+        return (C.c_uint32 * max(1, len(deps)))(*deps), len(deps)
+
+    def kernel(self, launch: Launch, deps=()):
+        d, nd = self._deps(deps)
+        node = C.c_uint32()
+        self.ctx._check(lib().dagrt_graph_add_kernel(
+            self.ctx._c, self._h, launch.kernel.handle, launch.grid, launch.block, launch.smem,
+            launch.args, launch.n, d, nd, C.byref(node)))
+        return node.value
+
+    def copy(self, arr: Array, direction, off=0, nbytes=None, deps=()):
+        d, nd = self._deps(deps)
+        node = C.c_uint32()
+        nb = arr.nbytes - off if nbytes is None else nbytes
+        self.ctx._check(lib().dagrt_graph_add_copy(self.ctx._c, self._h, arr.handle,
+                                                   0 if direction == "h2d" else 1, off, nb, d, nd,
+                                                   C.byref(node)))
+        return node.value
+
+    def instantiate(self):
+        self.ctx._check(lib().dagrt_graph_instantiate(self.ctx._c, self._h))
+
+    def run(self, wait=True):
+        self.ctx._check(lib().dagrt_graph_run(self.ctx._c, self._h, 1 if wait else 0))
+
+
+class Context:
+    def __init__(self, device=0, policy="parallel", prefetch=True, max_streams=0,
+                 record_dag=False, backend="cuda"):
+        L = lib()
+        cfg = Config(PARALLEL_ASYNC if policy == "parallel" else SERIAL_SYNC, 1 if prefetch else 0,
+                     max_streams, 1 if record_dag else 0,
+                     BACKEND_CUDA if backend == "cuda" else BACKEND_RECORD)
+        h = C.c_void_p()
+        s = L.dagrt_create(device, C.byref(cfg), C.byref(h))
+        if s:
+            raise DagrtError(s, "dagrt_create failed (CUDA device unavailable?)")
+        self._c = h
+        self.policy, self.backend = policy, backend
+        self.arrays = {}      # handle -> Array
+        self._kernels = {}
+        self._kname = {}      # kernel handle -> name
+
+    # -- errors
+    def _raise(self, s):
+        raise DagrtError(s, lib().dagrt_last_error(self._c).decode())
+
+    def _check(self, s):
+        if s:
+            self._raise(s)
+
+    def close(self):
+        if self._c:
+            lib().dagrt_destroy(self._c)
+            self._c = None
+            self.arrays.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- arrays
+    def register(self, name, dev_ptr, nbytes, host_ptr=None, keep=()):
+        h = C.c_uint64()
+        self._check(lib().dagrt_array_register(self._c, C.c_void_p(dev_ptr),
+                                               C.c_void_p(host_ptr) if host_ptr else None,
+                                               nbytes, C.byref(h)))
+        a = Array(self, h.value, name, nbytes, dev_ptr, host_ptr, keep)
+        self.arrays[a.handle] = a
+        return a
+
+    def register_tensor(self, name, t, mirror=None):
+        """Register a device tensor (and optional pinned host mirror tensor)."""
+        nbytes = t.numel() * t.element_size()
+        if mirror is not None:
+            assert mirror.numel() * mirror.element_size() == nbytes
+        return self.register(name, t.data_ptr(), nbytes,
+                             mirror.data_ptr() if mirror is not None else None, keep=(t, mirror))
+
+    def unregister(self, a: Array):
+        self._check(lib().dagrt_array_unregister(self._c, a.handle))
+        self.arrays.pop(a.handle, None)
+
+    # -- kernels
+    def kernel(self, name):
+        k = self._kernels.get(name)
+        if k is not None:
+            return k
+        L = lib()
+        h = C.c_uint32()
+        self._check(L.dagrt_kernel_lookup(self._c, name.encode(), C.byref(h)))
+        n = C.c_int32(16)
+        kinds = (C.c_int32 * 16)()
+        self._check(L.dagrt_kernel_signature(self._c, h.value, kinds, C.byref(n)))
+        k = Kernel(h.value, name, list(kinds[:n.value]))
+        self._kernels[name] = k
+        self._kname[h.value] = name
+        return k
+
+    def register_kernel(self, fn_ptr, name, signature):
+        h = C.c_uint32()
+        self._check(lib().dagrt_kernel_register(self._c, C.c_void_p(fn_ptr), name.encode(),
+                                                signature.encode(), C.byref(h)))
+        self._kernels.pop(name, None)
+        return self.kernel(name)
+
+    def prepare(self, kernel, grid, block, args, smem=0):
+        if isinstance(kernel, str):
+            kernel = self.kernel(kernel)
+        return Launch(self, kernel, grid, block, args, smem)
+
+    def launch(self, kernel, grid, block, *args, smem=0):
+        self.prepare(kernel, grid, block, args, smem)()
+
+    # -- host access
+    def host_read(self, a: Array, dst_ptr, off=0, nbytes=None):
+        nb = a.nbytes - off if nbytes is None else nbytes
+        self._check(lib().dagrt_host_read(self._c, a.handle, off, nb, C.c_void_p(dst_ptr)))
+
+    def host_write(self, a: Array, src_ptr, off=0, nbytes=None):
+        nb = a.nbytes - off if nbytes is None else nbytes
+        self._check(lib().dagrt_host_write(self._c, a.handle, off, nb, C.c_void_p(src_ptr)))
+
+    def read_scalar(self, a: Array, ctype=C.c_float, index=0):
+        v = ctype()
+        self.host_read(a, C.addressof(v), off=index * C.sizeof(ctype), nbytes=C.sizeof(ctype))
+        return v.value
+
+    def host_map(self, a: Array, access=R):
+        p = C.c_void_p()
+        self._check(lib().dagrt_host_map(self._c, a.handle, access, C.byref(p)))
+        return p.value
+
+    def host_unmap(self, a: Array):
+        self._check(lib().dagrt_host_unmap(self._c, a.handle))
+
+    def sync(self):
+        self._check(lib().dagrt_sync(self._c))
+
+    # -- introspection
+    def dag(self):
+        """(vertices, edges): vertices = [(id, kind, name, stream)], edges = {(p, c, array_name)}."""
+        L = lib()
+        nv, ne = C.c_uint32(0), C.c_uint32(0)
+        self._check(L.dagrt_dag_export(self._c, None, C.byref(nv), None, C.byref(ne)))
+        V = (VertexInfo * max(1, nv.value))()
+        E = (EdgeInfo * max(1, ne.value))()
+        self._check(L.dagrt_dag_export(self._c, V, C.byref(nv), E, C.byref(ne)))
+        names = self._kname
+        arr = {h: a.name for h, a in self.arrays.items()}
+        verts = []
+        for v in V[:nv.value]:
+            if v.kind == 0:
+                verts.append((v.id, "kernel", names.get(v.kernel, f"k{v.kernel}"), v.stream))
+            else:
+                verts.append((v.id, "host", arr.get(v.array, hex(v.array)), -1))
+        edges = {(e.parent, e.child, arr.get(e.array, hex(e.array))) for e in E[:ne.value]}
+        return verts, edges
+
+    def dag_clear(self):
+        self._check(lib().dagrt_dag_clear(self._c))
+
+    def trace(self):
+        L = lib()
+        n = C.c_uint32(0)
+        self._check(L.dagrt_trace_export(self._c, None, C.byref(n)))
+        T = (TraceOp * max(1, n.value))()
+        self._check(L.dagrt_trace_export(self._c, T, C.byref(n)))
+        return [(OPS[t.op], t.stream, t.a, t.b, t.bytes) for t in T[:n.value]]
+
+    def stats(self):
+        s = Stats()
+        self._check(lib().dagrt_stats(self._c, C.byref(s), C.sizeof(s)))
+        return {f: getattr(s, f) for f in STAT_FIELDS}
+
+    def stats_reset(self):
+        self._check(lib().dagrt_stats_reset(self._c))
+
+    def stream_count(self):
+        n = C.c_int32()
+        self._check(lib().dagrt_stream_count(self._c, C.byref(n)))
+        return n.value
+
+    def stream_handle(self, i):
+        p = C.c_void_p()
+        self._check(lib().dagrt_stream_handle(self._c, i, C.byref(p)))
+        return p.value
+
+    def graph(self):
+        return Graph(self)

@@ -1,0 +1,216 @@
+"""The C++ scheduler (libdagrt.so) through its C ABI with the RECORD backend
+(no GPU): DAG, stream assignment, event wiring and transfers must equal the
+brute-force oracle (oracle/dag.py) bit for bit, and the Appendix-A golden DAGs.
+"""
+import ctypes as C
+import itertools
+import random
+
+import pytest
+
+from golden_io import all_cases
+from oracle import dag as odag
+from paper_2012_09646_b200 import dagrt as D
+
+MODE_TOKEN = {"R": "const ptr", "RW": "ptr", "O": "out ptr"}
+CASES = all_cases()
+
+
+class Replayer:
+    """Replays an oracle-format trace through dagrt (record backend)."""
+
+    def __init__(self, arrays, nbytes=64, mirrors=True, policy="parallel", prefetch=True):
+        self.ctx = D.Context(backend="record", record_dag=True, policy=policy, prefetch=prefetch)
+        self.bufs = {}
+        self.arr = {}
+        self.nbytes = {}
+        for i, name in enumerate(sorted(arrays)):
+            host = None
+            if mirrors:
+                self.bufs[name] = (C.c_char * nbytes)()
+                host = C.addressof(self.bufs[name])
+            self.arr[name] = self.ctx.register(name, 0x100000 * (i + 1), nbytes, host)
+            self.nbytes[name] = nbytes
+        self.kernels = {}
+        self.scratch = (C.c_char * nbytes)()
+
+    def kernel(self, name, modes):
+        key = (name, tuple(modes))
+        if key not in self.kernels:
+            sig = ", ".join(MODE_TOKEN[m] for m in modes)
+            self.kernels[key] = self.ctx.register_kernel(None, name, sig)
+        return self.kernels[key]
+
+    def run(self, trace):
+        for op in trace:
+            if op[0] == "launch":
+                k = self.kernel(op[1], [m for _, m in op[2]])
+                self.ctx.prepare(k, 1, 32, [self.arr[a] for a, _ in op[2]])()
+            elif op[0] == "host":
+                _, a, m, off, nb = op
+                if m == "R":
+                    self.ctx.host_read(self.arr[a], C.addressof(self.scratch), off, nb)
+                else:
+                    self.ctx.host_write(self.arr[a], C.addressof(self.scratch), off, nb)
+            elif op[0] == "sync":
+                self.ctx.sync()
+        return self
+
+    def dag(self):
+        v, e = self.ctx.dag()
+        return v, e
+
+    def waits(self):
+        return [t for t in self.ctx.trace() if t[0] == "wait"]
+
+    def transfers(self):
+        idx = {a.handle & 0xffffffff: n for n, a in self.arr.items()}
+        out = []
+        for t in self.ctx.trace():
+            if t[0] in ("h2d", "d2h"):
+                out.append((t[0].upper(), idx[t[2]], t[4]))
+        return out
+
+
+def arrays_of(trace):
+    s = set()
+    for op in trace:
+        if op[0] == "launch":
+            s |= {a for a, _ in op[2]}
+        elif op[0] == "host":
+            s.add(op[1])
+    return s
+
+
+def check_against_oracle(trace, nbytes=128):
+    rp = Replayer(arrays_of(trace), nbytes).run(trace)
+    verts, edges = rp.dag()
+    o = odag.build_dag(trace)
+    ov = [(v[0], v[2], v[3], v[4]) for v in o.vertices]
+    gv = [(v[0], v[1], v[2], v[3]) for v in verts]
+    assert gv == ov, (trace, gv, ov)
+    assert edges == o.edges, (trace, edges ^ o.edges)
+    gw = sorted((t[1], t[2]) for t in rp.waits())  # (stream, parent vid)
+    stream_of = {v[0]: v[4] for v in o.vertices}
+    ow = sorted((stream_of[c], p) for c, p in o.waits)
+    assert gw == ow, trace
+    ot = [(d, a, b) for d, a, b, _ in odag.transfers(trace, {a: True for a in rp.arr}, rp.nbytes)]
+    assert rp.transfers() == ot, (trace, rp.transfers(), ot)
+    return rp
+
+
+@pytest.mark.parametrize("name,case", CASES, ids=[c[0] for c in CASES])
+def test_golden_dags_through_c_abi(name, case):
+    rp = check_against_oracle(case["trace"])
+    verts, edges = rp.dag()
+    got_v = [(v[0], v[2] if v[1] == "kernel" else "host:" + v[2], v[3]) for v in verts]
+    assert got_v == case["vertices"]
+    assert edges == case["edges"]
+    if case["waits"] is not None:
+        assert len(rp.waits()) == case["waits"]
+
+
+OPS = []
+for arrs in [("X",), ("Y",), ("X", "Y"), ("X", "X")]:
+    for modes in itertools.product(("R", "RW", "O"), repeat=len(arrs)):
+        OPS.append(("launch", "k", list(zip(arrs, modes))))
+for arr in ("X", "Y"):
+    for m in ("R", "W"):
+        OPS.append(("host", arr, m, 0, 128))
+OPS.append(("host", "X", "R", 8, 16))
+OPS.append(("host", "X", "W", 8, 16))
+
+
+def test_exhaustive_traces_len3():
+    n = 0
+    for tr in itertools.product(OPS, repeat=3):
+        check_against_oracle(list(tr))
+        n += 1
+    assert n == len(OPS) ** 3
+
+
+def test_random_traces():
+    rng = random.Random(1234)
+    names = list("ABCDEF")
+    for _ in range(300):
+        tr = []
+        for _ in range(rng.randint(1, 80)):
+            r = rng.random()
+            if r < 0.8:
+                tr.append(("launch", rng.choice(["k", "m"]),
+                           [(rng.choice(names), rng.choice(["R", "R", "RW", "O"]))
+                            for _ in range(rng.randint(1, 5))]))
+            elif r < 0.97:
+                off = rng.choice([0, 0, 8])
+                nb = 128 - off if rng.random() < 0.7 else 8
+                tr.append(("host", rng.choice(names), rng.choice("RW"), off, nb))
+            else:
+                tr.append(("sync",))
+        check_against_oracle(tr)
+
+
+def test_serial_policy_has_no_edges_and_one_stream():
+    tr = CASES[0][1]["trace"]
+    rp = Replayer(arrays_of(tr), policy="serial").run(tr)
+    verts, edges = rp.dag()
+    assert edges == set()
+    assert all(v[3] == -1 for v in verts)
+    t = rp.ctx.trace()
+    assert all(op[1] == -3 for op in t if op[0] == "launch")
+
+
+def test_errors():
+    ctx = D.Context(backend="record", record_dag=True)
+    a = ctx.register("a", 0x1000, 256)
+    with pytest.raises(D.DagrtError) as e:
+        ctx.register("b", 0x1080, 256)
+    assert e.value.status == D.EALIAS
+    with pytest.raises(D.DagrtError) as e:
+        ctx.register_kernel(None, "bad", "const ptr, wat")
+    assert e.value.status == D.ESIG
+    k = ctx.register_kernel(None, "k2", "const ptr, sint32")
+    with pytest.raises(D.DagrtError) as e:
+        ctx.prepare(k, 1, 1, [a, 3])  # ok
+        D.lib().dagrt_launch(ctx._c, k.handle, D.dim3(1), D.dim3(1), 0, (D.Arg * 1)(), 1) and \
+            ctx._raise(D.ESIG)
+    assert e.value.status == D.ESIG
+    with pytest.raises(D.DagrtError) as e:
+        ctx.kernel("nope")
+    assert e.value.status == D.ENOTFOUND
+    ctx.unregister(a)
+    with pytest.raises(D.DagrtError) as e:
+        ctx.launch(k, 1, 1, a, 1)
+    assert e.value.status == D.ENOTFOUND
+    with pytest.raises(D.DagrtError) as e:
+        ctx.host_map(ctx.register("c", 0x9000, 64), D.R)
+    assert e.value.status == D.ESTATE
+    b = ctx.register("b2", 0x20000, 64)
+    with pytest.raises(D.DagrtError) as e:
+        ctx.host_read(b, 0, 60, 8)
+    assert e.value.status == D.EINVAL
+
+
+def test_host_map_marks_host_newer_and_prefetches_once():
+    rp = Replayer({"x", "y"})
+    ctx = rp.ctx
+    ctx.host_map(rp.arr["x"], D.W)
+    ctx.host_unmap(rp.arr["x"])
+    k = rp.kernel("k", ["R", "O"])
+    ctx.prepare(k, 1, 1, [rp.arr["x"], rp.arr["y"]])()
+    ctx.prepare(k, 1, 1, [rp.arr["x"], rp.arr["y"]])()
+    h2d = [t for t in ctx.trace() if t[0] == "h2d"]
+    assert len(h2d) == 1 and h2d[0][1] == -2  # one copy, on the copy stream
+    waits = [t for t in ctx.trace() if t[0] == "wait_copy"]
+    assert len(waits) >= 1
+
+
+def test_all_symbols_exported():
+    """Every function declared in include/dagrt.h is exported by libdagrt.so."""
+    import os
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "dagrt.h")).read()
+    names = set(re.findall(r"\b(dagrt_[a-z_0-9]+)\s*\(", hdr))
+    L = D.lib()
+    missing = [n for n in sorted(names) if not hasattr(L, n)]
+    assert not missing, missing
+    assert len(names) >= 30
