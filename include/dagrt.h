@@ -241,6 +241,17 @@ dagrt_status dagrt_stream_count(dagrt_ctx ctx, int32_t* n);
 /* The cudaStream_t of compute stream i (as void*), e.g. for profiling marks. */
 dagrt_status dagrt_stream_handle(dagrt_ctx ctx, int32_t i, void** stream);
 
+/* Kernel timing on the launching stream: while enabled for kernel k, every
+ * launch of k is bracketed by two timing events recorded on the stream the
+ * scheduler put it on (2 extra cudaEventRecord per launch). */
+dagrt_status dagrt_profile_enable(dagrt_ctx ctx, dagrt_kernel k, int32_t on);
+/* Wait for the recorded launches of k and report: *count launches, *sum_ms
+ * the sum of their durations, *busy_ms the length of the union of their
+ * [start, end] intervals (time during which at least one launch of k was
+ * running; concurrent launches overlap).  Clears the records. */
+dagrt_status dagrt_profile_collect(dagrt_ctx ctx, dagrt_kernel k, int32_t* count, double* sum_ms,
+                                   double* busy_ms);
+
 /* ---------------------------------------------------------------- baselines */
 
 /* Direct launch on a caller-given cudaStream_t with no scheduling at all

@@ -58,6 +58,8 @@ struct Backend {
   virtual cudaError_t stream_create(void** s) = 0;
   virtual cudaError_t stream_destroy(void* s) = 0;
   virtual cudaError_t event_create(void** e) = 0;
+  virtual cudaError_t event_create_timing(void** e) = 0;
+  virtual cudaError_t elapsed(float* ms, void* a, void* b) = 0;
   virtual cudaError_t event_destroy(void* e) = 0;
   virtual cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
                              bool coop) = 0;
@@ -77,6 +79,12 @@ struct CudaBackend final : Backend {
   cudaError_t stream_destroy(void* s) override { return cudaStreamDestroy((cudaStream_t)s); }
   cudaError_t event_create(void** e) override {
     return cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(e), cudaEventDisableTiming);
+  }
+  cudaError_t event_create_timing(void** e) override {
+    return cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(e), cudaEventDefault);
+  }
+  cudaError_t elapsed(float* ms, void* a, void* b) override {
+    return cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b);
   }
   cudaError_t event_destroy(void* e) override { return cudaEventDestroy((cudaEvent_t)e); }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
@@ -104,6 +112,8 @@ struct RecordBackend final : Backend {
   cudaError_t stream_create(void** s) override { *s = (void*)(next += 16); return cudaSuccess; }
   cudaError_t stream_destroy(void*) override { return cudaSuccess; }
   cudaError_t event_create(void** e) override { *e = (void*)(next += 16); return cudaSuccess; }
+  cudaError_t event_create_timing(void** e) override { *e = (void*)(next += 16); return cudaSuccess; }
+  cudaError_t elapsed(float* ms, void*, void*) override { *ms = 0.f; return cudaSuccess; }
   cudaError_t event_destroy(void*) override { return cudaSuccess; }
   cudaError_t launch(const void*, dim3, dim3, void**, size_t, void*, bool) override {
     return cudaSuccess;
@@ -131,6 +141,13 @@ struct KernelRec {
   int32_t nparams;
   uint8_t kind[kMaxArgs];
   bool coop;
+  bool prof = false;
+};
+
+struct ProfRec {
+  uint32_t kernel;
+  void* ev0;
+  void* ev1;
 };
 
 struct ArrayRec {
@@ -197,6 +214,9 @@ struct dagrt_ctx_s {
   void* graph_stream = nullptr;
   void* serial_stream = nullptr;
   std::vector<dagrt_graph_s*> graphs;
+  std::vector<ProfRec> prof;           // timed launches awaiting collection
+  std::vector<void*> tev_pool;         // free timing events
+  std::vector<void*> all_tev;
 
   // introspection
   std::vector<dagrt_vertex_info> rec_v;
@@ -270,6 +290,35 @@ dagrt_status get_event(dagrt_ctx c, void** ev) {
   CK(c->be->event_create(ev), "cudaEventCreate");
   c->all_events.push_back(*ev);
   c->st.events_created++;
+  return DAGRT_OK;
+}
+
+dagrt_status get_timing_event(dagrt_ctx c, void** ev) {
+  if (!c->tev_pool.empty()) {
+    *ev = c->tev_pool.back();
+    c->tev_pool.pop_back();
+    return DAGRT_OK;
+  }
+  CK(c->be->event_create_timing(ev), "cudaEventCreate timing");
+  c->all_tev.push_back(*ev);
+  return DAGRT_OK;
+}
+
+// The one place kernels are enqueued; optionally bracketed by timing events
+// on the launching stream (dagrt_profile_enable).
+dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim3 b, void** argv,
+                       uint32_t smem, void* s) {
+  void *e0 = nullptr, *e1 = nullptr;
+  if (k->prof) {
+    if (dagrt_status st = get_timing_event(c, &e0)) return st;
+    if (dagrt_status st = get_timing_event(c, &e1)) return st;
+    CK(c->be->record(e0, s), "cudaEventRecord profile");
+  }
+  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+  if (k->prof) {
+    CK(c->be->record(e1, s), "cudaEventRecord profile");
+    c->prof.push_back(ProfRec{kh, e0, e1});
+  }
   return DAGRT_OK;
 }
 
@@ -552,6 +601,7 @@ dagrt_status dagrt_destroy(dagrt_ctx c) {
     delete g;
   }
   for (void* e : c->all_events) c->be->event_destroy(e);
+  for (void* e : c->all_tev) c->be->event_destroy(e);
   for (auto& s : c->streams) c->be->stream_destroy(s.s);
   for (void* s : {c->copy_stream, c->d2h_stream, c->graph_stream, c->serial_stream})
     if (s) c->be->stream_destroy(s);
@@ -733,7 +783,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       }
     }
     trace_op(c, DAGRT_OP_LAUNCH, -3, vid, kh, 0);
-    CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s)) return st_;
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
     c->st.host_syncs++;
     c->vertices.push_back(VertexRec{0, 0, -1, nullptr, 0, 0});
@@ -796,7 +846,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   void* ev;
   if (dagrt_status st = get_event(c, &ev)) return st;
   trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
-  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s)) return st_;
   trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
   CK(c->be->record(ev, s), "cudaEventRecord");
 
@@ -992,6 +1042,54 @@ dagrt_status dagrt_stream_handle(dagrt_ctx c, int32_t i, void** s) {
   if (i == -4) { *s = c->graph_stream; return DAGRT_OK; }
   if (i < 0 || (size_t)i >= c->streams.size()) return DAGRT_EINVAL;
   *s = c->streams[i].s;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_profile_enable(dagrt_ctx c, dagrt_kernel kh, int32_t on) {
+  GUARD(c);
+  KernelRec* k;
+  if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  k->prof = on != 0;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_profile_collect(dagrt_ctx c, dagrt_kernel kh, int32_t* count, double* sum_ms,
+                                   double* busy_ms) {
+  GUARD(c);
+  if (!count || !sum_ms || !busy_ms) return fail(c, DAGRT_EINVAL, "null out");
+  *count = 0;
+  *sum_ms = 0.0;
+  *busy_ms = 0.0;
+  std::vector<std::pair<double, double>> iv;
+  void* ref = nullptr;
+  std::vector<ProfRec> keep;
+  for (const ProfRec& p : c->prof) {
+    if (p.kernel != kh) { keep.push_back(p); continue; }
+    CK(c->be->event_sync(p.ev1), "cudaEventSynchronize profile");
+    if (!ref) ref = p.ev0;
+    float a = 0.f, b = 0.f, d = 0.f;
+    CK(c->be->elapsed(&a, ref, p.ev0), "cudaEventElapsedTime");
+    CK(c->be->elapsed(&b, ref, p.ev1), "cudaEventElapsedTime");
+    CK(c->be->elapsed(&d, p.ev0, p.ev1), "cudaEventElapsedTime");
+    iv.push_back({a, b});
+    *sum_ms += d;
+    (*count)++;
+    c->tev_pool.push_back(p.ev0);
+    c->tev_pool.push_back(p.ev1);
+  }
+  c->prof.swap(keep);
+  std::sort(iv.begin(), iv.end());
+  double cs = 0, ce = -1e300;
+  for (auto& x : iv) {
+    if (x.first > ce) {
+      if (ce > -1e300) *busy_ms += ce - cs;
+      cs = x.first;
+      ce = x.second;
+    } else if (x.second > ce) {
+      ce = x.second;
+    }
+  }
+  if (ce > -1e300) *busy_ms += ce - cs;
   return DAGRT_OK;
 }
 

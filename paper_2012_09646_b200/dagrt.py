@@ -110,6 +110,9 @@ def lib():
     L.dagrt_stats_reset.argtypes = [ctx]
     L.dagrt_stream_count.argtypes = [ctx, C.POINTER(C.c_int32)]
     L.dagrt_stream_handle.argtypes = [ctx, C.c_int32, C.POINTER(C.c_void_p)]
+    L.dagrt_profile_enable.argtypes = [ctx, C.c_uint32, C.c_int32]
+    L.dagrt_profile_collect.argtypes = [ctx, C.c_uint32, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.dagrt_graph_create.argtypes = [ctx, C.POINTER(C.c_void_p)]
     L.dagrt_graph_add_kernel.argtypes = [ctx, C.c_void_p, C.c_uint32, Dim3, Dim3, C.c_uint32,
                                          C.POINTER(Arg), C.c_int32, C.POINTER(C.c_uint32), C.c_int32,
@@ -127,6 +130,7 @@ def lib():
                "dagrt_host_write", "dagrt_host_map", "dagrt_host_unmap", "dagrt_sync",
                "dagrt_dag_export", "dagrt_dag_clear", "dagrt_trace_export", "dagrt_stats",
                "dagrt_stats_reset", "dagrt_stream_count", "dagrt_stream_handle",
+               "dagrt_profile_enable", "dagrt_profile_collect",
                "dagrt_graph_create", "dagrt_graph_add_kernel", "dagrt_graph_add_copy",
                "dagrt_graph_instantiate", "dagrt_graph_run", "dagrt_graph_destroy"):
         getattr(L, fn).restype = st
@@ -416,3 +420,14 @@ class Context:
 
     def graph(self):
         return Graph(self)
+
+    def profile(self, kernel, on=True):
+        k = self.kernel(kernel) if isinstance(kernel, str) else kernel
+        self._check(lib().dagrt_profile_enable(self._c, k.handle, 1 if on else 0))
+
+    def profile_collect(self, kernel):
+        """(launches, sum of launch ms, busy ms = union of launch intervals)."""
+        k = self.kernel(kernel) if isinstance(kernel, str) else kernel
+        n, s, b = C.c_int32(), C.c_double(), C.c_double()
+        self._check(lib().dagrt_profile_collect(self._c, k.handle, C.byref(n), C.byref(s), C.byref(b)))
+        return n.value, s.value, b.value

@@ -1,0 +1,157 @@
+"""Common scaffolding of the benchmark host programs.
+
+A program owns its device tensors (torch, for memory only), registers them
+with a dagrt Context, and exposes ``run()``: the benchmark's host code written
+sequentially, as the paper's users write it -- kernel
+launches followed by host reads of the sinks, with no streams or events in
+sight.  The same ``run()`` executes under the parallel-async scheduler and
+under the serial-sync policy (the GrCUDA baseline, L559-569).  ``graph()``
+builds the hand-written CUDA Graph baseline (manual dependencies, L1062-1067).
+
+Modes:
+* ``resident`` -- inputs are device-valid before the run; the host reads one
+  element of each sink (the ``Z[0]`` pattern of Fig. 4);
+* ``stream``   -- inputs are rewritten by the host before every run (host
+  newer => H2D inside the run, overlapped by the prefetcher, L356-366) and the
+  host reads whole sink arrays (D2H inside the run).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+import synth
+from .. import dagrt as D
+
+SMS = 148
+
+
+def grid_1d(n_items, block=256, per_thread=1, waves=8):
+    """Grid for a grid-stride kernel: enough CTAs for `n_items`, capped at
+    `waves` CTAs per SM (148 SMs)."""
+    need = max(1, -(-n_items // (block * per_thread)))
+    return int(min(need, SMS * waves))
+
+
+class Program:
+    name = "?"
+    red_bytes = 8 + 8 * 1024  # RedOut: float result, counter, 1024 fp64 partials
+
+    def __init__(self, ctx: D.Context, mode="resident", seed=synth.BASE_SEED, device=None,
+                 share=None):
+        self.ctx = ctx
+        self.mode = mode
+        self.share = share  # another Program whose tensors this one reuses (baseline runs)
+        self.seed = seed
+        self.record = ctx.backend == "record"
+        self.device = torch.device("cpu") if self.record else (device or torch.device("cuda"))
+        self.t = {}        # name -> device tensor
+        self.mirror = {}   # name -> pinned host tensor
+        self.a = {}        # name -> dagrt.Array
+        self.inputs = []   # arrays the host rewrites before every run (stream mode)
+        self.sinks = []    # arrays the host reads at the end of every run
+        self._scalar = (C.c_char * 8)()
+        self.red = set()   # scalar-reduction outputs (the host reads only the result)
+
+    # ---------------------------------------------------------- allocation
+    def alloc(self, name, numel, dtype, mirror=False, zero=False, nbytes=None):
+        if self.share is not None and name in self.share.t:
+            t = self.share.t[name]
+            m = self.share.mirror.get(name) if mirror else None
+            if mirror and m is None:
+                m = torch.empty(t.numel(), dtype=t.dtype, pin_memory=not self.record)
+                m.copy_(t.cpu() if self.record else t)
+            if m is not None:
+                self.mirror[name] = m
+            self.t[name] = t
+            self.a[name] = self.ctx.register_tensor(name, t, m)
+            return t
+        if nbytes is not None:
+            t = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        elif zero:
+            t = torch.zeros(numel, dtype=dtype, device=self.device)
+        else:
+            t = torch.empty(numel, dtype=dtype, device=self.device)
+        m = None
+        if mirror:
+            m = torch.empty(t.numel(), dtype=t.dtype, pin_memory=not self.record)
+            self.mirror[name] = m
+        self.t[name] = t
+        self.a[name] = self.ctx.register_tensor(name, t, m)
+        return t
+
+    def alloc_red(self, name):
+        """Scalar-reduction output: RedOut layout (see csrc/kcommon.cuh)."""
+        self.red.add(name)
+        return self.alloc(name, 0, None, mirror=self.mode == "stream", nbytes=self.red_bytes)
+
+    def fill(self, name, spec, set_index=0):
+        """Seeded input (synth) into the device tensor; stream mode: and its mirror."""
+        if self.record or (self.share is not None and name in self.share.t
+                           and (name not in self.mirror or name in self.share.mirror)):
+            return
+        import synth.gpu as sg
+        sg.fill_tensor(self.t[name].view(-1), self.seed + set_index, name, spec)
+        if name in self.mirror:
+            self.mirror[name].copy_(self.t[name].view(self.mirror[name].dtype).view(-1))
+
+    def upload(self, name, host_array):
+        """Static data written once from the host (weights, graph)."""
+        src = torch.from_numpy(host_array).reshape(-1)
+        if self.record:
+            return
+        self.t[name].view(src.dtype).copy_(src)
+
+    # ---------------------------------------------------------- the run
+    def begin_run(self):
+        """Stream mode: the host writes fresh inputs (host copy becomes newer)."""
+        if self.mode == "stream":
+            for n in self.inputs:
+                self.ctx.host_map(self.a[n], D.W)
+                self.ctx.host_unmap(self.a[n])
+
+    def end_run(self):
+        """Host reads of the sinks: one element (resident) or whole arrays (stream)."""
+        for n in self.sinks:
+            arr = self.a[n]
+            if self.mode == "stream" and n not in self.red:
+                self.ctx.host_map(arr, D.R)
+                self.ctx.host_unmap(arr)
+            else:
+                self.ctx.host_read(arr, C.addressof(self._scalar), 0, min(4, arr.nbytes))
+
+    def run(self):
+        self.begin_run()
+        self.launch_all()
+        self.end_run()
+
+    def launch_all(self):
+        raise NotImplementedError
+
+    # ---------------------------------------------------------- baseline
+    def graph(self):
+        """Hand-written CUDA graph with manual dependencies (no inference)."""
+        raise NotImplementedError
+
+    def graph_io(self, g):
+        """Stream mode: H2D nodes for inputs; returns {input name: node}."""
+        if self.mode != "stream":
+            return {}
+        return {n: g.copy(self.a[n], "h2d") for n in self.inputs}
+
+    def graph_sinks(self, g, deps_of, only=None):
+        if self.mode == "stream":
+            for n in (only or self.sinks):
+                g.copy(self.a[n], "d2h", nbytes=4 if n in self.red else None, deps=[deps_of[n]])
+
+    # ---------------------------------------------------------- bytes
+    def kernel_bytes(self):
+        """Algorithmic HBM bytes per vertex: {label: bytes}."""
+        raise NotImplementedError
+
+    def io_bytes(self):
+        h2d = sum(self.t[n].numel() * self.t[n].element_size() for n in self.inputs)
+        d2h = sum(4 if n in self.red else self.t[n].numel() * self.t[n].element_size()
+                  for n in self.sinks)
+        return (h2d, d2h) if self.mode == "stream" else (0, 4 * len(self.sinks))

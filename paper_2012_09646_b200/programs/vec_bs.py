@@ -1,0 +1,98 @@
+"""VEC and Black & Scholes host programs (§V-B, Fig. 4, Fig. 6)."""
+from __future__ import annotations
+
+import torch
+
+import synth
+from .base import Program, grid_1d
+
+# B&S constants (readings R-BS in DESIGN.md; the paper prints none)
+BS_R, BS_V, BS_T, BS_K = 0.08, 0.30, 1.0, 60.0
+
+
+class Vec(Program):
+    """x1 = x^2; y1 = y^2; z = sum(x1 - y1); host reads z[0] (Fig. 4)."""
+    name = "vec"
+
+    def __init__(self, ctx, n=1_000_000, **kw):
+        super().__init__(ctx, **kw)
+        self.n = n
+        stream = self.mode == "stream"
+        self.alloc("x", n, torch.float32, mirror=stream)
+        self.alloc("y", n, torch.float32, mirror=stream)
+        self.alloc("x1", n, torch.float32)
+        self.alloc("y1", n, torch.float32)
+        self.alloc_red("z")
+        self.inputs, self.sinks = ["x", "y"], ["z"]
+        a = self.a
+        g = grid_1d(n, 256, 8, waves=8)
+        self.L = [
+            ctx.prepare("square", g, 256, [a["x"], a["x1"], n]),
+            ctx.prepare("square", g, 256, [a["y"], a["y1"], n]),
+            ctx.prepare("reduce_diff", min(g, 1024), 256, [a["x1"], a["y1"], a["z"], n]),
+        ]
+
+    def load_inputs(self, set_index=0):
+        spec = synth.spec_vec(self.n)
+        self.fill("x", spec["x"], set_index)
+        self.fill("y", spec["y"], set_index)
+
+    def launch_all(self):
+        for L in self.L:
+            L()
+
+    def result(self):
+        return float(self.t["z"][:4].view(torch.float32)[0])
+
+    def graph(self):
+        g = self.ctx.graph()
+        io = self.graph_io(g)
+        sx = g.kernel(self.L[0], deps=[io["x"]] if io else [])
+        sy = g.kernel(self.L[1], deps=[io["y"]] if io else [])
+        r = g.kernel(self.L[2], deps=[sx, sy])
+        self.graph_sinks(g, {"z": r})
+        g.instantiate()
+        return g
+
+    def kernel_bytes(self):
+        n = self.n * 4
+        return {"square_x": 2 * n, "square_y": 2 * n, "reduce_diff": 2 * n}
+
+
+class BlackScholes(Program):
+    """10 independent pricing kernels (L865-870); host reads each price vector."""
+    name = "bs"
+
+    def __init__(self, ctx, n=10_000_000, nvec=synth.BS_NVEC, **kw):
+        super().__init__(ctx, **kw)
+        self.n, self.nvec = n, nvec
+        stream = self.mode == "stream"
+        for i in range(nvec):
+            self.alloc(f"s{i}", n, torch.float64, mirror=stream)
+            self.alloc(f"c{i}", n, torch.float64, mirror=stream)
+        self.inputs = [f"s{i}" for i in range(nvec)]
+        self.sinks = [f"c{i}" for i in range(nvec)]
+        g = grid_1d(n, 256, 2, waves=8)
+        self.L = [ctx.prepare("bs", g, 256, [self.a[f"s{i}"], self.a[f"c{i}"], n,
+                                              BS_R, BS_V, BS_T, BS_K]) for i in range(nvec)]
+
+    def load_inputs(self, set_index=0):
+        spec = synth.spec_bs(self.n, self.nvec)
+        for i in range(self.nvec):
+            self.fill(f"s{i}", spec[f"s{i}"], set_index)
+
+    def launch_all(self):
+        for L in self.L:
+            L()
+
+    def graph(self):
+        g = self.ctx.graph()
+        io = self.graph_io(g)
+        for i, L in enumerate(self.L):
+            k = g.kernel(L, deps=[io[f"s{i}"]] if io else [])
+            self.graph_sinks(g, {f"c{i}": k}, only=[f"c{i}"])
+        g.instantiate()
+        return g
+
+    def kernel_bytes(self):
+        return {f"bs{i}": 16 * self.n for i in range(self.nvec)}

@@ -1,0 +1,142 @@
+"""GPU parity (B200): VEC and B&S through the C ABI vs the fp64 oracle.
+
+Tolerances (north_star): fp32 elementwise
+|g-o| <= 1e-4|o| + 1e-4 rms(o); reductions 1e-3 relative; fp64 B&S
+1e-10 relative + 1e-12 absolute.  DAG edge sets bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import bs as obs
+from oracle import dag as odag
+from oracle import vec as ovec
+from paper_2012_09646_b200 import dagrt as D
+from paper_2012_09646_b200.programs import BlackScholes, Vec
+
+pytestmark = pytest.mark.gpu
+
+
+def f32_close(g, o):
+    o = np.asarray(o, np.float64)
+    g = np.asarray(g, np.float64)
+    rms = np.sqrt(np.mean(o * o)) if o.size else 0.0
+    return np.all(np.abs(g - o) <= 1e-4 * np.abs(o) + 1e-4 * rms)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = D.Context(device=0, record_dag=True)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("n", [1, 5, 1000, 100_003, 1_000_000])
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+def test_vec_parity(ctx, n, mode):
+    p = Vec(ctx, n=n, mode=mode)
+    p.load_inputs(1)
+    p.run()
+    ctx.sync()
+    spec = synth.spec_vec(n)
+    x = synth.draw(p.seed + 1, "x", spec["x"])
+    y = synth.draw(p.seed + 1, "y", spec["y"])
+    x1, y1, z = ovec.vec(x, y)
+    assert f32_close(p.t["x1"].cpu().numpy(), x1)
+    assert f32_close(p.t["y1"].cpu().numpy(), y1)
+    assert abs(p.result() - z) <= 1e-3 * abs(z) + 1e-30
+
+
+def test_vec_closed_form(ctx):
+    """x_i = 1/(i+1), y_i = 2/(i+1): z = -3 H_N^(2) (fp32 inputs rounded)."""
+    n = 1_000_000
+    p = Vec(ctx, n=n)
+    i = torch.arange(n, dtype=torch.float64)
+    p.t["x"].copy_((1.0 / (i + 1)).float())
+    p.t["y"].copy_((2.0 / (i + 1)).float())
+    p.run()
+    ctx.sync()
+    x = (1.0 / (np.arange(n) + 1.0)).astype(np.float32)
+    y = (2.0 / (np.arange(n) + 1.0)).astype(np.float32)
+    z = ovec.vec(x, y)[2]
+    assert abs(p.result() - z) <= 1e-6 * abs(z)
+    assert abs(p.result() - (-4.934799200546)) < 1e-3
+
+
+def test_vec_dag_matches_oracle(ctx):
+    ctx.dag_clear()
+    p = Vec(ctx, n=4096)
+    p.load_inputs(0)
+    p.run()
+    verts, edges = ctx.dag()
+    tr = [("launch", "square", [("x", "R"), ("x1", "O")]),
+          ("launch", "square", [("y", "R"), ("y1", "O")]),
+          ("launch", "reduce_diff", [("x1", "R"), ("y1", "R"), ("z", "O")]),
+          ("host", "z", "R", 0, 4)]
+    o = odag.build_dag(tr)
+    assert edges == o.edges
+    assert [(v[2], v[3]) for v in verts] == [(v[3], v[4]) for v in o.vertices]
+
+
+@pytest.mark.parametrize("n", [1, 3, 4099, 1_000_001])
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+def test_bs_parity(ctx, n, mode):
+    p = BlackScholes(ctx, n=n, mode=mode)
+    p.load_inputs(2)
+    p.run()
+    ctx.sync()
+    sp = synth.spec_bs(n)
+    for i in range(synth.BS_NVEC):
+        ref = obs.call(synth.draw(p.seed + 2, f"s{i}", sp[f"s{i}"]))
+        out = p.t[f"c{i}"].cpu().numpy()
+        err = np.abs(out - ref) - (1e-10 * np.abs(ref) + 1e-12)
+        assert np.all(err <= 0), (i, float(np.max(err)))
+        if mode == "stream":
+            assert np.array_equal(p.mirror[f"c{i}"].numpy(), out)
+
+
+def test_bs_full_size_sampled(ctx):
+    """BASELINE configs[1] size, launch config of bench.py; 20k sampled options."""
+    n = 10_000_000
+    p = BlackScholes(ctx, n=n)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(n, 20000, replace=False))
+    idx[-1] = n - 1
+    sp = synth.spec_bs(n)
+    for i in range(synth.BS_NVEC):
+        ref = obs.call(synth.draw(p.seed, f"s{i}", sp[f"s{i}"], idx))
+        out = p.t[f"c{i}"][torch.from_numpy(idx).cuda()].cpu().numpy()
+        assert np.all(np.abs(out - ref) <= 1e-10 * np.abs(ref) + 1e-12)
+    del p
+
+
+def test_bs_streams_and_serial_policy(ctx):
+    ctx.dag_clear()
+    p = BlackScholes(ctx, n=1000)
+    p.load_inputs(0)
+    p.run()
+    verts, edges = ctx.dag()
+    ks = [v for v in verts if v[1] == "kernel"]
+    assert sorted(v[3] for v in ks) == list(range(10))
+    assert len(edges) == 10 and all(e[1] - e[0] == 10 for e in edges)
+    sctx = D.Context(device=0, policy="serial")
+    sp = BlackScholes(sctx, n=1000, share=p)
+    sp.run()
+    sctx.sync()
+    sctx.close()
+
+
+def test_graph_baseline_matches(ctx):
+    p = Vec(ctx, n=77777)
+    p.load_inputs(3)
+    p.run()
+    ctx.sync()
+    z1 = p.result()
+    p.t["z"][:4].zero_()
+    g = p.graph()
+    g.run()
+    assert p.result() == z1  # deterministic reduction, same kernels
