@@ -25,13 +25,29 @@ N_CLASSES = 10   # reading; parity unpinned (constant)
 N_FEATURES = 200
 
 
+def norm_stats(X, chunk=1 << 20):
+    """Per-feature population mean and std of integer X (exact int64 column
+    sums of x and x^2, then fp64): mu = S/N, sd = sqrt(Q/N - mu^2); sd = 0 -> 1."""
+    X = np.asarray(X)
+    n = X.shape[0]
+    S = np.zeros(X.shape[1], dtype=np.int64)
+    Q = np.zeros(X.shape[1], dtype=np.int64)
+    for i in range(0, n, chunk):
+        c = X[i:i + chunk].astype(np.int64)
+        S += c.sum(axis=0)
+        Q += (c * c).sum(axis=0)
+    mu = S / n
+    sd = np.sqrt(Q / n - mu * mu)
+    return mu, np.where(sd > 0, sd, 1.0)
+
+
+def apply_norm(X, mu, sd):
+    return (np.asarray(X, dtype=np.float64) - mu) / sd
+
+
 def norm(X):
     """NORM: per-feature standardisation over rows (population std)."""
-    X = np.asarray(X, dtype=np.float64)
-    mu = X.mean(axis=0)
-    sd = np.sqrt((X * X).mean(axis=0) - mu * mu)
-    sd = np.where(sd > 0, sd, 1.0)
-    return (X - mu) / sd
+    return apply_norm(X, *norm_stats(X))
 
 
 def mmul(A, Wt):

@@ -1,0 +1,221 @@
+// Deep-learning (DL) kernels for sm_100a (§V-B; Fig. 6
+// L702-710; architecture: DESIGN.md reading R-DL).  NHWC fp32,
+// cross-correlation, zero padding, shared weights for both branches.
+//
+//   conv1: x (H x W x 1)   -> c1 (H1 x W1 x 8),  3x3 stride 2 pad 1, ReLU
+//   pool : c1              -> p  (H1/2 x W1/2 x 8), 2x2 mean, stride 2
+//   conv2: p (H2 x W2 x 8) -> c2 (H3 x W3 x 16), 3x3 stride 2 pad 1, ReLU
+//   concat, dot (dense layer, one output)
+#include "kcommon.cuh"
+
+namespace dagrt {
+
+// CONV (first layer): one thread computes two horizontally adjacent output
+// pixels x 8 channels.  Inputs: per tap row a float4 (columns 4j..4j+3) and
+// column 4j-1 taken from the neighbouring lane (shuffle) -> 3 LDG.128 per
+// thread-row; outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
+__global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
+                                               const float* __restrict__ w,
+                                               float* __restrict__ out, int H, int W) {
+  const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
+  float wr[72];
+#pragma unroll
+  for (int i = 0; i < 72; ++i) wr[i] = __ldg(w + i);
+  const int pairs = (W1 + 1) / 2;  // output column pairs per row
+  const long long total = (long long)H1 * pairs;
+  const bool vec = ((W & 3) == 0) && aligned16(x);
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       id - threadIdx.x < total;  // whole warps stay in the loop (shuffles)
+       id += (long long)gridDim.x * blockDim.x) {
+    const bool live = id < total;
+    const int p = live ? (int)(id / pairs) : 0;
+    const int j = live ? (int)(id % pairs) : 0;  // columns q = 2j, 2j+1 -> input cols 4j-1..4j+3
+    float v[3][5];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int y = 2 * p + a - 1;
+      const bool rowok = live && y >= 0 && y < H;
+      const float* row = x + (size_t)(rowok ? y : 0) * W;
+      float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int c0 = 4 * j;
+      if (rowok) {
+        if (vec && c0 + 3 < W) {
+          q4 = __ldg(reinterpret_cast<const float4*>(row + c0));
+        } else {
+          if (c0 + 0 < W) q4.x = row[c0 + 0];
+          if (c0 + 1 < W) q4.y = row[c0 + 1];
+          if (c0 + 2 < W) q4.z = row[c0 + 2];
+          if (c0 + 3 < W) q4.w = row[c0 + 3];
+        }
+      }
+      // column 4j-1: the .w of the lane handling pair j-1 on the same row,
+      // unless this lane is the first of its row segment in the warp
+      float left = __shfl_up_sync(0xffffffffu, q4.w, 1);
+      const int prev_lane_ok = ((threadIdx.x & 31) != 0) && (j != 0);
+      if (!prev_lane_ok) left = (rowok && c0 - 1 >= 0) ? row[c0 - 1] : 0.f;
+      v[a][0] = left;
+      v[a][1] = q4.x;
+      v[a][2] = q4.y;
+      v[a][3] = q4.z;
+      v[a][4] = q4.w;
+    }
+    if (!live) continue;
+    float o[2][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const float ww = wr[k * 9 + a * 3 + b];
+          s0 = fmaf(ww, v[a][b], s0);      // q = 2j   -> cols 4j-1+b
+          s1 = fmaf(ww, v[a][b + 2], s1);  // q = 2j+1 -> cols 4j+1+b
+        }
+      o[0][k] = fmaxf(s0, 0.f);
+      o[1][k] = fmaxf(s1, 0.f);
+    }
+    float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W1 + 2 * j) * 8);
+    dst[0] = make_float4(o[0][0], o[0][1], o[0][2], o[0][3]);
+    dst[1] = make_float4(o[0][4], o[0][5], o[0][6], o[0][7]);
+    if (2 * j + 1 < W1) {
+      dst[2] = make_float4(o[1][0], o[1][1], o[1][2], o[1][3]);
+      dst[3] = make_float4(o[1][4], o[1][5], o[1][6], o[1][7]);
+    }
+  }
+}
+
+// POOL: 2x2 mean, stride 2, 8 channels (two float4 per pixel).
+__global__ void __launch_bounds__(256) k_pool(const float* __restrict__ in, float* __restrict__ out,
+                                              int H1, int W1) {
+  const int H2 = H1 / 2, W2 = W1 / 2;
+  const long long total = (long long)H2 * W2 * 2;  // half-pixels (4 channels each)
+  const float4* src = reinterpret_cast<const float4*>(in);
+  float4* dst = reinterpret_cast<float4*>(out);
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
+       id += (long long)gridDim.x * blockDim.x) {
+    const long long pix = id >> 1;
+    const int h = (int)(id & 1);
+    const int i = (int)(pix / W2), jj = (int)(pix % W2);
+    const size_t r0 = ((size_t)(2 * i) * W1 + 2 * jj) * 2 + h;
+    const size_t r1 = r0 + (size_t)W1 * 2;
+    float4 a = ldg_stream(src + r0), b = ldg_stream(src + r0 + 2);
+    float4 c = ldg_stream(src + r1), d = ldg_stream(src + r1 + 2);
+    float4 o;
+    o.x = 0.25f * (a.x + b.x + c.x + d.x);
+    o.y = 0.25f * (a.y + b.y + c.y + d.y);
+    o.z = 0.25f * (a.z + b.z + c.z + d.z);
+    o.w = 0.25f * (a.w + b.w + c.w + d.w);
+    dst[id] = o;
+  }
+}
+
+// CONV (second layer, 8 -> 16 channels).  One thread per output pixel; the
+// 3x3x8 input patch (18 x LDG.128) stays in registers; weights (16 x 72)
+// in shared memory, read with broadcast 128-bit loads.
+__global__ void __launch_bounds__(256) k_conv2(const float* __restrict__ in,
+                                               const float* __restrict__ w,
+                                               float* __restrict__ out, int H2, int W2) {
+  __shared__ __align__(16) float sw[16 * 72];
+  for (int i = threadIdx.x; i < 16 * 72; i += blockDim.x) sw[i] = w[i];
+  __syncthreads();
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const long long total = (long long)H3 * W3;
+  const float4* src = reinterpret_cast<const float4*>(in);
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
+       id += (long long)gridDim.x * blockDim.x) {
+    const int p = (int)(id / W3), q = (int)(id % W3);
+    float4 v[9][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int y = 2 * p + a - 1, xx = 2 * q + b - 1;
+        if (y >= 0 && y < H2 && xx >= 0 && xx < W2) {
+          const size_t base = ((size_t)y * W2 + xx) * 2;
+          v[a * 3 + b][0] = __ldg(src + base);
+          v[a * 3 + b][1] = __ldg(src + base + 1);
+        } else {
+          v[a * 3 + b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    float o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const float4 w0 = *reinterpret_cast<const float4*>(sw + k * 72 + t * 8);
+        const float4 w1 = *reinterpret_cast<const float4*>(sw + k * 72 + t * 8 + 4);
+        s = fmaf(w0.x, v[t][0].x, s);
+        s = fmaf(w0.y, v[t][0].y, s);
+        s = fmaf(w0.z, v[t][0].z, s);
+        s = fmaf(w0.w, v[t][0].w, s);
+        s = fmaf(w1.x, v[t][1].x, s);
+        s = fmaf(w1.y, v[t][1].y, s);
+        s = fmaf(w1.z, v[t][1].z, s);
+        s = fmaf(w1.w, v[t][1].w, s);
+      }
+      o[k] = fmaxf(s, 0.f);
+    }
+    float4* dst = reinterpret_cast<float4*>(out + (size_t)id * 16);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  }
+}
+
+// CONCAT: z = [a; b]
+__global__ void __launch_bounds__(256) k_concat(const float* __restrict__ a,
+                                                const float* __restrict__ b, float* __restrict__ z,
+                                                long long na, long long nb) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  if (aligned16(a) && aligned16(b) && aligned16(z) && (na & 3) == 0 && (nb & 3) == 0) {
+    const long long a4 = na >> 2, b4 = nb >> 2;
+    const float4* A = reinterpret_cast<const float4*>(a);
+    const float4* B = reinterpret_cast<const float4*>(b);
+    float4* Z = reinterpret_cast<float4*>(z);
+    for (long long i = tid; i < a4 + b4; i += nth) Z[i] = i < a4 ? ldg_stream(A + i) : ldg_stream(B + (i - a4));
+  } else {
+    for (long long i = tid; i < na + nb; i += nth) z[i] = i < na ? a[i] : b[i - na];
+  }
+}
+
+// DOT (dense layer): r = sum_i z_i wd_i, fp64 accumulation, deterministic.
+__global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
+                                             const float* __restrict__ wd, RedOut* r, long long n) {
+  __shared__ double sh[32];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  long long done = 0;
+  if (aligned16(z) && aligned16(wd)) {
+    const long long n4 = n >> 2;
+    const float4* Z = reinterpret_cast<const float4*>(z);
+    const float4* Wd = reinterpret_cast<const float4*>(wd);
+    for (long long i = tid; i < n4; i += nth) {
+      float4 a = ldg_stream(Z + i), b = ldg_stream(Wd + i);
+      acc = fma((double)a.x, (double)b.x, acc);
+      acc = fma((double)a.y, (double)b.y, acc);
+      acc = fma((double)a.z, (double)b.z, acc);
+      acc = fma((double)a.w, (double)b.w, acc);
+    }
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nth) acc = fma((double)z[i], (double)wd[i], acc);
+  double blk = block_reduce(acc, OpAdd(), sh);
+  double total;
+  if (grid_finish(r, blk, OpAdd(), 0.0, &total, sh) && threadIdx.x == 0) r->result = (float)total;
+}
+
+static const Builtin kDl[] = {
+    {"conv1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv2", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"concat", (const void*)k_concat, "const ptr, const ptr, out ptr, sint64, sint64", KF_NONE},
+    {"dot", (const void*)k_dot, "const ptr, const ptr, out ptr, sint64", KF_NONE},
+};
+DAGRT_REGISTER_BUILTINS(kDl);
+
+}  // namespace dagrt

@@ -1,0 +1,277 @@
+// HITS kernels for sm_100a (§V-B; Fig. 6;
+// reading R-HITS in DESIGN.md): 0/1 CSR SpMV, L2 norm, divide.
+//
+// SpMV on a power-law graph (20M rows, average degree 3, hub rows with
+// ~1.5M non-zeros).  The paper used LightSpMV [31] (Kepler-era dynamic row
+// distribution).  On B200 the kernel is a deterministic MERGE-PATH SpMV:
+// the merged sequence of N row-ends and E non-zeros is cut into equal tiles
+// of 2048 items (one CTA each), so every CTA does the same work whatever
+// the degree distribution:
+//   1. two warps locate the tile's (row, nnz) start/end coordinates with a
+//      32-ary merge-path search over row_ptr (5 probes instead of 25);
+//   2. the CTA stages its gathered x[col] values and row ends in shared
+//      memory with coalesced loads;
+//   3. each thread consumes 8 items (binary-searched inside shared memory),
+//      completed rows are written directly;
+//   4. a fixed-shape block scan carries partial row sums across threads;
+//   5. rows spanning several CTAs are finished by the LAST CTA to deposit
+//      its partial (atomic arrival count per row), which adds the partials
+//      in CTA order with a fixed warp tree -> bit-deterministic results,
+//      no spinning, no float atomics.
+// The output array y carries the cross-CTA workspace after its N floats
+// (see spmv_ws_bytes), like the reduction outputs (kcommon.cuh RedOut).
+#include "kcommon.cuh"
+
+namespace dagrt {
+
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvItems = 8;
+constexpr int kSpmvTile = kSpmvThreads * kSpmvItems;  // merge items per CTA
+
+struct SpmvWs {
+  float* part;    // [ncta] partial of the row crossing the CTA's end
+  float* head;    // [ncta] partial of the row crossing the CTA's start (its end part)
+  unsigned* cnt;  // [ncta] arrival counters, indexed by the row's first CTA
+};
+
+__device__ __forceinline__ SpmvWs spmv_ws(float* y, long long n, long long ncta) {
+  uintptr_t base = (uintptr_t)(y + n);
+  base = (base + 15) & ~(uintptr_t)15;
+  SpmvWs w;
+  w.part = reinterpret_cast<float*>(base);
+  w.head = w.part + ncta;
+  w.cnt = reinterpret_cast<unsigned*>(w.head + ncta);
+  return w;
+}
+
+// Merge-path coordinate of diagonal d: rows consumed i (row-end items) and
+// non-zeros consumed j = d - i.  Row-end i precedes nnz j iff row_ptr[i+1] <= j.
+// Executed by one full warp; 32-ary search.
+__device__ __forceinline__ long long warp_merge_search(const int* __restrict__ row_ptr, long long N,
+                                                       long long E, long long d) {
+  const int lane = threadIdx.x & 31;
+  long long lo = d - E > 0 ? d - E : 0;
+  long long hi = d < N ? d : N;
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long p = lo + lane * step;
+    bool pred = false;
+    if (p < hi) pred = (long long)__ldg(row_ptr + p + 1) <= d - p - 1;
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    const int cnt = __popc(b);  // predicate holds on a prefix of the probes
+    const long long nlo = cnt > 0 ? lo + (long long)(cnt - 1) * step + 1 : lo;
+    const long long nhi = min(hi, lo + (long long)cnt * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  const long long p = lo + lane;
+  bool pred = false;
+  if (p < hi) pred = (long long)__ldg(row_ptr + p + 1) <= d - p - 1;
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  return lo + __popc(b);
+}
+
+// Sum v[first..last] (fixed order: lane-strided partial sums, fixed tree) by one warp.
+__device__ __forceinline__ float warp_ordered_sum(const volatile float* v, long long first,
+                                                  long long last) {
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  for (long long k = first + lane; k <= last; k += 32) s += v[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// Deposit `val` for row r (spanning CTAs cs..ce) and finish the row if last.
+// Executed by warp 0 of the CTA.  `is_head` = this CTA is the row's last (ce).
+__device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long long r, long long cs,
+                                             long long ce, long long c, float val, bool is_head) {
+  const int lane = threadIdx.x & 31;
+  unsigned old = 0;
+  if (lane == 0) {
+    if (is_head) ws.head[c] = val;
+    else ws.part[c] = val;
+    __threadfence();
+    old = atomicAdd(ws.cnt + cs, 1u);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == (unsigned)(ce - cs)) {  // last of the (ce - cs + 1) participants
+    __threadfence();
+    float s = warp_ordered_sum(ws.part, cs, ce - 1);
+    if (lane == 0) {
+      s += ((volatile float*)ws.head)[ce];
+      y[r] = s;
+      ws.cnt[cs] = 0;  // reusable by the next launch
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ row_ptr,
+                                                       const int* __restrict__ col,
+                                                       const float* __restrict__ x,
+                                                       float* __restrict__ y, long long N) {
+  __shared__ long long s_coord[4];
+  __shared__ float s_val[kSpmvTile];
+  __shared__ int s_rend[kSpmvTile + 1];
+  __shared__ float s_scan[kSpmvThreads];
+  __shared__ unsigned char s_flag[kSpmvThreads];
+  const long long E = (long long)__ldg(row_ptr + N);
+  const long long total = N + E;
+  const long long ncta = (total + kSpmvTile - 1) / kSpmvTile;
+  const long long c = blockIdx.x;
+  const SpmvWs ws = spmv_ws(y, N, ncta);
+  const int t = threadIdx.x, warp = t >> 5;
+  const long long d0 = c * kSpmvTile;
+  const long long d1 = min(total, d0 + kSpmvTile);
+  if (d0 >= total) return;  // uniform per CTA
+
+  if (warp < 2) {
+    const long long d = warp == 0 ? d0 : d1;
+    const long long i = warp_merge_search(row_ptr, N, E, d);
+    if ((t & 31) == 0) { s_coord[2 * warp] = i; s_coord[2 * warp + 1] = d - i; }
+  }
+  __syncthreads();
+  const long long i0 = s_coord[0], j0 = s_coord[1], i1 = s_coord[2], j1 = s_coord[3];
+  const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
+  // stage gathered values and row ends (rows i0 .. i1, clamped to N-1)
+  for (int k = t; k < nn; k += kSpmvThreads) s_val[k] = __ldg(x + __ldg(col + j0 + k));
+  const int nre = (int)(min(i1, N - 1) - i0 + 1);
+  for (int k = t; k < nre; k += kSpmvThreads) s_rend[k] = __ldg(row_ptr + i0 + k + 1);
+  __syncthreads();
+
+  // thread-local merge-path search inside the tile (binary, shared memory)
+  const int dl = min(t * kSpmvItems, nn + nr);
+  int lo = max(0, dl - nn), hi = min(dl, nr);
+  while (lo < hi) {
+    const int p = (lo + hi) >> 1;
+    if ((long long)s_rend[p] - j0 <= dl - p - 1) lo = p + 1;
+    else hi = p;
+  }
+  int ri = lo, nj = dl - lo;  // local row index, local nnz index
+  const int de = min(dl + kSpmvItems, nn + nr);
+  float sum = 0.f;
+  bool emitted = false;
+  long long first_row = -1;
+  float first_val = 0.f;
+  for (int it = dl; it < de; ++it) {
+    const bool row_end = (ri < nr) && ((long long)s_rend[ri] - j0 <= nj);
+    if (row_end) {
+      if (!emitted) {
+        emitted = true;
+        first_row = i0 + ri;
+        first_val = sum;
+      } else {
+        y[i0 + ri] = sum;
+      }
+      sum = 0.f;
+      ++ri;
+    } else {
+      sum += s_val[nj];
+      ++nj;
+    }
+  }
+  // block segmented inclusive scan: s(t) = sum(t) + (emitted(t) ? 0 : s(t-1))
+  s_scan[t] = sum;
+  s_flag[t] = emitted ? 1 : 0;
+  __syncthreads();
+  for (int off = 1; off < kSpmvThreads; off <<= 1) {
+    float v = 0.f;
+    unsigned char f = 0;
+    if (t >= off) { v = s_scan[t - off]; f = s_flag[t - off]; }
+    __syncthreads();
+    if (t >= off && !s_flag[t]) { s_scan[t] += v; s_flag[t] = f; }
+    __syncthreads();
+  }
+  // incoming carry for this thread's first emitted row = s(t-1)
+  const float incoming = t > 0 ? s_scan[t - 1] : 0.f;
+  // did the carry chain reach back to the CTA start? (no emission in 0..t-1)
+  __shared__ int s_first_emitter;
+  if (t == 0) s_first_emitter = kSpmvThreads;
+  __syncthreads();
+  if (emitted) atomicMin(&s_first_emitter, t);
+  __syncthreads();
+  const int fe = s_first_emitter;
+  __shared__ float s_head_val;
+  if (emitted) {
+    const float v = first_val + incoming;
+    bool spans = false;
+    if (t == fe && first_row == i0) {
+      const long long rs = __ldg(row_ptr + i0);
+      spans = ((i0 + rs) / kSpmvTile) < c;  // row started in an earlier CTA
+    }
+    if (spans) s_head_val = v;
+    else y[first_row] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // (a) row i0 crossing the CTA start and ending here
+    if (fe < kSpmvThreads && i0 < N) {
+      const long long rs = __ldg(row_ptr + i0), re = __ldg(row_ptr + i0 + 1);
+      const long long cs = (i0 + rs) / kSpmvTile, ce = (i0 + re) / kSpmvTile;
+      if (cs < c && ce == c) spmv_deposit(ws, y, i0, cs, ce, c, s_head_val, true);
+    }
+    // (b) carry row i1 crossing the CTA end
+    if (i1 < N) {
+      const long long rs = __ldg(row_ptr + i1), re = __ldg(row_ptr + i1 + 1);
+      const long long cs = (i1 + rs) / kSpmvTile, ce = (i1 + re) / kSpmvTile;
+      if (ce > c && cs <= c) {
+        const float carry = s_scan[kSpmvThreads - 1];
+        spmv_deposit(ws, y, i1, cs, ce, c, carry, false);
+      }
+    }
+  }
+}
+
+// SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
+__global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, RedOut* out,
+                                                long long n) {
+  __shared__ double sh[32];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  long long done = 0;
+  if (aligned16(v)) {
+    const long long n4 = n >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    for (long long i = tid; i < n4; i += nth) {
+      float4 a = ldg_stream(v4 + i);
+      acc += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
+    }
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];
+  double blk = block_reduce(acc, OpAdd(), sh);
+  double total;
+  if (grid_finish(out, blk, OpAdd(), 0.0, &total, sh) && threadIdx.x == 0)
+    out->result = (float)sqrt(total);
+}
+
+// DIV node: out = v / ||v|| (zeros if the norm is 0).
+__global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
+                                                const RedOut* __restrict__ nrm,
+                                                float* __restrict__ out, long long n) {
+  const float s = nrm->result;
+  const float is = s > 0.f ? 1.f / s : 0.f;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (aligned16(v) && aligned16(out)) {
+    const long long n4 = n >> 2;
+    for (long long i = tid; i < n4; i += nth) {
+      float4 a = ldg_stream(reinterpret_cast<const float4*>(v) + i);
+      a.x *= is; a.y *= is; a.z *= is; a.w *= is;
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nth) out[i] = v[i] * is;
+}
+
+static const Builtin kHits[] = {
+    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE},
+    {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE},
+};
+DAGRT_REGISTER_BUILTINS(kHits);
+
+}  // namespace dagrt

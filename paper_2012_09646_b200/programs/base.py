@@ -103,6 +103,20 @@ class Program:
             return
         self.t[name].view(src.dtype).copy_(src)
 
+    def load_inputs(self, set_index=0):
+        """Seeded inputs into HBM (and mirrors), then a device-wide sync so
+        torch's asynchronous allocations/zero-fills (on torch's stream) are
+        complete before any dagrt stream touches the memory."""
+        self._inputs(set_index)
+        self.settle()
+
+    def _inputs(self, set_index):
+        raise NotImplementedError
+
+    def settle(self):
+        if not self.record:
+            torch.cuda.synchronize()
+
     # ---------------------------------------------------------- the run
     def begin_run(self):
         """Stream mode: the host writes fresh inputs (host copy becomes newer)."""

@@ -1,0 +1,190 @@
+"""HITS and DL host programs (§V-B; Fig. 6)."""
+from __future__ import annotations
+
+import math
+
+import torch
+
+import synth
+from .base import Program, grid_1d
+
+HITS_ITERS = 10          # reading; parity unpinned (constant)
+SPMV_TILE = 256 * 8      # merge items per CTA (csrc/kernels_hits.cu)
+
+
+def spmv_out_bytes(n, e):
+    ncta = -(-(n + e) // SPMV_TILE)
+    return 4 * n + 16 + 12 * ncta, max(1, ncta)
+
+
+class Hits(Program):
+    """HITS hub/authority iteration with two SpMV branches per iteration (L882-886)."""
+    name = "hits"
+
+    def __init__(self, ctx, n=20_000_000, e=60_000_000, iters=HITS_ITERS, graph=None, **kw):
+        super().__init__(ctx, **kw)
+        self.n, self.iters = n, iters
+        if graph is None:
+            src = self.share.csr if self.share is not None else None
+            graph = src if src is not None else synth.powerlaw_graph(self.seed, n, e)
+        self.csr = graph
+        rp, ci, rpt, cit = graph
+        self.e = int(rp[-1])
+        stream = self.mode == "stream"
+        for name, arr in (("rp", rp), ("ci", ci), ("rpt", rpt), ("cit", cit)):
+            self.alloc(name, max(1, arr.size), torch.int32)
+            if arr.size:
+                self.upload(name, arr)
+        self.alloc("a1", n, torch.float32, mirror=stream)
+        self.alloc("h1", n, torch.float32, mirror=stream)
+        ob, self.ncta = spmv_out_bytes(n, self.e)
+        self.alloc("a2", 0, None, nbytes=ob)
+        self.alloc("h2", 0, None, nbytes=ob)
+        self.alloc_red("an")
+        self.alloc_red("hn")
+        self.inputs, self.sinks = ["a1", "h1"], ["a1", "h1"]
+        a = self.a
+        P = ctx.prepare
+        ge = grid_1d(n, 256, 4)
+        gr = min(grid_1d(n, 256, 8), 1024)
+        self.it = [
+            P("spmv", self.ncta, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
+            P("spmv", self.ncta, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
+            P("l2norm", gr, 256, [a["a2"], a["an"], n]),
+            P("l2norm", gr, 256, [a["h2"], a["hn"], n]),
+            P("divide", ge, 256, [a["a2"], a["an"], a["a1"], n]),
+            P("divide", ge, 256, [a["h2"], a["hn"], a["h1"], n]),
+        ]
+
+    def _inputs(self, set_index=0):
+        v = 1.0 / math.sqrt(self.n) if self.n else 0.0
+        for name in ("a1", "h1"):
+            if not self.record:
+                self.t[name].fill_(v)
+            if name in self.mirror:
+                self.mirror[name].fill_(v)
+
+    def launch_all(self):
+        for _ in range(self.iters):
+            for L in self.it:
+                L()
+
+    def graph(self):
+        g = self.ctx.graph()
+        io = self.graph_io(g)
+        prev = {"a1": [io["a1"]] if io else [], "h1": [io["h1"]] if io else []}
+        sa = sh = sma = smh = da = dh = None
+        for k in range(self.iters):
+            L = self.it
+            # a2 = A^T h1 needs h1 (div_h of the previous iteration) and the
+            # previous readers of a2 (sum_a, div_a) to be done.
+            sa = g.kernel(L[0], ([dh] if dh is not None else prev["h1"]) + ([da] if da is not None else []))
+            sh = g.kernel(L[1], ([da] if da is not None else prev["a1"]) + ([dh] if dh is not None else []))
+            sma = g.kernel(L[2], [sa] + ([da] if da is not None else []))
+            smh = g.kernel(L[3], [sh] + ([dh] if dh is not None else []))
+            da = g.kernel(L[4], [sa, sh, sma])
+            dh = g.kernel(L[5], [sa, sh, smh])
+        self.graph_sinks(g, {"a1": da, "h1": dh})
+        g.instantiate()
+        return g
+
+    def kernel_bytes(self):
+        n, e = self.n, self.e
+        sp = 4 * (n + 1) + 4 * e + 4 * n + 4 * n
+        out = {}
+        for k in range(self.iters):
+            out.update({f"spmv_a{k}": sp, f"spmv_h{k}": sp, f"l2norm_a{k}": 4 * n,
+                        f"l2norm_h{k}": 4 * n, f"divide_a{k}": 8 * n, f"divide_h{k}": 8 * n})
+        return out
+
+    def vec(self, name):
+        return self.t[name][: 4 * self.n].view(torch.float32) if self.t[name].dtype == torch.uint8 \
+            else self.t[name]
+
+
+def dl_shapes(h, w):
+    h1, w1 = (h + 1) // 2, (w + 1) // 2
+    h2, w2 = h1 // 2, w1 // 2
+    h3, w3 = (h2 + 1) // 2, (w2 + 1) // 2
+    return (h1, w1), (h2, w2), (h3, w3)
+
+
+class DeepLearning(Program):
+    """Two-branch CNN projecting two images, merged by a dense layer (L887-891)."""
+    name = "dl"
+
+    def __init__(self, ctx, h=16384, w=16384, **kw):
+        super().__init__(ctx, **kw)
+        self.h, self.w = h, w
+        (h1, w1), (h2, w2), (h3, w3) = dl_shapes(h, w)
+        self.shapes = ((h1, w1), (h2, w2), (h3, w3))
+        stream = self.mode == "stream"
+        nz = 2 * h3 * w3 * 16
+        self.alloc("x", h * w, torch.float32, mirror=stream)
+        self.alloc("y", h * w, torch.float32, mirror=stream)
+        self.alloc("w1", 72, torch.float32)
+        self.alloc("w2", 16 * 72, torch.float32)
+        self.alloc("wd", max(1, nz), torch.float32)
+        for b in ("x", "y"):
+            self.alloc(f"c1{b}", max(1, h1 * w1 * 8), torch.float32)
+            self.alloc(f"p{b}", max(1, h2 * w2 * 8), torch.float32)
+            self.alloc(f"c2{b}", max(1, h3 * w3 * 16), torch.float32)
+        self.alloc("z", max(1, nz), torch.float32)
+        self.alloc_red("r")
+        self.inputs, self.sinks = ["x", "y"], ["r"]
+        self.nz = nz
+        a = self.a
+        P = ctx.prepare
+        g1 = grid_1d(h1 * ((w1 + 1) // 2), 256)
+        gp = grid_1d(h2 * w2 * 2, 256)
+        g2 = grid_1d(h3 * w3, 256)
+        gc = grid_1d(nz // 4 + 1, 256)
+        self.L = [
+            P("conv1", g1, 256, [a["x"], a["w1"], a["c1x"], h, w]),
+            P("conv1", g1, 256, [a["y"], a["w1"], a["c1y"], h, w]),
+            P("pool", gp, 256, [a["c1x"], a["px"], h1, w1]),
+            P("pool", gp, 256, [a["c1y"], a["py"], h1, w1]),
+            P("conv2", g2, 256, [a["px"], a["w2"], a["c2x"], h2, w2]),
+            P("conv2", g2, 256, [a["py"], a["w2"], a["c2y"], h2, w2]),
+            P("concat", gc, 256, [a["c2x"], a["c2y"], a["z"], nz // 2, nz // 2]),
+            P("dot", min(gc, 1024), 256, [a["z"], a["wd"], a["r"], nz]),
+        ]
+
+    def _inputs(self, set_index=0):
+        spec = synth.spec_dl(self.h, self.w)
+        self.fill("x", spec["x"], set_index)
+        self.fill("y", spec["y"], set_index)
+        for k in ("w1", "w2", "wd"):
+            self.fill(k, spec[k], 0)
+
+    def launch_all(self):
+        for L in self.L:
+            L()
+
+    def graph(self):
+        g = self.ctx.graph()
+        io = self.graph_io(g)
+        L = self.L
+        cx = g.kernel(L[0], [io["x"]] if io else [])
+        cy = g.kernel(L[1], [io["y"]] if io else [])
+        px = g.kernel(L[2], [cx])
+        py = g.kernel(L[3], [cy])
+        c2x = g.kernel(L[4], [px])
+        c2y = g.kernel(L[5], [py])
+        cc = g.kernel(L[6], [c2x, c2y])
+        dt = g.kernel(L[7], [cc])
+        self.graph_sinks(g, {"r": dt})
+        g.instantiate()
+        return g
+
+    def kernel_bytes(self):
+        h, w = self.h, self.w
+        (h1, w1), (h2, w2), (h3, w3) = self.shapes
+        c1 = 4 * h * w + 32 * h1 * w1
+        pl = 32 * h1 * w1 + 32 * h2 * w2
+        c2 = 32 * h2 * w2 + 64 * h3 * w3
+        return {"conv1_x": c1, "conv1_y": c1, "pool_x": pl, "pool_y": pl, "conv2_x": c2,
+                "conv2_y": c2, "concat": 8 * self.nz, "dot": 8 * self.nz}
+
+    def result(self):
+        return float(self.t["r"][:4].view(torch.float32)[0])

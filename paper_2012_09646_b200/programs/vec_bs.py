@@ -32,7 +32,7 @@ class Vec(Program):
             ctx.prepare("reduce_diff", min(g, 1024), 256, [a["x1"], a["y1"], a["z"], n]),
         ]
 
-    def load_inputs(self, set_index=0):
+    def _inputs(self, set_index=0):
         spec = synth.spec_vec(self.n)
         self.fill("x", spec["x"], set_index)
         self.fill("y", spec["y"], set_index)
@@ -76,7 +76,7 @@ class BlackScholes(Program):
         self.L = [ctx.prepare("bs", g, 256, [self.a[f"s{i}"], self.a[f"c{i}"], n,
                                               BS_R, BS_V, BS_T, BS_K]) for i in range(nvec)]
 
-    def load_inputs(self, set_index=0):
+    def _inputs(self, set_index=0):
         spec = synth.spec_bs(self.n, self.nvec)
         for i in range(self.nvec):
             self.fill(f"s{i}", spec[f"s{i}"], set_index)

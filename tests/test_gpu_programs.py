@@ -1,0 +1,341 @@
+"""GPU parity (B200): IMG, ML, HITS, DL through the C ABI vs the fp64 oracle,
+at small ragged sizes (several tiles + tails) and at BASELINE.json full size
+(sampled outputs / properties), plus the synth GPU twin vs the host generator.
+
+Criteria (north_star): DAG edges bit-exact;
+integer labels bit-exact except oracle near-ties (top-2 gap <= 1e-5, which
+must pick one of the tied classes); fp32 elementwise |g-o| <= 1e-4|o| +
+1e-4 rms(o); fp32 reductions 1e-3 relative.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+import synth.gpu as sg
+from oracle import dl as odl
+from oracle import hits as ohits
+from oracle import img as oimg
+from oracle import ml as oml
+from paper_2012_09646_b200 import dagrt as D
+from paper_2012_09646_b200.programs import DeepLearning, Hits, Images, MLEnsemble
+
+pytestmark = pytest.mark.gpu
+
+
+def close(g, o, rel=1e-4):
+    o = np.asarray(o, np.float64)
+    g = np.asarray(g, np.float64)
+    rms = np.sqrt(np.mean(o * o)) if o.size else 0.0
+    bad = np.abs(g - o) > rel * np.abs(o) + rel * rms
+    return not bad.any(), (int(bad.sum()), float(np.max(np.abs(g - o))) if o.size else 0.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = D.Context(device=0, record_dag=True)
+    yield c
+    c.close()
+
+
+# ------------------------------------------------------------------ synth twin
+@pytest.mark.parametrize("kind,args,dtype", [
+    (synth.KIND_F32_UNIT, (), torch.float32),
+    (synth.KIND_F64_RANGE, (30.0, 90.0), torch.float64),
+    (synth.KIND_I32_BELOW, (10,), torch.int32),
+    (synth.KIND_F32_SYM, (1.0 / math.sqrt(72.0),), torch.float32)])
+def test_synth_gpu_twin_bit_exact(kind, args, dtype):
+    n = 1_000_003
+    t = torch.empty(n, dtype=dtype, device="cuda")
+    spec = (kind, n, args)
+    sg.fill_tensor(t, 77, "arr", spec)
+    assert np.array_equal(t.cpu().numpy(), synth.draw(77, "arr", spec))
+
+
+# ------------------------------------------------------------------ IMG
+@pytest.mark.parametrize("h,w", [(1, 1), (7, 9), (65, 513), (200, 1100), (1024, 1024)])
+def test_img_parity(ctx, h, w):
+    p = Images(ctx, h=h, w=w)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    img = synth.draw(p.seed, "img", synth.spec_img(h, w)["img"]).reshape(h, w)
+    o = oimg.img_pipeline(img)
+    for name in ("bs", "bl", "bu", "ms", "iu", "i2", "i3"):
+        ok, info = close(p.t[name].cpu().numpy().reshape(h, w), o[name])
+        assert ok, (name, info)
+    ok, info = close(p.t["ml"].cpu().numpy().reshape(h, w), o["ml"])
+    assert ok, ("ml", info)
+    mx = float(p.t["mx"][:4].view(torch.float32)[0])
+    mn = float(p.t["mn"][:4].view(torch.float32)[0])
+    assert abs(mx - o["mx"]) <= 1e-4 * abs(o["mx"]) + 1e-6
+    assert abs(mn - o["mn"]) <= 1e-4 * abs(o["mx"]) + 1e-6
+
+
+def _img_chunk_oracle(seed, h, w, r0, r1):
+    """Oracle over rows [r0, r1) of the full image (with a 4-row halo)."""
+    a0, a1 = max(0, r0 - 4), min(h, r1 + 4)
+    spec = synth.spec_img(h, w)["img"]
+    idx = np.arange(a0 * w, a1 * w, dtype=np.uint64)
+    img = synth.draw(seed, "img", spec, idx).reshape(a1 - a0, w).astype(np.float64)
+    # zero padding only at the true image border: pad the halo-less sides
+    bl = oimg.blur(img, *oimg.BLUR_L)
+    ml = oimg.sobel(bl)
+    lo, hi = r0 - a0, r1 - a0
+    return img, ml[lo:hi], (a0, lo, hi)
+
+
+def test_img_full_size_sampled(ctx):
+    """16384^2 (BASELINE configs[2]), bench.py launch configuration: the global
+    extrema over the full oracle sobel mask, and sampled rows of every stage."""
+    h = w = 16384
+    p = Images(ctx, h=h, w=w)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    mx_o, mn_o = -np.inf, np.inf
+    sample_rows = [0, 1, 63, 64, 8191, 16320, 16383]
+    checks = {}
+    for r0 in range(0, h, 512):
+        r1 = min(h, r0 + 512)
+        img, ml, (a0, lo, hi) = _img_chunk_oracle(p.seed, h, w, r0, r1)
+        mx_o = max(mx_o, float(ml.max()))
+        mn_o = min(mn_o, float(ml.min()))
+        for r in sample_rows:
+            if r0 <= r < r1:
+                checks[r] = (img, a0, r - a0)
+    mx = float(p.t["mx"][:4].view(torch.float32)[0])
+    mn = float(p.t["mn"][:4].view(torch.float32)[0])
+    assert abs(mx - mx_o) <= 1e-4 * abs(mx_o)
+    assert abs(mn - mn_o) <= 1e-4 * abs(mx_o)
+    for r, (img, a0, k) in checks.items():
+        bs = oimg.blur(img, *oimg.BLUR_S)
+        bl = oimg.blur(img, *oimg.BLUR_L)
+        bu = oimg.blur(img, *oimg.BLUR_U)
+        ms = oimg.sobel(bs)
+        ml = oimg.extend(oimg.sobel(bl), mx_o, mn_o)
+        iu = oimg.unsharpen(img, bu)
+        i3 = oimg.combine(oimg.combine(iu, bl, ml), bs, ms)
+        for name, ref in (("bs", bs), ("bl", bl), ("ms", ms), ("ml", ml), ("i3", i3)):
+            got = p.t[name][r * w:(r + 1) * w].cpu().numpy()
+            ok, info = close(got, ref[k])
+            assert ok, (name, r, info)
+    del p
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ ML
+def _ml_ref(p, X):
+    pr = {k: v.astype(np.float64) for k, v in p.params.items()}
+    return oml.ml(X, pr["theta"], pr["prior"], pr["W"], pr["b"])
+
+
+def _check_labels(got, o):
+    gap = oml.top2_gap(o["r1"], o["r2"])
+    s = o["r1"] + o["r2"]
+    tied = gap <= 1e-5
+    exact = ~tied
+    assert np.array_equal(got[exact], o["r"][exact])
+    for i in np.nonzero(tied)[0]:
+        assert s[i, got[i]] >= s[i].max() - 1e-5
+    return int(tied.sum())
+
+
+@pytest.mark.parametrize("n", [1, 37, 4099, 100_000])
+def test_ml_parity(ctx, n):
+    p = MLEnsemble(ctx, n=n)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    f, c = p.f, p.c
+    X = synth.draw(p.seed, "X", synth.spec_ml_x(n, f)["X"]).reshape(n, f)
+    o = _ml_ref(p, X)
+    ok, info = close(p.t["Z"].cpu().numpy().reshape(n, f), o["Z"])
+    assert ok, ("Z", info)
+    ok, info = close(p.t["r1"].cpu().numpy().reshape(n, c), o["r1"])
+    assert ok, ("r1", info)
+    ok, info = close(p.t["r2"].cpu().numpy().reshape(n, c), o["r2"])
+    assert ok, ("r2", info)
+    ok, info = close(p.t["l"].cpu().numpy(), o["l"])
+    assert ok, ("lse", info)
+    _check_labels(p.t["r"].cpu().numpy(), o)
+
+
+def test_ml_full_size_sampled(ctx):
+    """10M x 200 (BASELINE configs[3]): exact oracle statistics over all of X
+    (X is generator output, checked bit-equal to the host generator above),
+    then the oracle on 20k sampled rows; NORM moments on all rows."""
+    n, f = 10_000_000, 200
+    p = MLEnsemble(ctx, n=n)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    X = p.t["X"].view(n, f).cpu().numpy()
+    rng = np.random.default_rng(1)
+    rows = np.sort(rng.choice(n, 20000, replace=False))
+    rows[-1] = n - 1
+    spec = synth.spec_ml_x(n, f)["X"]
+    idx = (rows[:, None] * f + np.arange(f)[None, :]).ravel().astype(np.uint64)
+    assert np.array_equal(X[rows], synth.draw(p.seed, "X", spec, idx).reshape(-1, f))
+    mu, sd = oml.norm_stats(X)
+    del X
+    Xs = synth.draw(p.seed, "X", spec, idx).reshape(-1, f)
+    pr = {k: v.astype(np.float64) for k, v in p.params.items()}
+    Z = oml.apply_norm(Xs, mu, sd)
+    r1 = oml.softmax(oml.exp_sub(*(lambda s: (s, oml.lse(s, oml.rowmax(s))))(
+        oml.nb_mmul(Xs, pr["theta"], pr["prior"]))))
+    r2 = oml.softmax(oml.addv(oml.mmul(Z, pr["W"]), pr["b"]))
+    o = {"r1": r1, "r2": r2, "r": oml.argmax(r1, r2)}
+    tr = torch.from_numpy(rows).cuda()
+    ok, info = close(p.t["Z"].view(n, f)[tr].cpu().numpy(), Z)
+    assert ok, ("Z", info)
+    ok, info = close(p.t["r1"].view(n, 10)[tr].cpu().numpy(), r1)
+    assert ok, ("r1", info)
+    ok, info = close(p.t["r2"].view(n, 10)[tr].cpu().numpy(), r2)
+    assert ok, ("r2", info)
+    _check_labels(p.t["r"][tr].cpu().numpy(), o)
+    Zd = p.t["Z"].view(n, f).double()
+    assert torch.allclose(Zd.mean(0), torch.zeros(f, dtype=torch.float64, device="cuda"), atol=1e-5)
+    assert torch.allclose(Zd.std(0, unbiased=False), torch.ones(f, dtype=torch.float64, device="cuda"),
+                          atol=1e-5)
+    del p, Zd
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ HITS
+def _hits_check(p, graph, iters):
+    ctx = p.ctx
+    o = ohits.hits(*graph, iterations=iters)
+    for name in ("a1", "h1"):
+        ok, info = close(p.t[name].cpu().numpy(), o[name])
+        assert ok, (name, info)
+    an = float(p.t["an"][:4].view(torch.float32)[0])
+    hn = float(p.t["hn"][:4].view(torch.float32)[0])
+    assert abs(an - o["norms"][-1][0]) <= 1e-3 * o["norms"][-1][0] + 1e-30
+    assert abs(hn - o["norms"][-1][1]) <= 1e-3 * o["norms"][-1][1] + 1e-30
+    ok, info = close(p.vec("a2").cpu().numpy(), o["a2"])
+    assert ok, ("a2", info)
+
+
+@pytest.mark.parametrize("n,e", [(1, 0), (10, 30), (5000, 15000), (200_000, 600_000)])
+def test_hits_parity(ctx, n, e):
+    graph = synth.powerlaw_graph(5, n, e)
+    p = Hits(ctx, n=n, e=e, iters=3, graph=graph)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    _hits_check(p, graph, 3)
+
+
+def test_hits_star_and_chain():
+    """Hand-made graphs exercising rows spanning many SpMV tiles (a hub with
+    20k out-edges) and empty rows."""
+    c = D.Context(device=0)
+    n = 30000
+    src = np.concatenate([np.zeros(20000, np.int64), np.arange(1, 5000)])
+    dst = np.concatenate([np.arange(1, 20001), np.arange(2, 5001)])
+    import scipy.sparse as sp
+    A = sp.csr_matrix((np.ones(len(src)), (src, dst)), shape=(n, n))
+    A.sort_indices()
+    At = A.T.tocsr()
+    At.sort_indices()
+    graph = (A.indptr.astype(np.int32), A.indices.astype(np.int32),
+             At.indptr.astype(np.int32), At.indices.astype(np.int32))
+    p = Hits(c, n=n, iters=2, graph=graph)
+    p.load_inputs(0)
+    p.run()
+    c.sync()
+    _hits_check(p, graph, 2)
+    c.close()
+
+
+def test_hits_full_size(ctx):
+    """20M-vertex power-law graph (BASELINE configs[4]), 10 iterations, full
+    oracle (every element)."""
+    p = Hits(ctx)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    _hits_check(p, p.csr, p.iters)
+    deg = np.diff(p.csr[0])
+    assert deg.max() > 100_000  # the hub spans many merge-path tiles
+    del p
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ DL
+@pytest.mark.parametrize("h,w", [(1, 1), (9, 9), (19, 23), (64, 64), (515, 517), (1024, 1000)])
+def test_dl_parity(ctx, h, w):
+    p = DeepLearning(ctx, h=h, w=w)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    spec = synth.spec_dl(h, w)
+    x = synth.draw(p.seed, "x", spec["x"]).reshape(h, w)
+    y = synth.draw(p.seed, "y", spec["y"]).reshape(h, w)
+    w1 = synth.draw(p.seed, "w1", spec["w1"])
+    w2 = synth.draw(p.seed, "w2", spec["w2"])
+    wd = synth.draw(p.seed, "wd", spec["wd"])
+    o = odl.dl(x, y, w1, w2, wd)
+    (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
+    for name, shp in (("c1x", (h1, w1s, 8)), ("c1y", (h1, w1s, 8)), ("px", (h2, w2s, 8)),
+                      ("c2x", (h3, w3s, 16)), ("c2y", (h3, w3s, 16))):
+        if np.prod(shp) == 0:
+            continue
+        got = p.t[name][:int(np.prod(shp))].cpu().numpy().reshape(shp)
+        ok, info = close(got, o[name])
+        assert ok, (name, info)
+    if o["z"].size:
+        ok, info = close(p.t["z"][:o["z"].size].cpu().numpy(), o["z"])
+        assert ok, ("z", info)
+        assert abs(p.result() - o["r"]) <= 1e-3 * abs(o["r"]) + 1e-6
+
+
+def test_dl_full_size_sampled(ctx):
+    """2 x 16384^2 (BASELINE configs[4] DL): sampled conv2 outputs from the
+    oracle on local input patches; r against the fp64 dot of the produced z."""
+    h = w = 16384
+    p = DeepLearning(ctx, h=h, w=w)
+    p.load_inputs(0)
+    p.run()
+    ctx.sync()
+    spec = synth.spec_dl(h, w)
+    w1 = synth.draw(p.seed, "w1", spec["w1"])
+    w2 = synth.draw(p.seed, "w2", spec["w2"])
+    (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
+    rng = np.random.default_rng(3)
+    pts = [(0, 0), (h3 - 1, w3s - 1), (0, w3s - 1)] + [tuple(rng.integers(0, h3, 2)) for _ in range(12)]
+    for (pp, qq) in pts:
+        # c2[pp,qq] needs p rows 2pp-1..2pp+1 -> c1 rows 4pp-2..4pp+3 -> x rows 8pp-5..8pp+7
+        ylo, yhi = max(0, 8 * pp - 8), min(h, 8 * pp + 8)
+        xlo, xhi = max(0, 8 * qq - 8), min(w, 8 * qq + 8)
+        ys, xs = np.arange(ylo, yhi), np.arange(xlo, xhi)
+        idx = (ys[:, None] * w + xs[None, :]).ravel().astype(np.uint64)
+        xpatch = synth.draw(p.seed, "x", spec["x"], idx).reshape(len(ys), len(xs))
+        # embed the patch at its true position parity so strides line up
+        c1 = odl.conv3x3s2(np.pad(xpatch, ((ylo % 2, 0), (xlo % 2, 0))), w1.reshape(8, 3, 3, 1))
+        # c1 local index a <-> global row (ylo - ylo%2)/2 + a
+        g0r, g0c = (ylo - ylo % 2) // 2, (xlo - xlo % 2) // 2
+        pool = odl.pool2x2(np.pad(c1, ((g0r % 2, 0), (g0c % 2, 0), (0, 0))))
+        p0r, p0c = (g0r - g0r % 2) // 2, (g0c - g0c % 2) // 2
+        # the needed pool entries lie >= 1 c1 row/col inside the patch, so the
+        # patch's artificial zero border never reaches them
+        acc = np.zeros(16)
+        W2 = w2.reshape(16, 3, 3, 8).astype(np.float64)
+        for a in range(3):
+            for b in range(3):
+                gy, gx = 2 * pp + a - 1, 2 * qq + b - 1
+                if 0 <= gy < h2 and 0 <= gx < w2s:
+                    acc += W2[:, a, b, :] @ pool[gy - p0r, gx - p0c, :]
+        ref = np.maximum(acc, 0.0)
+        got = p.t["c2x"][(pp * w3s + qq) * 16:(pp * w3s + qq + 1) * 16].cpu().numpy()
+        ok, info = close(got, ref)
+        assert ok, ((pp, qq), info, got, ref)
+    z = p.t["z"].double()
+    wd = p.t["wd"].double()
+    r_ref = float((z * wd).sum())
+    assert abs(p.result() - r_ref) <= 1e-3 * abs(r_ref)
+    del p, z, wd
+    torch.cuda.empty_cache()

@@ -55,6 +55,7 @@ def test_vec_closed_form(ctx):
     i = torch.arange(n, dtype=torch.float64)
     p.t["x"].copy_((1.0 / (i + 1)).float())
     p.t["y"].copy_((2.0 / (i + 1)).float())
+    p.settle()
     p.run()
     ctx.sync()
     x = (1.0 / (np.arange(n) + 1.0)).astype(np.float32)
@@ -137,6 +138,7 @@ def test_graph_baseline_matches(ctx):
     ctx.sync()
     z1 = p.result()
     p.t["z"][:4].zero_()
+    p.settle()
     g = p.graph()
     g.run()
     assert p.result() == z1  # deterministic reduction, same kernels
