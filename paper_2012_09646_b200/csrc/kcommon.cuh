@@ -50,6 +50,19 @@ __device__ __forceinline__ T warp_min(T v) {
   return v;
 }
 
+struct OpAdd {
+  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+  template <typename T> __device__ __forceinline__ T identity() const { return T(0); }
+};
+struct OpMax {
+  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
+  template <typename T> __device__ __forceinline__ T identity() const { return -INFINITY; }
+};
+struct OpMin {
+  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a < b ? a : b; }
+  template <typename T> __device__ __forceinline__ T identity() const { return INFINITY; }
+};
+
 // Block-wide reduction in a fixed order (deterministic).  All threads get
 // the result.  blockDim.x must be a multiple of 32, <= 1024.
 template <typename T, typename Op>
@@ -61,7 +74,7 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* sh /* >= 32 */) {
   if (lane == 0) sh[wid] = v;
   __syncthreads();
   if (wid == 0) {
-    T x = lane < nw ? sh[lane] : sh[0];
+    T x = lane < nw ? sh[lane] : op.template identity<T>();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
     if (lane == 0) sh[0] = x;
@@ -71,16 +84,6 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* sh /* >= 32 */) {
   __syncthreads();
   return r;
 }
-
-struct OpAdd {
-  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
-};
-struct OpMax {
-  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
-};
-struct OpMin {
-  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a < b ? a : b; }
-};
 
 // Layout of a scalar-reduction output array ("out ptr" of a reduction
 // vertex): the fp32 result first (what the host reads), then the grid
