@@ -13,6 +13,7 @@ struct Builtin {
   const void* fn;
   const char* signature;
   int32_t flags;
+  int32_t smem_max;  // > 0: opt in to this much dynamic shared memory (bytes)
 };
 
 int register_builtins(const Builtin* table, int n);  // returns n

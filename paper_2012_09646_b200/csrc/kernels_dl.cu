@@ -11,36 +11,33 @@
 namespace dagrt {
 
 // CONV (first layer): one thread computes two horizontally adjacent output
-// pixels x 8 channels.  Inputs: per tap row a float4 (columns 4j..4j+3) and
-// column 4j-1 taken from the neighbouring lane (shuffle) -> 3 LDG.128 per
-// thread-row; outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
+// pixels x 8 channels.  2-D grid: blockIdx.y walks output rows, x covers
+// column pairs (no integer division).  Inputs: per tap row one float4
+// (columns 4j..4j+3) plus column 4j-1 from the neighbouring lane (shuffle);
+// outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
 __global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
                                                const float* __restrict__ w,
                                                float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
+  const int pairs = (W1 + 1) / 2;
   float wr[72];
 #pragma unroll
   for (int i = 0; i < 72; ++i) wr[i] = __ldg(w + i);
-  const int pairs = (W1 + 1) / 2;  // output column pairs per row
-  const long long total = (long long)H1 * pairs;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live_j = j < pairs;
   const bool vec = ((W & 3) == 0) && aligned16(x);
-  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-       id - threadIdx.x < total;  // whole warps stay in the loop (shuffles)
-       id += (long long)gridDim.x * blockDim.x) {
-    const bool live = id < total;
-    const int p = live ? (int)(id / pairs) : 0;
-    const int j = live ? (int)(id % pairs) : 0;  // columns q = 2j, 2j+1 -> input cols 4j-1..4j+3
+  const int c0 = 4 * j;
+  for (int p = blockIdx.y; p < H1; p += gridDim.y) {  // uniform per block
     float v[3][5];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int y = 2 * p + a - 1;
-      const bool rowok = live && y >= 0 && y < H;
+      const bool rowok = live_j && y >= 0 && y < H;
       const float* row = x + (size_t)(rowok ? y : 0) * W;
       float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      const int c0 = 4 * j;
       if (rowok) {
         if (vec && c0 + 3 < W) {
-          q4 = __ldg(reinterpret_cast<const float4*>(row + c0));
+          q4 = ldg_stream(reinterpret_cast<const float4*>(row + c0));
         } else {
           if (c0 + 0 < W) q4.x = row[c0 + 0];
           if (c0 + 1 < W) q4.y = row[c0 + 1];
@@ -48,18 +45,15 @@ __global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
           if (c0 + 3 < W) q4.w = row[c0 + 3];
         }
       }
-      // column 4j-1: the .w of the lane handling pair j-1 on the same row,
-      // unless this lane is the first of its row segment in the warp
       float left = __shfl_up_sync(0xffffffffu, q4.w, 1);
-      const int prev_lane_ok = ((threadIdx.x & 31) != 0) && (j != 0);
-      if (!prev_lane_ok) left = (rowok && c0 - 1 >= 0) ? row[c0 - 1] : 0.f;
+      if ((threadIdx.x & 31) == 0 || j == 0) left = (rowok && c0 > 0) ? row[c0 - 1] : 0.f;
       v[a][0] = left;
       v[a][1] = q4.x;
       v[a][2] = q4.y;
       v[a][3] = q4.z;
       v[a][4] = q4.w;
     }
-    if (!live) continue;
+    if (!live_j) continue;
     float o[2][8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -110,9 +104,11 @@ __global__ void __launch_bounds__(256) k_pool(const float* __restrict__ in, floa
   }
 }
 
-// CONV (second layer, 8 -> 16 channels).  One thread per output pixel; the
-// 3x3x8 input patch (18 x LDG.128) stays in registers; weights (16 x 72)
-// in shared memory, read with broadcast 128-bit loads.
+// CONV (second layer, 8 -> 16 channels).  One thread computes two
+// horizontally adjacent output pixels (2-D grid, no integer division).  Per
+// tap row it loads the 5 input pixels both outputs need (10 x LDG.128) and
+// accumulates 2 x 16 outputs; the 16 x 72 weights sit in shared memory and
+// are read with broadcast 128-bit loads, each reused for the two pixels.
 __global__ void __launch_bounds__(256) k_conv2(const float* __restrict__ in,
                                                const float* __restrict__ w,
                                                float* __restrict__ out, int H2, int W2) {
@@ -120,48 +116,64 @@ __global__ void __launch_bounds__(256) k_conv2(const float* __restrict__ in,
   for (int i = threadIdx.x; i < 16 * 72; i += blockDim.x) sw[i] = w[i];
   __syncthreads();
   const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
-  const long long total = (long long)H3 * W3;
+  const int pairs = (W3 + 1) / 2;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= pairs) return;
   const float4* src = reinterpret_cast<const float4*>(in);
-  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
-       id += (long long)gridDim.x * blockDim.x) {
-    const int p = (int)(id / W3), q = (int)(id % W3);
-    float4 v[9][2];
+  for (int p = blockIdx.y; p < H3; p += gridDim.y) {
+    float o[2][16];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < 16; ++k) { o[0][k] = 0.f; o[1][k] = 0.f; }
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const int y = 2 * p + a - 1, xx = 2 * q + b - 1;
+    for (int a = 0; a < 3; ++a) {
+      const int y = 2 * p + a - 1;
+      float4 v[5][2];  // input columns 4j-1 .. 4j+3
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        const int xx = 4 * j - 1 + b;
         if (y >= 0 && y < H2 && xx >= 0 && xx < W2) {
           const size_t base = ((size_t)y * W2 + xx) * 2;
-          v[a * 3 + b][0] = __ldg(src + base);
-          v[a * 3 + b][1] = __ldg(src + base + 1);
+          v[b][0] = ldg_stream(src + base);
+          v[b][1] = ldg_stream(src + base + 1);
         } else {
-          v[a * 3 + b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
-          v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-    float o[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      float s = 0.f;
+      for (int k = 0; k < 16; ++k) {
 #pragma unroll
-      for (int t = 0; t < 9; ++t) {
-        const float4 w0 = *reinterpret_cast<const float4*>(sw + k * 72 + t * 8);
-        const float4 w1 = *reinterpret_cast<const float4*>(sw + k * 72 + t * 8 + 4);
-        s = fmaf(w0.x, v[t][0].x, s);
-        s = fmaf(w0.y, v[t][0].y, s);
-        s = fmaf(w0.z, v[t][0].z, s);
-        s = fmaf(w0.w, v[t][0].w, s);
-        s = fmaf(w1.x, v[t][1].x, s);
-        s = fmaf(w1.y, v[t][1].y, s);
-        s = fmaf(w1.z, v[t][1].z, s);
-        s = fmaf(w1.w, v[t][1].w, s);
+        for (int b = 0; b < 3; ++b) {
+          const float4 w0 = *reinterpret_cast<const float4*>(sw + k * 72 + (a * 3 + b) * 8);
+          const float4 w1 = *reinterpret_cast<const float4*>(sw + k * 72 + (a * 3 + b) * 8 + 4);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const float4 x0 = v[b + 2 * q][0], x1 = v[b + 2 * q][1];
+            float s = o[q][k];
+            s = fmaf(w0.x, x0.x, s);
+            s = fmaf(w0.y, x0.y, s);
+            s = fmaf(w0.z, x0.z, s);
+            s = fmaf(w0.w, x0.w, s);
+            s = fmaf(w1.x, x1.x, s);
+            s = fmaf(w1.y, x1.y, s);
+            s = fmaf(w1.z, x1.z, s);
+            s = fmaf(w1.w, x1.w, s);
+            o[q][k] = s;
+          }
+        }
       }
-      o[k] = fmaxf(s, 0.f);
     }
-    float4* dst = reinterpret_cast<float4*>(out + (size_t)id * 16);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+    for (int q = 0; q < 2; ++q) {
+      const int qq = 2 * j + q;
+      if (qq < W3) {
+        float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + qq) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          dst[k] = make_float4(fmaxf(o[q][4 * k], 0.f), fmaxf(o[q][4 * k + 1], 0.f),
+                               fmaxf(o[q][4 * k + 2], 0.f), fmaxf(o[q][4 * k + 3], 0.f));
+      }
+    }
   }
 }
 

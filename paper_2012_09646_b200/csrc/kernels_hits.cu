@@ -133,10 +133,42 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
   __syncthreads();
   const long long i0 = s_coord[0], j0 = s_coord[1], i1 = s_coord[2], j1 = s_coord[3];
   const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
-  // stage gathered values and row ends (rows i0 .. i1, clamped to N-1)
-  for (int k = t; k < nn; k += kSpmvThreads) s_val[k] = __ldg(x + __ldg(col + j0 + k));
-  const int nre = (int)(min(i1, N - 1) - i0 + 1);
-  for (int k = t; k < nre; k += kSpmvThreads) s_rend[k] = __ldg(row_ptr + i0 + k + 1);
+  // stage gathered values and row ends (rows i0 .. i1, clamped to N-1):
+  // all column indices of the thread first, then all gathers (8 independent
+  // loads in flight each); the streamed CSR arrays are evict-first in L2,
+  // the gathered vector evict-last (it is reused by every tile).
+  {
+    const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+    int ci[kSpmvItems];
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int k = t + u * kSpmvThreads;
+      ci[u] = k < nn ? ldg_hint(col + j0 + k, pol_stream) : 0;
+    }
+    float xv[kSpmvItems];
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int k = t + u * kSpmvThreads;
+      xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int k = t + u * kSpmvThreads;
+      if (k < nn) s_val[k] = xv[u];
+    }
+    const int nre = (int)(min(i1, N - 1) - i0 + 1);
+    int re[kSpmvItems + 1];
+#pragma unroll
+    for (int u = 0; u <= kSpmvItems; ++u) {
+      const int k = t + u * kSpmvThreads;
+      re[u] = k < nre ? ldg_hint(row_ptr + i0 + k + 1, pol_stream) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u <= kSpmvItems; ++u) {
+      const int k = t + u * kSpmvThreads;
+      if (k < nre) s_rend[k] = re[u];
+    }
+  }
   __syncthreads();
 
   // thread-local merge-path search inside the tile (binary, shared memory)

@@ -4,6 +4,8 @@
 // X is N x F int32 row-major (F = 200, L879-880), C = 10 classes.  Every
 // kernel is HBM-bound; the row-wise ones use one thread per row (C floats =
 // 40 B per row, 8-byte vector accesses, a warp covers 1280 contiguous bytes).
+#include <type_traits>
+
 #include "kcommon.cuh"
 
 namespace dagrt {
@@ -221,14 +223,106 @@ __device__ __forceinline__ void mmul_generic(const T* __restrict__ A, const floa
   }
 }
 
+// Tiled fast path (C = 10, F % 40 == 0, 128 threads): a CTA takes tiles of
+// 256 rows; the tile's X is staged through shared memory in 40-feature
+// chunks with coalesced 128-bit loads (row stride padded to 44 words so the
+// per-thread 128-bit reads are conflict-free); each thread accumulates TWO
+// rows x 10 classes (the broadcast weight loads are reused for both rows):
+// per 4 features 2 + 10 LDS.128 feed 80 FFMA, so the kernel is FFMA-bound
+// below the HBM time instead of L1-bound on strided row reads.
+constexpr int kMmThreads = 128;
+constexpr int kMmRows = 2 * kMmThreads;
+constexpr int kMmChunk = 40;
+constexpr int kMmStride = kMmChunk + 4;
+constexpr int kMmSmem = 4 * (10 * 200 + kMmRows * kMmStride);  // bytes for F = 200
+
+template <typename T>
+__device__ __forceinline__ float4 to_f4(const T& v);
+template <>
+__device__ __forceinline__ float4 to_f4<int4>(const int4& v) {
+  return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
+}
+template <>
+__device__ __forceinline__ float4 to_f4<float4>(const float4& v) { return v; }
+
+template <typename T, typename V4>
+__device__ __forceinline__ void mmul_tiled10(const T* __restrict__ A, const float* __restrict__ sW,
+                                             V4* __restrict__ sx, const float* __restrict__ bias,
+                                             float* __restrict__ out, long long N, int F) {
+  const int t = threadIdx.x;
+  const int F4 = F / 4;
+  const long long ntiles = (N + kMmRows - 1) / kMmRows;
+  const V4* A4 = reinterpret_cast<const V4*>(A);
+  float b[10];
+#pragma unroll
+  for (int c = 0; c < 10; ++c) b[c] = bias ? __ldg(bias + c) : 0.f;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long r0 = tile * kMmRows;
+    const int nrows = (int)min((long long)kMmRows, N - r0);
+    float a0[10], a1[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) { a0[c] = b[c]; a1[c] = b[c]; }
+    for (int f0 = 0; f0 < F; f0 += kMmChunk) {
+      __syncthreads();  // the previous chunk has been consumed
+      constexpr int G = kMmChunk / 4;  // 10 vectors per row chunk
+#pragma unroll 4
+      for (int k = t; k < kMmRows * G; k += kMmThreads) {
+        const int rr = k / G, gg = k - rr * G;
+        V4 v;
+        if (rr < nrows) v = ldg_stream(A4 + (r0 + rr) * F4 + f0 / 4 + gg);
+        else v = V4{0, 0, 0, 0};
+        sx[rr * (kMmStride / 4) + gg] = v;
+      }
+      __syncthreads();
+      const V4* x0p = sx + t * (kMmStride / 4);
+      const V4* x1p = sx + (t + kMmThreads) * (kMmStride / 4);
+#pragma unroll 2
+      for (int g = 0; g < G; ++g) {
+        const float4 x0 = to_f4(x0p[g]), x1 = to_f4(x1p[g]);
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const float4 w = *reinterpret_cast<const float4*>(sW + c * F + f0 + 4 * g);
+          a0[c] = fmaf(x0.x, w.x, a0[c]);
+          a0[c] = fmaf(x0.y, w.y, a0[c]);
+          a0[c] = fmaf(x0.z, w.z, a0[c]);
+          a0[c] = fmaf(x0.w, w.w, a0[c]);
+          a1[c] = fmaf(x1.x, w.x, a1[c]);
+          a1[c] = fmaf(x1.y, w.y, a1[c]);
+          a1[c] = fmaf(x1.z, w.z, a1[c]);
+          a1[c] = fmaf(x1.w, w.w, a1[c]);
+        }
+      }
+    }
+    if (t < nrows) {
+      float2* o = reinterpret_cast<float2*>(out + (r0 + t) * 10);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) o[c] = make_float2(a0[2 * c], a0[2 * c + 1]);
+    }
+    if (t + kMmThreads < nrows) {
+      float2* o = reinterpret_cast<float2*>(out + (r0 + t + kMmThreads) * 10);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) o[c] = make_float2(a1[2 * c], a1[2 * c + 1]);
+    }
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void mmul_body(const T* A, const float* W, const float* bias, float* out,
                                           long long N, int F, int C) {
   extern __shared__ __align__(16) float sW[];
   for (int i = threadIdx.x; i < C * F; i += blockDim.x) sW[i] = W[i];
   __syncthreads();
-  if (C == 10) mmul_rows<T, 10>(A, sW, bias, out, N, F);
-  else mmul_generic<T>(A, sW, bias, out, N, F, C);
+  const bool tiled = C == 10 && F % kMmChunk == 0 && F <= 200 && blockDim.x == kMmThreads &&
+                     aligned16(A) && (((uintptr_t)out) & 7) == 0;
+  if (tiled) {
+    using V4 = typename std::conditional<std::is_same<T, int>::value, int4, float4>::type;
+    V4* sx = reinterpret_cast<V4*>(sW + 10 * F + ((10 * F) & 3 ? 4 - ((10 * F) & 3) : 0));
+    mmul_tiled10<T, V4>(A, sW, sx, bias, out, N, F);
+  } else if (C == 10) {
+    mmul_rows<T, 10>(A, sW, bias, out, N, F);
+  } else {
+    mmul_generic<T>(A, sW, bias, out, N, F, C);
+  }
 }
 
 // NB MMUL: r1 = X theta^T + prior (prior is a const input).
@@ -247,35 +341,88 @@ __global__ void __launch_bounds__(256) k_rr_mmul(const float* __restrict__ Zm,
 }
 
 // ---------------------------------------------------------------- row-wise (C columns)
+// C = 10 fast path: a thread owns a PAIR of rows = 20 floats = 5 x 128-bit
+// accesses (row pairs are 80 B, so 16-B aligned); per-row scalars move as
+// float2/int2.  Other C: one thread per row, scalar accesses.
 #define ROW_LOOP for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; \
                       r += (long long)gridDim.x * blockDim.x)
+#define PAIR_LOOP for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; \
+                       i += (long long)gridDim.x * blockDim.x)
+#define TAIL_ROW if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+
+__device__ __forceinline__ void ld20(const float* base, long long i, float (&v)[20]) {
+  const float4* p = reinterpret_cast<const float4*>(base) + i * 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const float4 q = p[k];
+    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+  }
+}
+__device__ __forceinline__ void st20(float* base, long long i, const float (&v)[20]) {
+  float4* p = reinterpret_cast<float4*>(base) + i * 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) p[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+}
+__device__ __forceinline__ bool pair_ok(int C, const void* a, const void* b = nullptr) {
+  return C == 10 && aligned16(a) && (b == nullptr || (((uintptr_t)b) & 7) == 0);
+}
 
 // MAX: m[i] = max_c r1[i, c]
+__device__ __forceinline__ float rmax(const float* p, int C) {
+  float v = p[0];
+  for (int c = 1; c < C; ++c) v = fmaxf(v, p[c]);
+  return v;
+}
 __global__ void __launch_bounds__(256) k_rowmax(const float* __restrict__ r1, float* __restrict__ m,
                                                 long long N, int C) {
-  ROW_LOOP {
-    const float* p = r1 + r * C;
-    float v = p[0];
-    for (int c = 1; c < C; ++c) v = fmaxf(v, p[c]);
-    m[r] = v;
+  if (pair_ok(C, r1, m)) {
+    PAIR_LOOP {
+      float v[20];
+      ld20(r1, i, v);
+      reinterpret_cast<float2*>(m)[i] = make_float2(rmax(v, 10), rmax(v + 10, 10));
+    }
+    TAIL_ROW m[N - 1] = rmax(r1 + (N - 1) * C, C);
+    return;
   }
+  ROW_LOOP m[r] = rmax(r1 + r * C, C);
 }
 
 // LSE: l[i] = m[i] + ln sum_c exp(r1[i,c] - m[i])
+__device__ __forceinline__ float rlse(const float* p, float mm, int C) {
+  float s = 0.f;
+  for (int c = 0; c < C; ++c) s += expf(p[c] - mm);
+  return mm + logf(s);
+}
 __global__ void __launch_bounds__(256) k_lse(const float* __restrict__ r1, const float* __restrict__ m,
                                              float* __restrict__ l, long long N, int C) {
-  ROW_LOOP {
-    const float* p = r1 + r * C;
-    const float mm = m[r];
-    float s = 0.f;
-    for (int c = 0; c < C; ++c) s += expf(p[c] - mm);
-    l[r] = mm + logf(s);
+  if (pair_ok(C, r1, m) && (((uintptr_t)l) & 7) == 0) {
+    PAIR_LOOP {
+      float v[20];
+      ld20(r1, i, v);
+      const float2 mm = reinterpret_cast<const float2*>(m)[i];
+      reinterpret_cast<float2*>(l)[i] = make_float2(rlse(v, mm.x, 10), rlse(v + 10, mm.y, 10));
+    }
+    TAIL_ROW l[N - 1] = rlse(r1 + (N - 1) * C, m[N - 1], C);
+    return;
   }
+  ROW_LOOP l[r] = rlse(r1 + r * C, m[r], C);
 }
 
 // EXP: r1[i,c] = exp(r1[i,c] - l[i])   (in place)
 __global__ void __launch_bounds__(256) k_exp_sub(float* __restrict__ r1, const float* __restrict__ l,
                                                  long long N, int C) {
+  if (pair_ok(C, r1, l)) {
+    PAIR_LOOP {
+      float v[20];
+      ld20(r1, i, v);
+      const float2 ll = reinterpret_cast<const float2*>(l)[i];
+#pragma unroll
+      for (int c = 0; c < 10; ++c) { v[c] = expf(v[c] - ll.x); v[10 + c] = expf(v[10 + c] - ll.y); }
+      st20(r1, i, v);
+    }
+    TAIL_ROW for (int c = 0; c < C; ++c) r1[(N - 1) * C + c] = expf(r1[(N - 1) * C + c] - l[N - 1]);
+    return;
+  }
   ROW_LOOP {
     float* p = r1 + r * C;
     const float ll = l[r];
@@ -286,53 +433,94 @@ __global__ void __launch_bounds__(256) k_exp_sub(float* __restrict__ r1, const f
 // ADDV: r2[i,c] += b[c]   (in place)
 __global__ void __launch_bounds__(256) k_addv(float* __restrict__ r2, const float* __restrict__ b,
                                               long long N, int C) {
-  __shared__ float sb[kMaxClasses];
-  if (threadIdx.x < C && threadIdx.x < kMaxClasses) sb[threadIdx.x] = b[threadIdx.x];
-  __syncthreads();
+  if (pair_ok(C, r2)) {
+    float bb[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) bb[c] = __ldg(b + c);
+    PAIR_LOOP {
+      float v[20];
+      ld20(r2, i, v);
+#pragma unroll
+      for (int c = 0; c < 10; ++c) { v[c] += bb[c]; v[10 + c] += bb[c]; }
+      st20(r2, i, v);
+    }
+    TAIL_ROW for (int c = 0; c < C; ++c) r2[(N - 1) * C + c] += b[c];
+    return;
+  }
   ROW_LOOP {
     float* p = r2 + r * C;
-    for (int c = 0; c < C; ++c) p[c] += (c < kMaxClasses ? sb[c] : b[c]);
+    for (int c = 0; c < C; ++c) p[c] += b[c];
   }
 }
 
 // SOFTMAX: row softmax in place (max-shifted)
+__device__ __forceinline__ void rsoftmax(float* v, int C) {
+  float m = v[0];
+  for (int c = 1; c < C; ++c) m = fmaxf(m, v[c]);
+  float s = 0.f;
+  for (int c = 0; c < C; ++c) { v[c] = expf(v[c] - m); s += v[c]; }
+  const float is = 1.f / s;
+  for (int c = 0; c < C; ++c) v[c] *= is;
+}
 __global__ void __launch_bounds__(256) k_softmax(float* __restrict__ x, long long N, int C) {
+  if (pair_ok(C, x)) {
+    PAIR_LOOP {
+      float v[20];
+      ld20(x, i, v);
+      rsoftmax(v, 10);
+      rsoftmax(v + 10, 10);
+      st20(x, i, v);
+    }
+    TAIL_ROW {
+      float v[kMaxClasses];
+      for (int c = 0; c < C; ++c) v[c] = x[(N - 1) * C + c];
+      rsoftmax(v, C);
+      for (int c = 0; c < C; ++c) x[(N - 1) * C + c] = v[c];
+    }
+    return;
+  }
   ROW_LOOP {
-    float* p = x + r * C;
     float v[kMaxClasses];
-    float m = -INFINITY;
     const int CC = min(C, kMaxClasses);
-    for (int c = 0; c < CC; ++c) { v[c] = p[c]; m = fmaxf(m, v[c]); }
-    float s = 0.f;
-    for (int c = 0; c < CC; ++c) { v[c] = expf(v[c] - m); s += v[c]; }
-    const float is = 1.f / s;
-    for (int c = 0; c < CC; ++c) p[c] = v[c] * is;
+    float* p = x + r * C;
+    for (int c = 0; c < CC; ++c) v[c] = p[c];
+    rsoftmax(v, CC);
+    for (int c = 0; c < CC; ++c) p[c] = v[c];
   }
 }
 
 // ARGMAX: r[i] = lowest c maximising r1[i,c] + r2[i,c]
+__device__ __forceinline__ int rargmax(const float* a, const float* b, int C) {
+  float best = a[0] + b[0];
+  int bi = 0;
+  for (int c = 1; c < C; ++c) {
+    const float s = a[c] + b[c];
+    if (s > best) { best = s; bi = c; }
+  }
+  return bi;
+}
 __global__ void __launch_bounds__(256) k_argmax(const float* __restrict__ r1,
                                                 const float* __restrict__ r2, int* __restrict__ out,
                                                 long long N, int C) {
-  ROW_LOOP {
-    const float* a = r1 + r * C;
-    const float* b = r2 + r * C;
-    float best = a[0] + b[0];
-    int bi = 0;
-    for (int c = 1; c < C; ++c) {
-      float s = a[c] + b[c];
-      if (s > best) { best = s; bi = c; }
+  if (pair_ok(C, r1, out) && aligned16(r2)) {
+    PAIR_LOOP {
+      float a[20], b[20];
+      ld20(r1, i, a);
+      ld20(r2, i, b);
+      reinterpret_cast<int2*>(out)[i] = make_int2(rargmax(a, b, 10), rargmax(a + 10, b + 10, 10));
     }
-    out[r] = bi;
+    TAIL_ROW out[N - 1] = rargmax(r1 + (N - 1) * C, r2 + (N - 1) * C, C);
+    return;
   }
+  ROW_LOOP out[r] = rargmax(r1 + r * C, r2 + r * C, C);
 }
 
 static const Builtin kMl[] = {
     {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_NONE},
     {"nb_mmul", (const void*)k_nb_mmul,
-     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE},
+     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 96 * 1024},
     {"rr_mmul", (const void*)k_rr_mmul, "const ptr, const ptr, out ptr, sint64, sint32, sint32",
-     KF_NONE},
+     KF_NONE, 96 * 1024},
     {"rowmax", (const void*)k_rowmax, "const ptr, out ptr, sint64, sint32", KF_NONE},
     {"lse", (const void*)k_lse, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE},
     {"exp_sub", (const void*)k_exp_sub, "ptr, const ptr, sint64, sint32", KF_NONE},

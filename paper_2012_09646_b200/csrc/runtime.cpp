@@ -571,6 +571,8 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
     k.name = b->name;
     k.fn = b->fn;
     k.coop = (b->flags & KF_COOPERATIVE) != 0;
+    if (b->smem_max > 0 && c->be->real() && b->fn)
+      cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
     if (parse_signature(b->signature, &k) != DAGRT_OK) {
       delete c->be;
       delete c;

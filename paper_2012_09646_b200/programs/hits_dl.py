@@ -135,9 +135,10 @@ class DeepLearning(Program):
         self.nz = nz
         a = self.a
         P = ctx.prepare
-        g1 = grid_1d(h1 * ((w1 + 1) // 2), 256)
+        # conv grids: x = column pairs / 256, y = output rows (<= 65535, kernels loop)
+        g1 = (max(1, -(-((w1 + 1) // 2) // 256)), max(1, min(h1, 65535)))
         gp = grid_1d(h2 * w2 * 2, 256)
-        g2 = grid_1d(h3 * w3, 256)
+        g2 = (max(1, -(-((w3 + 1) // 2) // 256)), max(1, min(h3, 65535)))
         gc = grid_1d(nz // 4 + 1, 256)
         self.L = [
             P("conv1", g1, 256, [a["x"], a["w1"], a["c1x"], h, w]),

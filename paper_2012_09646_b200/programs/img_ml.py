@@ -85,6 +85,7 @@ class Images(Program):
 
 ML_C, ML_F = 10, 200  # classes (reading), features (L879-880)
 NORM_THREADS = 512
+MM_THREADS = 128  # csrc/kernels_ml.cu kMmThreads
 NORM_GRID = 2 * SMS
 
 
@@ -115,11 +116,15 @@ class MLEnsemble(Program):
         self.inputs, self.sinks = ["X"], ["r"]
         a = self.a
         P = ctx.prepare
-        gr = grid_1d(n, 256, 1)
+        gr = grid_1d(n, 256, 2)
+        # MMUL: 128 threads, persistent over 256-row tiles; W + padded X chunk in smem
+        gm = max(1, min(-(-n // (2 * MM_THREADS)), 4 * SMS))
+        mm_smem = 4 * c * f + 16 + 4 * (2 * MM_THREADS) * 44
         self.L = [
             P("norm", NORM_GRID, NORM_THREADS, [a["X"], a["Z"], a["stats"], n, f], smem=norm_smem(f)),
-            P("nb_mmul", gr, 256, [a["X"], a["theta"], a["prior"], a["r1"], n, f, c], smem=4 * c * f),
-            P("rr_mmul", gr, 256, [a["Z"], a["W"], a["r2"], n, f, c], smem=4 * c * f),
+            P("nb_mmul", gm, MM_THREADS, [a["X"], a["theta"], a["prior"], a["r1"], n, f, c],
+              smem=mm_smem),
+            P("rr_mmul", gm, MM_THREADS, [a["Z"], a["W"], a["r2"], n, f, c], smem=mm_smem),
             P("rowmax", gr, 256, [a["r1"], a["amax"], n, c]),
             P("lse", gr, 256, [a["r1"], a["amax"], a["l"], n, c]),
             P("addv", gr, 256, [a["r2"], a["b"], n, c]),

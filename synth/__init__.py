@@ -135,7 +135,7 @@ def spec_dl(h: int, w: int):
         "y": (KIND_F32_UNIT, h * w, ()),
         "w1": (KIND_F32_SYM, 8 * 9 * 1, (1.0 / math.sqrt(9.0),)),
         "w2": (KIND_F32_SYM, 16 * 9 * 8, (1.0 / math.sqrt(72.0),)),
-        "wd": (KIND_F32_SYM, nz, (1.0 / math.sqrt(float(nz)),)),
+        "wd": (KIND_F32_SYM, nz, (1.0 / math.sqrt(float(max(nz, 1))),)),
     }
 
 

@@ -65,8 +65,8 @@ def test_vec_closed_form(ctx):
     assert abs(p.result() - (-4.934799200546)) < 1e-3
 
 
-def test_vec_dag_matches_oracle(ctx):
-    ctx.dag_clear()
+def test_vec_dag_matches_oracle():
+    ctx = D.Context(device=0, record_dag=True)
     p = Vec(ctx, n=4096)
     p.load_inputs(0)
     p.run()
@@ -78,6 +78,7 @@ def test_vec_dag_matches_oracle(ctx):
     o = odag.build_dag(tr)
     assert edges == o.edges
     assert [(v[2], v[3]) for v in verts] == [(v[3], v[4]) for v in o.vertices]
+    ctx.close()
 
 
 @pytest.mark.parametrize("n", [1, 3, 4099, 1_000_001])
