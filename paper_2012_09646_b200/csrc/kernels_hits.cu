@@ -113,8 +113,6 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
   __shared__ long long s_coord[4];
   __shared__ float s_val[kSpmvTile];
   __shared__ int s_rend[kSpmvTile + 1];
-  __shared__ float s_scan[kSpmvThreads];
-  __shared__ unsigned char s_flag[kSpmvThreads];
   const long long E = (long long)__ldg(row_ptr + N);
   const long long total = N + E;
   const long long ncta = (total + kSpmvTile - 1) / kSpmvTile;
@@ -202,25 +200,32 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
       ++nj;
     }
   }
-  // block segmented inclusive scan: s(t) = sum(t) + (emitted(t) ? 0 : s(t-1))
-  s_scan[t] = sum;
-  s_flag[t] = emitted ? 1 : 0;
-  __syncthreads();
-  for (int off = 1; off < kSpmvThreads; off <<= 1) {
-    float v = 0.f;
-    unsigned char f = 0;
-    if (t >= off) { v = s_scan[t - off]; f = s_flag[t - off]; }
-    __syncthreads();
-    if (t >= off && !s_flag[t]) { s_scan[t] += v; s_flag[t] = f; }
-    __syncthreads();
+  // segmented inclusive scan s(t) = sum(t) + (emitted(t) ? 0 : s(t-1)):
+  // warp shuffles, then one cross-warp step through shared memory (fixed
+  // combination order -> deterministic)
+  const int lane = t & 31;
+  float sc = sum;
+  bool fl = emitted;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float yv = __shfl_up_sync(0xffffffffu, sc, off);
+    const bool f = __shfl_up_sync(0xffffffffu, fl, off);
+    if (lane >= off && !fl) { sc += yv; fl = f; }
   }
-  // incoming carry for this thread's first emitted row = s(t-1)
-  const float incoming = t > 0 ? s_scan[t - 1] : 0.f;
-  // did the carry chain reach back to the CTA start? (no emission in 0..t-1)
+  __shared__ float s_wsum[kSpmvThreads / 32];
+  __shared__ int s_wflag[kSpmvThreads / 32];
   __shared__ int s_first_emitter;
+  __shared__ float s_carry;
   if (t == 0) s_first_emitter = kSpmvThreads;
+  if (lane == 31) { s_wsum[warp] = sc; s_wflag[warp] = fl ? 1 : 0; }
   __syncthreads();
   if (emitted) atomicMin(&s_first_emitter, t);
+  float win = 0.f;  // carry into this warp from warps 0 .. warp-1
+  for (int w = 0; w < warp; ++w) win = s_wflag[w] ? s_wsum[w] : win + s_wsum[w];
+  const float s_incl = fl ? sc : sc + win;
+  float incoming = __shfl_up_sync(0xffffffffu, s_incl, 1);  // s(t-1)
+  if (lane == 0) incoming = win;
+  if (t == kSpmvThreads - 1) s_carry = s_incl;
   __syncthreads();
   const int fe = s_first_emitter;
   __shared__ float s_head_val;
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
       const long long rs = __ldg(row_ptr + i1), re = __ldg(row_ptr + i1 + 1);
       const long long cs = (i1 + rs) / kSpmvTile, ce = (i1 + re) / kSpmvTile;
       if (ce > c && cs <= c) {
-        const float carry = s_scan[kSpmvThreads - 1];
+        const float carry = s_carry;
         spmv_deposit(ws, y, i1, cs, ce, c, carry, false);
       }
     }

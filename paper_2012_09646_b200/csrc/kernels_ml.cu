@@ -223,87 +223,137 @@ __device__ __forceinline__ void mmul_generic(const T* __restrict__ A, const floa
   }
 }
 
-// Tiled fast path (C = 10, F % 40 == 0, 128 threads): a CTA takes tiles of
-// 256 rows; the tile's X is staged through shared memory in 40-feature
-// chunks with coalesced 128-bit loads (row stride padded to 44 words so the
-// per-thread 128-bit reads are conflict-free); each thread accumulates TWO
-// rows x 10 classes (the broadcast weight loads are reused for both rows):
-// per 4 features 2 + 10 LDS.128 feed 80 FFMA, so the kernel is FFMA-bound
-// below the HBM time instead of L1-bound on strided row reads.
+// TMA fast path (C = 10, F % 4 == 0, F <= 200, 128 threads): each CTA walks
+// tiles of 64 consecutive rows.  A tile is ONE contiguous chunk of A
+// (64 x 4F bytes), brought into shared memory by a single cp.async.bulk
+// (TMA, completion on an mbarrier), double-buffered so the next tile streams
+// in while this one is multiplied.  Two threads share a row (features
+// [0, F/2) and [F/2, F)): with rows contiguous in smem their 128-bit reads
+// are bank-conflict-free, the 10 weight rows are read with 2-address
+// broadcast loads, and the two partial dot products are combined with one
+// shuffle per class.  Per 4 features a warp issues 1 + 10 LDS.128 for 40 FFMA.
 constexpr int kMmThreads = 128;
-constexpr int kMmRows = 2 * kMmThreads;
-constexpr int kMmChunk = 40;
-constexpr int kMmStride = kMmChunk + 4;
-constexpr int kMmSmem = 4 * (10 * 200 + kMmRows * kMmStride);  // bytes for F = 200
+constexpr int kMmRows = kMmThreads / 2;  // rows per tile
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
 
 template <typename T>
-__device__ __forceinline__ float4 to_f4(const T& v);
+__device__ __forceinline__ float4 as_f4(const T* p);
 template <>
-__device__ __forceinline__ float4 to_f4<int4>(const int4& v) {
+__device__ __forceinline__ float4 as_f4<int>(const int* p) {
+  const int4 v = *reinterpret_cast<const int4*>(p);
   return make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w);
 }
 template <>
-__device__ __forceinline__ float4 to_f4<float4>(const float4& v) { return v; }
+__device__ __forceinline__ float4 as_f4<float>(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
 
-template <typename T, typename V4>
-__device__ __forceinline__ void mmul_tiled10(const T* __restrict__ A, const float* __restrict__ sW,
-                                             V4* __restrict__ sx, const float* __restrict__ bias,
-                                             float* __restrict__ out, long long N, int F) {
-  const int t = threadIdx.x;
-  const int F4 = F / 4;
+template <typename T>
+__device__ __forceinline__ void mmul_tma10(const T* __restrict__ A, const float* __restrict__ sW,
+                                           unsigned char* smem_tiles, uint64_t* full,
+                                           const float* __restrict__ bias, float* __restrict__ out,
+                                           long long N, int F) {
+  const int t = threadIdx.x, h = t & 1, row = t >> 1;
+  const int half = F / 2;                     // features per thread (multiple of 2)
+  const size_t tile_bytes = (size_t)kMmRows * F * 4;
+  auto buf = [&](int st) { return reinterpret_cast<T*>(smem_tiles + st * tile_bytes); };
   const long long ntiles = (N + kMmRows - 1) / kMmRows;
-  const V4* A4 = reinterpret_cast<const V4*>(A);
   float b[10];
 #pragma unroll
   for (int c = 0; c < 10; ++c) b[c] = bias ? __ldg(bias + c) : 0.f;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  auto issue = [&](long long tile, int stage) {
+    const long long r0 = tile * kMmRows;
+    const unsigned bytes = (unsigned)(min((long long)kMmRows, N - r0) * F * 4);
+    mbar_expect_tx(&full[stage], bytes);
+    tma_bulk_g2s(buf(stage), A + r0 * F, bytes, &full[stage]);
+  };
+  if (t == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((long long)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  int k = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int stage = k & 1;
+    mbar_wait(&full[stage], (k >> 1) & 1);
     const long long r0 = tile * kMmRows;
     const int nrows = (int)min((long long)kMmRows, N - r0);
-    float a0[10], a1[10];
+    float acc[10];
 #pragma unroll
-    for (int c = 0; c < 10; ++c) { a0[c] = b[c]; a1[c] = b[c]; }
-    for (int f0 = 0; f0 < F; f0 += kMmChunk) {
-      __syncthreads();  // the previous chunk has been consumed
-      constexpr int G = kMmChunk / 4;  // 10 vectors per row chunk
-#pragma unroll 4
-      for (int k = t; k < kMmRows * G; k += kMmThreads) {
-        const int rr = k / G, gg = k - rr * G;
-        V4 v;
-        if (rr < nrows) v = ldg_stream(A4 + (r0 + rr) * F4 + f0 / 4 + gg);
-        else v = V4{0, 0, 0, 0};
-        sx[rr * (kMmStride / 4) + gg] = v;
-      }
-      __syncthreads();
-      const V4* x0p = sx + t * (kMmStride / 4);
-      const V4* x1p = sx + (t + kMmThreads) * (kMmStride / 4);
-#pragma unroll 2
-      for (int g = 0; g < G; ++g) {
-        const float4 x0 = to_f4(x0p[g]), x1 = to_f4(x1p[g]);
+    for (int c = 0; c < 10; ++c) acc[c] = h == 0 ? b[c] : 0.f;
+    if (row < nrows) {
+      const T* xr = buf(stage) + (size_t)row * F + h * half;
+      const float* wr = sW + h * half;
+#pragma unroll 5
+      for (int f = 0; f < half; f += 4) {
+        const float4 x = as_f4<T>(xr + f);
 #pragma unroll
         for (int c = 0; c < 10; ++c) {
-          const float4 w = *reinterpret_cast<const float4*>(sW + c * F + f0 + 4 * g);
-          a0[c] = fmaf(x0.x, w.x, a0[c]);
-          a0[c] = fmaf(x0.y, w.y, a0[c]);
-          a0[c] = fmaf(x0.z, w.z, a0[c]);
-          a0[c] = fmaf(x0.w, w.w, a0[c]);
-          a1[c] = fmaf(x1.x, w.x, a1[c]);
-          a1[c] = fmaf(x1.y, w.y, a1[c]);
-          a1[c] = fmaf(x1.z, w.z, a1[c]);
-          a1[c] = fmaf(x1.w, w.w, a1[c]);
+          const float4 w = *reinterpret_cast<const float4*>(wr + c * F + f);
+          acc[c] = fmaf(x.x, w.x, acc[c]);
+          acc[c] = fmaf(x.y, w.y, acc[c]);
+          acc[c] = fmaf(x.z, w.z, acc[c]);
+          acc[c] = fmaf(x.w, w.w, acc[c]);
         }
       }
     }
-    if (t < nrows) {
-      float2* o = reinterpret_cast<float2*>(out + (r0 + t) * 10);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) o[c] = make_float2(a0[2 * c], a0[2 * c + 1]);
+    for (int c = 0; c < 10; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+    if (row < nrows) {
+      float2* o = reinterpret_cast<float2*>(out + (r0 + row) * 10);
+      if (h == 0) {
+        o[0] = make_float2(acc[0], acc[1]);
+        o[1] = make_float2(acc[2], acc[3]);
+      } else {
+        o[2] = make_float2(acc[4], acc[5]);
+        o[3] = make_float2(acc[6], acc[7]);
+        o[4] = make_float2(acc[8], acc[9]);
+      }
     }
-    if (t + kMmThreads < nrows) {
-      float2* o = reinterpret_cast<float2*>(out + (r0 + t + kMmThreads) * 10);
-#pragma unroll
-      for (int c = 0; c < 5; ++c) o[c] = make_float2(a1[2 * c], a1[2 * c + 1]);
+    __syncthreads();  // every thread is done with buf[stage]
+    if (t == 0 && tile + 2 * (long long)gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + 2 * (long long)gridDim.x, stage);
     }
   }
+}
+
+// shared-memory bytes of the TMA path: W, 2 mbarriers, two row tiles
+__host__ __device__ constexpr size_t mmul_tma_smem(int F) {
+  return (size_t)10 * F * 4 + 16 + 2 * (size_t)kMmRows * F * 4;
 }
 
 template <typename T>
@@ -312,12 +362,12 @@ __device__ __forceinline__ void mmul_body(const T* A, const float* W, const floa
   extern __shared__ __align__(16) float sW[];
   for (int i = threadIdx.x; i < C * F; i += blockDim.x) sW[i] = W[i];
   __syncthreads();
-  const bool tiled = C == 10 && F % kMmChunk == 0 && F <= 200 && blockDim.x == kMmThreads &&
-                     aligned16(A) && (((uintptr_t)out) & 7) == 0;
-  if (tiled) {
-    using V4 = typename std::conditional<std::is_same<T, int>::value, int4, float4>::type;
-    V4* sx = reinterpret_cast<V4*>(sW + 10 * F + ((10 * F) & 3 ? 4 - ((10 * F) & 3) : 0));
-    mmul_tiled10<T, V4>(A, sW, sx, bias, out, N, F);
+  const bool tma = C == 10 && (F & 3) == 0 && F <= 200 && ((F / 2) & 3) == 0 &&
+                   blockDim.x == kMmThreads && aligned16(A) && (((uintptr_t)out) & 7) == 0;
+  if (tma) {
+    uint64_t* full = reinterpret_cast<uint64_t*>(sW + 10 * F);   // 10F*4 is a multiple of 16
+    unsigned char* tiles = reinterpret_cast<unsigned char*>(full + 2);
+    mmul_tma10<T>(A, sW, tiles, full, bias, out, N, F);
   } else if (C == 10) {
     mmul_rows<T, 10>(A, sW, bias, out, N, F);
   } else {
@@ -518,9 +568,9 @@ __global__ void __launch_bounds__(256) k_argmax(const float* __restrict__ r1,
 static const Builtin kMl[] = {
     {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_NONE},
     {"nb_mmul", (const void*)k_nb_mmul,
-     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 96 * 1024},
+     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 120 * 1024},
     {"rr_mmul", (const void*)k_rr_mmul, "const ptr, const ptr, out ptr, sint64, sint32, sint32",
-     KF_NONE, 96 * 1024},
+     KF_NONE, 120 * 1024},
     {"rowmax", (const void*)k_rowmax, "const ptr, out ptr, sint64, sint32", KF_NONE},
     {"lse", (const void*)k_lse, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE},
     {"exp_sub", (const void*)k_exp_sub, "ptr, const ptr, sint64, sint32", KF_NONE},

@@ -175,7 +175,7 @@ __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsT
 
 // K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores,
 // two options per thread per iteration.
-__global__ void __launch_bounds__(256) k_bs(const double* __restrict__ s, double* __restrict__ c,
+__global__ void __launch_bounds__(256, 5) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
   __shared__ BsTables T;
   bs_tables_init(T);
@@ -194,12 +194,15 @@ __global__ void __launch_bounds__(256) k_bs(const double* __restrict__ s, double
     const long long n2 = n >> 1;
     const double2* s2 = reinterpret_cast<const double2*>(s);
     double2* c2 = reinterpret_cast<double2*>(c);
+    // software pipelined: the next pair is in flight while this one is priced
+    double2 x = tid < n2 ? ldg_stream(s2 + tid) : make_double2(1.0, 1.0);
     for (long long i = tid; i < n2; i += nth) {
-      double2 x = ldg_stream(s2 + i);
+      const double2 nx = i + nth < n2 ? ldg_stream(s2 + i + nth) : x;
       double2 y;
       y.x = bs_price(x.x, C, T);
       y.y = bs_price(x.y, C, T);
       c2[i] = y;
+      x = nx;
     }
     done = n2 << 1;
   }

@@ -6,7 +6,7 @@ import math
 import torch
 
 import synth
-from .base import Program, grid_1d
+from .base import SMS, Program, grid_1d
 
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 256 * 8      # merge items per CTA (csrc/kernels_hits.cu)
@@ -136,9 +136,11 @@ class DeepLearning(Program):
         a = self.a
         P = ctx.prepare
         # conv grids: x = column pairs / 256, y = output rows (<= 65535, kernels loop)
-        g1 = (max(1, -(-((w1 + 1) // 2) // 256)), max(1, min(h1, 65535)))
+        x1b = max(1, -(-((w1 + 1) // 2) // 256))
+        g1 = (x1b, max(1, min(h1, -(-8 * SMS // x1b))))  # blocks loop over output rows
         gp = grid_1d(h2 * w2 * 2, 256)
-        g2 = (max(1, -(-((w3 + 1) // 2) // 256)), max(1, min(h3, 65535)))
+        x2b = max(1, -(-((w3 + 1) // 2) // 256))
+        g2 = (x2b, max(1, min(h3, -(-8 * SMS // x2b))))
         gc = grid_1d(nz // 4 + 1, 256)
         self.L = [
             P("conv1", g1, 256, [a["x"], a["w1"], a["c1x"], h, w]),

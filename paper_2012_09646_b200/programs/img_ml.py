@@ -118,8 +118,9 @@ class MLEnsemble(Program):
         P = ctx.prepare
         gr = grid_1d(n, 256, 2)
         # MMUL: 128 threads, persistent over 256-row tiles; W + padded X chunk in smem
-        gm = max(1, min(-(-n // (2 * MM_THREADS)), 4 * SMS))
-        mm_smem = 4 * c * f + 16 + 4 * (2 * MM_THREADS) * 44
+        # MMUL (TMA path): 2 CTAs/SM, 64-row tiles double-buffered in smem
+        gm = max(1, min(-(-n // (MM_THREADS // 2)), 2 * SMS))
+        mm_smem = 4 * c * f + 16 + 2 * (MM_THREADS // 2) * 4 * f
         self.L = [
             P("norm", NORM_GRID, NORM_THREADS, [a["X"], a["Z"], a["stats"], n, f], smem=norm_smem(f)),
             P("nb_mmul", gm, MM_THREADS, [a["X"], a["theta"], a["prior"], a["r1"], n, f, c],
