@@ -40,5 +40,7 @@ def fill(dev_ptr, seed, name, spec, idx0=0, n=None, sync=True):
 
 
 def fill_tensor(t, seed, name, spec):
-    assert t.numel() == spec[1], (t.numel(), spec[1])
-    fill(t.data_ptr(), seed, name, spec)
+    """Fill the first spec[1] elements of t (allocations may be padded to >= 1)."""
+    assert t.numel() >= spec[1], (t.numel(), spec[1])
+    if spec[1]:
+        fill(t.data_ptr(), seed, name, spec)
