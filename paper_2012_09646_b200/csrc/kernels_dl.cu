@@ -20,9 +20,11 @@ __global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
                                                float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
   const int pairs = (W1 + 1) / 2;
-  float wr[72];
-#pragma unroll
-  for (int i = 0; i < 72; ++i) wr[i] = __ldg(w + i);
+  // weights in shared memory (uniform 128-bit broadcast reads): keeping all
+  // 72 in registers would cap occupancy at 25% and starve the loads
+  __shared__ __align__(16) float wr[72];
+  if (threadIdx.x < 72) wr[threadIdx.x] = __ldg(w + threadIdx.x);
+  __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live_j = j < pairs;
   const bool vec = ((W & 3) == 0) && aligned16(x);
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(256) k_pool(const float* __restrict__ in, floa
 // tap row it loads the 5 input pixels both outputs need (10 x LDG.128) and
 // accumulates 2 x 16 outputs; the 16 x 72 weights sit in shared memory and
 // are read with broadcast 128-bit loads, each reused for the two pixels.
-__global__ void __launch_bounds__(256) k_conv2(const float* __restrict__ in,
+__global__ void __launch_bounds__(256, 3) k_conv2(const float* __restrict__ in,
                                                const float* __restrict__ w,
                                                float* __restrict__ out, int H2, int W2) {
   __shared__ __align__(16) float sw[16 * 72];

@@ -106,30 +106,16 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
   }
 }
 
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ row_ptr,
-                                                       const int* __restrict__ col,
-                                                       const float* __restrict__ x,
-                                                       float* __restrict__ y, long long N) {
-  __shared__ long long s_coord[4];
+// One merge-path tile c = diagonals [c*T, min((c+1)*T, N+E)) with start
+// coordinate (i0, j0) and end coordinate (i1, j1).  Called by all threads.
+__device__ __forceinline__ void spmv_tile(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                          const float* __restrict__ x, float* __restrict__ y,
+                                          long long N, const SpmvWs& ws, long long c, long long i0,
+                                          long long j0, long long i1, long long j1) {
   __shared__ float s_val[kSpmvTile];
   __shared__ int s_rend[kSpmvTile + 1];
-  const long long E = (long long)__ldg(row_ptr + N);
-  const long long total = N + E;
-  const long long ncta = (total + kSpmvTile - 1) / kSpmvTile;
-  const long long c = blockIdx.x;
-  const SpmvWs ws = spmv_ws(y, N, ncta);
   const int t = threadIdx.x, warp = t >> 5;
-  const long long d0 = c * kSpmvTile;
-  const long long d1 = min(total, d0 + kSpmvTile);
-  if (d0 >= total) return;  // uniform per CTA
-
-  if (warp < 2) {
-    const long long d = warp == 0 ? d0 : d1;
-    const long long i = warp_merge_search(row_ptr, N, E, d);
-    if ((t & 31) == 0) { s_coord[2 * warp] = i; s_coord[2 * warp + 1] = d - i; }
-  }
-  __syncthreads();
-  const long long i0 = s_coord[0], j0 = s_coord[1], i1 = s_coord[2], j1 = s_coord[3];
+  __syncthreads();  // the previous tile's readers of shared memory are done
   const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
   // stage gathered values and row ends (rows i0 .. i1, clamped to N-1):
   // all column indices of the thread first, then all gathers (8 independent
@@ -255,6 +241,43 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
         const float carry = s_carry;
         spmv_deposit(ws, y, i1, cs, ce, c, carry, false);
       }
+    }
+  }
+}
+
+// Persistent merge-path SpMV: each CTA owns a contiguous range of tiles.  All
+// its tile boundaries (up to 256 at a time) are located first, by all 8
+// warps in parallel (32-ary searches), so the per-tile critical path is only
+// the staging gathers; consecutive tiles share their boundary.
+constexpr int kSpmvChunk = 256;
+
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ row_ptr,
+                                                       const int* __restrict__ col,
+                                                       const float* __restrict__ x,
+                                                       float* __restrict__ y, long long N) {
+  __shared__ int s_bnd[kSpmvChunk + 1];
+  const long long E = (long long)__ldg(row_ptr + N);
+  const long long total = N + E;
+  const long long ntiles = (total + kSpmvTile - 1) / kSpmvTile;
+  const SpmvWs ws = spmv_ws(y, N, ntiles);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const long long tb0 = (long long)blockIdx.x * per;
+  const long long te0 = min(ntiles, tb0 + per);
+  for (long long tb = tb0; tb < te0; tb += kSpmvChunk) {
+    const long long te = min(te0, tb + kSpmvChunk);
+    const int nb = (int)(te - tb) + 1;
+    __syncthreads();  // s_bnd of the previous chunk consumed
+    for (int b = warp; b < nb; b += kSpmvThreads / 32) {
+      const long long d = min(total, (tb + b) * (long long)kSpmvTile);
+      const long long i = warp_merge_search(row_ptr, N, E, d);
+      if (lane == 0) s_bnd[b] = (int)i;
+    }
+    __syncthreads();
+    for (long long c = tb; c < te; ++c) {
+      const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
+      const long long i0 = s_bnd[c - tb], i1 = s_bnd[c - tb + 1];
+      spmv_tile(row_ptr, col, x, y, N, ws, c, i0, d0 - i0, i1, d1 - i1);
     }
   }
 }

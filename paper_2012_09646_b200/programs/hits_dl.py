@@ -47,9 +47,10 @@ class Hits(Program):
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
+        gs = min(self.ncta, 6 * SMS)  # persistent merge-path CTAs (6 resident per SM)
         self.it = [
-            P("spmv", self.ncta, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
-            P("spmv", self.ncta, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
+            P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
+            P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
             P("l2norm", gr, 256, [a["a2"], a["an"], n]),
             P("l2norm", gr, 256, [a["h2"], a["hn"], n]),
             P("divide", ge, 256, [a["a2"], a["an"], a["a1"], n]),
