@@ -252,6 +252,22 @@ dagrt_status dagrt_profile_enable(dagrt_ctx ctx, dagrt_kernel k, int32_t on);
 dagrt_status dagrt_profile_collect(dagrt_ctx ctx, dagrt_kernel k, int32_t* count, double* sum_ms,
                                    double* busy_ms);
 
+/* Execution timeline (schedule evidence, the paper's Fig. 10 / L1265-1291):
+ * while enabled, every kernel launch and every H2D/D2H copy issued by the
+ * scheduler is bracketed by timing events on its own stream.  Export waits
+ * for them and returns one record per item, times in ms relative to the
+ * first recorded item, then clears the records. */
+typedef struct {
+  int32_t kind;    /* 0 kernel, 1 H2D copy, 2 D2H copy */
+  int32_t stream;  /* compute stream index, -2 copy stream, -3 serial stream, -5 D2H stream */
+  int64_t vertex;  /* vertex id (kernels; H2D: consuming vertex; D2H: -1) */
+  int64_t id;      /* kernel handle (kind 0) or array index (copies) */
+  uint64_t bytes;  /* copy size (copies) */
+  double start_ms, end_ms;
+} dagrt_timeline_rec;
+dagrt_status dagrt_timeline_enable(dagrt_ctx ctx, int32_t on);
+dagrt_status dagrt_timeline_export(dagrt_ctx ctx, dagrt_timeline_rec* recs, uint32_t* n);
+
 /* ---------------------------------------------------------------- baselines */
 
 /* Direct launch on a caller-given cudaStream_t with no scheduling at all

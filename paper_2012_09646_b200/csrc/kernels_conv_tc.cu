@@ -1,0 +1,219 @@
+// DL second convolution on the 5th-generation tensor cores (tcgen05, TMEM).
+//
+// conv2 (§V-B, Fig. 6; reading R-DL) is a real
+// dense contraction: an implicit GEMM with M = output pixels, N = 16 output
+// channels, K = 72 = 9 taps x 8 input channels.  Its arithmetic intensity
+// (~12 flop/B) sits on the FFMA/HBM ridge of B200, so on CUDA cores it is
+// ALU-co-bound; on tcgen05 it becomes purely HBM-bound.
+//
+// Precision: fp32 inputs, north_star tolerance 1e-4 relative.  Plain TF32
+// (10-bit mantissa) would miss it, so the kernel uses the 3xTF32 split
+// x = x_hi + x_lo (both TF32): D = A_hi B_hi + A_lo B_hi + A_hi B_lo,
+// accumulated in fp32 in TMEM (error ~2^-21 relative, like FFMA).
+//
+// Per CTA (128 threads, persistent over 128-pixel tiles):
+//   * B_hi/B_lo (16 x 72 weights) staged once in shared memory in the UMMA
+//     K-major no-swizzle ("interleaved") canonical layout: 8-row x 16-byte
+//     core matrices, LBO = 128 B (K direction), SBO = 256 B (8-row groups);
+//   * each thread gathers its pixel's 9 input taps (18 x 128-bit loads in
+//     flight), splits them into TF32 hi/lo and writes the A tiles (one 4 KB
+//     tile per tap per part) in the same layout;
+//   * one elected thread issues 27 tcgen05.mma.kind::tf32 (M=128, N=16,
+//     K=8: one tap each) into a 32-column TMEM accumulator and commits to an
+//     mbarrier;
+//   * the 4 warps read their 32 TMEM lanes back with tcgen05.ld 32x32b.x16
+//     (one pixel = one lane = 16 channels), apply ReLU and store 64 B/pixel.
+#include "kcommon.cuh"
+
+namespace dagrt {
+
+constexpr int kTcThreads = 128;     // = M of the MMA (one pixel per thread / TMEM lane)
+constexpr int kTcTaps = 9;
+constexpr int kTcATile = 128 * 32;  // bytes per tap per part (128 rows x 8 tf32)
+constexpr int kTcBTile = 16 * 32;   // bytes per tap per part (16 rows x 8 tf32)
+constexpr int kTcSmem = 2 * kTcTaps * kTcBTile + 2 * kTcTaps * kTcATile + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle (CuTe "INTERLEAVE").
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, N = 16, M = 128.
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(kTcIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  long long spins = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (++spins > (1ll << 28)) __trap();  // never hang the GPU on a protocol bug
+  }
+}
+
+// Write 16 bytes (4 tf32 of one row) into an interleaved K-major tile.
+__device__ __forceinline__ void put16(unsigned char* tile, int row, int khalf, float4 v) {
+  *reinterpret_cast<float4*>(tile + (row & 7) * 16 + (row >> 3) * 256 + khalf * 128) = v;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restrict__ in,
+                                                            const float* __restrict__ w,
+                                                            float* __restrict__ out, int H2, int W2) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* bhi = sm;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  unsigned char* ahi = blo + kTcTaps * kTcBTile;
+  unsigned char* alo = ahi + kTcTaps * kTcATile;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(alo + kTcTaps * kTcATile);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int t = threadIdx.x, warp = t >> 5;
+
+  // ---- one-time setup: weights (hi/lo), mbarrier, TMEM (32 columns)
+  for (int i = t; i < 16 * 72; i += kTcThreads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const long long npix = (long long)H3 * W3;
+  const long long ntiles = (npix + kTcThreads - 1) / kTcThreads;
+  const float4* src = reinterpret_cast<const float4*>(in);
+  uint32_t phase = 0;
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long m = tile * kTcThreads + t;
+    const bool live = m < npix;
+    const int p = live ? (int)(m / W3) : 0, q = live ? (int)(m % W3) : 0;
+    // ---- gather the 9 taps (18 x LDG.128 in flight), split, write A tiles
+    float4 v[kTcTaps][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int y = 2 * p + a - 1, x = 2 * q + b - 1;
+        if (live && y >= 0 && y < H2 && x >= 0 && x < W2) {
+          const size_t base = ((size_t)y * W2 + x) * 2;
+          v[a * 3 + b][0] = ldg_stream(src + base);
+          v[a * 3 + b][1] = ldg_stream(src + base + 1);
+        } else {
+          v[a * 3 + b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x = v[tap][h];
+        float4 hi, lo;
+        hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
+        hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
+        hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
+        hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+        put16(ahi + tap * kTcATile, t, h, hi);
+        put16(alo + tap * kTcATile, t, h, lo);
+      }
+    // make the generic-proxy smem writes visible to the tensor core
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- 27 MMAs by one thread, commit to the mbarrier
+    if (t == 0) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256);
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(tmem, dah, dbh, acc);
+        acc = 1;
+        tc_mma(tmem, dal, dbh, 1);
+        tc_mma(tmem, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar))
+                   : "memory");
+    }
+    tc_mbar_wait(mbar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue: lane t of TMEM = pixel m, 16 fp32 columns = 16 channels
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (live) {
+      float4* dst = reinterpret_cast<float4*>(out + (size_t)m * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    // TMEM and the A tiles are reused by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
+static const Builtin kConvTc[] = {
+    {"conv2", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kTcSmem},
+};
+DAGRT_REGISTER_BUILTINS(kConvTc);
+
+}  // namespace dagrt

@@ -226,7 +226,8 @@ __global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
 static const Builtin kDl[] = {
     {"conv1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
-    {"conv2", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    // CUDA-core variant of the second convolution (the tcgen05 one is "conv2")
+    {"conv2_ffma", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"concat", (const void*)k_concat, "const ptr, const ptr, out ptr, sint64, sint64", KF_NONE},
     {"dot", (const void*)k_dot, "const ptr, const ptr, out ptr, sint64", KF_NONE},
 };

@@ -106,54 +106,61 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
   }
 }
 
-// One merge-path tile c = diagonals [c*T, min((c+1)*T, N+E)) with start
-// coordinate (i0, j0) and end coordinate (i1, j1).  Called by all threads.
-__device__ __forceinline__ void spmv_tile(const int* __restrict__ row_ptr, const int* __restrict__ col,
-                                          const float* __restrict__ x, float* __restrict__ y,
-                                          long long N, const SpmvWs& ws, long long c, long long i0,
-                                          long long j0, long long i1, long long j1) {
-  __shared__ float s_val[kSpmvTile];
-  __shared__ int s_rend[kSpmvTile + 1];
-  const int t = threadIdx.x, warp = t >> 5;
-  __syncthreads();  // the previous tile's readers of shared memory are done
-  const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
-  // stage gathered values and row ends (rows i0 .. i1, clamped to N-1):
-  // all column indices of the thread first, then all gathers (8 independent
-  // loads in flight each); the streamed CSR arrays are evict-first in L2,
-  // the gathered vector evict-last (it is reused by every tile).
-  {
-    const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
-    int ci[kSpmvItems];
+// Tile geometry: tile c = diagonals [c*T, min((c+1)*T, N+E)), start
+// coordinate (i0, j0), end (i1, j1).
+struct SpmvTile {  // 32-bit: CSR offsets and row ids are int32 by construction
+  int c, i0, j0, i1, j1;
+};
+
+// Per-thread staging registers for one tile (loaded ahead of use).
+struct SpmvStage {
+  float xv[kSpmvItems];     // gathered x values
+  int re[kSpmvItems + 1];   // row ends
+  int rp0;                  // row_ptr[i0]
+};
+
+__device__ __forceinline__ void stage_cols(const int* __restrict__ col, const SpmvTile& T,
+                                           int (&ci)[kSpmvItems], uint64_t pol) {
+  const int t = threadIdx.x;
+  const int nn = T.j1 - T.j0;
 #pragma unroll
-    for (int u = 0; u < kSpmvItems; ++u) {
-      const int k = t + u * kSpmvThreads;
-      ci[u] = k < nn ? ldg_hint(col + j0 + k, pol_stream) : 0;
-    }
-    float xv[kSpmvItems];
-#pragma unroll
-    for (int u = 0; u < kSpmvItems; ++u) {
-      const int k = t + u * kSpmvThreads;
-      xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < kSpmvItems; ++u) {
-      const int k = t + u * kSpmvThreads;
-      if (k < nn) s_val[k] = xv[u];
-    }
-    const int nre = (int)(min(i1, N - 1) - i0 + 1);
-    int re[kSpmvItems + 1];
-#pragma unroll
-    for (int u = 0; u <= kSpmvItems; ++u) {
-      const int k = t + u * kSpmvThreads;
-      re[u] = k < nre ? ldg_hint(row_ptr + i0 + k + 1, pol_stream) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u <= kSpmvItems; ++u) {
-      const int k = t + u * kSpmvThreads;
-      if (k < nre) s_rend[k] = re[u];
-    }
+  for (int u = 0; u < kSpmvItems; ++u) {
+    const int k = t + u * kSpmvThreads;
+    ci[u] = k < nn ? ldg_hint(col + T.j0 + k, pol) : 0;
   }
-  __syncthreads();
+}
+
+__device__ __forceinline__ void stage_rows(const int* __restrict__ row_ptr, long long N,
+                                           const SpmvTile& T, SpmvStage& S, uint64_t pol) {
+  const int t = threadIdx.x;
+  const int nre = (int)(min((long long)T.i1, N - 1) - T.i0 + 1);
+#pragma unroll
+  for (int u = 0; u <= kSpmvItems; ++u) {
+    const int k = t + u * kSpmvThreads;
+    S.re[u] = k < nre ? ldg_hint(row_ptr + T.i0 + k + 1, pol) : 0;
+  }
+  S.rp0 = __ldg(row_ptr + T.i0);
+}
+
+__device__ __forceinline__ void stage_gather(const float* __restrict__ x, const SpmvTile& T,
+                                             const int (&ci)[kSpmvItems], SpmvStage& S, uint64_t pol) {
+  const int t = threadIdx.x;
+  const int nn = T.j1 - T.j0;
+#pragma unroll
+  for (int u = 0; u < kSpmvItems; ++u) {
+    const int k = t + u * kSpmvThreads;
+    S.xv[u] = k < nn ? ldg_hint(x + ci[u], pol) : 0.f;
+  }
+}
+
+// Process one staged tile (all threads): local merge search, sequential
+// consumption, segmented scan, cross-CTA deposits.
+__device__ __forceinline__ void spmv_process(float* __restrict__ y, long long N, const SpmvWs& ws,
+                                             const SpmvTile& T, const float* s_val, const int* s_rend,
+                                             int rp0) {
+  const long long c = T.c, i0 = T.i0, j0 = T.j0, i1 = T.i1;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int nn = (int)(T.j1 - T.j0), nr = (int)(T.i1 - T.i0);
 
   // thread-local merge-path search inside the tile (binary, shared memory)
   const int dl = min(t * kSpmvItems, nn + nr);
@@ -202,6 +209,7 @@ __device__ __forceinline__ void spmv_tile(const int* __restrict__ row_ptr, const
   __shared__ int s_wflag[kSpmvThreads / 32];
   __shared__ int s_first_emitter;
   __shared__ float s_carry;
+  __shared__ float s_head_val;
   if (t == 0) s_first_emitter = kSpmvThreads;
   if (lane == 31) { s_wsum[warp] = sc; s_wflag[warp] = fl ? 1 : 0; }
   __syncthreads();
@@ -214,56 +222,55 @@ __device__ __forceinline__ void spmv_tile(const int* __restrict__ row_ptr, const
   if (t == kSpmvThreads - 1) s_carry = s_incl;
   __syncthreads();
   const int fe = s_first_emitter;
-  __shared__ float s_head_val;
+  // row i0 started in an earlier tile iff row_ptr[i0] < j0
+  const bool i0_spans = (long long)rp0 < j0;
   if (emitted) {
     const float v = first_val + incoming;
-    bool spans = false;
-    if (t == fe && first_row == i0) {
-      const long long rs = __ldg(row_ptr + i0);
-      spans = ((i0 + rs) / kSpmvTile) < c;  // row started in an earlier CTA
-    }
-    if (spans) s_head_val = v;
+    if (t == fe && first_row == i0 && i0_spans) s_head_val = v;
     else y[first_row] = v;
   }
   __syncthreads();
   if (warp == 0) {
-    // (a) row i0 crossing the CTA start and ending here
-    if (fe < kSpmvThreads && i0 < N) {
-      const long long rs = __ldg(row_ptr + i0), re = __ldg(row_ptr + i0 + 1);
-      const long long cs = (i0 + rs) / kSpmvTile, ce = (i0 + re) / kSpmvTile;
-      if (cs < c && ce == c) spmv_deposit(ws, y, i0, cs, ce, c, s_head_val, true);
+    // (a) row i0 crossing the tile start and ending here
+    if (fe < kSpmvThreads && i0 < N && i0_spans) {
+      const long long cs = (i0 + rp0) / kSpmvTile;
+      spmv_deposit(ws, y, i0, cs, c, c, s_head_val, true);
     }
-    // (b) carry row i1 crossing the CTA end
+    // (b) carry row i1 crossing the tile end (its end item lies in a later tile)
     if (i1 < N) {
-      const long long rs = __ldg(row_ptr + i1), re = __ldg(row_ptr + i1 + 1);
+      const long long rs = nr > 0 ? (long long)s_rend[nr - 1] : (long long)rp0;  // row_ptr[i1]
+      const long long re = (long long)s_rend[nr];                               // row_ptr[i1+1]
       const long long cs = (i1 + rs) / kSpmvTile, ce = (i1 + re) / kSpmvTile;
-      if (ce > c && cs <= c) {
-        const float carry = s_carry;
-        spmv_deposit(ws, y, i1, cs, ce, c, carry, false);
-      }
+      if (ce > c && cs <= c) spmv_deposit(ws, y, i1, cs, ce, c, s_carry, false);
     }
   }
 }
 
 // Persistent merge-path SpMV: each CTA owns a contiguous range of tiles.  All
 // its tile boundaries (up to 256 at a time) are located first, by all 8
-// warps in parallel (32-ary searches), so the per-tile critical path is only
-// the staging gathers; consecutive tiles share their boundary.
+// warps in parallel (32-ary searches).  Tile staging is software-pipelined
+// two deep in registers: while tile c is processed from shared memory, the
+// gathers of tile c+1 and the column indices / row ends of tile c+2 are in
+// flight, so the dependent col -> x latency chain is off the critical path.
 constexpr int kSpmvChunk = 256;
 
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict__ row_ptr,
                                                        const int* __restrict__ col,
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, long long N) {
   __shared__ int s_bnd[kSpmvChunk + 1];
+  __shared__ float s_val[kSpmvTile];
+  __shared__ int s_rend[kSpmvTile + 1];
+  __shared__ int s_rp0;
   const long long E = (long long)__ldg(row_ptr + N);
   const long long total = N + E;
   const long long ntiles = (total + kSpmvTile - 1) / kSpmvTile;
   const SpmvWs ws = spmv_ws(y, N, ntiles);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
   const long long tb0 = (long long)blockIdx.x * per;
   const long long te0 = min(ntiles, tb0 + per);
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   for (long long tb = tb0; tb < te0; tb += kSpmvChunk) {
     const long long te = min(te0, tb + kSpmvChunk);
     const int nb = (int)(te - tb) + 1;
@@ -274,10 +281,60 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(const int* __restrict__ r
       if (lane == 0) s_bnd[b] = (int)i;
     }
     __syncthreads();
-    for (long long c = tb; c < te; ++c) {
+    auto tile_of = [&](long long c) {
+      SpmvTile T;
+      T.c = (int)c;
       const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
-      const long long i0 = s_bnd[c - tb], i1 = s_bnd[c - tb + 1];
-      spmv_tile(row_ptr, col, x, y, N, ws, c, i0, d0 - i0, i1, d1 - i1);
+      T.i0 = s_bnd[c - tb];
+      T.i1 = s_bnd[c - tb + 1];
+      T.j0 = (int)(d0 - T.i0);
+      T.j1 = (int)(d1 - T.i1);
+      return T;
+    };
+    // prologue: tile tb fully staged, column indices of tile tb+1 in flight
+    SpmvStage cur, nxt;
+    int ci[kSpmvItems];
+    SpmvTile Tc = tile_of(tb);
+    stage_cols(col, Tc, ci, pol_stream);
+    stage_rows(row_ptr, N, Tc, cur, pol_stream);
+    stage_gather(x, Tc, ci, cur, pol_keep);
+    SpmvTile Tn = Tc;
+    if (tb + 1 < te) {
+      Tn = tile_of(tb + 1);
+      stage_cols(col, Tn, ci, pol_stream);
+    }
+    for (long long c = tb; c < te; ++c) {
+      const int nn = Tc.j1 - Tc.j0;
+      const int nre = (int)(min((long long)Tc.i1, N - 1) - Tc.i0 + 1);
+      __syncthreads();  // previous tile's readers of s_val / s_rend are done
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        if (k < nn) s_val[k] = cur.xv[u];
+      }
+#pragma unroll
+      for (int u = 0; u <= kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        if (k < nre) s_rend[k] = cur.re[u];
+      }
+      if (t == 0) s_rp0 = cur.rp0;
+      __syncthreads();
+      const int rp0 = s_rp0;
+      // pipeline: gathers + row ends of tile c+1 (its column indices arrived
+      // during tile c-1), column indices of tile c+2
+      SpmvTile T2 = Tn;
+      if (c + 1 < te) {
+        stage_gather(x, Tn, ci, nxt, pol_keep);
+        stage_rows(row_ptr, N, Tn, nxt, pol_stream);
+      }
+      if (c + 2 < te) {
+        T2 = tile_of(c + 2);
+        stage_cols(col, T2, ci, pol_stream);
+      }
+      spmv_process(y, N, ws, Tc, s_val, s_rend, rp0);
+      cur = nxt;
+      Tc = Tn;
+      Tn = T2;
     }
   }
 }

@@ -458,49 +458,57 @@ __global__ void __launch_bounds__(256) k_lse(const float* __restrict__ r1, const
   ROW_LOOP l[r] = rlse(r1 + r * C, m[r], C);
 }
 
+// EXP and ADDV are elementwise over the flat N*C array (element e belongs
+// to row e / C, class e % C), so they stream it with fully coalesced 128-bit
+// accesses instead of per-row 80-byte strides.
+#define FLAT4_LOOP for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; \
+                        i += (long long)gridDim.x * blockDim.x)
+
 // EXP: r1[i,c] = exp(r1[i,c] - l[i])   (in place)
 __global__ void __launch_bounds__(256) k_exp_sub(float* __restrict__ r1, const float* __restrict__ l,
                                                  long long N, int C) {
-  if (pair_ok(C, r1, l)) {
-    PAIR_LOOP {
-      float v[20];
-      ld20(r1, i, v);
-      const float2 ll = reinterpret_cast<const float2*>(l)[i];
-#pragma unroll
-      for (int c = 0; c < 10; ++c) { v[c] = expf(v[c] - ll.x); v[10 + c] = expf(v[10 + c] - ll.y); }
-      st20(r1, i, v);
-    }
-    TAIL_ROW for (int c = 0; c < C; ++c) r1[(N - 1) * C + c] = expf(r1[(N - 1) * C + c] - l[N - 1]);
-    return;
+  const long long total = N * C;
+  const long long n4 = (C >= 4 && aligned16(r1)) ? total / 4 : 0;
+  float4* p4 = reinterpret_cast<float4*>(r1);
+  FLAT4_LOOP {
+    float4 v = p4[i];
+    const long long e = 4 * i, r = e / C;
+    const int rem = (int)(e - r * C);  // 4 elements span at most 2 rows (C >= 4)
+    const float la = __ldg(l + r);
+    const float lb = rem + 3 >= C ? __ldg(l + r + 1) : la;
+    v.x = expf(v.x - la);
+    v.y = expf(v.y - (rem + 1 < C ? la : lb));
+    v.z = expf(v.z - (rem + 2 < C ? la : lb));
+    v.w = expf(v.w - (rem + 3 < C ? la : lb));
+    p4[i] = v;
   }
-  ROW_LOOP {
-    float* p = r1 + r * C;
-    const float ll = l[r];
-    for (int c = 0; c < C; ++c) p[c] = expf(p[c] - ll);
-  }
+  for (long long e = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    r1[e] = expf(r1[e] - l[e / C]);
 }
 
 // ADDV: r2[i,c] += b[c]   (in place)
 __global__ void __launch_bounds__(256) k_addv(float* __restrict__ r2, const float* __restrict__ b,
                                               long long N, int C) {
-  if (pair_ok(C, r2)) {
-    float bb[10];
-#pragma unroll
-    for (int c = 0; c < 10; ++c) bb[c] = __ldg(b + c);
-    PAIR_LOOP {
-      float v[20];
-      ld20(r2, i, v);
-#pragma unroll
-      for (int c = 0; c < 10; ++c) { v[c] += bb[c]; v[10 + c] += bb[c]; }
-      st20(r2, i, v);
-    }
-    TAIL_ROW for (int c = 0; c < C; ++c) r2[(N - 1) * C + c] += b[c];
-    return;
+  __shared__ float sb[2 * kMaxClasses + 4];
+  const bool small = C <= kMaxClasses;
+  if (small && threadIdx.x < 2 * C + 4) sb[threadIdx.x] = __ldg(b + (threadIdx.x % C));
+  __syncthreads();
+  const long long total = N * C;
+  const long long n4 = (small && aligned16(r2)) ? total / 4 : 0;
+  float4* p4 = reinterpret_cast<float4*>(r2);
+  FLAT4_LOOP {
+    float4 v = p4[i];
+    const int c0 = (int)((4 * i) % C);  // sb[c0 + j] = b[(c0 + j) % C]
+    v.x += sb[c0];
+    v.y += sb[c0 + 1];
+    v.z += sb[c0 + 2];
+    v.w += sb[c0 + 3];
+    p4[i] = v;
   }
-  ROW_LOOP {
-    float* p = r2 + r * C;
-    for (int c = 0; c < C; ++c) p[c] += b[c];
-  }
+  for (long long e = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    r2[e] += b[e % C];
 }
 
 // SOFTMAX: row softmax in place (max-shifted)

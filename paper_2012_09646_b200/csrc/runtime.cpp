@@ -150,6 +150,14 @@ struct ProfRec {
   void* ev1;
 };
 
+struct TimeRec {
+  int32_t kind, stream;
+  int64_t vertex, id;
+  uint64_t bytes;
+  void* ev0;
+  void* ev1;
+};
+
 struct ArrayRec {
   char* dev = nullptr;
   char* host = nullptr;
@@ -215,6 +223,8 @@ struct dagrt_ctx_s {
   void* serial_stream = nullptr;
   std::vector<dagrt_graph_s*> graphs;
   std::vector<ProfRec> prof;           // timed launches awaiting collection
+  bool timeline = false;
+  std::vector<TimeRec> tl;             // timeline records awaiting export
   std::vector<void*> tev_pool;         // free timing events
   std::vector<void*> all_tev;
 
@@ -306,15 +316,37 @@ dagrt_status get_timing_event(dagrt_ctx c, void** ev) {
 
 // The one place kernels are enqueued; optionally bracketed by timing events
 // on the launching stream (dagrt_profile_enable).
+// Timeline bracket (dagrt_timeline_enable): opens before an item on stream s.
+dagrt_status tl_begin(dagrt_ctx c, void* s, void** e0) {
+  *e0 = nullptr;
+  if (!c->timeline) return DAGRT_OK;
+  if (dagrt_status st = get_timing_event(c, e0)) return st;
+  CK(c->be->record(*e0, s), "cudaEventRecord timeline");
+  return DAGRT_OK;
+}
+dagrt_status tl_end(dagrt_ctx c, void* s, void* e0, int32_t kind, int32_t sidx, int64_t vertex,
+                    int64_t id, uint64_t bytes) {
+  if (!c->timeline || !e0) return DAGRT_OK;
+  void* e1;
+  if (dagrt_status st = get_timing_event(c, &e1)) return st;
+  CK(c->be->record(e1, s), "cudaEventRecord timeline");
+  c->tl.push_back(TimeRec{kind, sidx, vertex, id, bytes, e0, e1});
+  return DAGRT_OK;
+}
+
+// The one place kernels are enqueued; optionally bracketed by timing events
+// on the launching stream (dagrt_profile_enable / dagrt_timeline_enable).
 dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim3 b, void** argv,
-                       uint32_t smem, void* s) {
-  void *e0 = nullptr, *e1 = nullptr;
+                       uint32_t smem, void* s, int32_t sidx = -1, int64_t vertex = -1) {
+  void *e0 = nullptr, *e1 = nullptr, *t0 = nullptr;
   if (k->prof) {
     if (dagrt_status st = get_timing_event(c, &e0)) return st;
     if (dagrt_status st = get_timing_event(c, &e1)) return st;
     CK(c->be->record(e0, s), "cudaEventRecord profile");
   }
+  if (dagrt_status st = tl_begin(c, s, &t0)) return st;
   CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+  if (dagrt_status st = tl_end(c, s, t0, 0, sidx, vertex, kh, 0)) return st;
   if (k->prof) {
     CK(c->be->record(e1, s), "cudaEventRecord profile");
     c->prof.push_back(ProfRec{kh, e0, e1});
@@ -451,8 +483,11 @@ dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   c->st.d2h_bytes += n;
   c->st.d2h_copies++;
   if (!c->be->real()) return DAGRT_OK;
+  void* t0;
+  if (dagrt_status st_ = tl_begin(c, c->d2h_stream, &t0)) return st_;
   CK(c->be->copy_async(dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream),
      "cudaMemcpyAsync D2H");
+  if (dagrt_status st_ = tl_end(c, c->d2h_stream, t0, 2, -5, -1, array_index(c, a), n)) return st_;
   CK(c->be->stream_sync(c->d2h_stream), "cudaStreamSynchronize D2H");
   c->st.host_syncs++;
   return DAGRT_OK;
@@ -777,7 +812,10 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
         c->st.h2d_bytes += a->bytes;
         c->st.h2d_copies++;
         if (c->be->real()) {
+          void* t0;
+          if (dagrt_status st_ = tl_begin(c, s, &t0)) return st_;
           CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
+          if (dagrt_status st_ = tl_end(c, s, t0, 1, -3, vid, array_index(c, a), a->bytes)) return st_;
           CK(c->be->stream_sync(s), "cudaStreamSynchronize");
           c->st.host_syncs++;
         }
@@ -785,7 +823,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       }
     }
     trace_op(c, DAGRT_OP_LAUNCH, -3, vid, kh, 0);
-    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s)) return st_;
+    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, -3, vid)) return st_;
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
     c->st.host_syncs++;
     c->vertices.push_back(VertexRec{0, 0, -1, nullptr, 0, 0});
@@ -825,7 +863,12 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       trace_op(c, DAGRT_OP_H2D, c->cfg.prefetch ? -2 : sid, array_index(c, a), 0, a->bytes);
       c->st.h2d_bytes += a->bytes;
       c->st.h2d_copies++;
+      void* t0;
+      if (dagrt_status st_ = tl_begin(c, cs, &t0)) return st_;
       CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, cs), "cudaMemcpyAsync H2D");
+      if (dagrt_status st_ = tl_end(c, cs, t0, 1, c->cfg.prefetch ? -2 : sid, vid, array_index(c, a),
+                                    a->bytes))
+        return st_;
       a->coh = COH_BOTH;
       if (c->cfg.prefetch) {
         if (!a->h2d_ev) CK(c->be->event_create(&a->h2d_ev), "cudaEventCreate");
@@ -848,7 +891,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   void* ev;
   if (dagrt_status st = get_event(c, &ev)) return st;
   trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
-  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s)) return st_;
+  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, vid)) return st_;
   trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
   CK(c->be->record(ev, s), "cudaEventRecord");
 
@@ -1092,6 +1135,36 @@ dagrt_status dagrt_profile_collect(dagrt_ctx c, dagrt_kernel kh, int32_t* count,
     }
   }
   if (ce > -1e300) *busy_ms += ce - cs;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_timeline_enable(dagrt_ctx c, int32_t on) {
+  GUARD(c);
+  c->timeline = on != 0;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_timeline_export(dagrt_ctx c, dagrt_timeline_rec* recs, uint32_t* n) {
+  GUARD(c);
+  if (!n) return fail(c, DAGRT_EINVAL, "null n");
+  uint32_t cap = *n;
+  *n = (uint32_t)c->tl.size();
+  if (!recs) return DAGRT_OK;
+  if (cap < *n) return fail(c, DAGRT_EINVAL, "capacity");
+  void* ref = c->tl.empty() ? nullptr : c->tl[0].ev0;
+  for (size_t i = 0; i < c->tl.size(); ++i) {
+    TimeRec& r = c->tl[i];
+    CK(c->be->event_sync(r.ev1), "cudaEventSynchronize timeline");
+    float a = 0.f, b = 0.f;
+    CK(c->be->elapsed(&a, ref, r.ev0), "cudaEventElapsedTime");
+    CK(c->be->elapsed(&b, ref, r.ev1), "cudaEventElapsedTime");
+    recs[i] = dagrt_timeline_rec{r.kind, r.stream, r.vertex, r.id, r.bytes, a, b};
+  }
+  for (TimeRec& r : c->tl) {
+    c->tev_pool.push_back(r.ev0);
+    c->tev_pool.push_back(r.ev1);
+  }
+  c->tl.clear();
   return DAGRT_OK;
 }
 

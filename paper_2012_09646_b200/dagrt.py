@@ -431,3 +431,32 @@ class Context:
         n, s, b = C.c_int32(), C.c_double(), C.c_double()
         self._check(lib().dagrt_profile_collect(self._c, k.handle, C.byref(n), C.byref(s), C.byref(b)))
         return n.value, s.value, b.value
+
+
+class TimelineRec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("stream", C.c_int32), ("vertex", C.c_int64), ("id", C.c_int64),
+                ("bytes", C.c_uint64), ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
+def _timeline_enable(self, on=True):
+    L = lib()
+    L.dagrt_timeline_enable.argtypes = [C.c_void_p, C.c_int32]
+    L.dagrt_timeline_enable.restype = C.c_int32
+    self._check(L.dagrt_timeline_enable(self._c, 1 if on else 0))
+
+
+def _timeline_export(self):
+    """[(kind, stream, vertex, id, bytes, start_ms, end_ms)]; kind 'kernel'|'h2d'|'d2h'."""
+    L = lib()
+    L.dagrt_timeline_export.argtypes = [C.c_void_p, C.POINTER(TimelineRec), C.POINTER(C.c_uint32)]
+    L.dagrt_timeline_export.restype = C.c_int32
+    n = C.c_uint32(0)
+    self._check(L.dagrt_timeline_export(self._c, None, C.byref(n)))
+    R = (TimelineRec * max(1, n.value))()
+    self._check(L.dagrt_timeline_export(self._c, R, C.byref(n)))
+    kinds = {0: "kernel", 1: "h2d", 2: "d2h"}
+    return [(kinds[r.kind], r.stream, r.vertex, r.id, r.bytes, r.start_ms, r.end_ms) for r in R[:n.value]]
+
+
+Context.timeline = _timeline_enable
+Context.timeline_export = _timeline_export

@@ -8,6 +8,8 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
+CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64  # csrc/kernels_conv_tc.cu kTcSmem
+G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 256 * 8      # merge items per CTA (csrc/kernels_hits.cu)
 
@@ -47,7 +49,7 @@ class Hits(Program):
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
-        gs = min(self.ncta, 6 * SMS)  # persistent merge-path CTAs (6 resident per SM)
+        gs = min(self.ncta, 3 * SMS)  # persistent merge-path CTAs (3 resident per SM)
         self.it = [
             P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
             P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
@@ -148,8 +150,8 @@ class DeepLearning(Program):
             P("conv1", g1, 256, [a["y"], a["w1"], a["c1y"], h, w]),
             P("pool", gp, 256, [a["c1x"], a["px"], h1, w1]),
             P("pool", gp, 256, [a["c1y"], a["py"], h1, w1]),
-            P("conv2", g2, 256, [a["px"], a["w2"], a["c2x"], h2, w2]),
-            P("conv2", g2, 256, [a["py"], a["w2"], a["c2y"], h2, w2]),
+            P("conv2", G2TC, 128, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", G2TC, 128, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
             P("concat", gc, 256, [a["c2x"], a["c2y"], a["z"], nz // 2, nz // 2]),
             P("dot", min(gc, 1024), 256, [a["z"], a["wd"], a["r"], nz]),
         ]

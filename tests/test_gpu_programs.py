@@ -339,3 +339,26 @@ def test_dl_full_size_sampled(ctx):
     assert abs(p.result() - r_ref) <= 1e-3 * abs(r_ref)
     del p, z, wd
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
+def test_dl_conv2_ffma_variant_matches_oracle(ctx, h, w):
+    """The CUDA-core conv2 variant (conv2_ffma) against the oracle too."""
+    p = DeepLearning(ctx, h=h, w=w)
+    p.load_inputs(1)
+    p.run()
+    ctx.sync()
+    (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
+    out = torch.zeros(h3 * w3s * 16, device="cuda")
+    torch.cuda.synchronize()
+    o_arr = ctx.register_tensor(f"c2_ffma_{h}", out)
+    ctx.launch("conv2_ffma", ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
+    ctx.sync()
+    spec = synth.spec_dl(h, w)
+    w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
+    px = p.t["px"][:h2 * w2s * 8].cpu().numpy().reshape(h2, w2s, 8)
+    ref = odl.conv3x3s2(px, w2)
+    ok, info = close(out.cpu().numpy().reshape(h3, w3s, 16), ref)
+    assert ok, info
+    ok, info = close(p.t["c2x"][:h3 * w3s * 16].cpu().numpy().reshape(h3, w3s, 16), ref)
+    assert ok, info
