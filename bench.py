@@ -247,6 +247,14 @@ def main():
         res["serial_stream_ms"] = time_steps(seprog.run, K, W, dist) / K
         eg = eprog.graph()
         res["graph_stream_ms"] = time_steps(eg.run, K, W, dist) / K
+        # NEXT(f1): the same scheduler with deferred submission + batch graph cache
+        cctx = D.Context(device=local, graph_cache=True)
+        cprog = make_program(name, cctx, "resident", share=prog)
+        res["f1_graph_cache_resident_ms"] = time_steps(cprog.run, K, W, dist) / K
+        res["f1_graph_replays"] = cctx.stats()["graph_replays"]
+        csctx = D.Context(device=local, graph_cache=True)
+        csprog = make_program(name, csctx, "stream", share=eprog)
+        res["f1_graph_cache_stream_ms"] = time_steps(csprog.run, K, W, dist) / K
 
     if rank != 0:
         return

@@ -72,6 +72,10 @@ typedef struct {
   int32_t max_streams; /* 0 = unlimited; otherwise cap on compute streams */
   int32_t record_dag;  /* 1: keep vertices/edges/trace for dagrt_dag_export/dagrt_trace_export */
   int32_t backend;     /* DAGRT_BACKEND_CUDA or DAGRT_BACKEND_RECORD */
+  int32_t graph_cache; /* 1: deferred submission + batch cache replayed as CUDA graphs
+                          (SURVEY §8(f) f1): launches are buffered until the next host
+                          synchronisation; a batch seen again is replayed with one
+                          cudaGraphLaunch.  Dependencies are still inferred per launch. */
 } dagrt_config;
 
 typedef struct { uint32_t x, y, z; } dagrt_dim3;
@@ -232,6 +236,9 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes, h2d_copies, d2h_copies;
   uint64_t host_syncs;         /* host-blocking waits (event or stream) */
   uint64_t sched_ns;           /* host ns spent inside dagrt_launch */
+  uint64_t graph_replays;      /* batches replayed from the graph cache */
+  uint64_t graph_captures;     /* batches captured into a new graph */
+  uint64_t eager_batches;      /* batches issued eagerly (first sighting) */
 } dagrt_stats_t;
 /* Copy min(size, sizeof(dagrt_stats_t)) bytes of the counters to out. */
 dagrt_status dagrt_stats(dagrt_ctx ctx, void* out, size_t size);

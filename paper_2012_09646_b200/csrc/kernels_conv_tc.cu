@@ -124,12 +124,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
   const float4* src = reinterpret_cast<const float4*>(in);
   uint32_t phase = 0;
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long m = tile * kTcThreads + t;
+  // gather the 9 taps of pixel m (18 x LDG.128 in flight)
+  float4 v[kTcTaps][2];
+  auto gather = [&](long long m) {
     const bool live = m < npix;
     const int p = live ? (int)(m / W3) : 0, q = live ? (int)(m % W3) : 0;
-    // ---- gather the 9 taps (18 x LDG.128 in flight), split, write A tiles
-    float4 v[kTcTaps][2];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -144,6 +143,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
           v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+  };
+  if ((long long)blockIdx.x < ntiles) gather((long long)blockIdx.x * kTcThreads + t);
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long m = tile * kTcThreads + t;
+    const bool live = m < npix;
+    // ---- split the staged taps into TF32 hi/lo and write the A tiles
 #pragma unroll
     for (int tap = 0; tap < kTcTaps; ++tap)
 #pragma unroll
@@ -180,6 +186,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
                        smem_u32(mbar))
                    : "memory");
     }
+    // next tile's gathers are in flight while the tensor core works
+    if (tile + gridDim.x < ntiles) gather((tile + gridDim.x) * kTcThreads + t);
     tc_mbar_wait(mbar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;");

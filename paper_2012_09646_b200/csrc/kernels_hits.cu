@@ -106,171 +106,41 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
   }
 }
 
-// Tile geometry: tile c = diagonals [c*T, min((c+1)*T, N+E)), start
-// coordinate (i0, j0), end (i1, j1).
-struct SpmvTile {  // 32-bit: CSR offsets and row ids are int32 by construction
-  int c, i0, j0, i1, j1;
-};
-
-// Per-thread staging registers for one tile (loaded ahead of use).
-struct SpmvStage {
-  float xv[kSpmvItems];     // gathered x values
-  int re[kSpmvItems + 1];   // row ends
-  int rp0;                  // row_ptr[i0]
-};
-
-__device__ __forceinline__ void stage_cols(const int* __restrict__ col, const SpmvTile& T,
-                                           int (&ci)[kSpmvItems], uint64_t pol) {
-  const int t = threadIdx.x;
-  const int nn = T.j1 - T.j0;
-#pragma unroll
-  for (int u = 0; u < kSpmvItems; ++u) {
-    const int k = t + u * kSpmvThreads;
-    ci[u] = k < nn ? ldg_hint(col + T.j0 + k, pol) : 0;
-  }
-}
-
-__device__ __forceinline__ void stage_rows(const int* __restrict__ row_ptr, long long N,
-                                           const SpmvTile& T, SpmvStage& S, uint64_t pol) {
-  const int t = threadIdx.x;
-  const int nre = (int)(min((long long)T.i1, N - 1) - T.i0 + 1);
-#pragma unroll
-  for (int u = 0; u <= kSpmvItems; ++u) {
-    const int k = t + u * kSpmvThreads;
-    S.re[u] = k < nre ? ldg_hint(row_ptr + T.i0 + k + 1, pol) : 0;
-  }
-  S.rp0 = __ldg(row_ptr + T.i0);
-}
-
-__device__ __forceinline__ void stage_gather(const float* __restrict__ x, const SpmvTile& T,
-                                             const int (&ci)[kSpmvItems], SpmvStage& S, uint64_t pol) {
-  const int t = threadIdx.x;
-  const int nn = T.j1 - T.j0;
-#pragma unroll
-  for (int u = 0; u < kSpmvItems; ++u) {
-    const int k = t + u * kSpmvThreads;
-    S.xv[u] = k < nn ? ldg_hint(x + ci[u], pol) : 0.f;
-  }
-}
-
-// Process one staged tile (all threads): local merge search, sequential
-// consumption, segmented scan, cross-CTA deposits.
-__device__ __forceinline__ void spmv_process(float* __restrict__ y, long long N, const SpmvWs& ws,
-                                             const SpmvTile& T, const float* s_val, const int* s_rend,
-                                             int rp0) {
-  const long long c = T.c, i0 = T.i0, j0 = T.j0, i1 = T.i1;
-  const int t = threadIdx.x, warp = t >> 5;
-  const int nn = (int)(T.j1 - T.j0), nr = (int)(T.i1 - T.i0);
-
-  // thread-local merge-path search inside the tile (binary, shared memory)
-  const int dl = min(t * kSpmvItems, nn + nr);
-  int lo = max(0, dl - nn), hi = min(dl, nr);
-  while (lo < hi) {
-    const int p = (lo + hi) >> 1;
-    if ((long long)s_rend[p] - j0 <= dl - p - 1) lo = p + 1;
-    else hi = p;
-  }
-  int ri = lo, nj = dl - lo;  // local row index, local nnz index
-  const int de = min(dl + kSpmvItems, nn + nr);
-  float sum = 0.f;
-  bool emitted = false;
-  long long first_row = -1;
-  float first_val = 0.f;
-  for (int it = dl; it < de; ++it) {
-    const bool row_end = (ri < nr) && ((long long)s_rend[ri] - j0 <= nj);
-    if (row_end) {
-      if (!emitted) {
-        emitted = true;
-        first_row = i0 + ri;
-        first_val = sum;
-      } else {
-        y[i0 + ri] = sum;
-      }
-      sum = 0.f;
-      ++ri;
-    } else {
-      sum += s_val[nj];
-      ++nj;
-    }
-  }
-  // segmented inclusive scan s(t) = sum(t) + (emitted(t) ? 0 : s(t-1)):
-  // warp shuffles, then one cross-warp step through shared memory (fixed
-  // combination order -> deterministic)
-  const int lane = t & 31;
-  float sc = sum;
-  bool fl = emitted;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const float yv = __shfl_up_sync(0xffffffffu, sc, off);
-    const bool f = __shfl_up_sync(0xffffffffu, fl, off);
-    if (lane >= off && !fl) { sc += yv; fl = f; }
-  }
-  __shared__ float s_wsum[kSpmvThreads / 32];
-  __shared__ int s_wflag[kSpmvThreads / 32];
-  __shared__ int s_first_emitter;
-  __shared__ float s_carry;
-  __shared__ float s_head_val;
-  if (t == 0) s_first_emitter = kSpmvThreads;
-  if (lane == 31) { s_wsum[warp] = sc; s_wflag[warp] = fl ? 1 : 0; }
-  __syncthreads();
-  if (emitted) atomicMin(&s_first_emitter, t);
-  float win = 0.f;  // carry into this warp from warps 0 .. warp-1
-  for (int w = 0; w < warp; ++w) win = s_wflag[w] ? s_wsum[w] : win + s_wsum[w];
-  const float s_incl = fl ? sc : sc + win;
-  float incoming = __shfl_up_sync(0xffffffffu, s_incl, 1);  // s(t-1)
-  if (lane == 0) incoming = win;
-  if (t == kSpmvThreads - 1) s_carry = s_incl;
-  __syncthreads();
-  const int fe = s_first_emitter;
-  // row i0 started in an earlier tile iff row_ptr[i0] < j0
-  const bool i0_spans = (long long)rp0 < j0;
-  if (emitted) {
-    const float v = first_val + incoming;
-    if (t == fe && first_row == i0 && i0_spans) s_head_val = v;
-    else y[first_row] = v;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    // (a) row i0 crossing the tile start and ending here
-    if (fe < kSpmvThreads && i0 < N && i0_spans) {
-      const long long cs = (i0 + rp0) / kSpmvTile;
-      spmv_deposit(ws, y, i0, cs, c, c, s_head_val, true);
-    }
-    // (b) carry row i1 crossing the tile end (its end item lies in a later tile)
-    if (i1 < N) {
-      const long long rs = nr > 0 ? (long long)s_rend[nr - 1] : (long long)rp0;  // row_ptr[i1]
-      const long long re = (long long)s_rend[nr];                               // row_ptr[i1+1]
-      const long long cs = (i1 + rs) / kSpmvTile, ce = (i1 + re) / kSpmvTile;
-      if (ce > c && cs <= c) spmv_deposit(ws, y, i1, cs, ce, c, s_carry, false);
-    }
-  }
-}
-
-// Persistent merge-path SpMV: each CTA owns a contiguous range of tiles.  All
-// its tile boundaries (up to 256 at a time) are located first, by all 8
-// warps in parallel (32-ary searches).  Tile staging is software-pipelined
-// two deep in registers: while tile c is processed from shared memory, the
-// gathers of tile c+1 and the column indices / row ends of tile c+2 are in
-// flight, so the dependent col -> x latency chain is off the critical path.
+// Persistent merge-path SpMV.  CTA b owns the contiguous tile range
+// [b*per, (b+1)*per).  All its tile boundaries (up to 256 at a time) are
+// located first by all 8 warps in parallel (32-ary searches).  Rows that
+// cross tile boundaries INSIDE the CTA's range are carried from tile to tile
+// in shared memory (no atomics, no fences); only the row crossing the CTA's
+// start and the row crossing its end are finished across CTAs (spmv_deposit,
+// slots indexed by CTA), so at most two deposits per CTA leave the per-tile
+// critical path clean.
 constexpr int kSpmvChunk = 256;
 
-__global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict__ row_ptr,
                                                        const int* __restrict__ col,
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, long long N) {
   __shared__ int s_bnd[kSpmvChunk + 1];
   __shared__ float s_val[kSpmvTile];
   __shared__ int s_rend[kSpmvTile + 1];
-  __shared__ int s_rp0;
+  __shared__ float s_wsum[kSpmvThreads / 32];
+  __shared__ int s_wflag[kSpmvThreads / 32];
+  __shared__ int s_first_emitter;
+  __shared__ float s_carry, s_head_val, s_cta_carry;
   const long long E = (long long)__ldg(row_ptr + N);
   const long long total = N + E;
   const long long ntiles = (total + kSpmvTile - 1) / kSpmvTile;
-  const SpmvWs ws = spmv_ws(y, N, ntiles);
+  const SpmvWs ws = spmv_ws(y, N, gridDim.x);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const long long tb0 = (long long)blockIdx.x * per;
+  const long long me = blockIdx.x;
+  const long long tb0 = me * per;
   const long long te0 = min(ntiles, tb0 + per);
+  if (tb0 >= te0) return;  // uniform per CTA
   const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+  auto cta_of_diag = [&](long long d) { return (d / kSpmvTile) / per; };
+  if (t == 0) s_cta_carry = 0.f;
+
   for (long long tb = tb0; tb < te0; tb += kSpmvChunk) {
     const long long te = min(te0, tb + kSpmvChunk);
     const int nb = (int)(te - tb) + 1;
@@ -281,60 +151,122 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict_
       if (lane == 0) s_bnd[b] = (int)i;
     }
     __syncthreads();
-    auto tile_of = [&](long long c) {
-      SpmvTile T;
-      T.c = (int)c;
-      const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
-      T.i0 = s_bnd[c - tb];
-      T.i1 = s_bnd[c - tb + 1];
-      T.j0 = (int)(d0 - T.i0);
-      T.j1 = (int)(d1 - T.i1);
-      return T;
-    };
-    // prologue: tile tb fully staged, column indices of tile tb+1 in flight
-    SpmvStage cur, nxt;
-    int ci[kSpmvItems];
-    SpmvTile Tc = tile_of(tb);
-    stage_cols(col, Tc, ci, pol_stream);
-    stage_rows(row_ptr, N, Tc, cur, pol_stream);
-    stage_gather(x, Tc, ci, cur, pol_keep);
-    SpmvTile Tn = Tc;
-    if (tb + 1 < te) {
-      Tn = tile_of(tb + 1);
-      stage_cols(col, Tn, ci, pol_stream);
-    }
     for (long long c = tb; c < te; ++c) {
-      const int nn = Tc.j1 - Tc.j0;
-      const int nre = (int)(min((long long)Tc.i1, N - 1) - Tc.i0 + 1);
-      __syncthreads();  // previous tile's readers of s_val / s_rend are done
+      const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
+      const long long i0 = s_bnd[c - tb], i1 = s_bnd[c - tb + 1];
+      const long long j0 = d0 - i0, j1 = d1 - i1;
+      const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
+      const int nre = (int)(min(i1, N - 1) - i0 + 1);
+      // ---- stage: column indices, then gathers (8 loads in flight each), row ends
+      int ci[kSpmvItems];
 #pragma unroll
       for (int u = 0; u < kSpmvItems; ++u) {
         const int k = t + u * kSpmvThreads;
-        if (k < nn) s_val[k] = cur.xv[u];
+        ci[u] = k < nn ? ldg_hint(col + j0 + k, pol_stream) : 0;
+      }
+      int re[kSpmvItems + 1];
+#pragma unroll
+      for (int u = 0; u <= kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        re[u] = k < nre ? ldg_hint(row_ptr + i0 + k + 1, pol_stream) : 0;
+      }
+      const int rp0 = __ldg(row_ptr + i0);
+      float xv[kSpmvItems];
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
+      }
+      __syncthreads();  // (A) the previous tile's readers of shared memory are done
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        if (k < nn) s_val[k] = xv[u];
       }
 #pragma unroll
       for (int u = 0; u <= kSpmvItems; ++u) {
         const int k = t + u * kSpmvThreads;
-        if (k < nre) s_rend[k] = cur.re[u];
+        if (k < nre) s_rend[k] = re[u];
       }
-      if (t == 0) s_rp0 = cur.rp0;
-      __syncthreads();
-      const int rp0 = s_rp0;
-      // pipeline: gathers + row ends of tile c+1 (its column indices arrived
-      // during tile c-1), column indices of tile c+2
-      SpmvTile T2 = Tn;
-      if (c + 1 < te) {
-        stage_gather(x, Tn, ci, nxt, pol_keep);
-        stage_rows(row_ptr, N, Tn, nxt, pol_stream);
+      if (t == 0) s_first_emitter = kSpmvThreads;
+      __syncthreads();  // (B)
+      // ---- thread-local merge-path search and sequential consumption
+      const int dl = min(t * kSpmvItems, nn + nr);
+      int lo = max(0, dl - nn), hi = min(dl, nr);
+      while (lo < hi) {
+        const int p = (lo + hi) >> 1;
+        if ((long long)s_rend[p] - j0 <= dl - p - 1) lo = p + 1;
+        else hi = p;
       }
-      if (c + 2 < te) {
-        T2 = tile_of(c + 2);
-        stage_cols(col, T2, ci, pol_stream);
+      int ri = lo, nj = dl - lo;
+      const int de = min(dl + kSpmvItems, nn + nr);
+      float sum = 0.f, first_val = 0.f;
+      bool emitted = false;
+      long long first_row = -1;
+      for (int it = dl; it < de; ++it) {
+        const bool row_end = (ri < nr) && ((long long)s_rend[ri] - j0 <= nj);
+        if (row_end) {
+          if (!emitted) {
+            emitted = true;
+            first_row = i0 + ri;
+            first_val = sum;
+          } else {
+            y[i0 + ri] = sum;
+          }
+          sum = 0.f;
+          ++ri;
+        } else {
+          sum += s_val[nj];
+          ++nj;
+        }
       }
-      spmv_process(y, N, ws, Tc, s_val, s_rend, rp0);
-      cur = nxt;
-      Tc = Tn;
-      Tn = T2;
+      // ---- segmented inclusive scan over threads (warp shuffles + one
+      // fixed-order cross-warp step): s(t) = sum(t) + (emitted(t) ? 0 : s(t-1))
+      float sc = sum;
+      bool fl = emitted;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float yv = __shfl_up_sync(0xffffffffu, sc, off);
+        const bool f = __shfl_up_sync(0xffffffffu, fl, off);
+        if (lane >= off && !fl) { sc += yv; fl = f; }
+      }
+      if (lane == 31) { s_wsum[warp] = sc; s_wflag[warp] = fl ? 1 : 0; }
+      if (emitted) atomicMin(&s_first_emitter, t);
+      __syncthreads();  // (C)
+      float win = 0.f;
+      for (int w = 0; w < warp; ++w) win = s_wflag[w] ? s_wsum[w] : win + s_wsum[w];
+      const float s_incl = fl ? sc : sc + win;
+      float incoming = __shfl_up_sync(0xffffffffu, s_incl, 1);  // s(t-1)
+      if (lane == 0) incoming = win;
+      const int fe = s_first_emitter;
+      const bool cont = (long long)rp0 < j0;  // row i0 started before this tile
+      const float carry_in = (cont && c > tb0) ? s_cta_carry : 0.f;
+      const bool head_x = cont && cta_of_diag(i0 + rp0) < me;  // row i0 began in an earlier CTA
+      if (emitted) {
+        float v = first_val + incoming;
+        if (t == fe && first_row == i0) {
+          v += carry_in;
+          if (head_x) s_head_val = v;
+          else y[i0] = v;
+        } else {
+          y[first_row] = v;
+        }
+      }
+      if (t == kSpmvThreads - 1) s_carry = s_incl;
+      __syncthreads();  // (D)
+      // running partial of the row crossing this tile's end (this CTA's share)
+      const float new_carry = fe < kSpmvThreads ? s_carry : carry_in + s_carry;
+      if (warp == 0) {
+        if (fe < kSpmvThreads && head_x)
+          spmv_deposit(ws, y, i0, cta_of_diag(i0 + rp0), me, me, s_head_val, true);
+        if (c == te0 - 1 && i1 < N) {
+          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] : (long long)rp0;  // row_ptr[i1]
+          const long long rend = (long long)s_rend[nr];                             // row_ptr[i1+1]
+          const long long as = cta_of_diag(i1 + rs), ae = cta_of_diag(i1 + rend);
+          if (ae > me && as <= me) spmv_deposit(ws, y, i1, as, ae, me, new_carry, false);
+        }
+      }
+      if (t == 0) s_cta_carry = new_carry;  // read by the next tile after barrier (C)
     }
   }
 }

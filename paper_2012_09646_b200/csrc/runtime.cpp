@@ -62,7 +62,7 @@ struct Backend {
   virtual cudaError_t elapsed(float* ms, void* a, void* b) = 0;
   virtual cudaError_t event_destroy(void* e) = 0;
   virtual cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
-                             bool coop) = 0;
+                             bool coop, int nargs) = 0;
   virtual cudaError_t record(void* e, void* s) = 0;
   virtual cudaError_t wait(void* s, void* e) = 0;
   virtual cudaError_t event_sync(void* e) = 0;
@@ -88,7 +88,7 @@ struct CudaBackend final : Backend {
   }
   cudaError_t event_destroy(void* e) override { return cudaEventDestroy((cudaEvent_t)e); }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
-                     bool coop) override {
+                     bool coop, int) override {
     if (coop) return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
     return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
   }
@@ -115,7 +115,7 @@ struct RecordBackend final : Backend {
   cudaError_t event_create_timing(void** e) override { *e = (void*)(next += 16); return cudaSuccess; }
   cudaError_t elapsed(float* ms, void*, void*) override { *ms = 0.f; return cudaSuccess; }
   cudaError_t event_destroy(void*) override { return cudaSuccess; }
-  cudaError_t launch(const void*, dim3, dim3, void**, size_t, void*, bool) override {
+  cudaError_t launch(const void*, dim3, dim3, void**, size_t, void*, bool, int) override {
     return cudaSuccess;
   }
   cudaError_t record(void*, void*) override { return cudaSuccess; }
@@ -126,6 +126,328 @@ struct RecordBackend final : Backend {
     return cudaSuccess;
   }
   bool real() const override { return false; }
+};
+
+// ------------------------------------------------------------ graph cache
+// Deferred submission + trace cache: while enabled, the stream operations
+// the scheduler decides (launches, event records, cross-stream waits, copies)
+// are buffered instead of issued.  At the next host synchronisation the
+// buffered batch is keyed by its exact content; a batch seen for the second
+// time is stream-captured into a CUDA graph (fork/join over every stream it
+// uses, so the graph reproduces the scheduler's multi-stream schedule), and
+// later identical batches replay that graph with one cudaGraphLaunch.
+// Dependencies are still inferred at run time for every launch; only the
+// CUDA submission is cached.  Events recorded inside a replayed graph are
+// aliased to one real "batch event" recorded after the graph, so host syncs
+// and later cross-batch waits stay correct (conservatively: they wait for
+// the whole batch).
+struct DeferBackend final : Backend {
+  enum : uint8_t { OP_LAUNCH, OP_RECORD, OP_WAIT, OP_COPY };
+  struct Op {
+    uint8_t kind;
+    bool coop;
+    int32_t nargs;
+    void* s;
+    void* e;
+    const void* fn;
+    dim3 g, b;
+    size_t smem;
+    uint64_t vals[16];
+    void* dst;
+    const void* src;
+    size_t n;
+    cudaMemcpyKind k;
+  };
+  struct Entry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+  };
+  Backend* in;
+  bool enabled = false;
+  void* origin = nullptr;
+  std::vector<Op> ops;
+  std::vector<uint64_t> key;
+  std::vector<Entry> cache;                 // small, linear search by hash first
+  std::vector<uint64_t> cache_hash;
+  std::vector<uint64_t> seen;               // batch hashes seen once (eager)
+  std::vector<std::pair<void*, void*>> alias;  // event -> batch event
+  std::vector<std::pair<void*, int>> bev_refs; // batch event -> alias count
+  std::vector<void*> bev_pool, join_evs;
+  void* fork_ev = nullptr;
+  uint64_t replays = 0, captures = 0, eager = 0;
+
+  explicit DeferBackend(Backend* inner) : in(inner) {}
+  ~DeferBackend() override {
+    for (auto& e : cache)
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+    for (auto& p : bev_refs) in->event_destroy(p.first);
+    for (void* e : bev_pool) in->event_destroy(e);
+    for (void* e : join_evs) in->event_destroy(e);
+    if (fork_ev) in->event_destroy(fork_ev);
+    if (origin) in->stream_destroy(origin);
+    delete in;
+  }
+  bool active() const { return enabled; }
+
+  void* resolve(void* e) const {
+    for (auto& a : alias)
+      if (a.first == e) return a.second;
+    return e;
+  }
+  void unalias(void* e) {
+    for (size_t i = 0; i < alias.size(); ++i)
+      if (alias[i].first == e) {
+        void* b = alias[i].second;
+        alias[i] = alias.back();
+        alias.pop_back();
+        for (size_t j = 0; j < bev_refs.size(); ++j)
+          if (bev_refs[j].first == b && --bev_refs[j].second == 0) {
+            bev_pool.push_back(b);
+            bev_refs[j] = bev_refs.back();
+            bev_refs.pop_back();
+            break;
+          }
+        return;
+      }
+  }
+
+  cudaError_t stream_create(void** s) override { return in->stream_create(s); }
+  cudaError_t stream_destroy(void* s) override { return in->stream_destroy(s); }
+  cudaError_t event_create(void** e) override { return in->event_create(e); }
+  cudaError_t event_create_timing(void** e) override { return in->event_create_timing(e); }
+  cudaError_t elapsed(float* ms, void* a, void* b) override { return in->elapsed(ms, a, b); }
+  cudaError_t event_destroy(void* e) override { return in->event_destroy(e); }
+  bool real() const override { return in->real(); }
+
+  cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop,
+                     int nargs) override {
+    if (!enabled || coop) {
+      if (cudaError_t e = flush()) return e;
+      return in->launch(fn, g, b, args, smem, s, coop, nargs);
+    }
+    Op o{};
+    o.kind = OP_LAUNCH;
+    o.fn = fn;
+    o.g = g;
+    o.b = b;
+    o.smem = smem;
+    o.s = s;
+    o.nargs = nargs;
+    for (int i = 0; i < nargs && i < 16; ++i) o.vals[i] = *reinterpret_cast<const uint64_t*>(args[i]);
+    ops.push_back(o);
+    return cudaSuccess;
+  }
+  cudaError_t record(void* e, void* s) override {
+    unalias(e);
+    if (!enabled) return in->record(e, s);
+    Op o{};
+    o.kind = OP_RECORD;
+    o.e = e;
+    o.s = s;
+    ops.push_back(o);
+    return cudaSuccess;
+  }
+  cudaError_t wait(void* s, void* e) override {
+    e = resolve(e);
+    if (!enabled) return in->wait(s, e);
+    Op o{};
+    o.kind = OP_WAIT;
+    o.e = e;
+    o.s = s;
+    ops.push_back(o);
+    return cudaSuccess;
+  }
+  cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, void* s) override {
+    if (!enabled) return in->copy_async(dst, src, n, k, s);
+    Op o{};
+    o.kind = OP_COPY;
+    o.dst = dst;
+    o.src = src;
+    o.n = n;
+    o.k = k;
+    o.s = s;
+    ops.push_back(o);
+    return cudaSuccess;
+  }
+  cudaError_t event_sync(void* e) override {
+    if (cudaError_t r = flush()) return r;
+    return in->event_sync(resolve(e));
+  }
+  cudaError_t stream_sync(void* s) override {
+    if (cudaError_t r = flush()) return r;
+    // work captured from stream s may be running inside a graph on `origin`
+    if (origin && (replays || captures))
+      if (cudaError_t r = in->stream_sync(origin)) return r;
+    return in->stream_sync(s);
+  }
+
+  cudaError_t issue(const Op& o, bool capturing) {
+    switch (o.kind) {
+      case OP_LAUNCH: {
+        void* argv[16];
+        for (int i = 0; i < o.nargs; ++i) argv[i] = const_cast<uint64_t*>(&o.vals[i]);
+        return in->launch(o.fn, o.g, o.b, argv, o.smem, o.s, false, o.nargs);
+      }
+      case OP_RECORD: return in->record(o.e, o.s);
+      case OP_WAIT: return capturing ? cudaSuccess : in->wait(o.s, o.e);
+      default: return in->copy_async(o.dst, o.src, o.n, o.k, o.s);
+    }
+  }
+
+  void build_key() {
+    key.clear();
+    for (const Op& o : ops) {
+      key.push_back(o.kind);
+      key.push_back((uint64_t)(uintptr_t)o.s);
+      key.push_back((uint64_t)(uintptr_t)o.e);
+      if (o.kind == OP_LAUNCH) {
+        key.push_back((uint64_t)(uintptr_t)o.fn);
+        key.push_back(((uint64_t)o.g.x << 32) | o.g.y);
+        key.push_back(((uint64_t)o.g.z << 32) | o.b.x);
+        key.push_back(((uint64_t)o.b.y << 32) | o.b.z);
+        key.push_back(o.smem);
+        key.push_back((uint64_t)o.nargs);
+        for (int i = 0; i < o.nargs; ++i) key.push_back(o.vals[i]);
+      } else if (o.kind == OP_COPY) {
+        key.push_back((uint64_t)(uintptr_t)o.dst);
+        key.push_back((uint64_t)(uintptr_t)o.src);
+        key.push_back(o.n);
+        key.push_back((uint64_t)o.k);
+      }
+    }
+  }
+  static uint64_t hash(const std::vector<uint64_t>& k) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (uint64_t v : k) {
+      h ^= v;
+      h *= 0x100000001b3ull;
+      h ^= h >> 29;
+    }
+    return h;
+  }
+
+  // Waits on events that were not recorded earlier in this batch are
+  // external dependencies: satisfied by making the origin stream wait on
+  // them before the graph (a capture may not reference outside events).
+  bool external_wait(size_t i) const {
+    for (size_t j = 0; j < i; ++j)
+      if (ops[j].kind == OP_RECORD && ops[j].e == ops[i].e) return false;
+    return true;
+  }
+
+  cudaError_t run_graph(cudaGraphExec_t exec) {
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].kind == OP_WAIT && external_wait(i))
+        if (cudaError_t e = in->wait(origin, ops[i].e)) return e;
+    if (cudaError_t e = cudaGraphLaunch(exec, (cudaStream_t)origin)) return e;
+    void* bev;
+    if (!bev_pool.empty()) {
+      bev = bev_pool.back();
+      bev_pool.pop_back();
+    } else if (cudaError_t e = in->event_create(&bev)) {
+      return e;
+    }
+    if (cudaError_t e = in->record(bev, origin)) return e;
+    int refs = 0;
+    for (const Op& o : ops)
+      if (o.kind == OP_RECORD) {
+        unalias(o.e);
+        alias.push_back({o.e, bev});
+        ++refs;
+      }
+    if (refs) bev_refs.push_back({bev, refs});
+    else bev_pool.push_back(bev);
+    return cudaSuccess;
+  }
+
+  cudaError_t capture(cudaGraphExec_t* out) {
+    std::vector<void*> streams;
+    for (const Op& o : ops)
+      if (std::find(streams.begin(), streams.end(), o.s) == streams.end()) streams.push_back(o.s);
+    while (join_evs.size() < streams.size()) {
+      void* e;
+      if (cudaError_t r = in->event_create(&e)) return r;
+      join_evs.push_back(e);
+    }
+    if (!fork_ev)
+      if (cudaError_t r = in->event_create(&fork_ev)) return r;
+    cudaStream_t org = (cudaStream_t)origin;
+    if (cudaError_t r = cudaStreamBeginCapture(org, cudaStreamCaptureModeRelaxed)) return r;
+    cudaError_t err = in->record(fork_ev, origin);
+    for (void* s : streams)
+      if (!err) err = in->wait(s, fork_ev);
+    for (size_t i = 0; i < ops.size() && !err; ++i) {
+      if (ops[i].kind == OP_WAIT) {
+        if (!external_wait(i)) err = in->wait(ops[i].s, ops[i].e);
+      } else {
+        err = issue(ops[i], true);
+      }
+    }
+    for (size_t i = 0; i < streams.size() && !err; ++i) {
+      err = in->record(join_evs[i], streams[i]);
+      if (!err) err = in->wait(origin, join_evs[i]);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t end = cudaStreamEndCapture(org, &g);
+    if (err) {
+      if (g) cudaGraphDestroy(g);
+      return err;
+    }
+    if (end) return end;
+    cudaError_t r = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    return r;
+  }
+
+  cudaError_t flush() {
+    if (ops.empty()) return cudaSuccess;
+    if (!origin)
+      if (cudaError_t e = in->stream_create(&origin)) return e;
+    build_key();
+    const uint64_t h = hash(key);
+    cudaError_t err = cudaSuccess;
+    bool done = false;
+    for (size_t i = 0; i < cache.size() && !done; ++i)
+      if (cache_hash[i] == h && cache[i].key == key) {
+        err = run_graph(cache[i].exec);
+        ++replays;
+        done = true;
+      }
+    if (!done && std::find(seen.begin(), seen.end(), h) != seen.end()) {
+      cudaGraphExec_t exec = nullptr;
+      err = capture(&exec);
+      if (!err) {
+        if (cache.size() >= 16) {
+          cudaGraphExecDestroy(cache.front().exec);
+          cache.erase(cache.begin());
+          cache_hash.erase(cache_hash.begin());
+        }
+        Entry en;
+        en.key = key;
+        en.exec = exec;
+        cache.push_back(std::move(en));
+        cache_hash.push_back(h);
+        err = run_graph(exec);
+        ++captures;
+        done = true;
+      }
+    }
+    if (!done) {  // first sighting: issue eagerly, remember the batch
+      err = cudaSuccess;
+      for (const Op& o : ops)
+        if (!err) err = issue(o, false);
+      if (seen.size() >= 64) seen.erase(seen.begin());
+      seen.push_back(h);
+      ++eager;
+    }
+    ops.clear();
+    return err;
+  }
+
+  cudaError_t launch_now(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop) {
+    if (cudaError_t e = flush()) return e;
+    return in->launch(fn, g, b, args, smem, s, coop, 0);
+  }
 };
 
 // ------------------------------------------------------------ context state
@@ -205,7 +527,7 @@ struct dagrt_graph_s {
 struct dagrt_ctx_s {
   dagrt_config cfg{};
   int device = 0;
-  Backend* be = nullptr;
+  DeferBackend* be = nullptr;  // wraps the CUDA / record backend (graph cache)
   std::string err;
   bool sticky = false;
 
@@ -345,7 +667,7 @@ dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim
     CK(c->be->record(e0, s), "cudaEventRecord profile");
   }
   if (dagrt_status st = tl_begin(c, s, &t0)) return st;
-  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop), "cudaLaunchKernel");
+  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop, k->nparams), "cudaLaunchKernel");
   if (dagrt_status st = tl_end(c, s, t0, 0, sidx, vertex, kh, 0)) return st;
   if (k->prof) {
     CK(c->be->record(e1, s), "cudaEventRecord profile");
@@ -586,17 +908,18 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
   dagrt_ctx c = new (std::nothrow) dagrt_ctx_s();
   if (!c) return DAGRT_ENOMEM;
   if (cfg) c->cfg = *cfg;
-  else c->cfg = dagrt_config{DAGRT_PARALLEL_ASYNC, 1, 0, 0, DAGRT_BACKEND_CUDA};
+  else c->cfg = dagrt_config{DAGRT_PARALLEL_ASYNC, 1, 0, 0, DAGRT_BACKEND_CUDA, 0};
   c->device = device;
   if (c->cfg.backend == DAGRT_BACKEND_RECORD) {
-    c->be = new RecordBackend();
+    c->be = new DeferBackend(new RecordBackend());
   } else {
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
       delete c;
       return DAGRT_ECUDA;
     }
-    c->be = new CudaBackend();
+    c->be = new DeferBackend(new CudaBackend());
+    c->be->enabled = c->cfg.graph_cache != 0 && c->cfg.policy == DAGRT_PARALLEL_ASYNC;
   }
   c->arrays.resize(1);
   // built-in kernels are pre-registered (handles 0..n-1)
@@ -628,6 +951,7 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
 
 dagrt_status dagrt_destroy(dagrt_ctx c) {
   if (!c) return DAGRT_OK;
+  c->be->flush();
   if (c->be->real()) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
@@ -1063,6 +1387,9 @@ dagrt_status dagrt_trace_export(dagrt_ctx c, dagrt_trace_op* ops, uint32_t* n) {
 
 dagrt_status dagrt_stats(dagrt_ctx c, void* out, size_t size) {
   if (!c || !out) return DAGRT_EINVAL;
+  c->st.graph_replays = c->be->replays;
+  c->st.graph_captures = c->be->captures;
+  c->st.eager_batches = c->be->eager;
   memcpy(out, &c->st, std::min(size, sizeof(dagrt_stats_t)));
   return DAGRT_OK;
 }
@@ -1070,6 +1397,7 @@ dagrt_status dagrt_stats(dagrt_ctx c, void* out, size_t size) {
 dagrt_status dagrt_stats_reset(dagrt_ctx c) {
   if (!c) return DAGRT_EINVAL;
   c->st = dagrt_stats_t{};
+  c->be->replays = c->be->captures = c->be->eager = 0;
   c->st.streams = c->streams.size();
   return DAGRT_OK;
 }
@@ -1095,6 +1423,12 @@ dagrt_status dagrt_profile_enable(dagrt_ctx c, dagrt_kernel kh, int32_t on) {
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
   k->prof = on != 0;
+  // per-launch timing events are not replayable: no deferral while profiling
+  bool any = false;
+  for (const KernelRec& kr : c->kernels) any = any || kr.prof;
+  if (cudaError_t e = c->be->flush()) return cuda_fail(c, e, "flush");
+  c->be->enabled = c->cfg.graph_cache && c->cfg.policy == DAGRT_PARALLEL_ASYNC && c->be->real() &&
+                   !any && !c->timeline;
   return DAGRT_OK;
 }
 
@@ -1141,6 +1475,11 @@ dagrt_status dagrt_profile_collect(dagrt_ctx c, dagrt_kernel kh, int32_t* count,
 dagrt_status dagrt_timeline_enable(dagrt_ctx c, int32_t on) {
   GUARD(c);
   c->timeline = on != 0;
+  if (cudaError_t e = c->be->flush()) return cuda_fail(c, e, "flush");
+  bool any = false;
+  for (const KernelRec& kr : c->kernels) any = any || kr.prof;
+  c->be->enabled = c->cfg.graph_cache && c->cfg.policy == DAGRT_PARALLEL_ASYNC && c->be->real() &&
+                   !any && !c->timeline;
   return DAGRT_OK;
 }
 
@@ -1177,7 +1516,7 @@ dagrt_status dagrt_launch_raw(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dag
   void* argv[kMaxArgs];
   ArrayRec* arrs[kMaxArgs];
   if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
-  CK(c->be->launch(k->fn, dim3(grid.x, grid.y, grid.z), dim3(block.x, block.y, block.z), argv, smem,
+  CK(c->be->launch_now(k->fn, dim3(grid.x, grid.y, grid.z), dim3(block.x, block.y, block.z), argv, smem,
                    stream, k->coop),
      "cudaLaunchKernel raw");
   return DAGRT_OK;

@@ -31,7 +31,7 @@ class DagrtError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("policy", C.c_int32), ("prefetch", C.c_int32), ("max_streams", C.c_int32),
-                ("record_dag", C.c_int32), ("backend", C.c_int32)]
+                ("record_dag", C.c_int32), ("backend", C.c_int32), ("graph_cache", C.c_int32)]
 
 
 class Dim3(C.Structure):
@@ -59,7 +59,8 @@ class TraceOp(C.Structure):
 
 STAT_FIELDS = ["launches", "vertices", "host_vertices", "edges", "cross_stream_waits",
                "copy_waits", "streams", "events_created", "h2d_bytes", "d2h_bytes",
-               "h2d_copies", "d2h_copies", "host_syncs", "sched_ns"]
+               "h2d_copies", "d2h_copies", "host_syncs", "sched_ns", "graph_replays",
+               "graph_captures", "eager_batches"]
 
 
 class Stats(C.Structure):
@@ -256,11 +257,11 @@ class Graph:
 
 class Context:
     def __init__(self, device=0, policy="parallel", prefetch=True, max_streams=0,
-                 record_dag=False, backend="cuda"):
+                 record_dag=False, backend="cuda", graph_cache=False):
         L = lib()
         cfg = Config(PARALLEL_ASYNC if policy == "parallel" else SERIAL_SYNC, 1 if prefetch else 0,
                      max_streams, 1 if record_dag else 0,
-                     BACKEND_CUDA if backend == "cuda" else BACKEND_RECORD)
+                     BACKEND_CUDA if backend == "cuda" else BACKEND_RECORD, 1 if graph_cache else 0)
         h = C.c_void_p()
         s = L.dagrt_create(device, C.byref(cfg), C.byref(h))
         if s:

@@ -49,7 +49,7 @@ class Hits(Program):
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
-        gs = min(self.ncta, 3 * SMS)  # persistent merge-path CTAs (3 resident per SM)
+        gs = min(self.ncta, 4 * SMS)  # persistent merge-path CTAs (4 resident per SM)
         self.it = [
             P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
             P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1

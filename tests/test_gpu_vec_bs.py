@@ -143,3 +143,38 @@ def test_graph_baseline_matches(ctx):
     g = p.graph()
     g.run()
     assert p.result() == z1  # deterministic reduction, same kernels
+
+
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+def test_graph_cache_replays_identical_results(mode):
+    """NEXT(f1): deferred submission + batch cache -> CUDA graph replay gives
+    the same results, and replays from the third identical DAG on."""
+    gctx = D.Context(device=0, graph_cache=True)
+    p = Vec(gctx, n=100_003, mode=mode)
+    p.load_inputs(4)
+    zs = []
+    for _ in range(5):
+        p.run()
+        gctx.sync()
+        zs.append(p.result())
+    st = gctx.stats()
+    assert st["graph_replays"] >= 2 and st["graph_captures"] >= 1, st
+    assert len(set(zs)) == 1
+    spec = synth.spec_vec(100_003)
+    x = synth.draw(p.seed + 4, "x", spec["x"])
+    y = synth.draw(p.seed + 4, "y", spec["y"])
+    z = ovec.vec(x, y)[2]
+    assert abs(zs[0] - z) <= 1e-3 * abs(z)
+    b = BlackScholes(gctx, n=4099, mode=mode)
+    b.load_inputs(5)
+    for _ in range(4):
+        b.run()
+    gctx.sync()
+    sp = synth.spec_bs(4099)
+    for i in range(synth.BS_NVEC):
+        ref = obs.call(synth.draw(b.seed + 5, f"s{i}", sp[f"s{i}"]))
+        out = b.t[f"c{i}"].cpu().numpy()
+        assert np.all(np.abs(out - ref) <= 1e-10 * np.abs(ref) + 1e-12)
+        if mode == "stream":
+            assert np.array_equal(b.mirror[f"c{i}"].numpy(), out)
+    gctx.close()
