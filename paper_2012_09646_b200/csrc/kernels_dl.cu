@@ -15,7 +15,7 @@ namespace dagrt {
 // column pairs (no integer division).  Inputs: per tap row one float4
 // (columns 4j..4j+3) plus column 4j-1 from the neighbouring lane (shuffle);
 // outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
-__global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
+__global__ void __launch_bounds__(256, 6) k_conv1(const float* __restrict__ x,
                                                const float* __restrict__ w,
                                                float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;

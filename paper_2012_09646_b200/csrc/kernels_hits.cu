@@ -121,8 +121,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, long long N) {
   __shared__ int s_bnd[kSpmvChunk + 1];
-  __shared__ float s_val[kSpmvTile];
-  __shared__ int s_rend[kSpmvTile + 1];
+  // double-buffered staging (tile parity): the next tile's writes never race
+  // with the previous tile's reads, so no barrier is needed before staging
+  __shared__ float s_val_buf[2][kSpmvTile];
+  __shared__ int s_rend_buf[2][kSpmvTile + 1];  // row ends relative to j0
   __shared__ float s_wsum[kSpmvThreads / 32];
   __shared__ int s_wflag[kSpmvThreads / 32];
   __shared__ int s_first_emitter;
@@ -177,7 +179,9 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
         const int k = t + u * kSpmvThreads;
         xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
       }
-      __syncthreads();  // (A) the previous tile's readers of shared memory are done
+      float* s_val = s_val_buf[c & 1];
+      int* s_rend = s_rend_buf[c & 1];
+      const int j0i = (int)j0;
 #pragma unroll
       for (int u = 0; u < kSpmvItems; ++u) {
         const int k = t + u * kSpmvThreads;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
 #pragma unroll
       for (int u = 0; u <= kSpmvItems; ++u) {
         const int k = t + u * kSpmvThreads;
-        if (k < nre) s_rend[k] = re[u];
+        if (k < nre) s_rend[k] = re[u] - j0i;
       }
       if (t == 0) s_first_emitter = kSpmvThreads;
       __syncthreads();  // (B)
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
       int lo = max(0, dl - nn), hi = min(dl, nr);
       while (lo < hi) {
         const int p = (lo + hi) >> 1;
-        if ((long long)s_rend[p] - j0 <= dl - p - 1) lo = p + 1;
+        if (s_rend[p] <= dl - p - 1) lo = p + 1;
         else hi = p;
       }
       int ri = lo, nj = dl - lo;
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
       bool emitted = false;
       long long first_row = -1;
       for (int it = dl; it < de; ++it) {
-        const bool row_end = (ri < nr) && ((long long)s_rend[ri] - j0 <= nj);
+        const bool row_end = (ri < nr) && (s_rend[ri] <= nj);
         if (row_end) {
           if (!emitted) {
             emitted = true;
@@ -260,8 +264,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
         if (fe < kSpmvThreads && head_x)
           spmv_deposit(ws, y, i0, cta_of_diag(i0 + rp0), me, me, s_head_val, true);
         if (c == te0 - 1 && i1 < N) {
-          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] : (long long)rp0;  // row_ptr[i1]
-          const long long rend = (long long)s_rend[nr];                             // row_ptr[i1+1]
+          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] + j0 : (long long)rp0;  // row_ptr[i1]
+          const long long rend = (long long)s_rend[nr] + j0;                            // row_ptr[i1+1]
           const long long as = cta_of_diag(i1 + rs), ae = cta_of_diag(i1 + rend);
           if (ae > me && as <= me) spmv_deposit(ws, y, i1, as, ae, me, new_carry, false);
         }

@@ -173,10 +173,12 @@ __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsT
   return fma(s, c1, -C.kexp * c2);
 }
 
-// K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores,
-// two options per thread per iteration.
-__global__ void __launch_bounds__(256, 5) k_bs(const double* __restrict__ s, double* __restrict__ c,
-                                            long long n, double r, double v, double t, double k) {
+// K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores.
+// PAIRS double2 per thread per iteration (independent chains for the FP64
+// pipe to interleave); the next group's loads are issued before pricing.
+template <int PAIRS>
+__device__ __forceinline__ void bs_body(const double* __restrict__ s, double* __restrict__ c,
+                                        long long n, double r, double v, double t, double k) {
   __shared__ BsTables T;
   bs_tables_init(T);
   BsConst C;
@@ -194,25 +196,69 @@ __global__ void __launch_bounds__(256, 5) k_bs(const double* __restrict__ s, dou
     const long long n2 = n >> 1;
     const double2* s2 = reinterpret_cast<const double2*>(s);
     double2* c2 = reinterpret_cast<double2*>(c);
-    // software pipelined: the next pair is in flight while this one is priced
-    double2 x = tid < n2 ? ldg_stream(s2 + tid) : make_double2(1.0, 1.0);
-    for (long long i = tid; i < n2; i += nth) {
-      const double2 nx = i + nth < n2 ? ldg_stream(s2 + i + nth) : x;
-      double2 y;
-      y.x = bs_price(x.x, C, T);
-      y.y = bs_price(x.y, C, T);
-      c2[i] = y;
-      x = nx;
+    double2 x[PAIRS];
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+      const long long i = tid + q * nth;
+      x[q] = i < n2 ? ldg_stream(s2 + i) : make_double2(1.0, 1.0);
+    }
+    for (long long i0 = tid; i0 < n2; i0 += PAIRS * nth) {
+      double2 nx[PAIRS];
+#pragma unroll
+      for (int q = 0; q < PAIRS; ++q) {
+        const long long i = i0 + (PAIRS + q) * nth;
+        nx[q] = i < n2 ? ldg_stream(s2 + i) : x[q];
+      }
+#pragma unroll
+      for (int q = 0; q < PAIRS; ++q) {
+        const long long i = i0 + q * nth;
+        double2 y;
+        y.x = bs_price(x[q].x, C, T);
+        y.y = bs_price(x[q].y, C, T);
+        if (i < n2) c2[i] = y;
+        x[q] = nx[q];
+      }
     }
     done = n2 << 1;
   }
   for (long long i = done + tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
 }
 
+__global__ void __launch_bounds__(256, 5) k_bs(const double* __restrict__ s, double* __restrict__ c,
+                                            long long n, double r, double v, double t, double k) {
+  bs_body<1>(s, c, n, r, v, t, k);
+}
+// tuning variants (same results; bench with tools/bs_variants.py)
+__global__ void __launch_bounds__(256, 3) k_bs_p2b3(const double* __restrict__ s, double* __restrict__ c,
+                                                 long long n, double r, double v, double t, double k) {
+  bs_body<2>(s, c, n, r, v, t, k);
+}
+__global__ void __launch_bounds__(256, 4) k_bs_p1b4(const double* __restrict__ s, double* __restrict__ c,
+                                                 long long n, double r, double v, double t, double k) {
+  bs_body<1>(s, c, n, r, v, t, k);
+}
+__global__ void __launch_bounds__(256, 4) k_bs_p2b4(const double* __restrict__ s, double* __restrict__ c,
+                                                 long long n, double r, double v, double t, double k) {
+  bs_body<2>(s, c, n, r, v, t, k);
+}
+__global__ void __launch_bounds__(256, 6) k_bs_p1b6(const double* __restrict__ s, double* __restrict__ c,
+                                                 long long n, double r, double v, double t, double k) {
+  bs_body<1>(s, c, n, r, v, t, k);
+}
+__global__ void __launch_bounds__(256, 2) k_bs_p4b2(const double* __restrict__ s, double* __restrict__ c,
+                                                 long long n, double r, double v, double t, double k) {
+  bs_body<4>(s, c, n, r, v, t, k);
+}
+
 static const Builtin kVecBs[] = {
     {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE},
     {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"bs", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p2b3", (const void*)k_bs_p2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p1b4", (const void*)k_bs_p1b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p2b4", (const void*)k_bs_p2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p1b6", (const void*)k_bs_p1b6, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p4b2", (const void*)k_bs_p4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
 };
 DAGRT_REGISTER_BUILTINS(kVecBs);
 

@@ -258,7 +258,12 @@ struct DeferBackend final : Backend {
     return cudaSuccess;
   }
   cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, void* s) override {
-    if (!enabled) return in->copy_async(dst, src, n, k, s);
+    // D2H copies belong to host accesses, which synchronise right after:
+    // a one-node graph would only add launch latency, so issue them directly
+    if (!enabled || k == cudaMemcpyDeviceToHost) {
+      if (cudaError_t e = flush()) return e;
+      return in->copy_async(dst, src, n, k, s);
+    }
     Op o{};
     o.kind = OP_COPY;
     o.dst = dst;

@@ -1,0 +1,47 @@
+"""Time the B&S kernel tuning variants (same math) on one 10M-option vector."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    import synth
+    import synth.gpu as sg
+    from paper_2012_09646_b200 import dagrt as D
+    n = 10_000_000
+    ctx = D.Context(device=0)
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    c = torch.empty(n, dtype=torch.float64, device="cuda")
+    sg.fill_tensor(s, 20120964, "s0", synth.spec_bs(n)["s0"])
+    S = ctx.register_tensor("s", s)
+    Cc = ctx.register_tensor("c", c)
+    st = torch.cuda.Stream()
+    out = {}
+    ref = None
+    for name, waves in (("bs", 5), ("bs_p1b4", 4), ("bs_p1b6", 6), ("bs_p2b3", 3), ("bs_p2b4", 4),
+                        ("bs_p4b2", 2)):
+        for grid_mult in (1, 2, 4):
+            grid = 148 * waves * grid_mult
+            L = ctx.prepare(name, grid, 256, [S, Cc, n, 0.08, 0.30, 1.0, 60.0])
+            for _ in range(3):
+                L.raw(st.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(st):
+                e0.record()
+                for _ in range(20):
+                    L.raw(st.cuda_stream)
+                e1.record()
+            e1.synchronize()
+            us = e0.elapsed_time(e1) / 20 * 1e3
+            if ref is None:
+                ref = c.clone()
+            same = bool(torch.equal(ref, c))
+            out[f"{name}_g{grid}"] = {"us": us, "GBps": 16 * n / us / 1e3, "bitwise_same": same}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
