@@ -54,6 +54,10 @@ __device__ __forceinline__ int ldg_hint(const int* p, uint64_t pol) {
   return r;
 }
 
+__device__ __forceinline__ void stg_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

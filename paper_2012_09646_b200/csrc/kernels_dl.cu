@@ -15,7 +15,7 @@ namespace dagrt {
 // column pairs (no integer division).  Inputs: per tap row one float4
 // (columns 4j..4j+3) plus column 4j-1 from the neighbouring lane (shuffle);
 // outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
-__global__ void __launch_bounds__(256, 6) k_conv1(const float* __restrict__ x,
+__global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
                                                const float* __restrict__ w,
                                                float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
@@ -29,32 +29,46 @@ __global__ void __launch_bounds__(256, 6) k_conv1(const float* __restrict__ x,
   const bool live_j = j < pairs;
   const bool vec = ((W & 3) == 0) && aligned16(x);
   const int c0 = 4 * j;
+  // the three input rows of output row p (one float4 each); the next row's
+  // loads are issued before this row is computed (software pipelining)
+  auto load_rows = [&](int p, float4 (&q)[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int y = 2 * p + a - 1;
+      q[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live_j && y >= 0 && y < H) {
+        const float* row = x + (size_t)y * W;
+        if (vec && c0 + 3 < W) {
+          q[a] = ldg_stream(reinterpret_cast<const float4*>(row + c0));
+        } else {
+          if (c0 + 0 < W) q[a].x = row[c0 + 0];
+          if (c0 + 1 < W) q[a].y = row[c0 + 1];
+          if (c0 + 2 < W) q[a].z = row[c0 + 2];
+          if (c0 + 3 < W) q[a].w = row[c0 + 3];
+        }
+      }
+    }
+  };
+  float4 q[3];
+  if ((int)blockIdx.y < H1) load_rows(blockIdx.y, q);
   for (int p = blockIdx.y; p < H1; p += gridDim.y) {  // uniform per block
+    float4 qn[3];
+    if (p + (int)gridDim.y < H1) load_rows(p + gridDim.y, qn);
     float v[3][5];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int y = 2 * p + a - 1;
       const bool rowok = live_j && y >= 0 && y < H;
-      const float* row = x + (size_t)(rowok ? y : 0) * W;
-      float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rowok) {
-        if (vec && c0 + 3 < W) {
-          q4 = ldg_stream(reinterpret_cast<const float4*>(row + c0));
-        } else {
-          if (c0 + 0 < W) q4.x = row[c0 + 0];
-          if (c0 + 1 < W) q4.y = row[c0 + 1];
-          if (c0 + 2 < W) q4.z = row[c0 + 2];
-          if (c0 + 3 < W) q4.w = row[c0 + 3];
-        }
-      }
-      float left = __shfl_up_sync(0xffffffffu, q4.w, 1);
-      if ((threadIdx.x & 31) == 0 || j == 0) left = (rowok && c0 > 0) ? row[c0 - 1] : 0.f;
+      float left = __shfl_up_sync(0xffffffffu, q[a].w, 1);
+      if ((threadIdx.x & 31) == 0 || j == 0) left = (rowok && c0 > 0) ? x[(size_t)y * W + c0 - 1] : 0.f;
       v[a][0] = left;
-      v[a][1] = q4.x;
-      v[a][2] = q4.y;
-      v[a][3] = q4.z;
-      v[a][4] = q4.w;
+      v[a][1] = q[a].x;
+      v[a][2] = q[a].y;
+      v[a][3] = q[a].z;
+      v[a][4] = q[a].w;
     }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) q[a] = qn[a];
     if (!live_j) continue;
     float o[2][8];
 #pragma unroll

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
             first_row = i0 + ri;
             first_val = sum;
           } else {
-            y[i0 + ri] = sum;
+            stg_hint(y + i0 + ri, sum, pol_stream);
           }
           sum = 0.f;
           ++ri;
@@ -251,9 +251,9 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
         if (t == fe && first_row == i0) {
           v += carry_in;
           if (head_x) s_head_val = v;
-          else y[i0] = v;
+          else stg_hint(y + i0, v, pol_stream);
         } else {
-          y[first_row] = v;
+          stg_hint(y + first_row, v, pol_stream);
         }
       }
       if (t == kSpmvThreads - 1) s_carry = s_incl;

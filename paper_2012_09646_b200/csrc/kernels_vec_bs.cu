@@ -224,7 +224,8 @@ __device__ __forceinline__ void bs_body(const double* __restrict__ s, double* __
   for (long long i = done + tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
 }
 
-__global__ void __launch_bounds__(256, 5) k_bs(const double* __restrict__ s, double* __restrict__ c,
+// default variant: 1 pair per iteration, 4 CTAs/SM (fastest in tools/bs_variants.py)
+__global__ void __launch_bounds__(256, 4) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
   bs_body<1>(s, c, n, r, v, t, k);
 }

@@ -299,12 +299,26 @@ struct DeferBackend final : Backend {
     }
   }
 
+  // Batch key.  Event handles are canonicalised to their first-appearance
+  // index: pooled events come back in varying order between identical runs,
+  // and a captured graph does not depend on them (recorded-and-waited events
+  // become graph edges; external waits and host-visible aliases are taken
+  // from the current batch when it is replayed).
+  std::vector<void*> key_events;
   void build_key() {
     key.clear();
+    key_events.clear();
     for (const Op& o : ops) {
       key.push_back(o.kind);
       key.push_back((uint64_t)(uintptr_t)o.s);
-      key.push_back((uint64_t)(uintptr_t)o.e);
+      uint64_t ev = 0;
+      if (o.e) {
+        size_t i = 0;
+        while (i < key_events.size() && key_events[i] != o.e) ++i;
+        if (i == key_events.size()) key_events.push_back(o.e);
+        ev = i + 1;
+      }
+      key.push_back(ev);
       if (o.kind == OP_LAUNCH) {
         key.push_back((uint64_t)(uintptr_t)o.fn);
         key.push_back(((uint64_t)o.g.x << 32) | o.g.y);
