@@ -115,35 +115,16 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
 // slots indexed by CTA), so at most two deposits per CTA leave the per-tile
 // critical path clean.
 constexpr int kSpmvChunk = 256;
-// dynamic shared memory of k_spmv (see the staging buffers below)
-constexpr int kSpmvSmem = 4 * ((kSpmvChunk + 1) + 2 * kSpmvTile + 2 * kSpmvTile + 3 * (kSpmvTile + 1) + 3) + 64;
 
-// cp.async (LDGSTS) 4-byte copies with an L2 cache policy: staging goes
-// global -> shared without registers, so a tile's loads can be in flight
-// while the previous tile is processed.
-__device__ __forceinline__ void cp4(void* sdst, const void* gsrc, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(sdst)),
-               "l"(gsrc), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-__global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict__ row_ptr,
                                                        const int* __restrict__ col,
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, long long N) {
-  // Three-stage asynchronous staging pipeline (cp.async), per tile t:
-  //   A(t): column indices and row ends of t      -> s_col[t%2], s_rend[t%3]
-  //   B(t): gathers x[col] of t (reads s_col)     -> s_val[t%2]
-  // While tile c is processed, B(c+1) and A(c+2) are in flight.
-  extern __shared__ __align__(16) int dsm[];
-  int* s_bnd = dsm;                                                   // [kSpmvChunk + 1]
-  int (*s_col_buf)[kSpmvTile] = reinterpret_cast<int (*)[kSpmvTile]>(s_bnd + kSpmvChunk + 1);
-  float (*s_val_buf)[kSpmvTile] = reinterpret_cast<float (*)[kSpmvTile]>(s_col_buf + 2);
-  int (*s_rend_buf)[kSpmvTile + 1] = reinterpret_cast<int (*)[kSpmvTile + 1]>(s_val_buf + 2);
-  int* s_rp0_buf = reinterpret_cast<int*>(s_rend_buf + 3);             // [3]
+  __shared__ int s_bnd[kSpmvChunk + 1];
+  // double-buffered staging (tile parity): the next tile's writes never race
+  // with the previous tile's reads, so no barrier is needed before staging
+  __shared__ float s_val_buf[2][kSpmvTile];
+  __shared__ int s_rend_buf[2][kSpmvTile + 1];  // row ends relative to j0
   __shared__ float s_wsum[kSpmvThreads / 32];
   __shared__ int s_wflag[kSpmvThreads / 32];
   __shared__ int s_first_emitter;
@@ -172,60 +153,45 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict_
       if (lane == 0) s_bnd[b] = (int)i;
     }
     __syncthreads();
-    auto stage_A = [&](long long tt) {
-      const long long d0 = tt * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
-      const long long i0 = s_bnd[tt - tb], i1 = s_bnd[tt - tb + 1];
-      const long long j0 = d0 - i0;
-      const int nn = (int)(d1 - i1 - j0);
-      const int nre = (int)(min(i1, N - 1) - i0 + 1);
-      int* sc = s_col_buf[tt & 1];
-      int* sr = s_rend_buf[tt % 3];
-#pragma unroll
-      for (int u = 0; u < kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        if (k < nn) cp4(sc + k, col + j0 + k, pol_stream);
-      }
-#pragma unroll
-      for (int u = 0; u <= kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        if (k < nre) cp4(sr + k, row_ptr + i0 + k + 1, pol_stream);
-      }
-      if (t == 0) cp4(&s_rp0_buf[tt % 3], row_ptr + i0, pol_stream);
-    };
-    auto stage_B = [&](long long tt) {
-      const long long d0 = tt * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
-      const long long i0 = s_bnd[tt - tb], i1 = s_bnd[tt - tb + 1];
-      const int nn = (int)(d1 - i1 - (d0 - i0));
-      const int* sc = s_col_buf[tt & 1];
-      float* sv = s_val_buf[tt & 1];
-#pragma unroll
-      for (int u = 0; u < kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        if (k < nn) cp4(sv + k, x + sc[k], pol_keep);
-      }
-    };
-    // prologue: A(tb), A(tb+1) -> B(tb)
-    stage_A(tb);
-    if (tb + 1 < te) stage_A(tb + 1);
-    cp_commit();
-    cp_wait_all();
-    __syncthreads();
-    stage_B(tb);
-    cp_commit();
     for (long long c = tb; c < te; ++c) {
-      cp_wait_all();     // B(c) (and A(c+1)) landed for this thread's copies
-      __syncthreads();   // ... and for everyone's
-      if (c + 1 < te) stage_B(c + 1);
-      if (c + 2 < te) stage_A(c + 2);
-      cp_commit();
       const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
       const long long i0 = s_bnd[c - tb], i1 = s_bnd[c - tb + 1];
       const long long j0 = d0 - i0, j1 = d1 - i1;
       const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
-      const float* s_val = s_val_buf[c & 1];
-      const int* s_rend = s_rend_buf[c % 3];
-      const int rp0 = s_rp0_buf[c % 3];
+      const int nre = (int)(min(i1, N - 1) - i0 + 1);
+      // ---- stage: column indices, then gathers (8 loads in flight each), row ends
+      int ci[kSpmvItems];
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        ci[u] = k < nn ? ldg_hint(col + j0 + k, pol_stream) : 0;
+      }
+      int re[kSpmvItems + 1];
+#pragma unroll
+      for (int u = 0; u <= kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        re[u] = k < nre ? ldg_hint(row_ptr + i0 + k + 1, pol_stream) : 0;
+      }
+      const int rp0 = __ldg(row_ptr + i0);
+      float xv[kSpmvItems];
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
+      }
+      float* s_val = s_val_buf[c & 1];
+      int* s_rend = s_rend_buf[c & 1];
       const int j0i = (int)j0;
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        if (k < nn) s_val[k] = xv[u];
+      }
+#pragma unroll
+      for (int u = 0; u <= kSpmvItems; ++u) {
+        const int k = t + u * kSpmvThreads;
+        if (k < nre) s_rend[k] = re[u] - j0i;
+      }
       if (t == 0) s_first_emitter = kSpmvThreads;
       __syncthreads();  // (B)
       // ---- thread-local merge-path search and sequential consumption
@@ -233,7 +199,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict_
       int lo = max(0, dl - nn), hi = min(dl, nr);
       while (lo < hi) {
         const int p = (lo + hi) >> 1;
-        if (s_rend[p] - j0i <= dl - p - 1) lo = p + 1;
+        if (s_rend[p] <= dl - p - 1) lo = p + 1;
         else hi = p;
       }
       int ri = lo, nj = dl - lo;
@@ -242,7 +208,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict_
       bool emitted = false;
       long long first_row = -1;
       for (int it = dl; it < de; ++it) {
-        const bool row_end = (ri < nr) && (s_rend[ri] - j0i <= nj);
+        const bool row_end = (ri < nr) && (s_rend[ri] <= nj);
         if (row_end) {
           if (!emitted) {
             emitted = true;
@@ -298,8 +264,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv(const int* __restrict_
         if (fe < kSpmvThreads && head_x)
           spmv_deposit(ws, y, i0, cta_of_diag(i0 + rp0), me, me, s_head_val, true);
         if (c == te0 - 1 && i1 < N) {
-          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] : (long long)rp0;  // row_ptr[i1]
-          const long long rend = (long long)s_rend[nr];                             // row_ptr[i1+1]
+          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] + j0 : (long long)rp0;  // row_ptr[i1]
+          const long long rend = (long long)s_rend[nr] + j0;                            // row_ptr[i1+1]
           const long long as = cta_of_diag(i1 + rs), ae = cta_of_diag(i1 + rend);
           if (ae > me && as <= me) spmv_deposit(ws, y, i1, as, ae, me, new_carry, false);
         }
@@ -355,8 +321,7 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 }
 
 static const Builtin kHits[] = {
-    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE,
-     kSpmvSmem},
+    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE},
     {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE},
 };

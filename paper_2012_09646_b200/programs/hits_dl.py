@@ -12,7 +12,6 @@ CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64  # csrc/kernels_conv_tc.cu kTcSm
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 256 * 8      # merge items per CTA (csrc/kernels_hits.cu)
-SPMV_SMEM = 4 * ((256 + 1) + 2 * SPMV_TILE + 2 * SPMV_TILE + 3 * (SPMV_TILE + 1) + 3) + 64  # kSpmvSmem
 
 
 def spmv_out_bytes(n, e):
@@ -50,10 +49,10 @@ class Hits(Program):
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
-        gs = min(self.ncta, 3 * SMS)  # persistent merge-path CTAs (3 resident per SM)
+        gs = min(self.ncta, 4 * SMS)  # persistent merge-path CTAs (4 resident per SM)
         self.it = [
-            P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n], smem=SPMV_SMEM),  # a2 = A^T h1
-            P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n], smem=SPMV_SMEM),    # h2 = A a1
+            P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
+            P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
             P("l2norm", gr, 256, [a["a2"], a["an"], n]),
             P("l2norm", gr, 256, [a["h2"], a["hn"], n]),
             P("divide", ge, 256, [a["a2"], a["an"], a["a1"], n]),
