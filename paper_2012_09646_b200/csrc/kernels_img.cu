@@ -98,42 +98,51 @@ __device__ __forceinline__ void stencil_body(const float* __restrict__ src, floa
 
   // stage input row y (zero outside the image) into buffer b; smem index
   // j holds column x0 - R + j
-  auto stage = [&](int y, int b) {
-    float* r = row[b];
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  // Row staging is software-pipelined: the global loads of row y+1 (the
+  // thread's 4 columns + halo) are issued before row y is filtered.
+  struct RowRegs {
+    float4 v;
+    float h;  // halo element (threads t < R and t >= T-R)
+  };
+  auto load_row = [&](int y, RowRegs& rr) {
+    rr.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    rr.h = 0.f;
     if (y >= 0 && y < H) {
       const float* s = src + (size_t)y * W;
       if (vec && cx + 3 < W) {
-        v = ldg_stream(reinterpret_cast<const float4*>(s + cx));
+        rr.v = ldg_stream(reinterpret_cast<const float4*>(s + cx));
       } else {
-        if (cx + 0 < W) v.x = s[cx + 0];
-        if (cx + 1 < W) v.y = s[cx + 1];
-        if (cx + 2 < W) v.z = s[cx + 2];
-        if (cx + 3 < W) v.w = s[cx + 3];
+        if (cx + 0 < W) rr.v.x = s[cx + 0];
+        if (cx + 1 < W) rr.v.y = s[cx + 1];
+        if (cx + 2 < W) rr.v.z = s[cx + 2];
+        if (cx + 3 < W) rr.v.w = s[cx + 3];
       }
-      if (t < R) {  // left halo
-        int xl = x0 - R + t;
-        r[t] = (xl >= 0) ? s[xl] : 0.f;
-      } else if (t >= kImgThreads - R) {  // right halo
-        int j = t - (kImgThreads - R);
-        int xr = x0 + kImgCols + j;
-        r[R + kImgCols + j] = (xr < W) ? s[xr] : 0.f;
+      if (t < R) {
+        const int xl = x0 - R + t;
+        rr.h = (xl >= 0) ? s[xl] : 0.f;
+      } else if (t >= kImgThreads - R) {
+        const int xr = x0 + kImgCols + (t - (kImgThreads - R));
+        rr.h = (xr < W) ? s[xr] : 0.f;
       }
-    } else if (t < R) {
-      r[t] = 0.f;
-    } else if (t >= kImgThreads - R) {
-      r[R + kImgCols + (t - (kImgThreads - R))] = 0.f;
     }
-    r[R + 4 * t + 0] = v.x;
-    r[R + 4 * t + 1] = v.y;
-    r[R + 4 * t + 2] = v.z;
-    r[R + 4 * t + 3] = v.w;
+  };
+  auto store_row = [&](const RowRegs& rr, int b) {
+    float* r = row[b];
+    if (t < R) r[t] = rr.h;
+    else if (t >= kImgThreads - R) r[R + kImgCols + (t - (kImgThreads - R))] = rr.h;
+    r[R + 4 * t + 0] = rr.v.x;
+    r[R + 4 * t + 1] = rr.v.y;
+    r[R + 4 * t + 2] = rr.v.z;
+    r[R + 4 * t + 3] = rr.v.w;
   };
 
   // prologue: rows y0-R .. y0+R-1 fill ring slots 1..D-1
   int b = 0;
+  RowRegs cur;
+  load_row(y0 - R, cur);
   for (int y = y0 - R; y < y1 + R; ++y, b ^= 1) {
-    stage(y, b);
+    store_row(cur, b);
+    if (y + 1 < y1 + R) load_row(y + 1, cur);
     __syncthreads();
     float win[4 + 2 * R];
 #pragma unroll

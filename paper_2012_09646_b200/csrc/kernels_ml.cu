@@ -64,7 +64,19 @@ __global__ void __launch_bounds__(512) k_norm(const int* __restrict__ X, float* 
   if (active) {
     if (vec) {
       const int4* X4 = reinterpret_cast<const int4*>(X);
-      for (long long r = r0 + rl; r < r1; r += RL) {
+      long long r = r0 + rl;
+      for (; r + 3 * RL < r1; r += 4 * RL) {  // 4 independent 128-bit loads in flight
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ldg_stream(X4 + (r + u * RL) * G + g);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s[0] += v[u].x; s[1] += v[u].y; s[2] += v[u].z; s[3] += v[u].w;
+          q[0] += v[u].x * v[u].x; q[1] += v[u].y * v[u].y;
+          q[2] += v[u].z * v[u].z; q[3] += v[u].w * v[u].w;
+        }
+      }
+      for (; r < r1; r += RL) {
         int4 v = ldg_stream(X4 + r * G + g);
         s[0] += v.x; s[1] += v.y; s[2] += v.z; s[3] += v.w;
         q[0] += v.x * v.x; q[1] += v.y * v.y; q[2] += v.z * v.z; q[3] += v.w * v.w;
@@ -130,7 +142,22 @@ __global__ void __launch_bounds__(512) k_norm(const int* __restrict__ X, float* 
       }
       const int4* X4 = reinterpret_cast<const int4*>(X);
       float4* Z4 = reinterpret_cast<float4*>(Z);
-      for (long long r = r0 + rl; r < r1; r += RL) {
+      long long r = r0 + rl;
+      for (; r + 3 * RL < r1; r += 4 * RL) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ldg_stream(X4 + (r + u * RL) * G + g);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float4 z;
+          z.x = ((float)v[u].x - mu[0]) * is[0];
+          z.y = ((float)v[u].y - mu[1]) * is[1];
+          z.z = ((float)v[u].z - mu[2]) * is[2];
+          z.w = ((float)v[u].w - mu[3]) * is[3];
+          Z4[(r + u * RL) * G + g] = z;
+        }
+      }
+      for (; r < r1; r += RL) {
         int4 v = ldg_stream(X4 + r * G + g);
         float4 z;
         z.x = ((float)v.x - mu[0]) * is[0];
