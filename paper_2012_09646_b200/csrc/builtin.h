@@ -13,9 +13,7 @@ struct Builtin {
   const void* fn;
   const char* signature;
   int32_t flags;
-  int32_t smem_max;     // > 0: opt in to this much dynamic shared memory (bytes)
-  int32_t persist_arg;  // k > 0: keep pointer argument k-1 resident in L2 (persisting
-                        // access-policy window over the array) while the kernel runs
+  int32_t smem_max;  // > 0: opt in to this much dynamic shared memory (bytes)
 };
 
 int register_builtins(const Builtin* table, int n);  // returns n

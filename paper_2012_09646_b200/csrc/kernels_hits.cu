@@ -321,8 +321,7 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 }
 
 static const Builtin kHits[] = {
-    // the gathered vector x (argument 3) is kept resident in L2 while the SpMV runs
-    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, 3},
+    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE},
     {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE},
 };

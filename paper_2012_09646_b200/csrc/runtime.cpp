@@ -63,8 +63,6 @@ struct Backend {
   virtual cudaError_t event_destroy(void* e) = 0;
   virtual cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
                              bool coop, int nargs) = 0;
-  // L2 residency hint for the next launch (persisting access-policy window)
-  virtual void hint_persist(const void*, size_t) {}
   virtual cudaError_t record(void* e, void* s) = 0;
   virtual cudaError_t wait(void* s, void* e) = 0;
   virtual cudaError_t event_sync(void* e) = 0;
@@ -89,36 +87,9 @@ struct CudaBackend final : Backend {
     return cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b);
   }
   cudaError_t event_destroy(void* e) override { return cudaEventDestroy((cudaEvent_t)e); }
-  const void* persist_p = nullptr;
-  size_t persist_n = 0;
-  size_t persist_max = 0;  // set at context creation (device persisting-L2 limit)
-  void hint_persist(const void* p, size_t n) override {
-    persist_p = p;
-    persist_n = n;
-  }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
                      bool coop, int) override {
     if (coop) return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
-    if (persist_p && persist_max) {
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = g;
-      cfg.blockDim = b;
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = (cudaStream_t)s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(persist_p);
-      at[0].val.accessPolicyWindow.num_bytes = persist_n;
-      at[0].val.accessPolicyWindow.hitRatio =
-          persist_n > persist_max ? (float)persist_max / (float)persist_n : 1.0f;
-      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      persist_p = nullptr;
-      return cudaLaunchKernelExC(&cfg, fn, args);
-    }
-    persist_p = nullptr;
     return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
   }
   cudaError_t record(void* e, void* s) override {
@@ -186,8 +157,6 @@ struct DeferBackend final : Backend {
     const void* src;
     size_t n;
     cudaMemcpyKind k;
-    const void* pp;  // persisting-L2 hint of a launch
-    size_t pn;
   };
   struct Entry {
     std::vector<uint64_t> key;
@@ -250,24 +219,13 @@ struct DeferBackend final : Backend {
   cudaError_t event_destroy(void* e) override { return in->event_destroy(e); }
   bool real() const override { return in->real(); }
 
-  const void* hint_p = nullptr;
-  size_t hint_n = 0;
-  void hint_persist(const void* p, size_t n) override {
-    hint_p = p;
-    hint_n = n;
-  }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop,
                      int nargs) override {
     if (!enabled || coop) {
       if (cudaError_t e = flush()) return e;
-      if (hint_p) in->hint_persist(hint_p, hint_n);
-      hint_p = nullptr;
       return in->launch(fn, g, b, args, smem, s, coop, nargs);
     }
     Op o{};
-    o.pp = hint_p;
-    o.pn = hint_n;
-    hint_p = nullptr;
     o.kind = OP_LAUNCH;
     o.fn = fn;
     o.g = g;
@@ -333,7 +291,6 @@ struct DeferBackend final : Backend {
       case OP_LAUNCH: {
         void* argv[16];
         for (int i = 0; i < o.nargs; ++i) argv[i] = const_cast<uint64_t*>(&o.vals[i]);
-        if (o.pp) in->hint_persist(o.pp, o.pn);
         return in->launch(o.fn, o.g, o.b, argv, o.smem, o.s, false, o.nargs);
       }
       case OP_RECORD: return in->record(o.e, o.s);
@@ -368,8 +325,6 @@ struct DeferBackend final : Backend {
         key.push_back(((uint64_t)o.g.z << 32) | o.b.x);
         key.push_back(((uint64_t)o.b.y << 32) | o.b.z);
         key.push_back(o.smem);
-        key.push_back((uint64_t)(uintptr_t)o.pp);
-        key.push_back(o.pn);
         key.push_back((uint64_t)o.nargs);
         for (int i = 0; i < o.nargs; ++i) key.push_back(o.vals[i]);
       } else if (o.kind == OP_COPY) {
@@ -528,7 +483,6 @@ struct KernelRec {
   uint8_t kind[kMaxArgs];
   bool coop;
   bool prof = false;
-  int32_t persist_arg = -1;  // pointer argument kept resident in L2 (-1: none)
 };
 
 struct ProfRec {
@@ -983,15 +937,7 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
       delete c;
       return DAGRT_ECUDA;
     }
-    auto* cb = new CudaBackend();
-    // L2 residency: enable the device's persisting-L2 carve-out (used by
-    // kernels that declare a gather target, e.g. the SpMV vector)
-    int maxp = 0;
-    if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
-        maxp > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess)
-      cb->persist_max = (size_t)maxp;
-    cudaGetLastError();
-    c->be = new DeferBackend(cb);
+    c->be = new DeferBackend(new CudaBackend());
     c->be->enabled = c->cfg.graph_cache != 0 && c->cfg.policy == DAGRT_PARALLEL_ASYNC;
   }
   c->arrays.resize(1);
@@ -1002,7 +948,6 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
     k.name = b->name;
     k.fn = b->fn;
     k.coop = (b->flags & KF_COOPERATIVE) != 0;
-    k.persist_arg = b->persist_arg - 1;
     if (b->smem_max > 0 && c->be->real() && b->fn)
       cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
     if (parse_signature(b->signature, &k) != DAGRT_OK) {
@@ -1221,8 +1166,6 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       }
     }
     trace_op(c, DAGRT_OP_LAUNCH, -3, vid, kh, 0);
-    if (k->persist_arg >= 0 && k->persist_arg < k->nparams && arrs[k->persist_arg])
-      c->be->hint_persist(arrs[k->persist_arg]->dev, arrs[k->persist_arg]->bytes);
     if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, -3, vid)) return st_;
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
     c->st.host_syncs++;
@@ -1291,8 +1234,6 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   void* ev;
   if (dagrt_status st = get_event(c, &ev)) return st;
   trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
-  if (k->persist_arg >= 0 && k->persist_arg < k->nparams && arrs[k->persist_arg])
-    c->be->hint_persist(arrs[k->persist_arg]->dev, arrs[k->persist_arg]->bytes);
   if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, vid)) return st_;
   trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
   CK(c->be->record(ev, s), "cudaEventRecord");
@@ -1645,22 +1586,6 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh,
   p.kernelParams = argv;
   cudaGraphNode_t n;
   CK(cudaGraphAddKernelNode(&n, g->r.g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
-  if (k->persist_arg >= 0 && k->persist_arg < k->nparams && arrs[k->persist_arg]) {
-    // same L2 residency hint as the scheduler's launches (fair baseline)
-    int maxp = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
-    if (maxp > 0) {
-      cudaKernelNodeAttrValue v{};
-      const size_t nb = arrs[k->persist_arg]->bytes;
-      v.accessPolicyWindow.base_ptr = arrs[k->persist_arg]->dev;
-      v.accessPolicyWindow.num_bytes = nb;
-      v.accessPolicyWindow.hitRatio = nb > (size_t)maxp ? (float)maxp / (float)nb : 1.0f;
-      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      CK(cudaGraphKernelNodeSetAttribute(n, cudaKernelNodeAttributeAccessPolicyWindow, &v),
-         "cudaGraphKernelNodeSetAttribute");
-    }
-  }
   g->r.nodes.push_back(n);
   *node = (uint32_t)g->r.nodes.size() - 1;
   return DAGRT_OK;
