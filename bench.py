@@ -61,6 +61,30 @@ WORKLOAD = {
 }
 
 
+SMS = 148
+# DFMA + DMUL + DADD executed per option by k_bs (ncu dynamic instruction
+# counts, profiles/r1_summary.md) and the FP64 pipe's peak per SM per clock
+# (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained).
+BS_FP64_OPS_PER_OPTION = 55
+FP64_OPS_PER_SM_CLK = 64
+
+
+def load_traffic(bench, kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu summary
+    (profiles/<round>_traffic.json, written by tools/collect_profiles.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    for p in reversed(files):
+        try:
+            with open(p) as f:
+                v = json.load(f).get(bench, {}).get(kernel)
+        except (OSError, ValueError):
+            continue
+        if v is not None:
+            return v, os.path.relpath(p, ROOT)
+    return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -272,6 +296,22 @@ def main():
                     "event-timed intervals on their launch streams"}
     total_bytes = sum(kb.values())
     roof["dag_work_roofline_ms"] = total_bytes / (peak * 1e9) * 1e3
+    if name == "bs" and busy_ms > 0:
+        # B&S is bound by the FP64 pipe, not HBM: report against it
+        n_opt = FULL["bs"]["n"]
+        ops = BS_FP64_OPS_PER_OPTION * n_opt * n_launch / (busy_ms * 1e-3) / 1e9
+        mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        fpeak = FP64_OPS_PER_SM_CLK * SMS * mhz * 1e6 / 1e9
+        roof.update({"bound": "alu", "pipe": "fp64", "achieved": ops, "peak": fpeak,
+                     "unit": "G fp64 ops/s", "frac": ops / fpeak,
+                     "peak_source": f"{FP64_OPS_PER_SM_CLK} fp64 ops/clk/SM (ncu peak_sustained) x "
+                                    f"{SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                     "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
+                     "hbm_achieved_gbs": achieved, "hbm_frac": achieved / peak if achieved else None})
+    tr, tr_src = load_traffic(name, "k_" + dom)
+    if tr is not None:
+        roof["traffic"] = tr
+        roof["traffic_source"] = tr_src
     cpu = None
     if world == 1 and not args.no_cpu:
         v, sample, cores = cpu_oracle_rate(name)

@@ -218,8 +218,228 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------
+// conv2, version 2: A operand in TMEM, raw input rows staged by cp.async.
+//
+// The first version fed A from shared memory: each thread gathered its
+// pixel's 9 taps with stride-2 128-bit loads (4x the L1 wavefronts of a
+// coalesced load) and wrote hi/lo A tiles that the tensor core then re-read
+// three times -- the L1/shared-memory data pipe, not HBM, set its speed.
+// Here, per 128-pixel tile (one output row segment p, q0..q0+127):
+//   * the 3 input rows it needs (129 pixel PAIRS each, 24.8 KB) are copied
+//     with coalesced 16-byte cp.async into an S-stage ring, de-interleaved
+//     by pixel parity and channel half so that every later shared-memory
+//     read is a conflict-free 16-byte-per-lane access; the copies run S-1
+//     tiles ahead of the math;
+//   * each thread (= TMEM lane = output pixel) reads its 9 taps, splits them
+//     into TF32 hi/lo and writes them to TMEM with tcgen05.st (A_hi in
+//     columns [0,72), A_lo in [72,144)), so A never touches shared memory;
+//   * one thread issues the 27 tcgen05.mma.kind::tf32 with A from TMEM and
+//     B (weights, hi/lo) from shared memory into one of two 16-column
+//     accumulators, and commits to an mbarrier;
+//   * while the tensor core runs, the threads drain the PREVIOUS tile's
+//     accumulator (tcgen05.ld, ReLU, coalesced 64-byte-per-pixel stores).
+// Two 128-thread CTAs per SM (256 TMEM columns each).
+constexpr int kC2Stages = 4;
+constexpr int kC2Pairs = 129;                      // input pixel pairs per row window
+constexpr int kC2Sub = kC2Pairs * 16;              // bytes per (parity, channel half) sub-row
+constexpr int kC2Row = 4 * kC2Sub;                 // bytes per staged input row
+constexpr int kC2Stage = 3 * kC2Row;               // bytes per stage (3 input rows)
+constexpr int kC2Chunks = kC2Stage / 16;           // 16-byte copies per stage
+constexpr int kC2Smem = 2 * kTcTaps * kTcBTile + kC2Stages * kC2Stage + 64;
+constexpr uint32_t kC2Cols = 256;                  // TMEM columns allocated per CTA
+constexpr uint32_t kC2ColLo = 72, kC2ColD = 144;   // A_lo, accumulators (2 x 16)
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bd, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a), "l"(bd), "r"(kTcIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __restrict__ in,
+                                                             const float* __restrict__ w,
+                                                             float* __restrict__ out, int H2, int W2) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* bhi = sm;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  unsigned char* ring = blo + kTcTaps * kTcBTile;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + kC2Stages * kC2Stage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int t = threadIdx.x, warp = t >> 5;
+
+  for (int i = t; i < 16 * 72; i += kTcThreads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kC2Cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lane quarter
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int tpr = (W3 + kTcThreads - 1) / kTcThreads;  // tiles per output row
+  const long long ntiles = (long long)H3 * tpr;
+  const uint32_t ring_s = smem_u32(ring);
+
+  // stage the input window of tile `tile` into ring slot `slot`
+  auto stage = [&](long long tile, int slot) {
+    const int p = (int)(tile / tpr), q0 = (int)(tile % tpr) * kTcThreads;
+    const uint32_t base = ring_s + slot * kC2Stage;
+    for (int c = t; c < kC2Chunks; c += kTcThreads) {
+      const int a = c / (4 * kC2Pairs), rem = c % (4 * kC2Pairs);
+      const int pair = rem >> 2, sub = rem & 3;  // sub = parity*2 + channel half
+      const int y = 2 * p + a - 1, x = 2 * (q0 - 1 + pair) + (sub >> 1);
+      const bool ok = y >= 0 && y < H2 && x >= 0 && x < W2;
+      const float* src = ok ? in + ((size_t)y * W2 + x) * 8 + (sub & 1) * 4 : in;
+      cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, src, ok);
+    }
+  };
+  // accumulator buffer `buf` of tile `tl` -> ReLU -> out (64 contiguous bytes per pixel)
+  auto drain = [&](long long tl, int buf) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(tlane + kC2ColD + 16 * buf));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * kTcThreads + t;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        dst[c] = make_float4(fmaxf(__uint_as_float(r[4 * c]), 0.f), fmaxf(__uint_as_float(r[4 * c + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * c + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * c + 3]), 0.f));
+    }
+  };
+  const long long first = blockIdx.x, step = gridDim.x;
+  // prologue: S-1 tiles in flight (one commit group per tile, empty groups keep the count)
+#pragma unroll
+  for (int s = 0; s < kC2Stages - 1; ++s) {
+    const long long tile = first + s * step;
+    if (tile < ntiles) stage(tile, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
+  uint32_t phase = 0;
+  long long prev = -1;
+  int k = 0;
+  for (long long tile = first; tile < ntiles; tile += step, ++k) {
+    const int slot = k % kC2Stages;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kC2Stages - 2) : "memory");
+    __syncthreads();  // tile's window visible to all; slot (k-1)%S free again
+    {
+      const long long nt = tile + (kC2Stages - 1) * step;
+      if (nt < ntiles) stage(nt, (k + kC2Stages - 1) % kC2Stages);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // this pixel's 9 taps (b=0: odd pixel of pair i; b=1: even of pair i+1; b=2: odd of pair i+1)
+    const unsigned char* win = ring + slot * kC2Stage;
+    float4 v[kTcTaps][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int par = b == 1 ? 0 : 1, rel = b == 0 ? t : t + 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          v[a * 3 + b][h] = *reinterpret_cast<const float4*>(win + a * kC2Row + (par * 2 + h) * kC2Sub + rel * 16);
+      }
+    if (prev >= 0) {  // the previous tile's MMAs have finished reading A
+      tc_mbar_wait(mbar, phase);
+      phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap) {
+      float hi[8], lo[8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float e[4] = {v[tap][h].x, v[tap][h].y, v[tap][h].z, v[tap][h].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          hi[h * 4 + j] = tf32_rna(e[j]);
+          lo[h * 4 + j] = tf32_rna(e[j] - hi[h * 4 + j]);
+        }
+      }
+      tmem_st8(tlane + tap * 8, hi);
+      tmem_st8(tlane + kC2ColLo + tap * 8, lo);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      const uint32_t d = tmem + kC2ColD + 16 * (k & 1);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma_ts(d, tmem + tap * 8, dbh, acc);
+        acc = 1;
+        tc_mma_ts(d, tmem + kC2ColLo + tap * 8, dbh, 1);
+        tc_mma_ts(d, tmem + tap * 8, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar))
+                   : "memory");
+    }
+    // drain the previous tile's accumulator while this tile's MMAs run
+    if (prev >= 0) drain(prev, (k - 1) & 1);
+    prev = tile;
+  }
+  if (prev >= 0) {
+    tc_mbar_wait(mbar, phase);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    drain(prev, (k - 1) & 1);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC2Cols));
+}
+
 static const Builtin kConvTc[] = {
-    {"conv2", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+    {"conv2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kC2Smem},
+    // first tcgen05 version (A from shared memory), kept for comparison
+    {"conv2_tc1", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},
 };
 DAGRT_REGISTER_BUILTINS(kConvTc);

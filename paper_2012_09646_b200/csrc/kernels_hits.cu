@@ -4,34 +4,29 @@
 // SpMV on a power-law graph (20M rows, average degree 3, hub rows with
 // ~1.5M non-zeros).  The paper used LightSpMV [31] (Kepler-era dynamic row
 // distribution).  On B200 the kernel is a deterministic MERGE-PATH SpMV:
-// the merged sequence of N row-ends and E non-zeros is cut into equal tiles
-// of 2048 items (one CTA each), so every CTA does the same work whatever
-// the degree distribution:
-//   1. two warps locate the tile's (row, nnz) start/end coordinates with a
-//      32-ary merge-path search over row_ptr (5 probes instead of 25);
-//   2. the CTA stages its gathered x[col] values and row ends in shared
-//      memory with coalesced loads;
-//   3. each thread consumes 8 items (binary-searched inside shared memory),
-//      completed rows are written directly;
-//   4. a fixed-shape block scan carries partial row sums across threads;
-//   5. rows spanning several CTAs are finished by the LAST CTA to deposit
-//      its partial (atomic arrival count per row), which adds the partials
-//      in CTA order with a fixed warp tree -> bit-deterministic results,
-//      no spinning, no float atomics.
-// The output array y carries the cross-CTA workspace after its N floats
-// (see spmv_ws_bytes), like the reduction outputs (kcommon.cuh RedOut).
+// the merged sequence of N row ends and E non-zeros is cut into equal
+// contiguous ranges, one per warp of a persistent grid, so every warp does
+// the same work whatever the degree distribution (k_spmv below).  Rows that
+// span several warp ranges are finished by the LAST participant to deposit
+// its share (atomic arrival count per row), which adds the shares in warp
+// order with a fixed tree -> bit-deterministic results, no spinning, no
+// float atomics.  The output array y carries that workspace after its N
+// floats (3 words per warp of the grid, zeroed once by the allocator), like
+// the reduction outputs (kcommon.cuh RedOut).
 #include "kcommon.cuh"
 
 namespace dagrt {
 
 constexpr int kSpmvThreads = 256;
-constexpr int kSpmvItems = 8;
-constexpr int kSpmvTile = kSpmvThreads * kSpmvItems;  // merge items per CTA
+constexpr int kSpmvWarps = kSpmvThreads / 32;
+constexpr int kSpmvItems = 8;                 // merge items per lane
+constexpr int kSpmvTile = 32 * kSpmvItems;    // merge items per warp tile
 
+// Cross-warp workspace, one slot per participant (global warp of the grid).
 struct SpmvWs {
-  float* part;    // [ncta] partial of the row crossing the CTA's end
-  float* head;    // [ncta] partial of the row crossing the CTA's start (its end part)
-  unsigned* cnt;  // [ncta] arrival counters, indexed by the row's first CTA
+  float* part;    // [G] share of the row crossing the warp range's end
+  float* head;    // [G] share of the row crossing the range's start (its end part)
+  unsigned* cnt;  // [G] arrival counters, indexed by the row's first participant
 };
 
 __device__ __forceinline__ SpmvWs spmv_ws(float* y, long long n, long long ncta) {
@@ -83,7 +78,7 @@ __device__ __forceinline__ float warp_ordered_sum(const volatile float* v, long 
 }
 
 // Deposit `val` for row r (spanning CTAs cs..ce) and finish the row if last.
-// Executed by warp 0 of the CTA.  `is_head` = this CTA is the row's last (ce).
+// Executed by one whole warp.  `is_head` = this participant holds the row's end (ce).
 __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long long r, long long cs,
                                              long long ce, long long c, float val, bool is_head) {
   const int lane = threadIdx.x & 31;
@@ -106,172 +101,166 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
   }
 }
 
-// Persistent merge-path SpMV.  CTA b owns the contiguous tile range
-// [b*per, (b+1)*per).  All its tile boundaries (up to 256 at a time) are
-// located first by all 8 warps in parallel (32-ary searches).  Rows that
-// cross tile boundaries INSIDE the CTA's range are carried from tile to tile
-// in shared memory (no atomics, no fences); only the row crossing the CTA's
-// start and the row crossing its end are finished across CTAs (spmv_deposit,
-// slots indexed by CTA), so at most two deposits per CTA leave the per-tile
-// critical path clean.
-constexpr int kSpmvChunk = 256;
-
+// Persistent merge-path SpMV with WARP tiles.  Global warp g of G owns the
+// contiguous merge range of tiles [g*per, (g+1)*per), each tile 256 items
+// (8 per lane).  Warps never wait for each other (no CTA barriers): a warp
+// finds its start with one 32-ary search, then walks its tiles with the row
+// ends and column indices of tile c+1 in flight while tile c is gathered and
+// reduced.  Per tile:
+//   1. nr = rows ending in the tile = #{p : pos(p) < L}, pos(p) = p +
+//      row_ptr[i0+p+1] - j0 the merge index of row end p (ballot counts;
+//      the predicate holds on a prefix, so no search is needed);
+//   2. gathers x[col] for the tile's nn = L - nr non-zeros;
+//   3. row ends are marked in a byte map; each lane reads the 8 marks of its
+//      items, an exclusive warp scan of the mark counts gives its first row
+//      and non-zero, and it reduces its items sequentially;
+//   4. a segmented warp scan carries partial rows across lanes, the warp's
+//      running carry across tiles; completed rows are written to y[i0..i1)
+//      from shared memory, coalesced.
+// Rows spanning several warp ranges are finished by spmv_deposit.
 __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict__ row_ptr,
                                                        const int* __restrict__ col,
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, long long N) {
-  __shared__ int s_bnd[kSpmvChunk + 1];
-  // double-buffered staging (tile parity): the next tile's writes never race
-  // with the previous tile's reads, so no barrier is needed before staging
-  __shared__ float s_val_buf[2][kSpmvTile];
-  __shared__ int s_rend_buf[2][kSpmvTile + 1];  // row ends relative to j0
-  __shared__ float s_wsum[kSpmvThreads / 32];
-  __shared__ int s_wflag[kSpmvThreads / 32];
-  __shared__ int s_first_emitter;
-  __shared__ float s_carry, s_head_val, s_cta_carry;
+  __shared__ float s_val_all[kSpmvWarps][kSpmvTile];
+  __shared__ float s_y_all[kSpmvWarps][kSpmvTile];
+  __shared__ __align__(16) unsigned char s_mark_all[kSpmvWarps][kSpmvTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* s_val = s_val_all[warp];
+  float* s_y = s_y_all[warp];
+  unsigned char* s_mark = s_mark_all[warp];
   const long long E = (long long)__ldg(row_ptr + N);
   const long long total = N + E;
   const long long ntiles = (total + kSpmvTile - 1) / kSpmvTile;
-  const SpmvWs ws = spmv_ws(y, N, gridDim.x);
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const long long me = blockIdx.x;
-  const long long tb0 = me * per;
-  const long long te0 = min(ntiles, tb0 + per);
-  if (tb0 >= te0) return;  // uniform per CTA
+  const long long G = (long long)gridDim.x * kSpmvWarps;
+  const long long g = (long long)blockIdx.x * kSpmvWarps + warp;
+  const long long per = (ntiles + G - 1) / G;
+  const long long tb = g * per, te = min(ntiles, tb + per);
+  if (tb >= te) return;  // warp-uniform; the kernel has no CTA barriers
+  const SpmvWs ws = spmv_ws(y, N, G);
   const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
-  auto cta_of_diag = [&](long long d) { return (d / kSpmvTile) / per; };
-  if (t == 0) s_cta_carry = 0.f;
+  auto warp_of_diag = [&](long long d) { return (d / kSpmvTile) / per; };
 
-  for (long long tb = tb0; tb < te0; tb += kSpmvChunk) {
-    const long long te = min(te0, tb + kSpmvChunk);
-    const int nb = (int)(te - tb) + 1;
-    __syncthreads();  // s_bnd of the previous chunk consumed
-    for (int b = warp; b < nb; b += kSpmvThreads / 32) {
-      const long long d = min(total, (tb + b) * (long long)kSpmvTile);
-      const long long i = warp_merge_search(row_ptr, N, E, d);
-      if (lane == 0) s_bnd[b] = (int)i;
+  long long i0 = warp_merge_search(row_ptr, N, E, tb * kSpmvTile);
+  long long j0 = tb * kSpmvTile - i0;
+  const long long rp_first = i0 < N ? (long long)__ldg(row_ptr + i0) : E;
+  bool head_pending = i0 < N && rp_first < j0;  // row i0 began in an earlier warp's range
+  float carry = 0.f;
+
+  int re[kSpmvItems], ci[kSpmvItems];
+#pragma unroll
+  for (int u = 0; u < kSpmvItems; ++u) {
+    const int p = lane + 32 * u;
+    re[u] = i0 + p < N ? ldg_hint(row_ptr + i0 + p + 1, pol_stream) : 0;
+    ci[u] = j0 + p < E ? ldg_hint(col + j0 + p, pol_stream) : 0;
+  }
+
+  for (long long c = tb; c < te; ++c) {
+    const long long d0 = c * kSpmvTile;
+    const int L = (int)(min(total, d0 + kSpmvTile) - d0);
+    const int j0i = (int)j0;
+    // ---- 1. rows ending in this tile
+    int pos[kSpmvItems];
+    int nr = 0;
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int p = lane + 32 * u;
+      pos[u] = i0 + p < N ? p + (re[u] - j0i) : 0x7fffffff;
+      nr += __popc(__ballot_sync(0xffffffffu, pos[u] < L));
     }
-    __syncthreads();
-    for (long long c = tb; c < te; ++c) {
-      const long long d0 = c * kSpmvTile, d1 = min(total, d0 + kSpmvTile);
-      const long long i0 = s_bnd[c - tb], i1 = s_bnd[c - tb + 1];
-      const long long j0 = d0 - i0, j1 = d1 - i1;
-      const int nn = (int)(j1 - j0), nr = (int)(i1 - i0);
-      const int nre = (int)(min(i1, N - 1) - i0 + 1);
-      // ---- stage: column indices, then gathers (8 loads in flight each), row ends
-      int ci[kSpmvItems];
+    const long long i1 = i0 + nr, j1 = d0 + L - i1;
+    const int nn = L - nr;
+    // ---- 2. gathers; then the next tile's row ends and columns go in flight
+    float xv[kSpmvItems];
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u)
+      xv[u] = lane + 32 * u < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
+    if (c + 1 < te) {
 #pragma unroll
       for (int u = 0; u < kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        ci[u] = k < nn ? ldg_hint(col + j0 + k, pol_stream) : 0;
+        const int p = lane + 32 * u;
+        re[u] = i1 + p < N ? ldg_hint(row_ptr + i1 + p + 1, pol_stream) : 0;
+        ci[u] = j1 + p < E ? ldg_hint(col + j1 + p, pol_stream) : 0;
       }
-      int re[kSpmvItems + 1];
+    }
+    // ---- 3. row-end marks and gathered values to shared memory
+    __syncwarp();  // the previous tile's shared-memory reads are done
+    reinterpret_cast<uint2*>(s_mark)[lane] = make_uint2(0u, 0u);
+    __syncwarp();
 #pragma unroll
-      for (int u = 0; u <= kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        re[u] = k < nre ? ldg_hint(row_ptr + i0 + k + 1, pol_stream) : 0;
-      }
-      const int rp0 = __ldg(row_ptr + i0);
-      float xv[kSpmvItems];
+    for (int u = 0; u < kSpmvItems; ++u)
+      if (pos[u] < L) s_mark[pos[u]] = 1;
 #pragma unroll
-      for (int u = 0; u < kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        xv[u] = k < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
-      }
-      float* s_val = s_val_buf[c & 1];
-      int* s_rend = s_rend_buf[c & 1];
-      const int j0i = (int)j0;
+    for (int u = 0; u < kSpmvItems; ++u) s_val[lane + 32 * u] = xv[u];
+    __syncwarp();
+    const int it0 = lane * kSpmvItems;
+    const int m = max(0, min(kSpmvItems, L - it0));
+    const uint2 mw = reinterpret_cast<const uint2*>(s_mark)[lane];
+    unsigned fl = 0;
 #pragma unroll
-      for (int u = 0; u < kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        if (k < nn) s_val[k] = xv[u];
-      }
+    for (int k = 0; k < 4; ++k) fl |= ((mw.x >> (8 * k)) & 1u) << k | ((mw.y >> (8 * k)) & 1u) << (k + 4);
+    fl &= (1u << m) - 1u;
+    const int cnt = __popc(fl);
+    int incl = cnt;
 #pragma unroll
-      for (int u = 0; u <= kSpmvItems; ++u) {
-        const int k = t + u * kSpmvThreads;
-        if (k < nre) s_rend[k] = re[u] - j0i;
-      }
-      if (t == 0) s_first_emitter = kSpmvThreads;
-      __syncthreads();  // (B)
-      // ---- thread-local merge-path search and sequential consumption
-      const int dl = min(t * kSpmvItems, nn + nr);
-      int lo = max(0, dl - nn), hi = min(dl, nr);
-      while (lo < hi) {
-        const int p = (lo + hi) >> 1;
-        if (s_rend[p] <= dl - p - 1) lo = p + 1;
-        else hi = p;
-      }
-      int ri = lo, nj = dl - lo;
-      const int de = min(dl + kSpmvItems, nn + nr);
-      float sum = 0.f, first_val = 0.f;
-      bool emitted = false;
-      long long first_row = -1;
-      for (int it = dl; it < de; ++it) {
-        const bool row_end = (ri < nr) && (s_rend[ri] <= nj);
-        if (row_end) {
-          if (!emitted) {
-            emitted = true;
-            first_row = i0 + ri;
-            first_val = sum;
-          } else {
-            stg_hint(y + i0 + ri, sum, pol_stream);
-          }
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    int ri = incl - cnt;          // local index of this lane's first row end
+    const int nj0 = it0 - ri;     // local index of this lane's first non-zero
+    float v[kSpmvItems];
+#pragma unroll
+    for (int k = 0; k < kSpmvItems; ++k)
+      v[k] = s_val[(nj0 + k - __popc(fl & ((1u << k) - 1u))) & (kSpmvTile - 1)];
+    float sum = 0.f, first_val = 0.f;
+    int first_row = -1;
+#pragma unroll
+    for (int k = 0; k < kSpmvItems; ++k) {
+      if (k < m) {
+        if ((fl >> k) & 1u) {
+          if (first_row < 0) { first_row = ri; first_val = sum; }
+          else s_y[ri] = sum;
           sum = 0.f;
           ++ri;
         } else {
-          sum += s_val[nj];
-          ++nj;
+          sum += v[k];
         }
       }
-      // ---- segmented inclusive scan over threads (warp shuffles + one
-      // fixed-order cross-warp step): s(t) = sum(t) + (emitted(t) ? 0 : s(t-1))
-      float sc = sum;
-      bool fl = emitted;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float yv = __shfl_up_sync(0xffffffffu, sc, off);
-        const bool f = __shfl_up_sync(0xffffffffu, fl, off);
-        if (lane >= off && !fl) { sc += yv; fl = f; }
-      }
-      if (lane == 31) { s_wsum[warp] = sc; s_wflag[warp] = fl ? 1 : 0; }
-      if (emitted) atomicMin(&s_first_emitter, t);
-      __syncthreads();  // (C)
-      float win = 0.f;
-      for (int w = 0; w < warp; ++w) win = s_wflag[w] ? s_wsum[w] : win + s_wsum[w];
-      const float s_incl = fl ? sc : sc + win;
-      float incoming = __shfl_up_sync(0xffffffffu, s_incl, 1);  // s(t-1)
-      if (lane == 0) incoming = win;
-      const int fe = s_first_emitter;
-      const bool cont = (long long)rp0 < j0;  // row i0 started before this tile
-      const float carry_in = (cont && c > tb0) ? s_cta_carry : 0.f;
-      const bool head_x = cont && cta_of_diag(i0 + rp0) < me;  // row i0 began in an earlier CTA
-      if (emitted) {
-        float v = first_val + incoming;
-        if (t == fe && first_row == i0) {
-          v += carry_in;
-          if (head_x) s_head_val = v;
-          else stg_hint(y + i0, v, pol_stream);
-        } else {
-          stg_hint(y + first_row, v, pol_stream);
-        }
-      }
-      if (t == kSpmvThreads - 1) s_carry = s_incl;
-      __syncthreads();  // (D)
-      // running partial of the row crossing this tile's end (this CTA's share)
-      const float new_carry = fe < kSpmvThreads ? s_carry : carry_in + s_carry;
-      if (warp == 0) {
-        if (fe < kSpmvThreads && head_x)
-          spmv_deposit(ws, y, i0, cta_of_diag(i0 + rp0), me, me, s_head_val, true);
-        if (c == te0 - 1 && i1 < N) {
-          const long long rs = nr > 0 ? (long long)s_rend[nr - 1] + j0 : (long long)rp0;  // row_ptr[i1]
-          const long long rend = (long long)s_rend[nr] + j0;                            // row_ptr[i1+1]
-          const long long as = cta_of_diag(i1 + rs), ae = cta_of_diag(i1 + rend);
-          if (ae > me && as <= me) spmv_deposit(ws, y, i1, as, ae, me, new_carry, false);
-        }
-      }
-      if (t == 0) s_cta_carry = new_carry;  // read by the next tile after barrier (C)
     }
+    // ---- 4. segmented scan across lanes, carry across tiles
+    float sc = sum;
+    bool f = first_row >= 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float yv = __shfl_up_sync(0xffffffffu, sc, off);
+      const bool fv = __shfl_up_sync(0xffffffffu, f, off);
+      if (lane >= off && !f) { sc += yv; f = fv; }
+    }
+    const float acc = f ? sc : sc + carry;  // running value of the open row at this lane
+    const float prev = __shfl_up_sync(0xffffffffu, acc, 1);
+    if (first_row >= 0) s_y[first_row] = first_val + (lane == 0 ? carry : prev);
+    carry = __shfl_sync(0xffffffffu, acc, 31);
+    __syncwarp();
+    int pstart = 0;
+    if (head_pending && nr > 0) {
+      spmv_deposit(ws, y, i0, warp_of_diag(i0 + rp_first), g, g, s_y[0], true);
+      head_pending = false;
+      pstart = 1;
+    }
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int p = lane + 32 * u;
+      if (p >= pstart && p < nr) stg_hint(y + i0 + p, s_y[p], pol_stream);
+    }
+    i0 = i1;
+    j0 = j1;
+  }
+  // the row crossing this range's end: deposit this warp's share
+  if (i0 < N) {
+    const long long rs = __ldg(row_ptr + i0), rend = __ldg(row_ptr + i0 + 1);
+    const long long as = warp_of_diag(i0 + rs), ae = warp_of_diag(i0 + rend);
+    if (ae > g && as <= g) spmv_deposit(ws, y, i0, as, ae, g, carry, false);
   }
 }
 

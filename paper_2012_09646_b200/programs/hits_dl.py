@@ -8,15 +8,18 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
-CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64  # csrc/kernels_conv_tc.cu kTcSmem
+CONV2_TC_SMEM = 2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 64  # csrc/kernels_conv_tc.cu kC2Smem
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
-SPMV_TILE = 256 * 8      # merge items per CTA (csrc/kernels_hits.cu)
+SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)
+SPMV_WARPS = 8           # warps per 256-thread CTA
 
 
 def spmv_out_bytes(n, e):
-    ncta = -(-(n + e) // SPMV_TILE)
-    return 4 * n + 16 + 12 * ncta, max(1, ncta)
+    """(bytes of an SpMV output: N floats + 3 workspace words per warp, grid)."""
+    ntiles = -(-(n + e) // SPMV_TILE)
+    grid = max(1, min(-(-ntiles // SPMV_WARPS), 4 * SMS))  # persistent, 4 CTAs per SM
+    return 4 * n + 16 + 12 * SPMV_WARPS * grid, grid
 
 
 class Hits(Program):
@@ -39,7 +42,7 @@ class Hits(Program):
                 self.upload(name, arr)
         self.alloc("a1", n, torch.float32, mirror=stream)
         self.alloc("h1", n, torch.float32, mirror=stream)
-        ob, self.ncta = spmv_out_bytes(n, self.e)
+        ob, gs = spmv_out_bytes(n, self.e)
         self.alloc("a2", 0, None, nbytes=ob)
         self.alloc("h2", 0, None, nbytes=ob)
         self.alloc_red("an")
@@ -49,7 +52,6 @@ class Hits(Program):
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
-        gs = min(self.ncta, 4 * SMS)  # persistent merge-path CTAs (4 resident per SM)
         self.it = [
             P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
             P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1

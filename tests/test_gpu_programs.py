@@ -341,9 +341,11 @@ def test_dl_full_size_sampled(ctx):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
-def test_dl_conv2_ffma_variant_matches_oracle(ctx, h, w):
-    """The CUDA-core conv2 variant (conv2_ffma) against the oracle too."""
+def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
+    """The other conv2 kernels (CUDA-core FFMA; first tcgen05 version with A
+    from shared memory) against the oracle too."""
     p = DeepLearning(ctx, h=h, w=w)
     p.load_inputs(1)
     p.run()
@@ -351,8 +353,12 @@ def test_dl_conv2_ffma_variant_matches_oracle(ctx, h, w):
     (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
     out = torch.zeros(h3 * w3s * 16, device="cuda")
     torch.cuda.synchronize()
-    o_arr = ctx.register_tensor(f"c2_ffma_{h}", out)
-    ctx.launch("conv2_ffma", ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
+    o_arr = ctx.register_tensor(f"c2_{variant}_{h}", out)
+    if variant == "conv2_ffma":
+        ctx.launch(variant, ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
+    else:
+        ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
+                   smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
     ctx.sync()
     spec = synth.spec_dl(h, w)
     w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)

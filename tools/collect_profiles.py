@@ -41,6 +41,7 @@ def main(tag):
                      f"{(r['frac'] or 0):.3f} | {d['clocks'].get('sm_mhz')} MHz {d['clocks'].get('reasons')} |")
         shutil.copy(p, os.path.join(PROF, f"{tag}_bench_{b}.json"))
     lines.append("")
+    traffic = {}
     for csvp in sorted(glob.glob(os.path.join(OUT, "ncu_*.csv"))):
         b = os.path.basename(csvp)[4:-4]
         buf = io.StringIO()
@@ -51,6 +52,7 @@ def main(tag):
         lines.append(buf.getvalue().rstrip())
         lines.append("```\n")
         shutil.copy(csvp, os.path.join(PROF, f"{tag}_ncu_{b}.csv"))
+        traffic[b] = ncu_summary.traffic(csvp)
     ov = sorted(glob.glob(os.path.join(OUT, "overlap_*.json")))
     if ov:
         lines.append("## Schedule overlap (PAPER.md §V-F metrics, from the scheduler's event timeline)\n")
@@ -74,6 +76,9 @@ def main(tag):
         lines.append("```")
         lines.append(buf.getvalue().rstrip())
         lines.append("```\n")
+    if traffic:  # read by bench.py for roofline.traffic (DRAM bytes per launch, ncu)
+        with open(os.path.join(PROF, f"{tag}_traffic.json"), "w") as f:
+            json.dump(traffic, f, indent=1, sort_keys=True)
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))

@@ -21,6 +21,21 @@ def load(path):
     return out
 
 
+def traffic(path):
+    """{kernel short name: mean DRAM bytes (read + write) per launch}."""
+    data = load(path)
+    agg = defaultdict(lambda: [0, 0.0])
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    for (i, name), m in data.items():
+        short = name.split("(")[0].replace("void ", "").replace("dagrt::", "").split("<")[0]
+        if "dram__bytes_read.sum" not in m:
+            continue
+        b = sum(m[k][0] * scale.get(m[k][1], 0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+        agg[short][0] += 1
+        agg[short][1] += b
+    return {k: v[1] / v[0] for k, v in agg.items() if v[0]}
+
+
 def main(path, peak=6540.8):
     data = load(path)
     agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0.0])
