@@ -271,9 +271,19 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
                : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __restrict__ in,
-                                                             const float* __restrict__ w,
-                                                             float* __restrict__ out, int H2, int W2) {
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])));
+}
+
+// NT = 128: one thread per pixel (both channel halves).  NT = 256: warps w
+// and w+4 share TMEM lane quarter w and split each pixel's channels (half
+// the per-thread work on the critical path, twice the warps to hide it).
+template <int NT>
+__device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, const float* __restrict__ w,
+                                                float* __restrict__ out, int H2, int W2) {
+  constexpr int NH = NT / 128;  // channel halves per thread: 2 (NT=128) or 1 (NT=256)
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* bhi = sm;
   unsigned char* blo = bhi + kTcTaps * kTcBTile;
@@ -281,8 +291,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __rest
   uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + kC2Stages * kC2Stage);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
   const int t = threadIdx.x, warp = t >> 5;
+  const int pix = t & 127, hh = NT == 256 ? t >> 7 : 0;
 
-  for (int i = t; i < 16 * 72; i += kTcThreads) {
+  for (int i = t; i < 16 * 72; i += NT) {
     const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
     const float x = w[i];
     const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
@@ -305,41 +316,57 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __rest
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lane quarter
+  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lane quarter
 
   const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
-  const int tpr = (W3 + kTcThreads - 1) / kTcThreads;  // tiles per output row
+  const int tpr = (W3 + 127) / 128;  // tiles per output row
   const long long ntiles = (long long)H3 * tpr;
   const uint32_t ring_s = smem_u32(ring);
 
-  // stage the input window of tile `tile` into ring slot `slot`
+  // stage the input window of tile `tile` (3 rows x 129 pixel pairs, each row
+  // contiguous in global memory) into ring slot `slot`
   auto stage = [&](long long tile, int slot) {
-    const int p = (int)(tile / tpr), q0 = (int)(tile % tpr) * kTcThreads;
+    const int p = (int)(tile / tpr), q0 = (int)(tile % tpr) * 128;
+    const int x0 = 2 * (q0 - 1);  // first input pixel of the window
+    const bool xin = x0 >= 0 && x0 + 2 * kC2Pairs <= W2;
     const uint32_t base = ring_s + slot * kC2Stage;
-    for (int c = t; c < kC2Chunks; c += kTcThreads) {
-      const int a = c / (4 * kC2Pairs), rem = c % (4 * kC2Pairs);
-      const int pair = rem >> 2, sub = rem & 3;  // sub = parity*2 + channel half
-      const int y = 2 * p + a - 1, x = 2 * (q0 - 1 + pair) + (sub >> 1);
-      const bool ok = y >= 0 && y < H2 && x >= 0 && x < W2;
-      const float* src = ok ? in + ((size_t)y * W2 + x) * 8 + (sub & 1) * 4 : in;
-      cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, src, ok);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int y = 2 * p + a - 1;
+      const bool yin = y >= 0 && y < H2;
+      const float* row = in + ((size_t)(yin ? y : 0) * W2 + x0) * 8;
+      for (int rem = t; rem < 4 * kC2Pairs; rem += NT) {  // 16-byte chunk of the window row
+        const int pair = rem >> 2, sub = rem & 3;         // sub = parity*2 + channel half
+        const int x = x0 + (rem >> 1);
+        const bool ok = yin && (xin || (x >= 0 && x < W2));
+        cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, ok ? row + rem * 4 : in, ok);
+      }
     }
   };
-  // accumulator buffer `buf` of tile `tl` -> ReLU -> out (64 contiguous bytes per pixel)
+  // accumulator buffer `buf` of tile `tl` -> ReLU -> out (this thread's channels of its pixel)
   auto drain = [&](long long tl, int buf) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(tlane + kC2ColD + 16 * buf));
+    constexpr int NC = 8 * NH;
+    uint32_t r[NC];
+    const uint32_t ta = tlane + kC2ColD + 16 * buf + 8 * hh;
+    if constexpr (NH == 2) {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15])
+          : "r"(ta));
+    } else {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                     "=r"(r[7])
+                   : "r"(ta));
+    }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * kTcThreads + t;
+    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * 128 + pix;
     if (q < W3) {
-      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16);
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16 + 8 * hh);
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < NC / 4; ++c)
         dst[c] = make_float4(fmaxf(__uint_as_float(r[4 * c]), 0.f), fmaxf(__uint_as_float(r[4 * c + 1]), 0.f),
                              fmaxf(__uint_as_float(r[4 * c + 2]), 0.f),
                              fmaxf(__uint_as_float(r[4 * c + 3]), 0.f));
@@ -368,15 +395,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __rest
     }
     // this pixel's 9 taps (b=0: odd pixel of pair i; b=1: even of pair i+1; b=2: odd of pair i+1)
     const unsigned char* win = ring + slot * kC2Stage;
-    float4 v[kTcTaps][2];
+    float4 v[kTcTaps][NH];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
-        const int par = b == 1 ? 0 : 1, rel = b == 0 ? t : t + 1;
+        const int par = b == 1 ? 0 : 1, rel = b == 0 ? pix : pix + 1;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          v[a * 3 + b][h] = *reinterpret_cast<const float4*>(win + a * kC2Row + (par * 2 + h) * kC2Sub + rel * 16);
+        for (int h = 0; h < NH; ++h)
+          v[a * 3 + b][h] =
+              *reinterpret_cast<const float4*>(win + a * kC2Row + (par * 2 + h + hh) * kC2Sub + rel * 16);
       }
     if (prev >= 0) {  // the previous tile's MMAs have finished reading A
       tc_mbar_wait(mbar, phase);
@@ -385,18 +413,26 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __rest
     }
 #pragma unroll
     for (int tap = 0; tap < kTcTaps; ++tap) {
-      float hi[8], lo[8];
+      float hi[4 * NH], lo[4 * NH];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < NH; ++h) {
         const float e[4] = {v[tap][h].x, v[tap][h].y, v[tap][h].z, v[tap][h].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          hi[h * 4 + j] = tf32_rna(e[j]);
-          lo[h * 4 + j] = tf32_rna(e[j] - hi[h * 4 + j]);
+          // hi = x truncated to TF32 (exact in TF32), lo = x - hi (exact in
+          // fp32; the tensor core keeps its top 10 mantissa bits: error
+          // <= 2^-20 |x|).  Two instructions per element.
+          hi[h * 4 + j] = __uint_as_float(__float_as_uint(e[j]) & 0xffffe000u);
+          lo[h * 4 + j] = e[j] - hi[h * 4 + j];
         }
       }
-      tmem_st8(tlane + tap * 8, hi);
-      tmem_st8(tlane + kC2ColLo + tap * 8, lo);
+      if constexpr (NH == 2) {
+        tmem_st8(tlane + tap * 8, hi);
+        tmem_st8(tlane + kC2ColLo + tap * 8, lo);
+      } else {
+        tmem_st4(tlane + tap * 8 + 4 * hh, hi);
+        tmem_st4(tlane + kC2ColLo + tap * 8 + 4 * hh, lo);
+      }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -435,8 +471,21 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc2(const float* __rest
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC2Cols));
 }
 
+__global__ void __launch_bounds__(128, 2) k_conv2_tc2(const float* __restrict__ in, const float* __restrict__ w,
+                                                      float* __restrict__ out, int H2, int W2) {
+  conv2_tmem_body<128>(in, w, out, H2, W2);
+}
+__global__ void __launch_bounds__(256, 2) k_conv2_tc3(const float* __restrict__ in, const float* __restrict__ w,
+                                                      float* __restrict__ out, int H2, int W2) {
+  conv2_tmem_body<256>(in, w, out, H2, W2);
+}
+
 static const Builtin kConvTc[] = {
-    {"conv2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+    // launch: 2 x 148 CTAs of 256 threads, kC2Smem bytes of dynamic shared memory
+    {"conv2", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kC2Smem},
+    // the same pipeline with one 128-thread warpgroup per CTA (kept for comparison)
+    {"conv2_tc2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC2Smem},
     // first tcgen05 version (A from shared memory), kept for comparison
     {"conv2_tc1", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,

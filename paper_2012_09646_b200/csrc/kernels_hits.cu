@@ -118,10 +118,26 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
 //      running carry across tiles; completed rows are written to y[i0..i1)
 //      from shared memory, coalesced.
 // Rows spanning several warp ranges are finished by spmv_deposit.
-__global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict__ row_ptr,
-                                                       const int* __restrict__ col,
-                                                       const float* __restrict__ x,
-                                                       float* __restrict__ y, long long N) {
+// L2 policy variants (tools/spmv_variants.py): XP for the x gathers (0 default,
+// 1 evict-last), SP for the streamed CSR arrays and y (0 default, 1 evict-first,
+// 2 evict-first and no L1 allocation).
+template <int XP, int SP>
+__device__ __forceinline__ int spmv_ld_stream(const int* p, uint64_t pol) {
+  if (SP == 0) return __ldg(p);
+  if (SP == 1) return ldg_hint(p, pol);
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <int XP>
+__device__ __forceinline__ float spmv_ld_x(const float* p, uint64_t pol) {
+  return XP == 1 ? ldg_hint(p, pol) : __ldg(p);
+}
+
+template <int XP, int SP>
+__device__ __forceinline__ void spmv_body(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                          const float* __restrict__ x, float* __restrict__ y,
+                                          long long N_) {
   __shared__ float s_val_all[kSpmvWarps][kSpmvTile];
   __shared__ float s_y_all[kSpmvWarps][kSpmvTile];
   __shared__ __align__(16) unsigned char s_mark_all[kSpmvWarps][kSpmvTile];
@@ -129,60 +145,65 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
   float* s_val = s_val_all[warp];
   float* s_y = s_y_all[warp];
   unsigned char* s_mark = s_mark_all[warp];
-  const long long E = (long long)__ldg(row_ptr + N);
-  const long long total = N + E;
-  const long long ntiles = (total + kSpmvTile - 1) / kSpmvTile;
-  const long long G = (long long)gridDim.x * kSpmvWarps;
-  const long long g = (long long)blockIdx.x * kSpmvWarps + warp;
-  const long long per = (ntiles + G - 1) / G;
-  const long long tb = g * per, te = min(ntiles, tb + per);
+  const long long E_ = (long long)__ldg(row_ptr + N_);
+  if (N_ + E_ + kSpmvTile >= (1ll << 31)) __trap();  // merge coordinates are 32-bit (documented limit)
+  const int N = (int)N_, E = (int)E_, total = N + E;
+  const int ntiles = (total + kSpmvTile - 1) / kSpmvTile;
+  const int G = (int)gridDim.x * kSpmvWarps;
+  const int g = (int)blockIdx.x * kSpmvWarps + warp;
+  const int per = (ntiles + G - 1) / G;
+  const int tb = g * per, te = min(ntiles, tb + per);
   if (tb >= te) return;  // warp-uniform; the kernel has no CTA barriers
-  const SpmvWs ws = spmv_ws(y, N, G);
+  const SpmvWs ws = spmv_ws(y, N_, G);
   const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   auto warp_of_diag = [&](long long d) { return (d / kSpmvTile) / per; };
 
-  long long i0 = warp_merge_search(row_ptr, N, E, tb * kSpmvTile);
-  long long j0 = tb * kSpmvTile - i0;
-  const long long rp_first = i0 < N ? (long long)__ldg(row_ptr + i0) : E;
+  int i0 = (int)warp_merge_search(row_ptr, N_, E_, (long long)tb * kSpmvTile);
+  int j0 = tb * kSpmvTile - i0;
+  const int rp_first = i0 < N ? __ldg(row_ptr + i0) : E;
   bool head_pending = i0 < N && rp_first < j0;  // row i0 began in an earlier warp's range
   float carry = 0.f;
 
+  // row ends (row_ptr[i+1]) and column indices of a tile starting at (i, j)
   int re[kSpmvItems], ci[kSpmvItems];
+  auto load_tile = [&](int i, int j) {
+    const int* rp = row_ptr + i + 1 + lane;
+    const int* cp = col + j + lane;
+    if (i + kSpmvTile <= N && j + kSpmvTile <= E) {  // interior tile: no bounds checks
 #pragma unroll
-  for (int u = 0; u < kSpmvItems; ++u) {
-    const int p = lane + 32 * u;
-    re[u] = i0 + p < N ? ldg_hint(row_ptr + i0 + p + 1, pol_stream) : 0;
-    ci[u] = j0 + p < E ? ldg_hint(col + j0 + p, pol_stream) : 0;
-  }
+      for (int u = 0; u < kSpmvItems; ++u) {
+        re[u] = spmv_ld_stream<XP, SP>(rp + 32 * u, pol_stream);
+        ci[u] = spmv_ld_stream<XP, SP>(cp + 32 * u, pol_stream);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int p = lane + 32 * u;
+        re[u] = i + p < N ? spmv_ld_stream<XP, SP>(rp + 32 * u, pol_stream) : 0x3fffffff;
+        ci[u] = j + p < E ? spmv_ld_stream<XP, SP>(cp + 32 * u, pol_stream) : 0;
+      }
+    }
+  };
+  load_tile(i0, j0);
 
-  for (long long c = tb; c < te; ++c) {
-    const long long d0 = c * kSpmvTile;
-    const int L = (int)(min(total, d0 + kSpmvTile) - d0);
-    const int j0i = (int)j0;
-    // ---- 1. rows ending in this tile
+  for (int c = tb; c < te; ++c) {
+    const int L = min(total - c * kSpmvTile, kSpmvTile);
+    // ---- 1. rows ending in this tile: pos(p) = p + row_ptr[i0+p+1] - j0 < L
     int pos[kSpmvItems];
     int nr = 0;
 #pragma unroll
     for (int u = 0; u < kSpmvItems; ++u) {
-      const int p = lane + 32 * u;
-      pos[u] = i0 + p < N ? p + (re[u] - j0i) : 0x7fffffff;
+      pos[u] = lane + 32 * u + (re[u] - j0);
       nr += __popc(__ballot_sync(0xffffffffu, pos[u] < L));
     }
-    const long long i1 = i0 + nr, j1 = d0 + L - i1;
+    const int i1 = i0 + nr, j1 = j0 + (L - nr);
     const int nn = L - nr;
     // ---- 2. gathers; then the next tile's row ends and columns go in flight
     float xv[kSpmvItems];
 #pragma unroll
     for (int u = 0; u < kSpmvItems; ++u)
-      xv[u] = lane + 32 * u < nn ? ldg_hint(x + ci[u], pol_keep) : 0.f;
-    if (c + 1 < te) {
-#pragma unroll
-      for (int u = 0; u < kSpmvItems; ++u) {
-        const int p = lane + 32 * u;
-        re[u] = i1 + p < N ? ldg_hint(row_ptr + i1 + p + 1, pol_stream) : 0;
-        ci[u] = j1 + p < E ? ldg_hint(col + j1 + p, pol_stream) : 0;
-      }
-    }
+      xv[u] = lane + 32 * u < nn ? spmv_ld_x<XP>(x + ci[u], pol_keep) : 0.f;
+    if (c + 1 < te) load_tile(i1, j1);
     // ---- 3. row-end marks and gathered values to shared memory
     __syncwarp();  // the previous tile's shared-memory reads are done
     reinterpret_cast<uint2*>(s_mark)[lane] = make_uint2(0u, 0u);
@@ -191,15 +212,11 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
     for (int u = 0; u < kSpmvItems; ++u)
       if (pos[u] < L) s_mark[pos[u]] = 1;
 #pragma unroll
-    for (int u = 0; u < kSpmvItems; ++u) s_val[lane + 32 * u] = xv[u];
+    for (int u = 0; u < kSpmvItems; ++u) s_val[lane + 32 * u] = xv[u];  // zeros past nn
     __syncwarp();
-    const int it0 = lane * kSpmvItems;
-    const int m = max(0, min(kSpmvItems, L - it0));
+    // 8 mark bytes (0/1) -> 8 flag bits: (w * 0x01020408) >> 24 packs a word's 4 bytes
     const uint2 mw = reinterpret_cast<const uint2*>(s_mark)[lane];
-    unsigned fl = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) fl |= ((mw.x >> (8 * k)) & 1u) << k | ((mw.y >> (8 * k)) & 1u) << (k + 4);
-    fl &= (1u << m) - 1u;
+    const unsigned fl = ((mw.x * 0x01020408u) >> 24) | (((mw.y * 0x01020408u) >> 24) << 4);
     const int cnt = __popc(fl);
     int incl = cnt;
 #pragma unroll
@@ -207,25 +224,23 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
       const int v = __shfl_up_sync(0xffffffffu, incl, off);
       if (lane >= off) incl += v;
     }
-    int ri = incl - cnt;          // local index of this lane's first row end
-    const int nj0 = it0 - ri;     // local index of this lane's first non-zero
+    int ri = incl - cnt;                       // local index of this lane's first row end
+    const int nj0 = lane * kSpmvItems - ri;    // local index of its first non-zero
+    // items past the tile's end carry no mark and read zeros (s_val past nn)
     float v[kSpmvItems];
 #pragma unroll
-    for (int k = 0; k < kSpmvItems; ++k)
-      v[k] = s_val[(nj0 + k - __popc(fl & ((1u << k) - 1u))) & (kSpmvTile - 1)];
+    for (int k = 0; k < kSpmvItems; ++k) v[k] = s_val[nj0 + k - __popc(fl & ((1u << k) - 1u))];
     float sum = 0.f, first_val = 0.f;
     int first_row = -1;
 #pragma unroll
     for (int k = 0; k < kSpmvItems; ++k) {
-      if (k < m) {
-        if ((fl >> k) & 1u) {
-          if (first_row < 0) { first_row = ri; first_val = sum; }
-          else s_y[ri] = sum;
-          sum = 0.f;
-          ++ri;
-        } else {
-          sum += v[k];
-        }
+      if ((fl >> k) & 1u) {
+        if (first_row < 0) { first_row = ri; first_val = sum; }
+        else s_y[ri] = sum;
+        sum = 0.f;
+        ++ri;
+      } else {
+        sum += v[k];
       }
     }
     // ---- 4. segmented scan across lanes, carry across tiles
@@ -244,14 +259,18 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
     __syncwarp();
     int pstart = 0;
     if (head_pending && nr > 0) {
-      spmv_deposit(ws, y, i0, warp_of_diag(i0 + rp_first), g, g, s_y[0], true);
+      spmv_deposit(ws, y, i0, warp_of_diag((long long)i0 + rp_first), g, g, s_y[0], true);
       head_pending = false;
       pstart = 1;
     }
+    float* yo = y + i0;
 #pragma unroll
     for (int u = 0; u < kSpmvItems; ++u) {
       const int p = lane + 32 * u;
-      if (p >= pstart && p < nr) stg_hint(y + i0 + p, s_y[p], pol_stream);
+      if (p >= pstart && p < nr) {
+        if (SP == 0) yo[p] = s_y[p];
+        else stg_hint(yo + p, s_y[p], pol_stream);
+      }
     }
     i0 = i1;
     j0 = j1;
@@ -263,6 +282,209 @@ __global__ void __launch_bounds__(kSpmvThreads, 4) k_spmv(const int* __restrict_
     if (ae > g && as <= g) spmv_deposit(ws, y, i0, as, ae, g, carry, false);
   }
 }
+
+// Version with the gathers one tile ahead: x[col] values of tile c+1 are
+// copied by 4-byte cp.async straight into the warp's second s_val buffer
+// while tile c is reduced, so the gather latency leaves the per-tile
+// critical path without costing registers.  Same arithmetic (bit-identical
+// results) as spmv_body.
+template <int SP>
+__device__ __forceinline__ void spmv_body_async(const int* __restrict__ row_ptr,
+                                                const int* __restrict__ col,
+                                                const float* __restrict__ x, float* __restrict__ y,
+                                                long long N_) {
+  __shared__ float s_val_all[kSpmvWarps][2][kSpmvTile];
+  __shared__ float s_y_all[kSpmvWarps][kSpmvTile];
+  __shared__ __align__(16) unsigned char s_mark_all[kSpmvWarps][kSpmvTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* s_y = s_y_all[warp];
+  unsigned char* s_mark = s_mark_all[warp];
+  const long long E_ = (long long)__ldg(row_ptr + N_);
+  if (N_ + E_ + kSpmvTile >= (1ll << 31)) __trap();  // merge coordinates are 32-bit (documented limit)
+  const int N = (int)N_, E = (int)E_, total = N + E;
+  const int ntiles = (total + kSpmvTile - 1) / kSpmvTile;
+  const int G = (int)gridDim.x * kSpmvWarps;
+  const int g = (int)blockIdx.x * kSpmvWarps + warp;
+  const int per = (ntiles + G - 1) / G;
+  const int tb = g * per, te = min(ntiles, tb + per);
+  if (tb >= te) return;  // warp-uniform; the kernel has no CTA barriers
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+  auto warp_of_diag = [&](long long d) { return (d / kSpmvTile) / per; };
+
+  int i0 = (int)warp_merge_search(row_ptr, N_, E_, (long long)tb * kSpmvTile);
+  int j0 = tb * kSpmvTile - i0;
+  const int rp_first = i0 < N ? __ldg(row_ptr + i0) : E;
+  bool head_pending = i0 < N && rp_first < j0;  // row i0 began in an earlier warp's range
+  float carry = 0.f;
+
+  int re[kSpmvItems], ci[kSpmvItems];
+  auto load_tile = [&](int i, int j) {
+    const int* rp = row_ptr + i + 1 + lane;
+    const int* cp = col + j + lane;
+    if (i + kSpmvTile <= N && j + kSpmvTile <= E) {
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        re[u] = spmv_ld_stream<1, SP>(rp + 32 * u, pol_stream);
+        ci[u] = spmv_ld_stream<1, SP>(cp + 32 * u, pol_stream);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kSpmvItems; ++u) {
+        const int p = lane + 32 * u;
+        re[u] = i + p < N ? spmv_ld_stream<1, SP>(rp + 32 * u, pol_stream) : 0x3fffffff;
+        ci[u] = j + p < E ? spmv_ld_stream<1, SP>(cp + 32 * u, pol_stream) : 0;
+      }
+    }
+  };
+  // merge positions of the row ends in a tile starting at (i, j) with re[] loaded;
+  // returns the number of rows ending in it
+  auto row_ends = [&](int j, int L, int (&pos)[kSpmvItems]) {
+    int nr = 0;
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      pos[u] = lane + 32 * u + (re[u] - j);
+      nr += __popc(__ballot_sync(0xffffffffu, pos[u] < L));
+    }
+    return nr;
+  };
+  // gathers of a tile with nn non-zeros into buffer b (zero-filled past nn), one commit group
+  auto gather = [&](int nn, int b) {
+    float* dst = s_val_all[warp][b];
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int k = lane + 32 * u;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + k);
+      const float* src = k < nn ? x + ci[u] : x;
+      asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;" ::"r"(d),
+                   "l"(src), "r"(k < nn ? 4 : 0), "l"(pol_keep)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  // prologue: tile tb's row ends and gathers, tile tb+1's indices in flight
+  load_tile(i0, j0);
+  int pos[kSpmvItems];
+  int L = min(total - tb * kSpmvTile, kSpmvTile);
+  int nr = row_ends(j0, L, pos);
+  int i1 = i0 + nr, j1 = j0 + (L - nr);
+  gather(L - nr, 0);
+  if (tb + 1 < te) load_tile(i1, j1);
+
+  for (int c = tb; c < te; ++c) {
+    const int b = (c - tb) & 1;
+    // ---- next tile: row ends, gathers (cp.async, other buffer), indices of the one after
+    int posn[kSpmvItems];
+    int Ln = 0, nrn = 0;
+    __syncwarp();  // all lanes finished reading buffer b^1 (tile c-1)
+    if (c + 1 < te) {
+      Ln = min(total - (c + 1) * kSpmvTile, kSpmvTile);
+      nrn = row_ends(j1, Ln, posn);
+      gather(Ln - nrn, b ^ 1);
+      if (c + 2 < te) load_tile(i1 + nrn, j1 + (Ln - nrn));
+    } else {
+      asm volatile("cp.async.commit_group;" ::: "memory");  // keep one group per step
+    }
+    // ---- tile c: marks, then wait for its gathers
+    reinterpret_cast<uint2*>(s_mark)[lane] = make_uint2(0u, 0u);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u)
+      if (pos[u] < L) s_mark[pos[u]] = 1;
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const float* s_val = s_val_all[warp][b];
+    const uint2 mw = reinterpret_cast<const uint2*>(s_mark)[lane];
+    const unsigned fl = ((mw.x * 0x01020408u) >> 24) | (((mw.y * 0x01020408u) >> 24) << 4);
+    const int cnt = __popc(fl);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    int ri = incl - cnt;
+    const int nj0 = lane * kSpmvItems - ri;
+    float v[kSpmvItems];
+#pragma unroll
+    for (int k = 0; k < kSpmvItems; ++k) v[k] = s_val[nj0 + k - __popc(fl & ((1u << k) - 1u))];
+    float sum = 0.f, first_val = 0.f;
+    int first_row = -1;
+#pragma unroll
+    for (int k = 0; k < kSpmvItems; ++k) {
+      if ((fl >> k) & 1u) {
+        if (first_row < 0) { first_row = ri; first_val = sum; }
+        else s_y[ri] = sum;
+        sum = 0.f;
+        ++ri;
+      } else {
+        sum += v[k];
+      }
+    }
+    float sc = sum;
+    bool f = first_row >= 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float yv = __shfl_up_sync(0xffffffffu, sc, off);
+      const bool fv = __shfl_up_sync(0xffffffffu, f, off);
+      if (lane >= off && !f) { sc += yv; f = fv; }
+    }
+    const float acc = f ? sc : sc + carry;
+    const float prev = __shfl_up_sync(0xffffffffu, acc, 1);
+    if (first_row >= 0) s_y[first_row] = first_val + (lane == 0 ? carry : prev);
+    carry = __shfl_sync(0xffffffffu, acc, 31);
+    __syncwarp();
+    int pstart = 0;
+    if (head_pending && nr > 0) {
+      spmv_deposit(ws, y, i0, warp_of_diag((long long)i0 + rp_first), g, g, s_y[0], true);
+      head_pending = false;
+      pstart = 1;
+    }
+    float* yo = y + i0;
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) {
+      const int p = lane + 32 * u;
+      if (p >= pstart && p < nr) {
+        if (SP == 0) yo[p] = s_y[p];
+        else stg_hint(yo + p, s_y[p], pol_stream);
+      }
+    }
+    // advance: tile c+1 becomes current
+    i0 = i1;
+    j0 = j1;
+    i1 = i0 + nrn;
+    j1 = j0 + (Ln - nrn);
+    L = Ln;
+    nr = nrn;
+#pragma unroll
+    for (int u = 0; u < kSpmvItems; ++u) pos[u] = posn[u];
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (i0 < N) {
+    const long long rs = __ldg(row_ptr + i0), rend = __ldg(row_ptr + i0 + 1);
+    const long long as = warp_of_diag(i0 + rs), ae = warp_of_diag(i0 + rend);
+    if (ae > g && as <= g) spmv_deposit(ws, y, i0, as, ae, g, carry, false);
+  }
+}
+
+#define SPMV_VARIANT(NAME, XP, SP)                                                                 \
+  __global__ void __launch_bounds__(kSpmvThreads, 4)                                               \
+      NAME(const int* __restrict__ row_ptr, const int* __restrict__ col, const float* __restrict__ x, \
+           float* __restrict__ y, long long N) {                                                     \
+    spmv_body<XP, SP>(row_ptr, col, x, y, N);                                                        \
+  }
+SPMV_VARIANT(k_spmv_sync, 1, 2)
+SPMV_VARIANT(k_spmv_x0s1, 0, 1)
+SPMV_VARIANT(k_spmv_x1s1, 1, 1)
+#define SPMV_ASYNC_VARIANT(NAME, SP)                                                               \
+  __global__ void __launch_bounds__(kSpmvThreads, 4)                                               \
+      NAME(const int* __restrict__ row_ptr, const int* __restrict__ col, const float* __restrict__ x, \
+           float* __restrict__ y, long long N) {                                                     \
+    spmv_body_async<SP>(row_ptr, col, x, y, N);                                                      \
+  }
+SPMV_ASYNC_VARIANT(k_spmv, 2)
+SPMV_ASYNC_VARIANT(k_spmv_as1, 1)
 
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
 __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, RedOut* out,
@@ -311,6 +533,11 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 
 static const Builtin kHits[] = {
     {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // variants (same results): gathers in registers (sync), L2 policies (tools/spmv_variants.py)
+    {"spmv_sync", (const void*)k_spmv_sync, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_x0s1", (const void*)k_spmv_x0s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_x1s1", (const void*)k_spmv_x1s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_as1", (const void*)k_spmv_as1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE},
     {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE},
 };

@@ -224,6 +224,69 @@ __device__ __forceinline__ void bs_body(const double* __restrict__ s, double* __
   for (long long i = done + tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
 }
 
+// Deeper prefetch without register cost: each thread keeps DEPTH of its own
+// option pairs in flight with 16-byte cp.async into a private shared-memory
+// ring of DEPTH+1 slots (it reads back only what it copied itself, so no
+// block barrier is needed), covering the HBM latency with DEPTH pricing
+// steps instead of one.  Same arithmetic and results as bs_body.
+template <int DEPTH>
+__device__ __forceinline__ void bs_body_async(const double* __restrict__ s, double* __restrict__ c,
+                                              long long n, double r, double v, double t, double k) {
+  __shared__ BsTables T;
+  __shared__ double2 ring[DEPTH + 1][256];
+  bs_tables_init(T);
+  BsConst C;
+  const double vst = v * sqrt(t);
+  C.vst = vst;
+  C.inv_vst = 1.0 / vst;
+  C.mu_s = (r + 0.5 * v * v) * t / vst;
+  C.inv_k = 1.0 / k;
+  C.c2 = exp(r * t) / k;
+  C.kexp = k * exp(-r * t);
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (aligned16(s) && aligned16(c) && blockDim.x == 256) {
+    const long long n2 = n >> 1;
+    const double2* s2 = reinterpret_cast<const double2*>(s);
+    double2* c2 = reinterpret_cast<double2*>(c);
+    auto fetch = [&](long long i, int slot) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[slot][threadIdx.x]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                   "l"(i < n2 ? s2 + i : s2), "r"(i < n2 ? 16 : 0)
+                   : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int q = 0; q < DEPTH; ++q) fetch(tid + q * nth, q);
+    int slot = 0;
+    for (long long i = tid; i < n2; i += nth) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH - 1) : "memory");
+      const double2 cur = ring[slot][threadIdx.x];
+      // refill the slot read in the previous step (its value is consumed)
+      fetch(i + DEPTH * nth, slot == 0 ? DEPTH : slot - 1);
+      double2 y;
+      y.x = bs_price(cur.x, C, T);
+      y.y = bs_price(cur.y, C, T);
+      c2[i] = y;
+      slot = slot == DEPTH ? 0 : slot + 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    done = n2 << 1;
+  }
+  for (long long i = done + tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
+}
+#define BS_ASYNC_VARIANT(NAME, DEPTH, MINB)                                                        \
+  __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs_body_async<DEPTH>(s, c, n, r, v, t, k);                                                     \
+  }
+BS_ASYNC_VARIANT(k_bs_a3b4, 3, 4)
+BS_ASYNC_VARIANT(k_bs_a5b4, 5, 4)
+BS_ASYNC_VARIANT(k_bs_a7b4, 7, 4)
+BS_ASYNC_VARIANT(k_bs_a5b3, 5, 3)
+
 // default variant: 1 pair per iteration, 4 CTAs/SM (fastest in tools/bs_variants.py)
 __global__ void __launch_bounds__(256, 4) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
@@ -255,6 +318,10 @@ static const Builtin kVecBs[] = {
     {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE},
     {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"bs", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_a3b4", (const void*)k_bs_a3b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_a5b4", (const void*)k_bs_a5b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_a7b4", (const void*)k_bs_a7b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_a5b3", (const void*)k_bs_a5b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p2b3", (const void*)k_bs_p2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p1b4", (const void*)k_bs_p1b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p2b4", (const void*)k_bs_p2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},

@@ -152,8 +152,8 @@ class DeepLearning(Program):
             P("conv1", g1, 256, [a["y"], a["w1"], a["c1y"], h, w]),
             P("pool", gp, 256, [a["c1x"], a["px"], h1, w1]),
             P("pool", gp, 256, [a["c1y"], a["py"], h1, w1]),
-            P("conv2", G2TC, 128, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
-            P("conv2", G2TC, 128, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", G2TC, 256, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", G2TC, 256, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
             P("concat", gc, 256, [a["c2x"], a["c2y"], a["z"], nz // 2, nz // 2]),
             P("dot", min(gc, 1024), 256, [a["z"], a["wd"], a["r"], nz]),
         ]

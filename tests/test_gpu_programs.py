@@ -20,6 +20,7 @@ from oracle import hits as ohits
 from oracle import img as oimg
 from oracle import ml as oml
 from paper_2012_09646_b200 import dagrt as D
+from paper_2012_09646_b200.programs.hits_dl import CONV2_TC_SMEM
 from paper_2012_09646_b200.programs import DeepLearning, Hits, Images, MLEnsemble
 
 pytestmark = pytest.mark.gpu
@@ -341,7 +342,7 @@ def test_dl_full_size_sampled(ctx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1"])
+@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc2"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
 def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     """The other conv2 kernels (CUDA-core FFMA; first tcgen05 version with A
@@ -356,9 +357,11 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     o_arr = ctx.register_tensor(f"c2_{variant}_{h}", out)
     if variant == "conv2_ffma":
         ctx.launch(variant, ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
-    else:
+    elif variant == "conv2_tc1":
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+    else:
+        ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TC_SMEM)
     ctx.sync()
     spec = synth.spec_dl(h, w)
     w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
@@ -368,3 +371,30 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     assert ok, info
     ok, info = close(p.t["c2x"][:h3 * w3s * 16].cpu().numpy().reshape(h3, w3s, 16), ref)
     assert ok, info
+
+
+@pytest.mark.parametrize("variant", ["spmv_sync", "spmv_as1", "spmv_x0s1", "spmv_x1s1"])
+def test_spmv_variants_bitwise(ctx, variant):
+    """SpMV variants (gathers in registers instead of cp.async; other L2
+    policies) give bit-identical y to the default kernel, which the HITS
+    parity tests pin to the oracle."""
+    from paper_2012_09646_b200.programs.hits_dl import spmv_out_bytes
+    n, e = 300_000, 900_000
+    rp, ci, _, _ = synth.powerlaw_graph(11, n, e)
+    ob, grid = spmv_out_bytes(n, int(rp[-1]))
+    t_rp = torch.from_numpy(rp).cuda()
+    t_ci = torch.from_numpy(ci).cuda()
+    t_x = torch.rand(n, device="cuda")
+    y0 = torch.zeros(ob // 4 + 1, device="cuda")
+    y1 = torch.zeros(ob // 4 + 1, device="cuda")
+    torch.cuda.synchronize()
+    A = [ctx.register_tensor(f"spv_{variant}_{k}", t) for k, t in
+         (("rp", t_rp), ("ci", t_ci), ("x", t_x), ("y0", y0), ("y1", y1))]
+    ctx.launch("spmv", grid, 256, A[0], A[1], A[2], A[3], n)
+    ctx.launch(variant, grid, 256, A[0], A[1], A[2], A[4], n)
+    ctx.sync()
+    assert torch.equal(y0[:n], y1[:n])
+    ok, info = close(y0[:n].cpu().numpy(), ohits.spmv(rp, ci, t_x.cpu().numpy().astype(np.float64)))
+    assert ok, info
+    for a in A:
+        ctx.unregister(a)

@@ -178,3 +178,27 @@ def test_graph_cache_replays_identical_results(mode):
         if mode == "stream":
             assert np.array_equal(b.mirror[f"c{i}"].numpy(), out)
     gctx.close()
+
+
+@pytest.mark.parametrize("variant", ["bs_a3b4", "bs_a5b4", "bs_a7b4", "bs_a5b3", "bs_p2b3",
+                                     "bs_p1b4", "bs_p2b4", "bs_p1b6", "bs_p4b2"])
+@pytest.mark.parametrize("n", [3, 200_001])
+def test_bs_variants_match_oracle(ctx, variant, n):
+    """Every B&S tuning variant (register or cp.async prefetch depths) prices
+    like the oracle on ragged sizes, in a grid that strides several times."""
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    c = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    import synth.gpu as sg
+    sp = synth.spec_bs(n)
+    sg.fill_tensor(s, 77, "s0", sp["s0"])
+    torch.cuda.synchronize()
+    S = ctx.register_tensor(f"bsv_s_{variant}_{n}", s)
+    C = ctx.register_tensor(f"bsv_c_{variant}_{n}", c)
+    ctx.launch(variant, 37, 256, S, C, n, obs.R, obs.V, obs.T, obs.K)
+    ctx.sync()
+    ref = obs.call(synth.draw(77, "s0", sp["s0"]))
+    out = c.cpu().numpy()
+    err = np.abs(out - ref) - (1e-10 * np.abs(ref) + 1e-12)
+    assert np.all(err <= 0), float(np.max(err))
+    ctx.unregister(S)
+    ctx.unregister(C)

@@ -13,12 +13,12 @@ if [ -z "$SKIP_TESTS" ]; then
   echo "smoke rc=$?" >> gpurun_out/smoke.log
 fi
 for b in ${BENCHES:-bs vec img ml hits dl}; do
-  timeout 900 python bench.py --bench $b > gpurun_out/bench_$b.json 2> gpurun_out/bench_$b.err
+  timeout 900 python bench.py --bench $b $BENCH_ARGS > gpurun_out/bench_$b.json 2> gpurun_out/bench_$b.err
 done
-timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+[ -z "$SKIP_REF" ] && timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+[ -z "$SKIP_REF" ] && timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 # launch list of the bench command (default workload), serialised by ncu
-timeout 900 ncu --metrics $M --clock-control none -c 400 --csv --log-file gpurun_out/ncu_benchcmd.csv \
+[ -z "$SKIP_REF" ] && timeout 900 ncu --metrics $M --clock-control none -c 400 --csv --log-file gpurun_out/ncu_benchcmd.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-baselines > gpurun_out/ncu_benchcmd.log 2>&1
 for b in ${PROF:-bs vec img ml hits dl}; do
   timeout 600 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_$b.csv \
@@ -33,7 +33,7 @@ for kb in ${FULL:-bs:k_bs img:k_blur ml:k_norm hits:k_spmv dl:k_conv1 dl:k_conv2
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"${k}" -c 1 -f \
     -o gpurun_out/prof_${k} python tools/profile_dag.py --bench $b --runs 1 > gpurun_out/prof_${k}.log 2>&1
 done
-timeout 600 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum \
+[ -z "$SKIP_REF" ] && timeout 600 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum \
   --clock-control none -k regex:"k_bs" -c 3 --csv --log-file gpurun_out/fp64_bs.csv \
   python tools/profile_dag.py --bench bs --runs 1 > gpurun_out/fp64_bs.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log
