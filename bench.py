@@ -168,10 +168,18 @@ def time_steps(fn, steps, warmup, dist):
 
 
 def cpu_oracle_rate(name, budget_s=10.0):
-    """Oracle (fp64, as it stands) on a bounded sample; returns (ms per DAG, sample text, cores)."""
+    """Oracle (fp64, as it stands) on a bounded sample; returns (ms per DAG,
+    sample text, cores).  BLAS thread pools are limited to one thread so the
+    core count is exact."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        return _cpu_oracle_rate(name, budget_s)
+
+
+def _cpu_oracle_rate(name, budget_s):
     import numpy as np
     import synth
-    cores = 1  # numpy elementwise/reductions here are single-threaded
+    cores = 1  # numpy is single-threaded here (BLAS pools limited above)
     if name == "bs":
         from oracle import bs as obs
         n = FULL["bs"]["n"]
@@ -196,7 +204,47 @@ def cpu_oracle_rate(name, budget_s=10.0):
             reps += 1
         el = time.perf_counter() - t0
         return el / reps * 1e3, f"{reps} full DAGs", cores
-    return None, "not implemented", cores
+    # The other four: the whole oracle DAG on a strip (IMG, DL: full-width
+    # row bands; ML: a row block) or a smaller graph of the same recipe
+    # (HITS), repeated within the budget and extrapolated linearly in the
+    # work unit (pixels, rows, vertices + edges) to one full-size DAG.
+    if name == "img":
+        from oracle import img as oi
+        rows, w = 128, FULL["img"]["w"]
+        im = synth.draw(synth.BASE_SEED, "img", synth.spec_img(rows, w)["img"]).reshape(rows, w)
+        fn = lambda: oi.img_pipeline(im)  # noqa: E731
+        scale, sample = FULL["img"]["h"] / rows, f"{rows}x{w} row band"
+    elif name == "ml":
+        from oracle import ml as om
+        rows, f = 20_000, 200
+        X = synth.draw(synth.BASE_SEED, "X", synth.spec_ml_x(rows, f)["X"]).reshape(rows, f)
+        p = synth.ml_params(synth.BASE_SEED, f, 10)
+        fn = lambda: om.ml(X, p["theta"], p["prior"], p["W"], p["b"])  # noqa: E731
+        scale, sample = FULL["ml"]["n"] / rows, f"{rows}x{f} row block"
+    elif name == "hits":
+        from oracle import hits as oh
+        n, e = 200_000, 600_000
+        g = synth.powerlaw_graph(synth.BASE_SEED, n, e)
+        fn = lambda: oh.hits(*g)  # noqa: E731
+        full = FULL["hits"]["n"] + FULL["hits"]["e"]
+        scale, sample = full / (n + len(g[1])), f"{n}-vertex {len(g[1])}-edge graph, same recipe, 10 iterations"
+    elif name == "dl":
+        from oracle import dl as odl
+        rows, w = 64, FULL["dl"]["w"]
+        sp = synth.spec_dl(rows, w)
+        x = synth.draw(synth.BASE_SEED, "x", sp["x"]).reshape(rows, w)
+        y = synth.draw(synth.BASE_SEED, "y", sp["y"]).reshape(rows, w)
+        w1, w2, wd = (synth.draw(synth.BASE_SEED, k, sp[k]) for k in ("w1", "w2", "wd"))
+        fn = lambda: odl.dl(x, y, w1, w2, wd)  # noqa: E731
+        scale, sample = FULL["dl"]["h"] / rows, f"two {rows}x{w} row bands"
+    else:
+        return None, "not implemented", cores
+    reps, t0 = 0, time.perf_counter()
+    while reps == 0 or time.perf_counter() - t0 < budget_s:
+        fn()
+        reps += 1
+    el = time.perf_counter() - t0
+    return el / reps * scale * 1e3, f"{reps} x oracle DAG on a {sample}, x{scale:.0f} to one DAG", cores
 
 
 def main():
