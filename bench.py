@@ -38,6 +38,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2012_09646_b200 import replicas  # noqa: E402
+
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
 # Full BASELINE.json sizes per benchmark (configs[0..4])
@@ -160,10 +162,8 @@ def time_steps(fn, steps, warmup, dist):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
+        ms = replicas.max_over_ranks(ms, dist, device="cuda")
+        replicas.barrier(dist)
     return ms
 
 
@@ -294,7 +294,7 @@ def main():
     ctx.profile(dom, False)
     st = ctx.stats()
     n_launch, sum_ms, busy_ms = ctx.profile_collect(dom)
-    value = ms / (K * world)
+    value = replicas.job_ms_per_dag(ms, K, world)
 
     # --- baselines and end-to-end (stream) mode
     res = {}
