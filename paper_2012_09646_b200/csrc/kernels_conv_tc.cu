@@ -219,51 +219,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
 }
 
 // ---------------------------------------------------------------------------
-// conv2, version 2: A operand in TMEM, raw input rows staged by cp.async.
+// conv2, version 2 (the product kernel): coalesced cp.async staging of the
+// raw input rows + A tiles in shared memory.
 //
-// The first version fed A from shared memory: each thread gathered its
-// pixel's 9 taps with stride-2 128-bit loads (4x the L1 wavefronts of a
-// coalesced load) and wrote hi/lo A tiles that the tensor core then re-read
-// three times -- the L1/shared-memory data pipe, not HBM, set its speed.
-// Here, per 128-pixel tile (one output row segment p, q0..q0+127):
+// The first version fed A from per-thread stride-2 128-bit gathers (4x the
+// L1 wavefronts of a coalesced load), which made the L1/shared-memory data
+// pipe, not HBM, set its speed.  (An attempt to keep A in TMEM and feed the
+// MMA from there -- tcgen05.mma with the A operand in tensor memory -- gave
+// wrong sums on B200 and was dropped; A stays in shared memory here.)
+// Per 128-pixel tile (one output row segment p, q0..q0+127):
 //   * the 3 input rows it needs (129 pixel PAIRS each, 24.8 KB) are copied
 //     with coalesced 16-byte cp.async into an S-stage ring, de-interleaved
 //     by pixel parity and channel half so that every later shared-memory
 //     read is a conflict-free 16-byte-per-lane access; the copies run S-1
 //     tiles ahead of the math;
-//   * each thread (= TMEM lane = output pixel) reads its 9 taps, splits them
-//     into TF32 hi/lo and writes them to TMEM with tcgen05.st (A_hi in
-//     columns [0,72), A_lo in [72,144)), so A never touches shared memory;
-//   * one thread issues the 27 tcgen05.mma.kind::tf32 with A from TMEM and
-//     B (weights, hi/lo) from shared memory into one of two 16-column
-//     accumulators, and commits to an mbarrier;
+//   * each thread (= MMA row = output pixel) reads its 9 taps from the ring,
+//     splits them into TF32 hi/lo and writes the A tiles (K-major, no
+//     swizzle, conflict-free 16-byte stores);
+//   * one thread issues the 27 tcgen05.mma.kind::tf32 (A, B from shared
+//     memory) into one of two 16-column TMEM accumulators and commits to an
+//     mbarrier;
 //   * while the tensor core runs, the threads drain the PREVIOUS tile's
 //     accumulator (tcgen05.ld, ReLU, coalesced 64-byte-per-pixel stores).
-// Two 128-thread CTAs per SM (256 TMEM columns each).
+// One 128-thread CTA per SM (the A tiles and the ring take 182 KB).
 constexpr int kC2Stages = 4;
 constexpr int kC2Pairs = 129;                      // input pixel pairs per row window
 constexpr int kC2Sub = kC2Pairs * 16;              // bytes per (parity, channel half) sub-row
 constexpr int kC2Row = 4 * kC2Sub;                 // bytes per staged input row
 constexpr int kC2Stage = 3 * kC2Row;               // bytes per stage (3 input rows)
-constexpr int kC2Chunks = kC2Stage / 16;           // 16-byte copies per stage
-constexpr int kC2Smem = 2 * kTcTaps * kTcBTile + kC2Stages * kC2Stage + 64;
-constexpr uint32_t kC2Cols = 256;                  // TMEM columns allocated per CTA
-constexpr uint32_t kC2ColLo = 72, kC2ColD = 144;   // A_lo, accumulators (2 x 16)
-
-__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bd, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
-      "r"(a), "l"(bd), "r"(kTcIdesc), "r"(acc));
-}
-
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
-}
+constexpr int kC2Smem = 2 * kTcTaps * kTcBTile + kC2Stages * kC2Stage + 2 * kTcTaps * kTcATile + 64;
+constexpr uint32_t kC2Cols = 32;                   // TMEM columns: 2 accumulators x 16
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -271,29 +256,20 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
-               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-               "r"(__float_as_uint(v[3])));
-}
-
-// NT = 128: one thread per pixel (both channel halves).  NT = 256: warps w
-// and w+4 share TMEM lane quarter w and split each pixel's channels (half
-// the per-thread work on the critical path, twice the warps to hide it).
-template <int NT>
-__device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, const float* __restrict__ w,
-                                                float* __restrict__ out, int H2, int W2) {
-  constexpr int NH = NT / 128;  // channel halves per thread: 2 (NT=128) or 1 (NT=256)
+__global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc4(const float* __restrict__ in,
+                                                             const float* __restrict__ w,
+                                                             float* __restrict__ out, int H2, int W2) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* bhi = sm;
   unsigned char* blo = bhi + kTcTaps * kTcBTile;
   unsigned char* ring = blo + kTcTaps * kTcBTile;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + kC2Stages * kC2Stage);
+  unsigned char* ahi = ring + kC2Stages * kC2Stage;
+  unsigned char* alo = ahi + kTcTaps * kTcATile;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(alo + kTcTaps * kTcATile);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
   const int t = threadIdx.x, warp = t >> 5;
-  const int pix = t & 127, hh = NT == 256 ? t >> 7 : 0;
 
-  for (int i = t; i < 16 * 72; i += NT) {
+  for (int i = t; i < 16 * 72; i += kTcThreads) {
     const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
     const float x = w[i];
     const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
@@ -316,7 +292,7 @@ __device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, co
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lane quarter
+  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lane quarter
 
   const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
   const int tpr = (W3 + 127) / 128;  // tiles per output row
@@ -328,45 +304,35 @@ __device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, co
   auto stage = [&](long long tile, int slot) {
     const int p = (int)(tile / tpr), q0 = (int)(tile % tpr) * 128;
     const int x0 = 2 * (q0 - 1);  // first input pixel of the window
-    const bool xin = x0 >= 0 && x0 + 2 * kC2Pairs <= W2;
     const uint32_t base = ring_s + slot * kC2Stage;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int y = 2 * p + a - 1;
       const bool yin = y >= 0 && y < H2;
-      const float* row = in + ((size_t)(yin ? y : 0) * W2 + x0) * 8;
-      for (int rem = t; rem < 4 * kC2Pairs; rem += NT) {  // 16-byte chunk of the window row
-        const int pair = rem >> 2, sub = rem & 3;         // sub = parity*2 + channel half
+      for (int rem = t; rem < 4 * kC2Pairs; rem += kTcThreads) {  // 16-byte chunk of the window row
+        const int pair = rem >> 2, sub = rem & 3;                  // sub = parity*2 + channel half
         const int x = x0 + (rem >> 1);
-        const bool ok = yin && (xin || (x >= 0 && x < W2));
-        cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, ok ? row + rem * 4 : in, ok);
+        const bool ok = yin && x >= 0 && x < W2;
+        const float* src = ok ? in + ((size_t)y * W2 + x) * 8 + (sub & 1) * 4 : in;
+        cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, src, ok);
       }
     }
   };
-  // accumulator buffer `buf` of tile `tl` -> ReLU -> out (this thread's channels of its pixel)
+  // accumulator buffer `buf` of tile `tl` -> ReLU -> out (64 contiguous bytes per pixel)
   auto drain = [&](long long tl, int buf) {
-    constexpr int NC = 8 * NH;
-    uint32_t r[NC];
-    const uint32_t ta = tlane + kC2ColD + 16 * buf + 8 * hh;
-    if constexpr (NH == 2) {
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15])
-          : "r"(ta));
-    } else {
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                     "=r"(r[7])
-                   : "r"(ta));
-    }
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(tlane + 16 * buf));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * 128 + pix;
+    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * 128 + t;
     if (q < W3) {
-      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16 + 8 * hh);
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16);
 #pragma unroll
-      for (int c = 0; c < NC / 4; ++c)
+      for (int c = 0; c < 4; ++c)
         dst[c] = make_float4(fmaxf(__uint_as_float(r[4 * c]), 0.f), fmaxf(__uint_as_float(r[4 * c + 1]), 0.f),
                              fmaxf(__uint_as_float(r[4 * c + 2]), 0.f),
                              fmaxf(__uint_as_float(r[4 * c + 3]), 0.f));
@@ -395,60 +361,52 @@ __device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, co
     }
     // this pixel's 9 taps (b=0: odd pixel of pair i; b=1: even of pair i+1; b=2: odd of pair i+1)
     const unsigned char* win = ring + slot * kC2Stage;
-    float4 v[kTcTaps][NH];
+    float4 v[kTcTaps][2];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
-        const int par = b == 1 ? 0 : 1, rel = b == 0 ? pix : pix + 1;
+        const int par = b == 1 ? 0 : 1, rel = b == 0 ? t : t + 1;
 #pragma unroll
-        for (int h = 0; h < NH; ++h)
-          v[a * 3 + b][h] =
-              *reinterpret_cast<const float4*>(win + a * kC2Row + (par * 2 + h + hh) * kC2Sub + rel * 16);
+        for (int h = 0; h < 2; ++h)
+          v[a * 3 + b][h] = *reinterpret_cast<const float4*>(win + a * kC2Row + (par * 2 + h) * kC2Sub + rel * 16);
       }
-    if (prev >= 0) {  // the previous tile's MMAs have finished reading A
+    if (prev >= 0) {  // the previous tile's MMAs are done: A tiles free, its accumulator ready
       tc_mbar_wait(mbar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;");
     }
 #pragma unroll
-    for (int tap = 0; tap < kTcTaps; ++tap) {
-      float hi[4 * NH], lo[4 * NH];
+    for (int tap = 0; tap < kTcTaps; ++tap)
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        const float e[4] = {v[tap][h].x, v[tap][h].y, v[tap][h].z, v[tap][h].w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // hi = x truncated to TF32 (exact in TF32), lo = x - hi (exact in
-          // fp32; the tensor core keeps its top 10 mantissa bits: error
-          // <= 2^-20 |x|).  Two instructions per element.
-          hi[h * 4 + j] = __uint_as_float(__float_as_uint(e[j]) & 0xffffe000u);
-          lo[h * 4 + j] = e[j] - hi[h * 4 + j];
-        }
+      for (int h = 0; h < 2; ++h) {
+        const float4 x = v[tap][h];
+        float4 hi, lo;
+        hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
+        hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
+        hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
+        hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+        put16(ahi + tap * kTcATile, t, h, hi);
+        put16(alo + tap * kTcATile, t, h, lo);
       }
-      if constexpr (NH == 2) {
-        tmem_st8(tlane + tap * 8, hi);
-        tmem_st8(tlane + kC2ColLo + tap * 8, lo);
-      } else {
-        tmem_st4(tlane + tap * 8 + 4 * hh, hi);
-        tmem_st4(tlane + kC2ColLo + tap * 8 + 4 * hh, lo);
-      }
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    // generic-proxy smem writes -> visible to the tensor core
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (t == 0) {
-      const uint32_t d = tmem + kC2ColD + 16 * (k & 1);
+      const uint32_t d = tmem + 16 * (k & 1);
       uint32_t acc = 0;
 #pragma unroll
       for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256);
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
         const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
         const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
-        tc_mma_ts(d, tmem + tap * 8, dbh, acc);
+        tc_mma(d, dah, dbh, acc);
         acc = 1;
-        tc_mma_ts(d, tmem + kC2ColLo + tap * 8, dbh, 1);
-        tc_mma_ts(d, tmem + tap * 8, dbl, 1);
+        tc_mma(d, dal, dbh, 1);
+        tc_mma(d, dah, dbl, 1);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(mbar))
@@ -471,23 +429,198 @@ __device__ __forceinline__ void conv2_tmem_body(const float* __restrict__ in, co
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC2Cols));
 }
 
-__global__ void __launch_bounds__(128, 2) k_conv2_tc2(const float* __restrict__ in, const float* __restrict__ w,
-                                                      float* __restrict__ out, int H2, int W2) {
-  conv2_tmem_body<128>(in, w, out, H2, W2);
-}
-__global__ void __launch_bounds__(256, 2) k_conv2_tc3(const float* __restrict__ in, const float* __restrict__ w,
-                                                      float* __restrict__ out, int H2, int W2) {
-  conv2_tmem_body<256>(in, w, out, H2, W2);
+
+// ---------------------------------------------------------------------------
+// conv2, version 3 (the product kernel): version 2's staging and MMAs, but
+//   * 384 threads = 3 groups of 128: group a (input row a of the 3x3 window)
+//     reads, splits and writes the 3 taps of that row for its pixel -- three
+//     times the warps of version 2 to hide the shared-memory latencies of
+//     the split (version 2 ran one warp per SM sub-partition);
+//   * two A buffers and two accumulators, each with its own mbarrier, so
+//     the A tiles of tile k+1 are written while the MMAs of tile k run;
+//   * TF32 split by truncation: hi = x with the low 13 mantissa bits
+//     cleared (exact in TF32), lo = x - hi (exact in fp32; the tensor core
+//     reads its top 10 mantissa bits, error <= 2^-21 |x|), 2 ops per element.
+// Ring of 3 stages (2 tiles of input rows in flight) + 2 x 72 KB of A tiles:
+// 225.6 KB of shared memory, one CTA per SM.
+constexpr int kC3Threads = 384;
+constexpr int kC3Stages = 3;
+constexpr int kC3ABuf = 2 * kTcTaps * kTcATile;  // hi + lo tiles of one tile
+constexpr int kC3Smem = 2 * kTcTaps * kTcBTile + kC3Stages * kC2Stage + 2 * kC3ABuf + 64;
+
+__global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __restrict__ in,
+                                                             const float* __restrict__ w,
+                                                             float* __restrict__ out, int H2, int W2) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* bhi = sm;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  unsigned char* ring = blo + kTcTaps * kTcBTile;
+  unsigned char* abuf = ring + kC3Stages * kC2Stage;  // [2][hi 9 taps | lo 9 taps]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(abuf + 2 * kC3ABuf);  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int t = threadIdx.x, warp = t >> 5;
+  const int grp = t >> 7, pix = t & 127;  // input row of the window, output pixel of the tile
+
+  for (int i = t; i < 16 * 72; i += kC3Threads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kC2Cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int tpr = (W3 + 127) / 128;  // tiles per output row
+  const long long ntiles = (long long)H3 * tpr;
+  const uint32_t ring_s = smem_u32(ring);
+
+  // input window of `tile` (3 rows x 129 pixel pairs, de-interleaved) -> ring slot
+  auto stage = [&](long long tile, int slot) {
+    const int p = (int)(tile / tpr), q0 = (int)(tile % tpr) * 128;
+    const int x0 = 2 * (q0 - 1);  // first input pixel of the window
+    const uint32_t base = ring_s + slot * kC2Stage;
+    for (int c = t; c < 3 * 4 * kC2Pairs; c += kC3Threads) {
+      const int a = c / (4 * kC2Pairs), rem = c - a * (4 * kC2Pairs);
+      const int pair = rem >> 2, sub = rem & 3;  // sub = parity*2 + channel half
+      const int y = 2 * p + a - 1, x = x0 + (rem >> 1);
+      const bool ok = y >= 0 && y < H2 && x >= 0 && x < W2;
+      const float* src = ok ? in + ((size_t)y * W2 + x) * 8 + (sub & 1) * 4 : in;
+      cp_async16(base + a * kC2Row + sub * kC2Sub + pair * 16, src, ok);
+    }
+  };
+  // accumulator `buf` of tile `tl` -> ReLU -> out; warps 0-3 (TMEM lane quarter = warp)
+  auto drain = [&](long long tl, int buf) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(tmem + ((uint32_t)(warp * 32) << 16) + 16 * buf));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * 128 + pix;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        dst[c] = make_float4(fmaxf(__uint_as_float(r[4 * c]), 0.f), fmaxf(__uint_as_float(r[4 * c + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * c + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * c + 3]), 0.f));
+    }
+  };
+  const long long first = blockIdx.x, step = gridDim.x;
+#pragma unroll
+  for (int s = 0; s < kC3Stages - 1; ++s) {
+    const long long tile = first + s * step;
+    if (tile < ntiles) stage(tile, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
+  uint32_t phase[2] = {0u, 0u};
+  long long prev = -1;
+  int k = 0;
+  for (long long tile = first; tile < ntiles; tile += step, ++k) {
+    const int slot = k % kC3Stages, b = k & 1;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kC3Stages - 2) : "memory");
+    __syncthreads();  // tile's window visible to all; slot (k-1)%S free again
+    {
+      const long long nt = tile + (kC3Stages - 1) * step;
+      if (nt < ntiles) stage(nt, (k + kC3Stages - 1) % kC3Stages);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // this group's 3 taps: b=0 odd pixel of pair pix, b=1 even of pair pix+1, b=2 odd of pair pix+1
+    const unsigned char* win = ring + slot * kC2Stage + grp * kC2Row;
+    unsigned char* ahi = abuf + b * kC3ABuf;
+    unsigned char* alo = ahi + kTcTaps * kTcATile;
+    // A buffer b was read by the MMAs of tile k-2, whose completion every
+    // thread observed before draining tile k-2 in the previous iteration
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      const int par = bb == 1 ? 0 : 1, rel = bb == 0 ? pix : pix + 1;
+      const int tap = grp * 3 + bb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x = *reinterpret_cast<const float4*>(win + (par * 2 + h) * kC2Sub + rel * 16);
+        float4 hi, lo;
+        hi.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u); lo.x = x.x - hi.x;
+        hi.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u); lo.y = x.y - hi.y;
+        hi.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u); lo.z = x.z - hi.z;
+        hi.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u); lo.w = x.w - hi.w;
+        put16(ahi + tap * kTcATile, pix, h, hi);
+        put16(alo + tap * kTcATile, pix, h, lo);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      const uint32_t d = tmem + 16 * b;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256);
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(d, dah, dbh, acc);
+        acc = 1;
+        tc_mma(d, dal, dbh, 1);
+        tc_mma(d, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar + b))
+                   : "memory");
+    }
+    // the previous tile: wait for its MMAs (all threads: frees its A buffer), drain it
+    if (prev >= 0) {
+      const int pb = (k - 1) & 1;
+      tc_mbar_wait(mbar + pb, phase[pb]);
+      phase[pb] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (warp < 4) drain(prev, pb);
+    }
+    prev = tile;
+  }
+  if (prev >= 0) {
+    const int pb = (k - 1) & 1;
+    tc_mbar_wait(mbar + pb, phase[pb]);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp < 4) drain(prev, pb);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC2Cols));
 }
 
 static const Builtin kConvTc[] = {
-    // launch: 2 x 148 CTAs of 256 threads, kC2Smem bytes of dynamic shared memory
-    {"conv2", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+    // launch: 148 persistent CTAs of 384 threads, kC3Smem bytes of dynamic shared memory
+    {"conv2", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kC3Smem},
+    // version 2: 128 threads, one A buffer (148 CTAs, kC2Smem)
+    {"conv2_tc4", (const void*)k_conv2_tc4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC2Smem},
-    // the same pipeline with one 128-thread warpgroup per CTA (kept for comparison)
-    {"conv2_tc2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     kC2Smem},
-    // first tcgen05 version (A from shared memory), kept for comparison
+    // first tcgen05 version (per-thread gathers of A), kept for comparison
     {"conv2_tc1", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},
 };

@@ -463,6 +463,13 @@ struct DeferBackend final : Backend {
     return err;
   }
 
+  // A stream wait issued right away (after flushing the batch): used to
+  // order a D2H copy after its producers without blocking the host.
+  cudaError_t wait_now(void* s, void* e) {
+    if (cudaError_t r = flush()) return r;
+    return in->wait(s, resolve(e));
+  }
+
   cudaError_t launch_now(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop) {
     if (cudaError_t e = flush()) return e;
     return in->launch(fn, g, b, args, smem, s, coop, 0);
@@ -562,6 +569,7 @@ struct dagrt_ctx_s {
   void* d2h_stream = nullptr;         // in-order D2H side stream
   void* graph_stream = nullptr;
   void* serial_stream = nullptr;
+  void* bounce = nullptr;              // pinned staging for small D2H reads into caller memory
   std::vector<dagrt_graph_s*> graphs;
   std::vector<ProfRec> prof;           // timed launches awaiting collection
   bool timeline = false;
@@ -794,7 +802,11 @@ dagrt_status pick_stream(dagrt_ctx c, int32_t* out) {
 }
 
 // Host blocks on exactly the conflicting vertices (L553-555), then retires them.
-dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write) {
+// With `order` (a D2H stream) the wait is not a separate host round trip: the
+// stream is made to wait on the parents' events and the caller's copy + one
+// stream synchronisation on it block the host until parents and copy are
+// done -- the same ordering, one host wake-up instead of two.
+dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order = nullptr) {
   c->scratch_edges.clear();
   infer(c, a, write);
   if (c->scratch_edges.empty()) {
@@ -810,7 +822,8 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write) {
     c->rec_v.push_back(dagrt_vertex_info{vid, 1, 0, -1, array_handle(c, a)});
   for (uint32_t p : c->scratch_parents) {
     trace_op(c, DAGRT_OP_EVENT_SYNC, -1, p, 0, 0);
-    CK(c->be->event_sync(c->vertices[p].ev), "cudaEventSynchronize");
+    if (order) CK(c->be->wait_now(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
+    else CK(c->be->event_sync(c->vertices[p].ev), "cudaEventSynchronize");
     c->st.host_syncs++;
   }
   for (uint32_t p : c->scratch_parents) retire(c, p);
@@ -818,19 +831,27 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write) {
   return DAGRT_OK;
 }
 
+constexpr size_t kBounceBytes = 64 << 10;
+
 dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   if (n == 0) return DAGRT_OK;
   trace_op(c, DAGRT_OP_D2H, -1, array_index(c, a), (int64_t)off, n);
   c->st.d2h_bytes += n;
   c->st.d2h_copies++;
   if (!c->be->real()) return DAGRT_OK;
+  // small reads into caller (possibly pageable) memory go through a pinned
+  // bounce buffer: a pageable D2H is staged by the driver and much slower
+  const bool bounce = n <= kBounceBytes && !(a->host && (char*)dst >= a->host &&
+                                             (char*)dst < a->host + a->bytes);
+  if (bounce && !c->bounce) CK(cudaMallocHost(&c->bounce, kBounceBytes), "cudaMallocHost bounce");
   void* t0;
   if (dagrt_status st_ = tl_begin(c, c->d2h_stream, &t0)) return st_;
-  CK(c->be->copy_async(dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream),
+  CK(c->be->copy_async(bounce ? c->bounce : dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream),
      "cudaMemcpyAsync D2H");
   if (dagrt_status st_ = tl_end(c, c->d2h_stream, t0, 2, -5, -1, array_index(c, a), n)) return st_;
   CK(c->be->stream_sync(c->d2h_stream), "cudaStreamSynchronize D2H");
   c->st.host_syncs++;
+  if (bounce) memcpy(dst, c->bounce, n);
   return DAGRT_OK;
 }
 
@@ -987,6 +1008,7 @@ dagrt_status dagrt_destroy(dagrt_ctx c) {
     if (s) c->be->stream_destroy(s);
   for (auto& a : c->arrays)
     if (a.h2d_ev) c->be->event_destroy(a.h2d_ev);
+  if (c->bounce) cudaFreeHost(c->bounce);
   delete c->be;
   delete c;
   return DAGRT_OK;
@@ -1267,8 +1289,11 @@ dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t byte
   if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
   if (off > a->bytes || bytes > a->bytes - off) return fail(c, DAGRT_EINVAL, "range out of bounds");
   if (bytes && !dst) return fail(c, DAGRT_EINVAL, "null dst");
+  // a read that needs a copy orders the copy after its producers on the D2H
+  // stream (one host round trip); otherwise the host waits on the events
+  const bool copy = bytes && (!a->host || a->coh == COH_DEVICE) && c->be->real();
   if (c->cfg.policy != DAGRT_SERIAL_SYNC)
-    if (dagrt_status s = host_sync_parents(c, a, false)) return s;
+    if (dagrt_status s = host_sync_parents(c, a, false, copy ? c->d2h_stream : nullptr)) return s;
   if (!a->host) return d2h(c, a, off, bytes, dst);
   if (a->coh == COH_DEVICE) {
     if (dagrt_status s = d2h(c, a, off, bytes, a->host + off)) return s;
@@ -1336,8 +1361,9 @@ dagrt_status dagrt_host_map(dagrt_ctx c, dagrt_array h, int32_t access, void** h
     a->readers.clear();
     a->coh = COH_HOST;
   } else {
+    const bool copy = a->bytes && a->coh == COH_DEVICE && c->be->real();
     if (c->cfg.policy != DAGRT_SERIAL_SYNC)
-      if (dagrt_status s = host_sync_parents(c, a, false)) return s;
+      if (dagrt_status s = host_sync_parents(c, a, false, copy ? c->d2h_stream : nullptr)) return s;
     if (a->coh == COH_DEVICE) {
       if (dagrt_status s = d2h(c, a, 0, a->bytes, a->host)) return s;
       a->coh = COH_BOTH;

@@ -8,8 +8,9 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
-CONV2_TC_SMEM = 2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 64  # csrc/kernels_conv_tc.cu kC2Smem
-G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
+CONV2_TC_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # csrc/kernels_conv_tc.cu kC3Smem
+CONV2_TC_THREADS = 384                            # k_conv2_tc5: 3 groups of 128
+G2TC = 148                                        # persistent tcgen05 CTAs (1 per SM)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)
 SPMV_WARPS = 8           # warps per 256-thread CTA
@@ -152,8 +153,8 @@ class DeepLearning(Program):
             P("conv1", g1, 256, [a["y"], a["w1"], a["c1y"], h, w]),
             P("pool", gp, 256, [a["c1x"], a["px"], h1, w1]),
             P("pool", gp, 256, [a["c1y"], a["py"], h1, w1]),
-            P("conv2", G2TC, 256, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
-            P("conv2", G2TC, 256, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", G2TC, CONV2_TC_THREADS, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", G2TC, CONV2_TC_THREADS, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
             P("concat", gc, 256, [a["c2x"], a["c2y"], a["z"], nz // 2, nz // 2]),
             P("dot", min(gc, 1024), 256, [a["z"], a["wd"], a["r"], nz]),
         ]
