@@ -52,6 +52,9 @@ FULL = {
     "dl": dict(h=16384, w=16384),
 }
 DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1"}
+# device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
+KSYM = {"square": "k_square", "bs": "k_bs", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv_plan",
+        "conv1": "k_conv1"}
 DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32"}
 WORKLOAD = {
     "vec": "VEC: 2 squares + sum of differences, N=1M fp32",
@@ -67,7 +70,7 @@ SMS = 148
 # DFMA + DMUL + DADD executed per option by k_bs (ncu dynamic instruction
 # counts, profiles/r1_summary.md) and the FP64 pipe's peak per SM per clock
 # (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained).
-BS_FP64_OPS_PER_OPTION = 55
+BS_FP64_OPS_PER_OPTION = 46  # 46.4 measured (gpurun_out fp64_bs2.csv -> profiles/)
 FP64_OPS_PER_SM_CLK = 64
 
 
@@ -362,7 +365,7 @@ def main():
                                     f"{SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                      "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
                      "hbm_achieved_gbs": achieved, "hbm_frac": achieved / peak if achieved else None})
-    tr, tr_src = load_traffic(name, "k_" + dom)
+    tr, tr_src = load_traffic(name, KSYM[dom])
     if tr is not None:
         roof["traffic"] = tr
         roof["traffic_source"] = tr_src

@@ -486,6 +486,163 @@ SPMV_VARIANT(k_spmv_x1s1, 1, 1)
 SPMV_ASYNC_VARIANT(k_spmv, 2)
 SPMV_ASYNC_VARIANT(k_spmv_as1, 1)
 
+
+// ---------------------------------------------------------------------------
+// SpMV by row class (the product kernel, "spmv").
+//
+// On the 20M-vertex power-law graph the merge-path kernels above run at
+// ~300 us whatever the gather footprint (tools/spmv_footprint.py: folding
+// the columns into N/64 entries saves only 18%): their per-item work (scans,
+// byte maps, shared-memory round trips) and its latency chains, not memory,
+// set the speed.  Here the rows are split by degree once, when the graph is
+// registered (a small "plan" array built from row_ptr, spmv_plan() in
+// programs/hits_dl.py), and each class gets the cheapest exact schedule:
+//   * short rows (deg <= 8; ~98% of rows, ~20% of non-zeros): one thread per
+//     row, 4 consecutive rows per thread 256 apart (coalesced row_ptr reads
+//     and y writes), all of a row's column loads then all its gathers in
+//     flight, summed in column order;
+//   * medium rows (8 < deg <= 4096): one warp per row, lanes stride the
+//     row's columns (coalesced), 4 gathers in flight per lane, fixed
+//     xor-tree warp reduction;
+//   * long rows (deg > 4096; ~1000 hubs holding ~45% of the non-zeros):
+//     chunks of 8192 non-zeros, one CTA per chunk (block reduction in a fixed
+//     tree); a hub's chunk sums are added in chunk order by the last chunk to
+//     arrive (atomic arrival count), so results are bit-reproducible.
+// One launch = one DAG vertex: CTA ranges [0, NL) long chunks (heaviest
+// first), then medium rows (8 per CTA), then short-row blocks (1024 rows).
+// Workspace after y's N floats (16-byte aligned): NL chunk sums, NL
+// arrival counters (zero at allocation; reset by the last arriver).
+constexpr int kPlanHeader = 16;    // [0] NL long chunks, [1] NM medium rows, [2] NS short blocks
+constexpr int kShortMax = 8;
+constexpr int kLongMin = 4096;
+constexpr int kLongChunk = 8192;
+constexpr int kShortRowsPerThread = 4;
+constexpr int kShortRowsPerCta = 256 * kShortRowsPerThread;
+
+// HINT 1: L2 evict-first for the streamed column indices, evict-last for the gathers
+template <int HINT>
+__device__ __forceinline__ float spmv_gather(const float* x, int c, uint64_t pol) {
+  return HINT ? ldg_hint(x + c, pol) : __ldg(x + c);
+}
+template <int HINT>
+__device__ __forceinline__ int spmv_col(const int* col, int k, uint64_t pol) {
+  return HINT ? ldg_hint(col + k, pol) : __ldg(col + k);
+}
+
+template <int HINT>
+__device__ __forceinline__ void spmv_plan_body(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                               const int* __restrict__ plan, const float* __restrict__ x,
+                                               float* __restrict__ y, long long N_) {
+  uint64_t pcol = 0, px = 0;
+  if (HINT) {
+    pcol = l2_policy_evict_first();
+    px = l2_policy_evict_last();
+  }
+  const int NL = __ldg(plan + 0), NM = __ldg(plan + 1);
+  const int NMC = (NM + 7) >> 3;
+  // the plan must have been built with this kernel's class bounds
+  if (__ldg(plan + 3) != kShortMax || __ldg(plan + 4) != kLongMin || __ldg(plan + 5) != kLongChunk) __trap();
+  const int bid = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int N = (int)N_;
+  if (bid < NL) {
+    // ---- long-row chunk: (row, k_begin, first chunk of the row, chunks of the row)
+    __shared__ float sh[32];
+    const int4 it = __ldg(reinterpret_cast<const int4*>(plan + kPlanHeader) + bid);
+    const int row = it.x, kb = it.y, first = it.z, cnt = it.w;
+    const int ke = min(kb + kLongChunk, __ldg(row_ptr + row + 1));
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k0 = kb + t; k0 < ke; k0 += 4 * 256) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = k0 + u * 256 < ke ? spmv_col<HINT>(col, k0 + u * 256, pcol) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += c[u] >= 0 ? spmv_gather<HINT>(x, c[u], px) : 0.f;
+    }
+    const float s = block_reduce((acc[0] + acc[1]) + (acc[2] + acc[3]), OpAdd(), sh);
+    if (cnt == 1) {
+      if (t == 0) y[row] = s;
+      return;
+    }
+    uintptr_t base = ((uintptr_t)(y + N) + 15) & ~(uintptr_t)15;
+    float* part = reinterpret_cast<float*>(base);
+    unsigned* arrive = reinterpret_cast<unsigned*>(part + NL);
+    __shared__ bool last;
+    if (t == 0) {
+      part[bid] = s;
+      __threadfence();
+      last = atomicAdd(arrive + first, 1u) == (unsigned)(cnt - 1);
+    }
+    __syncthreads();
+    if (!last || warp != 0) return;
+    __threadfence();
+    const volatile float* vp = part;
+    float v = 0.f;
+    for (int i = lane; i < cnt; i += 32) v += vp[first + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      y[row] = v;
+      arrive[first] = 0;  // reusable by the next launch
+    }
+    return;
+  }
+  if (bid < NL + NMC) {
+    // ---- medium row: one warp per row
+    const int m = (bid - NL) * 8 + warp;
+    if (m >= NM) return;
+    const int row = __ldg(plan + kPlanHeader + 4 * NL + m);
+    const int kb = __ldg(row_ptr + row), ke = __ldg(row_ptr + row + 1);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k0 = kb + lane; k0 < ke; k0 += 4 * 32) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = k0 + u * 32 < ke ? spmv_col<HINT>(col, k0 + u * 32, pcol) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += c[u] >= 0 ? spmv_gather<HINT>(x, c[u], px) : 0.f;
+    }
+    float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) y[row] = v;
+    return;
+  }
+  // ---- short rows: thread per row, 4 rows per thread 256 apart
+  const int r0 = (bid - NL - NMC) * kShortRowsPerCta + t;
+  int b[kShortRowsPerThread], d[kShortRowsPerThread];
+#pragma unroll
+  for (int j = 0; j < kShortRowsPerThread; ++j) {
+    const int r = r0 + 256 * j;
+    b[j] = r < N ? __ldg(row_ptr + r) : 0;
+    d[j] = r < N ? __ldg(row_ptr + r + 1) - b[j] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kShortRowsPerThread; ++j) {
+    const int r = r0 + 256 * j;
+    if (r >= N || d[j] > kShortMax) continue;  // medium / long rows are summed above
+    int c[kShortMax];
+#pragma unroll
+    for (int u = 0; u < kShortMax; ++u) c[u] = u < d[j] ? spmv_col<HINT>(col, b[j] + u, pcol) : 0;
+    float v[kShortMax];
+#pragma unroll
+    for (int u = 0; u < kShortMax; ++u) v[u] = u < d[j] ? spmv_gather<HINT>(x, c[u], px) : 0.f;
+    float sum = 0.f;
+#pragma unroll
+    for (int u = 0; u < kShortMax; ++u) sum += v[u];
+    y[r] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmv_plan(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                   const int* __restrict__ plan, const float* __restrict__ x,
+                                                   float* __restrict__ y, long long N) {
+  spmv_plan_body<0>(row_ptr, col, plan, x, y, N);
+}
+__global__ void __launch_bounds__(256) k_spmv_plan_h(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                     const int* __restrict__ plan, const float* __restrict__ x,
+                                                     float* __restrict__ y, long long N) {
+  spmv_plan_body<1>(row_ptr, col, plan, x, y, N);
+}
+
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
 __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, RedOut* out,
                                                 long long n) {
@@ -532,8 +689,12 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 }
 
 static const Builtin kHits[] = {
-    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
-    // variants (same results): gathers in registers (sync), L2 policies (tools/spmv_variants.py)
+    // row-class SpMV (product): row_ptr, col, plan (programs/hits_dl.py spmv_plan), x, y, N
+    {"spmv", (const void*)k_spmv_plan, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_plan_h", (const void*)k_spmv_plan_h, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // merge-path SpMV (previous default) and its variants: gathers in
+    // registers (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
+    {"spmv_merge", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_sync", (const void*)k_spmv_sync, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_x0s1", (const void*)k_spmv_x0s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_x1s1", (const void*)k_spmv_x1s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},

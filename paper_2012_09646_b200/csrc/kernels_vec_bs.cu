@@ -108,23 +108,24 @@ __device__ __forceinline__ double bs_log(double x, const BsTables& T) {
   const int j = (hi >> 13) & 127;
   const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
   const double r = fma(m, T.inv[j], -1.0);
-  double p = fma(r, 0.2, -0.25);
-  p = fma(r, p, 1.0 / 3.0);
+  // ln(1+r) to r^4: |r| <= 1/256, the dropped r^5/5 is < 2e-13 absolute
+  double p = fma(r, -0.25, 1.0 / 3.0);
   p = fma(r, p, -0.5);
   p = fma(r, p, 1.0);
   return fma((double)e, kLn2, fma(p, r, T.lninv[j]));
 }
 
-// exp(y) for y <= 0 (0 below -700, where it is < 1e-304)
+// exp(y) for y <= 0 (0 below about -700, where it is < 1e-304); the range
+// test is an integer compare of the high word (keeps it off the FP64 pipe)
 __device__ __forceinline__ double bs_exp(double y, const BsTables& T) {
-  if (y < -700.0) return 0.0;
+  if ((__double2hiint(y) & 0x7fffffff) > 0x4085E000) return 0.0;
   const double t = fma(y, k64_Ln2, kRound);
   const int n = __double2loint(t);
   const double nd = t - kRound;
   double r = fma(nd, -kLn2_64_hi, y);
   r = fma(nd, -kLn2_64_lo, r);
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(r, p, 1.0 / 6.0);
+  // e^r to r^4: |r| <= ln2/128, the dropped r^5/120 is < 4e-14 relative
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
@@ -154,9 +155,8 @@ __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsT
   const double P = D1 * D2;
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(P));
-  double er = fma(-P, y, 1.0);
-  y = fma(y, er, y);
-  er = fma(-P, y, 1.0);
+  // one Newton step on the ~2^-23 hardware estimate: ~2^-46 relative
+  const double er = fma(-P, y, 1.0);
   y = fma(y, er, y);
   const double k1 = D2 * y, k2 = D1 * y;
   double q1 = fma(k1, B5, B4);
@@ -168,8 +168,9 @@ __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsT
   q2 = fma(k2, q2, B2);
   q2 = fma(k2, q2, B1);
   const double p1 = (q1 * k1) * e1, p2 = (q2 * k2) * e2;
-  const double c1 = d1 > 0.0 ? 1.0 - p1 : p1;
-  const double c2 = d2 > 0.0 ? 1.0 - p2 : p2;
+  // CND = d > 0 ? 1 - p : p, with the sign test on the high word (integer pipe)
+  const double c1 = __double2hiint(d1) > 0 ? 1.0 - p1 : p1;
+  const double c2 = __double2hiint(d2) > 0 ? 1.0 - p2 : p2;
   return fma(s, c1, -C.kexp * c2);
 }
 
@@ -287,10 +288,11 @@ BS_ASYNC_VARIANT(k_bs_a5b4, 5, 4)
 BS_ASYNC_VARIANT(k_bs_a7b4, 7, 4)
 BS_ASYNC_VARIANT(k_bs_a5b3, 5, 3)
 
-// default variant: 1 pair per iteration, 4 CTAs/SM (fastest in tools/bs_variants.py)
-__global__ void __launch_bounds__(256, 4) k_bs(const double* __restrict__ s, double* __restrict__ c,
+// default variant: 2 pairs per iteration, 3 CTAs/SM (fastest in tools/bs_variants.py
+// with the 46-op pricing: 51.0 us per 10M options vs 52.8 us for 1 pair / 4 CTAs)
+__global__ void __launch_bounds__(256, 3) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
-  bs_body<1>(s, c, n, r, v, t, k);
+  bs_body<2>(s, c, n, r, v, t, k);
 }
 // tuning variants (same results; bench with tools/bs_variants.py)
 __global__ void __launch_bounds__(256, 3) k_bs_p2b3(const double* __restrict__ s, double* __restrict__ c,

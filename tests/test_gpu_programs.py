@@ -371,10 +371,10 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
 
 
 @pytest.mark.parametrize("variant", ["spmv_sync", "spmv_as1", "spmv_x0s1", "spmv_x1s1"])
-def test_spmv_variants_bitwise(ctx, variant):
-    """SpMV variants (gathers in registers instead of cp.async; other L2
-    policies) give bit-identical y to the default kernel, which the HITS
-    parity tests pin to the oracle."""
+def test_spmv_merge_variants_bitwise(ctx, variant):
+    """The merge-path SpMV (previous default) and its variants (gathers in
+    registers instead of cp.async; other L2 policies) give bit-identical y,
+    and match the oracle."""
     from paper_2012_09646_b200.programs.hits_dl import spmv_out_bytes
     n, e = 300_000, 900_000
     rp, ci, _, _ = synth.powerlaw_graph(11, n, e)
@@ -387,11 +387,41 @@ def test_spmv_variants_bitwise(ctx, variant):
     torch.cuda.synchronize()
     A = [ctx.register_tensor(f"spv_{variant}_{k}", t) for k, t in
          (("rp", t_rp), ("ci", t_ci), ("x", t_x), ("y0", y0), ("y1", y1))]
-    ctx.launch("spmv", grid, 256, A[0], A[1], A[2], A[3], n)
+    ctx.launch("spmv_merge", grid, 256, A[0], A[1], A[2], A[3], n)
     ctx.launch(variant, grid, 256, A[0], A[1], A[2], A[4], n)
     ctx.sync()
     assert torch.equal(y0[:n], y1[:n])
     ok, info = close(y0[:n].cpu().numpy(), ohits.spmv(rp, ci, t_x.cpu().numpy().astype(np.float64)))
+    assert ok, info
+    for a in A:
+        ctx.unregister(a)
+
+
+@pytest.mark.parametrize("n,e,seed", [(1, 0, 1), (1000, 0, 2), (5000, 200_000, 3), (300_000, 900_000, 11),
+                                      (50_000, 2_000_000, 5)])
+def test_spmv_plan_classes(ctx, n, e, seed):
+    """Row-class SpMV (product kernel) on graphs whose rows fall in every
+    class (short, medium, long, multi-chunk hubs), run twice (the arrival
+    counters must reset): matches the oracle and is bit-reproducible."""
+    from paper_2012_09646_b200.programs.hits_dl import spmv_plan
+    rp, ci, _, _ = synth.powerlaw_graph(seed, n, e) if e else (np.zeros(n + 1, np.int32),
+                                                                np.zeros(0, np.int32), None, None)
+    plan, grid, ws = spmv_plan(rp)
+    t_rp = torch.from_numpy(rp).cuda()
+    t_ci = torch.from_numpy(ci if ci.size else np.zeros(1, np.int32)).cuda()
+    t_pl = torch.from_numpy(plan).cuda()
+    t_x = torch.rand(n, device="cuda")
+    y = torch.zeros((4 * n + ws) // 4 + 1, device="cuda")
+    torch.cuda.synchronize()
+    A = [ctx.register_tensor(f"spp_{n}_{e}_{k}", t) for k, t in
+         (("rp", t_rp), ("ci", t_ci), ("pl", t_pl), ("x", t_x), ("y", y))]
+    ctx.launch("spmv", grid, 256, *A, n)
+    ctx.sync()
+    y1 = y[:n].clone()
+    ctx.launch("spmv", grid, 256, *A, n)
+    ctx.sync()
+    assert torch.equal(y1, y[:n])
+    ok, info = close(y1.cpu().numpy(), ohits.spmv(rp, ci, t_x.cpu().numpy().astype(np.float64)))
     assert ok, info
     for a in A:
         ctx.unregister(a)
