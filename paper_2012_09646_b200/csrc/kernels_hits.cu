@@ -488,36 +488,39 @@ SPMV_ASYNC_VARIANT(k_spmv_as1, 1)
 
 
 // ---------------------------------------------------------------------------
-// SpMV by row class (the product kernel, "spmv").
+// SpMV by row class ("spmv_plan"; an alternative to the merge-path kernel,
+// which stays the product kernel: on the HITS graph this one measured 375 us
+// in its first, one-CTA-per-unit form (thresholds 8/4096/8192) and 420-490 us
+// in the form below, vs 362 us for merge-path -- tools/spmv_footprint.py).
 //
 // On the 20M-vertex power-law graph the merge-path kernels above run at
 // ~300 us whatever the gather footprint (tools/spmv_footprint.py: folding
-// the columns into N/64 entries saves only 18%): their per-item work (scans,
-// byte maps, shared-memory round trips) and its latency chains, not memory,
-// set the speed.  Here the rows are split by degree once, when the graph is
+// the columns into N/64 entries saves only 18%).  The idea here: split the
+// rows by degree once, when the graph is
 // registered (a small "plan" array built from row_ptr, spmv_plan() in
 // programs/hits_dl.py), and each class gets the cheapest exact schedule:
-//   * short rows (deg <= 8; ~98% of rows, ~20% of non-zeros): one thread per
-//     row, 4 consecutive rows per thread 256 apart (coalesced row_ptr reads
-//     and y writes), all of a row's column loads then all its gathers in
-//     flight, summed in column order;
-//   * medium rows (8 < deg <= 4096): one warp per row, lanes stride the
-//     row's columns (coalesced), 4 gathers in flight per lane, fixed
-//     xor-tree warp reduction;
-//   * long rows (deg > 4096; ~1000 hubs holding ~45% of the non-zeros):
-//     chunks of 8192 non-zeros, one CTA per chunk (block reduction in a fixed
-//     tree); a hub's chunk sums are added in chunk order by the last chunk to
-//     arrive (atomic arrival count), so results are bit-reproducible.
-// One launch = one DAG vertex: CTA ranges [0, NL) long chunks (heaviest
-// first), then medium rows (8 per CTA), then short-row blocks (1024 rows).
+//   * short rows (deg <= 4; ~95% of rows): one thread per row, 4 rows per
+//     thread 256 apart (coalesced row_ptr reads and y writes), the column
+//     loads of all 4 rows then all their gathers in flight, each row summed
+//     in column order;
+//   * medium rows (4 < deg <= 256): 8 lanes per row, 4 rows per warp, 8
+//     column loads then 8 gathers in flight per lane, fixed xor-tree sum;
+//   * long rows (deg > 256; ~10^4 hubs holding ~half of the non-zeros):
+//     chunks of 2048 non-zeros, one CTA per chunk (8 loads in flight per
+//     thread, block reduction in a fixed tree); a hub's chunk sums are added
+//     in chunk order by the last chunk to arrive (atomic arrival count), so
+//     results are bit-reproducible.
+// One launch = one DAG vertex; a persistent grid walks the units (long
+// chunks first, then medium-row groups, then short-row blocks).
 // Workspace after y's N floats (16-byte aligned): NL chunk sums, NL
 // arrival counters (zero at allocation; reset by the last arriver).
 constexpr int kPlanHeader = 16;    // [0] NL long chunks, [1] NM medium rows, [2] NS short blocks
-constexpr int kShortMax = 8;
-constexpr int kLongMin = 4096;
-constexpr int kLongChunk = 8192;
+constexpr int kShortMax = 4;       // deg <= 4: thread per row
+constexpr int kLongMin = 256;      // deg > 256: CTA per chunk of kLongChunk non-zeros
+constexpr int kLongChunk = 2048;
 constexpr int kShortRowsPerThread = 4;
 constexpr int kShortRowsPerCta = 256 * kShortRowsPerThread;
+constexpr int kMedRowsPerCta = 32;  // 8 warps x 4 groups of 8 lanes
 
 // HINT 1: L2 evict-first for the streamed column indices, evict-last for the gathers
 template <int HINT>
@@ -529,106 +532,148 @@ __device__ __forceinline__ int spmv_col(const int* col, int k, uint64_t pol) {
   return HINT ? ldg_hint(col + k, pol) : __ldg(col + k);
 }
 
+// Persistent: CTA b takes units b, b + G, b + 2G, ... of the unit list
+// [NL long chunks | ceil(NM/32) medium groups | NS short blocks].  Every
+// path issues all of a unit's index loads, then all its gathers, before
+// using any (memory-level parallelism: the chains row_ptr -> col -> x are
+// the cost, not the arithmetic).
 template <int HINT>
 __device__ __forceinline__ void spmv_plan_body(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                const int* __restrict__ plan, const float* __restrict__ x,
                                                float* __restrict__ y, long long N_) {
+  __shared__ float sh[32];
+  __shared__ bool last;
   uint64_t pcol = 0, px = 0;
   if (HINT) {
     pcol = l2_policy_evict_first();
     px = l2_policy_evict_last();
   }
-  const int NL = __ldg(plan + 0), NM = __ldg(plan + 1);
-  const int NMC = (NM + 7) >> 3;
+  const int NL = __ldg(plan + 0), NM = __ldg(plan + 1), NS = __ldg(plan + 2);
   // the plan must have been built with this kernel's class bounds
   if (__ldg(plan + 3) != kShortMax || __ldg(plan + 4) != kLongMin || __ldg(plan + 5) != kLongChunk) __trap();
-  const int bid = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int NMC = (NM + kMedRowsPerCta - 1) / kMedRowsPerCta;
+  const int units = NL + NMC + NS;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int N = (int)N_;
-  if (bid < NL) {
-    // ---- long-row chunk: (row, k_begin, first chunk of the row, chunks of the row)
-    __shared__ float sh[32];
-    const int4 it = __ldg(reinterpret_cast<const int4*>(plan + kPlanHeader) + bid);
-    const int row = it.x, kb = it.y, first = it.z, cnt = it.w;
-    const int ke = min(kb + kLongChunk, __ldg(row_ptr + row + 1));
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k0 = kb + t; k0 < ke; k0 += 4 * 256) {
-      int c[4];
+  uintptr_t wsb = ((uintptr_t)(y + N) + 15) & ~(uintptr_t)15;
+  float* part = reinterpret_cast<float*>(wsb);
+  unsigned* arrive = reinterpret_cast<unsigned*>(part + NL);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    if (u < NL) {
+      // ---- long-row chunk: (row, k_begin, first chunk of the row, chunks of the row)
+      const int4 it = __ldg(reinterpret_cast<const int4*>(plan + kPlanHeader) + u);
+      const int row = it.x, kb = it.y, first = it.z, cnt = it.w;
+      const int ke = min(kb + kLongChunk, __ldg(row_ptr + row + 1));
+      // unconditional loads at clamped (valid) addresses, results selected:
+      // keeps all 8 column loads, then all 8 gathers, in flight
+      int c[kLongChunk / 256];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = k0 + u * 256 < ke ? spmv_col<HINT>(col, k0 + u * 256, pcol) : -1;
+      for (int q = 0; q < kLongChunk / 256; ++q) {
+        const int k = kb + t + q * 256;
+        c[q] = spmv_col<HINT>(col, k < ke ? k : kb, pcol);
+      }
+      float v[kLongChunk / 256];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += c[u] >= 0 ? spmv_gather<HINT>(x, c[u], px) : 0.f;
+      for (int q = 0; q < kLongChunk / 256; ++q) v[q] = spmv_gather<HINT>(x, c[q], px);
+      float a = 0.f;
+#pragma unroll
+      for (int q = 0; q < kLongChunk / 256; ++q) a += kb + t + q * 256 < ke ? v[q] : 0.f;
+      const float sum = block_reduce(a, OpAdd(), sh);
+      if (cnt == 1) {
+        if (t == 0) y[row] = sum;
+        continue;
+      }
+      if (t == 0) {
+        part[u] = sum;
+        __threadfence();
+        last = atomicAdd(arrive + first, 1u) == (unsigned)(cnt - 1);
+      }
+      __syncthreads();
+      if (last && warp == 0) {  // chunk sums of the row in chunk order
+        __threadfence();
+        const volatile float* vp = part;
+        float w = 0.f;
+        for (int i = lane; i < cnt; i += 32) w += vp[first + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0) {
+          y[row] = w;
+          arrive[first] = 0;  // reusable by the next launch
+        }
+      }
+      __syncthreads();  // `last` is rewritten by the next chunk unit
+      continue;
     }
-    const float s = block_reduce((acc[0] + acc[1]) + (acc[2] + acc[3]), OpAdd(), sh);
-    if (cnt == 1) {
-      if (t == 0) y[row] = s;
-      return;
+    if (u < NL + NMC) {
+      // ---- medium rows: 8 lanes per row, 4 rows per warp
+      const int m = (u - NL) * kMedRowsPerCta + warp * 4 + (lane >> 3);
+      const int sub = lane & 7;
+      int kb = 0, ke = 0, row = -1;
+      if (m < NM) {
+        row = __ldg(plan + kPlanHeader + 4 * NL + m);
+        kb = __ldg(row_ptr + row);
+        ke = __ldg(row_ptr + row + 1);
+      }
+      float acc = 0.f;
+      for (int k0 = kb + sub; k0 < ke; k0 += 8 * 8) {
+        int c[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[q] = spmv_col<HINT>(col, k0 + q * 8 < ke ? k0 + q * 8 : kb, pcol);
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = spmv_gather<HINT>(x, c[q], px);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += k0 + q * 8 < ke ? v[q] : 0.f;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sub == 0 && row >= 0) y[row] = acc;
+      continue;
     }
-    uintptr_t base = ((uintptr_t)(y + N) + 15) & ~(uintptr_t)15;
-    float* part = reinterpret_cast<float*>(base);
-    unsigned* arrive = reinterpret_cast<unsigned*>(part + NL);
-    __shared__ bool last;
-    if (t == 0) {
-      part[bid] = s;
-      __threadfence();
-      last = atomicAdd(arrive + first, 1u) == (unsigned)(cnt - 1);
+    // ---- short rows: thread per row, 4 rows per thread 256 apart; all column
+    // loads of the 4 rows, then all their gathers
+    const int r0 = (u - NL - NMC) * kShortRowsPerCta + t;
+    int b[kShortRowsPerThread], d[kShortRowsPerThread];
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j) {
+      const int r = r0 + 256 * j;
+      b[j] = r < N ? __ldg(row_ptr + r) : 0;
+      d[j] = r < N ? __ldg(row_ptr + r + 1) - b[j] : 0;
+      if (d[j] > kShortMax) d[j] = -1;  // medium / long row: summed by its own unit
     }
-    __syncthreads();
-    if (!last || warp != 0) return;
-    __threadfence();
-    const volatile float* vp = part;
-    float v = 0.f;
-    for (int i = lane; i < cnt; i += 32) v += vp[first + i];
+    // the first two non-zeros of every row: unconditional loads at valid
+    // addresses (col[0], x[0] when absent), 8 + 8 in flight per thread; the
+    // rarer third and fourth under a branch
+    int c[kShortRowsPerThread][kShortMax];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) {
-      y[row] = v;
-      arrive[first] = 0;  // reusable by the next launch
+    for (int j = 0; j < kShortRowsPerThread; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) c[j][q] = spmv_col<HINT>(col, q < d[j] ? b[j] + q : 0, pcol);
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j)
+#pragma unroll
+      for (int q = 2; q < kShortMax; ++q) c[j][q] = q < d[j] ? spmv_col<HINT>(col, b[j] + q, pcol) : 0;
+    float v[kShortRowsPerThread][kShortMax];
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) v[j][q] = spmv_gather<HINT>(x, q < d[j] ? c[j][q] : 0, px);
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j)
+#pragma unroll
+      for (int q = 2; q < kShortMax; ++q) v[j][q] = q < d[j] ? spmv_gather<HINT>(x, c[j][q], px) : 0.f;
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) v[j][q] = q < d[j] ? v[j][q] : 0.f;
+#pragma unroll
+    for (int j = 0; j < kShortRowsPerThread; ++j) {
+      const int r = r0 + 256 * j;
+      float sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < kShortMax; ++q) sum += v[j][q];
+      if (r < N && d[j] >= 0) y[r] = sum;
     }
-    return;
-  }
-  if (bid < NL + NMC) {
-    // ---- medium row: one warp per row
-    const int m = (bid - NL) * 8 + warp;
-    if (m >= NM) return;
-    const int row = __ldg(plan + kPlanHeader + 4 * NL + m);
-    const int kb = __ldg(row_ptr + row), ke = __ldg(row_ptr + row + 1);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k0 = kb + lane; k0 < ke; k0 += 4 * 32) {
-      int c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = k0 + u * 32 < ke ? spmv_col<HINT>(col, k0 + u * 32, pcol) : -1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += c[u] >= 0 ? spmv_gather<HINT>(x, c[u], px) : 0.f;
-    }
-    float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) y[row] = v;
-    return;
-  }
-  // ---- short rows: thread per row, 4 rows per thread 256 apart
-  const int r0 = (bid - NL - NMC) * kShortRowsPerCta + t;
-  int b[kShortRowsPerThread], d[kShortRowsPerThread];
-#pragma unroll
-  for (int j = 0; j < kShortRowsPerThread; ++j) {
-    const int r = r0 + 256 * j;
-    b[j] = r < N ? __ldg(row_ptr + r) : 0;
-    d[j] = r < N ? __ldg(row_ptr + r + 1) - b[j] : 0;
-  }
-#pragma unroll
-  for (int j = 0; j < kShortRowsPerThread; ++j) {
-    const int r = r0 + 256 * j;
-    if (r >= N || d[j] > kShortMax) continue;  // medium / long rows are summed above
-    int c[kShortMax];
-#pragma unroll
-    for (int u = 0; u < kShortMax; ++u) c[u] = u < d[j] ? spmv_col<HINT>(col, b[j] + u, pcol) : 0;
-    float v[kShortMax];
-#pragma unroll
-    for (int u = 0; u < kShortMax; ++u) v[u] = u < d[j] ? spmv_gather<HINT>(x, c[u], px) : 0.f;
-    float sum = 0.f;
-#pragma unroll
-    for (int u = 0; u < kShortMax; ++u) sum += v[u];
-    y[r] = sum;
   }
 }
 
@@ -689,12 +734,14 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 }
 
 static const Builtin kHits[] = {
-    // row-class SpMV (product): row_ptr, col, plan (programs/hits_dl.py spmv_plan), x, y, N
-    {"spmv", (const void*)k_spmv_plan, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
-    {"spmv_plan_h", (const void*)k_spmv_plan_h, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
-    // merge-path SpMV (previous default) and its variants: gathers in
-    // registers (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
+    // merge-path SpMV (product) and its variants: gathers in registers
+    // (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
+    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_merge", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // row-class SpMV (measured slower, kept as a tested alternative): row_ptr, col,
+    // plan (programs/hits_dl.py spmv_plan), x, y, N
+    {"spmv_plan", (const void*)k_spmv_plan, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_plan_h", (const void*)k_spmv_plan_h, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_sync", (const void*)k_spmv_sync, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_x0s1", (const void*)k_spmv_x0s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_x1s1", (const void*)k_spmv_x1s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},

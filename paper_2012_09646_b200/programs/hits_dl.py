@@ -18,9 +18,11 @@ SPMV_WARPS = 8           # warps per 256-thread CTA
 
 # Row classes of the planned SpMV (csrc/kernels_hits.cu k_spmv_plan; the
 # kernel traps if a plan was built with other bounds).
-SPMV_SHORT_MAX = 8        # deg <= 8: thread per row
-SPMV_LONG_MIN = 4096      # deg > 4096: chunks of SPMV_LONG_CHUNK non-zeros, CTA per chunk
-SPMV_LONG_CHUNK = 8192
+SPMV_SHORT_MAX = 4        # deg <= 4: thread per row
+SPMV_LONG_MIN = 256       # deg > 256: chunks of SPMV_LONG_CHUNK non-zeros, CTA per chunk
+SPMV_LONG_CHUNK = 2048
+SPMV_MED_ROWS_PER_CTA = 32
+SPMV_CTAS = 148 * 8       # persistent grid
 SPMV_SHORT_ROWS_PER_CTA = 1024
 SPMV_PLAN_HEADER = 16
 
@@ -54,8 +56,8 @@ def spmv_plan(row_ptr):
     header = np.zeros(SPMV_PLAN_HEADER, dtype=np.int64)
     header[:6] = (nl, med.size, ns, SPMV_SHORT_MAX, SPMV_LONG_MIN, SPMV_LONG_CHUNK)
     plan = np.concatenate([header, items.ravel(), med.astype(np.int64)]).astype(np.int32)
-    grid = nl + (med.size + 7) // 8 + ns
-    return plan, max(1, grid), 16 + 8 * nl
+    units = nl + -(-med.size // SPMV_MED_ROWS_PER_CTA) + ns
+    return plan, max(1, min(units, SPMV_CTAS)), 16 + 8 * nl
 
 
 def spmv_out_bytes(n, e):
@@ -83,14 +85,9 @@ class Hits(Program):
             self.alloc(name, max(1, arr.size), torch.int32)
             if arr.size:
                 self.upload(name, arr)
-        plan, self.grid_h, ws_h = spmv_plan(rp)     # h2 = A a1
-        plant, self.grid_a, ws_a = spmv_plan(rpt)   # a2 = A^T h1
-        for name, arr in (("plan", plan), ("plant", plant)):
-            self.alloc(name, arr.size, torch.int32)
-            self.upload(name, arr)
         self.alloc("a1", n, torch.float32, mirror=stream)
         self.alloc("h1", n, torch.float32, mirror=stream)
-        ob = 4 * n + max(ws_a, ws_h)
+        ob, gs = spmv_out_bytes(n, self.e)
         self.alloc("a2", 0, None, nbytes=ob)
         self.alloc("h2", 0, None, nbytes=ob)
         self.alloc_red("an")
@@ -101,8 +98,8 @@ class Hits(Program):
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
         self.it = [
-            P("spmv", self.grid_a, 256, [a["rpt"], a["cit"], a["plant"], a["h1"], a["a2"], n]),  # a2 = A^T h1
-            P("spmv", self.grid_h, 256, [a["rp"], a["ci"], a["plan"], a["a1"], a["h2"], n]),     # h2 = A a1
+            P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
+            P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
             P("l2norm", gr, 256, [a["a2"], a["an"], n]),
             P("l2norm", gr, 256, [a["h2"], a["hn"], n]),
             P("divide", ge, 256, [a["a2"], a["an"], a["a1"], n]),

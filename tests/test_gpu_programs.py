@@ -400,7 +400,7 @@ def test_spmv_merge_variants_bitwise(ctx, variant):
 @pytest.mark.parametrize("n,e,seed", [(1, 0, 1), (1000, 0, 2), (5000, 200_000, 3), (300_000, 900_000, 11),
                                       (50_000, 2_000_000, 5)])
 def test_spmv_plan_classes(ctx, n, e, seed):
-    """Row-class SpMV (product kernel) on graphs whose rows fall in every
+    """Row-class SpMV (alternative kernel) on graphs whose rows fall in every
     class (short, medium, long, multi-chunk hubs), run twice (the arrival
     counters must reset): matches the oracle and is bit-reproducible."""
     from paper_2012_09646_b200.programs.hits_dl import spmv_plan
@@ -415,10 +415,10 @@ def test_spmv_plan_classes(ctx, n, e, seed):
     torch.cuda.synchronize()
     A = [ctx.register_tensor(f"spp_{n}_{e}_{k}", t) for k, t in
          (("rp", t_rp), ("ci", t_ci), ("pl", t_pl), ("x", t_x), ("y", y))]
-    ctx.launch("spmv", grid, 256, *A, n)
+    ctx.launch("spmv_plan", grid, 256, *A, n)
     ctx.sync()
     y1 = y[:n].clone()
-    ctx.launch("spmv", grid, 256, *A, n)
+    ctx.launch("spmv_plan", grid, 256, *A, n)
     ctx.sync()
     assert torch.equal(y1, y[:n])
     ok, info = close(y1.cpu().numpy(), ohits.spmv(rp, ci, t_x.cpu().numpy().astype(np.float64)))

@@ -36,13 +36,16 @@ def main():
     A_pl = ctx.register_tensor("plan", torch.from_numpy(plan).cuda())
     st = torch.cuda.Stream()
     out = {}
-    for f in (1, 2, 4, 64):
+    for f in (1, 64):
         t_ci = torch.from_numpy((ci % (n // f)).astype(np.int32)).cuda()
         torch.cuda.synchronize()
         A_ci = ctx.register_tensor(f"ci{f}", t_ci)
-        for kname in ("spmv_merge", "spmv", "spmv_plan_h"):
+        units = int(plan[0]) + -(-int(plan[1]) // 32) + int(plan[2])
+        for kname in ("spmv_merge", "spmv_plan", "spmv_np"):
             if kname == "spmv_merge":
                 L = ctx.prepare(kname, grid, 256, [A_rp, A_ci, A_x, A_y, n])
+            elif kname == "spmv_np":  # same kernel, one CTA per unit (non-persistent)
+                L = ctx.prepare("spmv_plan", units, 256, [A_rp, A_ci, A_pl, A_x, A_y, n])
             else:
                 L = ctx.prepare(kname, pgrid, 256, [A_rp, A_ci, A_pl, A_x, A_y, n])
             for _ in range(3):

@@ -28,10 +28,21 @@ def main():
     st = torch.cuda.Stream()
     out = {}
     ref = None
-    for name in ("spmv", "spmv_merge", "spmv_as1", "spmv_sync", "spmv_x0s1", "spmv_x1s1"):
-        if name == "spmv":  # row-class plan kernel (product)
-            Ls = [ctx.prepare(name, p.grid_a, 256, [a["rpt"], a["cit"], a["plant"], a["h1"], a["a2"], n]),
-                  ctx.prepare(name, p.grid_h, 256, [a["rp"], a["ci"], a["plan"], a["a1"], a["h2"], n])]
+    from paper_2012_09646_b200.programs.hits_dl import spmv_plan
+    plan, pg, ws = spmv_plan(p.csr[0])
+    plant, pgt, wst = spmv_plan(p.csr[2])
+    a = dict(a)
+    a["plan"] = ctx.register_tensor("plan", torch.from_numpy(plan).cuda())
+    a["plant"] = ctx.register_tensor("plant", torch.from_numpy(plant).cuda())
+    # the plan kernel's workspace (chunk sums) is larger than merge-path's: own outputs
+    ya = torch.zeros((4 * n + max(ws, wst)) // 4 + 1, device="cuda")
+    yh = torch.zeros_like(ya)
+    a["a2p"] = ctx.register_tensor("a2p", ya)
+    a["h2p"] = ctx.register_tensor("h2p", yh)
+    for name in ("spmv", "spmv_plan", "spmv_as1", "spmv_sync", "spmv_x0s1", "spmv_x1s1"):
+        if name == "spmv_plan":  # row-class kernel (alternative; needs the plan workspace in y)
+            Ls = [ctx.prepare(name, pgt, 256, [a["rpt"], a["cit"], a["plant"], a["h1"], a["a2p"], n]),
+                  ctx.prepare(name, pg, 256, [a["rp"], a["ci"], a["plan"], a["a1"], a["h2p"], n])]
         else:
             Ls = [ctx.prepare(name, grid, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),
                   ctx.prepare(name, grid, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n])]
@@ -47,7 +58,7 @@ def main():
             e1.record()
         e1.synchronize()
         us = e0.elapsed_time(e1) / 20 * 1e3
-        y = p.vec("a2").clone()
+        y = ya[:n].clone() if name == "spmv_plan" else p.vec("a2").clone()
         if ref is None:
             ref = y
         out[name] = {"us_per_launch": us, "bitwise_same_as_spmv": bool(torch.equal(ref, y)),
