@@ -287,13 +287,22 @@ def main():
     prog.load_inputs(0)
     dom = DOMINANT[name]
     ctx.profile(dom, False)
-    for _ in range(W):
-        prog.run()
-    torch.cuda.synchronize()
-    ctx.stats_reset()
+    # nvidia-smi samples every 100 ms and takes ~0.2 s to start: the sampler
+    # runs from before the warm-up through the timed region (same load), so
+    # short regions (B&S: ~5 ms) still get clock samples
     with Clocks(local) as clk:
+        time.sleep(0.3)
+        for _ in range(W):
+            prog.run()
+        torch.cuda.synchronize()
+        ctx.stats_reset()
         ms = time_steps(prog.run, K, 0, dist)
-    st = ctx.stats()
+        st = ctx.stats()  # launches etc. of exactly the K timed steps
+        # keep the GPU under the same load until the sampler has seen it
+        t_end = time.perf_counter() + 0.3
+        while time.perf_counter() < t_end:
+            prog.run()
+        torch.cuda.synchronize()
     value = replicas.job_ms_per_dag(ms, K, world)
     # roofline: the same K steps again with the dominant kernel's launches
     # bracketed by CUDA events on their own launch streams (kept out of the

@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc4(const float* __rest
 //     the split (version 2 ran one warp per SM sub-partition);
 //   * two A buffers and two accumulators, each with its own mbarrier, so
 //     the A tiles of tile k+1 are written while the MMAs of tile k run;
+//   * the 27 MMAs of a tile feed three independent TMEM accumulators
+//     (hi*hi, lo*hi, hi*lo), issued interleaved, summed in the epilogue --
+//     one accumulator would chain 27 dependent N=16 MMAs;
 //   * TF32 split by truncation: hi = x with the low 13 mantissa bits
 //     cleared (exact in TF32), lo = x - hi (exact in fp32; the tensor core
 //     reads its top 10 mantissa bits, error <= 2^-21 |x|), 2 ops per element.
@@ -447,6 +450,7 @@ constexpr int kC3Threads = 384;
 constexpr int kC3Stages = 3;
 constexpr int kC3ABuf = 2 * kTcTaps * kTcATile;  // hi + lo tiles of one tile
 constexpr int kC3Smem = 2 * kTcTaps * kTcBTile + kC3Stages * kC2Stage + 2 * kC3ABuf + 64;
+constexpr uint32_t kC3Cols = 128;  // TMEM: 2 buffers x 3 partial accumulators x 16 columns
 
 __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __restrict__ in,
                                                              const float* __restrict__ w,
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(kC2Cols));
+                 "n"(kC3Cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -506,23 +510,28 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
     }
   };
   // accumulator `buf` of tile `tl` -> ReLU -> out; warps 0-3 (TMEM lane quarter = warp)
+  // (three partial accumulators: hi*hi, lo*hi, hi*lo; summed here)
   auto drain = [&](long long tl, int buf) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(tmem + ((uint32_t)(warp * 32) << 16) + 16 * buf));
+    uint32_t r[3][16];
+#pragma unroll
+    for (int part = 0; part < 3; ++part)
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[part][0]), "=r"(r[part][1]), "=r"(r[part][2]), "=r"(r[part][3]), "=r"(r[part][4]),
+            "=r"(r[part][5]), "=r"(r[part][6]), "=r"(r[part][7]), "=r"(r[part][8]), "=r"(r[part][9]),
+            "=r"(r[part][10]), "=r"(r[part][11]), "=r"(r[part][12]), "=r"(r[part][13]), "=r"(r[part][14]),
+            "=r"(r[part][15])
+          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + 48 * buf + 16 * part));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float o[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      o[c] = fmaxf(__uint_as_float(r[0][c]) + (__uint_as_float(r[1][c]) + __uint_as_float(r[2][c])), 0.f);
     const int pp = (int)(tl / tpr), q = (int)(tl % tpr) * 128 + pix;
     if (q < W3) {
       float4* dst = reinterpret_cast<float4*>(out + ((size_t)pp * W3 + q) * 16);
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        dst[c] = make_float4(fmaxf(__uint_as_float(r[4 * c]), 0.f), fmaxf(__uint_as_float(r[4 * c + 1]), 0.f),
-                             fmaxf(__uint_as_float(r[4 * c + 2]), 0.f),
-                             fmaxf(__uint_as_float(r[4 * c + 3]), 0.f));
+      for (int c = 0; c < 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
     }
   };
   const long long first = blockIdx.x, step = gridDim.x;
@@ -572,7 +581,9 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (t == 0) {
-      const uint32_t d = tmem + 16 * b;
+      // three independent accumulation chains (hi*hi, lo*hi, hi*lo), issued
+      // interleaved so consecutive MMAs do not wait on each other's sums
+      const uint32_t d = tmem + 48 * b;
       uint32_t acc = 0;
 #pragma unroll
       for (int tap = 0; tap < kTcTaps; ++tap) {
@@ -581,9 +592,9 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
         const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
         const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
         tc_mma(d, dah, dbh, acc);
+        tc_mma(d + 16, dal, dbh, acc);
+        tc_mma(d + 32, dah, dbl, acc);
         acc = 1;
-        tc_mma(d, dal, dbh, 1);
-        tc_mma(d, dah, dbl, 1);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(mbar + b))
@@ -610,7 +621,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC2Cols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC3Cols));
 }
 
 static const Builtin kConvTc[] = {

@@ -15,9 +15,8 @@ namespace dagrt {
 // column pairs (no integer division).  Inputs: per tap row one float4
 // (columns 4j..4j+3) plus column 4j-1 from the neighbouring lane (shuffle);
 // outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
-__global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
-                                               const float* __restrict__ w,
-                                               float* __restrict__ out, int H, int W) {
+__device__ __forceinline__ void conv1_body(const float* __restrict__ x, const float* __restrict__ w,
+                                           float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
   const int pairs = (W1 + 1) / 2;
   // weights in shared memory (uniform 128-bit broadcast reads): keeping all
@@ -93,6 +92,20 @@ __global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x,
       dst[3] = make_float4(o[1][4], o[1][5], o[1][6], o[1][7]);
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x, const float* __restrict__ w,
+                                               float* __restrict__ out, int H, int W) {
+  conv1_body(x, w, out, H, W);
+}
+// occupancy variants (same results): registers capped for 3 / 4 CTAs per SM
+__global__ void __launch_bounds__(256, 3) k_conv1_b3(const float* __restrict__ x, const float* __restrict__ w,
+                                                     float* __restrict__ out, int H, int W) {
+  conv1_body(x, w, out, H, W);
+}
+__global__ void __launch_bounds__(256, 4) k_conv1_b4(const float* __restrict__ x, const float* __restrict__ w,
+                                                     float* __restrict__ out, int H, int W) {
+  conv1_body(x, w, out, H, W);
 }
 
 // POOL: 2x2 mean, stride 2, 8 channels (two float4 per pixel).
@@ -239,6 +252,8 @@ __global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
 
 static const Builtin kDl[] = {
     {"conv1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_b3", (const void*)k_conv1_b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_b4", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
     // CUDA-core variant of the second convolution (the tcgen05 one is "conv2")
     {"conv2_ffma", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},

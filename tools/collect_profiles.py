@@ -79,6 +79,22 @@ def main(tag):
     if traffic:  # read by bench.py for roofline.traffic (DRAM bytes per launch, ncu)
         with open(os.path.join(PROF, f"{tag}_traffic.json"), "w") as f:
             json.dump(traffic, f, indent=1, sort_keys=True)
+    # the default bench line, the reference arm, the B&S FP64 op count, the GPU test result
+    extra = [("bench_default.json", "bench_default.json"), ("bench_reference.json", "bench_reference.json"),
+             ("fp64_bs.csv", "fp64_bs.csv"), ("smoke.log", "smoke.log")]
+    for src, dst in extra:
+        sp = os.path.join(OUT, src)
+        if os.path.exists(sp):
+            shutil.copy(sp, os.path.join(PROF, f"{tag}_{dst}"))
+    pl = os.path.join(OUT, "pytest_gpu.log")
+    if os.path.exists(pl):
+        tail = open(pl).read().strip().splitlines()[-3:]
+        with open(os.path.join(PROF, f"{tag}_pytest_gpu.txt"), "w") as f:
+            f.write("\n".join(tail) + "\n")
+        lines.append("## pytest -m gpu\n")
+        lines.append("```")
+        lines.extend(tail)
+        lines.append("```\n")
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))

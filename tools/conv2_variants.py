@@ -47,6 +47,16 @@ def main():
     for i, name in ((0, "conv1"), (2, "pool")):
         us = timeit(p.L[i])
         out[name] = {"us": us, "GBps": kb[name + "_x"] / us / 1e3}
+    c1ref = p.t["c1x"].clone()
+    L0 = p.L[0]
+    for v in ("conv1_b3", "conv1_b4"):
+        for rows_per in (8, 16):
+            g = (L0.grid.x, max(1, min(h1, -(-rows_per * 148 // L0.grid.x))))
+            L = ctx.prepare(v, g, 256, [p.a["x"], p.a["w1"], p.a["c1x"], a.h, a.h])
+            us = timeit(L)
+            torch.cuda.synchronize()
+            out[f"{v}_r{rows_per}"] = {"us": us, "GBps": kb["conv1_x"] / us / 1e3,
+                                      "same": bool(torch.equal(c1ref, p.t["c1x"]))}
     for v in a.variants.split(","):
         o = torch.full((h3 * w3 * 16,), -1.0, device="cuda")
         torch.cuda.synchronize()
