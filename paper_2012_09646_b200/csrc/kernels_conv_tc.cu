@@ -625,8 +625,15 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
 }
 
 static const Builtin kConvTc[] = {
-    // launch: 148 persistent CTAs of 384 threads, kC3Smem bytes of dynamic shared memory
-    {"conv2", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+    // product: the first version (A from per-thread gathers, next tile's loads
+    // in flight during the MMAs, 2 CTAs/SM): 441 us per branch on the full DL
+    // shapes vs 580 (tc4) / 656 (tc5) us for the cp.async-ring versions, whose
+    // loop-top barrier waits on the ring dominate (tools/conv2_variants.py,
+    // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
+    {"conv2", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kTcSmem},
+    // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
+    {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC3Smem},
     // version 2: 128 threads, one A buffer (148 CTAs, kC2Smem)
     {"conv2_tc4", (const void*)k_conv2_tc4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,

@@ -251,9 +251,11 @@ __global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
 }
 
 static const Builtin kDl[] = {
-    {"conv1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    // product: registers capped for 4 CTAs/SM (687 us vs 710 us uncapped, tools/conv2_variants.py)
+    {"conv1", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b3", (const void*)k_conv1_b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_b1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
     // CUDA-core variant of the second convolution (the tcgen05 one is "conv2")
     {"conv2_ffma", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},

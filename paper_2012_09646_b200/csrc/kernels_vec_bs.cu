@@ -85,11 +85,23 @@ struct BsTables {
   double exp2j[64];   // 2^(j/64)
 };
 
-constexpr double kLn2 = 0.6931471805599453;
-constexpr double kLn2_64_hi = 0.01083042469326756;      // ln2/64, 32 significant bits
-constexpr double kLn2_64_lo = 2.9815858269852933e-12;   // ln2/64 - hi
-constexpr double k64_Ln2 = 92.33248261689366;
-constexpr double kRound = 6755399441055744.0;           // 1.5 * 2^52
+constexpr double kRound = 6755399441055744.0;           // 1.5 * 2^52 (low word 0: an immediate)
+// Constants whose low 32 bits are not zero live in the constant bank: DFMA
+// and DMUL read a c[][] operand directly, whereas a literal would be
+// rematerialised with two register moves per use inside the loop.
+enum { kcThird, kcLn2, kc64Ln2, kcNegLn2_64Hi, kcNegLn2_64Lo, kc24th, kc6th, kcB1, kcB2, kcB3, kcB4, kcB5,
+       kcA, kcCount };
+__constant__ double kBsK[kcCount] = {
+    1.0 / 3.0,
+    0.6931471805599453,       // ln 2
+    92.33248261689366,        // 64 / ln 2
+    -0.01083042469326756,     // -(ln2/64), 32 significant bits
+    -2.9815858269852933e-12,  // -(ln2/64 - hi)
+    1.0 / 24.0,
+    1.0 / 6.0,
+    // A&S 26.2.17 coefficients times 1/sqrt(2 pi), and its p = 0.2316419
+    0.1274147958962986, -0.1422483682996393, 0.7107068706716199, -0.7265760130580615,
+    0.5307027142649737, 0.2316419};
 
 __device__ __forceinline__ void bs_tables_init(BsTables& T) {
   for (int j = threadIdx.x; j < 128; j += blockDim.x) {
@@ -109,23 +121,23 @@ __device__ __forceinline__ double bs_log(double x, const BsTables& T) {
   const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
   const double r = fma(m, T.inv[j], -1.0);
   // ln(1+r) to r^4: |r| <= 1/256, the dropped r^5/5 is < 2e-13 absolute
-  double p = fma(r, -0.25, 1.0 / 3.0);
+  double p = fma(r, -0.25, kBsK[kcThird]);
   p = fma(r, p, -0.5);
   p = fma(r, p, 1.0);
-  return fma((double)e, kLn2, fma(p, r, T.lninv[j]));
+  return fma((double)e, kBsK[kcLn2], fma(p, r, T.lninv[j]));
 }
 
 // exp(y) for y <= 0 (0 below about -700, where it is < 1e-304); the range
 // test is an integer compare of the high word (keeps it off the FP64 pipe)
 __device__ __forceinline__ double bs_exp(double y, const BsTables& T) {
   if ((__double2hiint(y) & 0x7fffffff) > 0x4085E000) return 0.0;
-  const double t = fma(y, k64_Ln2, kRound);
+  const double t = fma(y, kBsK[kc64Ln2], kRound);
   const int n = __double2loint(t);
   const double nd = t - kRound;
-  double r = fma(nd, -kLn2_64_hi, y);
-  r = fma(nd, -kLn2_64_lo, r);
+  double r = fma(nd, kBsK[kcNegLn2_64Hi], y);
+  r = fma(nd, kBsK[kcNegLn2_64Lo], r);
   // e^r to r^4: |r| <= ln2/128, the dropped r^5/120 is < 4e-14 relative
-  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  double p = fma(r, kBsK[kc24th], kBsK[kc6th]);
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
@@ -143,9 +155,8 @@ struct BsConst {
 };
 
 __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsTables& T) {
-  // A&S 26.2.17 coefficients times 1/sqrt(2 pi)
-  const double B1 = 0.1274147958962986, B2 = -0.1422483682996393, B3 = 0.7107068706716199,
-               B4 = -0.7265760130580615, B5 = 0.5307027142649737, A = 0.2316419;
+  const double B1 = kBsK[kcB1], B2 = kBsK[kcB2], B3 = kBsK[kcB3], B4 = kBsK[kcB4], B5 = kBsK[kcB5],
+               A = kBsK[kcA];
   const double L = bs_log(s * C.inv_k, T);
   const double d1 = fma(L, C.inv_vst, C.mu_s);
   const double d2 = d1 - C.vst;

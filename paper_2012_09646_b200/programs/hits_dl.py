@@ -8,9 +8,10 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
-CONV2_TC_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # csrc/kernels_conv_tc.cu kC3Smem
-CONV2_TC_THREADS = 384                            # k_conv2_tc5: 3 groups of 128
-G2TC = 148                                        # persistent tcgen05 CTAs (1 per SM)
+CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64    # csrc/kernels_conv_tc.cu kTcSmem ("conv2" = k_conv2_tc)
+CONV2_TC_THREADS = 128
+G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
+CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)
 SPMV_WARPS = 8           # warps per 256-thread CTA
@@ -187,7 +188,7 @@ class DeepLearning(Program):
         P = ctx.prepare
         # conv grids: x = column pairs / 256, y = output rows (<= 65535, kernels loop)
         x1b = max(1, -(-((w1 + 1) // 2) // 256))
-        g1 = (x1b, max(1, min(h1, -(-8 * SMS // x1b))))  # blocks loop over output rows
+        g1 = (x1b, max(1, min(h1, -(-16 * SMS // x1b))))  # blocks loop over output rows
         gp = grid_1d(h2 * w2 * 2, 256)
         x2b = max(1, -(-((w3 + 1) // 2) // 256))
         g2 = (x2b, max(1, min(h3, -(-8 * SMS // x2b))))

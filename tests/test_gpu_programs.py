@@ -341,11 +341,11 @@ def test_dl_full_size_sampled(ctx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1"])
+@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc4", "conv2_tc5"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
 def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
-    """The other conv2 kernels (CUDA-core FFMA; first tcgen05 version with A
-    from shared memory) against the oracle too."""
+    """The other conv2 kernels (CUDA-core FFMA; the tcgen05 versions with a
+    cp.async ring) against the oracle too."""
     p = DeepLearning(ctx, h=h, w=w)
     p.load_inputs(1)
     p.run()
@@ -359,6 +359,12 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     elif variant == "conv2_tc1":
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+    elif variant == "conv2_tc4":
+        ctx.launch(variant, 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
+                   smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
+    else:
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_TC5_SMEM
+        ctx.launch(variant, 148, 384, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TC5_SMEM)
     ctx.sync()
     spec = synth.spec_dl(h, w)
     w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)

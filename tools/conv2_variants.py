@@ -15,12 +15,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--h", type=int, default=16384)
-    ap.add_argument("--variants", default="conv2_ffma,conv2_tc1,conv2_tc4,conv2")
+    ap.add_argument("--variants", default="conv2_ffma,conv2_tc1,conv2_tc4,conv2_tc5,conv2")
     a = ap.parse_args()
     import torch
     from paper_2012_09646_b200 import dagrt as D
     from paper_2012_09646_b200.programs import DeepLearning
-    from paper_2012_09646_b200.programs.hits_dl import CONV2_TC_SMEM, CONV2_TC_THREADS, G2TC
+    from paper_2012_09646_b200.programs.hits_dl import CONV2_TC5_SMEM, CONV2_TC_SMEM, CONV2_TC_THREADS, G2TC
     ctx = D.Context(device=0)
     p = DeepLearning(ctx, h=a.h, w=a.h)
     p.load_inputs(0)
@@ -66,6 +66,8 @@ def main():
             L = ctx.prepare(v, ((w3 + 1) // 2 // 256 + 1, min(h3, 65535)), 256, args)
         elif v == "conv2_tc1":
             L = ctx.prepare(v, 2 * 148, 128, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+        elif v == "conv2_tc5":
+            L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
             L = ctx.prepare(v, G2TC, 128, args, smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
         else:
