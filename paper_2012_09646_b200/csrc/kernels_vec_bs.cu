@@ -299,11 +299,12 @@ BS_ASYNC_VARIANT(k_bs_a5b4, 5, 4)
 BS_ASYNC_VARIANT(k_bs_a7b4, 7, 4)
 BS_ASYNC_VARIANT(k_bs_a5b3, 5, 3)
 
-// default variant: 2 pairs per iteration, 3 CTAs/SM (fastest in tools/bs_variants.py
-// with the 46-op pricing: 51.0 us per 10M options vs 52.8 us for 1 pair / 4 CTAs)
-__global__ void __launch_bounds__(256, 3) k_bs(const double* __restrict__ s, double* __restrict__ c,
+// default variant: 4 pairs per iteration, 2 CTAs/SM, one wave (fastest in
+// tools/bs_variants.py with the 46-op pricing: 49.7 us per 10M options vs 51.3
+// for 2 pairs / 3 CTAs and 52.8 for 1 pair / 4 CTAs)
+__global__ void __launch_bounds__(256, 2) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
-  bs_body<2>(s, c, n, r, v, t, k);
+  bs_body<4>(s, c, n, r, v, t, k);
 }
 // tuning variants (same results; bench with tools/bs_variants.py)
 __global__ void __launch_bounds__(256, 3) k_bs_p2b3(const double* __restrict__ s, double* __restrict__ c,

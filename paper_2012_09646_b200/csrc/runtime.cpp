@@ -257,10 +257,21 @@ struct DeferBackend final : Backend {
     ops.push_back(o);
     return cudaSuccess;
   }
+  // A D2H copy into pinned memory (a host mirror or the context's bounce
+  // buffer) joins the batch: the host access that issued it synchronises
+  // right after, so the whole batch -- kernels, waits and the read-back --
+  // replays as ONE graph launch, like a hand-written graph with a memcpy
+  // node.  Other D2H copies (possibly pageable destinations) are issued
+  // directly after the batch.
+  bool d2h_pinned = false;
+  cudaError_t copy_d2h_pinned(void* dst, const void* src, size_t n, void* s) {
+    d2h_pinned = true;
+    cudaError_t e = copy_async(dst, src, n, cudaMemcpyDeviceToHost, s);
+    d2h_pinned = false;
+    return e;
+  }
   cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, void* s) override {
-    // D2H copies belong to host accesses, which synchronise right after:
-    // a one-node graph would only add launch latency, so issue them directly
-    if (!enabled || k == cudaMemcpyDeviceToHost) {
+    if (!enabled || (k == cudaMemcpyDeviceToHost && !d2h_pinned)) {
       if (cudaError_t e = flush()) return e;
       return in->copy_async(dst, src, n, k, s);
     }
@@ -822,7 +833,9 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order
     c->rec_v.push_back(dagrt_vertex_info{vid, 1, 0, -1, array_handle(c, a)});
   for (uint32_t p : c->scratch_parents) {
     trace_op(c, DAGRT_OP_EVENT_SYNC, -1, p, 0, 0);
-    if (order) CK(c->be->wait_now(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
+    // (with the graph cache on, the wait joins the pending batch with the copy)
+    if (order && c->be->active()) CK(c->be->wait(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
+    else if (order) CK(c->be->wait_now(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
     else CK(c->be->event_sync(c->vertices[p].ev), "cudaEventSynchronize");
     c->st.host_syncs++;
   }
@@ -846,8 +859,12 @@ dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   if (bounce && !c->bounce) CK(cudaMallocHost(&c->bounce, kBounceBytes), "cudaMallocHost bounce");
   void* t0;
   if (dagrt_status st_ = tl_begin(c, c->d2h_stream, &t0)) return st_;
-  CK(c->be->copy_async(bounce ? c->bounce : dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream),
-     "cudaMemcpyAsync D2H");
+  const bool pinned = bounce || (a->host && (char*)dst >= a->host && (char*)dst < a->host + a->bytes);
+  if (pinned) {
+    CK(c->be->copy_d2h_pinned(bounce ? c->bounce : dst, a->dev + off, n, c->d2h_stream), "cudaMemcpyAsync D2H");
+  } else {
+    CK(c->be->copy_async(dst, a->dev + off, n, cudaMemcpyDeviceToHost, c->d2h_stream), "cudaMemcpyAsync D2H");
+  }
   if (dagrt_status st_ = tl_end(c, c->d2h_stream, t0, 2, -5, -1, array_index(c, a), n)) return st_;
   CK(c->be->stream_sync(c->d2h_stream), "cudaStreamSynchronize D2H");
   c->st.host_syncs++;

@@ -72,7 +72,7 @@ class BlackScholes(Program):
             self.alloc(f"c{i}", n, torch.float64, mirror=stream)
         self.inputs = [f"s{i}" for i in range(nvec)]
         self.sinks = [f"c{i}" for i in range(nvec)]
-        g = grid_1d(n, 256, 4, waves=6)  # 2 waves of the 3 resident CTAs/SM
+        g = grid_1d(n, 256, 8, waves=2)  # one wave of the 2 resident CTAs/SM
         self.L = [ctx.prepare("bs", g, 256, [self.a[f"s{i}"], self.a[f"c{i}"], n,
                                               BS_R, BS_V, BS_T, BS_K]) for i in range(nvec)]
 
