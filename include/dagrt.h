@@ -156,6 +156,19 @@ const char* dagrt_builtin_signature(int32_t i);
 dagrt_status dagrt_launch(dagrt_ctx ctx, dagrt_kernel k, dagrt_dim3 grid, dagrt_dim3 block,
                           uint32_t smem, const dagrt_arg* args, int32_t nargs);
 
+/* The same call with its arguments in one caller-owned descriptor (read
+ * during the call only): identical semantics to dagrt_launch, for bindings
+ * whose per-argument marshalling cost is comparable to the launch itself
+ * (one pointer instead of seven arguments per call from Python). */
+typedef struct {
+  dagrt_kernel kernel;
+  dagrt_dim3 grid, block;
+  uint32_t smem;
+  int32_t nargs;
+  const dagrt_arg* args;
+} dagrt_launch_desc;
+dagrt_status dagrt_launch_prepared(dagrt_ctx ctx, const dagrt_launch_desc* d);
+
 /* ---------------------------------------------------------------- host access */
 
 /* Host read of bytes [off, off+bytes) of array a into dst (L505-516): if the
@@ -297,6 +310,14 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx ctx, dagrt_graph g, dagrt_kernel k
  * dir 0 = H2D, 1 = D2H, bytes [off, off+bytes). */
 dagrt_status dagrt_graph_add_copy(dagrt_ctx ctx, dagrt_graph g, dagrt_array a, int32_t dir,
                                   size_t off, size_t bytes, const uint32_t* deps, int32_t ndeps,
+                                  uint32_t* node);
+/* D2H copy node from array a's device bytes [off, off+bytes) into
+ * caller-owned PINNED host memory dst (which must stay valid while the graph
+ * exists): the graph's equivalent of a host read of a sink (resident mode
+ * reads one element per sink), so that every compared schedule
+ * ends with the host holding the outputs. */
+dagrt_status dagrt_graph_add_read(dagrt_ctx ctx, dagrt_graph g, dagrt_array a, size_t off,
+                                  size_t bytes, void* dst, const uint32_t* deps, int32_t ndeps,
                                   uint32_t* node);
 dagrt_status dagrt_graph_instantiate(dagrt_ctx ctx, dagrt_graph g);
 /* Launch the instantiated graph on the context's graph stream and wait for it. */

@@ -20,6 +20,10 @@ int register_builtins(const Builtin* table, int n);  // returns n
 int builtin_count();
 const Builtin* builtin_at(int i);
 
+// Scheduler-internal kernel (kernels_runtime.cu): small host reads through
+// mapped pinned memory; args (src, dst_mapped_dev, n, flag_dev, seq).
+const void* read_mapped_kernel();
+
 }  // namespace dagrt
 
 #define DAGRT_REGISTER_BUILTINS(tbl) \

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -87,10 +88,46 @@ struct CudaBackend final : Backend {
     return cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b);
   }
   cudaError_t event_destroy(void* e) override { return cudaEventDestroy((cudaEvent_t)e); }
+  // Kernels are enqueued through the driver's cuLaunchKernel on the kernel's
+  // CUfunction (resolved once per host stub): measured 2.4 us per launch on
+  // the B200 box's host vs 3.0 us for cudaLaunchKernel, which re-resolves the
+  // stub on every call (tools/launch_cost.cu).  The entry point is fetched
+  // from the runtime, so the library has no link-time dependency on libcuda.
+  typedef int (*LaunchFn)(void* f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by,
+                          unsigned bz, unsigned smem, void* stream, void** params, void** extra);
+  LaunchFn cu_launch = nullptr;
+  bool cu_tried = false;
+  std::vector<std::pair<const void*, void*>> funcs;  // host stub -> CUfunction
+  void* cufunc(const void* fn) {
+    for (auto& p : funcs)
+      if (p.first == fn) return p.second;
+    cudaFunction_t f = nullptr;
+    if (cudaGetFuncBySymbol(&f, fn) != cudaSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    funcs.push_back({fn, (void*)f});
+    return (void*)f;
+  }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
                      bool coop, int) override {
     if (coop) return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
-    return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
+    if (!cu_tried) {
+      cu_tried = true;
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        cu_launch = (LaunchFn)p;
+      else
+        cudaGetLastError();
+    }
+    void* f = cu_launch ? cufunc(fn) : nullptr;
+    if (!f) return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
+    int r = cu_launch(f, g.x, g.y, g.z, b.x, b.y, b.z, (unsigned)smem, s, args, nullptr);
+    // CUresult and cudaError_t share their numeric codes for launch failures
+    // (invalid value 1, out of memory 2, invalid image 200, handle 400, 7xx)
+    return (cudaError_t)r;
   }
   cudaError_t record(void* e, void* s) override {
     return cudaEventRecord((cudaEvent_t)e, (cudaStream_t)s);
@@ -581,6 +618,9 @@ struct dagrt_ctx_s {
   void* graph_stream = nullptr;
   void* serial_stream = nullptr;
   void* bounce = nullptr;              // pinned staging for small D2H reads into caller memory
+  void* mapped = nullptr;              // mapped pinned memory for small host reads (+ flag word)
+  void* mapped_dev = nullptr;          // its device address
+  uint32_t read_seq = 0;
   std::vector<dagrt_graph_s*> graphs;
   std::vector<ProfRec> prof;           // timed launches awaiting collection
   bool timeline = false;
@@ -845,6 +885,45 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order
 }
 
 constexpr size_t kBounceBytes = 64 << 10;
+constexpr size_t kMappedReadBytes = 4096;
+
+// Small read through mapped pinned memory: a one-CTA kernel on the D2H stream
+// (ordered after the producers by the waits host_sync_parents put there)
+// copies the bytes and publishes a sequence number; the host spins on it,
+// polling the stream every 256 spins so a failed or finished stream is seen.
+dagrt_status d2h_mapped(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
+  if (!c->mapped) {
+    CK(cudaHostAlloc(&c->mapped, kMappedReadBytes + 64, cudaHostAllocMapped), "cudaHostAlloc mapped");
+    CK(cudaHostGetDevicePointer(&c->mapped_dev, c->mapped, 0), "cudaHostGetDevicePointer");
+  }
+  volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>((char*)c->mapped + kMappedReadBytes);
+  uint32_t seq = ++c->read_seq;
+  if (seq == 0) seq = c->read_seq = 1;
+  const char* src = a->dev + off;
+  char* ddst = (char*)c->mapped_dev;
+  uint32_t nn = (uint32_t)n;
+  uint32_t* dflag = reinterpret_cast<uint32_t*>(ddst + kMappedReadBytes);
+  void* argv[] = {&src, &ddst, &nn, &dflag, &seq};
+  void* t0;
+  if (dagrt_status st_ = tl_begin(c, c->d2h_stream, &t0)) return st_;
+  CK(c->be->launch(read_mapped_kernel(), dim3(1), dim3(256), argv, 0, c->d2h_stream, false, 5),
+     "cudaLaunchKernel mapped read");
+  if (dagrt_status st_ = tl_end(c, c->d2h_stream, t0, 2, -5, -1, array_index(c, a), n)) return st_;
+  for (uint32_t it = 1; *flag != seq; ++it) {
+    if ((it & 255) == 0) {
+      cudaError_t q = cudaStreamQuery((cudaStream_t)c->d2h_stream);
+      if (q == cudaSuccess) {
+        if (*flag != seq) return fail(c, DAGRT_ECUDA, "mapped host read: stream idle, flag not set");
+        break;
+      }
+      if (q != cudaErrorNotReady) CK(q, "cudaStreamQuery D2H");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  c->st.host_syncs++;
+  memcpy(dst, c->mapped, n);
+  return DAGRT_OK;
+}
 
 dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   if (n == 0) return DAGRT_OK;
@@ -852,6 +931,13 @@ dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   c->st.d2h_bytes += n;
   c->st.d2h_copies++;
   if (!c->be->real()) return DAGRT_OK;
+  // Small reads use the mapped-memory kernel only when none of this
+  // context's vertices is still active: then the one-CTA kernel starts at
+  // once.  With kernels in flight it would queue behind their CTAs for an SM
+  // slot (B&S: reads of the first sinks while nine pricing kernels fill the
+  // GPU measured 0.54 vs 0.45 ms per DAG), so the copy engine does the read.
+  // (With the graph cache on, reads stay memcpy nodes of the replayed batch.)
+  if (n <= kMappedReadBytes && !c->be->active() && c->n_active == 0) return d2h_mapped(c, a, off, n, dst);
   // small reads into caller (possibly pageable) memory go through a pinned
   // bounce buffer: a pageable D2H is staged by the driver and much slower
   const bool bounce = n <= kBounceBytes && !(a->host && (char*)dst >= a->host &&
@@ -1026,6 +1112,7 @@ dagrt_status dagrt_destroy(dagrt_ctx c) {
   for (auto& a : c->arrays)
     if (a.h2d_ev) c->be->event_destroy(a.h2d_ev);
   if (c->bounce) cudaFreeHost(c->bounce);
+  if (c->mapped) cudaFreeHost(c->mapped);
   delete c->be;
   delete c;
   return DAGRT_OK;
@@ -1298,6 +1385,11 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   c->st.sched_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
                         std::chrono::steady_clock::now() - t0).count();
   return DAGRT_OK;
+}
+
+dagrt_status dagrt_launch_prepared(dagrt_ctx c, const dagrt_launch_desc* d) {
+  if (!d) return c ? fail(c, DAGRT_EINVAL, "null launch descriptor") : DAGRT_EINVAL;
+  return dagrt_launch(c, d->kernel, d->grid, d->block, d->smem, d->args, d->nargs);
 }
 
 dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes, void* dst) {
@@ -1651,6 +1743,23 @@ dagrt_status dagrt_graph_add_copy(dagrt_ctx c, dagrt_graph g, dagrt_array h, int
   else
     CK(cudaGraphAddMemcpyNode1D(&n, g->r.g, d.data(), d.size(), a->host + off, a->dev + off, bytes,
                                 cudaMemcpyDeviceToHost), "cudaGraphAddMemcpyNode1D");
+  g->r.nodes.push_back(n);
+  *node = (uint32_t)g->r.nodes.size() - 1;
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_graph_add_read(dagrt_ctx c, dagrt_graph g, dagrt_array h, size_t off, size_t bytes,
+                                  void* dst, const uint32_t* deps, int32_t ndeps, uint32_t* node) {
+  GUARD(c);
+  if (!g || !node || !dst) return fail(c, DAGRT_EINVAL, "null graph/node/dst");
+  ArrayRec* a = get_array(c, h);
+  if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
+  if (off > a->bytes || bytes > a->bytes - off) return fail(c, DAGRT_EINVAL, "range");
+  std::vector<cudaGraphNode_t> d;
+  if (dagrt_status s = graph_deps(c, g, deps, ndeps, &d)) return s;
+  cudaGraphNode_t n;
+  CK(cudaGraphAddMemcpyNode1D(&n, g->r.g, d.data(), d.size(), dst, a->dev + off, bytes,
+                              cudaMemcpyDeviceToHost), "cudaGraphAddMemcpyNode1D");
   g->r.nodes.push_back(n);
   *node = (uint32_t)g->r.nodes.size() - 1;
   return DAGRT_OK;

@@ -43,6 +43,12 @@ class Arg(C.Union):
                 ("f32", C.c_float), ("f64", C.c_double)]
 
 
+class LaunchDesc(C.Structure):
+    """dagrt_launch_desc (include/dagrt.h)."""
+    _fields_ = [("kernel", C.c_uint32), ("grid", Dim3), ("block", Dim3), ("smem", C.c_uint32),
+                ("nargs", C.c_int32), ("args", C.POINTER(Arg))]
+
+
 class VertexInfo(C.Structure):
     _fields_ = [("id", C.c_uint32), ("kind", C.c_uint32), ("kernel", C.c_uint32),
                 ("stream", C.c_int32), ("array", C.c_uint64)]
@@ -98,6 +104,7 @@ def lib():
     L.dagrt_launch.argtypes = [ctx, C.c_uint32, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32]
     L.dagrt_launch_raw.argtypes = [ctx, C.c_uint32, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32,
                                    C.c_void_p]
+    L.dagrt_launch_prepared.argtypes = [ctx, C.c_void_p]
     L.dagrt_host_read.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
     L.dagrt_host_write.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
     L.dagrt_host_map.argtypes = [ctx, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p)]
@@ -120,6 +127,8 @@ def lib():
                                          C.POINTER(C.c_uint32)]
     L.dagrt_graph_add_copy.argtypes = [ctx, C.c_void_p, C.c_uint64, C.c_int32, C.c_size_t, C.c_size_t,
                                        C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_uint32)]
+    L.dagrt_graph_add_read.argtypes = [ctx, C.c_void_p, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p,
+                                       C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_uint32)]
     L.dagrt_graph_instantiate.argtypes = [ctx, C.c_void_p]
     L.dagrt_graph_run.argtypes = [ctx, C.c_void_p, C.c_int32]
     L.dagrt_graph_destroy.argtypes = [ctx, C.c_void_p]
@@ -127,13 +136,14 @@ def lib():
         pass
     for fn in ("dagrt_create", "dagrt_destroy", "dagrt_array_register", "dagrt_array_unregister",
                "dagrt_array_device_ptr", "dagrt_kernel_register", "dagrt_kernel_lookup",
-               "dagrt_kernel_signature", "dagrt_launch", "dagrt_launch_raw", "dagrt_host_read",
+               "dagrt_kernel_signature", "dagrt_launch", "dagrt_launch_prepared", "dagrt_launch_raw",
+               "dagrt_host_read",
                "dagrt_host_write", "dagrt_host_map", "dagrt_host_unmap", "dagrt_sync",
                "dagrt_dag_export", "dagrt_dag_clear", "dagrt_trace_export", "dagrt_stats",
                "dagrt_stats_reset", "dagrt_stream_count", "dagrt_stream_handle",
                "dagrt_profile_enable", "dagrt_profile_collect",
                "dagrt_graph_create", "dagrt_graph_add_kernel", "dagrt_graph_add_copy",
-               "dagrt_graph_instantiate", "dagrt_graph_run", "dagrt_graph_destroy"):
+               "dagrt_graph_add_read", "dagrt_graph_instantiate", "dagrt_graph_run", "dagrt_graph_destroy"):
         getattr(L, fn).restype = st
     _lib = L
     return L
@@ -192,7 +202,7 @@ def _set_arg(slot, kind, v):
 
 class Launch:
     """A prepared launch (args marshalled once; calling it enqueues it)."""
-    __slots__ = ("ctx", "kernel", "grid", "block", "smem", "args", "n", "_fn", "_c")
+    __slots__ = ("ctx", "kernel", "grid", "block", "smem", "args", "n", "_fn", "_c", "_desc", "_dp")
 
     def __init__(self, ctx, kernel, grid, block, args, smem=0):
         if len(args) != len(kernel.kinds):
@@ -203,11 +213,15 @@ class Launch:
         self.args = (Arg * max(1, self.n))()
         for i, (k, v) in enumerate(zip(kernel.kinds, args)):
             _set_arg(self.args[i], k, v)
-        self._fn = lib().dagrt_launch
+        # one descriptor per prepared launch: each call passes two pointers
+        # (dagrt_launch_prepared) instead of marshalling seven arguments
+        self._desc = LaunchDesc(kernel.handle, self.grid, self.block, smem, self.n, self.args)
+        self._dp = C.addressof(self._desc)
+        self._fn = lib().dagrt_launch_prepared
         self._c = ctx._c
 
     def __call__(self):
-        s = self._fn(self._c, self.kernel.handle, self.grid, self.block, self.smem, self.args, self.n)
+        s = self._fn(self._c, self._dp)
         if s:
             self.ctx._raise(s)
 
@@ -246,6 +260,14 @@ class Graph:
         self.ctx._check(lib().dagrt_graph_add_copy(self.ctx._c, self._h, arr.handle,
                                                    0 if direction == "h2d" else 1, off, nb, d, nd,
                                                    C.byref(node)))
+        return node.value
+
+    def read(self, arr: Array, dst_ptr, off=0, nbytes=4, deps=()):
+        """D2H node into caller-owned pinned host memory at address dst_ptr."""
+        d, nd = self._deps(deps)
+        node = C.c_uint32()
+        self.ctx._check(lib().dagrt_graph_add_read(self.ctx._c, self._h, arr.handle, off, nbytes,
+                                                   C.c_void_p(dst_ptr), d, nd, C.byref(node)))
         return node.value
 
     def instantiate(self):

@@ -155,9 +155,23 @@ class Program:
         return {n: g.copy(self.a[n], "h2d") for n in self.inputs}
 
     def graph_sinks(self, g, deps_of, only=None):
+        """The graph's host reads of the sinks, so that it ends, like run(),
+        with the host holding the outputs (same timed region for every
+        schedule): whole arrays through the mirrors (stream) or
+        one element per sink into pinned host memory (resident)."""
         if self.mode == "stream":
             for n in (only or self.sinks):
                 g.copy(self.a[n], "d2h", nbytes=4 if n in self.red else None, deps=[deps_of[n]])
+            return
+        if self.record:
+            return
+        if getattr(self, "_graph_pin", None) is None:
+            self._graph_pin = torch.zeros(16 * max(1, len(self.sinks)), dtype=torch.uint8,
+                                          pin_memory=True)
+        base = self._graph_pin.data_ptr()
+        for n in (only or self.sinks):
+            i = self.sinks.index(n)
+            g.read(self.a[n], base + 16 * i, nbytes=min(4, self.a[n].nbytes), deps=[deps_of[n]])
 
     # ---------------------------------------------------------- bytes
     def kernel_bytes(self):
