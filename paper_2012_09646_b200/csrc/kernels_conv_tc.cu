@@ -50,6 +50,17 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // Instruction descriptor: D f32, A/B tf32, both K-major, N = 16, M = 128.
 constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 
+// Split of an activation for 3xTF32 on the ALU/FMA pipes: hi = x with the 13
+// low mantissa bits cleared (exactly representable in TF32, so the tensor
+// core sees it unchanged whatever its fp32->tf32 rounding), lo = x - hi
+// (exact in fp32; the tensor core's own rounding of lo costs ~2^-21 |x|).
+// cvt.rna.tf32.f32 runs on the XU pipe: two per input value kept it 58% busy
+// and bounded the first tcgen05 kernel (ncu, profiles/).
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  lo = x - hi;
+}
+
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -136,8 +147,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
         const int y = 2 * p + a - 1, x = 2 * q + b - 1;
         if (live && y >= 0 && y < H2 && x >= 0 && x < W2) {
           const size_t base = ((size_t)y * W2 + x) * 2;
-          v[a * 3 + b][0] = ldg_stream(src + base);
-          v[a * 3 + b][1] = ldg_stream(src + base + 1);
+          // L1-allocating loads: neighbouring pixels share input pixels and
+          // sectors (tap b=2 of pixel q is tap b=0 of pixel q+1)
+          v[a * 3 + b][0] = __ldg(src + base);
+          v[a * 3 + b][1] = __ldg(src + base + 1);
         } else {
           v[a * 3 + b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
           v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -156,10 +169,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
       for (int h = 0; h < 2; ++h) {
         const float4 x = v[tap][h];
         float4 hi, lo;
-        hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
-        hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
-        hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
-        hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
         put16(ahi + tap * kTcATile, t, h, hi);
         put16(alo + tap * kTcATile, t, h, lo);
       }
@@ -210,6 +223,134 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
                              fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
     }
     // TMEM and the A tiles are reused by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
+// Version 1 with two threads per pixel (256 threads): thread t gathers
+// channel half h = t / 128 of the 9 taps of pixel t % 128 (9 x LDG.128
+// instead of 18), so half the registers per thread and twice the warps per
+// SM cover the gather latency (version 1 ran 8 warps per SM at 167
+// registers: long-scoreboard bound, profiles/).  Same A/B layout, MMAs and
+// results; the epilogue reads each half's 8 TMEM columns (tcgen05.ld x8).
+constexpr int kTc2Threads = 256;
+__global__ void __launch_bounds__(kTc2Threads, 2) k_conv2_tc2(const float* __restrict__ in,
+                                                              const float* __restrict__ w,
+                                                              float* __restrict__ out, int H2, int W2) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* bhi = sm;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  unsigned char* ahi = blo + kTcTaps * kTcBTile;
+  unsigned char* alo = ahi + kTcTaps * kTcATile;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(alo + kTcTaps * kTcATile);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int t = threadIdx.x, warp = t >> 5, pix = t & 127, h = t >> 7;
+
+  for (int i = t; i < 16 * 72; i += kTc2Threads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const long long npix = (long long)H3 * W3;
+  const long long ntiles = (npix + 127) / 128;
+  const float4* src = reinterpret_cast<const float4*>(in);
+  uint32_t phase = 0;
+
+  float4 v[kTcTaps];
+  auto gather = [&](long long m) {
+    const bool live = m < npix;
+    const int p = live ? (int)(m / W3) : 0, q = live ? (int)(m % W3) : 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int y = 2 * p + a - 1, x = 2 * q + b - 1;
+        v[a * 3 + b] = (live && y >= 0 && y < H2 && x >= 0 && x < W2)
+                           ? __ldg(src + ((size_t)y * W2 + x) * 2 + h)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  };
+  if ((long long)blockIdx.x < ntiles) gather((long long)blockIdx.x * 128 + pix);
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long m = tile * 128 + pix;
+    const bool live = m < npix;
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap) {
+      const float4 x = v[tap];
+      float4 hi, lo;
+      tf32_split(x.x, hi.x, lo.x);
+      tf32_split(x.y, hi.y, lo.y);
+      tf32_split(x.z, hi.z, lo.z);
+      tf32_split(x.w, hi.w, lo.w);
+      put16(ahi + tap * kTcATile, pix, h, hi);
+      put16(alo + tap * kTcATile, pix, h, lo);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256);
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(tmem, dah, dbh, acc);
+        acc = 1;
+        tc_mma(tmem, dal, dbh, 1);
+        tc_mma(tmem, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar))
+                   : "memory");
+    }
+    if (tile + gridDim.x < ntiles) gather((tile + gridDim.x) * 128 + pix);
+    tc_mbar_wait(mbar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // epilogue: warp w owns TMEM lanes 32 (w % 4) .. +31 (its pixels) and
+    // columns 8h .. 8h+7 (its channel half)
+    uint32_t r[8];
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(8 * h);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (live) {
+      float4* dst = reinterpret_cast<float4*>(out + (size_t)m * 16 + 8 * h);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -382,10 +523,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc4(const float* __rest
       for (int h = 0; h < 2; ++h) {
         const float4 x = v[tap][h];
         float4 hi, lo;
-        hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
-        hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
-        hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
-        hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
         put16(ahi + tap * kTcATile, t, h, hi);
         put16(alo + tap * kTcATile, t, h, lo);
       }
@@ -626,9 +767,11 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
 
 static const Builtin kConvTc[] = {
     // product: the first version (A from per-thread gathers, next tile's loads
-    // in flight during the MMAs, 2 CTAs/SM): 441 us per branch on the full DL
-    // shapes vs 580 (tc4) / 656 (tc5) us for the cp.async-ring versions, whose
-    // loop-top barrier waits on the ring dominate (tools/conv2_variants.py,
+    // in flight during the MMAs, 2 CTAs/SM): 357 us per branch on the full DL
+    // shapes with L1-allocating gathers and the ALU hi/lo split (441 us with
+    // L1-bypassing loads and cvt.rna on the XU pipe) vs 546 (tc4) / 656 (tc5)
+    // us for the cp.async-ring versions, whose loop-top barrier waits on the
+    // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
     {"conv2", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},
@@ -638,6 +781,9 @@ static const Builtin kConvTc[] = {
     // version 2: 128 threads, one A buffer (148 CTAs, kC2Smem)
     {"conv2_tc4", (const void*)k_conv2_tc4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC2Smem},
+    // version 1 with two threads per pixel (256 threads, 2 x 148 CTAs, kTcSmem)
+    {"conv2_tc2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kTcSmem},
     // first tcgen05 version (per-thread gathers of A), kept for comparison
     {"conv2_tc1", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},

@@ -236,6 +236,87 @@ __device__ __forceinline__ void bs_body(const double* __restrict__ s, double* __
   for (long long i = done + tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
 }
 
+// Lean form of bs_body: 32-bit pair indices, no bounds tests in the main
+// loop (full groups first, then one checked tail), and two register buffers
+// used in turn (load group j+1 into one while the other is priced) instead of
+// copying the prefetched group into the working one -- the integer
+// bookkeeping of the 64-bit, per-pair-checked loop was ~10 of the ~100 issue
+// slots per option (SASS of k_bs_p4b2).  Same arithmetic and results.
+template <int PAIRS>
+__device__ __forceinline__ void bs_body_lean(const double* __restrict__ s, double* __restrict__ c,
+                                             long long n, double r, double v, double t, double k) {
+  __shared__ BsTables T;
+  bs_tables_init(T);
+  BsConst C;
+  const double vst = v * sqrt(t);
+  C.vst = vst;
+  C.inv_vst = 1.0 / vst;
+  C.mu_s = (r + 0.5 * v * v) * t / vst;
+  C.inv_k = 1.0 / k;
+  C.c2 = exp(r * t) / k;
+  C.kexp = k * exp(-r * t);
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned nth = gridDim.x * blockDim.x;
+  if (!(aligned16(s) && aligned16(c)) || n >= (1ll << 31)) {
+    for (long long i = tid; i < n; i += nth) c[i] = bs_price(s[i], C, T);
+    return;
+  }
+  const unsigned n2 = (unsigned)(n >> 1);
+  const unsigned step = PAIRS * nth;
+  const unsigned nfull = n2 / step;  // groups in which every pair of every thread is in range
+  const double2* s2 = reinterpret_cast<const double2*>(s);
+  double2* c2 = reinterpret_cast<double2*>(c);
+  double2 xa[PAIRS], xb[PAIRS];
+  auto load = [&](double2(&x)[PAIRS], unsigned base) {
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) x[q] = ldg_stream(s2 + base + q * nth);
+  };
+  auto price = [&](const double2(&x)[PAIRS], unsigned base) {
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+      double2 y;
+      y.x = bs_price(x[q].x, C, T);
+      y.y = bs_price(x[q].y, C, T);
+      c2[base + q * nth] = y;
+    }
+  };
+  unsigned base = tid, j = 0;
+  if (nfull > 0) load(xa, base);
+  for (; j + 2 <= nfull; j += 2) {
+    load(xb, base + step);
+    price(xa, base);
+    if (j + 2 < nfull) load(xa, base + 2 * step);
+    price(xb, base + step);
+    base += 2 * step;
+  }
+  if (j < nfull) {
+    price(xa, base);
+    base += step;
+  }
+#pragma unroll
+  for (int q = 0; q < PAIRS; ++q) {  // tail: the last partial group
+    const unsigned i = base + q * nth;
+    if (i < n2) {
+      const double2 x = ldg_stream(s2 + i);
+      double2 y;
+      y.x = bs_price(x.x, C, T);
+      y.y = bs_price(x.y, C, T);
+      c2[i] = y;
+    }
+  }
+  if ((n & 1) && tid == 0) c[n - 1] = bs_price(s[n - 1], C, T);
+}
+#define BS_LEAN_VARIANT(NAME, PAIRS, MINB)                                                        \
+  __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs_body_lean<PAIRS>(s, c, n, r, v, t, k);                                                      \
+  }
+BS_LEAN_VARIANT(k_bs_l4b2, 4, 2)
+BS_LEAN_VARIANT(k_bs_l2b3, 2, 3)
+BS_LEAN_VARIANT(k_bs_l2b4, 2, 4)
+BS_LEAN_VARIANT(k_bs_l1b4, 1, 4)
+
 // Deeper prefetch without register cost: each thread keeps DEPTH of its own
 // option pairs in flight with 16-byte cp.async into a private shared-memory
 // ring of DEPTH+1 slots (it reads back only what it copied itself, so no
@@ -299,9 +380,9 @@ BS_ASYNC_VARIANT(k_bs_a5b4, 5, 4)
 BS_ASYNC_VARIANT(k_bs_a7b4, 7, 4)
 BS_ASYNC_VARIANT(k_bs_a5b3, 5, 3)
 
-// default variant: 4 pairs per iteration, 2 CTAs/SM, one wave (fastest in
-// tools/bs_variants.py with the 46-op pricing: 49.7 us per 10M options vs 51.3
-// for 2 pairs / 3 CTAs and 52.8 for 1 pair / 4 CTAs)
+// previous default (now "bs_p4"): 4 pairs per iteration, 2 CTAs/SM, one wave
+// (49.7 us per 10M options vs 51.3 for 2 pairs / 3 CTAs and 52.8 for 1 pair /
+// 4 CTAs); the product is its lean form k_bs_l4b2 (45.2 us)
 __global__ void __launch_bounds__(256, 2) k_bs(const double* __restrict__ s, double* __restrict__ c,
                                             long long n, double r, double v, double t, double k) {
   bs_body<4>(s, c, n, r, v, t, k);
@@ -331,7 +412,10 @@ __global__ void __launch_bounds__(256, 2) k_bs_p4b2(const double* __restrict__ s
 static const Builtin kVecBs[] = {
     {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE},
     {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE},
-    {"bs", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    // product: lean loop, 4 pairs per thread, 2 CTAs/SM, one wave (45.2 us per
+    // 10M options vs 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
+    {"bs", (const void*)k_bs_l4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_p4", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a3b4", (const void*)k_bs_a3b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a5b4", (const void*)k_bs_a5b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a7b4", (const void*)k_bs_a7b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
@@ -341,6 +425,10 @@ static const Builtin kVecBs[] = {
     {"bs_p2b4", (const void*)k_bs_p2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p1b6", (const void*)k_bs_p1b6, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p4b2", (const void*)k_bs_p4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l4b2", (const void*)k_bs_l4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l2b3", (const void*)k_bs_l2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l2b4", (const void*)k_bs_l2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l1b4", (const void*)k_bs_l1b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
 };
 DAGRT_REGISTER_BUILTINS(kVecBs);
 

@@ -21,8 +21,12 @@ def main():
     st = torch.cuda.Stream()
     out = {}
     ref = None
-    for name, waves in (("bs", 4), ("bs_p1b6", 6), ("bs_p2b3", 3), ("bs_p2b4", 4), ("bs_p4b2", 2),
-                        ("bs_a3b4", 4), ("bs_a5b4", 4), ("bs_a7b4", 4), ("bs_a5b3", 3)):
+    sel = sys.argv[1].split(",") if len(sys.argv) > 1 else None
+    for name, waves in (("bs", 2), ("bs_p1b6", 6), ("bs_p2b3", 3), ("bs_p2b4", 4), ("bs_p4b2", 2),
+                        ("bs_a3b4", 4), ("bs_a5b4", 4), ("bs_a7b4", 4), ("bs_a5b3", 3),
+                        ("bs_l4b2", 2), ("bs_l2b3", 3), ("bs_l2b4", 4), ("bs_l1b4", 4)):
+        if sel and name not in sel:
+            continue
         for grid_mult in (1, 2, 4):
             grid = 148 * waves * grid_mult
             L = ctx.prepare(name, grid, 256, [S, Cc, n, 0.08, 0.30, 1.0, 60.0])

@@ -66,6 +66,8 @@ def main():
             L = ctx.prepare(v, ((w3 + 1) // 2 // 256 + 1, min(h3, 65535)), 256, args)
         elif v == "conv2_tc1":
             L = ctx.prepare(v, 2 * 148, 128, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+        elif v == "conv2_tc2":
+            L = ctx.prepare(v, 2 * 148, 256, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
         elif v == "conv2_tc5":
             L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
