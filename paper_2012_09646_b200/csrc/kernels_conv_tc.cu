@@ -231,6 +231,151 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tc(const float* __restr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
+// Version 1 with the gathers two tiles ahead (two register buffers).
+__global__ void __launch_bounds__(kTcThreads, 2) k_conv2_tc3(const float* __restrict__ in,
+                                                            const float* __restrict__ w,
+                                                            float* __restrict__ out, int H2, int W2) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* bhi = sm;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  unsigned char* ahi = blo + kTcTaps * kTcBTile;
+  unsigned char* alo = ahi + kTcTaps * kTcATile;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(alo + kTcTaps * kTcATile);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int t = threadIdx.x, warp = t >> 5;
+
+  // ---- one-time setup: weights (hi/lo), mbarrier, TMEM (32 columns)
+  for (int i = t; i < 16 * 72; i += kTcThreads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;  // w[k][a][b][c], tap = a*3+b
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const long long npix = (long long)H3 * W3;
+  const long long ntiles = (npix + kTcThreads - 1) / kTcThreads;
+  const float4* src = reinterpret_cast<const float4*>(in);
+  uint32_t phase = 0;
+
+  // gather the 9 taps of pixel m (18 x LDG.128 in flight)
+  float4 va[kTcTaps][2], vb[kTcTaps][2];
+  auto gather = [&](float4 (&v)[kTcTaps][2], long long m) {
+    const bool live = m < npix;
+    const int p = live ? (int)(m / W3) : 0, q = live ? (int)(m % W3) : 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int y = 2 * p + a - 1, x = 2 * q + b - 1;
+        if (live && y >= 0 && y < H2 && x >= 0 && x < W2) {
+          const size_t base = ((size_t)y * W2 + x) * 2;
+          // L1-allocating loads: neighbouring pixels share input pixels and
+          // sectors (tap b=2 of pixel q is tap b=0 of pixel q+1)
+          v[a * 3 + b][0] = __ldg(src + base);
+          v[a * 3 + b][1] = __ldg(src + base + 1);
+        } else {
+          v[a * 3 + b][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          v[a * 3 + b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+  };
+  if ((long long)blockIdx.x < ntiles) gather(va, (long long)blockIdx.x * kTcThreads + t);
+  if ((long long)blockIdx.x + gridDim.x < ntiles) gather(vb, ((long long)blockIdx.x + gridDim.x) * kTcThreads + t);
+
+  // two tiles per trip: the gathers run two tiles ahead (buffers va, vb in turn)
+  auto step = [&](float4 (&v)[kTcTaps][2], long long tile) {
+    const long long m = tile * kTcThreads + t;
+    const bool live = m < npix;
+    // ---- split the staged taps into TF32 hi/lo and write the A tiles
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x = v[tap][h];
+        float4 hi, lo;
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
+        put16(ahi + tap * kTcATile, t, h, hi);
+        put16(alo + tap * kTcATile, t, h, lo);
+      }
+    // make the generic-proxy smem writes visible to the tensor core
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- 27 MMAs by one thread, commit to the mbarrier
+    if (t == 0) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256);
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(tmem, dah, dbh, acc);
+        acc = 1;
+        tc_mma(tmem, dal, dbh, 1);
+        tc_mma(tmem, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar))
+                   : "memory");
+    }
+    // the gathers of the tile after next go into this tile's (consumed) buffer
+    if (tile + 2 * (long long)gridDim.x < ntiles) gather(v, (tile + 2 * (long long)gridDim.x) * kTcThreads + t);
+    tc_mbar_wait(mbar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue: lane t of TMEM = pixel m, 16 fp32 columns = 16 channels
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (live) {
+      float4* dst = reinterpret_cast<float4*>(out + (size_t)m * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    // TMEM and the A tiles are reused by the next tile
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  };
+  for (long long tile = blockIdx.x; tile < ntiles; tile += 2 * (long long)gridDim.x) {
+    step(va, tile);
+    if (tile + gridDim.x < ntiles) step(vb, tile + gridDim.x);
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
 // Version 1 with two threads per pixel (256 threads): thread t gathers
 // channel half h = t / 128 of the 9 taps of pixel t % 128 (9 x LDG.128
 // instead of 18), so half the registers per thread and twice the warps per
@@ -766,14 +911,15 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
 }
 
 static const Builtin kConvTc[] = {
-    // product: the first version (A from per-thread gathers, next tile's loads
+    // product: the first version with its gathers two tiles ahead (k_conv2_tc3,
+    // 350 us); the first version (A from per-thread gathers, next tile's loads
     // in flight during the MMAs, 2 CTAs/SM): 357 us per branch on the full DL
     // shapes with L1-allocating gathers and the ALU hi/lo split (441 us with
     // L1-bypassing loads and cvt.rna on the XU pipe) vs 546 (tc4) / 656 (tc5)
     // us for the cp.async-ring versions, whose loop-top barrier waits on the
     // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
-    {"conv2", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+    {"conv2", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},
     // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
     {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
@@ -781,6 +927,9 @@ static const Builtin kConvTc[] = {
     // version 2: 128 threads, one A buffer (148 CTAs, kC2Smem)
     {"conv2_tc4", (const void*)k_conv2_tc4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC2Smem},
+    // version 1 with gathers two tiles ahead (128 threads, 2 x 148 CTAs, kTcSmem)
+    {"conv2_tc3", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     kTcSmem},
     // version 1 with two threads per pixel (256 threads, 2 x 148 CTAs, kTcSmem)
     {"conv2_tc2", (const void*)k_conv2_tc2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},

@@ -8,7 +8,7 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
-CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64    # csrc/kernels_conv_tc.cu kTcSmem ("conv2" = k_conv2_tc)
+CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64    # csrc/kernels_conv_tc.cu kTcSmem ("conv2" = k_conv2_tc3)
 CONV2_TC_THREADS = 128
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)

@@ -341,7 +341,7 @@ def test_dl_full_size_sampled(ctx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc4", "conv2_tc5"])
+@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc2", "conv2_tc4", "conv2_tc5"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
 def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     """The other conv2 kernels (CUDA-core FFMA; the tcgen05 versions with a
@@ -358,6 +358,9 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
         ctx.launch(variant, ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
     elif variant == "conv2_tc1":
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
+                   smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+    elif variant == "conv2_tc2":
+        ctx.launch(variant, 2 * 148, 256, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
     elif variant == "conv2_tc4":
         ctx.launch(variant, 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,

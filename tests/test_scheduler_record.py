@@ -214,3 +214,27 @@ def test_all_symbols_exported():
     missing = [n for n in sorted(names) if not hasattr(L, n)]
     assert not missing, missing
     assert len(names) >= 30
+
+
+@pytest.mark.parametrize("idx", range(0, len(CASES), max(1, len(CASES) // 6)))
+def test_prepared_and_plain_launch_same_dag(idx):
+    """dagrt_launch_prepared (one descriptor pointer per call) and dagrt_launch
+    (seven arguments) are the same call: identical DAGs and traces on golden
+    traces."""
+    trace = CASES[idx][1]["trace"]
+    out = []
+    for plain in (False, True):
+        rp = Replayer(arrays_of(trace), 128)
+        for op in trace:
+            if op[0] == "launch":
+                k = rp.kernel(op[1], [m for _, m in op[2]])
+                L = rp.ctx.prepare(k, 1, 32, [rp.arr[a] for a, _ in op[2]])
+                if plain:
+                    assert D.lib().dagrt_launch(rp.ctx._c, L.kernel.handle, L.grid, L.block, L.smem,
+                                                L.args, L.n) == 0
+                else:
+                    L()
+            else:
+                rp.run([op])
+        out.append((rp.dag(), rp.ctx.trace()))
+    assert out[0] == out[1]

@@ -64,7 +64,7 @@ def main():
         args = [p.a["px"], p.a["w2"], arr, h2, w2]
         if v == "conv2_ffma":
             L = ctx.prepare(v, ((w3 + 1) // 2 // 256 + 1, min(h3, 65535)), 256, args)
-        elif v == "conv2_tc1":
+        elif v in ("conv2_tc1", "conv2_tc3"):
             L = ctx.prepare(v, 2 * 148, 128, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
         elif v == "conv2_tc2":
             L = ctx.prepare(v, 2 * 148, 256, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
