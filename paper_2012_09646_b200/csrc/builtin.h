@@ -8,12 +8,20 @@ namespace dagrt {
 
 enum : int32_t { KF_NONE = 0, KF_COOPERATIVE = 1 };
 
+// Host-side pre-launch hook of a built-in kernel: given the marshalled
+// argument values of the C-ABI signature (device pointers, scalars), returns
+// one extra pointer-sized value passed to the CUDA kernel BEFORE them (e.g.
+// a TMA tensor-map descriptor in device memory built from the pointer and
+// shape arguments).  The signature -- and so the DAG -- is unchanged.
+typedef int (*PrelaunchFn)(const uint64_t* vals, int nargs, void** extra);
+
 struct Builtin {
   const char* name;
   const void* fn;
   const char* signature;
   int32_t flags;
-  int32_t smem_max;  // > 0: opt in to this much dynamic shared memory (bytes)
+  int32_t smem_max;        // > 0: opt in to this much dynamic shared memory (bytes)
+  PrelaunchFn prelaunch;   // optional (nullptr)
 };
 
 int register_builtins(const Builtin* table, int n);  // returns n

@@ -23,6 +23,12 @@
 //     mbarrier;
 //   * the 4 warps read their 32 TMEM lanes back with tcgen05.ld 32x32b.x16
 //     (one pixel = one lane = 16 channels), apply ReLU and store 64 B/pixel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <vector>
+
 #include "kcommon.cuh"
 
 namespace dagrt {
@@ -910,23 +916,829 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_conv2_tc5(const float* __rest
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kC3Cols));
 }
 
+// ---------------------------------------------------------------------------
+// conv2, TMA version: the tensor memory accelerator gathers the A operand.
+//
+// The stride-2 tap gathers that bound the per-thread versions (L1 65% busy,
+// 4x the wavefronts of a coalesced load) are done by TMA instead: the input
+// p (H2 x W2 x 8, NHWC) is described as a 3-D tensor {8 channels, W2 pixels,
+// H2 rows} with TRAVERSAL STRIDE 2 along the pixels, so one box {8, 256 -> 128
+// pixels, 1 row} at pixel 2*q0 + b - 1 of row 2p + a - 1 is exactly tap (a, b)
+// of the 128 output pixels q0 .. q0+127: 128 rows x 32 bytes, written in the
+// 32-byte-swizzled K-major layout the UMMA descriptor reads directly.
+// Out-of-range pixels and rows (the zero padding) are filled with zeros by
+// TMA.  Nine boxes (36 KB) per tile, S = 3 stages in flight.
+//
+// 3xTF32: the raw box is used as A_hi when the tensor core's fp32 -> tf32
+// conversion of it is known (MODE 1: truncation, lo = x - trunc(x); MODE 2:
+// round to nearest, lo = x - rn(x)); MODE 0 makes no assumption and writes
+// both hi (13 low bits cleared) and lo into interleaved tiles.  The 4 warps
+// read their pixel's taps from the swizzled box (conflict-free), write the lo
+// (and hi) tiles, one thread issues the 27 MMAs, all drain the accumulator.
+//
+// The tensor map lives in device memory (one per (input pointer, shape),
+// built on the host by the pre-launch hook below) and is the kernel's first
+// parameter; the C-ABI signature -- and the DAG -- are those of "conv2".
+constexpr int kTmaStages = 3;
+constexpr int kTmaTap = 128 * 32;            // one box: 128 pixels x 8 fp32
+constexpr int kTmaStage = kTcTaps * kTmaTap; // 36 KB
+template <int MODE>
+constexpr int tma_smem() {
+  return 1024 /*align*/ + kTmaStages * kTmaStage + (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile +
+         2 * kTcTaps * kTcBTile + 64;
+}
+
+// Rows one TMA box delivers (= bytes / 32): 128, or ceil(W2/2) for inputs
+// narrower than the 256-pixel box (conv2_tma_prelaunch).  Rows past it are
+// not written and only feed output pixels q >= W3, which are not stored.
+__device__ __forceinline__ int tma_box_rows(int W2) { return W2 < 256 ? (W2 + 1) / 2 : 128; }
+
+// UMMA descriptor, K-major, 32-byte swizzle: SBO = 256 B (8 rows x 32 B),
+// LBO unused (the K extent of one MMA, 8 tf32, is the swizzle width).
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)((256 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                  // descriptor version (Blackwell)
+  d |= (uint64_t)6 << 61;                  // layout: SWIZZLE_32B
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTcThreads, 1) k_conv2_tma(const CUtensorMap* __restrict__ tmap,
+                                                             const float* __restrict__ in,
+                                                             const float* __restrict__ w,
+                                                             float* __restrict__ out, int H2, int W2) {
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = sm;                                        // [S][9][128 x 32 B], SW32
+  unsigned char* alo = raw + kTmaStages * kTmaStage;              // [9][4 KB] interleaved
+  unsigned char* ahi = MODE == 0 ? alo + kTcTaps * kTcATile : nullptr;
+  unsigned char* bhi = alo + (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(blo + kTcTaps * kTcBTile);  // [S]
+  uint64_t* mbar = full + kTmaStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int t = threadIdx.x, warp = t >> 5;
+  (void)in;
+
+  for (int i = t; i < 16 * 72; i += kTcThreads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (t == 0) {
+    for (int q = 0; q < kTmaStages; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long G = gridDim.x;
+  // issue the 9 boxes of tile `tile` into stage st (thread 0)
+  auto issue = [&](long long tile, int st) {
+    const int p = (int)(tile / nqb), q0 = (int)(tile % nqb) * 128;
+    const uint32_t bar = smem_u32(full + st);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(9 * 32 * tma_box_rows(W2))
+                 : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        tma_load_3d(smem_u32(raw + st * kTmaStage + (a * 3 + b) * kTmaTap), tmap, 0, 2 * q0 + b - 1,
+                    2 * p + a - 1, bar);
+  };
+  if (t == 0)
+    for (int q = 0; q < kTmaStages; ++q)
+      if ((long long)blockIdx.x + q * G < ntiles) issue((long long)blockIdx.x + q * G, q);
+
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
+    const int st = it % kTmaStages;
+    tc_mbar_wait(full + st, (uint32_t)((it / kTmaStages) & 1));
+    // ---- lo (and hi) tiles from the swizzled box: pixel row t, chunk c of
+    // row t sits at 32 t + 16 (c ^ ((t >> 2) & 1))
+    const unsigned char* rs = raw + st * kTmaStage;
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x =
+            *reinterpret_cast<const float4*>(rs + tap * kTmaTap + 32 * t + 16 * (h ^ ((t >> 2) & 1)));
+        float4 hi, lo;
+        if (MODE == 2) {  // tensor core rounds to nearest (ties away): rn(x) by integer ops
+          hi.x = __uint_as_float((__float_as_uint(x.x) + 0x1000u) & 0xffffe000u);
+          hi.y = __uint_as_float((__float_as_uint(x.y) + 0x1000u) & 0xffffe000u);
+          hi.z = __uint_as_float((__float_as_uint(x.z) + 0x1000u) & 0xffffe000u);
+          hi.w = __uint_as_float((__float_as_uint(x.w) + 0x1000u) & 0xffffe000u);
+          lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;
+        } else {
+          tf32_split(x.x, hi.x, lo.x);
+          tf32_split(x.y, hi.y, lo.y);
+          tf32_split(x.z, hi.z, lo.z);
+          tf32_split(x.w, hi.w, lo.w);
+        }
+        put16(alo + tap * kTcATile, t, h, lo);
+        if (MODE == 0) put16(ahi + tap * kTcATile, t, h, hi);
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      // MODE 0: the raw stage is consumed -> refill it now
+      if (MODE == 0 && tile + kTmaStages * G < ntiles) issue(tile + kTmaStages * G, st);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = MODE == 0 ? umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256)
+                                       : umma_desc_sw32(smem_u32(rs + tap * kTmaTap));
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(tmem, dah, dbh, acc);
+        acc = 1;
+        tc_mma(tmem, dal, dbh, 1);
+        tc_mma(tmem, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar))
+                   : "memory");
+    }
+    tc_mbar_wait(mbar, (uint32_t)(it & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // MODE 1/2: the MMAs read the raw stage as A_hi -> refill it after them
+    if (MODE != 0 && t == 0 && tile + kTmaStages * G < ntiles) issue(tile + kTmaStages * G, st);
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int p = (int)(tile / nqb), q = (int)(tile % nqb) * 128 + t;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
+// Two consumer groups: 256 threads = two groups of 4 warps that take
+// alternate tiles, each with its own lo (and hi) A tiles, TMEM accumulator
+// (columns 32g..32g+15) and MMA mbarrier, so one group's hi/lo split runs
+// while the other's MMAs and epilogue do (the single-group kernel serialised
+// TMA wait -> split -> MMA -> epilogue: 534 us).  Each group owns SG stages
+// (2, or 1 for MODE 0 whose hi tiles take the room) and waits only on them,
+// in order, so an mbarrier parity can never be mistaken for a later phase.
+template <int MODE>
+constexpr int tma2g_stages() { return MODE == 0 ? 1 : 2; }  // per group
+template <int MODE>
+constexpr int tma2g_smem() {
+  return 1024 + 2 * tma2g_stages<MODE>() * kTmaStage + 2 * (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile +
+         2 * kTcTaps * kTcBTile + 64;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k_conv2_tma2g(const CUtensorMap* __restrict__ tmap,
+                                                        const float* __restrict__ in,
+                                                        const float* __restrict__ w,
+                                                        float* __restrict__ out, int H2, int W2) {
+  constexpr int SG = tma2g_stages<MODE>();
+  constexpr int S = 2 * SG;
+  constexpr int APART = (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile;  // A tiles per group
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = sm;                                        // [S][9][128 x 32 B], SW32
+  unsigned char* agrp = raw + S * kTmaStage;                      // [2][lo (, hi)]
+  unsigned char* bhi = agrp + 2 * APART;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(blo + kTcTaps * kTcBTile);  // [S]
+  uint64_t* mbar = full + S;                                               // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int tid = threadIdx.x, grp = tid >> 7, t = tid & 127, warp = tid >> 5;
+  unsigned char* alo = agrp + grp * APART;
+  unsigned char* ahi = MODE == 0 ? alo + kTcTaps * kTcATile : nullptr;
+  (void)in;
+
+  for (int i = tid; i < 16 * 72; i += 256) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)));
+    for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot + (uint32_t)(32 * grp);
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long G = gridDim.x;
+  auto issue = [&](long long tile, int st) {
+    const int p = (int)(tile / nqb), q0 = (int)(tile % nqb) * 128;
+    const uint32_t bar = smem_u32(full + st);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(9 * 32 * tma_box_rows(W2))
+                 : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        tma_load_3d(smem_u32(raw + st * kTmaStage + (a * 3 + b) * kTmaTap), tmap, 0, 2 * q0 + b - 1,
+                    2 * p + a - 1, bar);
+  };
+  if (t == 0)  // group g's first SG tiles (it = g + 2k) into its stages g*SG + k
+    for (int k = 0; k < SG; ++k)
+      if ((long long)blockIdx.x + (grp + 2 * k) * G < ntiles)
+        issue((long long)blockIdx.x + (grp + 2 * k) * G, grp * SG + k);
+  auto group_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+
+  for (int it = grp;; it += 2) {
+    const long long tile = (long long)blockIdx.x + (long long)it * G;
+    if (tile >= ntiles) break;
+    const int k = it >> 1;  // the group's k-th tile
+    const int st = grp * SG + k % SG;
+    const long long next = tile + 2LL * SG * G;  // the group's tile k + SG, into the same stage
+    tc_mbar_wait(full + st, (uint32_t)((k / SG) & 1));
+    const unsigned char* rs = raw + st * kTmaStage;
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x =
+            *reinterpret_cast<const float4*>(rs + tap * kTmaTap + 32 * t + 16 * (h ^ ((t >> 2) & 1)));
+        float4 hi, lo;
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
+        put16(alo + tap * kTcATile, t, h, lo);
+        if (MODE == 0) put16(ahi + tap * kTcATile, t, h, hi);
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      if (MODE == 0 && next < ntiles) issue(next, st);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = MODE == 0 ? umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256)
+                                       : umma_desc_sw32(smem_u32(rs + tap * kTmaTap));
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+        const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+        tc_mma(tmem, dah, dbh, acc);
+        acc = 1;
+        tc_mma(tmem, dal, dbh, 1);
+        tc_mma(tmem, dah, dbl, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar + grp))
+                   : "memory");
+    }
+    tc_mbar_wait(mbar + grp, (uint32_t)(k & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (MODE != 0 && t == 0 && next < ntiles) issue(next, st);
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int p = (int)(tile / nqb), q = (int)(tile % nqb) * 128 + t;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(*tmem_slot));
+}
+
+// Two-group TMA kernel with the 3xTF32 products in two independent chains:
+// acc0 (N = 32) = A_hi x [B_hi | B_lo], acc1 (N = 16) = A_lo x B_hi, summed in
+// the epilogue: 18 MMAs per tile instead of 27 and A_hi read once (the
+// two-group kernel spent a quarter of its stall samples waiting for its 27
+// dependent N = 16 MMAs, ncu source page).
+constexpr uint32_t kTcIdescN32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void tc_mma_n(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t acc, uint32_t idesc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <int MODE, int ROWACC>
+__global__ void __launch_bounds__(256, 1) k_conv2_tma2n(const CUtensorMap* __restrict__ tmap,
+                                                        const float* __restrict__ in,
+                                                        const float* __restrict__ w,
+                                                        float* __restrict__ out, int H2, int W2) {
+  constexpr int SG = tma2g_stages<MODE>();
+  constexpr int S = 2 * SG;
+  constexpr int APART = (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile;  // A tiles per group
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = sm;                                        // [S][9][128 x 32 B], SW32
+  unsigned char* agrp = raw + S * kTmaStage;                      // [2][lo (, hi)]
+  unsigned char* bcat = agrp + 2 * APART;  // [9][32 rows x 8 tf32]: rows 0-15 B_hi, 16-31 B_lo
+  uint64_t* full = reinterpret_cast<uint64_t*>(bcat + 2 * kTcTaps * kTcBTile);  // [S]
+  uint64_t* mbar = full + S;                                               // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int tid = threadIdx.x, grp = tid >> 7, t = tid & 127, warp = tid >> 5;
+  unsigned char* alo = agrp + grp * APART;
+  unsigned char* ahi = MODE == 0 ? alo + kTcTaps * kTcATile : nullptr;
+  (void)in;
+
+  for (int i = tid; i < 16 * 72; i += 256) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    auto off = [&](int n) { return 2 * tap * kTcBTile + (n & 7) * 16 + (n >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4; };
+    *reinterpret_cast<float*>(bcat + off(k)) = hi;
+    *reinterpret_cast<float*>(bcat + off(16 + k)) = lo;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)));
+    for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tmem_slot)), "n"(ROWACC ? 512 : 128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // per group: acc0 = 32 columns (A_hi x [B_hi | B_lo]), acc1 = 16 columns (A_lo x B_hi)
+  // (ROWACC: one such pair per input row a of the window, 64 columns apart)
+  const uint32_t tmem = *tmem_slot + (uint32_t)((ROWACC ? 192 : 64) * grp);
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long G = gridDim.x;
+  auto issue = [&](long long tile, int st) {
+    const int p = (int)(tile / nqb), q0 = (int)(tile % nqb) * 128;
+    const uint32_t bar = smem_u32(full + st);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(9 * 32 * tma_box_rows(W2))
+                 : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        tma_load_3d(smem_u32(raw + st * kTmaStage + (a * 3 + b) * kTmaTap), tmap, 0, 2 * q0 + b - 1,
+                    2 * p + a - 1, bar);
+  };
+  if (t == 0)  // group g's first SG tiles (it = g + 2k) into its stages g*SG + k
+    for (int k = 0; k < SG; ++k)
+      if ((long long)blockIdx.x + (grp + 2 * k) * G < ntiles)
+        issue((long long)blockIdx.x + (grp + 2 * k) * G, grp * SG + k);
+  auto group_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+
+  for (int it = grp;; it += 2) {
+    const long long tile = (long long)blockIdx.x + (long long)it * G;
+    if (tile >= ntiles) break;
+    const int k = it >> 1;  // the group's k-th tile
+    const int st = grp * SG + k % SG;
+    const long long next = tile + 2LL * SG * G;  // the group's tile k + SG, into the same stage
+    tc_mbar_wait(full + st, (uint32_t)((k / SG) & 1));
+    const unsigned char* rs = raw + st * kTmaStage;
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x =
+            *reinterpret_cast<const float4*>(rs + tap * kTmaTap + 32 * t + 16 * (h ^ ((t >> 2) & 1)));
+        float4 hi, lo;
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
+        put16(alo + tap * kTcATile, t, h, lo);
+        if (MODE == 0) put16(ahi + tap * kTcATile, t, h, hi);
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      if (MODE == 0 && next < ntiles) issue(next, st);
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = MODE == 0 ? umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256)
+                                       : umma_desc_sw32(smem_u32(rs + tap * kTmaTap));
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbc = umma_desc(smem_u32(bcat + 2 * tap * kTcBTile), 128, 256);
+        // two independent accumulation chains (18 MMAs instead of 27)
+        const uint32_t ta = ROWACC ? tmem + 64 * (tap / 3) : tmem;
+        const uint32_t first = ROWACC ? (tap % 3 > 0) : (tap > 0);
+        tc_mma_n(ta, dah, dbc, first, kTcIdescN32);
+        tc_mma_n(ta + 32, dal, dbc, first, kTcIdesc);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar + grp))
+                   : "memory");
+    }
+    tc_mbar_wait(mbar + grp, (uint32_t)(k & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (MODE != 0 && t == 0 && next < ntiles) issue(next, st);
+    uint32_t r[16], r1[16], r2[16];
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    tmem_ld16(taddr, r);
+    tmem_ld16(taddr + 16, r1);
+    tmem_ld16(taddr + 32, r2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int n = 0; n < 16; ++n)
+      r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r2[n]) + __uint_as_float(r1[n]));
+    if (ROWACC) {
+#pragma unroll
+      for (int a = 1; a < 3; ++a) {
+        tmem_ld16(taddr + 64 * a, r1);
+        tmem_ld16(taddr + 64 * a + 16, r2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int n = 0; n < 16; ++n)
+          r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r1[n]) + __uint_as_float(r2[n]));
+        tmem_ld16(taddr + 64 * a + 32, r1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int n = 0; n < 16; ++n) r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r1[n]));
+      }
+    }
+    const int p = (int)(tile / nqb), q = (int)(tile % nqb) * 128 + t;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(ROWACC ? 512 : 128));
+}
+
+// Ring version: the TMA pipeline is cut per INPUT ROW instead of per tile.
+// Slot = the 3 boxes of one input row a of one tile (12 KB); R = 12 slots =
+// 4 tiles in flight (the two-group kernel held 2: its waits on TMA data --
+// long_scoreboard -- dominated, tensor pipe 8%, L1 41%, L2 44%).  A producer
+// warp fills slots in order, waiting on each slot's "empty" barrier; two
+// consumer groups take alternate tiles: per row a they wait for the slot,
+// split lo for the 3 taps of that row, issue those 9 MMAs (A_hi = the raw
+// box, MODE 1: the tensor core truncates fp32 to tf32 -- established by the
+// conv2_tma1 / conv2_tma2 parity tests) and commit to the slot's empty
+// barrier, so a slot is refilled as soon as its MMAs have read it.
+constexpr int kRingSlots = 12;
+constexpr int kSlotBytes = 3 * kTmaTap;  // 12 KB
+constexpr int kRingThreads = 256 + 32;
+constexpr int tmar_smem() {
+  return 1024 + kRingSlots * kSlotBytes + 2 * kTcTaps * kTcATile + 2 * kTcTaps * kTcBTile + 256;
+}
+
+__global__ void __launch_bounds__(kRingThreads, 1) k_conv2_tmar(const CUtensorMap* __restrict__ tmap,
+                                                                const float* __restrict__ in,
+                                                                const float* __restrict__ w,
+                                                                float* __restrict__ out, int H2, int W2) {
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* ring = sm;                                   // [R][3 taps][128 x 32 B], SW32
+  unsigned char* agrp = ring + kRingSlots * kSlotBytes;       // [2 groups][9 taps][4 KB] lo
+  unsigned char* bhi = agrp + 2 * kTcTaps * kTcATile;
+  unsigned char* blo = bhi + kTcTaps * kTcBTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(blo + kTcTaps * kTcBTile);  // [R]
+  uint64_t* empty = full + kRingSlots;                                       // [R]
+  uint64_t* mbar = empty + kRingSlots;                                       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  (void)in;
+
+  for (int i = tid; i < 16 * 72; i += kRingThreads) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int off = tap * kTcBTile + (k & 7) * 16 + (k >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4;
+    *reinterpret_cast<float*>(bhi + off) = hi;
+    *reinterpret_cast<float*>(blo + off) = lo;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < kRingSlots; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(empty + q)));
+    }
+    for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long G = gridDim.x;
+  const long long my_tiles = ntiles > (long long)blockIdx.x ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+
+  if (warp == 8) {
+    // ---- producer: slot u = 3 j + a holds input row a of the CTA's j-th tile
+    if ((tid & 31) == 0) {
+      for (long long u = 0; u < 3 * my_tiles; ++u) {
+        const int slot = (int)(u % kRingSlots);
+        const long long use = u / kRingSlots;
+        if (use > 0) tc_mbar_wait(empty + slot, (uint32_t)((use - 1) & 1));
+        const long long tile = (long long)blockIdx.x + (u / 3) * G;
+        const int a = (int)(u % 3);
+        const int p = (int)(tile / nqb), q0 = (int)(tile % nqb) * 128;
+        const uint32_t bar = smem_u32(full + slot);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(3 * 32 * tma_box_rows(W2))
+                     : "memory");
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          tma_load_3d(smem_u32(ring + slot * kSlotBytes + b * kTmaTap), tmap, 0, 2 * q0 + b - 1,
+                      2 * p + a - 1, bar);
+      }
+    }
+  } else {
+    // ---- consumers: group g takes the CTA's tiles j = g, g + 2, ...
+    const int grp = tid >> 7, t = tid & 127;
+    unsigned char* alo = agrp + grp * kTcTaps * kTcATile;
+    const uint32_t tmem = *tmem_slot + (uint32_t)(32 * grp);
+    auto group_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+    for (long long j = grp; j < my_tiles; j += 2) {
+      const long long tile = (long long)blockIdx.x + j * G;
+#pragma unroll 1
+      for (int a = 0; a < 3; ++a) {
+        const long long u = 3 * j + a;
+        const int slot = (int)(u % kRingSlots);
+        tc_mbar_wait(full + slot, (uint32_t)((u / kRingSlots) & 1));
+        const unsigned char* rs = ring + slot * kSlotBytes;
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 x =
+                *reinterpret_cast<const float4*>(rs + b * kTmaTap + 32 * t + 16 * (h ^ ((t >> 2) & 1)));
+            float4 hi, lo;
+            tf32_split(x.x, hi.x, lo.x);
+            tf32_split(x.y, hi.y, lo.y);
+            tf32_split(x.z, hi.z, lo.z);
+            tf32_split(x.w, hi.w, lo.w);
+            put16(alo + (a * 3 + b) * kTcATile, t, h, lo);
+          }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        group_sync();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (t == 0) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const int tap = a * 3 + b;
+            const uint64_t dah = umma_desc_sw32(smem_u32(rs + b * kTmaTap));
+            const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+            const uint64_t dbh = umma_desc(smem_u32(bhi + tap * kTcBTile), 128, 256);
+            const uint64_t dbl = umma_desc(smem_u32(blo + tap * kTcBTile), 128, 256);
+            tc_mma(tmem, dah, dbh, tap > 0 ? 1u : 0u);
+            tc_mma(tmem, dal, dbh, 1);
+            tc_mma(tmem, dah, dbl, 1);
+          }
+          // the slot is free once these MMAs have read it
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(empty + slot))
+                       : "memory");
+          if (a == 2)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(mbar + grp))
+                         : "memory");
+        }
+      }
+      tc_mbar_wait(mbar + grp, (uint32_t)((j >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int p = (int)(tile / nqb), q = (int)(tile % nqb) * 128 + t;
+      if (q < W3) {
+        float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                               fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                               fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+      }
+      // TMEM accumulator and lo tiles are rewritten by this group's next tile
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      group_sync();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(*tmem_slot));
+}
+
+// Pre-launch hook: the tensor map of the conv2 input (vals = in, w, out, H2,
+// W2), encoded with the driver's cuTensorMapEncodeTiled and copied once to
+// device memory; cached per (device, pointer, shape).
+namespace {
+struct TmapEntry {
+  int dev;
+  uint64_t ptr;
+  int h2, w2;
+  void* dmap;
+};
+std::mutex g_tmap_mu;
+std::vector<TmapEntry> g_tmaps;
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
+
+int conv2_tma_prelaunch(const uint64_t* vals, int nargs, void** extra) {
+  if (nargs != 5) return (int)cudaErrorInvalidValue;
+  const uint64_t ptr = vals[0];
+  const int h2 = (int)(uint32_t)vals[3], w2 = (int)(uint32_t)vals[4];
+  if (h2 < 1 || w2 < 1) {  // empty input: no tiles, the kernel issues no TMA
+    *extra = nullptr;
+    return 0;
+  }
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return (int)e;
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  for (const TmapEntry& e : g_tmaps)
+    if (e.dev == dev && e.ptr == ptr && e.h2 == h2 && e.w2 == w2) {
+      *extra = e.dmap;
+      return 0;
+    }
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fp)
+      return (int)cudaErrorNotSupported;
+    encode = (EncodeFn)fp;
+  }
+  if (ptr & 15) return (int)cudaErrorMisalignedAddress;
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {8, (cuuint64_t)w2, (cuuint64_t)h2};
+  const cuuint64_t strides[2] = {32, (cuuint64_t)w2 * 32};  // bytes, dims 1..2
+  // the box may not exceed the tensor: narrow inputs get a box of W2 pixels
+  // (ceil(W2/2) rows = every output pixel of the row); see tma_box_rows()
+  const cuuint32_t box[3] = {8, (cuuint32_t)(w2 < 256 ? w2 : 256), 1};
+  const cuuint32_t estr[3] = {1, 2, 1};
+  CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)(uintptr_t)ptr, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
+  void* d = nullptr;
+  if (cudaError_t e = cudaMalloc(&d, sizeof(CUtensorMap))) return (int)e;
+  if (cudaError_t e = cudaMemcpy(d, &m, sizeof(CUtensorMap), cudaMemcpyHostToDevice)) return (int)e;
+  g_tmaps.push_back(TmapEntry{dev, ptr, h2, w2, d});
+  *extra = d;
+  return 0;
+}
+
 static const Builtin kConvTc[] = {
-    // product: the first version with its gathers two tiles ahead (k_conv2_tc3,
-    // 350 us); the first version (A from per-thread gathers, next tile's loads
+    // product: TMA-gathered A (k_conv2_tma2n<1,0> = "conv2_tman1": 303 us per
+    // branch; 148 CTAs of 256 threads, tma2g_smem<1>() bytes, tensor map built by
+    // the pre-launch hook).  Before it: the first version with its gathers two
+    // tiles ahead (k_conv2_tc3 = "conv2_tc3", 350 us); the first version (A from per-thread gathers, next tile's loads
     // in flight during the MMAs, 2 CTAs/SM): 357 us per branch on the full DL
     // shapes with L1-allocating gathers and the ALU hi/lo split (441 us with
     // L1-bypassing loads and cvt.rna on the XU pipe) vs 546 (tc4) / 656 (tc5)
     // us for the cp.async-ring versions, whose loop-top barrier waits on the
     // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
-    {"conv2", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     kTcSmem},
+    {"conv2", (const void*)k_conv2_tma2n<1, 0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma2g_smem<1>(), conv2_tma_prelaunch},
     // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
     {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC3Smem},
     // version 2: 128 threads, one A buffer (148 CTAs, kC2Smem)
     {"conv2_tc4", (const void*)k_conv2_tc4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC2Smem},
+    // TMA-gathered A (pre-launch hook builds the tensor map): MODE 0 makes no
+    // assumption on the tensor core's fp32->tf32 rounding; MODE 1 / 2 use the
+    // raw box as A_hi (truncation / round-to-nearest).  148 CTAs of 128 threads.
+    // input-row ring + producer warp + two consumer groups (288 threads, 148 CTAs)
+    {"conv2_tmar", (const void*)k_conv2_tmar, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tmar_smem(), conv2_tma_prelaunch},
+    // two consumer groups, 3xTF32 as two chains (N = 32 and N = 16), 148 CTAs of 256
+    {"conv2_tman1", (const void*)k_conv2_tma2n<1, 0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma2g_smem<1>(), conv2_tma_prelaunch},
+    // ... and one accumulator pair per input row of the window (6 chains of 3 MMAs)
+    {"conv2_tmanr1", (const void*)k_conv2_tma2n<1, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma2g_smem<1>(), conv2_tma_prelaunch},
+    // two consumer groups (256 threads, 148 CTAs)
+    {"conv2_tmag0", (const void*)k_conv2_tma2g<0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma2g_smem<0>(), conv2_tma_prelaunch},
+    {"conv2_tmag1", (const void*)k_conv2_tma2g<1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma2g_smem<1>(), conv2_tma_prelaunch},
+    {"conv2_tma0", (const void*)k_conv2_tma<0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma_smem<0>(), conv2_tma_prelaunch},
+    {"conv2_tma1", (const void*)k_conv2_tma<1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma_smem<1>(), conv2_tma_prelaunch},
+    {"conv2_tma2", (const void*)k_conv2_tma<2>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tma_smem<2>(), conv2_tma_prelaunch},
     // version 1 with gathers two tiles ahead (128 threads, 2 x 148 CTAs, kTcSmem)
     {"conv2_tc3", (const void*)k_conv2_tc3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},

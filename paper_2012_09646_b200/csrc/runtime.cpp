@@ -534,6 +534,7 @@ constexpr int kMaxArgs = 16;
 struct KernelRec {
   std::string name;
   const void* fn;
+  PrelaunchFn pre = nullptr;  // built-in pre-launch hook (extra leading kernel argument)
   int32_t nparams;
   uint8_t kind[kMaxArgs];
   bool coop;
@@ -745,7 +746,7 @@ dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim
     CK(c->be->record(e0, s), "cudaEventRecord profile");
   }
   if (dagrt_status st = tl_begin(c, s, &t0)) return st;
-  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop, k->nparams), "cudaLaunchKernel");
+  CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop, k->nparams + (k->pre ? 1 : 0)), "cudaLaunchKernel");
   if (dagrt_status st = tl_end(c, s, t0, 0, sidx, vertex, kh, 0)) return st;
   if (k->prof) {
     CK(c->be->record(e1, s), "cudaEventRecord profile");
@@ -1031,6 +1032,14 @@ dagrt_status marshal(dagrt_ctx c, const KernelRec& k, const dagrt_arg* args, int
     }
     argv[i] = &vals[i];
   }
+  if (k.pre) {  // the hook's value becomes the kernel's first parameter
+    void* extra = nullptr;  // (no device work on the record backend: no hook)
+    if (c->be->real())
+      if (int e = k.pre(vals, nargs, &extra)) return cuda_fail(c, (cudaError_t)e, "pre-launch hook");
+    for (int i = nargs; i > 0; --i) vals[i] = vals[i - 1];
+    vals[0] = (uint64_t)(uintptr_t)extra;
+    for (int i = 0; i <= nargs; ++i) argv[i] = &vals[i];
+  }
   return DAGRT_OK;
 }
 
@@ -1072,6 +1081,7 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
     k.name = b->name;
     k.fn = b->fn;
     k.coop = (b->flags & KF_COOPERATIVE) != 0;
+    k.pre = b->prelaunch;
     if (b->smem_max > 0 && c->be->real() && b->fn)
       cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
     if (parse_signature(b->signature, &k) != DAGRT_OK) {

@@ -8,8 +8,20 @@ import torch
 import synth
 from .base import SMS, Program, grid_1d
 
-CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64    # csrc/kernels_conv_tc.cu kTcSmem ("conv2" = k_conv2_tc3)
+CONV2_TC_SMEM = 2 * 9 * 512 + 2 * 9 * 4096 + 64    # csrc/kernels_conv_tc.cu kTcSmem (conv2_tc1/tc2/tc3)
 CONV2_TC_THREADS = 128
+# conv2_tma<MODE> dynamic shared memory (csrc/kernels_conv_tc.cu tma_smem<MODE>):
+# 1 KB alignment slack + 3 x 36 KB TMA stages + lo (and hi) A tiles + B tiles + barriers
+CONV2_TMA_SMEM = {m: 1024 + 3 * 9 * 4096 + (2 if m == 0 else 1) * 9 * 4096 + 2 * 9 * 512 + 64 for m in (0, 1, 2)}
+# two-group TMA kernels (conv2_tmag<MODE>, 256 threads): 1 (MODE 0) / 2 stages per group, A tiles per group
+CONV2_TMAG_SMEM = {m: 1024 + 2 * (1 if m == 0 else 2) * 9 * 4096 + 2 * (2 if m == 0 else 1) * 9 * 4096
+                   + 2 * 9 * 512 + 64 for m in (0, 1)}
+# input-row ring TMA kernel (conv2_tmar, 288 threads): 12 slots x 12 KB + 2 groups' lo tiles + B + barriers
+CONV2_TMAR_SMEM = 1024 + 12 * 3 * 4096 + 2 * 9 * 4096 + 2 * 9 * 512 + 256
+CONV2_TMAR_THREADS = 288
+# product "conv2" = conv2_tman1 (TMA-gathered A, two consumer groups, 3xTF32 in two chains)
+CONV2_GRID, CONV2_THREADS = 148, 256
+CONV2_SMEM = CONV2_TMAG_SMEM[1]
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
@@ -198,8 +210,8 @@ class DeepLearning(Program):
             P("conv1", g1, 256, [a["y"], a["w1"], a["c1y"], h, w]),
             P("pool", gp, 256, [a["c1x"], a["px"], h1, w1]),
             P("pool", gp, 256, [a["c1y"], a["py"], h1, w1]),
-            P("conv2", G2TC, CONV2_TC_THREADS, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_TC_SMEM),
-            P("conv2", G2TC, CONV2_TC_THREADS, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_TC_SMEM),
+            P("conv2", CONV2_GRID, CONV2_THREADS, [a["px"], a["w2"], a["c2x"], h2, w2], smem=CONV2_SMEM),
+            P("conv2", CONV2_GRID, CONV2_THREADS, [a["py"], a["w2"], a["c2y"], h2, w2], smem=CONV2_SMEM),
             P("concat", gc, 256, [a["c2x"], a["c2y"], a["z"], nz // 2, nz // 2]),
             P("dot", min(gc, 1024), 256, [a["z"], a["wd"], a["r"], nz]),
         ]

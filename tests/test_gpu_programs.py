@@ -341,7 +341,9 @@ def test_dl_full_size_sampled(ctx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc2", "conv2_tc4", "conv2_tc5"])
+@pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc2", "conv2_tc3", "conv2_tc4",
+                                     "conv2_tc5", "conv2_tma0", "conv2_tma1", "conv2_tmag0", "conv2_tmag1",
+                                     "conv2_tman1", "conv2_tmanr1", "conv2_tmar"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
 def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     """The other conv2 kernels (CUDA-core FFMA; the tcgen05 versions with a
@@ -356,9 +358,20 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     o_arr = ctx.register_tensor(f"c2_{variant}_{h}", out)
     if variant == "conv2_ffma":
         ctx.launch(variant, ((w3s + 1) // 2 // 256 + 1, h3), 256, p.a["px"], p.a["w2"], o_arr, h2, w2s)
-    elif variant == "conv2_tc1":
+    elif variant in ("conv2_tc1", "conv2_tc3"):
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+    elif variant == "conv2_tmar":
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAR_SMEM, CONV2_TMAR_THREADS
+        ctx.launch(variant, 148, CONV2_TMAR_THREADS, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TMAR_SMEM)
+    elif variant.startswith("conv2_tmag") or variant.startswith("conv2_tman"):
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAG_SMEM
+        ctx.launch(variant, 148, 256, p.a["px"], p.a["w2"], o_arr, h2, w2s,
+                   smem=CONV2_TMAG_SMEM[int(variant[-1])])
+    elif variant.startswith("conv2_tma"):
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_TMA_SMEM
+        ctx.launch(variant, 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
+                   smem=CONV2_TMA_SMEM[int(variant[-1])])
     elif variant == "conv2_tc2":
         ctx.launch(variant, 2 * 148, 256, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
@@ -377,6 +390,32 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     assert ok, info
     ok, info = close(p.t["c2x"][:h3 * w3s * 16].cpu().numpy().reshape(h3, w3s, 16), ref)
     assert ok, info
+
+
+@pytest.mark.parametrize("h,w", [(515, 517)])
+def test_tensor_core_truncates_fp32_to_tf32(ctx, h, w):
+    """Pins the hardware behaviour the product conv2 relies on: kind::tf32
+    MMAs read an fp32 operand by TRUNCATING it to tf32.  conv2_tma1 (raw TMA
+    box as A_hi, lo = x - trunc(x)) matches the oracle (test above) while
+    conv2_tma2 (same kernel assuming round-to-nearest, lo = x - rn(x)) misses
+    the tolerance on many outputs."""
+    p = DeepLearning(ctx, h=h, w=w)
+    p.load_inputs(1)
+    p.run()
+    ctx.sync()
+    (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
+    from paper_2012_09646_b200.programs.hits_dl import CONV2_TMA_SMEM
+    out = torch.zeros(h3 * w3s * 16, device="cuda")
+    torch.cuda.synchronize()
+    o_arr = ctx.register_tensor(f"c2_rn_{h}", out)
+    ctx.launch("conv2_tma2", 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TMA_SMEM[2])
+    ctx.sync()
+    spec = synth.spec_dl(h, w)
+    w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
+    px = p.t["px"][:h2 * w2s * 8].cpu().numpy().reshape(h2, w2s, 8)
+    ref = odl.conv3x3s2(px, w2)
+    ok, info = close(out.cpu().numpy().reshape(h3, w3s, 16), ref)
+    assert not ok, "round-to-nearest reading unexpectedly within tolerance"
 
 
 @pytest.mark.parametrize("variant", ["spmv_sync", "spmv_as1", "spmv_x0s1", "spmv_x1s1"])
