@@ -15,6 +15,9 @@ namespace dagrt {
 // column pairs (no integer division).  Inputs: per tap row one float4
 // (columns 4j..4j+3) plus column 4j-1 from the neighbouring lane (shuffle);
 // outputs: 4 x 128-bit stores (64 contiguous bytes per thread).
+// CS: stores with the evict-first (.cs) policy -- the 2 GB output streams
+// through L2 without evicting the input rows the next output row re-reads.
+template <bool CS = false>
 __device__ __forceinline__ void conv1_body(const float* __restrict__ x, const float* __restrict__ w,
                                            float* __restrict__ out, int H, int W) {
   const int H1 = (H + 1) / 2, W1 = (W + 1) / 2;
@@ -85,11 +88,15 @@ __device__ __forceinline__ void conv1_body(const float* __restrict__ x, const fl
       o[1][k] = fmaxf(s1, 0.f);
     }
     float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W1 + 2 * j) * 8);
-    dst[0] = make_float4(o[0][0], o[0][1], o[0][2], o[0][3]);
-    dst[1] = make_float4(o[0][4], o[0][5], o[0][6], o[0][7]);
+    auto st = [&](float4* d, float4 v) {
+      if (CS) __stcs(d, v);
+      else *d = v;
+    };
+    st(dst + 0, make_float4(o[0][0], o[0][1], o[0][2], o[0][3]));
+    st(dst + 1, make_float4(o[0][4], o[0][5], o[0][6], o[0][7]));
     if (2 * j + 1 < W1) {
-      dst[2] = make_float4(o[1][0], o[1][1], o[1][2], o[1][3]);
-      dst[3] = make_float4(o[1][4], o[1][5], o[1][6], o[1][7]);
+      st(dst + 2, make_float4(o[1][0], o[1][1], o[1][2], o[1][3]));
+      st(dst + 3, make_float4(o[1][4], o[1][5], o[1][6], o[1][7]));
     }
   }
 }
@@ -106,6 +113,10 @@ __global__ void __launch_bounds__(256, 3) k_conv1_b3(const float* __restrict__ x
 __global__ void __launch_bounds__(256, 4) k_conv1_b4(const float* __restrict__ x, const float* __restrict__ w,
                                                      float* __restrict__ out, int H, int W) {
   conv1_body(x, w, out, H, W);
+}
+__global__ void __launch_bounds__(256, 4) k_conv1_b4cs(const float* __restrict__ x, const float* __restrict__ w,
+                                                       float* __restrict__ out, int H, int W) {
+  conv1_body<true>(x, w, out, H, W);
 }
 
 // POOL: 2x2 mean, stride 2, 8 channels (two float4 per pixel).
@@ -255,6 +266,7 @@ static const Builtin kDl[] = {
     {"conv1", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b3", (const void*)k_conv1_b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_b4cs", (const void*)k_conv1_b4cs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
     // CUDA-core variant of the second convolution (the tcgen05 one is "conv2")

@@ -31,3 +31,43 @@ __global__ void __launch_bounds__(256) k_read_mapped(const unsigned char* __rest
 const void* read_mapped_kernel() { return (const void*)k_read_mapped; }
 
 }  // namespace dagrt
+
+namespace dagrt {
+
+// Peak probes (tools/box_peaks.py, SURVEY §8(d) "peaks to measure once per
+// box"): `iters` x 8 independent FMA chains per thread, result kept live
+// through a data-dependent store.  Not DAG vertices of any benchmark.
+__global__ void __launch_bounds__(256) k_peak_dfma(double* out, long long iters) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-9 + i;
+  const double m = 1.0000001, c = 1e-7;
+  for (long long k = 0; k < iters; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == -1.0) out[threadIdx.x] = s;
+}
+__global__ void __launch_bounds__(256) k_peak_ffma(float* out, long long iters) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-9f + i;
+  const float m = 1.0000001f, c = 1e-7f;
+  for (long long k = 0; k < iters; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], m, c);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == -1.f) out[threadIdx.x] = s;
+}
+
+static const Builtin kProbes[] = {
+    {"peak_dfma", (const void*)k_peak_dfma, "out ptr, sint64", KF_NONE},
+    {"peak_ffma", (const void*)k_peak_ffma, "out ptr, sint64", KF_NONE},
+};
+DAGRT_REGISTER_BUILTINS(kProbes);
+
+}  // namespace dagrt

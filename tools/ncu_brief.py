@@ -20,12 +20,12 @@ def main(rep):
                 return float("nan")
         tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(
             units.get("gpu__time_duration.sum", "ns"), 1e-3)
-        bscale = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}.get(
-            units.get("dram__bytes_read.sum", "byte"), 1e-9)
+        def bsc(k):  # read and write sums can come in different units
+            return {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}.get(units.get(k, "byte"), 1e-9)
         print(f"== {name}  dur {g('gpu__time_duration.sum')*tscale:.1f} us  dram {g('dram__throughput.avg.pct_of_peak_sustained_elapsed'):.1f}%  "
               f"sm {g('sm__throughput.avg.pct_of_peak_sustained_elapsed'):.1f}%  occ {g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f}%  "
               f"regs {g('launch__registers_per_thread'):.0f}  L2hit {g('lts__t_sector_hit_rate.pct'):.1f}%  "
-              f"dramGB {(g('dram__bytes_read.sum')+g('dram__bytes_write.sum'))*bscale:.3f}")
+              f"dramGB {g('dram__bytes_read.sum')*bsc('dram__bytes_read.sum')+g('dram__bytes_write.sum')*bsc('dram__bytes_write.sum'):.3f}")
         st = [(k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''), g(k))
               for k in hdr if k.startswith('smsp__average_warps_issue_stalled_') and k.endswith('_per_issue_active.ratio')]
         st = sorted([s for s in st if s[1] == s[1]], key=lambda s: -s[1])[:6]
