@@ -168,6 +168,13 @@ typedef struct {
   const dagrt_arg* args;
 } dagrt_launch_desc;
 dagrt_status dagrt_launch_prepared(dagrt_ctx ctx, const dagrt_launch_desc* d);
+/* n consecutive launches descs[0..n-1] in program order: exactly the same as
+ * n dagrt_launch_prepared calls (each is its own DAG vertex, dependencies are
+ * inferred launch by launch); stops at the first failing launch and returns
+ * its status (the launches before it have been issued).  For bindings whose
+ * per-call cost is comparable to a launch (Python: ~2.5 us per call on the
+ * B200 box host). */
+dagrt_status dagrt_launch_batch(dagrt_ctx ctx, const dagrt_launch_desc* descs, int32_t n);
 
 /* ---------------------------------------------------------------- host access */
 

@@ -1402,6 +1402,14 @@ dagrt_status dagrt_launch_prepared(dagrt_ctx c, const dagrt_launch_desc* d) {
   return dagrt_launch(c, d->kernel, d->grid, d->block, d->smem, d->args, d->nargs);
 }
 
+dagrt_status dagrt_launch_batch(dagrt_ctx c, const dagrt_launch_desc* d, int32_t n) {
+  if (n < 0 || (n > 0 && !d)) return c ? fail(c, DAGRT_EINVAL, "bad launch batch") : DAGRT_EINVAL;
+  for (int32_t i = 0; i < n; ++i)
+    if (dagrt_status s = dagrt_launch(c, d[i].kernel, d[i].grid, d[i].block, d[i].smem, d[i].args, d[i].nargs))
+      return s;
+  return DAGRT_OK;
+}
+
 dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes, void* dst) {
   GUARD(c);
   ArrayRec* a = get_array(c, h);

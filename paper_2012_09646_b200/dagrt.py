@@ -105,6 +105,7 @@ def lib():
     L.dagrt_launch_raw.argtypes = [ctx, C.c_uint32, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32,
                                    C.c_void_p]
     L.dagrt_launch_prepared.argtypes = [ctx, C.c_void_p]
+    L.dagrt_launch_batch.argtypes = [ctx, C.c_void_p, C.c_int32]
     L.dagrt_host_read.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
     L.dagrt_host_write.argtypes = [ctx, C.c_uint64, C.c_size_t, C.c_size_t, C.c_void_p]
     L.dagrt_host_map.argtypes = [ctx, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p)]
@@ -136,7 +137,8 @@ def lib():
         pass
     for fn in ("dagrt_create", "dagrt_destroy", "dagrt_array_register", "dagrt_array_unregister",
                "dagrt_array_device_ptr", "dagrt_kernel_register", "dagrt_kernel_lookup",
-               "dagrt_kernel_signature", "dagrt_launch", "dagrt_launch_prepared", "dagrt_launch_raw",
+               "dagrt_kernel_signature", "dagrt_launch", "dagrt_launch_prepared", "dagrt_launch_batch",
+               "dagrt_launch_raw",
                "dagrt_host_read",
                "dagrt_host_write", "dagrt_host_map", "dagrt_host_unmap", "dagrt_sync",
                "dagrt_dag_export", "dagrt_dag_clear", "dagrt_trace_export", "dagrt_stats",
@@ -228,6 +230,28 @@ class Launch:
     def raw(self, stream_ptr):
         s = lib().dagrt_launch_raw(self._c, self.kernel.handle, self.grid, self.block, self.smem,
                                    self.args, self.n, C.c_void_p(stream_ptr))
+        if s:
+            self.ctx._raise(s)
+
+
+class Batch:
+    """Prepared launches issued in program order by ONE call
+    (dagrt_launch_batch): the same DAG, streams and events as calling each
+    Launch in turn, one Python->C transition instead of len(launches)."""
+    __slots__ = ("ctx", "launches", "_arr", "_n", "_fn", "_c", "_p")
+
+    def __init__(self, ctx, launches):
+        self.ctx, self.launches = ctx, list(launches)
+        self._n = len(self.launches)
+        self._arr = (LaunchDesc * max(1, self._n))()
+        for i, L in enumerate(self.launches):
+            C.memmove(C.byref(self._arr, i * C.sizeof(LaunchDesc)), L._dp, C.sizeof(LaunchDesc))
+        self._p = C.addressof(self._arr)
+        self._fn = lib().dagrt_launch_batch
+        self._c = ctx._c
+
+    def __call__(self):
+        s = self._fn(self._c, self._p, self._n)
         if s:
             self.ctx._raise(s)
 
@@ -366,6 +390,10 @@ class Context:
 
     def launch(self, kernel, grid, block, *args, smem=0):
         self.prepare(kernel, grid, block, args, smem)()
+
+    def batch(self, launches):
+        """Prepared launches -> one callable that issues them in order (Batch)."""
+        return Batch(self, launches)
 
     # -- host access
     def host_read(self, a: Array, dst_ptr, off=0, nbytes=None):

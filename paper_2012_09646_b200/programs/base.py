@@ -141,7 +141,21 @@ class Program:
         self.end_run()
 
     def launch_all(self):
-        raise NotImplementedError
+        """The program's launches in order, issued by one dagrt_launch_batch
+        call (identical to calling each prepared launch in turn).  The batch
+        is rebuilt if the launch list changed; callables that are not
+        prepared launches (e.g. tracing wrappers in tests) are called in turn."""
+        seq = self.launch_sequence()
+        key = tuple(map(id, seq))
+        if getattr(self, "_batch_key", None) != key:
+            self._batch_key = key
+            self._batch = (self.ctx.batch(seq) if all(isinstance(L, D.Launch) for L in seq)
+                           else (lambda: [L() for L in seq]))
+        self._batch()
+
+    def launch_sequence(self):
+        """The prepared launches of one run, in program order."""
+        return list(self.L)
 
     # ---------------------------------------------------------- baseline
     def graph(self):

@@ -127,10 +127,8 @@ class Hits(Program):
             if name in self.mirror:
                 self.mirror[name].fill_(v)
 
-    def launch_all(self):
-        for _ in range(self.iters):
-            for L in self.it:
-                L()
+    def launch_sequence(self):
+        return [L for _ in range(self.iters) for L in self.it]
 
     def graph(self):
         g = self.ctx.graph()
@@ -222,10 +220,6 @@ class DeepLearning(Program):
         self.fill("y", spec["y"], set_index)
         for k in ("w1", "w2", "wd"):
             self.fill(k, spec[k], 0)
-
-    def launch_all(self):
-        for L in self.L:
-            L()
 
     def graph(self):
         g = self.ctx.graph()

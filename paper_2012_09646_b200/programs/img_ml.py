@@ -52,10 +52,6 @@ class Images(Program):
     def _inputs(self, set_index=0):
         self.fill("img", synth.spec_img(self.h, self.w)["img"], set_index)
 
-    def launch_all(self):
-        for L in self.L:
-            L()
-
     def graph(self):
         g = self.ctx.graph()
         io = self.graph_io(g)
@@ -140,10 +136,6 @@ class MLEnsemble(Program):
 
     def _inputs(self, set_index=0):
         self.fill("X", synth.spec_ml_x(self.n, self.f)["X"], set_index)
-
-    def launch_all(self):
-        for L in self.L:
-            L()
 
     def graph(self):
         g = self.ctx.graph()

@@ -37,10 +37,6 @@ class Vec(Program):
         self.fill("x", spec["x"], set_index)
         self.fill("y", spec["y"], set_index)
 
-    def launch_all(self):
-        for L in self.L:
-            L()
-
     def result(self):
         return float(self.t["z"][:4].view(torch.float32)[0])
 
@@ -80,10 +76,6 @@ class BlackScholes(Program):
         spec = synth.spec_bs(self.n, self.nvec)
         for i in range(self.nvec):
             self.fill(f"s{i}", spec[f"s{i}"], set_index)
-
-    def launch_all(self):
-        for L in self.L:
-            L()
 
     def graph(self):
         g = self.ctx.graph()

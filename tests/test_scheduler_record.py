@@ -238,3 +238,33 @@ def test_prepared_and_plain_launch_same_dag(idx):
                 rp.run([op])
         out.append((rp.dag(), rp.ctx.trace()))
     assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("idx", range(0, len(CASES), max(1, len(CASES) // 6)))
+def test_launch_batch_same_dag(idx):
+    """dagrt_launch_batch over each run of consecutive launches gives the DAG
+    and trace of issuing them one by one."""
+    trace = CASES[idx][1]["trace"]
+    out = []
+    for batched in (False, True):
+        rp = Replayer(arrays_of(trace), 128)
+        pending = []
+
+        def flush():
+            if pending:
+                rp.ctx.batch(pending)()
+                pending.clear()
+        for op in trace:
+            if op[0] == "launch":
+                k = rp.kernel(op[1], [m for _, m in op[2]])
+                L = rp.ctx.prepare(k, 1, 32, [rp.arr[a] for a, _ in op[2]])
+                if batched:
+                    pending.append(L)
+                else:
+                    L()
+            else:
+                flush()
+                rp.run([op])
+        flush()
+        out.append((rp.dag(), rp.ctx.trace()))
+    assert out[0] == out[1]

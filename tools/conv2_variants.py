@@ -81,6 +81,9 @@ def main():
             L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
             L = ctx.prepare(v, G2TC, 128, args, smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
+        elif v == "conv2":  # the product launch configuration (programs/hits_dl.py)
+            from paper_2012_09646_b200.programs.hits_dl import CONV2_GRID, CONV2_SMEM, CONV2_THREADS
+            L = ctx.prepare(v, CONV2_GRID, CONV2_THREADS, args, smem=CONV2_SMEM)
         else:
             L = ctx.prepare(v, G2TC, CONV2_TC_THREADS, args, smem=CONV2_TC_SMEM)
         us = timeit(L)

@@ -116,6 +116,40 @@ int main() {
     k_read<<<1, 32, 0, s>>>(a, dm, 2);
     while (((volatile float*)hm)[1] == -1.f) {}
   });
+  // VEC (Fig. 4) through the C ABI, no Python: 2 squares + reduce_diff + host
+  // read of z, N = 1M, resident inputs -- the C-level floor of bench.py's VEC
+  {
+    const long long N = 1000000;
+    float *x, *y, *x1, *y1;
+    void* z;
+    cudaMalloc(&x, N * 4); cudaMalloc(&y, N * 4); cudaMalloc(&x1, N * 4); cudaMalloc(&y1, N * 4);
+    cudaMalloc(&z, 8 + 8 * 1024);
+    cudaMemset(x, 0, N * 4); cudaMemset(y, 0, N * 4); cudaMemset(z, 0, 8 + 8 * 1024);
+    cudaDeviceSynchronize();
+    dagrt_array X, Y, X1, Y1, Z;
+    dagrt_array_register(c, x, nullptr, N * 4, &X);
+    dagrt_array_register(c, y, nullptr, N * 4, &Y);
+    dagrt_array_register(c, x1, nullptr, N * 4, &X1);
+    dagrt_array_register(c, y1, nullptr, N * 4, &Y1);
+    dagrt_array_register(c, z, nullptr, 8 + 8 * 1024, &Z);
+    dagrt_kernel ksq, kred;
+    dagrt_kernel_lookup(c, "square", &ksq);
+    dagrt_kernel_lookup(c, "reduce_diff", &kred);
+    const unsigned g = (unsigned)((N + 2047) / 2048);  // programs/vec_bs.py grid_1d(n, 256, 8)
+    dagrt_arg ax[3], ay[3], ar[4];
+    ax[0].array = X; ax[1].array = X1; ax[2].i64 = N;
+    ay[0].array = Y; ay[1].array = Y1; ay[2].i64 = N;
+    ar[0].array = X1; ar[1].array = Y1; ar[2].array = Z; ar[3].i64 = N;
+    dagrt_dim3 G = {g, 1, 1}, Gr = {g < 1024 ? g : 1024, 1, 1}, B = {256, 1, 1};
+    float zz;
+    bench("VEC DAG via C ABI (3 launches + host read)", [&](int) {
+      dagrt_launch(c, ksq, G, B, 0, ax, 3);
+      dagrt_launch(c, ksq, G, B, 0, ay, 3);
+      dagrt_launch(c, kred, Gr, B, 0, ar, 4);
+      dagrt_host_read(c, Z, 0, 4, &zz);
+    });
+    if (const char* e = dagrt_last_error(c)) if (*e) printf("dagrt: %s\n", e);
+  }
   dagrt_destroy(c);
   return 0;
 }
