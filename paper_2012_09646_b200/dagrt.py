@@ -400,6 +400,19 @@ class Context:
         nb = a.nbytes - off if nbytes is None else nbytes
         self._check(lib().dagrt_host_read(self._c, a.handle, off, nb, C.c_void_p(dst_ptr)))
 
+    def prepare_read(self, a: Array, dst_ptr, off=0, nbytes=None):
+        """A host read with its arguments converted once: calling the result
+        is dagrt_host_read(a, off, nbytes, dst) (same semantics as host_read)."""
+        nb = a.nbytes - off if nbytes is None else nbytes
+        fn, c, args = lib().dagrt_host_read, self._c, (C.c_uint64(a.handle), C.c_size_t(off),
+                                                       C.c_size_t(nb), C.c_void_p(dst_ptr))
+
+        def read():
+            s = fn(c, *args)
+            if s:
+                self._raise(s)
+        return read
+
     def host_write(self, a: Array, src_ptr, off=0, nbytes=None):
         nb = a.nbytes - off if nbytes is None else nbytes
         self._check(lib().dagrt_host_write(self._c, a.handle, off, nb, C.c_void_p(src_ptr)))

@@ -127,9 +127,16 @@ class Program:
 
     def end_run(self):
         """Host reads of the sinks: one element (resident) or whole arrays (stream)."""
+        if self.mode != "stream":
+            if getattr(self, "_reads", None) is None:  # arguments converted once
+                self._reads = [self.ctx.prepare_read(self.a[n], C.addressof(self._scalar), 0,
+                                                     min(4, self.a[n].nbytes)) for n in self.sinks]
+            for r in self._reads:
+                r()
+            return
         for n in self.sinks:
             arr = self.a[n]
-            if self.mode == "stream" and n not in self.red:
+            if n not in self.red:
                 self.ctx.host_map(arr, D.R)
                 self.ctx.host_unmap(arr)
             else:

@@ -80,7 +80,17 @@ def test_program_two_runs_against_oracle(name, mode):
         nb = a.nbytes - off if nbytes is None else nbytes
         calls.append(("host", a.name, "R", off, nb))
         return orig_read(a, dst, off, nbytes)
-    ctx.host_map, ctx.host_read = host_map, host_read
+    orig_prep = ctx.prepare_read
+
+    def prepare_read(a, dst, off=0, nbytes=None):
+        nb = a.nbytes - off if nbytes is None else nbytes
+        r = orig_prep(a, dst, off, nbytes)
+
+        def f():
+            calls.append(("host", a.name, "R", off, nb))
+            r()
+        return f
+    ctx.host_map, ctx.host_read, ctx.prepare_read = host_map, host_read, prepare_read
     mode_of = {D.K_CONST: "R", D.K_INOUT: "RW", D.K_OUT: "O"}
 
     def wrap(L):
