@@ -392,6 +392,30 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     assert ok, info
 
 
+@pytest.mark.parametrize("variant", ["conv1_b1", "conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3cs",
+                                     "conv1_r2b2"])
+@pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
+def test_dl_conv1_variants_bitwise(ctx, h, w, variant):
+    """Every conv1 variant (one or two output rows per iteration, store
+    policies, register caps) gives the product kernel's output bit for bit
+    (same arithmetic in the same order) -- the product is checked against the
+    oracle in test_dl_parity."""
+    p = DeepLearning(ctx, h=h, w=w)
+    p.load_inputs(1)
+    p.run()
+    ctx.sync()
+    (h1, w1s), _, _ = p.shapes
+    out = torch.full_like(p.t["c1x"], -1.0)
+    torch.cuda.synchronize()
+    o_arr = ctx.register_tensor(f"c1_{variant}_{h}", out)
+    L0 = p.L[0]
+    rows = (h1 + 1) // 2 if "_r2" in variant else h1
+    ctx.launch(variant, (L0.grid.x, max(1, min(rows, 7))), 256, p.a["x"], p.a["w1"], o_arr, h, w)
+    ctx.sync()
+    n = h1 * w1s * 8
+    assert torch.equal(out[:n], p.t["c1x"][:n])
+
+
 @pytest.mark.parametrize("h,w", [(515, 517)])
 def test_tensor_core_truncates_fp32_to_tf32(ctx, h, w):
     """Pins the hardware behaviour the product conv2 relies on: kind::tf32

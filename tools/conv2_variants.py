@@ -49,9 +49,10 @@ def main():
         out[name] = {"us": us, "GBps": kb[name + "_x"] / us / 1e3}
     c1ref = p.t["c1x"].clone()
     L0 = p.L[0]
-    for v in ("conv1_b3", "conv1_b4", "conv1_b4cs"):
-        for rows_per in (8, 16):
-            g = (L0.grid.x, max(1, min(h1, -(-rows_per * 148 // L0.grid.x))))
+    for v in ("conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3", "conv1_r2b3cs", "conv1_r2b2"):
+        for rows_per in ((8, 16, 24, 32) if "_r2" in v else (8, 16)):
+            nrows = (h1 + 1) // 2 if "_r2" in v else h1  # the r2 kernels' grid.y walks row pairs
+            g = (L0.grid.x, max(1, min(nrows, -(-rows_per * 148 // L0.grid.x))))
             L = ctx.prepare(v, g, 256, [p.a["x"], p.a["w1"], p.a["c1x"], a.h, a.h])
             us = timeit(L)
             torch.cuda.synchronize()
