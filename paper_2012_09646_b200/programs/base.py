@@ -149,12 +149,14 @@ class Program:
 
     def launch_all(self):
         """The program's launches in order, issued by one dagrt_launch_batch
-        call (identical to calling each prepared launch in turn).  The batch
-        is rebuilt if the launch list changed; callables that are not
-        prepared launches (e.g. tracing wrappers in tests) are called in turn."""
-        seq = self.launch_sequence()
-        key = tuple(map(id, seq))
-        if getattr(self, "_batch_key", None) != key:
+        call (identical to calling each prepared launch in turn).  Callables
+        that are not prepared launches (e.g. tracing wrappers in tests) are
+        called in turn."""
+        # rebuilt when a launch list is replaced (set _batch = None after an
+        # in-place edit of self.L / self.it)
+        key = (id(getattr(self, "L", None)), id(getattr(self, "it", None)))
+        if getattr(self, "_batch", None) is None or self._batch_key != key:
+            seq = self.launch_sequence()
             self._batch_key = key
             self._batch = (self.ctx.batch(seq) if all(isinstance(L, D.Launch) for L in seq)
                            else (lambda: [L() for L in seq]))
