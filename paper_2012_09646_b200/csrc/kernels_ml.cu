@@ -378,88 +378,6 @@ __device__ __forceinline__ void mmul_tma10(const T* __restrict__ A, const float*
   }
 }
 
-// Four threads per row (256 threads, same 64-row TMA tiles): thread q of a
-// row takes the 16-byte feature chunks q, q+4, q+8, ... so the 4 lanes of a
-// row read 64 contiguous bytes per step; twice the warps per SM of the
-// two-threads-per-row version to cover the shared-memory latency of its
-// 11 LDS.128 per 40 FFMA.  The four partial sums are combined with two
-// shuffles per class (fixed tree: deterministic).
-template <typename T>
-__device__ __forceinline__ void mmul_tma10_q4(const T* __restrict__ A, const float* __restrict__ sW,
-                                              unsigned char* smem_tiles, uint64_t* full,
-                                              const float* __restrict__ bias, float* __restrict__ out,
-                                              long long N, int F) {
-  const int t = threadIdx.x, q = t & 3, row = t >> 2;
-  const int nch = F / 4;
-  const size_t tile_bytes = (size_t)kMmRows * F * 4;
-  auto buf = [&](int st) { return reinterpret_cast<T*>(smem_tiles + st * tile_bytes); };
-  const long long ntiles = (N + kMmRows - 1) / kMmRows;
-  float b[10];
-#pragma unroll
-  for (int c = 0; c < 10; ++c) b[c] = bias ? __ldg(bias + c) : 0.f;
-  auto issue = [&](long long tile, int stage) {
-    const long long r0 = tile * kMmRows;
-    const unsigned bytes = (unsigned)(min((long long)kMmRows, N - r0) * F * 4);
-    mbar_expect_tx(&full[stage], bytes);
-    tma_bulk_g2s(buf(stage), A + r0 * F, bytes, &full[stage]);
-  };
-  if (t == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (t == 0) {
-    if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    if ((long long)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
-  }
-  int k = 0;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-    const int stage = k & 1;
-    mbar_wait(&full[stage], (k >> 1) & 1);
-    const long long r0 = tile * kMmRows;
-    const int nrows = (int)min((long long)kMmRows, N - r0);
-    float acc[10];
-#pragma unroll
-    for (int c = 0; c < 10; ++c) acc[c] = q == 0 ? b[c] : 0.f;
-    if (row < nrows) {
-      const T* xr = buf(stage) + (size_t)row * F;
-#pragma unroll 4
-      for (int ch = q; ch < nch; ch += 4) {
-        const float4 x = as_f4<T>(xr + 4 * ch);
-#pragma unroll
-        for (int c = 0; c < 10; ++c) {
-          const float4 w = *reinterpret_cast<const float4*>(sW + c * F + 4 * ch);
-          acc[c] = fmaf(x.x, w.x, acc[c]);
-          acc[c] = fmaf(x.y, w.y, acc[c]);
-          acc[c] = fmaf(x.z, w.z, acc[c]);
-          acc[c] = fmaf(x.w, w.w, acc[c]);
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 10; ++c) {
-      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
-    }
-    if (row < nrows) {
-      float2* o = reinterpret_cast<float2*>(out + (r0 + row) * 10);
-      // lane q writes classes 2q, 2q+1 (and lane 0 also 8, 9)
-      float2 v = make_float2(acc[0], acc[1]);
-      if (q == 1) v = make_float2(acc[2], acc[3]);
-      if (q == 2) v = make_float2(acc[4], acc[5]);
-      if (q == 3) v = make_float2(acc[6], acc[7]);
-      o[q] = v;
-      if (q == 0) o[4] = make_float2(acc[8], acc[9]);
-    }
-    __syncthreads();  // every thread is done with buf[stage]
-    if (t == 0 && tile + 2 * (long long)gridDim.x < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(tile + 2 * (long long)gridDim.x, stage);
-    }
-  }
-}
-
 // shared-memory bytes of the TMA path: W, 2 mbarriers, two row tiles
 __host__ __device__ constexpr size_t mmul_tma_smem(int F) {
   return (size_t)10 * F * 4 + 16 + 2 * (size_t)kMmRows * F * 4;
@@ -473,16 +391,10 @@ __device__ __forceinline__ void mmul_body(const T* A, const float* W, const floa
   __syncthreads();
   const bool tma = C == 10 && (F & 3) == 0 && F <= 200 && ((F / 2) & 3) == 0 &&
                    blockDim.x == kMmThreads && aligned16(A) && (((uintptr_t)out) & 7) == 0;
-  const bool tma4 = C == 10 && (F & 3) == 0 && F <= 200 && blockDim.x == 2 * kMmThreads &&
-                    aligned16(A) && (((uintptr_t)out) & 7) == 0;
   if (tma) {
     uint64_t* full = reinterpret_cast<uint64_t*>(sW + 10 * F);   // 10F*4 is a multiple of 16
     unsigned char* tiles = reinterpret_cast<unsigned char*>(full + 2);
     mmul_tma10<T>(A, sW, tiles, full, bias, out, N, F);
-  } else if (tma4) {
-    uint64_t* full = reinterpret_cast<uint64_t*>(sW + 10 * F);
-    unsigned char* tiles = reinterpret_cast<unsigned char*>(full + 2);
-    mmul_tma10_q4<T>(A, sW, tiles, full, bias, out, N, F);
   } else if (C == 10) {
     mmul_rows<T, 10>(A, sW, bias, out, N, F);
   } else {

@@ -392,34 +392,6 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     assert ok, info
 
 
-@pytest.mark.parametrize("n", [1000, 64 * 37 + 5])
-def test_ml_mmul_four_threads_per_row(ctx, n):
-    """The 256-thread MMUL path (four threads per row, interleaved 16-byte
-    feature chunks) against the oracle's matmul on the program's own inputs."""
-    p = MLEnsemble(ctx, n=n)
-    p.load_inputs(0)
-    p.run()
-    ctx.sync()
-    f, c = p.f, p.c
-    smem = 4 * c * f + 16 + 2 * 64 * 4 * f
-    o1 = torch.zeros(n * c, device="cuda")
-    o2 = torch.zeros(n * c, device="cuda")
-    torch.cuda.synchronize()
-    A1 = ctx.register_tensor(f"mm4_nb_{n}", o1)
-    A2 = ctx.register_tensor(f"mm4_rr_{n}", o2)
-    g = min(-(-n // 64), 296)
-    ctx.launch("nb_mmul", g, 256, p.a["X"], p.a["theta"], p.a["prior"], A1, n, f, c, smem=smem)
-    ctx.launch("rr_mmul", g, 256, p.a["Z"], p.a["W"], A2, n, f, c, smem=smem)
-    ctx.sync()
-    X = p.t["X"].view(n, f).cpu().numpy().astype(np.float64)
-    Z = p.t["Z"].view(n, f).cpu().numpy().astype(np.float64)
-    pr = {k: v.astype(np.float64) for k, v in p.params.items()}
-    ok, info = close(o1.view(n, c).cpu().numpy(), oml.nb_mmul(X, pr["theta"], pr["prior"]))
-    assert ok, ("nb", info)
-    ok, info = close(o2.view(n, c).cpu().numpy(), oml.mmul(Z, pr["W"]))
-    assert ok, ("rr", info)
-
-
 @pytest.mark.parametrize("variant", ["conv1_b1", "conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3cs",
                                      "conv1_r2b2"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])

@@ -1,6 +1,6 @@
 """Time the ML MMUL kernels on the full ML shapes (BASELINE configs[3]:
 10M x 200) with two (128-thread CTAs, the product) and four (256-thread
-CTAs) threads per row; compare their outputs.
+CTAs) threads per row; compare their outputs.  (The four-per-row path was measured slower and removed; the tool now times the product only.)
 
     python tools/mmul_variants.py [--n 10000000]
 """
@@ -41,7 +41,7 @@ def main():
         return e0.elapsed_time(e1) / reps * 1e3
 
     res = {}
-    for threads in (128, 256):
+    for threads in (128,):
         rows = 64
         gm = max(1, min(-(-n // rows), 2 * 148))
         smem = 4 * c * f + 16 + 2 * rows * 4 * f
@@ -54,10 +54,6 @@ def main():
             torch.cuda.synchronize()
             res[(name, threads)] = o
             out[f"{name}_t{threads}"] = {"us": us, "GBps": (4 * n * f + 4 * n * c) / us / 1e3}
-    for name in ("nb_mmul", "rr_mmul"):
-        d = (res[(name, 128)] - res[(name, 256)]).abs()
-        ref = res[(name, 128)].abs()
-        out[f"{name}_max_rel_diff"] = float((d / (ref + 1e-6)).max())
     print(json.dumps(out, indent=1))
 
 
