@@ -1463,6 +1463,173 @@ __global__ void __launch_bounds__(256, 1) k_conv2_tma2n(const CUtensorMap* __res
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(ROWACC ? 512 : 128));
 }
 
+// NG consumer groups with SG TMA stages each (MODE 1, two MMA chains): the
+// two-group kernel generalised, e.g. 3 groups x 1 stage (384 threads).
+template <int NG, int SG>
+constexpr int tmang_smem() {
+  return 1024 + NG * SG * kTmaStage + NG * kTcTaps * kTcATile + 2 * kTcTaps * kTcBTile + 64;
+}
+template <int NG, int SG>
+__global__ void __launch_bounds__(128 * NG, 1) k_conv2_tmang(const CUtensorMap* __restrict__ tmap,
+                                                        const float* __restrict__ in,
+                                                        const float* __restrict__ w,
+                                                        float* __restrict__ out, int H2, int W2) {
+  constexpr int MODE = 1, ROWACC = 0;
+  constexpr int S = NG * SG;
+  constexpr int APART = (MODE == 0 ? 2 : 1) * kTcTaps * kTcATile;  // A tiles per group
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = sm;                                        // [S][9][128 x 32 B], SW32
+  unsigned char* agrp = raw + S * kTmaStage;                      // [2][lo (, hi)]
+  unsigned char* bcat = agrp + NG * APART;  // [9][32 rows x 8 tf32]: rows 0-15 B_hi, 16-31 B_lo
+  uint64_t* full = reinterpret_cast<uint64_t*>(bcat + 2 * kTcTaps * kTcBTile);  // [S]
+  uint64_t* mbar = full + S;                                               // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + NG);
+  const int tid = threadIdx.x, grp = tid >> 7, t = tid & 127, warp = tid >> 5;
+  unsigned char* alo = agrp + grp * APART;
+  unsigned char* ahi = MODE == 0 ? alo + kTcTaps * kTcATile : nullptr;
+  (void)in;
+
+  for (int i = tid; i < 16 * 72; i += 128 * NG) {
+    const int k = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    auto off = [&](int n) { return 2 * tap * kTcBTile + (n & 7) * 16 + (n >> 3) * 256 + (c >> 2) * 128 + (c & 3) * 4; };
+    *reinterpret_cast<float*>(bcat + off(k)) = hi;
+    *reinterpret_cast<float*>(bcat + off(16 + k)) = lo;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)));
+    for (int q = 0; q < NG; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tmem_slot)), "n"(NG <= 2 ? 128 : 256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // per group: acc0 = 32 columns (A_hi x [B_hi | B_lo]), acc1 = 16 columns (A_lo x B_hi)
+  // (ROWACC: one such pair per input row a of the window, 64 columns apart)
+  const uint32_t tmem = *tmem_slot + (uint32_t)((ROWACC ? 192 : 64) * grp);
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long G = gridDim.x;
+  auto issue = [&](long long tile, int st) {
+    const int p = (int)(tile / nqb), q0 = (int)(tile % nqb) * 128;
+    const uint32_t bar = smem_u32(full + st);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(9 * 32 * tma_box_rows(W2))
+                 : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        tma_load_3d(smem_u32(raw + st * kTmaStage + (a * 3 + b) * kTmaTap), tmap, 0, 2 * q0 + b - 1,
+                    2 * p + a - 1, bar);
+  };
+  if (t == 0)  // group g's first SG tiles (it = g + NG k) into its stages g*SG + k
+    for (int k = 0; k < SG; ++k)
+      if ((long long)blockIdx.x + (grp + NG * k) * G < ntiles)
+        issue((long long)blockIdx.x + (grp + NG * k) * G, grp * SG + k);
+  auto group_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+
+  for (int it = grp;; it += NG) {
+    const long long tile = (long long)blockIdx.x + (long long)it * G;
+    if (tile >= ntiles) break;
+    const int k = it / NG;  // the group's k-th tile
+    const int st = grp * SG + k % SG;
+    const long long next = tile + (long long)NG * SG * G;  // the group's tile k + SG, into the same stage
+    tc_mbar_wait(full + st, (uint32_t)((k / SG) & 1));
+    const unsigned char* rs = raw + st * kTmaStage;
+#pragma unroll
+    for (int tap = 0; tap < kTcTaps; ++tap)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x =
+            *reinterpret_cast<const float4*>(rs + tap * kTmaTap + 32 * t + 16 * (h ^ ((t >> 2) & 1)));
+        float4 hi, lo;
+        tf32_split(x.x, hi.x, lo.x);
+        tf32_split(x.y, hi.y, lo.y);
+        tf32_split(x.z, hi.z, lo.z);
+        tf32_split(x.w, hi.w, lo.w);
+        put16(alo + tap * kTcATile, t, h, lo);
+        if (MODE == 0) put16(ahi + tap * kTcATile, t, h, hi);
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0) {
+      if (MODE == 0 && next < ntiles) issue(next, st);
+#pragma unroll
+      for (int tap = 0; tap < kTcTaps; ++tap) {
+        const uint64_t dah = MODE == 0 ? umma_desc(smem_u32(ahi + tap * kTcATile), 128, 256)
+                                       : umma_desc_sw32(smem_u32(rs + tap * kTmaTap));
+        const uint64_t dal = umma_desc(smem_u32(alo + tap * kTcATile), 128, 256);
+        const uint64_t dbc = umma_desc(smem_u32(bcat + 2 * tap * kTcBTile), 128, 256);
+        // two independent accumulation chains (18 MMAs instead of 27)
+        const uint32_t ta = ROWACC ? tmem + 64 * (tap / 3) : tmem;
+        const uint32_t first = ROWACC ? (tap % 3 > 0) : (tap > 0);
+        tc_mma_n(ta, dah, dbc, first, kTcIdescN32);
+        tc_mma_n(ta + 32, dal, dbc, first, kTcIdesc);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(mbar + grp))
+                   : "memory");
+    }
+    tc_mbar_wait(mbar + grp, (uint32_t)(k & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (MODE != 0 && t == 0 && next < ntiles) issue(next, st);
+    uint32_t r[16], r1[16], r2[16];
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    tmem_ld16(taddr, r);
+    tmem_ld16(taddr + 16, r1);
+    tmem_ld16(taddr + 32, r2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int n = 0; n < 16; ++n)
+      r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r2[n]) + __uint_as_float(r1[n]));
+    if (ROWACC) {
+#pragma unroll
+      for (int a = 1; a < 3; ++a) {
+        tmem_ld16(taddr + 64 * a, r1);
+        tmem_ld16(taddr + 64 * a + 16, r2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int n = 0; n < 16; ++n)
+          r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r1[n]) + __uint_as_float(r2[n]));
+        tmem_ld16(taddr + 64 * a + 32, r1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int n = 0; n < 16; ++n) r[n] = __float_as_uint(__uint_as_float(r[n]) + __uint_as_float(r1[n]));
+      }
+    }
+    const int p = (int)(tile / nqb), q = (int)(tile % nqb) * 128 + t;
+    if (q < W3) {
+      float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(fmaxf(__uint_as_float(r[4 * k]), 0.f), fmaxf(__uint_as_float(r[4 * k + 1]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 2]), 0.f),
+                             fmaxf(__uint_as_float(r[4 * k + 3]), 0.f));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    group_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(NG <= 2 ? 128 : 256));
+}
+
 // Ring version: the TMA pipeline is cut per INPUT ROW instead of per tile.
 // Slot = the 3 boxes of one input row a of one tile (12 KB); R = 12 slots =
 // 4 tiles in flight (the two-group kernel held 2: its waits on TMA data --
@@ -1698,9 +1865,10 @@ int conv2_tma_prelaunch(const uint64_t* vals, int nargs, void** extra) {
 }
 
 static const Builtin kConvTc[] = {
-    // product: TMA-gathered A (k_conv2_tma2n<1,0> = "conv2_tman1": 303 us per
-    // branch; 148 CTAs of 256 threads, tma2g_smem<1>() bytes, tensor map built by
-    // the pre-launch hook).  Before it: the first version with its gathers two
+    // product: TMA-gathered A, three consumer groups with one TMA stage each
+    // (k_conv2_tmang<3,1> = "conv2_tman3x1": 285 us per branch; 148 CTAs of 384
+    // threads, tmang_smem<3,1>() bytes, tensor map built by the pre-launch
+    // hook); two groups x two stages (k_conv2_tma2n<1,0> = "conv2_tman1") 303-320 us.  Before it: the first version with its gathers two
     // tiles ahead (k_conv2_tc3 = "conv2_tc3", 350 us); the first version (A from per-thread gathers, next tile's loads
     // in flight during the MMAs, 2 CTAs/SM): 357 us per branch on the full DL
     // shapes with L1-allocating gathers and the ALU hi/lo split (441 us with
@@ -1708,8 +1876,8 @@ static const Builtin kConvTc[] = {
     // us for the cp.async-ring versions, whose loop-top barrier waits on the
     // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
-    {"conv2", (const void*)k_conv2_tma2n<1, 0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     tma2g_smem<1>(), conv2_tma_prelaunch},
+    {"conv2", (const void*)k_conv2_tmang<3, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
+     tmang_smem<3, 1>(), conv2_tma_prelaunch},
     // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
     {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC3Smem},
@@ -1725,6 +1893,9 @@ static const Builtin kConvTc[] = {
     // two consumer groups, 3xTF32 as two chains (N = 32 and N = 16), 148 CTAs of 256
     {"conv2_tman1", (const void*)k_conv2_tma2n<1, 0>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      tma2g_smem<1>(), conv2_tma_prelaunch},
+    // NG groups x SG stages (128 NG threads, 148 CTAs)
+    {"conv2_tman3x1", (const void*)k_conv2_tmang<3, 1>, "const ptr, const ptr, out ptr, sint32, sint32",
+     KF_NONE, tmang_smem<3, 1>(), conv2_tma_prelaunch},
     // ... and one accumulator pair per input row of the window (6 chains of 3 MMAs)
     {"conv2_tmanr1", (const void*)k_conv2_tma2n<1, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      tma2g_smem<1>(), conv2_tma_prelaunch},

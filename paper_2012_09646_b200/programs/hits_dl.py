@@ -19,9 +19,10 @@ CONV2_TMAG_SMEM = {m: 1024 + 2 * (1 if m == 0 else 2) * 9 * 4096 + 2 * (2 if m =
 # input-row ring TMA kernel (conv2_tmar, 288 threads): 12 slots x 12 KB + 2 groups' lo tiles + B + barriers
 CONV2_TMAR_SMEM = 1024 + 12 * 3 * 4096 + 2 * 9 * 4096 + 2 * 9 * 512 + 256
 CONV2_TMAR_THREADS = 288
-# product "conv2" = conv2_tman1 (TMA-gathered A, two consumer groups, 3xTF32 in two chains)
-CONV2_GRID, CONV2_THREADS = 148, 256
-CONV2_SMEM = CONV2_TMAG_SMEM[1]
+# product "conv2" = conv2_tman3x1 (TMA-gathered A, three consumer groups with one
+# TMA stage each, 3xTF32 in two MMA chains); csrc/kernels_conv_tc.cu tmang_smem<3, 1>
+CONV2_GRID, CONV2_THREADS = 148, 384
+CONV2_SMEM = 1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)

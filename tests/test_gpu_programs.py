@@ -343,7 +343,7 @@ def test_dl_full_size_sampled(ctx):
 
 @pytest.mark.parametrize("variant", ["conv2_ffma", "conv2_tc1", "conv2_tc2", "conv2_tc3", "conv2_tc4",
                                      "conv2_tc5", "conv2_tma0", "conv2_tma1", "conv2_tmag0", "conv2_tmag1",
-                                     "conv2_tman1", "conv2_tmanr1", "conv2_tmar"])
+                                     "conv2_tman1", "conv2_tmanr1", "conv2_tmar", "conv2_tman3x1"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
 def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     """The other conv2 kernels (CUDA-core FFMA; the tcgen05 versions with a
@@ -361,6 +361,9 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
     elif variant in ("conv2_tc1", "conv2_tc3"):
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+    elif variant == "conv2_tman3x1":
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_SMEM
+        ctx.launch(variant, 148, 384, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_SMEM)
     elif variant == "conv2_tmar":
         from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAR_SMEM, CONV2_TMAR_THREADS
         ctx.launch(variant, 148, CONV2_TMAR_THREADS, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TMAR_SMEM)

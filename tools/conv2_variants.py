@@ -67,6 +67,8 @@ def main():
             L = ctx.prepare(v, ((w3 + 1) // 2 // 256 + 1, min(h3, 65535)), 256, args)
         elif v in ("conv2_tc1", "conv2_tc3"):
             L = ctx.prepare(v, 2 * 148, 128, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
+        elif v == "conv2_tman3x1":
+            L = ctx.prepare(v, 148, 384, args, smem=1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64)
         elif v == "conv2_tmar":
             from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAR_SMEM, CONV2_TMAR_THREADS
             L = ctx.prepare(v, 148, CONV2_TMAR_THREADS, args, smem=CONV2_TMAR_SMEM)
