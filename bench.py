@@ -343,6 +343,12 @@ def main():
         csctx = D.Context(device=local, graph_cache=True)
         csprog = make_program(name, csctx, "stream", share=eprog)
         res["f1_graph_cache_stream_ms"] = time_steps(csprog.run, K, W, dist) / K
+        # ablation: the parallel scheduler with the
+        # prefetcher off -- each H2D is issued on its consumer's own stream
+        # (L356-366 / L662-664 describe the prefetch this removes)
+        nctx = D.Context(device=local, prefetch=False)
+        nprog = make_program(name, nctx, "stream", share=eprog)
+        res["parallel_no_prefetch_stream_ms"] = time_steps(nprog.run, K, W, dist) / K
 
     if rank != 0:
         return
