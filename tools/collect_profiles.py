@@ -41,6 +41,23 @@ def main(tag):
                      f"{(r['frac'] or 0):.3f} | {d['clocks'].get('sm_mhz')} MHz {d['clocks'].get('reasons')} |")
         shutil.copy(p, os.path.join(PROF, f"{tag}_bench_{b}.json"))
     lines.append("")
+    abl = []
+    for b in ["vec", "bs", "img", "ml", "hits", "dl"]:
+        p = os.path.join(OUT, f"bench_{b}.json")
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        bl = d.get("baselines", {})
+        if "parallel_no_prefetch_stream_ms" in bl:
+            abl.append(f"| {b} | {d['e2e']['value']:.3f} | {bl['parallel_no_prefetch_stream_ms']:.3f} | "
+                       f"{bl.get('serial_stream_ms', float('nan')):.3f} |")
+    if abl:
+        lines.append("## Ablation: the prefetcher (stream mode, ms per DAG; PAPER.md L356-366)\n")
+        lines.append("| bench | parallel + prefetch | parallel, prefetch off | serial-sync |")
+        lines.append("|---|---|---|---|")
+        lines += abl
+        lines.append("")
     traffic = {}
     for csvp in sorted(glob.glob(os.path.join(OUT, "ncu_*.csv"))):
         b = os.path.basename(csvp)[4:-4]
