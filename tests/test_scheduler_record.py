@@ -268,3 +268,20 @@ def test_launch_batch_same_dag(idx):
         flush()
         out.append((rp.dag(), rp.ctx.trace()))
     assert out[0] == out[1]
+
+
+def test_launch_batch_stops_at_first_error():
+    """dagrt_launch_batch issues the launches before a failing one and
+    returns that launch's status (ESIG for an argument-count mismatch)."""
+    rp = Replayer({"x", "y"}, 64)
+    k = rp.kernel("k", ["R", "O"])
+    good = rp.ctx.prepare(k, 1, 32, [rp.arr["x"], rp.arr["y"]])
+    arr = (D.LaunchDesc * 3)()
+    for i in range(3):
+        C.memmove(C.byref(arr, i * C.sizeof(D.LaunchDesc)), good._dp, C.sizeof(D.LaunchDesc))
+    arr[1].nargs = 1  # signature has 2
+    s = D.lib().dagrt_launch_batch(rp.ctx._c, C.addressof(arr), 3)
+    assert s == D.ESIG
+    verts, _ = rp.dag()
+    assert len(verts) == 1  # only the first launch became a vertex
+    assert D.lib().dagrt_launch_batch(rp.ctx._c, None, 0) == 0
