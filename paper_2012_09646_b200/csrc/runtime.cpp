@@ -1349,16 +1349,19 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
                                     a->bytes))
         return st_;
       a->coh = COH_BOTH;
+      // the copy's event orders every later reader on another stream after
+      // it (with prefetch off the copy runs on this consumer's own stream, so
+      // only those other readers wait)
+      if (!a->h2d_ev) CK(c->be->event_create(&a->h2d_ev), "cudaEventCreate");
+      CK(c->be->record(a->h2d_ev, cs), "cudaEventRecord copy");
       if (c->cfg.prefetch) {
-        if (!a->h2d_ev) CK(c->be->event_create(&a->h2d_ev), "cudaEventCreate");
-        CK(c->be->record(a->h2d_ev, cs), "cudaEventRecord copy");
         trace_op(c, DAGRT_OP_WAIT_COPY, sid, array_index(c, a), 0, 0);
         CK(c->be->wait(s, a->h2d_ev), "cudaStreamWaitEvent copy");
         c->st.copy_waits++;
-        a->h2d_pending = true;
-        a->h2d_consumer = vid;
-        a->h2d_stream = sid;
       }
+      a->h2d_pending = true;
+      a->h2d_consumer = vid;
+      a->h2d_stream = sid;  // ordered after the copy in both modes
     } else if (a->h2d_pending && a->h2d_stream != sid) {
       trace_op(c, DAGRT_OP_WAIT_COPY, sid, array_index(c, a), 0, 0);
       CK(c->be->wait(s, a->h2d_ev), "cudaStreamWaitEvent copy");

@@ -74,6 +74,33 @@ def test_img_parity(ctx, h, w):
     assert abs(mn - o["mn"]) <= 1e-4 * abs(o["mx"]) + 1e-6
 
 
+@pytest.mark.parametrize("prefetch", [True, False])
+def test_img_stream_copy_precedes_all_readers(prefetch):
+    """Stream mode: the input image (host-newer every run) is read by three
+    blurs on three streams; its H2D must precede all of them, with and
+    without the prefetcher.  The device copy is poisoned with NaN before the
+    run, so a reader that is not ordered after the copy shows up as NaN."""
+    from paper_2012_09646_b200 import dagrt as D
+    c = D.Context(device=0, prefetch=prefetch)
+    h = w = 2048
+    p = Images(c, h=h, w=w, mode="stream")
+    p.load_inputs(0)
+    for _ in range(2):
+        p.t["img"].fill_(float("nan"))
+        torch.cuda.synchronize()
+        p.run()
+        c.sync()
+        for name in ("bs", "bl", "bu", "i3"):
+            assert not torch.isnan(p.t[name]).any(), name
+    img = synth.draw(p.seed, "img", synth.spec_img(h, w)["img"]).reshape(h, w)
+    o = oimg.img_pipeline(img)
+    ok, info = close(p.t["i3"].cpu().numpy().reshape(h, w), o["i3"])
+    assert ok, info
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
 def _img_chunk_oracle(seed, h, w, r0, r1):
     """Oracle over rows [r0, r1) of the full image (with a 4-row halo)."""
     a0, a1 = max(0, r0 - 4), min(h, r1 + 4)

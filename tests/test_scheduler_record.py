@@ -285,3 +285,27 @@ def test_launch_batch_stops_at_first_error():
     verts, _ = rp.dag()
     assert len(verts) == 1  # only the first launch became a vertex
     assert D.lib().dagrt_launch_batch(rp.ctx._c, None, 0) == 0
+
+
+@pytest.mark.parametrize("prefetch", [True, False])
+def test_copy_orders_readers_on_other_streams(prefetch):
+    """A host-newer input read by two independent kernels (two streams): its
+    one H2D must precede BOTH.  With the prefetcher the copy runs on the copy
+    stream and both consumers wait on its event; without it the copy runs on
+    the first consumer's stream and the second consumer (other stream) waits
+    on the copy's event."""
+    rp = Replayer({"x", "y", "z"}, prefetch=prefetch)
+    ctx = rp.ctx
+    ctx.host_map(rp.arr["x"], D.W)
+    ctx.host_unmap(rp.arr["x"])
+    k = rp.kernel("k", ["R", "O"])
+    ctx.prepare(k, 1, 1, [rp.arr["x"], rp.arr["y"]])()
+    ctx.prepare(k, 1, 1, [rp.arr["x"], rp.arr["z"]])()
+    tr = ctx.trace()
+    h2d = [t for t in tr if t[0] == "h2d"]
+    assert len(h2d) == 1
+    verts, _ = rp.dag()
+    s0, s1 = verts[0][3], verts[1][3]
+    assert s0 != s1
+    waits = [t for t in tr if t[0] == "wait_copy"]
+    assert sorted(t[1] for t in waits) == (sorted([s0, s1]) if prefetch else [s1])
