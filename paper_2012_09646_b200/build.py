@@ -77,7 +77,25 @@ def build(verbose=False):
     sdir = os.path.join(ROOT, "synth", "csrc")
     ssrcs = [os.path.join(sdir, f) for f in sorted(os.listdir(sdir)) if f.endswith(".cu")]
     slib = _lib("synth", ssrcs, [], [sdir], os.path.join(ROOT, "synth", "libsynth.so"), verbose)
-    return lib, slib
+    ext = build_fastcall(lib, verbose)
+    return lib, slib, ext
+
+
+def build_fastcall(lib, verbose=False):
+    """CPython METH_FASTCALL module over libdagrt.so (pyext/dagrt_fastcall.c):
+    the per-step calls of the Python binding without ctypes' marshalling."""
+    import sysconfig
+    src = os.path.join(HERE, "pyext", "dagrt_fastcall.c")
+    out = os.path.join(HERE, "_dagrt_fastcall" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not _needs(out, [src, lib, os.path.join(ROOT, "include", "dagrt.h")]):
+        return out
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", f"-I{sysconfig.get_paths()['include']}",
+           f"-I{os.path.join(ROOT, 'include')}", src, "-o", out, f"-L{HERE}", "-ldagrt",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"gcc failed for {src}:\n{r.stderr}")
+    return out
 
 
 if __name__ == "__main__":

@@ -74,6 +74,22 @@ class Stats(C.Structure):
 
 
 _lib = None
+_fast = False
+
+
+def fast():
+    """The CPython fastcall module over libdagrt.so (pyext/dagrt_fastcall.c),
+    or None if it was not built: the same C calls, without ctypes' ~1-2 us of
+    argument marshalling per call."""
+    global _fast
+    if _fast is False:
+        lib()
+        try:
+            from . import _dagrt_fastcall as m
+        except ImportError:
+            m = None
+        _fast = m
+    return _fast
 
 
 def lib():
@@ -247,11 +263,17 @@ class Batch:
         for i, L in enumerate(self.launches):
             C.memmove(C.byref(self._arr, i * C.sizeof(LaunchDesc)), L._dp, C.sizeof(LaunchDesc))
         self._p = C.addressof(self._arr)
-        self._fn = lib().dagrt_launch_batch
         self._c = ctx._c
+        f = fast()
+        if f is not None:
+            cv, p, n, fn = ctx._c.value, self._p, self._n, f.launch_batch
+            self._fn = lambda: fn(cv, p, n)
+        else:
+            cfn, c, p, n = lib().dagrt_launch_batch, ctx._c, self._p, self._n
+            self._fn = lambda: cfn(c, p, n)
 
     def __call__(self):
-        s = self._fn(self._c, self._p, self._n)
+        s = self._fn()
         if s:
             self.ctx._raise(s)
 
@@ -298,7 +320,13 @@ class Graph:
         self.ctx._check(lib().dagrt_graph_instantiate(self.ctx._c, self._h))
 
     def run(self, wait=True):
-        self.ctx._check(lib().dagrt_graph_run(self.ctx._c, self._h, 1 if wait else 0))
+        f = fast()
+        if f is not None:  # same binding speed as the scheduler's batch/read calls
+            s = f.graph_run(self.ctx._c.value, self._h.value, 1 if wait else 0)
+        else:
+            s = lib().dagrt_graph_run(self.ctx._c, self._h, 1 if wait else 0)
+        if s:
+            self.ctx._raise(s)
 
 
 class Context:
@@ -404,11 +432,15 @@ class Context:
         """A host read with its arguments converted once: calling the result
         is dagrt_host_read(a, off, nbytes, dst) (same semantics as host_read)."""
         nb = a.nbytes - off if nbytes is None else nbytes
-        fn, c, args = lib().dagrt_host_read, self._c, (C.c_uint64(a.handle), C.c_size_t(off),
-                                                       C.c_size_t(nb), C.c_void_p(dst_ptr))
+        f = fast()
+        if f is not None:
+            fn, args = f.host_read, (self._c.value, a.handle, off, nb, dst_ptr)
+        else:
+            fn, args = lib().dagrt_host_read, (self._c, C.c_uint64(a.handle), C.c_size_t(off),
+                                               C.c_size_t(nb), C.c_void_p(dst_ptr))
 
         def read():
-            s = fn(c, *args)
+            s = fn(*args)
             if s:
                 self._raise(s)
         return read

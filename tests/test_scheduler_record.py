@@ -309,3 +309,9 @@ def test_copy_orders_readers_on_other_streams(prefetch):
     assert s0 != s1
     waits = [t for t in tr if t[0] == "wait_copy"]
     assert sorted(t[1] for t in waits) == (sorted([s0, s1]) if prefetch else [s1])
+
+
+def test_fastcall_binding_built():
+    """The CPython fastcall module (pyext/dagrt_fastcall.c) is built in-tree
+    and used by the per-step calls (batch, prepared reads, graph runs)."""
+    assert D.fast() is not None
