@@ -9,6 +9,7 @@ the native library is missing it raises.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -265,12 +266,10 @@ class Batch:
         self._p = C.addressof(self._arr)
         self._c = ctx._c
         f = fast()
-        if f is not None:
-            cv, p, n, fn = ctx._c.value, self._p, self._n, f.launch_batch
-            self._fn = lambda: fn(cv, p, n)
+        if f is not None:  # functools.partial: no Python frame per call
+            self._fn = functools.partial(f.launch_batch, ctx._c.value, self._p, self._n)
         else:
-            cfn, c, p, n = lib().dagrt_launch_batch, ctx._c, self._p, self._n
-            self._fn = lambda: cfn(c, p, n)
+            self._fn = functools.partial(lib().dagrt_launch_batch, ctx._c, self._p, self._n)
 
     def __call__(self):
         s = self._fn()
@@ -434,15 +433,17 @@ class Context:
         nb = a.nbytes - off if nbytes is None else nbytes
         f = fast()
         if f is not None:
-            fn, args = f.host_read, (self._c.value, a.handle, off, nb, dst_ptr)
+            call = functools.partial(f.host_read, self._c.value, a.handle, off, nb, dst_ptr)
         else:
-            fn, args = lib().dagrt_host_read, (self._c, C.c_uint64(a.handle), C.c_size_t(off),
-                                               C.c_size_t(nb), C.c_void_p(dst_ptr))
+            call = functools.partial(lib().dagrt_host_read, self._c, C.c_uint64(a.handle),
+                                     C.c_size_t(off), C.c_size_t(nb), C.c_void_p(dst_ptr))
+        raise_ = self._raise
 
         def read():
-            s = fn(*args)
+            s = call()
             if s:
-                self._raise(s)
+                raise_(s)
+        read.call = call  # the bare call (returns the status)
         return read
 
     def host_write(self, a: Array, src_ptr, off=0, nbytes=None):

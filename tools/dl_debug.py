@@ -46,7 +46,7 @@ def main():
                     p.L[i] = ctx.prepare(a.variant, ((w3s + 1) // 2 // 256 + 1, h3), 256, args)
                 elif a.variant == "conv2_tc1":
                     p.L[i] = ctx.prepare(a.variant, 2 * G2TC, 128, args, smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
-        p._batch = None  # the launch list was edited in place
+        p._batch = p._steps = None  # the launch list was edited in place
         p.load_inputs(0)
         if a.trace:
             import torch
