@@ -1804,7 +1804,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_conv2_tmar(const CUtensorMa
 
 // Pre-launch hook: the tensor map of the conv2 input (vals = in, w, out, H2,
 // W2), encoded with the driver's cuTensorMapEncodeTiled and copied once to
-// device memory; cached per (device, pointer, shape).
+// device memory; cached per (device, pointer, shape).  The 128-byte
+// descriptors live for the process (one per distinct input buffer and
+// shape; a reused address with the same shape reuses its still-valid
+// descriptor).  The device is the calling thread's current device, which
+// the scheduler context made current (dagrt_create / the launch thread).
 namespace {
 struct TmapEntry {
   int dev;
