@@ -316,6 +316,9 @@ BS_LEAN_VARIANT(k_bs_l4b2, 4, 2)
 BS_LEAN_VARIANT(k_bs_l2b3, 2, 3)
 BS_LEAN_VARIANT(k_bs_l2b4, 2, 4)
 BS_LEAN_VARIANT(k_bs_l1b4, 1, 4)
+BS_LEAN_VARIANT(k_bs_l3b2, 3, 2)
+BS_LEAN_VARIANT(k_bs_l3b3, 3, 3)
+BS_LEAN_VARIANT(k_bs_l8b1, 8, 1)
 
 // Deeper prefetch without register cost: each thread keeps DEPTH of its own
 // option pairs in flight with 16-byte cp.async into a private shared-memory
@@ -429,6 +432,9 @@ static const Builtin kVecBs[] = {
     {"bs_l2b3", (const void*)k_bs_l2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_l2b4", (const void*)k_bs_l2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_l1b4", (const void*)k_bs_l1b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l3b2", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l3b3", (const void*)k_bs_l3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs_l8b1", (const void*)k_bs_l8b1, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
 };
 DAGRT_REGISTER_BUILTINS(kVecBs);
 

@@ -24,7 +24,8 @@ def main():
     sel = sys.argv[1].split(",") if len(sys.argv) > 1 else None
     for name, waves in (("bs", 2), ("bs_p1b6", 6), ("bs_p2b3", 3), ("bs_p2b4", 4), ("bs_p4b2", 2),
                         ("bs_a3b4", 4), ("bs_a5b4", 4), ("bs_a7b4", 4), ("bs_a5b3", 3),
-                        ("bs_l4b2", 2), ("bs_l2b3", 3), ("bs_l2b4", 4), ("bs_l1b4", 4)):
+                        ("bs_l4b2", 2), ("bs_l2b3", 3), ("bs_l2b4", 4), ("bs_l1b4", 4),
+                        ("bs_l3b2", 2), ("bs_l3b3", 3), ("bs_l8b1", 1)):
         if sel and name not in sel:
             continue
         for grid_mult in (1, 2, 4):
