@@ -22,7 +22,7 @@ namespace dagrt {
 
 constexpr int kImgThreads = 128;
 constexpr int kImgCols = 4 * kImgThreads;  // 512 columns per CTA
-constexpr int kImgRows = 64;               // output rows per CTA
+constexpr int kImgRows = 64;               // default output rows per CTA (the host sizes grid.y)
 
 // Horizontal/vertical 1-D filter functors.
 template <int R>
@@ -83,8 +83,9 @@ __device__ __forceinline__ void stencil_body(const float* __restrict__ src, floa
   __shared__ __align__(16) float row[2][ROWLEN + (4 - (ROWLEN & 3)) % 4];
   const int t = threadIdx.x;
   const int x0 = blockIdx.x * kImgCols;
-  const int y0 = blockIdx.y * kImgRows;
-  const int y1 = min(H, y0 + kImgRows);
+  const int rows = (H + (int)gridDim.y - 1) / (int)gridDim.y;  // output rows per CTA (grid.y sets it)
+  const int y0 = blockIdx.y * rows;
+  const int y1 = min(H, y0 + rows);
   const int cx = x0 + 4 * t;  // first of this thread's 4 columns
   const bool vec = ((W & 3) == 0) && aligned16(src) && aligned16(dst);
 

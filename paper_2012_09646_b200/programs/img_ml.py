@@ -1,6 +1,8 @@
 """IMG and ML host programs (§V-B; Fig. 6; Fig. 10)."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -10,7 +12,8 @@ from .base import SMS, Program, grid_1d
 # IMG readings R-IMG: (diameter, sigma^2); unsharp amount; extend factor
 IMG_BLUR_S, IMG_BLUR_L, IMG_BLUR_U = (3, 0.1), (5, 10.0), (3, 5.0)
 IMG_UNSHARP, IMG_EXTEND = 0.5, 5.0
-IMG_COLS, IMG_ROWS, IMG_THREADS = 512, 64, 128  # stencil tile (csrc/kernels_img.cu)
+IMG_COLS, IMG_THREADS = 512, 128  # stencil tile (csrc/kernels_img.cu)
+IMG_ROWS = int(os.environ.get("DAGRT_IMG_ROWS", "64"))  # output rows per CTA (grid.y = ceil(h / rows))
 
 
 class Images(Program):
