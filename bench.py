@@ -53,7 +53,7 @@ FULL = {
 }
 DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1"}
 # device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
-KSYM = {"square": "k_square", "bs": "k_bs_l4b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv",
+KSYM = {"square": "k_square", "bs": "k_bs_l3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv",
         "conv1": "k_conv1_r2b3"}
 DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32"}
 WORKLOAD = {

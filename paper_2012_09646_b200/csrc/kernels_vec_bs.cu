@@ -415,9 +415,10 @@ __global__ void __launch_bounds__(256, 2) k_bs_p4b2(const double* __restrict__ s
 static const Builtin kVecBs[] = {
     {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE},
     {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE},
-    // product: lean loop, 4 pairs per thread, 2 CTAs/SM, one wave (45.2 us per
-    // 10M options vs 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
-    {"bs", (const void*)k_bs_l4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    // product: lean loop, 3 pairs per thread, 2 CTAs/SM, one wave (44.8 us per
+    // 10M options vs 46.2 for 4 pairs (k_bs_l4b2) in three back-to-back runs,
+    // 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
+    {"bs", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_p4", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a3b4", (const void*)k_bs_a3b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a5b4", (const void*)k_bs_a5b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},

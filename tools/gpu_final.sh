@@ -28,12 +28,12 @@ for b in ${OVERLAP:-bs vec img ml hits dl}; do
   timeout 600 python tools/overlap.py --bench $b --mode stream --out gpurun_out/overlap_${b}_stream.json > gpurun_out/overlap_$b.log 2>&1
   timeout 600 python tools/overlap.py --bench $b --mode resident --out gpurun_out/overlap_${b}_resident.json >> gpurun_out/overlap_$b.log 2>&1
 done
-for kb in ${FULL:-bs:k_bs_l4b2 img:k_blur ml:k_norm hits:k_spmv$ dl:k_conv1_r2b3 dl:k_conv2_tmang}; do
+for kb in ${FULL:-bs:k_bs_l3b2 img:k_blur ml:k_norm hits:k_spmv$ dl:k_conv1_r2b3 dl:k_conv2_tmang}; do
   b=${kb%%:*}; k=${kb##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"${k}" -c 1 -f \
     -o gpurun_out/prof_${k} python tools/profile_dag.py --bench $b --runs 1 > gpurun_out/prof_${k}.log 2>&1
 done
 [ -z "$SKIP_REF" ] && timeout 600 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum \
-  --clock-control none -k regex:"k_bs_l4b2" -c 3 --csv --log-file gpurun_out/fp64_bs.csv \
+  --clock-control none -k regex:"k_bs_l3b2" -c 3 --csv --log-file gpurun_out/fp64_bs.csv \
   python tools/profile_dag.py --bench bs --runs 1 > gpurun_out/fp64_bs.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log
