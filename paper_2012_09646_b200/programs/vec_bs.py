@@ -1,6 +1,8 @@
 """VEC and Black & Scholes host programs (§V-B, Fig. 4, Fig. 6)."""
 from __future__ import annotations
 
+import os
+
 import torch
 
 import synth
@@ -8,6 +10,10 @@ from .base import Program, grid_1d
 
 # B&S constants (readings R-BS in DESIGN.md; the paper prints none)
 BS_R, BS_V, BS_T, BS_K = 0.08, 0.30, 1.0, 60.0
+
+
+# reduce_diff CTAs (deterministic last-block finish over this many partials)
+VEC_RED_CTAS = int(os.environ.get("DAGRT_VEC_RED_CTAS", "1024"))
 
 
 class Vec(Program):
@@ -29,7 +35,7 @@ class Vec(Program):
         self.L = [
             ctx.prepare("square", g, 256, [a["x"], a["x1"], n]),
             ctx.prepare("square", g, 256, [a["y"], a["y1"], n]),
-            ctx.prepare("reduce_diff", min(g, 1024), 256, [a["x1"], a["y1"], a["z"], n]),
+            ctx.prepare("reduce_diff", min(g, VEC_RED_CTAS), 256, [a["x1"], a["y1"], a["z"], n]),
         ]
 
     def _inputs(self, set_index=0):
