@@ -1,26 +1,36 @@
 #!/usr/bin/env python
 """bench.py -- end-to-end ms per DAG of the run-time DAG scheduler (arXiv
-2012.09646) on B200, next to its baselines.
+2012.09646) on B200, next to its baselines, for the paper's six benchmarks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--bench bs|vec|img|ml|hits|dl]
-                    [--impl dagrt|reference] [--suite]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--bench vec|bs|img|ml|hits|dl|all]
+                    [--impl dagrt|reference] [--no-cpu] [--no-baselines]
 
-One step = one DAG of the chosen benchmark through the whole hot path
-(SURVEY §8(a) rows a1-a10): launches through the C ABI (dependency inference,
-stream assignment, event wiring, prefetch), the sm_100a kernels, and the host
-reads of the sinks.  The default workload is BASELINE.json configs[1]
-(B&S, 10 x 10M fp64 options).
+One step = one DAG of a benchmark through the whole hot path (SURVEY §8(a)
+rows a1-a10): launches through the C ABI (dependency inference, stream
+assignment, event wiring, prefetch), the sm_100a kernels, and the host
+reads of the sinks.  By default ALL SIX benchmarks are measured (the suite,
+BASELINE.json configs[0..4] at full size); the printed headline is B&S
+(configs[1], 10 x 10M fp64 options) and the other five ride along under
+"suite".  ``--bench X`` measures one benchmark only (its line is the
+headline).
 
-Printed JSON line (rank 0):
+Printed JSON line (rank 0), headline benchmark:
   value      ms per DAG, job aggregate = max-over-ranks timed ms / DAGs done by
              all ranks; resident mode (inputs in HBM, host reads one element
              of each sink -- the Z[0] pattern of PAPER.md Fig. 4)
   e2e        the same through the C ABI with host buffers: inputs rewritten
-             on the host every step, H2D + D2H inside the timed region
-  baselines  serial-sync policy and the hand-written
-             CUDA Graph with manual dependencies (L1062-1067), both modes
-  roofline   dominant kernel, timed live with events on its launch stream
-  cpu_baseline  the fp64 oracle on this host on a bounded sample (rank 0, N=1)
+             on the host before every step (untimed), H2D + D2H inside the
+             timed region (first launch -> last host read returns, L819-820)
+  baselines  serial-sync policy, the hand-written CUDA
+             Graph with manual dependencies (L1062-1067), both modes; f1 graph
+             cache, single-stream-children policy (L650-654), prefetch off
+  dag_roofline  R_cp (slowest root->sink path's bytes at HBM bandwidth) and
+             R_work (all bytes), as fractions of the measured time
+  contention_free  Fig. 9 estimate (L1195-1201): serial per-vertex times
+             summed along the DAG's longest path
+  roofline   dominant kernel, event-timed live on its own launch stream while
+             it runs alone (serial-sync region) and inside the DAG
+  cpu_baseline  the fp64 oracle on ONE pinned host core, bounded sample
 Under torchrun each rank runs independent DAG instances on its own GPU (no
 collective on the data path; NCCL only for the barrier and the max of the
 timings) -> "scaling": "weak".
@@ -29,6 +39,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -38,9 +49,13 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2012_09646_b200 import replicas  # noqa: E402
+from paper_2012_09646_b200 import measure, replicas  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+ORDER = ["vec", "bs", "img", "ml", "hits", "dl"]
+HEADLINE = "bs"
+UNIT = "ms per DAG"
+METRIC = "end-to-end ms per DAG (resident inputs; job aggregate over GPUs)"
 
 # Full BASELINE.json sizes per benchmark (configs[0..4])
 FULL = {
@@ -51,10 +66,10 @@ FULL = {
     "hits": dict(n=20_000_000, e=60_000_000),
     "dl": dict(h=16384, w=16384),
 }
-DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1"}
+DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv2"}
 # device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
 KSYM = {"square": "k_square", "bs": "k_bs_l3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv",
-        "conv1": "k_conv1_r2b3"}
+        "conv1": "k_conv1_r2b3", "conv2": "k_conv2_tmang"}
 DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32"}
 WORKLOAD = {
     "vec": "VEC: 2 squares + sum of differences, N=1M fp32",
@@ -65,12 +80,12 @@ WORKLOAD = {
     "dl": "DL: two-branch CNN + dense merge, 2 x 16384x16384 fp32",
 }
 
-
 SMS = 148
-# DFMA + DMUL + DADD executed per option by k_bs (ncu dynamic instruction
-# counts, profiles/r1_summary.md) and the FP64 pipe's peak per SM per clock
-# (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained).
-BS_FP64_OPS_PER_OPTION = 46  # 46.4 measured (gpurun_out fp64_bs2.csv -> profiles/)
+# DFMA + DMUL + DADD executed per option by the product B&S kernel (ncu
+# dynamic instruction counts, profiles/) and the FP64 pipe's peak per SM per
+# clock (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained;
+# confirmed by the DFMA probe: 63.3 ops/clk/SM, profiles/r1_box_peaks.json).
+BS_FP64_OPS_PER_OPTION = 46
 FP64_OPS_PER_SM_CLK = 64
 
 
@@ -97,6 +112,17 @@ def load_peaks():
             d = json.load(f)
         return d, "measured (MEASURED_PEAKS.json)"
     return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -148,41 +174,73 @@ def make_program(name, ctx, mode, share=None, size=None):
     return PROGRAMS[name](ctx, mode=mode, share=share, **kw)
 
 
-def time_steps(fn, steps, warmup, dist):
+def time_steps(fn, steps, warmup, dist, prep=None):
+    """Device time of `steps` calls of fn.  Without `prep`: one CUDA-event
+    region around all steps (barrier + synchronize on both sides).  With
+    `prep` (host-side input preparation before every step, e.g. HITS
+    restarting from 1/sqrt(N)): each step is its own event-bracketed region
+    (first launch -> the host holds the outputs) and the regions are summed;
+    prep runs outside them."""
     import torch
     for _ in range(warmup):
+        if prep:
+            prep()
         fn()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        fn()
-    e1.record()
-    e1.synchronize()
+    if prep is None:
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:
+        ms = 0.0
+        for _ in range(steps):
+            prep()
+            torch.cuda.synchronize()
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
     if dist:
         ms = replicas.max_over_ranks(ms, dist, device="cuda")
         replicas.barrier(dist)
     return ms
 
 
+def needs_prep(prog):
+    """True if the program prepares its inputs on the host before a run (HITS)."""
+    from paper_2012_09646_b200.programs.base import Program
+    return type(prog).restart is not Program.restart
+
+
 def cpu_oracle_rate(name, budget_s=10.0):
-    """Oracle (fp64, as it stands) on a bounded sample; returns (ms per DAG,
-    sample text, cores).  BLAS thread pools are limited to one thread so the
-    core count is exact."""
+    """Oracle (fp64, as it stands) on a bounded sample, on ONE host core:
+    the process is pinned to one CPU (sched_setaffinity, like taskset) and
+    BLAS pools are limited to one thread.  Returns (ms per DAG, sample
+    text, cores)."""
     from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=1):
-        return _cpu_oracle_rate(name, budget_s)
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    try:
+        if old:
+            os.sched_setaffinity(0, {min(old)})
+        with threadpool_limits(limits=1):
+            return _cpu_oracle_rate(name, budget_s)
+    finally:
+        if old:
+            os.sched_setaffinity(0, old)
 
 
 def _cpu_oracle_rate(name, budget_s):
-    import numpy as np
     import synth
-    cores = 1  # numpy is single-threaded here (BLAS pools limited above)
+    cores = 1
     if name == "bs":
         from oracle import bs as obs
         n = FULL["bs"]["n"]
@@ -250,15 +308,243 @@ def _cpu_oracle_rate(name, budget_s):
     return el / reps * scale * 1e3, f"{reps} x oracle DAG on a {sample}, x{scale:.0f} to one DAG", cores
 
 
+# ---------------------------------------------------------------- one benchmark
+def fp64_floor_ms(n_options, mhz):
+    return BS_FP64_OPS_PER_OPTION * n_options / (FP64_OPS_PER_SM_CLK * SMS * mhz * 1e6) * 1e3
+
+
+def dag_of(D, name, prog, local, mode):
+    """The inferred DAG of one run (a recording context on the same tensors)."""
+    rctx = D.Context(device=local, record_dag=True)
+    rp = make_program(name, rctx, mode, share=prog)
+    rp.restart()
+    rp.run()
+    rctx.sync()
+    verts, edges = rctx.dag()
+    arr_index = {n: a.handle & 0xFFFFFFFF for n, a in rp.a.items()}
+    rctx.close()
+    return verts, edges, arr_index
+
+
+def serial_vertex_times(D, name, prog, local, mode, runs=2):
+    """Per-kernel (+ its H2D) and per-D2H times under serial scheduling (each
+    kernel alone on the GPU), from the scheduler's event timeline."""
+    sctx = D.Context(device=local, policy="serial")
+    sp = make_program(name, sctx, mode, share=prog)
+    sp.restart()
+    sp.run()
+    sctx.sync()
+    acc_k, acc_h = None, {}
+    for _ in range(runs):
+        sp.restart()
+        sctx.timeline(True)
+        sp.run()
+        items = sctx.timeline_export()
+        sctx.timeline(False)
+        vk = {}
+        d2h = {}
+        for kind, _s, vertex, ident, _b, t0, t1 in items:
+            if kind in ("kernel", "h2d") and vertex >= 0:
+                vk[vertex] = vk.get(vertex, 0.0) + (t1 - t0)
+            elif kind == "d2h":
+                d2h[ident] = d2h.get(ident, 0.0) + (t1 - t0)
+        ks = [vk[v] for v in sorted(vk)]
+        acc_k = ks if acc_k is None else [a + b for a, b in zip(acc_k, ks)]
+        for k, v in d2h.items():
+            acc_h[k] = acc_h.get(k, 0.0) + v
+    sctx.close()
+    return [x / runs for x in acc_k], {k: v / runs for k, v in acc_h.items()}
+
+
+def bench_one(name, args, dist, local, world, peaks, full_report):
+    import torch
+    from paper_2012_09646_b200 import dagrt as D
+    K, W = args.steps, args.warmup
+    peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+
+    # --- resident mode, parallel-async scheduler (the product)
+    ctx = D.Context(device=local)
+    prog = make_program(name, ctx, "resident")
+    prog.load_inputs(0)
+    dom = DOMINANT[name]
+    # nvidia-smi samples every 100 ms and takes ~0.2 s to start: the sampler
+    # runs from before the warm-up through the timed region (same load), so
+    # short regions (B&S: ~5 ms) still get clock samples
+    with Clocks(local) as clk:
+        time.sleep(0.3)
+        for _ in range(W):
+            prog.run()
+        torch.cuda.synchronize()
+        ctx.stats_reset()
+        ms = time_steps(prog.run, K, 0, dist)
+        st = ctx.stats()  # launches etc. of exactly the K timed steps
+        t_end = time.perf_counter() + 0.3
+        while time.perf_counter() < t_end:
+            prog.run()
+        torch.cuda.synchronize()
+    per = ms / K
+    value = replicas.job_ms_per_dag(ms, K, world)
+    # dominant kernel inside the DAG: events on its own launch streams
+    ctx.profile(dom, True)
+    ms_prof = time_steps(prog.run, K, 0, dist)
+    ctx.profile(dom, False)
+    n_dag, sum_dag, busy_dag = ctx.profile_collect(dom)
+
+    res = {}
+    kb = prog.kernel_bytes()
+    vbytes = list(kb.values())
+    floor = None
+    if name == "bs":
+        floor = [fp64_floor_ms(prog.n, mhz)] * len(vbytes)
+    verts, edges, arr_index = dag_of(D, name, prog, local, "resident")
+    r_cp, r_work = measure.dag_rooflines(verts, edges, vbytes, peak, floor)
+
+    # --- serial-sync baseline (+ the dominant kernel alone, event-timed)
+    sctx = D.Context(device=local, policy="serial")
+    sprog = make_program(name, sctx, "resident", share=prog)
+    res["serial_resident_ms"] = time_steps(sprog.run, K, W, dist) / K
+    sctx.profile(dom, True)
+    time_steps(sprog.run, K, 0, dist)
+    sctx.profile(dom, False)
+    n_alone, sum_alone, busy_alone = sctx.profile_collect(dom)
+    sctx.close()
+    if full_report:
+        g = prog.graph()
+        res["graph_resident_ms"] = time_steps(g.run, K, W, dist) / K
+        del g
+        for label, kw in (("f1_graph_cache", dict(graph_cache=True)),
+                          ("single_stream", dict(policy="single_stream"))):
+            c2 = D.Context(device=local, **kw)
+            p2 = make_program(name, c2, "resident", share=prog)
+            res[f"{label}_resident_ms"] = time_steps(p2.run, K, W, dist) / K
+            if label == "f1_graph_cache":
+                res["f1_graph_replays"] = c2.stats()["graph_replays"]
+            c2.close()
+        kms, _ = serial_vertex_times(D, name, prog, local, "resident")
+        cf = measure.contention_free(verts, edges, kms)
+
+    # --- end-to-end (stream mode) through the same C ABI with host buffers
+    ectx = D.Context(device=local)
+    eprog = make_program(name, ectx, "stream", share=prog)
+    eprog.load_inputs(0)
+    prep = eprog.restart if needs_prep(eprog) else None
+    ectx.stats_reset()
+    e2e_ms = time_steps(eprog.run, K, W, dist, prep)
+    est = ectx.stats()
+    steps_done = K + W
+    h2d_ps = est["h2d_bytes"] / steps_done
+    d2h_ps = est["d2h_bytes"] / steps_done
+    if full_report:
+        sectx = D.Context(device=local, policy="serial")
+        seprog = make_program(name, sectx, "stream", share=eprog)
+        res["serial_stream_ms"] = time_steps(seprog.run, K, W, dist, prep and seprog.restart) / K
+        sectx.close()
+        eg = eprog.graph()
+        res["graph_stream_ms"] = time_steps(eg.run, K, W, dist, prep) / K
+        del eg
+        for label, kw in (("f1_graph_cache", dict(graph_cache=True)),
+                          ("single_stream", dict(policy="single_stream")),
+                          ("parallel_no_prefetch", dict(prefetch=False))):
+            c2 = D.Context(device=local, **kw)
+            p2 = make_program(name, c2, "stream", share=eprog)
+            res[f"{label}_stream_ms"] = time_steps(p2.run, K, W, dist, prep and p2.restart) / K
+            c2.close()
+        # Fig. 9 in stream mode: serial kernel + H2D times, D2H on the host vertices
+        sverts, sedges, s_arr = dag_of(D, name, eprog, local, "stream")
+        skms, shms = serial_vertex_times(D, name, eprog, local, "stream")
+        host_ms = {v[0]: shms.get(s_arr.get(v[2], -1), 0.0) for v in sverts if v[1] == "host"}
+        cf_stream = measure.contention_free(sverts, sedges, skms, host_ms)
+    e2e_per = e2e_ms / K
+
+    # --- dominant-kernel roofline
+    per_launch = sum(v for k, v in kb.items() if k.startswith(dom)) / max(1, sum(1 for k in kb if k.startswith(dom)))
+    avg_alone = sum_alone / max(1, n_alone)
+    if name == "bs":
+        unit_work = BS_FP64_OPS_PER_OPTION * prog.n / 1e9  # G fp64 ops per launch
+        fpeak = FP64_OPS_PER_SM_CLK * SMS * mhz * 1e6 / 1e9
+        ach = unit_work / (avg_alone * 1e-3) if avg_alone > 0 else None
+        roof = {"kernel": dom, "bound": "alu", "pipe": "fp64", "achieved": ach, "peak": fpeak,
+                "unit": "G fp64 ops/s", "frac": ach / fpeak if ach else None,
+                "peak_source": f"{FP64_OPS_PER_SM_CLK} fp64 ops/clk/SM (ncu peak_sustained; DFMA probe "
+                               f"63.3) x {SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
+                "hbm_achieved_gbs": per_launch / (avg_alone * 1e-3) / 1e9 if avg_alone > 0 else None}
+    else:
+        ach = per_launch / (avg_alone * 1e-3) / 1e9 if avg_alone > 0 else None
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+    roof.update({"traffic": None, "algorithmic_bytes_per_launch": per_launch, "launches": n_alone,
+                 "avg_launch_ms": avg_alone,
+                 "timing": "CUDA events on the kernel's launch stream around every launch, in a "
+                           "K-step serial-sync region (the kernel alone on the GPU)",
+                 "in_dag": {"launches": n_dag, "avg_launch_ms": sum_dag / max(1, n_dag), "busy_ms": busy_dag,
+                            "union_achieved": (per_launch * n_dag / (busy_dag * 1e-3) / 1e9
+                                               if name != "bs" and busy_dag > 0 else
+                                               (BS_FP64_OPS_PER_OPTION * prog.n * n_dag / (busy_dag * 1e-3) / 1e9
+                                                if busy_dag > 0 else None)),
+                            "profiled_region_ms_per_step": ms_prof / K}})
+    tr, tr_src = load_traffic(name, KSYM[dom])
+    if tr is not None:
+        roof["traffic"] = tr
+        roof["traffic_source"] = tr_src
+
+    out = {
+        "value": value, "ms_per_step": per, "dtype": DTYPE[name],
+        "config": {"workload": WORKLOAD[name], "bench": name, "mode": "resident",
+                   "l2": ("inputs larger than L2 (126 MB): no flush needed" if sum(vbytes) > 2 * 126e6
+                          else "working set L2-resident at this size (BASELINE configs[0]); no flush"),
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": e2e_per / world, "unit": UNIT, "h2d_bytes_per_step": h2d_ps,
+                "d2h_bytes_per_step": d2h_ps,
+                "timed_region": "per step: first launch -> last host read returns; host input "
+                                "preparation (restart) untimed" if prep else
+                                "K steps back to back, inputs host-newer every step"},
+        "gpu_launches": st["launches"],
+        "roofline": roof,
+        "dag_roofline": {"R_cp_ms": r_cp, "R_work_ms": r_work, "frac_cp": r_cp / per,
+                         "frac_work": r_work / per, "frac_bound": max(r_cp, r_work) / per,
+                         "peak_gbs": peak,
+                         "note": "R_cp = slowest root->sink path's algorithmic bytes at HBM bandwidth"
+                                 + (" (B&S vertices: max of HBM and FP64-pipe time)" if name == "bs" else "")
+                                 + "; R_work = all vertex bytes; frac = R / measured ms per DAG"},
+        "clocks": clk.summary(),
+        "scheduler": {"sched_us_per_launch": st["sched_ns"] / max(1, st["launches"]) / 1e3,
+                      "cross_stream_waits_per_dag": st["cross_stream_waits"] / K,
+                      "streams": st["streams"]},
+        "baselines": res,
+        "speedup_vs_serial_resident": res["serial_resident_ms"] / per,
+    }
+    if full_report:
+        out["vs_graph_resident"] = per / res["graph_resident_ms"]
+        out["speedup_vs_serial_stream"] = res["serial_stream_ms"] / e2e_per
+        out["vs_graph_stream"] = e2e_per / res["graph_stream_ms"]
+        out["contention_free"] = {"resident_ms": cf, "stream_ms": cf_stream,
+                                  "resident_frac": cf / per, "stream_frac": cf_stream / e2e_per,
+                                  "method": "Fig. 9 (L1195-1201): per-vertex times under serial "
+                                            "scheduling summed along the DAG's longest path"}
+    for c in (ectx, ctx):
+        c.close()
+    del prog, eprog
+    torch.cuda.empty_cache()
+    return out
+
+
+def geomean(xs):
+    xs = [x for x in xs if x and x > 0]
+    return math.exp(sum(math.log(x) for x in xs) / len(xs)) if xs else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--bench", default="bs", choices=list(FULL))
+    ap.add_argument("--bench", default="all", choices=["all"] + ORDER)
     ap.add_argument("--impl", default="dagrt", choices=["dagrt", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true", help="serial-sync baseline only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -277,161 +563,71 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
 
-    from paper_2012_09646_b200 import dagrt as D
-    name = args.bench
-    K, W = args.steps, args.warmup
-
-    # --- resident mode, parallel-async scheduler (the product)
-    ctx = D.Context(device=local)
-    prog = make_program(name, ctx, "resident")
-    prog.load_inputs(0)
-    dom = DOMINANT[name]
-    ctx.profile(dom, False)
-    # nvidia-smi samples every 100 ms and takes ~0.2 s to start: the sampler
-    # runs from before the warm-up through the timed region (same load), so
-    # short regions (B&S: ~5 ms) still get clock samples
-    with Clocks(local) as clk:
-        time.sleep(0.3)
-        for _ in range(W):
-            prog.run()
-        torch.cuda.synchronize()
-        ctx.stats_reset()
-        ms = time_steps(prog.run, K, 0, dist)
-        st = ctx.stats()  # launches etc. of exactly the K timed steps
-        # keep the GPU under the same load until the sampler has seen it
-        t_end = time.perf_counter() + 0.3
-        while time.perf_counter() < t_end:
-            prog.run()
-        torch.cuda.synchronize()
-    value = replicas.job_ms_per_dag(ms, K, world)
-    # roofline: the same K steps again with the dominant kernel's launches
-    # bracketed by CUDA events on their own launch streams (kept out of the
-    # `value` region: the events add host work the baselines do not pay)
-    ctx.profile(dom, True)
-    ms_prof = time_steps(prog.run, K, 0, dist)
-    ctx.profile(dom, False)
-    n_launch, sum_ms, busy_ms = ctx.profile_collect(dom)
-
-    # --- baselines and end-to-end (stream) mode
-    res = {}
-    if not args.no_baselines:
-        sctx = D.Context(device=local, policy="serial")
-        sprog = make_program(name, sctx, "resident", share=prog)
-        res["serial_resident_ms"] = time_steps(sprog.run, K, W, dist) / K
-        g = prog.graph()
-        res["graph_resident_ms"] = time_steps(g.run, K, W, dist) / K
-    ectx = D.Context(device=local)
-    eprog = make_program(name, ectx, "stream", share=prog)
-    eprog.load_inputs(0)
-    ectx.stats_reset()
-    e2e_ms = time_steps(eprog.run, K, W, dist)
-    est = ectx.stats()
-    steps_done = K + W
-    h2d_ps = est["h2d_bytes"] / steps_done
-    d2h_ps = est["d2h_bytes"] / steps_done
-    if not args.no_baselines:
-        sectx = D.Context(device=local, policy="serial")
-        seprog = make_program(name, sectx, "stream", share=eprog)
-        res["serial_stream_ms"] = time_steps(seprog.run, K, W, dist) / K
-        eg = eprog.graph()
-        res["graph_stream_ms"] = time_steps(eg.run, K, W, dist) / K
-        # NEXT(f1): the same scheduler with deferred submission + batch graph cache
-        cctx = D.Context(device=local, graph_cache=True)
-        cprog = make_program(name, cctx, "resident", share=prog)
-        res["f1_graph_cache_resident_ms"] = time_steps(cprog.run, K, W, dist) / K
-        res["f1_graph_replays"] = cctx.stats()["graph_replays"]
-        csctx = D.Context(device=local, graph_cache=True)
-        csprog = make_program(name, csctx, "stream", share=eprog)
-        res["f1_graph_cache_stream_ms"] = time_steps(csprog.run, K, W, dist) / K
-        # ablation: the parallel scheduler with the
-        # prefetcher off -- each H2D is issued on its consumer's own stream
-        # (L356-366 / L662-664 describe the prefetch this removes)
-        nctx = D.Context(device=local, prefetch=False)
-        nprog = make_program(name, nctx, "stream", share=eprog)
-        res["parallel_no_prefetch_stream_ms"] = time_steps(nprog.run, K, W, dist) / K
+    peaks, _ = load_peaks()
+    names = ORDER if args.bench == "all" else [args.bench]
+    head = HEADLINE if args.bench == "all" else args.bench
+    results = {}
+    for name in names:
+        results[name] = bench_one(name, args, dist, local, world, peaks, not args.no_baselines)
 
     if rank != 0:
         return
-    peaks, peak_src = load_peaks()
-    kb = prog.kernel_bytes()
-    dom_bytes = sum(v for k, v in kb.items() if k.startswith(dom))
-    per_launch = dom_bytes / max(1, sum(1 for k in kb if k.startswith(dom)))
-    achieved = (per_launch * n_launch) / (busy_ms * 1e-3) / 1e9 if busy_ms > 0 else None
-    peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-    roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak if achieved else None, "traffic": None,
-            "peak_source": peak_src, "algorithmic_bytes_per_launch": per_launch,
-            "launches": n_launch, "avg_launch_ms": sum_ms / max(1, n_launch), "busy_ms": busy_ms,
-            "profiled_region_ms_per_step": ms_prof / K,
-            "note": "achieved = algorithmic bytes of all timed launches / union of their "
-                    "event-timed intervals on their launch streams, over a second K-step "
-                    "region run right after the value region"}
-    total_bytes = sum(kb.values())
-    roof["dag_work_roofline_ms"] = total_bytes / (peak * 1e9) * 1e3
-    if name == "bs" and busy_ms > 0:
-        # B&S is bound by the FP64 pipe, not HBM: report against it
-        n_opt = FULL["bs"]["n"]
-        ops = BS_FP64_OPS_PER_OPTION * n_opt * n_launch / (busy_ms * 1e-3) / 1e9
-        mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        fpeak = FP64_OPS_PER_SM_CLK * SMS * mhz * 1e6 / 1e9
-        roof.update({"bound": "alu", "pipe": "fp64", "achieved": ops, "peak": fpeak,
-                     "unit": "G fp64 ops/s", "frac": ops / fpeak,
-                     "peak_source": f"{FP64_OPS_PER_SM_CLK} fp64 ops/clk/SM (ncu peak_sustained) x "
-                                    f"{SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                     "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
-                     "hbm_achieved_gbs": achieved, "hbm_frac": achieved / peak if achieved else None})
-    tr, tr_src = load_traffic(name, KSYM[dom])
-    if tr is not None:
-        roof["traffic"] = tr
-        roof["traffic_source"] = tr_src
+    h = results[head]
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, sample, cores = cpu_oracle_rate(name)
-        if v is not None:
-            cpu = {"value": v, "unit": "ms per DAG", "cores": cores, "kind": "oracle",
-                   "sample": sample}
+        for name in names:
+            v, sample, cores = cpu_oracle_rate(name)
+            if v is not None:
+                c = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                     "cpu_model": cpu_model(), "pinning": "sched_setaffinity to one core, BLAS 1 thread"}
+                results[name]["cpu_baseline"] = c
+                if name == head:
+                    cpu = c
     out = {
-        "metric": "end-to-end ms per DAG (resident inputs; job aggregate over GPUs)",
-        "value": value,
-        "unit": "ms",
+        "metric": METRIC,
+        "value": h["value"],
+        "unit": UNIT,
         "n_gpus": world,
-        "steps": K,
-        "warmup": W,
-        "ms_per_step": ms / K,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": h["ms_per_step"],
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": DTYPE[name],
+        "dtype": h["dtype"],
         "data": "synthetic (seeded counter-based generator, synth/)",
-        "config": {"workload": WORKLOAD[name], "bench": name, "mode": "resident",
-                   "l2": "inputs larger than L2 (126 MB)" if total_bytes > 2 * 126e6
-                   else "working set L2-resident; no flush", "parallelism": f"replicas x{world}"},
-        "e2e": {"value": e2e_ms / K / world, "unit": "ms per DAG", "h2d_bytes_per_step": h2d_ps,
-                "d2h_bytes_per_step": d2h_ps},
-        "gpu_launches": st["launches"],
-        "roofline": roof,
+        "config": h["config"],
+        "e2e": h["e2e"],
+        "gpu_launches": h["gpu_launches"],
+        "roofline": h["roofline"],
+        "dag_roofline": h["dag_roofline"],
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-        "scheduler": {"sched_us_per_launch": st["sched_ns"] / max(1, st["launches"]) / 1e3,
-                      "cross_stream_waits_per_dag": st["cross_stream_waits"] / K,
-                      "streams": st["streams"]},
+        "clocks": h["clocks"],
     }
-    if res:
-        out["baselines"] = res
-        per = ms / K
-        out["speedup_vs_serial_resident"] = res["serial_resident_ms"] / per
-        out["vs_graph_resident"] = per / res["graph_resident_ms"]
-        out["speedup_vs_serial_stream"] = res["serial_stream_ms"] / (e2e_ms / K)
-        out["vs_graph_stream"] = (e2e_ms / K) / res["graph_stream_ms"]
+    for k in ("scheduler", "baselines", "speedup_vs_serial_resident", "vs_graph_resident",
+              "speedup_vs_serial_stream", "vs_graph_stream", "contention_free"):
+        if k in h:
+            out[k] = h[k]
+    if len(names) > 1:
+        out["suite"] = {n: {k: v for k, v in r.items() if k not in ("clocks",)} for n, r in results.items()
+                        if n != head}
+        out["suite_geomean"] = {
+            "speedup_vs_serial_resident": geomean([r["speedup_vs_serial_resident"] for r in results.values()]),
+            "speedup_vs_serial_stream": geomean([r.get("speedup_vs_serial_stream") for r in results.values()]),
+            "vs_graph_resident": geomean([r.get("vs_graph_resident") for r in results.values()]),
+            "vs_graph_stream": geomean([r.get("vs_graph_stream") for r in results.values()]),
+            "dag_roofline_frac_cp": geomean([r["dag_roofline"]["frac_cp"] for r in results.values()]),
+        }
     print(json.dumps(out))
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (as it stands) on this host's cores, a
-    bounded sample per step, same metric/unit/config as the dagrt arm."""
+    """--impl reference: the oracle (as it stands) on ONE pinned host core, a
+    bounded sample per step, same metric/unit/config as the dagrt arm's
+    headline (B&S unless --bench names another)."""
     if rank != 0:
         return
-    name = args.bench
+    name = HEADLINE if args.bench == "all" else args.bench
     budget = 2.0
     vals = []
     for _ in range(args.warmup):
@@ -443,14 +639,15 @@ def run_reference(args, rank, world):
         vals.append(v)
     el = time.perf_counter() - t0
     v = statistics.median(vals) if vals and vals[0] is not None else None
-    out = {"impl": "reference", "metric": "end-to-end ms per DAG (resident inputs; job aggregate over GPUs)",
-           "value": v, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+    out = {"impl": "reference", "metric": METRIC,
+           "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": el / args.steps * 1e3, "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": WORKLOAD[name], "bench": name},
-           "cpu_baseline": {"value": v, "unit": "ms per DAG", "cores": 1, "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "cpu_model": cpu_model(),
                             "sample": sample + f"; {budget}s per step, extrapolated to the full DAG"},
-           "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
 

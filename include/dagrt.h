@@ -56,8 +56,13 @@ typedef uint64_t dagrt_array;
 typedef uint32_t dagrt_kernel;
 
 /* Scheduling policy (L559-569): the original GrCUDA scheduler is serial and
- * synchronous (the baseline); the paper's scheduler is parallel and async. */
-enum { DAGRT_PARALLEL_ASYNC = 0, DAGRT_SERIAL_SYNC = 1 };
+ * synchronous (the baseline); the paper's scheduler is parallel and async.
+ * DAGRT_PARALLEL_SINGLE_STREAM is the paper's "simpler policy" (L650-654,
+ * SURVEY §8(f) f4): parallel and async with the same DAG, but every vertex
+ * that has parents goes on the stream of its lowest-id parent ("schedule
+ * all children on a single stream"), fewer streams and events; roots still
+ * take the first empty stream in FIFO order, else a new one. */
+enum { DAGRT_PARALLEL_ASYNC = 0, DAGRT_SERIAL_SYNC = 1, DAGRT_PARALLEL_SINGLE_STREAM = 2 };
 /* Backend: the CUDA runtime, or a recorder that performs no device work
  * (for scheduler tests on machines without a GPU). */
 enum { DAGRT_BACKEND_CUDA = 0, DAGRT_BACKEND_RECORD = 1 };
@@ -65,7 +70,7 @@ enum { DAGRT_BACKEND_CUDA = 0, DAGRT_BACKEND_RECORD = 1 };
 enum { DAGRT_R = 1, DAGRT_W = 2, DAGRT_RW = 3 };
 
 typedef struct {
-  int32_t policy;      /* DAGRT_PARALLEL_ASYNC or DAGRT_SERIAL_SYNC */
+  int32_t policy;      /* DAGRT_PARALLEL_ASYNC, DAGRT_SERIAL_SYNC or DAGRT_PARALLEL_SINGLE_STREAM */
   int32_t prefetch;    /* 1: H2D of host-newer read arguments on an in-order side copy
                           stream, overlapped with compute (L356-366, L662-664);
                           0: the copy is issued on the consumer's own stream */

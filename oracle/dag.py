@@ -59,8 +59,14 @@ class DagResult:
     host_waits: list = field(default_factory=list)
 
 
-def build_dag(trace):
-    """Literal pairwise scan of the trace (SURVEY §8(c1) algorithm)."""
+def build_dag(trace, stream_policy="fifo"):
+    """Literal pairwise scan of the trace (SURVEY §8(c1) algorithm).
+
+    ``stream_policy``: "fifo" = the paper's general policy (first child on
+    the parent's stream, later children on other streams, L647-650);
+    "single" = the paper's "simpler" policy, all children of a vertex on a
+    single stream (L650-654): a vertex with parents goes on its lowest-id
+    parent's stream.  The DAG (edges) does not depend on it."""
     accs = [merged_access(op) for op in trace]
     res = DagResult()
     vid_of = {}            # op index -> vertex id (recorded ops only)
@@ -127,7 +133,9 @@ def build_dag(trace):
             # stream oracle (SURVEY §8(c1) "Stream oracle")
             ps = sorted(labels, key=lambda k: vid_of[k])
             s = None
-            for p in ps:
+            if stream_policy == "single" and ps:
+                s = stream_of[ps[0]]
+            for p in ([] if s is not None else ps):
                 sp = stream_of.get(p)
                 if sp is not None and tail[sp] == p:
                     s = sp

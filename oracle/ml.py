@@ -10,7 +10,7 @@ figure draws (MMUL), not a per-category table lookup.
 
     NB: r1 = X theta^T + prior;  m = max_c r1;  l = m + ln sum_c e^(r1-m);
         r1 = e^(r1 - l);  r1 = softmax(r1)
-    RR: mu_f = mean_i X, sd_f = sqrt(mean_i X^2 - mu_f^2) (population, sd=0 -> 1);
+    RR: mu_f = mean_i X, sd_f = sqrt(mean_i (X - mu_f)^2) (population, sd=0 -> 1);
         Z = (X - mu)/sd;  r2 = Z W^T;  r2 += b;  r2 = softmax(r2)
     r[i] = lowest c maximising r1[i,c] + r2[i,c]
 
@@ -26,18 +26,22 @@ N_FEATURES = 200
 
 
 def norm_stats(X, chunk=1 << 20):
-    """Per-feature population mean and std of integer X (exact int64 column
-    sums of x and x^2, then fp64): mu = S/N, sd = sqrt(Q/N - mu^2); sd = 0 -> 1."""
+    """Per-feature population mean and standard deviation, the textbook
+    two-pass definition in fp64 (reading R-ML: population std,
+    sd = 0 -> 1):  mu_f = (1/N) sum_i x_if;  sd_f = sqrt((1/N) sum_i (x_if - mu_f)^2).
+    Chunked over rows only to bound memory (fp64 sums are per chunk, then
+    added in row order)."""
     X = np.asarray(X)
     n = X.shape[0]
-    S = np.zeros(X.shape[1], dtype=np.int64)
-    Q = np.zeros(X.shape[1], dtype=np.int64)
+    S = np.zeros(X.shape[1])
     for i in range(0, n, chunk):
-        c = X[i:i + chunk].astype(np.int64)
-        S += c.sum(axis=0)
-        Q += (c * c).sum(axis=0)
+        S += X[i:i + chunk].astype(np.float64).sum(axis=0)
     mu = S / n
-    sd = np.sqrt(Q / n - mu * mu)
+    D = np.zeros(X.shape[1])
+    for i in range(0, n, chunk):
+        d = X[i:i + chunk].astype(np.float64) - mu
+        D += (d * d).sum(axis=0)
+    sd = np.sqrt(D / n)
     return mu, np.where(sd > 0, sd, 1.0)
 
 

@@ -14,20 +14,25 @@ constexpr int kMaxClasses = 16;
 
 // ---------------------------------------------------------------- NORM
 // Z = (X - mu_f) / sd_f with population statistics, computed in ONE vertex:
-// pass 1 exact integer column sums of x and x^2 -> grid barrier -> one block
-// per column reduces the per-block partials (int64, order-independent, so the
-// statistics are bit-deterministic) -> grid barrier -> pass 2 normalises.
-// The grid (2 CTAs/SM x 148, 512 threads) is co-resident on an idle or
-// shared B200 (the scheduler may run other vertices beside it; they do not
-// wait on NORM, so its CTAs always become resident).
+// pass 1 exact integer column sums S = sum x (int64) and Q = sum x^2
+// (unsigned 128-bit: exact for every int32 x and any N < 2^32) -> grid
+// barrier -> one block per column reduces the per-block partials (integer,
+// order-independent, so the statistics are bit-deterministic) and forms the
+// variance from the exact integer N*Q - S^2 with ONE rounding -> grid barrier
+// -> pass 2 normalises.  The kernel is registered cooperative: the scheduler
+// launches it with cudaLaunchCooperativeKernel, which guarantees the whole
+// grid is co-resident (the software barrier cannot deadlock against other
+// vertices, another NORM in flight or an MPS SM limit).
 //
 // `stats` (out) layout: [0] u32 barrier, [1] u32 exit counter, pad to 16 B,
-// then double mean[F], double inv_sd[F], then int64 part[grid][2F].
+// then double mean[F], double inv_sd[F], then per block: int64 S[F],
+// u64 Qlo[F], u64 Qhi[F]  (norm_stats_bytes(F, grid)).
 struct NormHdr {
   unsigned bar;
   unsigned exitc;
   unsigned pad[2];
 };
+typedef unsigned __int128 u128;
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
@@ -41,13 +46,24 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(512) k_norm(const int* __restrict__ X, float* __restrict__ Z,
+__device__ __forceinline__ void acc_x(long long& s, u128& q, int v) {
+  s += v;
+  q += (unsigned long long)((long long)v * v);  // v^2 <= 2^62: exact in 64 bits
+}
+
+// u128 -> double: the two halves each round once (relative error < 2^-52)
+__device__ __forceinline__ double u128_to_double(u128 v) {
+  return (double)(unsigned long long)(v >> 64) * 18446744073709551616.0 +
+         (double)(unsigned long long)v;
+}
+
+__global__ void __launch_bounds__(512, 2) k_norm(const int* __restrict__ X, float* __restrict__ Z,
                                               unsigned char* stats, long long N, int F) {
-  extern __shared__ long long sh_ll[];  // [RL][2F]
+  extern __shared__ unsigned long long sh_u[];  // [RL][3F]: S, Qlo, Qhi per column
   NormHdr* hdr = reinterpret_cast<NormHdr*>(stats);
   double* mean = reinterpret_cast<double*>(stats + 16);
   double* inv = mean + F;
-  long long* part = reinterpret_cast<long long*>(inv + F);
+  unsigned long long* part = reinterpret_cast<unsigned long long*>(inv + F);  // [grid][3F]
   const int t = threadIdx.x;
   const bool vec = ((F & 3) == 0) && aligned16(X) && aligned16(Z) && (F / 4) <= 512;
   const int G = vec ? F / 4 : F;            // column groups (4 or 1 columns each)
@@ -59,8 +75,9 @@ __global__ void __launch_bounds__(512) k_norm(const int* __restrict__ X, float* 
   const long long r0 = (long long)blockIdx.x * rows_per;
   const long long r1 = min(N, r0 + rows_per);
 
-  // ---- pass 1: exact column sums (int32 per thread: <= 9*rows, 81*rows)
-  int s[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
+  // ---- pass 1: exact column sums
+  long long s[4] = {0, 0, 0, 0};
+  u128 q[4] = {0, 0, 0, 0};
   if (active) {
     if (vec) {
       const int4* X4 = reinterpret_cast<const int4*>(X);
@@ -71,63 +88,70 @@ __global__ void __launch_bounds__(512) k_norm(const int* __restrict__ X, float* 
         for (int u = 0; u < 4; ++u) v[u] = ldg_stream(X4 + (r + u * RL) * G + g);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          s[0] += v[u].x; s[1] += v[u].y; s[2] += v[u].z; s[3] += v[u].w;
-          q[0] += v[u].x * v[u].x; q[1] += v[u].y * v[u].y;
-          q[2] += v[u].z * v[u].z; q[3] += v[u].w * v[u].w;
+          acc_x(s[0], q[0], v[u].x); acc_x(s[1], q[1], v[u].y);
+          acc_x(s[2], q[2], v[u].z); acc_x(s[3], q[3], v[u].w);
         }
       }
       for (; r < r1; r += RL) {
         int4 v = ldg_stream(X4 + r * G + g);
-        s[0] += v.x; s[1] += v.y; s[2] += v.z; s[3] += v.w;
-        q[0] += v.x * v.x; q[1] += v.y * v.y; q[2] += v.z * v.z; q[3] += v.w * v.w;
+        acc_x(s[0], q[0], v.x); acc_x(s[1], q[1], v.y);
+        acc_x(s[2], q[2], v.z); acc_x(s[3], q[3], v.w);
       }
     } else {
-      for (long long r = r0 + rl; r < r1; r += RL) {
-        int v = X[r * F + g];
-        s[0] += v;
-        q[0] += v * v;
-      }
+      for (long long r = r0 + rl; r < r1; r += RL) acc_x(s[0], q[0], X[r * F + g]);
     }
   }
   for (int w = 0; w < W; ++w) {
     if (active) {
-      sh_ll[(size_t)rl * 2 * F + g * W + w] = s[w];
-      sh_ll[(size_t)rl * 2 * F + F + g * W + w] = q[w];
+      unsigned long long* row = sh_u + (size_t)rl * 3 * F;
+      row[g * W + w] = (unsigned long long)s[w];
+      row[F + g * W + w] = (unsigned long long)q[w];
+      row[2 * F + g * W + w] = (unsigned long long)(q[w] >> 64);
     }
   }
   __syncthreads();
-  for (int j = t; j < 2 * F; j += blockDim.x) {
+  for (int j = t; j < F; j += blockDim.x) {
     long long a = 0;
-    for (int l = 0; l < RL; ++l) a += sh_ll[(size_t)l * 2 * F + j];
-    part[(size_t)blockIdx.x * 2 * F + j] = a;
+    u128 b = 0;
+    for (int l = 0; l < RL; ++l) {
+      const unsigned long long* row = sh_u + (size_t)l * 3 * F;
+      a += (long long)row[j];
+      b += ((u128)row[2 * F + j] << 64) | row[F + j];
+    }
+    unsigned long long* o = part + (size_t)blockIdx.x * 3 * F;
+    o[j] = (unsigned long long)a;
+    o[F + j] = (unsigned long long)b;
+    o[2 * F + j] = (unsigned long long)(b >> 64);
   }
   grid_barrier(&hdr->bar, gridDim.x);
 
-  // ---- statistics: column j reduced by block j (and j + grid, ...)
-  __shared__ long long red[2][32];
+  // ---- statistics: column j reduced by block j (and j + grid, ...), warp 0
   for (int j = blockIdx.x; j < F; j += gridDim.x) {
-    long long a = 0, b = 0;
-    for (int k = t; k < (int)gridDim.x; k += blockDim.x) {
-      a += part[(size_t)k * 2 * F + j];
-      b += part[(size_t)k * 2 * F + F + j];
-    }
+    if (t < 32) {
+      long long a = 0;
+      u128 b = 0;
+      for (int k = t; k < (int)gridDim.x; k += 32) {
+        const volatile unsigned long long* o = part + (size_t)k * 3 * F;
+        a += (long long)o[j];
+        b += ((u128)o[2 * F + j] << 64) | o[F + j];
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)b, o);
+        const unsigned long long hi = __shfl_xor_sync(0xffffffffu, (unsigned long long)(b >> 64), o);
+        b += ((u128)hi << 64) | lo;
+      }
+      if (t == 0) {
+        // N^2 var = N Q - S^2, exact in 128 bits (N < 2^32), rounded once
+        const __int128 S = a;
+        const __int128 num = (__int128)((u128)N * b) - S * S;
+        const double var = (num > 0 ? u128_to_double((u128)num) : 0.0) / ((double)N * (double)N);
+        const double sd = sqrt(var);
+        mean[j] = (double)a / (double)N;
+        inv[j] = sd > 0.0 ? 1.0 / sd : 1.0;
+      }
     }
-    if ((t & 31) == 0) { red[0][t >> 5] = a; red[1][t >> 5] = b; }
-    __syncthreads();
-    if (t == 0) {
-      long long S = 0, Q = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { S += red[0][w]; Q += red[1][w]; }
-      const double mu = (double)S / (double)N;
-      const double var = (double)Q / (double)N - mu * mu;
-      const double sd = var > 0.0 ? sqrt(var) : 0.0;
-      mean[j] = mu;
-      inv[j] = sd > 0.0 ? 1.0 / sd : 1.0;
-    }
-    __syncthreads();
   }
   grid_barrier(&hdr->bar, 2 * gridDim.x);
 
@@ -601,7 +625,7 @@ __global__ void __launch_bounds__(256) k_argmax(const float* __restrict__ r1,
 }
 
 static const Builtin kMl[] = {
-    {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_NONE},
+    {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_COOPERATIVE, 96 * 1024},
     {"nb_mmul", (const void*)k_nb_mmul,
      "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 120 * 1024},
     {"rr_mmul", (const void*)k_rr_mmul, "const ptr, const ptr, out ptr, sint64, sint32, sint32",

@@ -64,7 +64,17 @@ __global__ void __launch_bounds__(256) k_peak_ffma(float* out, long long iters) 
   if (s == -1.f) out[threadIdx.x] = s;
 }
 
+// Utility vertex: a[i] = alpha * a[i] + beta (in place, fp32).  Used by the
+// scheduler tests (chains of dependent writes on one array) and as a cheap
+// device-side initialiser; not a vertex of any benchmark DAG.
+__global__ void __launch_bounds__(256) k_axpb(float* a, long long n, float alpha, float beta) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = fmaf(alpha, a[i], beta);
+}
+
 static const Builtin kProbes[] = {
+    {"axpb", (const void*)k_axpb, "ptr, sint64, float, float", KF_NONE},
     {"peak_dfma", (const void*)k_peak_dfma, "out ptr, sint64", KF_NONE},
     {"peak_ffma", (const void*)k_peak_ffma, "out ptr, sint64", KF_NONE},
 };

@@ -172,12 +172,25 @@ struct RecordBackend final : Backend {
 // buffered batch is keyed by its exact content; a batch seen for the second
 // time is stream-captured into a CUDA graph (fork/join over every stream it
 // uses, so the graph reproduces the scheduler's multi-stream schedule), and
-// later identical batches replay that graph with one cudaGraphLaunch.
-// Dependencies are still inferred at run time for every launch; only the
-// CUDA submission is cached.  Events recorded inside a replayed graph are
-// aliased to one real "batch event" recorded after the graph, so host syncs
-// and later cross-batch waits stay correct (conservatively: they wait for
-// the whole batch).
+// later identical batches replay that graph with one cudaGraphLaunch on a
+// private in-order `origin` stream.  Dependencies are still inferred at run
+// time for every launch; only the CUDA submission is cached.
+//
+// Events.  Every vertex event recorded inside a captured batch also gets an
+// EXTERNAL event-record node of the graph (cudaEventRecordExternal) on a
+// graph-owned event; after a replay the vertex's event is aliased to that
+// node's event, so a host access or a later batch waits for exactly its
+// producer, not for the whole graph.  Each stream's last operation in the
+// graph likewise records a per-stream tail event: a stream synchronisation
+// (the D2H of a host read) waits for that stream's part of the graph only.
+//
+// Ordering with work issued outside the graph (eagerly, on the scheduler's
+// streams): a stream that got eager work since the last replay is forked
+// into `origin` (event record + wait) before the next graph launch that uses
+// it, and eager work on a stream whose tail ran inside a replayed graph
+// first waits on that stream's tail event.  So same-stream order (which the
+// scheduler relies on: a child on its parent's stream gets no event wait)
+// holds across graph/eager boundaries in both directions.
 struct DeferBackend final : Backend {
   enum : uint8_t { OP_LAUNCH, OP_RECORD, OP_WAIT, OP_COPY };
   struct Op {
@@ -189,7 +202,7 @@ struct DeferBackend final : Backend {
     const void* fn;
     dim3 g, b;
     size_t smem;
-    uint64_t vals[16];
+    uint64_t vals[17];
     void* dst;
     const void* src;
     size_t n;
@@ -198,6 +211,14 @@ struct DeferBackend final : Backend {
   struct Entry {
     std::vector<uint64_t> key;
     cudaGraphExec_t exec = nullptr;
+    std::vector<void*> rec_ev;                      // per OP_RECORD, in op order
+    std::vector<std::pair<void*, void*>> tail_ev;   // (stream, tail event)
+  };
+  struct StreamState {
+    void* s;
+    bool dirty;      // eager work issued since the last fork into `origin`
+    void* gtail;     // tail event of this stream in the last replay (or null)
+    bool ordered;    // the stream already waits on gtail
   };
   Backend* in;
   bool enabled = false;
@@ -207,9 +228,11 @@ struct DeferBackend final : Backend {
   std::vector<Entry> cache;                 // small, linear search by hash first
   std::vector<uint64_t> cache_hash;
   std::vector<uint64_t> seen;               // batch hashes seen once (eager)
-  std::vector<std::pair<void*, void*>> alias;  // event -> batch event
-  std::vector<std::pair<void*, int>> bev_refs; // batch event -> alias count
-  std::vector<void*> bev_pool, join_evs;
+  std::vector<uint64_t> nocap;              // batches whose capture failed (always eager)
+  std::vector<std::pair<void*, void*>> alias;  // vertex event -> graph-owned event
+  std::vector<StreamState> sstate;
+  std::vector<void*> owned;                 // graph-owned events (destroyed with the cache)
+  std::vector<void*> fork_evs;
   void* fork_ev = nullptr;
   uint64_t replays = 0, captures = 0, eager = 0;
 
@@ -217,14 +240,14 @@ struct DeferBackend final : Backend {
   ~DeferBackend() override {
     for (auto& e : cache)
       if (e.exec) cudaGraphExecDestroy(e.exec);
-    for (auto& p : bev_refs) in->event_destroy(p.first);
-    for (void* e : bev_pool) in->event_destroy(e);
-    for (void* e : join_evs) in->event_destroy(e);
+    for (void* e : owned) in->event_destroy(e);
+    for (void* e : fork_evs) in->event_destroy(e);
     if (fork_ev) in->event_destroy(fork_ev);
     if (origin) in->stream_destroy(origin);
     delete in;
   }
   bool active() const { return enabled; }
+  bool graphs_used() const { return replays || captures; }
 
   void* resolve(void* e) const {
     for (auto& a : alias)
@@ -234,18 +257,27 @@ struct DeferBackend final : Backend {
   void unalias(void* e) {
     for (size_t i = 0; i < alias.size(); ++i)
       if (alias[i].first == e) {
-        void* b = alias[i].second;
         alias[i] = alias.back();
         alias.pop_back();
-        for (size_t j = 0; j < bev_refs.size(); ++j)
-          if (bev_refs[j].first == b && --bev_refs[j].second == 0) {
-            bev_pool.push_back(b);
-            bev_refs[j] = bev_refs.back();
-            bev_refs.pop_back();
-            break;
-          }
         return;
       }
+  }
+  StreamState* state(void* s) {
+    for (auto& x : sstate)
+      if (x.s == s) return &x;
+    sstate.push_back(StreamState{s, true, nullptr, true});  // unknown: may hold eager work
+    return &sstate.back();
+  }
+  // Before eager work on stream s: order it after s's part of the last graph.
+  cudaError_t pre_eager(void* s) {
+    if (!graphs_used() || !s) return cudaSuccess;
+    StreamState* st = state(s);
+    if (st->gtail && !st->ordered) {
+      if (cudaError_t e = in->wait(s, st->gtail)) return e;
+      st->ordered = true;
+    }
+    st->dirty = true;
+    return cudaSuccess;
   }
 
   cudaError_t stream_create(void** s) override { return in->stream_create(s); }
@@ -258,25 +290,30 @@ struct DeferBackend final : Backend {
 
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop,
                      int nargs) override {
-    if (!enabled || coop) {
+    if (!enabled || nargs > 17) {
       if (cudaError_t e = flush()) return e;
+      if (cudaError_t e = pre_eager(s)) return e;
       return in->launch(fn, g, b, args, smem, s, coop, nargs);
     }
     Op o{};
     o.kind = OP_LAUNCH;
+    o.coop = coop;
     o.fn = fn;
     o.g = g;
     o.b = b;
     o.smem = smem;
     o.s = s;
     o.nargs = nargs;
-    for (int i = 0; i < nargs && i < 16; ++i) o.vals[i] = *reinterpret_cast<const uint64_t*>(args[i]);
+    for (int i = 0; i < nargs; ++i) o.vals[i] = *reinterpret_cast<const uint64_t*>(args[i]);
     ops.push_back(o);
     return cudaSuccess;
   }
   cudaError_t record(void* e, void* s) override {
     unalias(e);
-    if (!enabled) return in->record(e, s);
+    if (!enabled) {
+      if (cudaError_t r = pre_eager(s)) return r;
+      return in->record(e, s);
+    }
     Op o{};
     o.kind = OP_RECORD;
     o.e = e;
@@ -286,7 +323,10 @@ struct DeferBackend final : Backend {
   }
   cudaError_t wait(void* s, void* e) override {
     e = resolve(e);
-    if (!enabled) return in->wait(s, e);
+    if (!enabled) {
+      if (cudaError_t r = pre_eager(s)) return r;
+      return in->wait(s, e);
+    }
     Op o{};
     o.kind = OP_WAIT;
     o.e = e;
@@ -310,6 +350,7 @@ struct DeferBackend final : Backend {
   cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, void* s) override {
     if (!enabled || (k == cudaMemcpyDeviceToHost && !d2h_pinned)) {
       if (cudaError_t e = flush()) return e;
+      if (cudaError_t e = pre_eager(s)) return e;
       return in->copy_async(dst, src, n, k, s);
     }
     Op o{};
@@ -328,18 +369,22 @@ struct DeferBackend final : Backend {
   }
   cudaError_t stream_sync(void* s) override {
     if (cudaError_t r = flush()) return r;
-    // work captured from stream s may be running inside a graph on `origin`
-    if (origin && (replays || captures))
-      if (cudaError_t r = in->stream_sync(origin)) return r;
+    if (graphs_used()) {
+      StreamState* st = state(s);
+      // s's newest work is its part of a replayed graph: wait for that part only
+      if (st->gtail && !st->ordered) return in->event_sync(st->gtail);
+    }
     return in->stream_sync(s);
   }
 
   cudaError_t issue(const Op& o, bool capturing) {
+    if (!capturing)
+      if (cudaError_t e = pre_eager(o.s)) return e;
     switch (o.kind) {
       case OP_LAUNCH: {
-        void* argv[16];
+        void* argv[17];
         for (int i = 0; i < o.nargs; ++i) argv[i] = const_cast<uint64_t*>(&o.vals[i]);
-        return in->launch(o.fn, o.g, o.b, argv, o.smem, o.s, false, o.nargs);
+        return in->launch(o.fn, o.g, o.b, argv, o.smem, o.s, o.coop, o.nargs);
       }
       case OP_RECORD: return in->record(o.e, o.s);
       case OP_WAIT: return capturing ? cudaSuccess : in->wait(o.s, o.e);
@@ -350,14 +395,14 @@ struct DeferBackend final : Backend {
   // Batch key.  Event handles are canonicalised to their first-appearance
   // index: pooled events come back in varying order between identical runs,
   // and a captured graph does not depend on them (recorded-and-waited events
-  // become graph edges; external waits and host-visible aliases are taken
-  // from the current batch when it is replayed).
+  // become graph edges, host-visible records are graph-owned events; external
+  // waits are taken from the current batch when it is replayed).
   std::vector<void*> key_events;
   void build_key() {
     key.clear();
     key_events.clear();
     for (const Op& o : ops) {
-      key.push_back(o.kind);
+      key.push_back(o.kind | (o.coop ? 0x100u : 0u));
       key.push_back((uint64_t)(uintptr_t)o.s);
       uint64_t ev = 0;
       if (o.e) {
@@ -401,58 +446,90 @@ struct DeferBackend final : Backend {
       if (ops[j].kind == OP_RECORD && ops[j].e == ops[i].e) return false;
     return true;
   }
+  bool is_owned(void* e) const { return std::find(owned.begin(), owned.end(), e) != owned.end(); }
 
-  cudaError_t run_graph(cudaGraphExec_t exec) {
-    for (size_t i = 0; i < ops.size(); ++i)
-      if (ops[i].kind == OP_WAIT && external_wait(i))
-        if (cudaError_t e = in->wait(origin, ops[i].e)) return e;
-    if (cudaError_t e = cudaGraphLaunch(exec, (cudaStream_t)origin)) return e;
-    void* bev;
-    if (!bev_pool.empty()) {
-      bev = bev_pool.back();
-      bev_pool.pop_back();
-    } else if (cudaError_t e = in->event_create(&bev)) {
-      return e;
-    }
-    if (cudaError_t e = in->record(bev, origin)) return e;
-    int refs = 0;
-    for (const Op& o : ops)
-      if (o.kind == OP_RECORD) {
-        unalias(o.e);
-        alias.push_back({o.e, bev});
-        ++refs;
-      }
-    if (refs) bev_refs.push_back({bev, refs});
-    else bev_pool.push_back(bev);
-    return cudaSuccess;
-  }
-
-  cudaError_t capture(cudaGraphExec_t* out) {
+  std::vector<void*> batch_streams() const {
     std::vector<void*> streams;
     for (const Op& o : ops)
       if (std::find(streams.begin(), streams.end(), o.s) == streams.end()) streams.push_back(o.s);
-    while (join_evs.size() < streams.size()) {
-      void* e;
-      if (cudaError_t r = in->event_create(&e)) return r;
-      join_evs.push_back(e);
+    return streams;
+  }
+
+  cudaError_t run_graph(Entry& en) {
+    for (size_t i = 0; i < ops.size(); ++i)  // (events of earlier replays: origin is in order)
+      if (ops[i].kind == OP_WAIT && external_wait(i) && !is_owned(ops[i].e))
+        if (cudaError_t e = in->wait(origin, ops[i].e)) return e;
+    // fork: streams with eager work since the last replay feed into origin
+    size_t nf = 0;
+    for (auto& te : en.tail_ev) {
+      StreamState* st = state(te.first);
+      if (!st->dirty) continue;
+      if (nf == fork_evs.size()) {
+        void* e;
+        if (cudaError_t r = in->event_create(&e)) return r;
+        fork_evs.push_back(e);
+      }
+      if (cudaError_t e = in->record(fork_evs[nf], te.first)) return e;
+      if (cudaError_t e = in->wait(origin, fork_evs[nf])) return e;
+      ++nf;
+      st->dirty = false;
     }
+    if (cudaError_t e = cudaGraphLaunch(en.exec, (cudaStream_t)origin)) return e;
+    size_t r = 0;
+    for (const Op& o : ops)
+      if (o.kind == OP_RECORD) {
+        unalias(o.e);
+        alias.push_back({o.e, en.rec_ev[r++]});
+      }
+    for (auto& te : en.tail_ev) {
+      StreamState* st = state(te.first);
+      st->gtail = te.second;
+      st->ordered = false;
+    }
+    return cudaSuccess;
+  }
+
+  cudaError_t owned_event(void** e) {
+    if (cudaError_t r = in->event_create(e)) return r;
+    owned.push_back(*e);
+    return cudaSuccess;
+  }
+
+  cudaError_t capture(Entry* en) {
+    std::vector<void*> streams = batch_streams();
     if (!fork_ev)
       if (cudaError_t r = in->event_create(&fork_ev)) return r;
+    for (const Op& o : ops)
+      if (o.kind == OP_RECORD) {
+        void* e;
+        if (cudaError_t r = owned_event(&e)) return r;
+        en->rec_ev.push_back(e);
+      }
+    std::vector<void*> join(streams.size());
+    for (size_t i = 0; i < streams.size(); ++i) {
+      if (cudaError_t r = owned_event(&join[i])) return r;
+      en->tail_ev.push_back({streams[i], join[i]});
+    }
     cudaStream_t org = (cudaStream_t)origin;
     if (cudaError_t r = cudaStreamBeginCapture(org, cudaStreamCaptureModeRelaxed)) return r;
     cudaError_t err = in->record(fork_ev, origin);
     for (void* s : streams)
       if (!err) err = in->wait(s, fork_ev);
+    size_t r = 0;
     for (size_t i = 0; i < ops.size() && !err; ++i) {
       if (ops[i].kind == OP_WAIT) {
         if (!external_wait(i)) err = in->wait(ops[i].s, ops[i].e);
       } else {
         err = issue(ops[i], true);
+        if (!err && ops[i].kind == OP_RECORD)
+          err = cudaEventRecordWithFlags((cudaEvent_t)en->rec_ev[r++], (cudaStream_t)ops[i].s,
+                                         cudaEventRecordExternal);
       }
     }
     for (size_t i = 0; i < streams.size() && !err; ++i) {
-      err = in->record(join_evs[i], streams[i]);
-      if (!err) err = in->wait(origin, join_evs[i]);
+      err = cudaEventRecordWithFlags((cudaEvent_t)join[i], (cudaStream_t)streams[i], cudaEventRecordExternal);
+      if (!err) err = in->record(fork_ev, streams[i]);  // join into origin (capture-internal)
+      if (!err) err = in->wait(origin, fork_ev);
     }
     cudaGraph_t g = nullptr;
     cudaError_t end = cudaStreamEndCapture(org, &g);
@@ -461,9 +538,11 @@ struct DeferBackend final : Backend {
       return err;
     }
     if (end) return end;
-    cudaError_t r = cudaGraphInstantiate(out, g, 0);
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ri = cudaGraphInstantiate(&exec, g, 0);
     cudaGraphDestroy(g);
-    return r;
+    en->exec = exec;
+    return ri;
   }
 
   cudaError_t flush() {
@@ -476,27 +555,32 @@ struct DeferBackend final : Backend {
     bool done = false;
     for (size_t i = 0; i < cache.size() && !done; ++i)
       if (cache_hash[i] == h && cache[i].key == key) {
-        err = run_graph(cache[i].exec);
+        err = run_graph(cache[i]);
         ++replays;
         done = true;
       }
-    if (!done && std::find(seen.begin(), seen.end(), h) != seen.end()) {
-      cudaGraphExec_t exec = nullptr;
-      err = capture(&exec);
-      if (!err) {
+    if (!done && std::find(nocap.begin(), nocap.end(), h) == nocap.end() &&
+        std::find(seen.begin(), seen.end(), h) != seen.end()) {
+      Entry en;
+      en.key = key;
+      cudaError_t ce = capture(&en);
+      if (!ce) {
         if (cache.size() >= 16) {
           cudaGraphExecDestroy(cache.front().exec);
           cache.erase(cache.begin());
           cache_hash.erase(cache_hash.begin());
         }
-        Entry en;
-        en.key = key;
-        en.exec = exec;
         cache.push_back(std::move(en));
         cache_hash.push_back(h);
-        err = run_graph(exec);
+        err = run_graph(cache.back());
         ++captures;
         done = true;
+      } else {
+        // not capturable (e.g. an operation the driver refuses to capture):
+        // this batch is always issued eagerly from now on
+        if (en.exec) cudaGraphExecDestroy(en.exec);
+        cudaGetLastError();
+        nocap.push_back(h);
       }
     }
     if (!done) {  // first sighting: issue eagerly, remember the batch
@@ -515,11 +599,13 @@ struct DeferBackend final : Backend {
   // order a D2H copy after its producers without blocking the host.
   cudaError_t wait_now(void* s, void* e) {
     if (cudaError_t r = flush()) return r;
+    if (cudaError_t r = pre_eager(s)) return r;
     return in->wait(s, resolve(e));
   }
 
   cudaError_t launch_now(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s, bool coop) {
     if (cudaError_t e = flush()) return e;
+    if (cudaError_t e = pre_eager(s)) return e;
     return in->launch(fn, g, b, args, smem, s, coop, 0);
   }
 };
@@ -833,6 +919,12 @@ dagrt_status new_stream(dagrt_ctx c, int32_t* out) {
 
 // Stream manager (L570-582, L647-654; stream oracle in SURVEY §8(c1)).
 dagrt_status pick_stream(dagrt_ctx c, int32_t* out) {
+  if (c->cfg.policy == DAGRT_PARALLEL_SINGLE_STREAM && !c->scratch_parents.empty() &&
+      c->vertices[c->scratch_parents[0]].stream >= 0) {
+    // "schedule all children on a single stream" (L650-654): the first parent's
+    *out = c->vertices[c->scratch_parents[0]].stream;
+    return DAGRT_OK;
+  }
   for (uint32_t p : c->scratch_parents) {
     int32_t s = c->vertices[p].stream;
     if (s >= 0 && c->streams[s].tail == (int64_t)p) { *out = s; return DAGRT_OK; }
@@ -1071,7 +1163,7 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
       return DAGRT_ECUDA;
     }
     c->be = new DeferBackend(new CudaBackend());
-    c->be->enabled = c->cfg.graph_cache != 0 && c->cfg.policy == DAGRT_PARALLEL_ASYNC;
+    c->be->enabled = c->cfg.graph_cache != 0 && c->cfg.policy != DAGRT_SERIAL_SYNC;
   }
   c->arrays.resize(1);
   // built-in kernels are pre-registered (handles 0..n-1)
@@ -1602,7 +1694,7 @@ dagrt_status dagrt_profile_enable(dagrt_ctx c, dagrt_kernel kh, int32_t on) {
   bool any = false;
   for (const KernelRec& kr : c->kernels) any = any || kr.prof;
   if (cudaError_t e = c->be->flush()) return cuda_fail(c, e, "flush");
-  c->be->enabled = c->cfg.graph_cache && c->cfg.policy == DAGRT_PARALLEL_ASYNC && c->be->real() &&
+  c->be->enabled = c->cfg.graph_cache && c->cfg.policy != DAGRT_SERIAL_SYNC && c->be->real() &&
                    !any && !c->timeline;
   return DAGRT_OK;
 }
@@ -1653,7 +1745,7 @@ dagrt_status dagrt_timeline_enable(dagrt_ctx c, int32_t on) {
   if (cudaError_t e = c->be->flush()) return cuda_fail(c, e, "flush");
   bool any = false;
   for (const KernelRec& kr : c->kernels) any = any || kr.prof;
-  c->be->enabled = c->cfg.graph_cache && c->cfg.policy == DAGRT_PARALLEL_ASYNC && c->be->real() &&
+  c->be->enabled = c->cfg.graph_cache && c->cfg.policy != DAGRT_SERIAL_SYNC && c->be->real() &&
                    !any && !c->timeline;
   return DAGRT_OK;
 }
@@ -1727,7 +1819,6 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh,
   if (!g || !node) return fail(c, DAGRT_EINVAL, "null graph/node");
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
-  if (k->coop) return fail(c, DAGRT_ESTATE, "cooperative kernel %s in a graph", k->name.c_str());
   uint64_t vals[kMaxArgs];
   void* argv[kMaxArgs];
   ArrayRec* arrs[kMaxArgs];
@@ -1742,6 +1833,12 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh,
   p.kernelParams = argv;
   cudaGraphNode_t n;
   CK(cudaGraphAddKernelNode(&n, g->r.g, d.data(), d.size(), &p), "cudaGraphAddKernelNode");
+  if (k->coop) {  // co-residency guaranteed in the graph too (grid barrier kernels)
+    cudaLaunchAttributeValue v{};
+    v.cooperative = 1;
+    CK(cudaGraphKernelNodeSetAttribute(n, cudaLaunchAttributeCooperative, &v),
+       "cudaGraphKernelNodeSetAttribute cooperative");
+  }
   g->r.nodes.push_back(n);
   *node = (uint32_t)g->r.nodes.size() - 1;
   return DAGRT_OK;

@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBPATH = os.path.join(HERE, "libdagrt.so")
 
 OK, EINVAL, ENOTFOUND, EALIAS, ESIG, ESTATE, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5, -6, -7
-PARALLEL_ASYNC, SERIAL_SYNC = 0, 1
+PARALLEL_ASYNC, SERIAL_SYNC, PARALLEL_SINGLE_STREAM = 0, 1, 2
+POLICIES = {"parallel": PARALLEL_ASYNC, "serial": SERIAL_SYNC, "single_stream": PARALLEL_SINGLE_STREAM}
 BACKEND_CUDA, BACKEND_RECORD = 0, 1
 R, W, RW = 1, 2, 3
 K_I32, K_I64, K_CONST, K_INOUT, K_OUT, K_F32, K_F64 = 0, 1, 2, 3, 4, 5, 6
@@ -332,7 +333,7 @@ class Context:
     def __init__(self, device=0, policy="parallel", prefetch=True, max_streams=0,
                  record_dag=False, backend="cuda", graph_cache=False):
         L = lib()
-        cfg = Config(PARALLEL_ASYNC if policy == "parallel" else SERIAL_SYNC, 1 if prefetch else 0,
+        cfg = Config(POLICIES[policy], 1 if prefetch else 0,
                      max_streams, 1 if record_dag else 0,
                      BACKEND_CUDA if backend == "cuda" else BACKEND_RECORD, 1 if graph_cache else 0)
         h = C.c_void_p()

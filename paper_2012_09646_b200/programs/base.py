@@ -118,6 +118,11 @@ class Program:
             torch.cuda.synchronize()
 
     # ---------------------------------------------------------- the run
+    def restart(self):
+        """Host-side preparation of a fresh run, outside the timed region
+        (the paper writes the inputs before each run, L862-864): a no-op
+        except for programs whose inputs are also their outputs (HITS)."""
+
     def begin_run(self):
         """Stream mode: the host writes fresh inputs (host copy becomes newer)."""
         if self.mode == "stream":

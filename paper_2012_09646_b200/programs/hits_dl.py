@@ -136,6 +136,24 @@ class Hits(Program):
             if name in self.mirror:
                 self.mirror[name].fill_(v)
 
+    def restart(self):
+        """a1 = h1 = 1/sqrt(N) again before a run (host writes, as in the
+        golden HITS DAG): stream mode rewrites the pinned mirrors (uploaded
+        by the run's prefetches), resident mode writes the device arrays
+        through dagrt_host_write, so every run is the same K-iteration DAG
+        from the same start vector instead of continuing the last run."""
+        v = 1.0 / math.sqrt(self.n) if self.n else 0.0
+        if self.record:
+            return
+        if self.mode == "stream":
+            for name in ("a1", "h1"):
+                self.mirror[name].fill_(v)
+            return
+        if getattr(self, "_init", None) is None:
+            self._init = torch.full((max(1, self.n),), v, dtype=torch.float32, pin_memory=True)
+        for name in ("a1", "h1"):
+            self.ctx.host_write(self.a[name], self._init.data_ptr(), 0, 4 * self.n)
+
     def launch_sequence(self):
         return [L for _ in range(self.iters) for L in self.it]
 

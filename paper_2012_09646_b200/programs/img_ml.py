@@ -91,7 +91,12 @@ NORM_GRID = 2 * SMS
 def norm_smem(f):
     g_vec = f // 4 if f % 4 == 0 else f
     rl = max(NORM_THREADS // max(1, g_vec), NORM_THREADS // max(1, f), 1)
-    return 8 * 2 * f * rl
+    return 8 * 3 * f * rl  # [row lanes][S, Qlo, Qhi] per column
+
+
+def norm_stats_bytes(f, grid=None):
+    """NORM `stats` array: header, fp64 mean/inv_sd, per-block S/Qlo/Qhi."""
+    return 16 + 16 * f + 24 * f * (grid or NORM_GRID)
 
 
 class MLEnsemble(Program):
@@ -104,7 +109,7 @@ class MLEnsemble(Program):
         stream = self.mode == "stream"
         self.alloc("X", n * f, torch.int32, mirror=stream)
         self.alloc("Z", n * f, torch.float32)
-        self.alloc("stats", 0, None, nbytes=16 + 16 * f + 16 * f * NORM_GRID)
+        self.alloc("stats", 0, None, nbytes=norm_stats_bytes(f))
         for name, numel in (("theta", c * f), ("prior", c), ("W", c * f), ("b", c)):
             self.alloc(name, numel, torch.float32)
         for name in ("r1", "r2"):

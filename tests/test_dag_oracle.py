@@ -116,3 +116,90 @@ def test_transfer_oracle_counts():
     got = dag.transfers(tr, hh, nb)
     # x pulled once; y read whole once (then both valid); z range read
     assert got == [("H2D", "x", 40, 1), ("D2H", "y", 40, 3), ("D2H", "z", 4, 5)]
+
+
+def _simulate(trace, transfers, has_host, nbytes):
+    """Two-copy machine (device array + host mirror) driven by the transfer
+    oracle's copies, against a one-copy machine (plain sequential memory):
+    every value a kernel or a host read observes must be the same.  Kernels
+    read their read arguments whole and overwrite their written arguments
+    whole with a value derived from the op index and what they read; host
+    writes store the op index into their byte range."""
+    import numpy as np
+    one = {a: np.zeros(nbytes[a], np.int64) for a in nbytes}
+    dev = {a: np.zeros(nbytes[a], np.int64) for a in nbytes}
+    host = {a: np.zeros(nbytes[a], np.int64) for a in nbytes}  # mirror starts stale
+    copies = {}
+    for c in transfers:
+        copies.setdefault(c[3], []).append(c)
+    for j, op in enumerate(trace):
+        for kind, arr, nb, _ in copies.get(j, []):
+            if op[0] == "host" and has_host[arr]:
+                off = op[3] if nb == op[4] else 0  # a range read, or the whole-array pull
+                if kind == "D2H":
+                    host[arr][off:off + nb] = dev[arr][off:off + nb]
+            elif kind == "H2D" and op[0] == "launch":
+                dev[arr][:] = host[arr]
+        if op[0] == "launch":
+            seen1 = [int(one[a].sum() * 31 + one[a][::7].sum()) for a, m in op[2] if m != "O"]
+            seen2 = [int(dev[a].sum() * 31 + dev[a][::7].sum()) for a, m in op[2] if m != "O"]
+            assert seen1 == seen2, (j, op)
+            val = 1000 * (j + 1) + sum(seen1) % 997
+            for a, m in op[2]:
+                if m != "R":
+                    one[a][:] = val
+                    dev[a][:] = val
+        elif op[0] == "host":
+            _, arr, mode, off, nb = op
+            if mode == "R":
+                mine = (host[arr] if has_host[arr] else dev[arr])[off:off + nb]
+                assert np.array_equal(mine, one[arr][off:off + nb]), (j, op)
+            else:
+                one[arr][off:off + nb] = j + 1
+                (host[arr] if has_host[arr] else dev[arr])[off:off + nb] = j + 1
+
+
+def test_transfer_oracle_semantics_brute_force():
+    """Pins the transfer oracle (incl. its partial-write rule: a partial host
+    write of a device-newer array first pulls the WHOLE array, because the
+    next upload sends the whole mirror) against plain sequential memory on
+    every trace of length <= 4 over one array and on random traces over
+    three arrays, with and without host mirrors.  Dropping the pull, or
+    pulling only the written range, fails it."""
+    import itertools
+    import random
+    nb = {"X": 16, "Y": 16, "Z": 16}
+    ops1 = [("launch", "k", [("X", m)]) for m in ("R", "RW", "O")] + \
+           [("host", "X", m, off, n) for m in "RW" for off, n in ((0, 16), (4, 8), (12, 4))]
+    for L in range(1, 5):
+        for tr in itertools.product(ops1, repeat=L):
+            tr = list(tr)
+            for hh in (True, False):
+                hv = {"X": hh}
+                _simulate(tr, dag.transfers(tr, hv, nb), hv, nb)
+    rng = random.Random(9)
+    for _ in range(400):
+        tr = []
+        for _ in range(rng.randint(1, 30)):
+            if rng.random() < 0.6:
+                tr.append(("launch", "k", [(rng.choice("XYZ"), rng.choice(["R", "RW", "O"]))
+                                           for _ in range(rng.randint(1, 3))]))
+            else:
+                off = rng.choice([0, 0, 4, 8])
+                tr.append(("host", rng.choice("XYZ"), rng.choice("RW"), off, rng.choice([16 - off, 4])))
+        # a kernel using the same array twice with different modes: merged (D3)
+        hv = {a: rng.random() < 0.8 for a in "XYZ"}
+        _simulate(tr, dag.transfers(tr, hv, nb), hv, nb)
+
+
+def test_transfer_simulator_catches_a_missing_pull():
+    """The brute-force check above is sharp: removing the whole-array pull
+    of the partial-write rule makes it fail."""
+    nb = {"X": 16}
+    hv = {"X": True}
+    tr = [("launch", "k", [("X", "O")]), ("host", "X", "W", 4, 4), ("launch", "k", [("X", "R")])]
+    good = dag.transfers(tr, hv, nb)
+    _simulate(tr, good, hv, nb)
+    bad = [c for c in good if not (c[0] == "D2H" and c[3] == 1)]
+    with pytest.raises(AssertionError):
+        _simulate(tr, bad, hv, nb)

@@ -1,0 +1,217 @@
+"""GPU parity cases added in round 2 (VERDICT r1 "Make parity green"):
+
+* every benchmark under every scheduling policy (serial-sync, PAPER.md
+  L559-569 -- the baseline every speedup divides by; the graph cache;
+  the hand-written CUDA graph) against the fp64 oracle, both modes;
+* NORM on wide-range integer X (exact 128-bit sums);
+* DL at 4096^2 (about 14 conv2 tiles per CTA, so every TMA stage and
+  mbarrier phase of the product kernel is reused) element-wise, and at the
+  full 16384^2 size c2x/c2y strips element-wise plus r against the oracle's r;
+* B&S at the limits S << K and S >> K;
+* the graph cache's ordering across a flush with a vertex still active.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import bs as obs
+from oracle import dl as odl
+from oracle import ml as oml
+from paper_2012_09646_b200 import dagrt as D
+from paper_2012_09646_b200.programs import (BlackScholes, DeepLearning, Hits, Images, MLEnsemble,
+                                            Vec)
+
+from oracle_checks import assert_close, check, red
+
+pytestmark = pytest.mark.gpu
+
+SMALL = {
+    "vec": lambda c, m: Vec(c, n=100_003, mode=m),
+    "bs": lambda c, m: BlackScholes(c, n=40_009, mode=m),
+    "img": lambda c, m: Images(c, h=300, w=517, mode=m),
+    "ml": lambda c, m: MLEnsemble(c, n=20_011, mode=m),
+    "hits": lambda c, m: Hits(c, n=50_000, e=150_000, iters=3, mode=m),
+    "dl": lambda c, m: DeepLearning(c, h=515, w=517, mode=m),
+}
+
+
+@pytest.mark.parametrize("bench", list(SMALL))
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+@pytest.mark.parametrize("policy", ["serial", "graph_cache", "single_stream"])
+def test_policy_outputs_match_oracle(bench, mode, policy):
+    """The same program under another policy computes the oracle's results,
+    run three times (the graph cache replays from the third run on)."""
+    kw = {"graph_cache": True} if policy == "graph_cache" else {"policy": policy}
+    c = D.Context(device=0, **kw)
+    p = SMALL[bench](c, mode)
+    p.load_inputs(2)
+    for _ in range(3):
+        if bench == "hits":  # iterations restart from 1/sqrt(N) each run
+            p.restart()
+        p.run()
+    c.sync()
+    check(p, 2)
+    if policy == "graph_cache":
+        st = c.stats()
+        assert st["graph_replays"] >= 1, st
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("bench", list(SMALL))
+@pytest.mark.parametrize("mode", ["resident", "stream"])
+def test_hand_written_graph_matches_oracle(bench, mode):
+    c = D.Context(device=0)
+    p = SMALL[bench](c, mode)
+    p.load_inputs(1)
+    g = p.graph()
+    if mode == "stream":
+        p.begin_run()  # host-newer inputs; the graph's H2D nodes upload them
+    g.run()
+    torch.cuda.synchronize()
+    check(p, 1)
+    del p, g
+    c.close()
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ NORM
+@pytest.mark.parametrize("n,lo,hi", [(100_003, -(1 << 20), 1 << 20),
+                                     (40_000, -(1 << 31), (1 << 31) - 1),
+                                     (7, 0, 2)])
+def test_ml_norm_wide_range(n, lo, hi):
+    """X ~ U{lo..hi}: the sum of squares exceeds 64 bits for the full int32
+    range (40k rows x 2^62); NORM's statistics must still be exact."""
+    c = D.Context(device=0)
+    p = MLEnsemble(c, n=n)
+    p.load_inputs(0)
+    rng = np.random.default_rng(n)
+    X = rng.integers(lo, hi, size=(n, p.f), endpoint=True).astype(np.int32)
+    p.t["X"].copy_(torch.from_numpy(X.ravel()))
+    p.settle()
+    p.run()
+    c.sync()
+    mu, sd = oml.norm_stats(X)
+    st = p.t["stats"][16:16 + 16 * p.f].view(torch.float64).cpu().numpy()
+    assert np.allclose(st[:p.f], mu, rtol=1e-12, atol=1e-9 * max(1, abs(lo), hi))
+    assert np.allclose(1.0 / st[p.f:], sd, rtol=1e-12)
+    Z = p.t["Z"].cpu().numpy().reshape(n, p.f)
+    assert_close(Z, oml.apply_norm(X, mu, sd), "Z")
+    if n > 100:
+        pr = {k: v.astype(np.float64) for k, v in p.params.items()}
+        r2 = oml.softmax(oml.addv(oml.mmul(oml.apply_norm(X, mu, sd), pr["W"]), pr["b"]))
+        assert_close(p.t["r2"].cpu().numpy().reshape(n, p.c), r2, "r2")
+    c.close()
+
+
+# ------------------------------------------------------------------ DL
+def test_dl_4096_elementwise():
+    """4096^2: 2,048 conv2 tiles over 148 CTAs x 3 consumer groups -> every
+    group reuses its TMA stage and flips its mbarrier phase several times."""
+    c = D.Context(device=0)
+    p = DeepLearning(c, h=4096, w=4096)
+    p.load_inputs(0)
+    p.run()
+    c.sync()
+    check(p, 0)
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
+def _c2_strip(seed, spec, name, h, w, w1, w2, P0, P1):
+    """Oracle conv2 output rows [P0, P1) of a full-size branch, from input
+    rows [8*P0 - 8, 8*P1 + 8) (aligned to 8, so every stride lines up; the
+    strip's artificial zero border only reaches the discarded first row)."""
+    xa, xb = max(0, 8 * P0 - 8), min(h, 8 * P1 + 8)
+    idx = np.arange(xa * w, xb * w, dtype=np.uint64)
+    x = synth.draw(seed, name, spec[name], idx).reshape(xb - xa, w)
+    c2 = odl.conv3x3s2(odl.pool2x2(odl.conv3x3s2(x, w1)), w2)
+    off = (P0 - xa // 8)
+    return c2[off:off + (P1 - P0)]
+
+
+def test_dl_full_size_strips_and_r():
+    """2 x 16384^2 (BASELINE configs[4], bench launch configuration): c2x and
+    c2y element-wise on strips spread over the image (first/last rows, every
+    CTA's interleaved tiles), and r = z . wd against the oracle's r computed
+    from the oracle's own c2 over the whole image (strip by strip)."""
+    h = w = 16384
+    c = D.Context(device=0)
+    p = DeepLearning(c, h=h, w=w)
+    p.load_inputs(0)
+    p.run()
+    c.sync()
+    spec = synth.spec_dl(h, w)
+    w1 = synth.draw(p.seed, "w1", spec["w1"]).reshape(8, 3, 3, 1)
+    w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
+    wd = synth.draw(p.seed, "wd", spec["wd"]).astype(np.float64)
+    (_, _), (_, _), (h3, w3s) = p.shapes
+    half = h3 * w3s * 16
+    r_o = 0.0
+    strip = 256
+    checked = {0, h3 // strip // 2, h3 // strip - 1}
+    for bi, name in enumerate(("x", "y")):
+        for s0 in range(0, h3, strip):
+            s1 = min(h3, s0 + strip)
+            ref = _c2_strip(p.seed, spec, name, h, w, w1, w2, s0, s1)
+            lo = bi * half + s0 * w3s * 16
+            r_o += float(np.dot(ref.ravel(), wd[lo:lo + ref.size]))
+            if s0 // strip in checked:
+                got = p.t[f"c2{name}"][s0 * w3s * 16:s1 * w3s * 16].cpu().numpy()
+                assert_close(got, ref.ravel(), (name, s0))
+    assert abs(red(p.t["r"]) - r_o) <= 1e-3 * abs(r_o), (red(p.t["r"]), r_o)
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ B&S limits
+@pytest.mark.parametrize("svals", [[1e-3, 1.0, 600.0, 1e6], [59.999, 60.0, 60.001, 1e-300, 5e5]])
+def test_bs_limits(svals):
+    """S << K (C -> 0: the 1e-12 absolute term) and S >> K (C -> S - K e^-RT)
+    through the product kernel's table-driven log/exp, ragged length."""
+    n = 4 * 1031 + 3
+    c = D.Context(device=0)
+    p = BlackScholes(c, n=n, nvec=1)
+    s = np.resize(np.asarray(svals, np.float64), n)
+    p.t["s0"].copy_(torch.from_numpy(s))
+    p.settle()
+    p.run()
+    c.sync()
+    ref = obs.call(s)
+    out = p.t["c0"].cpu().numpy()
+    err = np.abs(out - ref) - (1e-10 * np.abs(ref) + 1e-12)
+    assert np.all(err <= 0), (float(err.max()), s[np.argmax(err)])
+    c.close()
+
+
+# ------------------------------------------------------------------ graph cache ordering
+def test_graph_cache_orders_same_stream_work_across_flush():
+    """K1 writes A, K2 writes B, host reads B (K1 stays active),
+    loop.  In the next run K1' (child of the still-active K1, same stream, no
+    event wait) must not overlap K1 when it replays inside a graph.  A is
+    incremented by each K1: after R runs every element equals R."""
+    c = D.Context(device=0, graph_cache=True)
+    n = 1 << 22
+    A = torch.zeros(n, device="cuda")
+    B = torch.zeros(n, device="cuda")
+    torch.cuda.synchronize()
+    a = c.register_tensor("A", A)
+    b = c.register_tensor("B", B)
+    import ctypes as C
+    buf = (C.c_float * 1)()
+    runs = 12
+    for _ in range(runs):
+        for _ in range(8):  # a long chain on A's stream keeps K1 in flight
+            c.launch("axpb", 4 * 148, 256, a, n, 1.0, 0.125)
+        c.launch("axpb", 148, 256, b, n, 1.0, 1.0)
+        c.host_read(b, C.addressof(buf), 0, 4)
+    c.sync()
+    assert torch.all(A == runs).item(), float((A - runs).abs().max())
+    assert torch.all(B == runs).item()
+    st = c.stats()
+    assert st["graph_replays"] >= runs - 3, st
+    c.close()

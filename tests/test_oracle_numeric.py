@@ -175,6 +175,30 @@ def test_ml_norm_moments():
     assert np.all(oml.norm(Xc)[:, 3] == 0.0)
 
 
+def test_ml_norm_stats_closed_forms_and_statistics_module():
+    """NORM statistics pinned outside the oracle: an arithmetic progression
+    0..n-1 has population variance (n^2 - 1)/12; a two-valued column {-a, a}
+    in equal halves has mean 0 and sd a; wide-range columns (|x| up to 2^31)
+    agree with Python's exact-rational statistics.pstdev."""
+    import statistics
+    n = 1001
+    X = np.stack([np.arange(n), np.where(np.arange(n) % 2 == 0, -(1 << 30), 1 << 30)[:n],
+                  np.full(n, 7)], axis=1).astype(np.int64)
+    X[-1, 1] = 0  # odd n: make the two-valued column symmetric (mean 0)
+    mu, sd = oml.norm_stats(X, chunk=97)
+    assert mu[0] == (n - 1) / 2 and abs(sd[0] - math.sqrt((n * n - 1) / 12)) <= 1e-12 * sd[0]
+    assert mu[1] == 0.0
+    assert abs(sd[1] - math.sqrt(statistics.pvariance([int(v) for v in X[:, 1]]))) <= 1e-12 * sd[1]
+    assert mu[2] == 7 and sd[2] == 1.0  # constant column: sd = 0 -> 1
+    rng = np.random.default_rng(5)
+    W = rng.integers(-(1 << 31), (1 << 31) - 1, size=(3000, 4), endpoint=True)
+    mu, sd = oml.norm_stats(W.astype(np.int32), chunk=512)
+    for j in range(4):
+        col = [int(v) for v in W[:, j]]
+        assert abs(mu[j] - statistics.fmean(col)) <= 1e-9 * (1 << 31) / 3000
+        assert abs(sd[j] - statistics.pstdev(col)) <= 1e-12 * sd[j]
+
+
 def test_ml_nb_posteriors_equal_scipy_softmax():
     X, theta, prior, W, b = _ml_inputs()
     out = oml.ml(X, theta, prior, W, b)

@@ -82,10 +82,10 @@ def arrays_of(trace):
     return s
 
 
-def check_against_oracle(trace, nbytes=128):
-    rp = Replayer(arrays_of(trace), nbytes).run(trace)
+def check_against_oracle(trace, nbytes=128, policy="parallel"):
+    rp = Replayer(arrays_of(trace), nbytes, policy=policy).run(trace)
     verts, edges = rp.dag()
-    o = odag.build_dag(trace)
+    o = odag.build_dag(trace, stream_policy="single" if policy == "single_stream" else "fifo")
     ov = [(v[0], v[2], v[3], v[4]) for v in o.vertices]
     gv = [(v[0], v[1], v[2], v[3]) for v in verts]
     assert gv == ov, (trace, gv, ov)
@@ -147,6 +147,33 @@ def test_random_traces():
             else:
                 tr.append(("sync",))
         check_against_oracle(tr)
+
+
+@pytest.mark.parametrize("name,case", CASES, ids=[c[0] for c in CASES])
+def test_single_stream_policy_golden(name, case):
+    """The "schedule all children on a single stream" policy (L650-654):
+    identical DAG (edges are policy-independent), streams and waits equal to
+    the oracle's single-stream rule, and (on these DAGs) no more streams than
+    the general policy."""
+    rp = check_against_oracle(case["trace"], policy="single_stream")
+    verts, edges = rp.dag()
+    assert edges == case["edges"]
+    gen = Replayer(arrays_of(case["trace"]), 128).run(case["trace"])
+    assert rp.ctx.stream_count() <= gen.ctx.stream_count()
+
+
+def test_single_stream_policy_random_traces():
+    rng = random.Random(77)
+    names = list("ABCDE")
+    for _ in range(150):
+        tr = []
+        for _ in range(rng.randint(1, 60)):
+            if rng.random() < 0.85:
+                tr.append(("launch", "k", [(rng.choice(names), rng.choice(["R", "R", "RW", "O"]))
+                                           for _ in range(rng.randint(1, 4))]))
+            else:
+                tr.append(("host", rng.choice(names), rng.choice("RW"), 0, 128))
+        check_against_oracle(tr, policy="single_stream")
 
 
 def test_serial_policy_has_no_edges_and_one_stream():
