@@ -511,6 +511,12 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
                                  + "; R_work = all vertex bytes; frac = R / measured ms per DAG"},
         "clocks": clk.summary(),
         "scheduler": {"sched_us_per_launch": st["sched_ns"] / max(1, st["launches"]) / 1e3,
+                      "breakdown_us_per_launch": {
+                          k: st[f] / max(1, st["launches"]) / 1e3 for k, f in
+                          (("cuLaunchKernel", "launch_ns"), ("cudaEventRecord", "record_ns"),
+                           ("waits_and_h2d_enqueue", "wait_ns"))} | {
+                          "bookkeeping": (st["sched_ns"] - st["launch_ns"] - st["record_ns"] - st["wait_ns"])
+                          / max(1, st["launches"]) / 1e3},
                       "cross_stream_waits_per_dag": st["cross_stream_waits"] / K,
                       "streams": st["streams"]},
         "baselines": res,

@@ -264,6 +264,11 @@ typedef struct {
   uint64_t graph_replays;      /* batches replayed from the graph cache */
   uint64_t graph_captures;     /* batches captured into a new graph */
   uint64_t eager_batches;      /* batches issued eagerly (first sighting) */
+  /* breakdown of sched_ns (host ns inside dagrt_launch): time in the CUDA
+   * enqueue calls themselves; the rest is the scheduler's own bookkeeping */
+  uint64_t launch_ns;          /* cuLaunchKernel / cudaLaunchCooperativeKernel */
+  uint64_t record_ns;          /* cudaEventRecord of the vertex event */
+  uint64_t wait_ns;            /* cudaStreamWaitEvent (cross-stream and copy waits) + H2D enqueue */
 } dagrt_stats_t;
 /* Copy min(size, sizeof(dagrt_stats_t)) bytes of the counters to out. */
 dagrt_status dagrt_stats(dagrt_ctx ctx, void* out, size_t size);

@@ -559,7 +559,14 @@ struct DeferBackend final : Backend {
         ++replays;
         done = true;
       }
-    if (!done && std::find(nocap.begin(), nocap.end(), h) == nocap.end() &&
+    // Only batches with kernel launches are worth a graph: a batch of waits and
+    // copies alone (the later host reads of a DAG whose kernels already went
+    // out in an earlier graph) is issued eagerly on its own streams, where it
+    // waits for exactly its producers -- a graph would queue it on `origin`
+    // behind the whole earlier graph.
+    bool has_launch = false;
+    for (const Op& o : ops) has_launch = has_launch || o.kind == OP_LAUNCH;
+    if (!done && has_launch && std::find(nocap.begin(), nocap.end(), h) == nocap.end() &&
         std::find(seen.begin(), seen.end(), h) != seen.end()) {
       Entry en;
       en.key = key;
@@ -839,6 +846,11 @@ dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim
     c->prof.push_back(ProfRec{kh, e0, e1});
   }
   return DAGRT_OK;
+}
+
+inline uint64_t now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
 // Retire vertex v and all its active ancestors (D4/D5: a host sync on v
@@ -1417,6 +1429,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   void* s = c->streams[sid].s;
 
   // (5) events: wait on parents running on other streams (one wait each)
+  const uint64_t tw0 = now_ns();
   for (uint32_t p : c->scratch_parents) {
     const VertexRec& pv = c->vertices[p];
     if (pv.stream != sid) {
@@ -1464,10 +1477,15 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   // (6) launch + event
   void* ev;
   if (dagrt_status st = get_event(c, &ev)) return st;
+  const uint64_t tl0 = now_ns();
+  c->st.wait_ns += tl0 - tw0;
   trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
   if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, vid)) return st_;
+  const uint64_t tr0 = now_ns();
+  c->st.launch_ns += tr0 - tl0;
   trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
   CK(c->be->record(ev, s), "cudaEventRecord");
+  c->st.record_ns += now_ns() - tr0;
 
   // bookkeeping: vertex, frontier, dependency sets
   uint32_t pbeg = (uint32_t)c->parent_pool.size();
