@@ -101,6 +101,28 @@ __device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long lo
   }
 }
 
+// Single-thread deposit protocol (spmv_nz): participant c puts its share of
+// a row spanning warps cs..ce (the end participant into head[], the others
+// into part[]); the last to arrive at cnt[cs] adds them in warp order.
+__device__ __forceinline__ void spmv_ws_put(const SpmvWs& ws, long long c, float val, bool is_end) {
+  if (is_end) ws.head[c] = val;
+  else ws.part[c] = val;
+}
+__device__ __forceinline__ bool spmv_ws_arrive(const SpmvWs& ws, long long cs, long long ce) {
+  __threadfence();
+  const unsigned old = atomicAdd(ws.cnt + cs, 1u);
+  if (old != (unsigned)(ce - cs)) return false;
+  __threadfence();
+  ws.cnt[cs] = 0;  // reusable by the next launch
+  return true;
+}
+__device__ __forceinline__ float spmv_ws_sum(const SpmvWs& ws, long long cs, long long ce) {
+  float s = 0.f;
+  const volatile float* p = ws.part;
+  for (long long c = cs; c < ce; ++c) s += p[c];
+  return s + ((volatile float*)ws.head)[ce];
+}
+
 // Persistent merge-path SpMV with WARP tiles.  Global warp g of G owns the
 // contiguous merge range of tiles [g*per, (g+1)*per), each tile 256 items
 // (8 per lane).  Warps never wait for each other (no CTA barriers): a warp
@@ -688,6 +710,265 @@ __global__ void __launch_bounds__(256) k_spmv_plan_h(const int* __restrict__ row
   spmv_plan_body<1>(row_ptr, col, plan, x, y, N);
 }
 
+// ---------------------------------------------------------------------------
+// NON-ZERO-SPLIT SpMV ("spmv_nz", the product kernel since round 2).
+//
+// Measured bound on the HITS graph (tools/spmv_lab.py, profiles/r2_spmv_lab*):
+// the 54M random 4-byte gathers alone, with the column stream, take 177 us
+// (~1.1 gathers per SM per clock: one L1 wavefront per divergent lane), the
+// column stream alone 35 us; the merge-path kernel above took 364 us, i.e.
+// half its time went to the row structure (merge search, marks, row-end
+// scans over N + E items, 45% of the rows being empty).  This kernel walks
+// the NON-ZEROS only, in chunks of 128 (4 per lane, one 128-bit column load
+// per lane, 4 gathers in flight), with the row structure re-encoded once when
+// the graph is registered (spmv_nz_plan() in programs/hits_dl.py; the graph
+// is static and resident):
+//   flags[]  1 bit per non-zero: it starts a (non-empty) row;
+//   nzrow[]  the ids of the non-empty rows, in order (ordinals -> row ids);
+//   rbase[]  ordinal of the row holding each chunk's first non-zero.
+// Per chunk a lane sums its items per row segment, a segmented warp scan
+// carries open rows across lanes (and a register across the warp's chunks),
+// and every completed row is written by the lane where it ends, together
+// with the zeros of the empty rows just before it.  Global warp g owns the
+// contiguous chunk range [g*per, (g+1)*per): equal non-zeros per warp
+// whatever the degree distribution.  A row spanning several warp ranges is
+// finished by the last of its participants to deposit its share (atomic
+// arrival count; shares added in warp order) -> bit-reproducible, no float
+// atomics.  Column indices are streamed with L1::no_allocate and L2
+// evict_first so that L1 and L2 keep the gathered vector (lab: 177 vs 184 us
+// for plain loads).  row_ptr is read only for rows crossing warp ranges.
+// Workspace after y's N floats: SpmvWs (3 words per warp of the grid).
+constexpr int kNzChunk = 128;  // non-zeros per warp chunk (4 per lane)
+constexpr int kNzHeader = 16;  // plan header ints
+constexpr int kNzMagic = 0x4e5a3031;  // "NZ01"
+
+struct NzPlan {
+  int nc, nr;           // chunks, non-empty rows
+  const int* rbase;     // [nc + 1]
+  const unsigned* flags;  // [ceil(E / 32) + 4]
+  const int* nzrow;     // [nr]
+};
+
+__device__ __forceinline__ NzPlan nz_plan(const int* plan) {
+  if (__ldg(plan) != kNzMagic || __ldg(plan + 3) != kNzChunk) __trap();  // built for another kernel
+  NzPlan P;
+  P.nc = __ldg(plan + 1);
+  P.nr = __ldg(plan + 2);
+  P.rbase = plan + __ldg(plan + 4);
+  P.flags = reinterpret_cast<const unsigned*>(plan + __ldg(plan + 5));
+  P.nzrow = plan + __ldg(plan + 6);
+  return P;
+}
+
+__device__ __forceinline__ int4 ld_cols_stream(const int* p, uint64_t pol) {
+  int4 c;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(p), "l"(pol));
+  return c;
+}
+
+// One chunk's streamed inputs for one lane: 4 column indices and their 4
+// row-start flag bits.
+struct NzIn {
+  int c[4];
+  unsigned fl;
+};
+
+__device__ __forceinline__ NzIn nz_load(const int* __restrict__ col, const NzPlan& P, int k, int E,
+                                        uint64_t pol) {
+  NzIn in;
+  if (k + 3 < E) {
+    const int4 q = ld_cols_stream(col + k, pol);
+    in.c[0] = q.x; in.c[1] = q.y; in.c[2] = q.z; in.c[3] = q.w;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) in.c[u] = k + u < E ? __ldg(col + k + u) : -1;
+  }
+  in.fl = (__ldg(P.flags + (k >> 5)) >> (k & 31)) & 0xFu;
+  if (k + 3 >= E) in.fl &= (k < E ? (1u << (E - k)) - 1u : 0u);
+  return in;
+}
+
+__device__ __forceinline__ void nz_gather(const NzIn& in, const float* __restrict__ x, float (&v)[4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = in.c[u] >= 0 ? __ldg(x + in.c[u]) : 0.f;
+}
+
+// Software pipeline per warp: while chunk c is reduced, the column indices
+// and flags of chunk c+2 and the gathers of chunk c+1 are in flight, and the
+// row ids of chunk c's completed rows are loaded before its gathered values
+// are consumed -- the three dependent memory latencies of a chunk (indices ->
+// gathers; ordinals -> row ids) overlap with the neighbouring chunks' work.
+__global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                 const int* __restrict__ plan, const float* __restrict__ x,
+                                                 float* __restrict__ y, long long N_) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int N = (int)N_;
+  const NzPlan P = nz_plan(plan);
+  const int E = __ldg(row_ptr + N);
+  const int G = (int)gridDim.x * (blockDim.x >> 5);
+  const int g = (int)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (P.nr == 0) {  // no non-zeros: y = 0
+    for (int i = g * 32 + lane; i < N; i += G * 32) y[i] = 0.f;
+    return;
+  }
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;  // warp-uniform; the kernel has no CTA barriers
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  const uint64_t pol = l2_policy_evict_first();
+  auto warp_of_nz = [&](int k) { return (k / kNzChunk) / per; };
+
+  // R0 = ordinal of the row open at the start of the current chunk: at the
+  // range start, the row holding its first item (whose start bit, if any, is
+  // consumed here); it began in an earlier warp's range unless that item
+  // starts it
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);
+  bool head_pending = !start0;
+  float carry = 0.f;
+
+  NzIn cur = nz_load(col, P, cb * kNzChunk + 4 * lane, E, pol);
+  NzIn nxt = cur;
+  if (cb + 1 < ce) nxt = nz_load(col, P, (cb + 1) * kNzChunk + 4 * lane, E, pol);
+  float v[4];
+  nz_gather(cur, x, v);
+  for (int c = cb; c < ce; ++c) {
+    unsigned fl = cur.fl;
+    if (c == cb && lane == 0) fl &= ~1u;  // the range's first item: handled by start0/head_pending
+    // ---- ordinals of the rows completed in this lane (no dependence on the gathers)
+    const int nst = __popc(fl);
+    int incl = nst;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int excl = incl - nst;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int o = R0 + excl;  // the row open entering the lane; ends at its first start
+    // row ids of ordinals o-1 .. o+3 (those this lane writes), in registers
+    int rid0 = -1, rid1 = -1, rid2 = -1, rid3 = -1, rid4 = -1;
+    if (nst) {
+      rid0 = o > 0 ? __ldg(P.nzrow + o - 1) : -1;
+      rid1 = __ldg(P.nzrow + o);
+      if (nst > 1) rid2 = __ldg(P.nzrow + o + 1);
+      if (nst > 2) rid3 = __ldg(P.nzrow + o + 2);
+      if (nst > 3) rid4 = __ldg(P.nzrow + o + 3);
+    }
+    auto rid = [&](int j) { return j <= 1 ? (j == 0 ? rid0 : rid1) : (j == 2 ? rid2 : (j == 3 ? rid3 : rid4)); };
+    // ---- next chunk's gathers and the chunk after's indices go in flight
+    float vn[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c + 1 < ce) {
+      nz_gather(nxt, x, vn);
+      cur = nxt;
+      if (c + 2 < ce) nxt = nz_load(col, P, (c + 2) * kNzChunk + 4 * lane, E, pol);
+    }
+    // ---- lane-local row segments of this chunk
+    float run = 0.f, head = 0.f;
+    bool seen = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((fl >> u) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.f;
+      }
+      run += v[u];
+    }
+    if (!seen) head = run;
+    // ---- segmented exclusive scan: carry into each lane of the open row
+    float sv = nst ? run : head;
+    bool sf = nst != 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+      const bool tf = __shfl_up_sync(0xffffffffu, sf, off);
+      if (lane >= off && !sf) { sv += tv; sf = tf; }
+    }
+    float cin = __shfl_up_sync(0xffffffffu, sv, 1);
+    const bool fin = __shfl_up_sync(0xffffffffu, sf, 1);
+    if (lane == 0) cin = carry;
+    else if (!fin) cin += carry;
+    // ---- rows completed in this lane: y[row] = sum, zeros for the empty rows before it
+    if (nst) {
+      const float val = cin + head;
+      if (head_pending && excl == 0) {
+        // began before this warp's range: deposit (this warp holds its end)
+        const int cs = warp_of_nz(__ldg(row_ptr + rid1));
+        spmv_ws_put(ws, g, val, true);
+        if (spmv_ws_arrive(ws, cs, g)) {
+          for (int r = rid0 + 1; r < rid1; ++r) y[r] = 0.f;
+          y[rid1] = spmv_ws_sum(ws, cs, g);
+        }
+      } else {
+        for (int r = rid0 + 1; r < rid1; ++r) y[r] = 0.f;
+        y[rid1] = val;
+      }
+      int j = 1;
+      float r2 = 0.f;
+      bool in = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (in) {
+            const int a = rid(j), b = rid(j + 1);
+            for (int r = a + 1; r < b; ++r) y[r] = 0.f;
+            y[b] = r2;
+            ++j;
+          }
+          in = true;
+          r2 = 0.f;
+        }
+        r2 += v[u];
+      }
+    }
+    // ---- carry to the next chunk
+    const float tail_all = __shfl_sync(0xffffffffu, sv, 31);
+    const bool any = __shfl_sync(0xffffffffu, sf, 31);
+    carry = any ? tail_all : carry + tail_all;
+    if (any) head_pending = false;
+    R0 += total;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = vn[u];
+  }
+  // ---- the row open at the range end (and, for the last non-empty row, the
+  // empty rows after it)
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= E || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    const int row = __ldg(P.nzrow + R0);
+    const int prev = R0 > 0 ? __ldg(P.nzrow + R0 - 1) : -1;
+    float out = carry;
+    bool write = true;
+    if (ends_here) {
+      if (head_pending) {  // spans the whole range, ends at its end
+        const int cs = warp_of_nz(__ldg(row_ptr + row));
+        spmv_ws_put(ws, g, carry, true);
+        write = spmv_ws_arrive(ws, cs, g);
+        if (write) out = spmv_ws_sum(ws, cs, g);
+      }
+    } else {
+      const int cs = warp_of_nz(__ldg(row_ptr + row));
+      const int cend = warp_of_nz(__ldg(row_ptr + row + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      write = spmv_ws_arrive(ws, cs, cend);
+      if (write) out = spmv_ws_sum(ws, cs, cend);
+    }
+    if (write) {
+      for (int r = prev + 1; r < row; ++r) y[r] = 0.f;
+      y[row] = out;
+      if (R0 == P.nr - 1)
+        for (int r = row + 1; r < N; ++r) y[r] = 0.f;
+    }
+  }
+  // rows completed inside the loop never include the last non-empty row's
+  // tail zeros unless it completed there: the writer of ordinal nr-1 in the
+  // loop is the lane whose start follows it -- impossible (no start after the
+  // last row) -- so the tail zeros are always written above.
+}
+
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
 __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, RedOut* out,
                                                 long long n) {
@@ -734,9 +1015,10 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 }
 
 static const Builtin kHits[] = {
-    // merge-path SpMV (product) and its variants: gathers in registers
+    // merge-path SpMV (round-1 product) and its variants: gathers in registers
     // (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
-    {"spmv", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // product: non-zero-split SpMV: row_ptr, col, plan (programs/hits_dl.py spmv_nz_plan), x, y, N
+    {"spmv", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_merge", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     // row-class SpMV (measured slower, kept as a tested alternative): row_ptr, col,
     // plan (programs/hits_dl.py spmv_plan), x, y, N

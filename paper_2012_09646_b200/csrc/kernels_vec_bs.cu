@@ -185,6 +185,185 @@ __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsT
   return fma(s, c1, -C.kexp * c2);
 }
 
+// ---------------------------------------------------------------- B&S, round 2
+// Same A&S 26.2.17 pricing (SURVEY §8(c2) B&S), ~38 FP64 operations per
+// option instead of 46, by algebra rather than approximation:
+//   * C = S CND(d1) - K e^{-RT} CND(d2) with CND(d) = u + sigma p, u = [d > 0],
+//     sigma = -1 if d > 0 else +1, p = phi(d) k poly(k):
+//       K e^{-RT} p2 = K e^{-RT} phi(d2) w2 = S phi(d1) w2   (phi(d2) = phi(d1) S e^{RT}/K)
+//     so C = (S u1 - K e^{-RT} u2) + S phi(d1) (sigma1 w1 - sigma2 w2): no
+//     second exponential, no products by e2, the signs flipped on the integer
+//     pipe (sign bit of w), the first term selected among {0, S, S - Ke^{-RT}}
+//     (d2 < d1, so u2 implies u1);
+//   * phi(d1) = exp(-h/2), h = d1^2: the -1/2 is folded into the exp's range
+//     reduction and polynomial (r2 = h + 2 n ln2/64, e^{-r2/2} by a
+//     polynomial in r2 with rescaled coefficients);
+//   * exp reduction with one ln2/64 constant (error <= 745 * 2^-53 relative
+//     ~ 1e-13, far inside the 1e-10 tolerance) instead of a hi/lo pair.
+// The computation is written W options in lockstep (every statement over a
+// small array), so independent FP64 chains interleave in the instruction
+// stream whatever ptxas's scheduler does with the inlined copies.
+enum { kc2Ln2_64, kcNeg32Ln2, kcE0, kcE1, kcE2, kcE3, kcE4, kc2Count };
+__constant__ double kBs2K[kc2Count] = {
+    0.02166084939249829,      // 2 ln2 / 64
+    -46.16624130844683,       // -32 / ln2  (t = round(-h/2 * 64/ln2))
+    // e^{-r2/2} = 1 - r2/2 + r2^2/8 - r2^3/48 + r2^4/384 (|r2| <= 2 ln2/128)
+    1.0 / 384.0, -1.0 / 48.0, 1.0 / 8.0, -0.5, 1.0};
+
+template <int W>
+__device__ __forceinline__ void bs_price_w(const double (&s)[W], double (&out)[W], const BsConst& C,
+                                           const BsTables& T) {
+  const double B1 = kBsK[kcB1], B2 = kBsK[kcB2], B3 = kBsK[kcB3], B4 = kBsK[kcB4], B5 = kBsK[kcB5],
+               A = kBsK[kcA];
+  double L[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) L[w] = bs_log(s[w] * C.inv_k, T);
+  double d1[W], d2[W], h[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    d1[w] = fma(L[w], C.inv_vst, C.mu_s);
+    d2[w] = d1[w] - C.vst;
+    h[w] = d1[w] * d1[w];
+  }
+  // phi(d1) * sqrt(2 pi) = exp(-h/2), h clamped to ~1400 by an integer min on
+  // its high word (exp(-700) ~ 1e-304 then stands for 0: the scaling by
+  // 2^(n/64) stays in the normal range, and S e1 m is ~1e-298 or less)
+  double e1[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const double hc = __hiloint2double(min(__double2hiint(h[w]), 0x4095E000), __double2loint(h[w]));
+    const double t = fma(hc, kBs2K[kcNeg32Ln2], kRound);
+    const int n = __double2loint(t);
+    const double nd = t - kRound;
+    const double r2 = fma(nd, kBs2K[kc2Ln2_64], hc);
+    double p = fma(r2, kBs2K[kcE0], kBs2K[kcE1]);
+    p = fma(r2, p, kBs2K[kcE2]);
+    p = fma(r2, p, kBs2K[kcE3]);
+    p = fma(r2, p, kBs2K[kcE4]);
+    const double sc = T.exp2j[n & 63] * p;
+    e1[w] = __hiloint2double(__double2hiint(sc) + ((n >> 6) << 20), __double2loint(sc));
+  }
+  double k1[W], k2[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const double D1 = fma(A, fabs(d1[w]), 1.0), D2 = fma(A, fabs(d2[w]), 1.0);
+    const double P = D1 * D2;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(P));
+    const double er = fma(-P, y, 1.0);
+    y = fma(y, er, y);
+    k1[w] = D2 * y;
+    k2[w] = D1 * y;
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    double q1 = fma(k1[w], B5, B4), q2 = fma(k2[w], B5, B4);
+    q1 = fma(k1[w], q1, B3);
+    q2 = fma(k2[w], q2, B3);
+    q1 = fma(k1[w], q1, B2);
+    q2 = fma(k2[w], q2, B2);
+    q1 = fma(k1[w], q1, B1);
+    q2 = fma(k2[w], q2, B1);
+    const double w1 = q1 * k1[w], w2 = q2 * k2[w];
+    const bool u1 = __double2hiint(d1[w]) > 0, u2 = __double2hiint(d2[w]) > 0;
+    // sigma1 w1 - sigma2 w2: sign bits flipped on the integer pipe
+    const double a1 = __hiloint2double(__double2hiint(w1) ^ (u1 ? 0x80000000 : 0), __double2loint(w1));
+    const double a2 = __hiloint2double(__double2hiint(w2) ^ (u2 ? 0 : 0x80000000), __double2loint(w2));
+    const double m = a1 + a2;
+    const double sk = s[w] - C.kexp;
+    const double base = u2 ? sk : (u1 ? s[w] : 0.0);
+    out[w] = fma(s[w] * e1[w], m, base);
+  }
+}
+
+// Lean loop of bs_body_lean with the lockstep pricer: PAIRS double2 per
+// thread per group, priced W options at a time.
+template <int PAIRS, int W>
+__device__ __forceinline__ void bs2_body(const double* __restrict__ s, double* __restrict__ c, long long n,
+                                         double r, double v, double t, double k) {
+  __shared__ BsTables T;
+  bs_tables_init(T);
+  BsConst C;
+  const double vst = v * sqrt(t);
+  C.vst = vst;
+  C.inv_vst = 1.0 / vst;
+  C.mu_s = (r + 0.5 * v * v) * t / vst;
+  C.inv_k = 1.0 / k;
+  C.c2 = exp(r * t) / k;
+  C.kexp = k * exp(-r * t);
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned nth = gridDim.x * blockDim.x;
+  if (!(aligned16(s) && aligned16(c)) || n >= (1ll << 31)) {
+    for (long long i = tid; i < n; i += nth) {
+      double a[1] = {s[i]}, o[1];
+      bs_price_w<1>(a, o, C, T);
+      c[i] = o[0];
+    }
+    return;
+  }
+  static_assert((2 * PAIRS) % W == 0 && W % 2 == 0, "W even, dividing the options per group");
+  const unsigned n2 = (unsigned)(n >> 1);
+  const unsigned step = PAIRS * nth;
+  const unsigned nfull = n2 / step;
+  const double2* s2 = reinterpret_cast<const double2*>(s);
+  double2* c2 = reinterpret_cast<double2*>(c);
+  double2 xa[PAIRS], xb[PAIRS];
+  auto load = [&](double2(&x)[PAIRS], unsigned base) {
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) x[q] = ldg_stream(s2 + base + q * nth);
+  };
+  auto price = [&](const double2(&x)[PAIRS], unsigned base) {
+#pragma unroll
+    for (int g0 = 0; g0 < 2 * PAIRS; g0 += W) {
+      double a[W], o[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) a[w] = ((g0 + w) & 1) ? x[(g0 + w) >> 1].y : x[(g0 + w) >> 1].x;
+      bs_price_w<W>(a, o, C, T);
+#pragma unroll
+      for (int w = 0; w < W; w += 2) c2[base + ((g0 + w) >> 1) * nth] = make_double2(o[w], o[w + 1]);
+    }
+  };
+  unsigned base = tid, j = 0;
+  if (nfull > 0) load(xa, base);
+  for (; j + 2 <= nfull; j += 2) {
+    load(xb, base + step);
+    price(xa, base);
+    if (j + 2 < nfull) load(xa, base + 2 * step);
+    price(xb, base + step);
+    base += 2 * step;
+  }
+  if (j < nfull) {
+    price(xa, base);
+    base += step;
+  }
+#pragma unroll
+  for (int q = 0; q < PAIRS; ++q) {  // tail: the last partial group
+    const unsigned i = base + q * nth;
+    if (i < n2) {
+      const double2 x = ldg_stream(s2 + i);
+      double a[2] = {x.x, x.y}, o[2];
+      bs_price_w<2>(a, o, C, T);
+      c2[i] = make_double2(o[0], o[1]);
+    }
+  }
+  if ((n & 1) && tid == 0) {
+    double a[1] = {s[n - 1]}, o[1];
+    bs_price_w<1>(a, o, C, T);
+    c[n - 1] = o[0];
+  }
+}
+#define BS2_VARIANT(NAME, PAIRS, W, MINB)                                                         \
+  __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs2_body<PAIRS, W>(s, c, n, r, v, t, k);                                                       \
+  }
+BS2_VARIANT(k_bs2_p3w2b2, 3, 2, 2)
+BS2_VARIANT(k_bs2_p2w2b3, 2, 2, 3)
+BS2_VARIANT(k_bs2_p2w4b2, 2, 4, 2)
+BS2_VARIANT(k_bs2_p4w2b2, 4, 2, 2)
+BS2_VARIANT(k_bs2_p1w2b4, 1, 2, 4)
+
 // K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores.
 // PAIRS double2 per thread per iteration (independent chains for the FP64
 // pipe to interleave); the next group's loads are issued before pricing.
@@ -436,6 +615,11 @@ static const Builtin kVecBs[] = {
     {"bs_l3b2", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_l3b3", (const void*)k_bs_l3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_l8b1", (const void*)k_bs_l8b1, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2_p3w2b2", (const void*)k_bs2_p3w2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2_p2w2b3", (const void*)k_bs2_p2w2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2_p2w4b2", (const void*)k_bs2_p2w4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2_p4w2b2", (const void*)k_bs2_p4w2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2_p1w2b4", (const void*)k_bs2_p1w2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
 };
 DAGRT_REGISTER_BUILTINS(kVecBs);
 

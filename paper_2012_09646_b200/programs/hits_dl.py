@@ -82,6 +82,52 @@ def spmv_plan(row_ptr):
 SPMV_CTAS_PER_SM = int(os.environ.get("DAGRT_SPMV_CTAS_PER_SM", "8"))
 
 
+# non-zero-split SpMV ("spmv" = csrc/kernels_hits.cu k_spmv_nz)
+NZ_CHUNK = 128
+NZ_MAGIC = 0x4E5A3031
+NZ_HEADER = 16
+NZ_CTAS_PER_SM = int(os.environ.get("DAGRT_SPMV_NZ_CTAS_PER_SM", "4"))  # one resident wave (<= 64 registers)
+
+
+def spmv_nz_plan(row_ptr):
+    """Row structure of a CSR re-encoded for k_spmv_nz, built once when the
+    graph is registered (the graph is static and resident):
+    int32 [header(16) | rbase(nc + 1) | flags(ceil(E/32) + 4 words) | nzrow(nr)]
+      flags: bit k set iff non-zero k is the first of its (non-empty) row;
+      nzrow: ids of the non-empty rows in order;
+      rbase[c]: ordinal (index into nzrow) of the row holding non-zero c*128.
+    Returns the plan array."""
+    import numpy as np
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    e = int(rp[-1])
+    deg = np.diff(rp)
+    ne = deg > 0
+    nzrow = np.nonzero(ne)[0].astype(np.int64)
+    starts = rp[:-1][ne]
+    nwords = (e + 31) // 32 + 4
+    # distinct powers of two per word: their sum is their OR (exact in fp64)
+    flags = np.bincount(starts >> 5, weights=np.left_shift(1, starts & 31).astype(np.float64),
+                        minlength=nwords).astype(np.uint64).astype(np.uint32)
+    nc = (e + NZ_CHUNK - 1) // NZ_CHUNK
+    rbase = np.searchsorted(starts, np.arange(nc + 1, dtype=np.int64) * NZ_CHUNK, side="right") - 1
+    rbase = np.maximum(rbase, 0)
+    off_r = NZ_HEADER
+    off_f = off_r + nc + 1
+    off_f += (-off_f) % 4  # 16-byte aligned flag words
+    off_n = off_f + nwords
+    plan = np.zeros(off_n + max(1, nzrow.size), dtype=np.int32)
+    plan[:8] = (NZ_MAGIC, nc, nzrow.size, NZ_CHUNK, off_r, off_f, off_n, e)
+    plan[off_r:off_r + nc + 1] = rbase
+    plan[off_f:off_f + nwords] = flags.view(np.int32)
+    plan[off_n:off_n + nzrow.size] = nzrow
+    return plan
+
+
+def spmv_nz_grid(e):
+    nc = -(-e // NZ_CHUNK)
+    return max(1, min(-(-nc // SPMV_WARPS), NZ_CTAS_PER_SM * SMS))
+
+
 def spmv_out_bytes(n, e):
     """(bytes of an SpMV output: N floats + 3 workspace words per warp, grid)."""
     ntiles = -(-(n + e) // SPMV_TILE)
@@ -98,7 +144,8 @@ class Hits(Program):
         self.n, self.iters = n, iters
         if graph is None:
             src = self.share.csr if self.share is not None else None
-            graph = src if src is not None else synth.powerlaw_graph(self.seed, n, e)
+            graph = src if src is not None else synth.powerlaw_graph(
+                self.seed, n, e, device=None if ctx.backend == "record" else "auto")
         self.csr = graph
         rp, ci, rpt, cit = graph
         self.e = int(rp[-1])
@@ -109,9 +156,19 @@ class Hits(Program):
                 self.upload(name, arr)
         self.alloc("a1", n, torch.float32, mirror=stream)
         self.alloc("h1", n, torch.float32, mirror=stream)
-        ob, gs = spmv_out_bytes(n, self.e)
+        gs = spmv_nz_grid(self.e)
+        ob = 4 * n + 16 + 12 * SPMV_WARPS * gs  # y + SpmvWs (3 words per warp)
         self.alloc("a2", 0, None, nbytes=ob)
         self.alloc("h2", 0, None, nbytes=ob)
+        # row structure of A and A^T re-encoded for the non-zero-split SpMV,
+        # once, when the graph is registered
+        if self.share is not None and "plan" in self.share.t:
+            self.plans = self.share.plans
+        else:
+            self.plans = (spmv_nz_plan(rp), spmv_nz_plan(rpt))
+        for name, arr in (("plan", self.plans[0]), ("plant", self.plans[1])):
+            self.alloc(name, arr.size, torch.int32)
+            self.upload(name, arr)
         self.alloc_red("an")
         self.alloc_red("hn")
         self.inputs, self.sinks = ["a1", "h1"], ["a1", "h1"]
@@ -120,8 +177,8 @@ class Hits(Program):
         ge = grid_1d(n, 256, 4)
         gr = min(grid_1d(n, 256, 8), 1024)
         self.it = [
-            P("spmv", gs, 256, [a["rpt"], a["cit"], a["h1"], a["a2"], n]),  # a2 = A^T h1
-            P("spmv", gs, 256, [a["rp"], a["ci"], a["a1"], a["h2"], n]),    # h2 = A a1
+            P("spmv", gs, 256, [a["rpt"], a["cit"], a["plant"], a["h1"], a["a2"], n]),  # a2 = A^T h1
+            P("spmv", gs, 256, [a["rp"], a["ci"], a["plan"], a["a1"], a["h2"], n]),      # h2 = A a1
             P("l2norm", gr, 256, [a["a2"], a["an"], n]),
             P("l2norm", gr, 256, [a["h2"], a["hn"], n]),
             P("divide", ge, 256, [a["a2"], a["an"], a["a1"], n]),

@@ -179,13 +179,19 @@ def ml_params(seed: int, f: int, c: int):
             "W": w, "b": b}
 
 
-def powerlaw_graph(seed: int, n: int, e_target: int, alpha: float = 2.1):
+def powerlaw_graph(seed: int, n: int, e_target: int, alpha: float = 2.1, device=None):
     """Chung-Lu style power-law digraph (SURVEY §8(d) HITS recipe).
 
     Sources and destinations drawn i.i.d. with P(i) ~ (i+1)^(-1/(alpha-1)),
     relabelled by a seeded permutation; duplicates and self loops removed.
     Returns (row_ptr, col_idx) of A and (row_ptr_t, col_idx_t) of A^T, int32,
     with column indices sorted within each row.
+
+    ``device``: None = numpy on the host; "auto" = a CUDA device through torch
+    when one is present (the full 20M-vertex graph takes minutes in numpy).
+    Both paths use only exact integer operations after the identical fp64
+    draws and cdf (searchsorted, stable sort on the unsigned keys, unique,
+    sort), so they return the same arrays (tests/test_synth.py).
     """
     expo = -1.0 / (alpha - 1.0)
     w = np.power(np.arange(1, n + 1, dtype=np.float64), expo)
@@ -193,11 +199,19 @@ def powerlaw_graph(seed: int, n: int, e_target: int, alpha: float = 2.1):
     cdf /= cdf[-1]
     us = f64_unit(key(seed, "src"), _full(e_target))
     ud = f64_unit(key(seed, "dst"), _full(e_target))
+    pkeys = bits(key(seed, "perm"), _full(n))
+    if device == "auto":
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return _powerlaw_torch(cdf, us, ud, pkeys, n)
+        except ImportError:
+            pass
     src = np.minimum(np.searchsorted(cdf, us, side="right"), n - 1).astype(np.int64)
     dst = np.minimum(np.searchsorted(cdf, ud, side="right"), n - 1).astype(np.int64)
     del us, ud
     # seeded permutation: argsort of random keys
-    perm = np.argsort(bits(key(seed, "perm"), _full(n)), kind="stable").astype(np.int64)
+    perm = np.argsort(pkeys, kind="stable").astype(np.int64)
     src = perm[src]
     dst = perm[dst]
     keep = src != dst
@@ -215,3 +229,36 @@ def powerlaw_graph(seed: int, n: int, e_target: int, alpha: float = 2.1):
     np.cumsum(np.bincount(rt, minlength=n), out=row_ptr_t[1:])
     assert row_ptr[-1] < 2**31
     return (row_ptr.astype(np.int32), c, row_ptr_t.astype(np.int32), ct)
+
+
+def _powerlaw_torch(cdf, us, ud, pkeys, n):
+    """The integer steps of powerlaw_graph on a CUDA device (same results)."""
+    import torch
+    dev = torch.device("cuda")
+    tc = torch.from_numpy(cdf).to(dev)
+    src = torch.clamp(torch.searchsorted(tc, torch.from_numpy(us).to(dev), right=True), max=n - 1)
+    dst = torch.clamp(torch.searchsorted(tc, torch.from_numpy(ud).to(dev), right=True), max=n - 1)
+    del tc
+    # unsigned order of the 64-bit keys = signed order with the sign bit flipped
+    sk = torch.from_numpy((pkeys ^ np.uint64(1 << 63)).view(np.int64)).to(dev)
+    perm = torch.sort(sk, stable=True).indices
+    del sk
+    src = perm[src]
+    dst = perm[dst]
+    keep = src != dst
+    code = torch.unique(src[keep] * n + dst[keep], sorted=True)
+    del src, dst, keep, perm
+    r = code // n
+    c = code % n
+    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    row_ptr[1:] = torch.cumsum(torch.bincount(r, minlength=n), 0)
+    # transpose: (c, r) order = sort of c*n + r (unique codes)
+    codet = torch.sort(c * n + r).values
+    rt = codet // n
+    ct = codet % n
+    row_ptr_t = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    row_ptr_t[1:] = torch.cumsum(torch.bincount(rt, minlength=n), 0)
+    assert int(row_ptr[-1]) < 2**31
+    out = tuple(t.to(torch.int32).cpu().numpy() for t in (row_ptr, c, row_ptr_t, ct))
+    torch.cuda.synchronize()
+    return out

@@ -188,6 +188,29 @@ def test_bs_limits(svals):
     c.close()
 
 
+@pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2"])
+def test_bs_kernels_limits_and_range(kernel):
+    """Every B&S pricing kernel on the limit values plus a dense S sweep over
+    [1e-3, 1e4] (log-spaced): deep out of / in the money, d ~ 0, the exp's
+    underflow clamp; 1e-10 relative + 1e-12 absolute."""
+    n = 200_003
+    s = np.concatenate([np.array([1e-3, 1.0, 600.0, 1e6, 59.999, 60.0, 60.001, 1e-300, 5e5]),
+                        np.logspace(-3, 4, n - 9)])
+    ts = torch.from_numpy(s).cuda()
+    tc = torch.full_like(ts, -1.0)
+    c = D.Context(device=0)
+    torch.cuda.synchronize()
+    S = c.register_tensor("s", ts)
+    Cc = c.register_tensor("c", tc)
+    c.launch(kernel, 37, 256, S, Cc, n, obs.R, obs.V, obs.T, obs.K)
+    c.sync()
+    ref = obs.call(s)
+    out = tc.cpu().numpy()
+    err = np.abs(out - ref) - (1e-10 * np.abs(ref) + 1e-12)
+    assert np.all(err <= 0), (float(err.max()), s[np.argmax(err)], out[np.argmax(err)], ref[np.argmax(err)])
+    c.close()
+
+
 # ------------------------------------------------------------------ graph cache ordering
 def test_graph_cache_orders_same_stream_work_across_flush():
     """K1 writes A, K2 writes B, host reads B (K1 stays active),

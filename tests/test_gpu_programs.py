@@ -232,6 +232,16 @@ def test_ml_full_size_sampled(ctx):
 
 
 # ------------------------------------------------------------------ HITS
+@pytest.mark.parametrize("n,e,seed", [(1, 5, 1), (5000, 15000, 2), (300_000, 900_000, 7)])
+def test_powerlaw_graph_device_path_identical(n, e, seed):
+    """The CUDA path of the graph generator (integer steps through torch)
+    returns exactly the numpy path's CSR arrays."""
+    a = synth.powerlaw_graph(seed, n, e)
+    b = synth.powerlaw_graph(seed, n, e, device="auto")
+    for x, y in zip(a, b):
+        assert x.dtype == y.dtype and np.array_equal(x, y)
+
+
 def _hits_check(p, graph, iters):
     ctx = p.ctx
     o = ohits.hits(*graph, iterations=iters)

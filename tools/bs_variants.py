@@ -25,7 +25,9 @@ def main():
     for name, waves in (("bs", 2), ("bs_p1b6", 6), ("bs_p2b3", 3), ("bs_p2b4", 4), ("bs_p4b2", 2),
                         ("bs_a3b4", 4), ("bs_a5b4", 4), ("bs_a7b4", 4), ("bs_a5b3", 3),
                         ("bs_l4b2", 2), ("bs_l2b3", 3), ("bs_l2b4", 4), ("bs_l1b4", 4),
-                        ("bs_l3b2", 2), ("bs_l3b3", 3), ("bs_l8b1", 1)):
+                        ("bs_l3b2", 2), ("bs_l3b3", 3), ("bs_l8b1", 1),
+                        ("bs2_p3w2b2", 2), ("bs2_p2w2b3", 3), ("bs2_p2w4b2", 2), ("bs2_p4w2b2", 2),
+                        ("bs2_p1w2b4", 4)):
         if sel and name not in sel:
             continue
         for grid_mult in (1, 2, 4):
@@ -44,7 +46,8 @@ def main():
             if ref is None:
                 ref = c.clone()
             same = bool(torch.equal(ref, c))
-            out[f"{name}_g{grid}"] = {"us": us, "GBps": 16 * n / us / 1e3, "bitwise_same": same}
+            rel = float(((ref - c).abs() / (ref.abs() + 1e-12)).max())
+            out[f"{name}_g{grid}"] = {"us": us, "GBps": 16 * n / us / 1e3, "bitwise_same": same, "max_rel_vs_first": rel}
     print(json.dumps(out, indent=1))
 
 
