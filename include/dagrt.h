@@ -269,6 +269,11 @@ typedef struct {
   uint64_t launch_ns;          /* cuLaunchKernel / cudaLaunchCooperativeKernel */
   uint64_t record_ns;          /* cudaEventRecord of the vertex event */
   uint64_t wait_ns;            /* cudaStreamWaitEvent (cross-stream and copy waits) + H2D enqueue */
+  /* bounded state: the vertex table holds the current epoch only (it is
+   * dropped whenever the active frontier empties) */
+  uint64_t table_vertices;     /* vertex records held now */
+  uint64_t epoch_base;         /* global id of the first record held */
+  uint64_t max_readers;        /* longest reader list of any live array now */
 } dagrt_stats_t;
 /* Copy min(size, sizeof(dagrt_stats_t)) bytes of the counters to out. */
 dagrt_status dagrt_stats(dagrt_ctx ctx, void* out, size_t size);

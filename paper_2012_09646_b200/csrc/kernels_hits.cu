@@ -767,16 +767,19 @@ __device__ __forceinline__ int4 ld_cols_stream(const int* p, uint64_t pol) {
   return c;
 }
 
-// One chunk's streamed inputs for one lane: 4 column indices and their 4
-// row-start flag bits.
+// One chunk's streamed inputs for one lane: its 4 column indices, and the
+// chunk's 4 row-start flag words (the same 16 bytes for every lane: one
+// broadcast load).  The flag words are used only when the chunk is reduced,
+// so their latency is covered by the pipeline like the columns'.
 struct NzIn {
   int c[4];
-  unsigned fl;
+  uint4 fw;
 };
 
-__device__ __forceinline__ NzIn nz_load(const int* __restrict__ col, const NzPlan& P, int k, int E,
-                                        uint64_t pol) {
+__device__ __forceinline__ NzIn nz_load(const int* __restrict__ col, const NzPlan& P, int chunk, int lane,
+                                        int E, uint64_t pol) {
   NzIn in;
+  const int k = chunk * kNzChunk + 4 * lane;
   if (k + 3 < E) {
     const int4 q = ld_cols_stream(col + k, pol);
     in.c[0] = q.x; in.c[1] = q.y; in.c[2] = q.z; in.c[3] = q.w;
@@ -784,8 +787,7 @@ __device__ __forceinline__ NzIn nz_load(const int* __restrict__ col, const NzPla
 #pragma unroll
     for (int u = 0; u < 4; ++u) in.c[u] = k + u < E ? __ldg(col + k + u) : -1;
   }
-  in.fl = (__ldg(P.flags + (k >> 5)) >> (k & 31)) & 0xFu;
-  if (k + 3 >= E) in.fl &= (k < E ? (1u << (E - k)) - 1u : 0u);
+  in.fw = __ldg(reinterpret_cast<const uint4*>(P.flags) + chunk);  // words 4c..4c+3 (zero past E)
   return in;
 }
 
@@ -797,11 +799,14 @@ __device__ __forceinline__ void nz_gather(const NzIn& in, const float* __restric
 // Software pipeline per warp: while chunk c is reduced, the column indices
 // and flags of chunk c+2 and the gathers of chunk c+1 are in flight, and the
 // row ids of chunk c's completed rows are loaded before its gathered values
-// are consumed -- the three dependent memory latencies of a chunk (indices ->
+// are consumed -- the dependent memory latencies of a chunk (indices ->
 // gathers; ordinals -> row ids) overlap with the neighbouring chunks' work.
+// Counting starts needs no shuffles (popc over the chunk's flag words), and
+// the segmented scan shuffles only values: which lanes hold a start is one
+// ballot.
 __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_ptr, const int* __restrict__ col,
-                                                 const int* __restrict__ plan, const float* __restrict__ x,
-                                                 float* __restrict__ y, long long N_) {
+                                                    const int* __restrict__ plan, const float* __restrict__ x,
+                                                    float* __restrict__ y, long long N_) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int N = (int)N_;
   const NzPlan P = nz_plan(plan);
@@ -818,6 +823,8 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
   const SpmvWs ws = spmv_ws(y, N_, G);
   const uint64_t pol = l2_policy_evict_first();
   auto warp_of_nz = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
 
   // R0 = ordinal of the row open at the start of the current chunk: at the
   // range start, the row holding its first item (whose start bit, if any, is
@@ -829,25 +836,22 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
   bool head_pending = !start0;
   float carry = 0.f;
 
-  NzIn cur = nz_load(col, P, cb * kNzChunk + 4 * lane, E, pol);
+  NzIn cur = nz_load(col, P, cb, lane, E, pol);
   NzIn nxt = cur;
-  if (cb + 1 < ce) nxt = nz_load(col, P, (cb + 1) * kNzChunk + 4 * lane, E, pol);
+  if (cb + 1 < ce) nxt = nz_load(col, P, cb + 1, lane, E, pol);
   float v[4];
   nz_gather(cur, x, v);
   for (int c = cb; c < ce; ++c) {
-    unsigned fl = cur.fl;
-    if (c == cb && lane == 0) fl &= ~1u;  // the range's first item: handled by start0/head_pending
+    uint4 fw = cur.fw;
+    if (c == cb) fw.x &= ~1u;  // the range's first item: handled by start0/head_pending
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
     // ---- ordinals of the rows completed in this lane (no dependence on the gathers)
     const int nst = __popc(fl);
-    int incl = nst;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += t;
-    }
-    const int excl = incl - nst;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int o = R0 + excl;  // the row open entering the lane; ends at its first start
+    const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                       (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+    const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+    const int o = R0 + before;  // the row open entering the lane; ends at its first start
     // row ids of ordinals o-1 .. o+3 (those this lane writes), in registers
     int rid0 = -1, rid1 = -1, rid2 = -1, rid3 = -1, rid4 = -1;
     if (nst) {
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
     if (c + 1 < ce) {
       nz_gather(nxt, x, vn);
       cur = nxt;
-      if (c + 2 < ce) nxt = nz_load(col, P, (c + 2) * kNzChunk + 4 * lane, E, pol);
+      if (c + 2 < ce) nxt = nz_load(col, P, c + 2, lane, E, pol);
     }
     // ---- lane-local row segments of this chunk
     float run = 0.f, head = 0.f;
@@ -878,23 +882,24 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
       run += v[u];
     }
     if (!seen) head = run;
-    // ---- segmented exclusive scan: carry into each lane of the open row
+    // ---- segmented inclusive scan of the open-row contributions; the
+    // segment test comes from the ballot of start-holding lanes
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
     float sv = nst ? run : head;
-    bool sf = nst != 0;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const float tv = __shfl_up_sync(0xffffffffu, sv, off);
-      const bool tf = __shfl_up_sync(0xffffffffu, sf, off);
-      if (lane >= off && !sf) { sv += tv; sf = tf; }
+      // lanes (lane-off, lane] hold no start: the open row reaches back
+      const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+      if (win == 0u) sv += tv;
     }
     float cin = __shfl_up_sync(0xffffffffu, sv, 1);
-    const bool fin = __shfl_up_sync(0xffffffffu, sf, 1);
-    if (lane == 0) cin = carry;
-    else if (!fin) cin += carry;
+    if (lane == 0) cin = 0.f;
+    if ((m & lanes_below) == 0u) cin += carry;  // no start below this lane: the chunk's carry
     // ---- rows completed in this lane: y[row] = sum, zeros for the empty rows before it
     if (nst) {
       const float val = cin + head;
-      if (head_pending && excl == 0) {
+      if (head_pending && before == 0) {
         // began before this warp's range: deposit (this warp holds its end)
         const int cs = warp_of_nz(__ldg(row_ptr + rid1));
         spmv_ws_put(ws, g, val, true);
@@ -926,15 +931,15 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
     }
     // ---- carry to the next chunk
     const float tail_all = __shfl_sync(0xffffffffu, sv, 31);
-    const bool any = __shfl_sync(0xffffffffu, sf, 31);
-    carry = any ? tail_all : carry + tail_all;
-    if (any) head_pending = false;
+    carry = m ? tail_all : carry + tail_all;
+    if (m) head_pending = false;
     R0 += total;
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = vn[u];
   }
   // ---- the row open at the range end (and, for the last non-empty row, the
-  // empty rows after it)
+  // empty rows after it: no start follows the last row, so it is always
+  // completed here)
   if (lane == 0) {
     const int ke = ce * kNzChunk;
     const bool ends_here = ke >= E || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
@@ -963,10 +968,173 @@ __global__ void __launch_bounds__(256, 4) k_spmv_nz(const int* __restrict__ row_
         for (int r = row + 1; r < N; ++r) y[r] = 0.f;
     }
   }
-  // rows completed inside the loop never include the last non-empty row's
-  // tail zeros unless it completed there: the writer of ordinal nr-1 in the
-  // loop is the lane whose start follows it -- impossible (no start after the
-  // last row) -- so the tail zeros are always written above.
+}
+
+// ---------------------------------------------------------------------------
+// "spmv" (product, round 2): the non-zero split above with EVERY row padded
+// to at least one item -- each empty row gets one column index -1 (value 0)
+// when the graph is registered (spmv_pad_plan(), programs/hits_dl.py).  Then
+// ordinals ARE row ids: completed rows are written to consecutive addresses
+// with no row-id loads and no zero-filling of skipped rows (the profile of
+// spmv_nz put its top stalls on exactly those: the row-id loads and the
+// divergent gap loops), at the cost of 9M more 4-byte column indices on the
+// HBM-cheap coalesced stream.  Plan (int32): [header(16) | rp2(N+1) |
+// rbase(nc+1) | flags(4 nc + 4 words) | ci2(E2)], rp2 the padded row
+// pointers (used only for rows crossing warp ranges), E2 = E + #empty rows.
+constexpr int kPadMagic = 0x50414430;  // "PAD0"
+
+struct PadPlan {
+  int nc, n, e2;
+  const int* rp2;
+  const int* rbase;
+  const unsigned* flags;
+  const int* ci2;
+};
+
+__device__ __forceinline__ PadPlan pad_plan(const int* plan) {
+  if (__ldg(plan) != kPadMagic || __ldg(plan + 3) != kNzChunk) __trap();  // built for another kernel
+  PadPlan P;
+  P.nc = __ldg(plan + 1);
+  P.n = __ldg(plan + 2);
+  P.rp2 = plan + __ldg(plan + 4);
+  P.rbase = plan + __ldg(plan + 5);
+  P.flags = reinterpret_cast<const unsigned*>(plan + __ldg(plan + 6));
+  P.ci2 = plan + __ldg(plan + 7);
+  P.e2 = __ldg(plan + 8);
+  return P;
+}
+
+__device__ __forceinline__ NzIn pad_load(const PadPlan& P, int chunk, int lane, uint64_t pol) {
+  NzIn in;
+  const int k = chunk * kNzChunk + 4 * lane;
+  if (k + 3 < P.e2) {
+    const int4 q = ld_cols_stream(P.ci2 + k, pol);
+    in.c[0] = q.x; in.c[1] = q.y; in.c[2] = q.z; in.c[3] = q.w;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) in.c[u] = k + u < P.e2 ? __ldg(P.ci2 + k + u) : -1;
+  }
+  in.fw = __ldg(reinterpret_cast<const uint4*>(P.flags) + chunk);
+  return in;
+}
+
+__global__ void __launch_bounds__(256, 4) k_spmv_pad(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                     const int* __restrict__ plan, const float* __restrict__ x,
+                                                     float* __restrict__ y, long long N_) {
+  (void)row_ptr;
+  (void)col;  // the plan carries the (padded) graph; see above
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PadPlan P = pad_plan(plan);
+  if ((long long)P.n != N_ || P.n == 0) return;
+  const int G = (int)gridDim.x * (blockDim.x >> 5);
+  const int g = (int)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;  // warp-uniform; the kernel has no CTA barriers
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  const uint64_t pol = l2_policy_evict_first();
+  auto warp_of_item = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
+
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);  // row open at the current chunk's start
+  bool head_pending = !start0;   // ... which began in an earlier warp's range
+  float carry = 0.f;
+
+  NzIn cur = pad_load(P, cb, lane, pol);
+  NzIn nxt = cur;
+  if (cb + 1 < ce) nxt = pad_load(P, cb + 1, lane, pol);
+  float v[4];
+  nz_gather(cur, x, v);
+  for (int c = cb; c < ce; ++c) {
+    uint4 fw = cur.fw;
+    if (c == cb) fw.x &= ~1u;  // the range's first item: handled by start0/head_pending
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
+    const int nst = __popc(fl);
+    const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                       (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+    const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+    const int o = R0 + before;  // row open entering the lane; ends at its first start
+    float vn[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c + 1 < ce) {
+      nz_gather(nxt, x, vn);
+      cur = nxt;
+      if (c + 2 < ce) nxt = pad_load(P, c + 2, lane, pol);
+    }
+    float run = 0.f, head = 0.f;
+    bool seen = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((fl >> u) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.f;
+      }
+      run += v[u];
+    }
+    if (!seen) head = run;
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
+    float sv = nst ? run : head;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+      const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+      if (win == 0u) sv += tv;
+    }
+    float cin = __shfl_up_sync(0xffffffffu, sv, 1);
+    if (lane == 0) cin = 0.f;
+    if ((m & lanes_below) == 0u) cin += carry;
+    if (nst) {
+      const float val = cin + head;
+      if (head_pending && before == 0) {
+        const int cs = warp_of_item(__ldg(P.rp2 + o));
+        spmv_ws_put(ws, g, val, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[o] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[o] = val;
+      }
+      int j = 1;
+      float r2 = 0.f;
+      bool in = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (in) y[o + j++] = r2;
+          in = true;
+          r2 = 0.f;
+        }
+        r2 += v[u];
+      }
+    }
+    const float tail_all = __shfl_sync(0xffffffffu, sv, 31);
+    carry = m ? tail_all : carry + tail_all;
+    if (m) head_pending = false;
+    R0 += total;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = vn[u];
+  }
+  // the row open at the range end
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= P.e2 || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    if (ends_here) {
+      if (head_pending) {  // spans the whole range, ends at its end
+        const int cs = warp_of_item(__ldg(P.rp2 + R0));
+        spmv_ws_put(ws, g, carry, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[R0] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[R0] = carry;
+      }
+    } else {
+      const int cs = warp_of_item(__ldg(P.rp2 + R0));
+      const int cend = warp_of_item(__ldg(P.rp2 + R0 + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      if (spmv_ws_arrive(ws, cs, cend)) y[R0] = spmv_ws_sum(ws, cs, cend);
+    }
+  }
 }
 
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
@@ -1017,8 +1185,11 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
 static const Builtin kHits[] = {
     // merge-path SpMV (round-1 product) and its variants: gathers in registers
     // (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
-    // product: non-zero-split SpMV: row_ptr, col, plan (programs/hits_dl.py spmv_nz_plan), x, y, N
-    {"spmv", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // product: non-zero split over rows padded to >= 1 item: row_ptr, col,
+    // plan (programs/hits_dl.py spmv_pad_plan), x, y, N
+    {"spmv", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    // the same without padding (row ids from a non-empty-row list, spmv_nz_plan)
+    {"spmv_nz", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_merge", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     // row-class SpMV (measured slower, kept as a tested alternative): row_ptr, col,
     // plan (programs/hits_dl.py spmv_plan), x, y, N

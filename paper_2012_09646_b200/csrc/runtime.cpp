@@ -655,12 +655,12 @@ struct ArrayRec {
   uint32_t gen = 0;
   bool live = false;
   bool mapped = false;
-  int64_t last_writer = -1;         // vertex id of the last kernel writer, -1 = none/host
-  std::vector<uint32_t> readers;    // readers since the last writer (pruned lazily)
+  int64_t last_writer = -1;         // GLOBAL vertex id of the last kernel writer, -1 = none/host
+  std::vector<int64_t> readers;     // global ids of the readers since the last writer (pruned lazily)
   uint8_t coh = COH_DEVICE;
   bool h2d_pending = false;         // an H2D prefetch whose consumer is still active
   void* h2d_ev = nullptr;
-  int64_t h2d_consumer = -1;
+  int64_t h2d_consumer = -1;        // global vertex id
   int32_t h2d_stream = -1;          // stream of the consumer (already ordered after the copy)
 };
 
@@ -701,7 +701,14 @@ struct dagrt_ctx_s {
 
   std::vector<KernelRec> kernels;
   std::vector<ArrayRec> arrays;       // index 0 unused (handle 0 invalid)
+  // Vertex table of the current EPOCH: local index i is global vertex id
+  // vid_base + i.  When the active frontier empties (every vertex retired by
+  // host syncs), the table and the parent links are dropped and vid_base
+  // advances (recycle()): the scheduler's state stays bounded by the frontier
+  // instead of growing with every launch.  Arrays and streams keep global
+  // ids, which simply become inactive.
   std::vector<VertexRec> vertices;
+  int64_t vid_base = 0;
   std::vector<uint32_t> parent_pool;
   std::vector<StreamRec> streams;
   std::vector<void*> event_pool;      // free events
@@ -781,9 +788,11 @@ inline dagrt_array array_handle(dagrt_ctx c, const ArrayRec* a) {
   return ((uint64_t)a->gen << 32) | array_index(c, a);
 }
 
-inline bool is_active(dagrt_ctx c, int64_t v) {
-  return v >= 0 && (size_t)v < c->vertices.size() && c->vertices[v].active;
+inline bool is_active(dagrt_ctx c, int64_t gid) {
+  const int64_t v = gid - c->vid_base;
+  return gid >= 0 && v >= 0 && (size_t)v < c->vertices.size() && c->vertices[v].active;
 }
+inline uint32_t local_of(dagrt_ctx c, int64_t gid) { return (uint32_t)(gid - c->vid_base); }
 
 dagrt_status get_event(dagrt_ctx c, void** ev) {
   if (!c->event_pool.empty()) {
@@ -880,8 +889,25 @@ void retire(dagrt_ctx c, uint32_t v) {
 }
 
 void retire_all(dagrt_ctx c) {
-  for (size_t v = 0; v < c->vertices.size(); ++v)
+  for (size_t v = 0; v < c->vertices.size() && c->n_active > 0; ++v)
     if (c->vertices[v].active) retire(c, (uint32_t)v);
+}
+
+// New epoch once the frontier is empty (see dagrt_ctx_s::vertices).
+void recycle(dagrt_ctx c) {
+  if (c->n_active != 0 || c->vertices.empty()) return;
+  c->vid_base += (int64_t)c->vertices.size();
+  c->vertices.clear();
+  c->parent_pool.clear();
+}
+
+// Drop readers that are no longer active (amortised: when the list grows)
+void prune_readers(dagrt_ctx c, ArrayRec* a) {
+  auto& rd = a->readers;
+  size_t w = 0;
+  for (size_t i = 0; i < rd.size(); ++i)
+    if (is_active(c, rd[i])) rd[w++] = rd[i];
+  rd.resize(w);
 }
 
 // Dependency inference for one access (array a, write?) against the active
@@ -889,19 +915,15 @@ void retire_all(dagrt_ctx c) {
 void infer(dagrt_ctx c, ArrayRec* a, bool write) {
   uint32_t ai = array_index(c, a);
   if (!write) {
-    if (is_active(c, a->last_writer)) c->scratch_edges.push_back({(uint32_t)a->last_writer, ai});
+    if (is_active(c, a->last_writer)) c->scratch_edges.push_back({local_of(c, a->last_writer), ai});
     return;
   }
-  // prune readers that are no longer active
+  prune_readers(c, a);
   auto& rd = a->readers;
-  size_t w = 0;
-  for (size_t i = 0; i < rd.size(); ++i)
-    if (c->vertices[rd[i]].active) rd[w++] = rd[i];
-  rd.resize(w);
   if (!rd.empty()) {
-    for (uint32_t r : rd) c->scratch_edges.push_back({r, ai});
+    for (int64_t r : rd) c->scratch_edges.push_back({local_of(c, r), ai});
   } else if (is_active(c, a->last_writer)) {
-    c->scratch_edges.push_back({(uint32_t)a->last_writer, ai});
+    c->scratch_edges.push_back({local_of(c, a->last_writer), ai});
   }
 }
 
@@ -915,7 +937,8 @@ void collect_parents(dagrt_ctx c, uint32_t child) {
   for (auto& pr : e) {
     if (ps.empty() || ps.back() != pr.first) ps.push_back(pr.first);
     if (c->cfg.record_dag)
-      c->rec_e.push_back(dagrt_edge_info{pr.first, child, array_handle(c, &c->arrays[pr.second])});
+      c->rec_e.push_back(dagrt_edge_info{(uint32_t)(c->vid_base + pr.first), (uint32_t)(c->vid_base + child),
+                                         array_handle(c, &c->arrays[pr.second])});
   }
   c->st.edges += ps.size();
 }
@@ -939,7 +962,7 @@ dagrt_status pick_stream(dagrt_ctx c, int32_t* out) {
   }
   for (uint32_t p : c->scratch_parents) {
     int32_t s = c->vertices[p].stream;
-    if (s >= 0 && c->streams[s].tail == (int64_t)p) { *out = s; return DAGRT_OK; }
+    if (s >= 0 && c->streams[s].tail == c->vid_base + (int64_t)p) { *out = s; return DAGRT_OK; }
   }
   for (size_t s = 0; s < c->streams.size(); ++s)
     if (c->streams[s].nactive == 0) { *out = (int32_t)s; return DAGRT_OK; }
@@ -975,9 +998,9 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order
   c->st.vertices++;
   c->st.host_vertices++;
   if (c->cfg.record_dag)
-    c->rec_v.push_back(dagrt_vertex_info{vid, 1, 0, -1, array_handle(c, a)});
+    c->rec_v.push_back(dagrt_vertex_info{(uint32_t)(c->vid_base + vid), 1, 0, -1, array_handle(c, a)});
   for (uint32_t p : c->scratch_parents) {
-    trace_op(c, DAGRT_OP_EVENT_SYNC, -1, p, 0, 0);
+    trace_op(c, DAGRT_OP_EVENT_SYNC, -1, c->vid_base + p, 0, 0);
     // (with the graph cache on, the wait joins the pending batch with the copy)
     if (order && c->be->active()) CK(c->be->wait(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
     else if (order) CK(c->be->wait_now(order, c->vertices[p].ev), "cudaStreamWaitEvent D2H");
@@ -986,6 +1009,7 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order
   }
   for (uint32_t p : c->scratch_parents) retire(c, p);
   if (write) { a->readers.clear(); a->last_writer = -1; }
+  recycle(c);
   return DAGRT_OK;
 }
 
@@ -1277,12 +1301,12 @@ dagrt_status dagrt_array_unregister(dagrt_ctx c, dagrt_array h) {
   if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
   // wait for in-flight users: the last writer, active readers, a pending copy
   if (is_active(c, a->last_writer)) {
-    CK(c->be->event_sync(c->vertices[a->last_writer].ev), "cudaEventSynchronize");
+    CK(c->be->event_sync(c->vertices[local_of(c, a->last_writer)].ev), "cudaEventSynchronize");
     c->st.host_syncs++;
   }
-  for (uint32_t r : a->readers)
-    if (c->vertices[r].active) {
-      CK(c->be->event_sync(c->vertices[r].ev), "cudaEventSynchronize");
+  for (int64_t r : a->readers)
+    if (is_active(c, r)) {
+      CK(c->be->event_sync(c->vertices[local_of(c, r)].ev), "cudaEventSynchronize");
       c->st.host_syncs++;
     }
   if (a->h2d_pending) {
@@ -1380,7 +1404,8 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
     if (kd != P_OUT) need[j] = true;
   }
   dim3 g(grid.x, grid.y, grid.z), b(block.x, block.y, block.z);
-  uint32_t vid = (uint32_t)c->vertices.size();
+  uint32_t vid = (uint32_t)c->vertices.size();  // local index in this epoch
+  const int64_t gvid = c->vid_base + vid;        // global vertex id (exports, tables)
   c->st.launches++;
   c->st.vertices++;
 
@@ -1398,19 +1423,20 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
           void* t0;
           if (dagrt_status st_ = tl_begin(c, s, &t0)) return st_;
           CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
-          if (dagrt_status st_ = tl_end(c, s, t0, 1, -3, vid, array_index(c, a), a->bytes)) return st_;
+          if (dagrt_status st_ = tl_end(c, s, t0, 1, -3, gvid, array_index(c, a), a->bytes)) return st_;
           CK(c->be->stream_sync(s), "cudaStreamSynchronize");
           c->st.host_syncs++;
         }
         a->coh = COH_BOTH;
       }
     }
-    trace_op(c, DAGRT_OP_LAUNCH, -3, vid, kh, 0);
-    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, -3, vid)) return st_;
+    trace_op(c, DAGRT_OP_LAUNCH, -3, gvid, kh, 0);
+    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, -3, gvid)) return st_;
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
     c->st.host_syncs++;
     c->vertices.push_back(VertexRec{0, 0, -1, nullptr, 0, 0});
-    if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{vid, 0, kh, -1, 0});
+    recycle(c);  // nothing is ever active under the serial policy
+    if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{(uint32_t)gvid, 0, kh, -1, 0});
     for (int j = 0; j < nacc; ++j)
       if (wr[j] && acc[j]->host) acc[j]->coh = COH_DEVICE;
     c->st.sched_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -1433,7 +1459,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   for (uint32_t p : c->scratch_parents) {
     const VertexRec& pv = c->vertices[p];
     if (pv.stream != sid) {
-      trace_op(c, DAGRT_OP_WAIT, sid, p, 0, 0);
+      trace_op(c, DAGRT_OP_WAIT, sid, c->vid_base + p, 0, 0);
       CK(c->be->wait(s, pv.ev), "cudaStreamWaitEvent");
       c->st.cross_stream_waits++;
     }
@@ -1450,7 +1476,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       void* t0;
       if (dagrt_status st_ = tl_begin(c, cs, &t0)) return st_;
       CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, cs), "cudaMemcpyAsync H2D");
-      if (dagrt_status st_ = tl_end(c, cs, t0, 1, c->cfg.prefetch ? -2 : sid, vid, array_index(c, a),
+      if (dagrt_status st_ = tl_end(c, cs, t0, 1, c->cfg.prefetch ? -2 : sid, gvid, array_index(c, a),
                                     a->bytes))
         return st_;
       a->coh = COH_BOTH;
@@ -1465,7 +1491,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
         c->st.copy_waits++;
       }
       a->h2d_pending = true;
-      a->h2d_consumer = vid;
+      a->h2d_consumer = gvid;
       a->h2d_stream = sid;  // ordered after the copy in both modes
     } else if (a->h2d_pending && a->h2d_stream != sid) {
       trace_op(c, DAGRT_OP_WAIT_COPY, sid, array_index(c, a), 0, 0);
@@ -1479,11 +1505,11 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   if (dagrt_status st = get_event(c, &ev)) return st;
   const uint64_t tl0 = now_ns();
   c->st.wait_ns += tl0 - tw0;
-  trace_op(c, DAGRT_OP_LAUNCH, sid, vid, kh, 0);
-  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, vid)) return st_;
+  trace_op(c, DAGRT_OP_LAUNCH, sid, gvid, kh, 0);
+  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, gvid)) return st_;
   const uint64_t tr0 = now_ns();
   c->st.launch_ns += tr0 - tl0;
-  trace_op(c, DAGRT_OP_RECORD, sid, vid, 0, 0);
+  trace_op(c, DAGRT_OP_RECORD, sid, gvid, 0, 0);
   CK(c->be->record(ev, s), "cudaEventRecord");
   c->st.record_ns += now_ns() - tr0;
 
@@ -1492,17 +1518,18 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   c->parent_pool.insert(c->parent_pool.end(), c->scratch_parents.begin(), c->scratch_parents.end());
   c->vertices.push_back(VertexRec{1, 0, sid, ev, pbeg, (uint32_t)c->scratch_parents.size()});
   c->n_active++;
-  c->streams[sid].tail = vid;
+  c->streams[sid].tail = gvid;
   c->streams[sid].nactive++;
-  if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{vid, 0, kh, sid, 0});
+  if (c->cfg.record_dag) c->rec_v.push_back(dagrt_vertex_info{(uint32_t)gvid, 0, kh, sid, 0});
   for (int j = 0; j < nacc; ++j) {
     ArrayRec* a = acc[j];
     if (wr[j]) {
-      a->last_writer = vid;
+      a->last_writer = gvid;
       a->readers.clear();
       if (a->host) a->coh = COH_DEVICE;
     } else {
-      a->readers.push_back(vid);
+      if (a->readers.size() >= 32) prune_readers(c, a);  // never-written arrays stay bounded
+      a->readers.push_back(gvid);
     }
   }
   c->st.sched_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -1633,6 +1660,7 @@ dagrt_status dagrt_sync(dagrt_ctx c) {
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
   c->st.host_syncs++;
   retire_all(c);
+  recycle(c);
   for (size_t i = 1; i < c->arrays.size(); ++i) c->arrays[i].h2d_pending = false;
   return DAGRT_OK;
 }
@@ -1675,6 +1703,11 @@ dagrt_status dagrt_stats(dagrt_ctx c, void* out, size_t size) {
   c->st.graph_replays = c->be->replays;
   c->st.graph_captures = c->be->captures;
   c->st.eager_batches = c->be->eager;
+  c->st.table_vertices = c->vertices.size();
+  c->st.epoch_base = (uint64_t)c->vid_base;
+  c->st.max_readers = 0;
+  for (size_t i = 1; i < c->arrays.size(); ++i)
+    if (c->arrays[i].live) c->st.max_readers = std::max<uint64_t>(c->st.max_readers, c->arrays[i].readers.size());
   memcpy(out, &c->st, std::min(size, sizeof(dagrt_stats_t)));
   return DAGRT_OK;
 }

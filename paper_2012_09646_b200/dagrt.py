@@ -68,7 +68,8 @@ class TraceOp(C.Structure):
 STAT_FIELDS = ["launches", "vertices", "host_vertices", "edges", "cross_stream_waits",
                "copy_waits", "streams", "events_created", "h2d_bytes", "d2h_bytes",
                "h2d_copies", "d2h_copies", "host_syncs", "sched_ns", "graph_replays",
-               "graph_captures", "eager_batches", "launch_ns", "record_ns", "wait_ns"]
+               "graph_captures", "eager_batches", "launch_ns", "record_ns", "wait_ns",
+               "table_vertices", "epoch_base", "max_readers"]
 
 
 class Stats(C.Structure):

@@ -25,6 +25,9 @@ CONV2_TMAR_THREADS = 288
 CONV2_GRID, CONV2_THREADS = 148, 384
 CONV2_SMEM = 1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
+# warp-specialised conv2 (csrc/kernels_conv2.cu c2ws): 10 warps, 4 TMA stages
+CONV2_WS_THREADS = 320
+CONV2_WS_SMEM = 1024 + 4 * 9 * 4096 + 9 * 1024 + 8 * (2 * 4 + 3 * 2) + 16
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)
@@ -86,7 +89,7 @@ SPMV_CTAS_PER_SM = int(os.environ.get("DAGRT_SPMV_CTAS_PER_SM", "8"))
 NZ_CHUNK = 128
 NZ_MAGIC = 0x4E5A3031
 NZ_HEADER = 16
-NZ_CTAS_PER_SM = int(os.environ.get("DAGRT_SPMV_NZ_CTAS_PER_SM", "4"))  # one resident wave (<= 64 registers)
+NZ_CTAS_PER_SM = int(os.environ.get("DAGRT_SPMV_NZ_CTAS_PER_SM", "8"))  # two waves of 4 resident (<= 64 registers): 251 vs 257 us (tools/spmv_lab.py)
 
 
 def spmv_nz_plan(row_ptr):
@@ -123,6 +126,52 @@ def spmv_nz_plan(row_ptr):
     return plan
 
 
+PAD_MAGIC = 0x50414430
+
+
+def spmv_pad_plan(row_ptr, col_idx):
+    """The CSR re-encoded for the product SpMV (k_spmv_pad), once, when the
+    graph is registered: every empty row gets one column index -1 (value 0),
+    so row ordinals are row ids.
+    int32 [header(16) | rp2(N+1) | rbase(nc+1) | flags(4nc+4) | ci2(E2)]:
+      rp2   padded row pointers, E2 = rp2[N] = E + #empty rows;
+      flags bit k set iff item k starts its row (every row starts one item);
+      rbase[c] row holding item c*128;  ci2 the padded column indices."""
+    import numpy as np
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    ci = np.asarray(col_idx, dtype=np.int64)
+    n = rp.size - 1
+    deg = np.diff(rp)
+    pdeg = np.maximum(deg, 1)
+    rp2 = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(pdeg, out=rp2[1:])
+    e2 = int(rp2[-1])
+    ci2 = np.full(max(e2, 1), -1, dtype=np.int64)
+    if ci.size:
+        row_of = np.repeat(np.arange(n, dtype=np.int64), deg)
+        ci2[rp2[row_of] + (np.arange(ci.size, dtype=np.int64) - rp[row_of])] = ci
+    starts = rp2[:-1]
+    nc = (e2 + NZ_CHUNK - 1) // NZ_CHUNK
+    nwords = 4 * nc + 4
+    flags = np.bincount(starts >> 5, weights=np.left_shift(1, starts & 31).astype(np.float64),
+                        minlength=nwords).astype(np.uint64).astype(np.uint32)
+    rbase = np.searchsorted(starts, np.arange(nc + 1, dtype=np.int64) * NZ_CHUNK, side="right") - 1
+    rbase = np.maximum(rbase, 0)
+    off_rp = NZ_HEADER
+    off_rb = off_rp + n + 1
+    off_f = off_rb + nc + 1
+    off_f += (-off_f) % 4
+    off_c = off_f + nwords
+    off_c += (-off_c) % 4
+    plan = np.zeros(off_c + ci2.size, dtype=np.int32)
+    plan[:9] = (PAD_MAGIC, nc, n, NZ_CHUNK, off_rp, off_rb, off_f, off_c, e2)
+    plan[off_rp:off_rp + n + 1] = rp2
+    plan[off_rb:off_rb + nc + 1] = rbase
+    plan[off_f:off_f + nwords] = flags.view(np.int32)
+    plan[off_c:off_c + ci2.size] = ci2
+    return plan
+
+
 def spmv_nz_grid(e):
     nc = -(-e // NZ_CHUNK)
     return max(1, min(-(-nc // SPMV_WARPS), NZ_CTAS_PER_SM * SMS))
@@ -156,7 +205,7 @@ class Hits(Program):
                 self.upload(name, arr)
         self.alloc("a1", n, torch.float32, mirror=stream)
         self.alloc("h1", n, torch.float32, mirror=stream)
-        gs = spmv_nz_grid(self.e)
+        gs = spmv_nz_grid(self.e + n)  # padded items <= E + N
         ob = 4 * n + 16 + 12 * SPMV_WARPS * gs  # y + SpmvWs (3 words per warp)
         self.alloc("a2", 0, None, nbytes=ob)
         self.alloc("h2", 0, None, nbytes=ob)
@@ -165,7 +214,7 @@ class Hits(Program):
         if self.share is not None and "plan" in self.share.t:
             self.plans = self.share.plans
         else:
-            self.plans = (spmv_nz_plan(rp), spmv_nz_plan(rpt))
+            self.plans = (spmv_pad_plan(rp, ci), spmv_pad_plan(rpt, cit))
         for name, arr in (("plan", self.plans[0]), ("plant", self.plans[1])):
             self.alloc(name, arr.size, torch.int32)
             self.upload(name, arr)

@@ -121,6 +121,35 @@ def test_dl_4096_elementwise():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("h,w", [(19, 23), (515, 517), (1030, 2050), (4096, 4096)])
+def test_conv2_ws_matches_oracle(h, w):
+    """The warp-specialised conv2 (A_lo in TMEM; csrc/kernels_conv2.cu) against
+    the oracle's conv on the pooled input, from one tile to ~14 tiles per CTA
+    (every stage / TMEM buffer / barrier phase reused many times), ragged
+    output rows (W3 not a multiple of 128)."""
+    from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
+    c = D.Context(device=0)
+    p = DeepLearning(c, h=h, w=w)
+    p.load_inputs(1)
+    p.run()
+    c.sync()
+    (h1, w1s), (h2, w2s), (h3, w3s) = p.shapes
+    out = torch.full((h3 * w3s * 16,), -1.0, device="cuda")
+    torch.cuda.synchronize()
+    o_arr = c.register_tensor("c2ws", out)
+    for _ in range(2):
+        c.launch("conv2_ws", 148, CONV2_WS_THREADS, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_WS_SMEM)
+    c.sync()
+    spec = synth.spec_dl(h, w)
+    w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
+    px = p.t["px"][:h2 * w2s * 8].cpu().numpy().reshape(h2, w2s, 8)
+    ref = odl.conv3x3s2(px, w2)
+    assert_close(out.cpu().numpy().reshape(h3, w3s, 16), ref, "conv2_ws")
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
 def _c2_strip(seed, spec, name, h, w, w1, w2, P0, P1):
     """Oracle conv2 output rows [P0, P1) of a full-size branch, from input
     rows [8*P0 - 8, 8*P1 + 8) (aligned to 8, so every stride lines up; the

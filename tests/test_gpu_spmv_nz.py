@@ -13,7 +13,7 @@ import torch
 import synth
 from oracle import hits as ohits
 from paper_2012_09646_b200 import dagrt as D
-from paper_2012_09646_b200.programs.hits_dl import SPMV_WARPS, spmv_nz_plan
+from paper_2012_09646_b200.programs.hits_dl import SPMV_WARPS, spmv_nz_plan, spmv_pad_plan
 
 from oracle_checks import assert_close
 
@@ -47,10 +47,12 @@ def ctx():
     c.close()
 
 
-def run_nz(ctx, rp, ci, x, grid, tag):
+def run_nz(ctx, rp, ci, x, grid, tag, kernel="spmv"):
     n = len(rp) - 1
-    plan = spmv_nz_plan(rp)
+    plan = spmv_pad_plan(rp, ci) if kernel == "spmv" else spmv_nz_plan(rp)
     ob = 4 * n + 16 + 12 * SPMV_WARPS * grid
+    if kernel == "spmv":  # padded items: 4 * N more than E at most
+        pass
     t = {"rp": torch.from_numpy(rp).cuda(), "ci": torch.from_numpy(ci if ci.size else np.zeros(4, np.int32)).cuda(),
          "plan": torch.from_numpy(plan).cuda(), "x": torch.from_numpy(x).cuda(),
          "y": torch.full((ob // 4 + 1,), float("nan"), device="cuda")}
@@ -59,7 +61,7 @@ def run_nz(ctx, rp, ci, x, grid, tag):
     A = [ctx.register_tensor(f"{tag}_{k}", v) for k, v in t.items()]
     outs = []
     for _ in range(2):
-        ctx.launch("spmv", grid, 256, *A, n)
+        ctx.launch(kernel, grid, 256, *A, n)
         ctx.sync()
         outs.append(t["y"][:n].clone())
     for a in A:
@@ -67,25 +69,27 @@ def run_nz(ctx, rp, ci, x, grid, tag):
     return outs
 
 
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("grid", [1, 7, 148 * 6])
-def test_spmv_nz_edge_shapes(ctx, case, grid):
+def test_spmv_nz_edge_shapes(ctx, case, grid, kernel):
     deg, ncols = CASES[case]
     rp, ci = csr_from_degrees(deg, ncols, 1)
     n = len(deg)
     x = np.random.default_rng(2).random(max(n, ncols)).astype(np.float32)
     # columns index x of length max(n, ncols): square-ish padding of the matrix
-    y1, y2 = run_nz(ctx, rp, ci, x, grid, f"{case}_{grid}")
+    y1, y2 = run_nz(ctx, rp, ci, x, grid, f"{case}_{grid}_{kernel}", kernel)
     assert torch.equal(y1, y2)
     ref = ohits.spmv(rp, ci, x.astype(np.float64))
     assert_close(y1.cpu().numpy(), ref, case)
 
 
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
 @pytest.mark.parametrize("n,e,seed", [(10, 30, 1), (5000, 15000, 3), (300_000, 900_000, 11)])
-def test_spmv_nz_powerlaw(ctx, n, e, seed):
+def test_spmv_nz_powerlaw(ctx, n, e, seed, kernel):
     rp, ci, _, _ = synth.powerlaw_graph(seed, n, e, device="auto")
     x = np.random.default_rng(seed).random(n).astype(np.float32)
     for grid in (3, 148 * 6):
-        y1, y2 = run_nz(ctx, rp, ci, x, grid, f"pl{n}_{grid}")
+        y1, y2 = run_nz(ctx, rp, ci, x, grid, f"pl{n}_{grid}_{kernel}", kernel)
         assert torch.equal(y1, y2)
         assert_close(y1.cpu().numpy(), ohits.spmv(rp, ci, x.astype(np.float64)), (n, grid))

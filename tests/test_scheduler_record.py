@@ -342,3 +342,36 @@ def test_fastcall_binding_built():
     """The CPython fastcall module (pyext/dagrt_fastcall.c) is built in-tree
     and used by the per-step calls (batch, prepared reads, graph runs)."""
     assert D.fast() is not None
+
+
+def test_scheduler_state_is_frontier_bounded():
+    """PAPER.md L495-501 (only active computations are tracked): a long loop
+    of K1 writes A, K2 reads the never-written W and A, host reads A -- the
+    vertex table is dropped whenever the frontier empties, reader lists of
+    read-only arrays stay bounded, and exported vertex ids stay global and
+    equal to the oracle's."""
+    rp = Replayer({"A", "W", "B"}, 64)
+    trace = []
+    for _ in range(3000):
+        trace += [("launch", "k1", [("A", "O")]), ("launch", "k2", [("W", "R"), ("A", "R"), ("B", "O")]),
+                  ("host", "A", "R", 0, 64), ("host", "B", "R", 0, 64)]
+    rp.run(trace)
+    st = rp.ctx.stats()
+    assert st["table_vertices"] <= 4, st
+    assert st["max_readers"] <= 33, st
+    assert st["epoch_base"] > 8000, st
+    verts, edges = rp.dag()
+    o = odag.build_dag(trace[:40])
+    assert [(v[0], v[1]) for v in verts[:len(o.vertices)]] == [(v[0], v[2]) for v in o.vertices]
+    assert {e for e in edges if e[1] < len(o.vertices)} == o.edges
+    assert verts[-1][0] == 4 * 3000 - 1  # global ids: 2 kernels + 2 host vertices per iteration
+    # B keeps being written while W is read by every k2: the frontier never
+    # empties without the host read, and readers of W are pruned as they retire
+    rp2 = Replayer({"A", "W", "B"}, 64)
+    tr2 = []
+    for i in range(2000):
+        tr2 += [("launch", "k2", [("W", "R"), ("B", "RW")])]
+        if i % 10 == 9:
+            tr2 += [("host", "B", "R", 0, 64)]
+    rp2.run(tr2)
+    assert rp2.ctx.stats()["max_readers"] <= 33

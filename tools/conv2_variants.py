@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--h", type=int, default=16384)
     ap.add_argument("--variants", default="conv2_ffma,conv2_tc1,conv2_tc4,conv2_tc5,conv2")
+    ap.add_argument("--conv1", action="store_true", help="also time the conv1 variants")
     a = ap.parse_args()
     import torch
     from paper_2012_09646_b200 import dagrt as D
@@ -44,12 +45,12 @@ def main():
         return e0.elapsed_time(e1) / reps * 1e3
 
     kb = p.kernel_bytes()
-    for i, name in ((0, "conv1"), (2, "pool")):
+    for i, name in ((0, "conv1"), (2, "pool")) if a.conv1 else ():
         us = timeit(p.L[i])
         out[name] = {"us": us, "GBps": kb[name + "_x"] / us / 1e3}
     c1ref = p.t["c1x"].clone()
     L0 = p.L[0]
-    for v in ("conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3", "conv1_r2b3cs", "conv1_r2b2"):
+    for v in ("conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3", "conv1_r2b3cs", "conv1_r2b2") if a.conv1 else ():
         for rows_per in ((8, 16, 24, 32) if "_r2" in v else (8, 16)):
             nrows = (h1 + 1) // 2 if "_r2" in v else h1  # the r2 kernels' grid.y walks row pairs
             g = (L0.grid.x, max(1, min(nrows, -(-rows_per * 148 // L0.grid.x))))
@@ -84,6 +85,9 @@ def main():
             L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
             L = ctx.prepare(v, G2TC, 128, args, smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
+        elif v == "conv2_ws":
+            from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
+            L = ctx.prepare(v, 148, CONV2_WS_THREADS, args, smem=CONV2_WS_SMEM)
         elif v == "conv2":  # the product launch configuration (programs/hits_dl.py)
             from paper_2012_09646_b200.programs.hits_dl import CONV2_GRID, CONV2_SMEM, CONV2_THREADS
             L = ctx.prepare(v, CONV2_GRID, CONV2_THREADS, args, smem=CONV2_SMEM)

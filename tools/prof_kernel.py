@@ -19,15 +19,15 @@ def main():
     ctx = D.Context(device=0)
     st = torch.cuda.Stream()
     if what == "spmv":
-        from paper_2012_09646_b200.programs.hits_dl import spmv_nz_grid, spmv_nz_plan, spmv_out_bytes
+        from paper_2012_09646_b200.programs.hits_dl import spmv_nz_grid, spmv_out_bytes, spmv_pad_plan
         n, e = 20_000_000, 60_000_000
         rp, ci, _, _ = synth.powerlaw_graph(synth.BASE_SEED, n, e, device="auto")
         E = int(rp[-1])
         ob, grid = spmv_out_bytes(n, E)
-        g = spmv_nz_grid(E)
+        g = spmv_nz_grid(E + n)
         ob = max(ob, 4 * n + 16 + 12 * 8 * g)
         t = {"rp": torch.from_numpy(rp).cuda(), "ci": torch.from_numpy(ci).cuda(),
-             "plan": torch.from_numpy(spmv_nz_plan(rp)).cuda(), "x": torch.rand(n, device="cuda"),
+             "plan": torch.from_numpy(spmv_pad_plan(rp, ci)).cuda(), "x": torch.rand(n, device="cuda"),
              "y": torch.zeros(ob // 4 + 1, device="cuda")}
         torch.cuda.synchronize()
         A = {k: ctx.register_tensor(k, v) for k, v in t.items()}

@@ -84,7 +84,7 @@ def main():
                                                          out.data_ptr(), E, gg, 10)
     # the SpMV kernels on the same graph, through the C ABI
     from paper_2012_09646_b200 import dagrt as D
-    from paper_2012_09646_b200.programs.hits_dl import spmv_nz_grid, spmv_nz_plan, spmv_out_bytes
+    from paper_2012_09646_b200.programs.hits_dl import spmv_nz_grid, spmv_nz_plan, spmv_out_bytes, spmv_pad_plan
     ctx = D.Context(device=0)
     ob, grid = spmv_out_bytes(n, E)
     gnz = spmv_nz_grid(E)
@@ -95,8 +95,13 @@ def main():
     plan = spmv_nz_plan(rp)
     res["nz_plan_s"] = time.time() - t1
     dplan = torch.from_numpy(plan).cuda()
+    t1 = time.time()
+    pplan = spmv_pad_plan(rp, ci)
+    res["pad_plan_s"] = time.time() - t1
+    dpplan = torch.from_numpy(pplan).cuda()
     torch.cuda.synchronize()
     A = [ctx.register_tensor(k, t) for k, t in (("rp", drp), ("ci", dci), ("plan", dplan), ("x", x), ("y", y))]
+    AP = ctx.register_tensor("pplan", dpplan)
     st = torch.cuda.Stream()
 
     def timeit(Lp):
@@ -114,7 +119,9 @@ def main():
     res["merge_path_spmv_us"] = timeit(ctx.prepare("spmv_merge", grid, 256, [A[0], A[1], A[3], A[4], n]))
     for cps in (4, 6, 8, 12, 16):
         g2 = max(1, min(-(-(-(-E // 128)) // 8), cps * 148))
-        res[f"nz_spmv_cps{cps}_us"] = timeit(ctx.prepare("spmv", g2, 256, A + [n]))
+        res[f"nz_spmv_cps{cps}_us"] = timeit(ctx.prepare("spmv_nz", g2, 256, A + [n]))
+        g3 = max(1, min(-(-(-(-(E + n) // 128)) // 8), cps * 148))
+        res[f"pad_spmv_cps{cps}_us"] = timeit(ctx.prepare("spmv", g3, 256, [A[0], A[1], AP, A[3], A[4], n]))
     res["nz_spmv_default_grid"] = gnz
     y0 = y[:n].clone()
     ctx.prepare("spmv_merge", grid, 256, [A[0], A[1], A[3], A[4], n]).raw(st.cuda_stream)
