@@ -181,6 +181,23 @@ dagrt_status dagrt_launch_prepared(dagrt_ctx ctx, const dagrt_launch_desc* d);
  * B200 box host). */
 dagrt_status dagrt_launch_batch(dagrt_ctx ctx, const dagrt_launch_desc* descs, int32_t n);
 
+/* A LIBRARY CALL as a DAG vertex (L516-519: besides kernels, "library
+ * functions" executed on the GPU are computational elements whose argument
+ * modes the scheduler uses).  The vertex is scheduled exactly like a kernel
+ * (dependencies from `arrays` with modes[i] in DAGRT_R / DAGRT_W (overwritten
+ * whole: not prefetched) / DAGRT_RW, stream choice, event wiring, prefetch);
+ * instead of a kernel launch the scheduler calls fn(stream, user) on the host
+ * with the CUDA stream (cudaStream_t) it picked.  fn must enqueue all its GPU
+ * work for these arrays on that stream, must not synchronise, and returns 0
+ * (nonzero: DAGRT_EINVAL, the vertex is not recorded).  `name` labels the
+ * vertex in dagrt_dag_export (a pseudo-kernel per distinct name).  Ownership:
+ * fn and user stay the caller's; fn is called during this call only.  With
+ * the graph cache on, pending deferred work is flushed first (a host callback
+ * cannot be captured). */
+typedef int32_t (*dagrt_library_fn)(void* stream, void* user);
+dagrt_status dagrt_launch_library(dagrt_ctx ctx, dagrt_library_fn fn, void* user, const char* name,
+                                  const dagrt_array* arrays, const int32_t* modes, int32_t n);
+
 /* ---------------------------------------------------------------- host access */
 
 /* Host read of bytes [off, off+bytes) of array a into dst (L505-516): if the

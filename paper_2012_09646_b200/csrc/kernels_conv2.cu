@@ -43,21 +43,25 @@ namespace dagrt {
 
 namespace c2ws {
 
-constexpr int kStages = 4;                 // TMA ring depth (tiles of input in flight)
-constexpr int kBufs = 2;                   // TMEM accumulator + A_lo buffers
 constexpr int kTaps = 9;
 constexpr int kBox = 128 * 32;             // one tap: 128 pixels x 8 fp32, SWIZZLE_32B
 constexpr int kStage = kTaps * kBox;       // 36 KB
 constexpr int kBTap = 32 * 32;             // B per tap: 32 rows (16 hi + 16 lo) x 8 tf32
-constexpr int kThreads = 320;              // 10 warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCols = 64;          // per buffer: acc32 (32) + acc16 (16), padded
-constexpr uint32_t kLoBase = kBufs * kAccCols;
 constexpr uint32_t kLoCols = kTaps * 8;    // 72 tf32 columns of A_lo per buffer
 
-constexpr size_t smem_bytes() {
-  return 1024 + (size_t)kStages * kStage + kTaps * kBTap + 8 * (2 * kStages + 3 * kBufs) + 16;
-}
+// S TMA stages, NB TMEM buffers, SW split warps (a multiple of 4: SW/4 warps
+// per TMEM lane quarter, sharing the 9 taps); warps 0-1 producer / MMA,
+// 2..2+SW-1 split, then 4 epilogue warps
+template <int S, int NB, int SW>
+struct Cfg {
+  static constexpr int kThreads = 32 * (2 + SW + 4);
+  static constexpr uint32_t kLoBase = NB * kAccCols;
+  static constexpr size_t smem() { return 1024 + (size_t)S * kStage + kTaps * kBTap + 8 * (2 * S + 3 * NB) + 16; }
+  static_assert(kLoBase + NB * kLoCols <= kTmemCols, "TMEM budget");
+  static_assert(SW % 4 == 0 && SW >= 4, "split warps per lane quarter");
+};
 
 // instruction descriptors: D f32, A/B tf32, K-major, M = 128
 constexpr uint32_t idesc(uint32_t n) {
@@ -119,11 +123,13 @@ __device__ __forceinline__ int box_rows(int W2) { return W2 < 256 ? (W2 + 1) / 2
 
 }  // namespace c2ws
 
-__global__ void __launch_bounds__(c2ws::kThreads, 1) k_conv2_ws(const CUtensorMap* __restrict__ tmap,
-                                                               const float* __restrict__ in,
-                                                               const float* __restrict__ w,
-                                                               float* __restrict__ out, int H2, int W2) {
+template <int S, int NB, int SW>
+__global__ void __launch_bounds__(c2ws::Cfg<S, NB, SW>::kThreads, 1)
+    k_conv2_ws(const CUtensorMap* __restrict__ tmap, const float* __restrict__ in, const float* __restrict__ w,
+               float* __restrict__ out, int H2, int W2) {
   using namespace c2ws;
+  constexpr int kStages = S, kBufs = NB, kThreads = Cfg<S, NB, SW>::kThreads;
+  constexpr uint32_t kLoBase = Cfg<S, NB, SW>::kLoBase;
   extern __shared__ unsigned char sm_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* raw = sm;                               // [S][9][128 x 32 B] SW32
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(c2ws::kThreads, 1) k_conv2_ws(const CUtensorMa
       mbar_init(empty + q, 1);
     }
     for (int b = 0; b < kBufs; ++b) {
-      mbar_init(loready + b, 4);
+      mbar_init(loready + b, SW);
       mbar_init(mmadone + b, 1);
       mbar_init(accempty + b, 4);
     }
@@ -223,9 +229,12 @@ __global__ void __launch_bounds__(c2ws::kThreads, 1) k_conv2_ws(const CUtensorMa
         commit(mmadone + b);  // accumulators ready; A_lo buffer free
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + SW) {
     // ---------------- split: lo = x - trunc_tf32(x) -> TMEM (lane = pixel row)
     const int quarter = warp & 3, r = quarter * 32 + lane;
+    const int part = (warp - 2) / 4;  // which share of the taps (SW / 4 shares)
+    constexpr int kShares = SW / 4;
+    constexpr int kPer = (kTaps + kShares - 1) / kShares;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int i = 0; i < nmine; ++i) {
       const int s = i % kStages, b = i % kBufs;
@@ -236,7 +245,9 @@ __global__ void __launch_bounds__(c2ws::kThreads, 1) k_conv2_ws(const CUtensorMa
       const int sw = (r >> 2) & 1;  // 32-byte swizzle: chunk c of row r at 16 (c ^ ((r >> 2) & 1))
       const uint32_t alo = tmem + lane_off + kLoBase + b * kLoCols;
 #pragma unroll
-      for (int tap = 0; tap < kTaps; ++tap) {
+      for (int tt = 0; tt < kPer; ++tt) {
+        const int tap = part * kPer + tt;
+        if (tap >= kTaps) break;
         const float4 x0 = *reinterpret_cast<const float4*>(rs + tap * kBox + 16 * sw);
         const float4 x1 = *reinterpret_cast<const float4*>(rs + tap * kBox + 16 * (sw ^ 1));
         asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(alo + tap * 8),
@@ -291,11 +302,36 @@ __global__ void __launch_bounds__(c2ws::kThreads, 1) k_conv2_ws(const CUtensorMa
 
 int conv2_tma_prelaunch(const uint64_t* vals, int nargs, void** extra);  // kernels_conv_tc.cu
 
+// launch contract (dagrt_launch validates it before the pre-launch hook)
+static const char* v_conv2_tc(const LaunchCheck& L, unsigned threads, unsigned smem_min) {  // in, w, out, H2, W2
+  const int H2 = L.i32(3), W2 = L.i32(4);
+  if (H2 < 0 || W2 < 0) return "negative size";
+  const uint64_t H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  if (!fits(L, 0, 32ull * H2 * W2) || !fits(L, 1, 4 * 16 * 72) || !fits(L, 2, 64 * H3 * W3))
+    return "in (32 H2 W2), w (4608) or out (64 H3 W3) too small";
+  if (L.vals[0] % 16) return "the input must be 16-byte aligned (TMA)";
+  if (L.block[0] != threads || L.block[1] != 1 || L.block[2] != 1) return "wrong block size for this kernel";
+  if (L.smem < smem_min) return "dynamic shared memory below the kernel's layout";
+  return nullptr;
+}
+template <int S, int NB, int SW>
+static const char* v_conv2_ws(const LaunchCheck& L) {
+  using C = c2ws::Cfg<S, NB, SW>;
+  return v_conv2_tc(L, C::kThreads, (unsigned)C::smem());
+}
+
+#define C2WS(NAME, S, NB, SW)                                                                            \
+  {NAME, (const void*)k_conv2_ws<S, NB, SW>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, \
+   (int)c2ws::Cfg<S, NB, SW>::smem(), conv2_tma_prelaunch, v_conv2_ws<S, NB, SW>}
 static const Builtin kConv2Ws[] = {
-    // warp-specialised TMA -> tcgen05 conv2 with A_lo in TMEM: 148 CTAs of 320
-    // threads, c2ws::smem_bytes() of dynamic shared memory
-    {"conv2_ws", (const void*)k_conv2_ws, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     (int)c2ws::smem_bytes(), conv2_tma_prelaunch},
+    // warp-specialised TMA -> tcgen05 conv2 with A_lo in TMEM, 148 CTAs:
+    // S TMA stages, NB TMEM buffers, SW split warps (threads 32 (6 + SW),
+    // c2ws::Cfg<S, NB, SW>::smem() bytes of dynamic shared memory)
+    C2WS("conv2_ws", 4, 2, 4),
+    C2WS("conv2_ws6", 6, 2, 4),
+    C2WS("conv2_ws6s8", 6, 2, 8),
+    C2WS("conv2_ws6b3", 6, 3, 4),
+    C2WS("conv2_ws5s8b3", 5, 3, 8),
 };
 DAGRT_REGISTER_BUILTINS(kConv2Ws);
 

@@ -1868,6 +1868,22 @@ int conv2_tma_prelaunch(const uint64_t* vals, int nargs, void** extra) {
   return 0;
 }
 
+// launch contract (dagrt_launch validates it before the pre-launch hook)
+static const char* v_conv2_tc(const LaunchCheck& L, unsigned threads, unsigned smem_min) {  // in, w, out, H2, W2
+  const int H2 = L.i32(3), W2 = L.i32(4);
+  if (H2 < 0 || W2 < 0) return "negative size";
+  const uint64_t H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  if (!fits(L, 0, 32ull * H2 * W2) || !fits(L, 1, 4 * 16 * 72) || !fits(L, 2, 64 * H3 * W3))
+    return "in (32 H2 W2), w (4608) or out (64 H3 W3) too small";
+  if (L.vals[0] % 16) return "the input must be 16-byte aligned (TMA)";
+  if (L.block[0] != threads || L.block[1] != 1 || L.block[2] != 1) return "wrong block size for this kernel";
+  if (L.smem < smem_min) return "dynamic shared memory below the kernel's layout";
+  return nullptr;
+}
+static const char* v_conv2_product(const LaunchCheck& L) {
+  return v_conv2_tc(L, 384, (unsigned)tmang_smem<3, 1>());
+}
+
 static const Builtin kConvTc[] = {
     // product: TMA-gathered A, three consumer groups with one TMA stage each
     // (k_conv2_tmang<3,1> = "conv2_tman3x1": 285 us per branch; 148 CTAs of 384
@@ -1881,7 +1897,7 @@ static const Builtin kConvTc[] = {
     // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
     {"conv2", (const void*)k_conv2_tmang<3, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     tmang_smem<3, 1>(), conv2_tma_prelaunch},
+     tmang_smem<3, 1>(), conv2_tma_prelaunch, v_conv2_product},
     // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
     {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC3Smem},

@@ -369,11 +369,36 @@ __global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
   if (grid_finish(r, blk, OpAdd(), 0.0, &total, sh) && threadIdx.x == 0) r->result = (float)total;
 }
 
+// launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)
+static const char* v_conv1(const LaunchCheck& L) {  // x, w1, out, H, W
+  const int H = L.i32(3), W = L.i32(4);
+  if (H < 0 || W < 0) return "negative image size";
+  const uint64_t h1 = (H + 1) / 2, w1 = (W + 1) / 2;
+  if (!fits(L, 0, 4ull * H * W) || !fits(L, 1, 4 * 72) || !fits(L, 2, 32 * h1 * w1))
+    return "x (4 H W), w1 (288) or out (32 ceil(H/2) ceil(W/2)) too small";
+  return L.nthreads() == 256 ? nullptr : "256 threads per CTA";
+}
+static const char* v_pool(const LaunchCheck& L) {  // in, out, H1, W1 (8 channels)
+  const int H = L.i32(2), W = L.i32(3);
+  if (H < 0 || W < 0) return "negative size";
+  if (!fits(L, 0, 32ull * H * W) || !fits(L, 1, 32ull * (H / 2) * (W / 2))) return "in / out too small";
+  return L.nthreads() <= 256 ? nullptr : "at most 256 threads per CTA";
+}
+static const char* v_concat(const LaunchCheck& L) {  // a, b, z, na, nb
+  const uint64_t na = (uint64_t)L.i(3), nb = (uint64_t)L.i(4);
+  return fits(L, 0, 4 * na) && fits(L, 1, 4 * nb) && fits(L, 2, 4 * (na + nb)) ? nullptr : "arrays too small";
+}
+static const char* v_dot(const LaunchCheck& L) {  // z, wd, r, n
+  const uint64_t n = (uint64_t)L.i(3);
+  if (!fits(L, 0, 4 * n) || !fits(L, 1, 4 * n)) return "vectors need 4 n bytes";
+  return check_reduction(L, 2);
+}
+
 static const Builtin kDl[] = {
     // one row per iteration, registers capped for 4 CTAs/SM (687 us vs 710 us uncapped)
     // product: two output rows per iteration, 3 CTAs/SM; grid.y walks row PAIRS
     // (633 us vs 690 us for one row per iteration, tools/conv2_variants.py)
-    {"conv1", (const void*)k_conv1_r2b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1", (const void*)k_conv1_r2b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 0, nullptr, v_conv1},
     {"conv1_b3", (const void*)k_conv1_b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4cs", (const void*)k_conv1_b4cs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
@@ -382,11 +407,11 @@ static const Builtin kDl[] = {
     {"conv1_r2b3cs", (const void*)k_conv1_r2b3cs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_r2b2", (const void*)k_conv1_r2b2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b1", (const void*)k_conv1, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
-    {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"pool", (const void*)k_pool, "const ptr, out ptr, sint32, sint32", KF_NONE, 0, nullptr, v_pool},
     // CUDA-core variant of the second convolution (the tcgen05 one is "conv2")
     {"conv2_ffma", (const void*)k_conv2, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
-    {"concat", (const void*)k_concat, "const ptr, const ptr, out ptr, sint64, sint64", KF_NONE},
-    {"dot", (const void*)k_dot, "const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"concat", (const void*)k_concat, "const ptr, const ptr, out ptr, sint64, sint64", KF_NONE, 0, nullptr, v_concat},
+    {"dot", (const void*)k_dot, "const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_dot},
 };
 DAGRT_REGISTER_BUILTINS(kDl);
 

@@ -1182,14 +1182,38 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
   for (long long i = done + tid; i < n; i += nth) out[i] = v[i] * is;
 }
 
+// launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)
+static const char* v_spmv_plan_kernel(const LaunchCheck& L) {  // row_ptr, col, plan, x, y, N
+  const int64_t N = L.i(5);
+  if (N < 0 || N >= (1ll << 31)) return "need 0 <= N < 2^31";
+  if (!fits(L, 0, 4ull * (N + 1))) return "row_ptr needs 4 (N + 1) bytes";
+  if (!fits(L, 2, 4ull * kNzHeader)) return "plan smaller than its header";
+  if (!fits(L, 3, 4ull * N)) return "x needs 4 N bytes";
+  if (L.block[0] % 32 || L.block[1] != 1 || L.block[2] != 1 || L.grid[1] != 1 || L.grid[2] != 1)
+    return "1-D launch, block a multiple of 32";
+  // y carries the cross-warp workspace: 16-byte aligned after N floats, 3 words per warp
+  if (!fits(L, 4, 4ull * N + 16 + 12ull * (L.block[0] / 32) * L.grid[0]))
+    return "y needs 4 N + 16 + 12 (warps of the grid) bytes";
+  return nullptr;
+}
+static const char* v_l2norm(const LaunchCheck& L) {
+  if (!fits(L, 0, 4ull * L.i(2))) return "vector needs 4 n bytes";
+  return check_reduction(L, 1);
+}
+static const char* v_divide(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(3);
+  if (!fits(L, 0, 4 * n) || !fits(L, 2, 4 * n)) return "vectors need 4 n bytes";
+  return fits(L, 1, 4) ? nullptr : "norm output too small";
+}
+
 static const Builtin kHits[] = {
     // merge-path SpMV (round-1 product) and its variants: gathers in registers
     // (sync), L2 policies (tools/spmv_variants.py); bit-identical to each other
     // product: non-zero split over rows padded to >= 1 item: row_ptr, col,
     // plan (programs/hits_dl.py spmv_pad_plan), x, y, N
-    {"spmv", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     // the same without padding (row ids from a non-empty-row list, spmv_nz_plan)
-    {"spmv_nz", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"spmv_nz", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_merge", (const void*)k_spmv, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     // row-class SpMV (measured slower, kept as a tested alternative): row_ptr, col,
     // plan (programs/hits_dl.py spmv_plan), x, y, N
@@ -1199,8 +1223,8 @@ static const Builtin kHits[] = {
     {"spmv_x0s1", (const void*)k_spmv_x0s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_x1s1", (const void*)k_spmv_x1s1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
     {"spmv_as1", (const void*)k_spmv_as1, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
-    {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE},
-    {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_l2norm},
+    {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_divide},
 };
 DAGRT_REGISTER_BUILTINS(kHits);
 

@@ -323,14 +323,39 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ x,
   for (long long i = done + tid; i < n; i += nth) out[i] = x[i] * m[i] + y[i] * (1.f - m[i]);
 }
 
+// launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)
+static const char* v_stencil(const LaunchCheck& L) {  // src, dst, H, W [, d, sigma^2]
+  const uint64_t n = (uint64_t)(uint32_t)L.i32(2) * (uint32_t)L.i32(3);
+  if (L.i32(2) < 0 || L.i32(3) < 0) return "negative image size";
+  if (!fits(L, 0, 4 * n) || !fits(L, 1, 4 * n)) return "images need 4 H W bytes";
+  if (L.block[0] != 128 || L.block[1] != 1 || L.block[2] != 1) return "the stencil tile needs 128 threads";
+  if (L.nargs > 4 && L.i32(4) != 1 && L.i32(4) != 3 && L.i32(4) != 5) return "blur diameter must be 1, 3 or 5";
+  return nullptr;
+}
+static const char* v_extremum(const LaunchCheck& L) {
+  if (!fits(L, 0, 4 * (uint64_t)L.i(2))) return "input needs 4 n bytes";
+  return check_reduction(L, 1);
+}
+static const char* v_extend(const LaunchCheck& L) {
+  if (!fits(L, 0, 4 * (uint64_t)L.i(3))) return "mask needs 4 n bytes";
+  return fits(L, 1, 4) && fits(L, 2, 4) ? nullptr : "extrema outputs too small";
+}
+template <int NA>  // NA fp32 arrays of n elements, then n
+static const char* v_pointwise(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(NA);
+  for (int a = 0; a < NA; ++a)
+    if (!fits(L, a, 4 * n)) return "arrays need 4 n bytes";
+  return nullptr;
+}
+
 static const Builtin kImg[] = {
-    {"blur", (const void*)k_blur, "const ptr, out ptr, sint32, sint32, sint32, float", KF_NONE},
-    {"sobel", (const void*)k_sobel, "const ptr, out ptr, sint32, sint32", KF_NONE},
-    {"maximum", (const void*)k_extremum<true>, "const ptr, out ptr, sint64", KF_NONE},
-    {"minimum", (const void*)k_extremum<false>, "const ptr, out ptr, sint64", KF_NONE},
-    {"extend", (const void*)k_extend, "ptr, const ptr, const ptr, sint64, float", KF_NONE},
-    {"unsharpen", (const void*)k_unsharpen, "const ptr, const ptr, out ptr, sint64, float", KF_NONE},
-    {"combine", (const void*)k_combine, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"blur", (const void*)k_blur, "const ptr, out ptr, sint32, sint32, sint32, float", KF_NONE, 0, nullptr, v_stencil},
+    {"sobel", (const void*)k_sobel, "const ptr, out ptr, sint32, sint32", KF_NONE, 0, nullptr, v_stencil},
+    {"maximum", (const void*)k_extremum<true>, "const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_extremum},
+    {"minimum", (const void*)k_extremum<false>, "const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_extremum},
+    {"extend", (const void*)k_extend, "ptr, const ptr, const ptr, sint64, float", KF_NONE, 0, nullptr, v_extend},
+    {"unsharpen", (const void*)k_unsharpen, "const ptr, const ptr, out ptr, sint64, float", KF_NONE, 0, nullptr, v_pointwise<3>},
+    {"combine", (const void*)k_combine, "const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_pointwise<4>},
 };
 DAGRT_REGISTER_BUILTINS(kImg);
 

@@ -624,18 +624,88 @@ __global__ void __launch_bounds__(256) k_argmax(const float* __restrict__ r1,
   ROW_LOOP out[r] = rargmax(r1 + r * C, r2 + r * C, C);
 }
 
+// launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)
+static const char* v_norm(const LaunchCheck& L) {  // X, Z, stats, N, F
+  const int64_t N = L.i(3);
+  const int F = L.i32(4);
+  if (N < 0 || N >= (1ll << 32) || F < 1) return "need 0 <= N < 2^32 rows and F >= 1 features";
+  const uint64_t nf = (uint64_t)N * F;
+  if (!fits(L, 0, 4 * nf) || !fits(L, 1, 4 * nf)) return "X and Z need 4 N F bytes";
+  if (!fits(L, 2, 16 + 16ull * F + 24ull * F * L.grid[0])) return "stats need 16 + 16 F + 24 F grid bytes";
+  if (L.block[0] > 512 || L.block[0] % 32 || L.block[1] != 1 || L.block[2] != 1 || L.grid[1] != 1 || L.grid[2] != 1)
+    return "1-D launch, block a multiple of 32 <= 512";
+  const bool vec = (F % 4 == 0) && ((L.vals[0] | L.vals[1]) % 16 == 0) && F / 4 <= 512;
+  const int G = vec ? F / 4 : F;
+  if (G > (int)L.block[0]) return "block smaller than the feature groups";
+  const int RL = (int)L.block[0] / G > 1 ? (int)L.block[0] / G : 1;
+  if (L.smem < 24u * F * RL) return "dynamic shared memory below 24 F (block / groups) bytes";
+  if (L.real) {  // the software grid barrier needs the whole grid co-resident
+    static int per_sm = -1, sms = 0;
+    static unsigned last_block = 0, last_smem = 0;
+    if (per_sm < 0 || last_block != L.block[0] || last_smem != L.smem) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute((const void*)k_norm, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_norm, (int)L.block[0], L.smem))
+        per_sm = 0;
+      cudaGetLastError();
+      last_block = L.block[0];
+      last_smem = L.smem;
+    }
+    if ((long long)L.grid[0] > (long long)per_sm * sms) return "grid larger than the co-resident CTAs (cooperative)";
+  }
+  return nullptr;
+}
+template <bool NB>
+static const char* v_mmul(const LaunchCheck& L) {  // A, W, [prior,] out, N, F, C
+  const int o = NB ? 1 : 0;
+  const int64_t N = L.i(3 + o);
+  const int F = L.i32(4 + o), C = L.i32(5 + o);
+  if (N < 0 || F < 1 || C < 1) return "need N >= 0, F >= 1, C >= 1";
+  if (!fits(L, 0, 4ull * N * F) || !fits(L, 1, 4ull * C * F) || !fits(L, 2 + o, 4ull * N * C))
+    return "A (4 N F), weights (4 C F) or output (4 N C) too small";
+  if (NB && !fits(L, 2, 4ull * C)) return "prior needs 4 C bytes";
+  if (L.nthreads() > 256 || L.block[1] != 1 || L.block[2] != 1) return "1-D block of <= 256 threads";
+  if (L.smem < 4u * C * F) return "dynamic shared memory below 4 C F bytes";
+  const bool tma = C == 10 && F % 4 == 0 && F <= 200 && (F / 2) % 4 == 0 && L.block[0] == kMmThreads &&
+                   L.vals[0] % 16 == 0 && L.vals[2 + o] % 8 == 0;
+  if (tma && L.smem < mmul_tma_smem(F)) return "TMA path needs mmul_tma_smem(F) bytes of shared memory";
+  return nullptr;
+}
+// row-wise kernels over an N x C score array: (arrays..., N, C)
+static const char* v_rows(const LaunchCheck& L, int na, const int* per_row_classes) {
+  const int64_t N = L.i(na);
+  const int C = L.i32(na + 1);
+  if (N < 0 || C < 1 || C > kMaxClasses) return "need N >= 0 and 1 <= C <= 16";
+  for (int a = 0; a < na; ++a)  // 1: N x C scores, 0: N per-row values, -1: checked by the caller
+    if (per_row_classes[a] >= 0 && !fits(L, a, 4ull * N * (per_row_classes[a] ? C : 1)))
+      return "an array is smaller than its N x C / N";
+  return L.nthreads() <= 256 ? nullptr : "at most 256 threads per CTA";
+}
+static const char* v_rowmax(const LaunchCheck& L) { static const int k[] = {1, 0}; return v_rows(L, 2, k); }
+static const char* v_lse(const LaunchCheck& L) { static const int k[] = {1, 0, 0}; return v_rows(L, 3, k); }
+static const char* v_exp_sub(const LaunchCheck& L) { static const int k[] = {1, 0}; return v_rows(L, 2, k); }
+static const char* v_addv(const LaunchCheck& L) {
+  static const int k[] = {1, -1};
+  if (const char* e = v_rows(L, 2, k)) return e;
+  return fits(L, 1, 4ull * L.i32(3)) ? nullptr : "bias needs 4 C bytes";
+}
+static const char* v_softmax(const LaunchCheck& L) { static const int k[] = {1}; return v_rows(L, 1, k); }
+static const char* v_argmax(const LaunchCheck& L) { static const int k[] = {1, 1, 0}; return v_rows(L, 3, k); }
+
 static const Builtin kMl[] = {
-    {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_COOPERATIVE, 96 * 1024},
+    {"norm", (const void*)k_norm, "const ptr, out ptr, out ptr, sint64, sint32", KF_COOPERATIVE, 96 * 1024, nullptr, v_norm},
     {"nb_mmul", (const void*)k_nb_mmul,
-     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 120 * 1024},
+     "const ptr, const ptr, const ptr, out ptr, sint64, sint32, sint32", KF_NONE, 120 * 1024, nullptr, v_mmul<true>},
     {"rr_mmul", (const void*)k_rr_mmul, "const ptr, const ptr, out ptr, sint64, sint32, sint32",
-     KF_NONE, 120 * 1024},
-    {"rowmax", (const void*)k_rowmax, "const ptr, out ptr, sint64, sint32", KF_NONE},
-    {"lse", (const void*)k_lse, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE},
-    {"exp_sub", (const void*)k_exp_sub, "ptr, const ptr, sint64, sint32", KF_NONE},
-    {"addv", (const void*)k_addv, "ptr, const ptr, sint64, sint32", KF_NONE},
-    {"softmax", (const void*)k_softmax, "ptr, sint64, sint32", KF_NONE},
-    {"argmax", (const void*)k_argmax, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE},
+     KF_NONE, 120 * 1024, nullptr, v_mmul<false>},
+    {"rowmax", (const void*)k_rowmax, "const ptr, out ptr, sint64, sint32", KF_NONE, 0, nullptr, v_rowmax},
+    {"lse", (const void*)k_lse, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE, 0, nullptr, v_lse},
+    {"exp_sub", (const void*)k_exp_sub, "ptr, const ptr, sint64, sint32", KF_NONE, 0, nullptr, v_exp_sub},
+    {"addv", (const void*)k_addv, "ptr, const ptr, sint64, sint32", KF_NONE, 0, nullptr, v_addv},
+    {"softmax", (const void*)k_softmax, "ptr, sint64, sint32", KF_NONE, 0, nullptr, v_softmax},
+    {"argmax", (const void*)k_argmax, "const ptr, const ptr, out ptr, sint64, sint32", KF_NONE, 0, nullptr, v_argmax},
 };
 DAGRT_REGISTER_BUILTINS(kMl);
 

@@ -73,8 +73,12 @@ __global__ void __launch_bounds__(256) k_axpb(float* a, long long n, float alpha
     a[i] = fmaf(alpha, a[i], beta);
 }
 
+static const char* v_axpb(const LaunchCheck& L) {
+  return fits(L, 0, 4ull * L.i(1)) ? nullptr : "a needs 4 n bytes";
+}
+
 static const Builtin kProbes[] = {
-    {"axpb", (const void*)k_axpb, "ptr, sint64, float, float", KF_NONE},
+    {"axpb", (const void*)k_axpb, "ptr, sint64, float, float", KF_NONE, 0, nullptr, v_axpb},
     {"peak_dfma", (const void*)k_peak_dfma, "out ptr, sint64", KF_NONE},
     {"peak_ffma", (const void*)k_peak_ffma, "out ptr, sint64", KF_NONE},
 };

@@ -364,6 +364,107 @@ BS2_VARIANT(k_bs2_p2w4b2, 2, 4, 2)
 BS2_VARIANT(k_bs2_p4w2b2, 4, 2, 2)
 BS2_VARIANT(k_bs2_p1w2b4, 1, 2, 4)
 
+// TMA-staged form: each CTA walks contiguous chunks of 256 * OPT options;
+// one thread streams chunk k + STAGES into a shared-memory ring with a bulk
+// copy (cp.async.bulk, completion on an mbarrier) while the CTA prices chunk
+// k -- deep prefetch at no register cost (the register-prefetched loops were
+// long-scoreboard bound: ncu, profiles/).  Each thread prices OPT options of a
+// chunk in lockstep, reading them with 128-bit shared loads; the prices go
+// straight to global memory (coalesced 16-byte stores).
+__device__ __forceinline__ void bs_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void bs_mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bs_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+template <int OPT, int STAGES>
+__device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, double* __restrict__ c, long long n,
+                                             double r, double v, double t, double k) {
+  constexpr int kChunk = 256 * OPT;  // options per chunk (blockDim.x == 256)
+  __shared__ BsTables T;
+  __shared__ __align__(128) double ring[STAGES][kChunk];
+  __shared__ uint64_t full[STAGES];
+  bs_tables_init(T);
+  BsConst C;
+  const double vst = v * sqrt(t);
+  C.vst = vst;
+  C.inv_vst = 1.0 / vst;
+  C.mu_s = (r + 0.5 * v * v) * t / vst;
+  C.inv_k = 1.0 / k;
+  C.c2 = exp(r * t) / k;
+  C.kexp = k * exp(-r * t);
+  const int tid = threadIdx.x;
+  if (!(aligned16(s) && aligned16(c)) || blockDim.x != 256) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < n; i += (long long)gridDim.x * blockDim.x) {
+      double a[2] = {s[i], 1.0}, o[2];
+      bs_price_w<2>(a, o, C, T);
+      c[i] = o[0];
+    }
+    return;
+  }
+  const long long nfullc = n / kChunk;  // whole chunks via the ring; the tail directly
+  const long long G = gridDim.x;
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) bs_mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < STAGES; ++q) {
+      const long long ch = blockIdx.x + q * G;
+      if (ch < nfullc) bs_bulk_g2s(ring[q], s + ch * kChunk, kChunk * 8, &full[q]);
+    }
+  int it = 0;
+  for (long long ch = blockIdx.x; ch < nfullc; ch += G, ++it) {
+    const int st = it % STAGES;
+    bs_mbar_wait(&full[st], (unsigned)((it / STAGES) & 1));
+    double a[OPT], o[OPT];
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) {  // options 2 (tid + 256 q) and +1: 16-byte shared loads
+      const double2 x = reinterpret_cast<const double2*>(ring[st])[tid + 256 * q];
+      a[2 * q] = x.x;
+      a[2 * q + 1] = x.y;
+    }
+    __syncthreads();  // every thread has its options: the stage may be refilled
+    if (tid == 0 && ch + STAGES * G < nfullc) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bs_bulk_g2s(ring[st], s + (ch + STAGES * G) * kChunk, kChunk * 8, &full[st]);
+    }
+    bs_price_w<OPT>(a, o, C, T);
+    double2* dst = reinterpret_cast<double2*>(c + ch * kChunk);
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) dst[tid + 256 * q] = make_double2(o[2 * q], o[2 * q + 1]);
+  }
+  for (long long i = nfullc * kChunk + (long long)blockIdx.x * blockDim.x + tid; i < n; i += G * blockDim.x) {
+    double a[2] = {s[i], 1.0}, o[2];
+    bs_price_w<2>(a, o, C, T);
+    c[i] = o[0];
+  }
+}
+#define BS2T_VARIANT(NAME, OPT, STAGES, MINB)                                                      \
+  __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs2_tma_body<OPT, STAGES>(s, c, n, r, v, t, k);                                                \
+  }
+BS2T_VARIANT(k_bs2t_o4s4b2, 4, 4, 2)
+BS2T_VARIANT(k_bs2t_o4s3b3, 4, 3, 3)
+BS2T_VARIANT(k_bs2t_o2s4b4, 2, 4, 4)
+BS2T_VARIANT(k_bs2t_o6s3b2, 6, 3, 2)
+
 // K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores.
 // PAIRS double2 per thread per iteration (independent chains for the FP64
 // pipe to interleave); the next group's loads are issued before pricing.
@@ -591,13 +692,29 @@ __global__ void __launch_bounds__(256, 2) k_bs_p4b2(const double* __restrict__ s
   bs_body<4>(s, c, n, r, v, t, k);
 }
 
+// launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)
+static const char* v_square(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(2);
+  return fits(L, 0, 4 * n) && fits(L, 1, 4 * n) ? nullptr : "x and x1 need 4 n bytes";
+}
+static const char* v_reduce_diff(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(3);
+  if (!fits(L, 0, 4 * n) || !fits(L, 1, 4 * n)) return "inputs need 4 n bytes";
+  return check_reduction(L, 2);
+}
+static const char* v_bs(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(2);
+  if (!fits(L, 0, 8 * n) || !fits(L, 1, 8 * n)) return "prices and calls need 8 n bytes";
+  return L.nthreads() <= 256 ? nullptr : "at most 256 threads per CTA";
+}
+
 static const Builtin kVecBs[] = {
-    {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE},
-    {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE},
+    {"square", (const void*)k_square, "const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_square},
+    {"reduce_diff", (const void*)k_reduce_diff, "const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_reduce_diff},
     // product: lean loop, 3 pairs per thread, 2 CTAs/SM, one wave (44.8 us per
     // 10M options vs 46.2 for 4 pairs (k_bs_l4b2) in three back-to-back runs,
     // 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
-    {"bs", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, 0, nullptr, v_bs},
     {"bs_p4", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a3b4", (const void*)k_bs_a3b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a5b4", (const void*)k_bs_a5b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
@@ -620,6 +737,10 @@ static const Builtin kVecBs[] = {
     {"bs2_p2w4b2", (const void*)k_bs2_p2w4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2_p4w2b2", (const void*)k_bs2_p4w2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2_p1w2b4", (const void*)k_bs2_p1w2b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2t_o4s4b2", (const void*)k_bs2t_o4s4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2t_o4s3b3", (const void*)k_bs2t_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2t_o2s4b4", (const void*)k_bs2t_o2s4b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2t_o6s3b2", (const void*)k_bs2t_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
 };
 DAGRT_REGISTER_BUILTINS(kVecBs);
 

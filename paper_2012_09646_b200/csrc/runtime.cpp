@@ -628,10 +628,12 @@ struct KernelRec {
   std::string name;
   const void* fn;
   PrelaunchFn pre = nullptr;  // built-in pre-launch hook (extra leading kernel argument)
+  ValidateFn validate = nullptr;  // built-in launch contract
   int32_t nparams;
   uint8_t kind[kMaxArgs];
   bool coop;
   bool prof = false;
+  bool lib = false;  // pseudo-kernel of library-call vertices (dagrt_launch_library)
 };
 
 struct ProfRec {
@@ -1138,9 +1140,28 @@ dagrt_status parse_signature(const char* sig, KernelRec* k) {
   return DAGRT_OK;
 }
 
+// Launch configuration limits of the device (any kernel), then the
+// built-in's own contract.  Both fail with DAGRT_EINVAL (not sticky): nothing
+// was enqueued.
+dagrt_status check_launch(dagrt_ctx c, const KernelRec& k, dim3 g, dim3 b, uint32_t smem, const uint64_t* vals,
+                          ArrayRec* const* arrs, int nargs) {
+  const uint64_t nt = (uint64_t)b.x * b.y * b.z;
+  if (nt == 0 || nt > 1024) return fail(c, DAGRT_EINVAL, "kernel %s: block of %llu threads", k.name.c_str(),
+                                        (unsigned long long)nt);
+  if (g.x == 0 || g.y == 0 || g.z == 0 || g.y > 65535 || g.z > 65535)
+    return fail(c, DAGRT_EINVAL, "kernel %s: grid (%u, %u, %u)", k.name.c_str(), g.x, g.y, g.z);
+  if (smem > 227u * 1024u) return fail(c, DAGRT_EINVAL, "kernel %s: %u bytes of shared memory", k.name.c_str(), smem);
+  if (!k.validate) return DAGRT_OK;
+  uint64_t bytes[kMaxArgs];
+  for (int i = 0; i < nargs; ++i) bytes[i] = arrs[i] ? arrs[i]->bytes : 0;
+  LaunchCheck L{vals, bytes, nargs, {g.x, g.y, g.z}, {b.x, b.y, b.z}, smem, c->be->real()};
+  if (const char* why = k.validate(L)) return fail(c, DAGRT_EINVAL, "kernel %s: %s", k.name.c_str(), why);
+  return DAGRT_OK;
+}
+
 // Resolve args to the kernel parameter buffer; validates kinds.
 dagrt_status marshal(dagrt_ctx c, const KernelRec& k, const dagrt_arg* args, int32_t nargs,
-                     uint64_t* vals, void** argv, ArrayRec** arrs) {
+                     uint64_t* vals, void** argv, ArrayRec** arrs, dim3 g, dim3 b, uint32_t smem) {
   if (nargs != k.nparams)
     return fail(c, DAGRT_ESIG, "kernel %s: %d args given, signature has %d", k.name.c_str(), nargs,
                 k.nparams);
@@ -1160,7 +1181,8 @@ dagrt_status marshal(dagrt_ctx c, const KernelRec& k, const dagrt_arg* args, int
     }
     argv[i] = &vals[i];
   }
-  if (k.pre) {  // the hook's value becomes the kernel's first parameter
+  if (dagrt_status st = check_launch(c, k, g, b, smem, vals, arrs, nargs)) return st;
+  if (k.pre) {  // the hook's value becomes the kernel's first parameter (after validation)
     void* extra = nullptr;  // (no device work on the record backend: no hook)
     if (c->be->real())
       if (int e = k.pre(vals, nargs, &extra)) return cuda_fail(c, (cudaError_t)e, "pre-launch hook");
@@ -1210,6 +1232,7 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
     k.fn = b->fn;
     k.coop = (b->flags & KF_COOPERATIVE) != 0;
     k.pre = b->prelaunch;
+    k.validate = b->validate;
     if (b->smem_max > 0 && c->be->real() && b->fn)
       cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
     if (parse_signature(b->signature, &k) != DAGRT_OK) {
@@ -1378,16 +1401,92 @@ const char* dagrt_builtin_signature(int32_t i) {
   return b ? b->signature : nullptr;
 }
 
+}  // extern "C"
+
+namespace {
+// One computational element (L388-396): a kernel (lib == nullptr) or a
+// library call that enqueues its own GPU work on the stream the scheduler
+// picks (L516-519).  arrs / kinds: the arguments and their access modes.
+dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
+                           uint32_t smem, void** argv, ArrayRec* const* arrs, const uint8_t* kinds, int32_t nargs,
+                           dagrt_library_fn lib, void* user, std::chrono::steady_clock::time_point t0);
+}  // namespace
+
+extern "C" {
+
 dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
                           uint32_t smem, const dagrt_arg* args, int32_t nargs) {
   GUARD(c);
   auto t0 = std::chrono::steady_clock::now();
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
-  uint64_t vals[kMaxArgs];
-  void* argv[kMaxArgs];
+  if (k->lib) return fail(c, DAGRT_EINVAL, "%s is a library-call name, not a kernel", k->name.c_str());
+  uint64_t vals[kMaxArgs + 1];
+  void* argv[kMaxArgs + 1];
   ArrayRec* arrs[kMaxArgs];
-  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs, dim3(grid.x, grid.y, grid.z),
+                               dim3(block.x, block.y, block.z), smem))
+    return s;
+  return launch_vertex(c, k, kh, grid, block, smem, argv, arrs, k->kind, nargs, nullptr, nullptr, t0);
+}
+
+dagrt_status dagrt_launch_library(dagrt_ctx c, dagrt_library_fn fn, void* user, const char* name,
+                                  const dagrt_array* arrays, const int32_t* modes, int32_t n) {
+  GUARD(c);
+  auto t0 = std::chrono::steady_clock::now();
+  if (!fn || !name || n < 0 || n > kMaxArgs || (n > 0 && (!arrays || !modes)))
+    return fail(c, DAGRT_EINVAL, "library call: null function / name or bad array list");
+  ArrayRec* arrs[kMaxArgs];
+  uint8_t kinds[kMaxArgs];
+  for (int i = 0; i < n; ++i) {
+    ArrayRec* a = get_array(c, arrays[i]);
+    if (!a) return fail(c, DAGRT_ENOTFOUND, "library call %s arg %d: not a live array handle", name, i);
+    if (a->mapped) return fail(c, DAGRT_ESTATE, "library call %s arg %d: array is host-mapped", name, i);
+    if (modes[i] < DAGRT_R || modes[i] > DAGRT_RW) return fail(c, DAGRT_EINVAL, "library call %s: mode %d", name, modes[i]);
+    arrs[i] = a;
+    kinds[i] = modes[i] == DAGRT_R ? P_CONST : (modes[i] == DAGRT_W ? P_OUT : P_INOUT);
+  }
+  // a pseudo-kernel per call name (for the DAG export and statistics)
+  dagrt_kernel kh = 0;
+  bool found = false;
+  for (size_t i = c->kernels.size(); i-- > 0;)
+    if (c->kernels[i].fn == nullptr && c->kernels[i].name == name && c->kernels[i].lib) {
+      kh = (dagrt_kernel)i;
+      found = true;
+      break;
+    }
+  if (!found) {
+    KernelRec kr;
+    kr.name = name;
+    kr.fn = nullptr;
+    kr.nparams = 0;
+    kr.coop = false;
+    kr.lib = true;
+    c->kernels.push_back(kr);
+    kh = (dagrt_kernel)(c->kernels.size() - 1);
+  }
+  return launch_vertex(c, &c->kernels[kh], kh, dagrt_dim3{1, 1, 1}, dagrt_dim3{1, 1, 1}, 0, nullptr, arrs, kinds, n,
+                       fn, user, t0);
+}
+
+}  // extern "C"
+
+namespace {
+// Enqueue the vertex's GPU work on stream s: the kernel, or the library call.
+dagrt_status enqueue(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dim3 g, dim3 b, void** argv, uint32_t smem, void* s,
+                     int32_t sidx, int64_t gvid, dagrt_library_fn lib, void* user) {
+  if (!lib) return do_launch(c, k, kh, g, b, argv, smem, s, sidx, gvid);
+  if (!c->be->real()) return DAGRT_OK;  // the recorder does no device work
+  // a host callback cannot be deferred into a captured batch
+  CK(c->be->flush(), "graph cache flush");
+  CK(c->be->pre_eager(s), "graph cache ordering");
+  if (int32_t r = lib(s, user)) return fail(c, DAGRT_EINVAL, "library call %s returned %d", k->name.c_str(), r);
+  return DAGRT_OK;
+}
+
+dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
+                           uint32_t smem, void** argv, ArrayRec* const* arrs, const uint8_t* kinds, int32_t nargs,
+                           dagrt_library_fn lib, void* user, std::chrono::steady_clock::time_point t0) {
 
   // merged access per distinct array (D3): write if any use writes,
   // needs data if any use reads (const / inout)
@@ -1399,7 +1498,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
     int j = 0;
     while (j < nacc && acc[j] != arrs[i]) ++j;
     if (j == nacc) { acc[nacc] = arrs[i]; wr[nacc] = false; need[nacc] = false; ++nacc; }
-    uint8_t kd = k->kind[i];
+    uint8_t kd = kinds[i];
     if (kd != P_CONST) wr[j] = true;
     if (kd != P_OUT) need[j] = true;
   }
@@ -1431,7 +1530,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
       }
     }
     trace_op(c, DAGRT_OP_LAUNCH, -3, gvid, kh, 0);
-    if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, -3, gvid)) return st_;
+    if (dagrt_status st_ = enqueue(c, k, kh, g, b, argv, smem, s, -3, gvid, lib, user)) return st_;
     CK(c->be->stream_sync(s), "cudaStreamSynchronize");
     c->st.host_syncs++;
     c->vertices.push_back(VertexRec{0, 0, -1, nullptr, 0, 0});
@@ -1506,7 +1605,7 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   const uint64_t tl0 = now_ns();
   c->st.wait_ns += tl0 - tw0;
   trace_op(c, DAGRT_OP_LAUNCH, sid, gvid, kh, 0);
-  if (dagrt_status st_ = do_launch(c, k, kh, g, b, argv, smem, s, sid, gvid)) return st_;
+  if (dagrt_status st_ = enqueue(c, k, kh, g, b, argv, smem, s, sid, gvid, lib, user)) return st_;
   const uint64_t tr0 = now_ns();
   c->st.launch_ns += tr0 - tl0;
   trace_op(c, DAGRT_OP_RECORD, sid, gvid, 0, 0);
@@ -1536,6 +1635,10 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
                         std::chrono::steady_clock::now() - t0).count();
   return DAGRT_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 dagrt_status dagrt_launch_prepared(dagrt_ctx c, const dagrt_launch_desc* d) {
   if (!d) return c ? fail(c, DAGRT_EINVAL, "null launch descriptor") : DAGRT_EINVAL;
@@ -1830,10 +1933,12 @@ dagrt_status dagrt_launch_raw(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dag
   GUARD(c);
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
-  uint64_t vals[kMaxArgs];
-  void* argv[kMaxArgs];
+  uint64_t vals[kMaxArgs + 1];
+  void* argv[kMaxArgs + 1];
   ArrayRec* arrs[kMaxArgs];
-  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs, dim3(grid.x, grid.y, grid.z),
+                               dim3(block.x, block.y, block.z), smem))
+    return s;
   CK(c->be->launch_now(k->fn, dim3(grid.x, grid.y, grid.z), dim3(block.x, block.y, block.z), argv, smem,
                    stream, k->coop),
      "cudaLaunchKernel raw");
@@ -1870,10 +1975,12 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh,
   if (!g || !node) return fail(c, DAGRT_EINVAL, "null graph/node");
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
-  uint64_t vals[kMaxArgs];
-  void* argv[kMaxArgs];
+  uint64_t vals[kMaxArgs + 1];
+  void* argv[kMaxArgs + 1];
   ArrayRec* arrs[kMaxArgs];
-  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs)) return s;
+  if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs, dim3(grid.x, grid.y, grid.z),
+                               dim3(block.x, block.y, block.z), smem))
+    return s;
   std::vector<cudaGraphNode_t> d;
   if (dagrt_status s = graph_deps(c, g, deps, ndeps, &d)) return s;
   cudaKernelNodeParams p{};

@@ -420,6 +420,40 @@ class Context:
     def launch(self, kernel, grid, block, *args, smem=0):
         self.prepare(kernel, grid, block, args, smem)()
 
+    LIBFN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p)
+
+    def launch_library(self, fn, name, arrays, modes):
+        """A library call as a DAG vertex (dagrt_launch_library): fn(stream)
+        is called with the CUDA stream (an int handle) the scheduler picked
+        and must enqueue its GPU work there; arrays/modes declare its accesses
+        (R, W, RW)."""
+        def tramp(stream, _user):
+            try:
+                fn(stream or 0)
+                return 0
+            except Exception:  # surfaced as DAGRT_EINVAL
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb = self.LIBFN(tramp)
+        self._keep = getattr(self, "_keep", [])
+        self._keep.append(cb)
+        n = len(arrays)
+        A = (C.c_uint64 * max(1, n))(*[a.handle for a in arrays])
+        M = (C.c_int32 * max(1, n))(*modes)
+        L = lib()
+        L.dagrt_launch_library.argtypes = [C.c_void_p, self.LIBFN, C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p,
+                                           C.c_int32]
+        L.dagrt_launch_library.restype = C.c_int32
+        self._check(L.dagrt_launch_library(self._c, cb, None, name.encode(), C.addressof(A), C.addressof(M), n))
+        self._kname.setdefault(self._lib_handle(name), name)
+
+    def _lib_handle(self, name):
+        k = C.c_uint32()
+        if lib().dagrt_kernel_lookup(self._c, name.encode(), C.byref(k)) == 0:
+            return k.value
+        return -1
+
     def batch(self, launches):
         """Prepared launches -> one callable that issues them in order (Batch)."""
         return Batch(self, launches)

@@ -25,9 +25,18 @@ CONV2_TMAR_THREADS = 288
 CONV2_GRID, CONV2_THREADS = 148, 384
 CONV2_SMEM = 1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
-# warp-specialised conv2 (csrc/kernels_conv2.cu c2ws): 10 warps, 4 TMA stages
-CONV2_WS_THREADS = 320
-CONV2_WS_SMEM = 1024 + 4 * 9 * 4096 + 9 * 1024 + 8 * (2 * 4 + 3 * 2) + 16
+# warp-specialised conv2 (csrc/kernels_conv2.cu c2ws::Cfg<S, NB, SW>): S TMA
+# stages, NB TMEM buffers, SW split warps -> (threads, dynamic shared memory)
+CONV2_WS_CFG = {"conv2_ws": (4, 2, 4), "conv2_ws6": (6, 2, 4), "conv2_ws6s8": (6, 2, 8),
+                "conv2_ws6b3": (6, 3, 4), "conv2_ws5s8b3": (5, 3, 8)}
+
+
+def conv2_ws_launch(name):
+    s, nb, sw = CONV2_WS_CFG[name]
+    return 32 * (6 + sw), 1024 + s * 9 * 4096 + 9 * 1024 + 8 * (2 * s + 3 * nb) + 16
+
+
+CONV2_WS_THREADS, CONV2_WS_SMEM = conv2_ws_launch("conv2_ws")
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)

@@ -121,13 +121,15 @@ def test_dl_4096_elementwise():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("kernel", ["conv2_ws", "conv2_ws6", "conv2_ws6s8", "conv2_ws6b3", "conv2_ws5s8b3"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517), (1030, 2050), (4096, 4096)])
-def test_conv2_ws_matches_oracle(h, w):
+def test_conv2_ws_matches_oracle(h, w, kernel):
     """The warp-specialised conv2 (A_lo in TMEM; csrc/kernels_conv2.cu) against
     the oracle's conv on the pooled input, from one tile to ~14 tiles per CTA
     (every stage / TMEM buffer / barrier phase reused many times), ragged
     output rows (W3 not a multiple of 128)."""
-    from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
+    from paper_2012_09646_b200.programs.hits_dl import conv2_ws_launch
+    threads, smem = conv2_ws_launch(kernel)
     c = D.Context(device=0)
     p = DeepLearning(c, h=h, w=w)
     p.load_inputs(1)
@@ -138,7 +140,7 @@ def test_conv2_ws_matches_oracle(h, w):
     torch.cuda.synchronize()
     o_arr = c.register_tensor("c2ws", out)
     for _ in range(2):
-        c.launch("conv2_ws", 148, CONV2_WS_THREADS, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_WS_SMEM)
+        c.launch(kernel, 148, threads, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=smem)
     c.sync()
     spec = synth.spec_dl(h, w)
     w2 = synth.draw(p.seed, "w2", spec["w2"]).reshape(16, 3, 3, 8)
@@ -217,7 +219,7 @@ def test_bs_limits(svals):
     c.close()
 
 
-@pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2"])
+@pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2", "bs2t_o4s4b2", "bs2t_o6s3b2"])
 def test_bs_kernels_limits_and_range(kernel):
     """Every B&S pricing kernel on the limit values plus a dense S sweep over
     [1e-3, 1e4] (log-spaced): deep out of / in the money, d ~ 0, the exp's
@@ -266,4 +268,38 @@ def test_graph_cache_orders_same_stream_work_across_flush():
     assert torch.all(B == runs).item()
     st = c.stats()
     assert st["graph_replays"] >= runs - 3, st
+    c.close()
+
+
+# ------------------------------------------------------------------ library-call vertices
+def test_library_call_vertex_on_the_gpu():
+    """A library call (torch.matmul on the stream the scheduler picked,
+    PAPER.md L516-519) between two kernels: X1 = X^2 (kernel), Y = X1 W
+    (library), Y1 = Y^2 (kernel); the host reads Y1.  Results equal the fp64
+    reference and the DAG is the chain the access modes imply."""
+    n, f = 4096, 64
+    c = D.Context(device=0, record_dag=True)
+    X = torch.rand(n * f, device="cuda")
+    X1 = torch.empty_like(X)
+    W = torch.rand(f, f, device="cuda")
+    Y = torch.empty(n * f, device="cuda")
+    Y1 = torch.empty_like(Y)
+    torch.cuda.synchronize()
+    a = {k: c.register_tensor(k, t) for k, t in (("X", X), ("X1", X1), ("W", W), ("Y", Y), ("Y1", Y1))}
+    c.launch("square", 64, 256, a["X"], a["X1"], n * f)
+
+    def mm(stream):
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+            torch.matmul(X1.view(n, f), W, out=Y.view(n, f))
+    c.launch_library(mm, "matmul", [a["X1"], a["W"], a["Y"]], [D.R, D.R, D.W])
+    c.launch("square", 64, 256, a["Y"], a["Y1"], n * f)
+    import ctypes as C
+    buf = (C.c_float * 1)()
+    c.host_read(a["Y1"], C.addressof(buf), 0, 4)
+    c.sync()
+    ref = ((X.double().view(n, f) ** 2) @ W.double()) ** 2
+    assert torch.allclose(Y1.view(n, f).double(), ref, rtol=2e-3)
+    verts, edges = c.dag()
+    assert [v[2] for v in verts[:3]] == ["square", "matmul", "square"]
+    assert {(p, ch) for p, ch, _ in edges} == {(0, 1), (1, 2), (2, 3)}
     c.close()

@@ -184,7 +184,7 @@ def test_graph_cache_replays_identical_results(mode):
                                      "bs_p1b4", "bs_p2b4", "bs_p1b6", "bs_p4b2", "bs_p4",
                                      "bs_l4b2", "bs_l2b3", "bs_l2b4", "bs_l1b4", "bs_l3b2", "bs_l3b3",
                                      "bs_l8b1", "bs2_p3w2b2", "bs2_p2w2b3", "bs2_p2w4b2", "bs2_p4w2b2",
-                                     "bs2_p1w2b4"])
+                                     "bs2_p1w2b4", "bs2t_o4s4b2", "bs2t_o4s3b3", "bs2t_o2s4b4", "bs2t_o6s3b2"])
 # 227_333: an odd number of full groups for the lean 4-pair loop (ping-pong tail)
 @pytest.mark.parametrize("n", [3, 200_001, 227_333])
 def test_bs_variants_match_oracle(ctx, variant, n):

@@ -375,3 +375,83 @@ def test_scheduler_state_is_frontier_bounded():
             tr2 += [("host", "B", "R", 0, 64)]
     rp2.run(tr2)
     assert rp2.ctx.stats()["max_readers"] <= 33
+
+
+def _reg(ctx, name, nbytes, base=[0x10_0000_0000]):
+    base[0] += 1 << 32
+    return ctx.register(name, base[0], nbytes)
+
+
+@pytest.mark.parametrize("case", [
+    ("reduce_diff", 2000, 256, 0, lambda c: [_reg(c, "a", 4000), _reg(c, "b", 4000), _reg(c, "z", 8 + 8 * 2000), 1000],
+     "<= 1024 CTAs"),
+    ("reduce_diff", 100, 256, 0, lambda c: [_reg(c, "a", 4000), _reg(c, "b", 4000), _reg(c, "z", 100), 1000],
+     "8 + 8 * grid"),
+    ("square", 10, 256, 0, lambda c: [_reg(c, "a", 400), _reg(c, "b", 396), 100], "4 n bytes"),
+    ("bs", 10, 256, 0, lambda c: [_reg(c, "s", 800), _reg(c, "c", 792), 100, 0.08, 0.3, 1.0, 60.0], "8 n"),
+    ("blur", (1, 1), 128, 0, lambda c: [_reg(c, "i", 400), _reg(c, "o", 400), 10, 10, 7, 1.0], "diameter"),
+    ("blur", (1, 1), 256, 0, lambda c: [_reg(c, "i", 400), _reg(c, "o", 400), 10, 10, 3, 1.0], "128 threads"),
+    ("norm", 296, 512, 48000, lambda c: [_reg(c, "X", 4 * 1000 * 200), _reg(c, "Z", 4 * 1000 * 200),
+                                         _reg(c, "st", 100), 1000, 200], "stats need"),
+    ("norm", 296, 512, 1000, lambda c: [_reg(c, "X", 4 * 1000 * 200), _reg(c, "Z", 4 * 1000 * 200),
+                                        _reg(c, "st", 16 + 16 * 200 + 24 * 200 * 296), 1000, 200], "shared memory"),
+    ("softmax", 10, 256, 0, lambda c: [_reg(c, "x", 4 * 100 * 20), 100, 20], "C <= 16"),
+    ("spmv", 10, 256, 0, lambda c: [_reg(c, "rp", 4 * 11), _reg(c, "ci", 40), _reg(c, "pl", 64), _reg(c, "x", 40),
+                                    _reg(c, "y", 40), 10], "y needs"),
+    ("conv2", 148, 384, 0, lambda c: [_reg(c, "p", 32 * 64 * 64), _reg(c, "w", 4608), _reg(c, "o", 64 * 32 * 32),
+                                      64, 64], "shared memory"),
+    ("square", 10, 2048, 0, lambda c: [_reg(c, "a", 400), _reg(c, "b", 400), 100], "block of 2048"),
+], ids=lambda x: x if isinstance(x, str) else None)
+def test_builtin_launch_contracts_reject_bad_launches(case):
+    """Every product built-in checks its launch contract before a vertex is
+    made (array sizes against the shape scalars, grid / block / shared
+    memory): a violation is DAGRT_EINVAL with a message, non-sticky, no
+    vertex recorded -- instead of an out-of-bounds write or a hang."""
+    name, grid, block, smem, args, msg = case
+    ctx = D.Context(backend="record", record_dag=True)
+    with pytest.raises(D.DagrtError) as e:
+        ctx.launch(name, grid, block, *args(ctx), smem=smem)
+    assert e.value.status == D.EINVAL and msg in str(e.value), str(e.value)
+    assert ctx.dag() == ([], set())
+    ok = [_reg(ctx, "a2", 400), _reg(ctx, "b2", 400), 100]
+    ctx.launch("square", 1, 256, *ok)  # the context is still usable
+    assert len(ctx.dag()[0]) == 1
+
+
+def test_library_call_vertices_follow_the_dag_rules():
+    """Library calls (dagrt_launch_library) are vertices
+    like kernels: the same trace with some launches replaced by library calls
+    of the same access modes gives the oracle's DAG and streams."""
+    rng = random.Random(5)
+    names = list("ABCD")
+    for _ in range(60):
+        tr = []
+        for _ in range(rng.randint(1, 25)):
+            if rng.random() < 0.8:
+                tr.append(("launch", rng.choice(["k", "lib"]),
+                           [(a, rng.choice(["R", "RW", "O"])) for a in rng.sample(names, rng.randint(1, 3))]))
+            else:
+                tr.append(("host", rng.choice(names), rng.choice("RW"), 0, 128))
+        rp = Replayer(arrays_of(tr), 128)
+        for op in tr:
+            if op[0] == "launch" and op[1] == "lib":
+                mode = {"R": D.R, "O": D.W, "RW": D.RW}
+                rp.ctx.launch_library(lambda s: None, "lib", [rp.arr[a] for a, _ in op[2]],
+                                      [mode[m] for _, m in op[2]])
+            else:
+                rp.run([op])
+        verts, edges = rp.dag()
+        o = odag.build_dag(tr)
+        assert [(v[0], v[1], v[2], v[3]) for v in verts] == [(v[0], v[2], v[3], v[4]) for v in o.vertices]
+        assert edges == o.edges
+
+
+def test_library_call_errors():
+    ctx = D.Context(backend="record", record_dag=True)
+    a = ctx.register("a", 0x1000, 64)
+    with pytest.raises(D.DagrtError) as e:
+        ctx.launch_library(lambda s: None, "f", [a], [7])
+    assert e.value.status == D.EINVAL
+    ctx.launch_library(lambda s: None, "f", [a], [D.RW])
+    with pytest.raises(D.DagrtError):  # a library-call name is not a launchable kernel
+        ctx.launch("f", 1, 32)

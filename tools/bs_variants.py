@@ -27,7 +27,8 @@ def main():
                         ("bs_l4b2", 2), ("bs_l2b3", 3), ("bs_l2b4", 4), ("bs_l1b4", 4),
                         ("bs_l3b2", 2), ("bs_l3b3", 3), ("bs_l8b1", 1),
                         ("bs2_p3w2b2", 2), ("bs2_p2w2b3", 3), ("bs2_p2w4b2", 2), ("bs2_p4w2b2", 2),
-                        ("bs2_p1w2b4", 4)):
+                        ("bs2_p1w2b4", 4), ("bs2t_o4s4b2", 2), ("bs2t_o4s3b3", 3), ("bs2t_o2s4b4", 4),
+                        ("bs2t_o6s3b2", 2)):
         if sel and name not in sel:
             continue
         for grid_mult in (1, 2, 4):

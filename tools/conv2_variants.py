@@ -85,9 +85,10 @@ def main():
             L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
             L = ctx.prepare(v, G2TC, 128, args, smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
-        elif v == "conv2_ws":
-            from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
-            L = ctx.prepare(v, 148, CONV2_WS_THREADS, args, smem=CONV2_WS_SMEM)
+        elif v.startswith("conv2_ws"):
+            from paper_2012_09646_b200.programs.hits_dl import conv2_ws_launch
+            th, sm = conv2_ws_launch(v)
+            L = ctx.prepare(v, 148, th, args, smem=sm)
         elif v == "conv2":  # the product launch configuration (programs/hits_dl.py)
             from paper_2012_09646_b200.programs.hits_dl import CONV2_GRID, CONV2_SMEM, CONV2_THREADS
             L = ctx.prepare(v, CONV2_GRID, CONV2_THREADS, args, smem=CONV2_SMEM)

@@ -48,7 +48,12 @@ def main():
         p.load_inputs(0)
         p.run()
         ctx.sync()
-        Ls = {"conv2": p.L[4]}
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
+        a = p.a
+        (_, _), (h2, w2), _ = p.shapes
+        Ls = {"conv2": p.L[4],
+              "conv2_ws": ctx.prepare("conv2_ws", 148, CONV2_WS_THREADS, [a["px"], a["w2"], a["c2x"], h2, w2],
+                                      smem=CONV2_WS_SMEM)}
     else:
         raise SystemExit(f"unknown {what}")
     for k in (names or list(Ls)):
