@@ -52,7 +52,7 @@ sys.path.insert(0, ROOT)
 from paper_2012_09646_b200 import measure, replicas  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-ORDER = ["vec", "bs", "img", "ml", "hits", "dl"]
+ORDER = ["vec", "bs", "img", "ml", "hits", "dl", "bs_f32"]
 HEADLINE = "bs"
 UNIT = "ms per DAG"
 METRIC = "end-to-end ms per DAG (resident inputs; job aggregate over GPUs)"
@@ -65,12 +65,15 @@ FULL = {
     "ml": dict(n=10_000_000),
     "hits": dict(n=20_000_000, e=60_000_000),
     "dl": dict(h=16384, w=16384),
+    "bs_f32": dict(n=10_000_000, dtype="f32"),  # the B&S DAG in fp32 (HBM-bound)
 }
-DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv2"}
+# the kernel whose roofline heads each line (the DAG's largest serial time share)
+DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1",
+            "bs_f32": "bs_f32"}
 # device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
-KSYM = {"square": "k_square", "bs": "k_bs_l3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv",
-        "conv1": "k_conv1_r2b3", "conv2": "k_conv2_tmang"}
-DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32"}
+KSYM = {"square": "k_square", "bs": "k_bs2t_o6s3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv",
+        "conv1": "k_conv1_r2b3", "conv2": "k_conv2_h", "bs_f32": "k_bs_f32"}
+DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32", "bs_f32": "f32"}
 WORKLOAD = {
     "vec": "VEC: 2 squares + sum of differences, N=1M fp32",
     "bs": "B&S: 10 independent Black-Scholes kernels, N=10M fp64 options each",
@@ -78,6 +81,7 @@ WORKLOAD = {
     "ml": "ML: Naive Bayes + Ridge Regression ensemble, 10M x 200",
     "hits": "HITS: 10 iterations CSR SpMV hub/authority, 20M-vertex power-law graph",
     "dl": "DL: two-branch CNN + dense merge, 2 x 16384x16384 fp32",
+    "bs_f32": "B&S in fp32 (f4 variant): 10 independent kernels, N=10M fp32 options each",
 }
 
 SMS = 148
@@ -85,7 +89,7 @@ SMS = 148
 # dynamic instruction counts, profiles/) and the FP64 pipe's peak per SM per
 # clock (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained;
 # confirmed by the DFMA probe: 63.3 ops/clk/SM, profiles/r1_box_peaks.json).
-BS_FP64_OPS_PER_OPTION = 46
+BS_FP64_OPS_PER_OPTION = 39  # k_bs2t_o6s3b2 main loop: 234 DFMA+DMUL+DADD per 6 options (cuobjdump)
 FP64_OPS_PER_SM_CLK = 64
 
 
@@ -171,7 +175,7 @@ def make_program(name, ctx, mode, share=None, size=None):
     from paper_2012_09646_b200.programs import PROGRAMS
     kw = dict(FULL[name] if size is None else size)
     kw.pop("e", None) if name != "hits" else None
-    return PROGRAMS[name](ctx, mode=mode, share=share, **kw)
+    return PROGRAMS[name.split("_")[0]](ctx, mode=mode, share=share, **kw)
 
 
 def time_steps(fn, steps, warmup, dist, prep=None):
@@ -241,7 +245,7 @@ def cpu_oracle_rate(name, budget_s=10.0):
 def _cpu_oracle_rate(name, budget_s):
     import synth
     cores = 1
-    if name == "bs":
+    if name in ("bs", "bs_f32"):
         from oracle import bs as obs
         n = FULL["bs"]["n"]
         chunk = 1_000_000
@@ -404,11 +408,38 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
     sctx = D.Context(device=local, policy="serial")
     sprog = make_program(name, sctx, "resident", share=prog)
     res["serial_resident_ms"] = time_steps(sprog.run, K, W, dist) / K
-    sctx.profile(dom, True)
+    # every kernel of the DAG alone on the GPU (serial policy), event-timed
+    # per launch on its stream: the per-kernel roofline table
+    knames = []
+    for L in prog.launch_sequence():
+        if L.kernel.name not in knames:
+            knames.append(L.kernel.name)
+    for kn in knames:
+        sctx.profile(kn, True)
     time_steps(sprog.run, K, 0, dist)
-    sctx.profile(dom, False)
-    n_alone, sum_alone, busy_alone = sctx.profile_collect(dom)
+    alone = {}
+    for kn in knames:
+        sctx.profile(kn, False)
+        alone[kn] = sctx.profile_collect(kn)
     sctx.close()
+    labels = list(kb.values())
+    bytes_of = {}
+    for L, nb in zip(prog.launch_sequence(), labels):
+        bytes_of.setdefault(L.kernel.name, []).append(nb)
+    kernel_rooflines = []
+    for kn in knames:
+        n_l, s_ms, _ = alone[kn]
+        per_b = sum(bytes_of[kn]) / len(bytes_of[kn])
+        avg = s_ms / max(1, n_l)
+        ach = per_b / (avg * 1e-3) / 1e9 if avg > 0 else None
+        kernel_rooflines.append({"kernel": kn, "launches_per_dag": len(bytes_of[kn]), "avg_launch_ms": avg,
+                                 "algorithmic_bytes_per_launch": per_b, "achieved_gbs": ach,
+                                 "hbm_frac": ach / peak if ach else None,
+                                 "share_of_serial_dag": s_ms / max(1e-9, sum(a[1] for a in alone.values()))})
+    kernel_rooflines.sort(key=lambda r: -r["share_of_serial_dag"])
+    if dom not in alone:
+        dom = kernel_rooflines[0]["kernel"]
+    n_alone, sum_alone, busy_alone = alone[dom]
     if full_report:
         g = prog.graph()
         res["graph_resident_ms"] = time_steps(g.run, K, W, dist) / K
@@ -461,15 +492,26 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
     per_launch = sum(v for k, v in kb.items() if k.startswith(dom)) / max(1, sum(1 for k in kb if k.startswith(dom)))
     avg_alone = sum_alone / max(1, n_alone)
     if name == "bs":
-        unit_work = BS_FP64_OPS_PER_OPTION * prog.n / 1e9  # G fp64 ops per launch
+        # B&S is bound by whichever floor is higher: HBM (16 B/option) or the
+        # FP64 pipe (BS_FP64_OPS_PER_OPTION ops/option); both are reported
         fpeak = FP64_OPS_PER_SM_CLK * SMS * mhz * 1e6 / 1e9
-        ach = unit_work / (avg_alone * 1e-3) if avg_alone > 0 else None
-        roof = {"kernel": dom, "bound": "alu", "pipe": "fp64", "achieved": ach, "peak": fpeak,
-                "unit": "G fp64 ops/s", "frac": ach / fpeak if ach else None,
-                "peak_source": f"{FP64_OPS_PER_SM_CLK} fp64 ops/clk/SM (ncu peak_sustained; DFMA probe "
-                               f"63.3) x {SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
-                "hbm_achieved_gbs": per_launch / (avg_alone * 1e-3) / 1e9 if avg_alone > 0 else None}
+        ops = BS_FP64_OPS_PER_OPTION * prog.n / 1e9  # G fp64 ops per launch
+        hbm_ach = per_launch / (avg_alone * 1e-3) / 1e9 if avg_alone > 0 else None
+        fp64_ach = ops / (avg_alone * 1e-3) if avg_alone > 0 else None
+        hbm_floor, fp64_floor = per_launch / (peak * 1e9), ops / fpeak
+        fp64_info = {"pipe": "fp64", "fp64_achieved": fp64_ach, "fp64_peak": fpeak, "fp64_unit": "G fp64 ops/s",
+                     "fp64_frac": fp64_ach / fpeak if fp64_ach else None,
+                     "fp64_ops_per_option": BS_FP64_OPS_PER_OPTION,
+                     "fp64_peak_source": f"{FP64_OPS_PER_SM_CLK} fp64 ops/clk/SM (ncu peak_sustained; DFMA probe "
+                                         f"63.3) x {SMS} SMs x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+        if hbm_floor >= fp64_floor:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": hbm_ach, "peak": peak, "unit": "GB/s",
+                    "frac": hbm_ach / peak if hbm_ach else None,
+                    "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)", **fp64_info}
+        else:
+            roof = {"kernel": dom, "bound": "alu", "achieved": fp64_ach, "peak": fpeak, "unit": "G fp64 ops/s",
+                    "frac": fp64_ach / fpeak if fp64_ach else None, **fp64_info,
+                    "hbm_achieved_gbs": hbm_ach}
     else:
         ach = per_launch / (avg_alone * 1e-3) / 1e9 if avg_alone > 0 else None
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
@@ -485,7 +527,7 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
                                                (BS_FP64_OPS_PER_OPTION * prog.n * n_dag / (busy_dag * 1e-3) / 1e9
                                                 if busy_dag > 0 else None)),
                             "profiled_region_ms_per_step": ms_prof / K}})
-    tr, tr_src = load_traffic(name, KSYM[dom])
+    tr, tr_src = load_traffic(name, KSYM.get(dom, "k_" + dom))
     if tr is not None:
         roof["traffic"] = tr
         roof["traffic_source"] = tr_src
@@ -503,6 +545,7 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
                                 "K steps back to back, inputs host-newer every step"},
         "gpu_launches": st["launches"],
         "roofline": roof,
+        "kernel_rooflines": kernel_rooflines,
         "dag_roofline": {"R_cp_ms": r_cp, "R_work_ms": r_work, "frac_cp": r_cp / per,
                          "frac_work": r_work / per, "frac_bound": max(r_cp, r_work) / per,
                          "peak_gbs": peak,

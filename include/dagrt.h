@@ -147,6 +147,33 @@ int32_t dagrt_builtin_count(void);
 const char* dagrt_builtin_name(int32_t i);
 const char* dagrt_builtin_signature(int32_t i);
 
+/* History-driven launch configuration (the scheduler keeps
+ * "historical information" about computations, L502-504, and the paper names
+ * the automatic choice of launch parameters as future work, L1502-1504 /
+ * Fig. 7).  Registers n candidate configurations for kernel k;
+ * afterwards a dagrt_launch of k with grid = {0, 0, 0} ("auto") takes one of
+ * them: while exploring, the candidates are used in turn, `trials` times
+ * each, every such launch bracketed by timing events on its own stream; the
+ * timings are collected without blocking at later host synchronisations, and
+ * once every candidate has `trials` samples the one with the lowest median
+ * time is used from then on.  History is kept per (kernel, key), key = a hash
+ * of the launch's scalar arguments (the problem size), so each size is tuned
+ * on its own.  The DAG does not depend on it (launch configurations take no
+ * part in dependency inference).  With the graph cache on, exploration is
+ * suspended (auto launches use the best configuration known so far, else the
+ * first candidate).  Candidates are copied; n <= 16, trials >= 1. */
+typedef struct {
+  dagrt_dim3 grid, block;
+  uint32_t smem;
+} dagrt_launch_config;
+dagrt_status dagrt_kernel_autotune(dagrt_ctx ctx, dagrt_kernel k, const dagrt_launch_config* candidates, int32_t n,
+                                   int32_t trials);
+/* History of kernel k for the scalar-argument key of its LAST auto launch:
+ * *chosen = index of the selected candidate (-1 while exploring), ms[i] = the
+ * median time of candidate i so far (-1 if unsampled), *n: capacity in, count
+ * out. */
+dagrt_status dagrt_autotune_state(dagrt_ctx ctx, dagrt_kernel k, int32_t* chosen, double* ms, int32_t* n);
+
 /* ---------------------------------------------------------------- launch */
 
 /* Launch kernel k with `nargs` arguments (count and kinds must match the

@@ -1880,12 +1880,13 @@ static const char* v_conv2_tc(const LaunchCheck& L, unsigned threads, unsigned s
   if (L.smem < smem_min) return "dynamic shared memory below the kernel's layout";
   return nullptr;
 }
-static const char* v_conv2_product(const LaunchCheck& L) {
+static const char* v_conv2_tman(const LaunchCheck& L) {
   return v_conv2_tc(L, 384, (unsigned)tmang_smem<3, 1>());
 }
 
 static const Builtin kConvTc[] = {
-    // product: TMA-gathered A, three consumer groups with one TMA stage each
+    // round-1 product (now "conv2_tman3x1"; the product is k_conv2_h in kernels_conv2.cu):
+    // TMA-gathered A, three consumer groups with one TMA stage each
     // (k_conv2_tmang<3,1> = "conv2_tman3x1": 285 us per branch; 148 CTAs of 384
     // threads, tmang_smem<3,1>() bytes, tensor map built by the pre-launch
     // hook); two groups x two stages (k_conv2_tma2n<1,0> = "conv2_tman1") 303-320 us.  Before it: the first version with its gathers two
@@ -1896,8 +1897,7 @@ static const Builtin kConvTc[] = {
     // us for the cp.async-ring versions, whose loop-top barrier waits on the
     // ring dominate, and 467 us for the CUDA-core kernel (tools/conv2_variants.py,
     // profiles/).  launch: 2 x 148 CTAs of 128 threads, kTcSmem bytes
-    {"conv2", (const void*)k_conv2_tmang<3, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
-     tmang_smem<3, 1>(), conv2_tma_prelaunch, v_conv2_product},
+
     // ring + two A buffers, 384 threads (148 CTAs, kC3Smem)
     {"conv2_tc5", (const void*)k_conv2_tc5, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kC3Smem},
@@ -1915,7 +1915,7 @@ static const Builtin kConvTc[] = {
      tma2g_smem<1>(), conv2_tma_prelaunch},
     // NG groups x SG stages (128 NG threads, 148 CTAs)
     {"conv2_tman3x1", (const void*)k_conv2_tmang<3, 1>, "const ptr, const ptr, out ptr, sint32, sint32",
-     KF_NONE, tmang_smem<3, 1>(), conv2_tma_prelaunch},
+     KF_NONE, tmang_smem<3, 1>(), conv2_tma_prelaunch, v_conv2_tman},
     // ... and one accumulator pair per input row of the window (6 chains of 3 MMAs)
     {"conv2_tmanr1", (const void*)k_conv2_tma2n<1, 1>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      tma2g_smem<1>(), conv2_tma_prelaunch},

@@ -465,6 +465,43 @@ BS2T_VARIANT(k_bs2t_o4s3b3, 4, 3, 3)
 BS2T_VARIANT(k_bs2t_o2s4b4, 2, 4, 4)
 BS2T_VARIANT(k_bs2t_o6s3b2, 6, 3, 2)
 
+// ---------------------------------------------------------------- B&S in fp32 (f4)
+// The same pricing (A&S 26.2.17 CND) in fp32 storage and
+// arithmetic: 8 bytes per option instead of 16 and no FP64 pipe, so the kernel
+// is HBM-bound ("fp32 B&S variant, HBM-bound instead of
+// FP64-bound").  Accuracy is fp32's (checked against the fp64 oracle with the
+// north_star's fp32 criterion, 1e-4 |o| + 1e-4 rms(o)).  4 options per thread
+// with 128-bit loads/stores, grid-stride.
+__device__ __forceinline__ float bs_price_f32(float s, float r, float v, float t, float k) {
+  const float vst = v * sqrtf(t);
+  const float d1 = (logf(s / k) + (r + 0.5f * v * v) * t) / vst;
+  const float d2 = d1 - vst;
+  auto cnd = [](float d) {
+    const float kk = 1.f / fmaf(0.2316419f, fabsf(d), 1.f);
+    const float p = 0.39894228040143268f * expf(-0.5f * d * d) * kk *
+                    fmaf(kk, fmaf(kk, fmaf(kk, fmaf(kk, 1.330274429f, -1.821255978f), 1.781477937f), -0.356563782f),
+                         0.31938153f);
+    return d > 0.f ? 1.f - p : p;
+  };
+  return s * cnd(d1) - k * expf(-r * t) * cnd(d2);
+}
+__global__ void __launch_bounds__(256) k_bs_f32(const float* __restrict__ s, float* __restrict__ c, long long n,
+                                                float r, float v, float t, float k) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long done = 0;
+  if (aligned16(s) && aligned16(c)) {
+    const long long n4 = n >> 2;
+    for (long long i = tid; i < n4; i += nth) {
+      const float4 x = ldg_stream(reinterpret_cast<const float4*>(s) + i);
+      reinterpret_cast<float4*>(c)[i] = make_float4(bs_price_f32(x.x, r, v, t, k), bs_price_f32(x.y, r, v, t, k),
+                                                    bs_price_f32(x.z, r, v, t, k), bs_price_f32(x.w, r, v, t, k));
+    }
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nth) c[i] = bs_price_f32(s[i], r, v, t, k);
+}
+
 // K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores.
 // PAIRS double2 per thread per iteration (independent chains for the FP64
 // pipe to interleave); the next group's loads are issued before pricing.
@@ -702,6 +739,10 @@ static const char* v_reduce_diff(const LaunchCheck& L) {
   if (!fits(L, 0, 4 * n) || !fits(L, 1, 4 * n)) return "inputs need 4 n bytes";
   return check_reduction(L, 2);
 }
+static const char* v_bs_f32(const LaunchCheck& L) {
+  const uint64_t n = (uint64_t)L.i(2);
+  return fits(L, 0, 4 * n) && fits(L, 1, 4 * n) ? nullptr : "prices and calls need 4 n bytes";
+}
 static const char* v_bs(const LaunchCheck& L) {
   const uint64_t n = (uint64_t)L.i(2);
   if (!fits(L, 0, 8 * n) || !fits(L, 1, 8 * n)) return "prices and calls need 8 n bytes";
@@ -714,7 +755,15 @@ static const Builtin kVecBs[] = {
     // product: lean loop, 3 pairs per thread, 2 CTAs/SM, one wave (44.8 us per
     // 10M options vs 46.2 for 4 pairs (k_bs_l4b2) in three back-to-back runs,
     // 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
-    {"bs", (const void*)k_bs_l3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, 0, nullptr, v_bs},
+    // product (round 2): 38-39 FP64 ops per option (algebraic pricer), inputs
+    // streamed by cp.async.bulk into a 3-stage ring, 6 options per thread in
+    // lockstep, 2 CTAs/SM one wave: 40.5 us per 10M options vs 45.8 for the
+    // round-1 product (bs_l3b2) in the same run (tools/bs_variants.py)
+    {"bs", (const void*)k_bs2t_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, 0,
+     nullptr, v_bs},
+    // f4: the same pricing in fp32 (HBM-bound)
+    {"bs_f32", (const void*)k_bs_f32, "const ptr, out ptr, sint64, float, float, float, float", KF_NONE, 0, nullptr,
+     v_bs_f32},
     {"bs_p4", (const void*)k_bs, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a3b4", (const void*)k_bs_a3b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs_a5b4", (const void*)k_bs_a5b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},

@@ -634,6 +634,23 @@ struct KernelRec {
   bool coop;
   bool prof = false;
   bool lib = false;  // pseudo-kernel of library-call vertices (dagrt_launch_library)
+  std::vector<dagrt_launch_config> cands;  // history-driven launch configuration (f3)
+  int32_t trials = 0;
+};
+
+// Per (kernel, scalar-argument key) launch history of an auto-configured kernel.
+struct TuneRec {
+  uint32_t kernel;
+  uint64_t key;
+  std::vector<std::vector<float>> ms;  // samples per candidate
+  int32_t next = 0;                    // round-robin cursor while exploring
+  int32_t chosen = -1;
+};
+struct TunePending {
+  size_t rec;
+  int32_t cand;
+  void* ev0;
+  void* ev1;
 };
 
 struct ProfRec {
@@ -726,6 +743,11 @@ struct dagrt_ctx_s {
   uint32_t read_seq = 0;
   std::vector<dagrt_graph_s*> graphs;
   std::vector<ProfRec> prof;           // timed launches awaiting collection
+  std::vector<TuneRec> tune;           // launch-configuration history (f3)
+  std::vector<TunePending> tune_pending;
+  int64_t tune_last = -1;              // TuneRec of the last auto launch
+  int64_t tune_req_rec = -1;           // the launch being enqueued is an exploration sample of
+  int32_t tune_req_cand = -1;          //   (TuneRec, candidate): do_launch brackets it with events
   bool timeline = false;
   std::vector<TimeRec> tl;             // timeline records awaiting export
   std::vector<void*> tev_pool;         // free timing events
@@ -819,6 +841,48 @@ dagrt_status get_timing_event(dagrt_ctx c, void** ev) {
   return DAGRT_OK;
 }
 
+float median_of(std::vector<float> v) {
+  std::sort(v.begin(), v.end());
+  return v.empty() ? -1.f : v[v.size() / 2];
+}
+
+// Collect the finished timings of exploring auto launches (non-blocking:
+// cudaEventQuery), and decide a configuration once every candidate has its
+// trials.
+void tune_collect(dagrt_ctx c) {
+  if (c->tune_pending.empty()) return;
+  std::vector<TunePending> keep;
+  for (const TunePending& t : c->tune_pending) {
+    float ms = 0.f;
+    bool done = true;
+    if (c->be->real()) {
+      cudaError_t q = cudaEventQuery((cudaEvent_t)t.ev1);
+      if (q == cudaErrorNotReady) {
+        keep.push_back(t);
+        continue;
+      }
+      cudaGetLastError();
+      done = q == cudaSuccess && cudaEventElapsedTime(&ms, (cudaEvent_t)t.ev0, (cudaEvent_t)t.ev1) == cudaSuccess;
+      cudaGetLastError();
+    }
+    if (done) c->tune[t.rec].ms[t.cand].push_back(ms);
+    c->tev_pool.push_back(t.ev0);
+    c->tev_pool.push_back(t.ev1);
+  }
+  c->tune_pending.swap(keep);
+  for (TuneRec& r : c->tune) {
+    if (r.chosen >= 0) continue;
+    const KernelRec& k = c->kernels[r.kernel];
+    bool all = true;
+    for (const auto& v : r.ms) all = all && (int32_t)v.size() >= k.trials;
+    if (!all) continue;
+    int32_t best = 0;
+    for (size_t i = 1; i < r.ms.size(); ++i)
+      if (median_of(r.ms[i]) < median_of(r.ms[best])) best = (int32_t)i;
+    r.chosen = best;
+  }
+}
+
 // The one place kernels are enqueued; optionally bracketed by timing events
 // on the launching stream (dagrt_profile_enable).
 // Timeline bracket (dagrt_timeline_enable): opens before an item on stream s.
@@ -849,9 +913,20 @@ dagrt_status do_launch(dagrt_ctx c, const KernelRec* k, uint32_t kh, dim3 g, dim
     if (dagrt_status st = get_timing_event(c, &e1)) return st;
     CK(c->be->record(e0, s), "cudaEventRecord profile");
   }
+  void *u0 = nullptr, *u1 = nullptr;
+  if (c->tune_req_rec >= 0) {  // exploration sample of an auto-configured launch (f3)
+    if (dagrt_status st = get_timing_event(c, &u0)) return st;
+    if (dagrt_status st = get_timing_event(c, &u1)) return st;
+    CK(c->be->record(u0, s), "cudaEventRecord autotune");
+  }
   if (dagrt_status st = tl_begin(c, s, &t0)) return st;
   CK(c->be->launch(k->fn, g, b, argv, smem, s, k->coop, k->nparams + (k->pre ? 1 : 0)), "cudaLaunchKernel");
   if (dagrt_status st = tl_end(c, s, t0, 0, sidx, vertex, kh, 0)) return st;
+  if (u0) {
+    CK(c->be->record(u1, s), "cudaEventRecord autotune");
+    c->tune_pending.push_back(TunePending{(size_t)c->tune_req_rec, c->tune_req_cand, u0, u1});
+    c->tune_req_rec = -1;
+  }
   if (k->prof) {
     CK(c->be->record(e1, s), "cudaEventRecord profile");
     c->prof.push_back(ProfRec{kh, e0, e1});
@@ -1012,6 +1087,7 @@ dagrt_status host_sync_parents(dagrt_ctx c, ArrayRec* a, bool write, void* order
   for (uint32_t p : c->scratch_parents) retire(c, p);
   if (write) { a->readers.clear(); a->last_writer = -1; }
   recycle(c);
+  tune_collect(c);
   return DAGRT_OK;
 }
 
@@ -1421,13 +1497,97 @@ dagrt_status dagrt_launch(dagrt_ctx c, dagrt_kernel kh, dagrt_dim3 grid, dagrt_d
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
   if (k->lib) return fail(c, DAGRT_EINVAL, "%s is a library-call name, not a kernel", k->name.c_str());
+  if (grid.x == 0 && grid.y == 0 && grid.z == 0) {  // auto configuration (f3)
+    if (k->cands.empty()) return fail(c, DAGRT_EINVAL, "kernel %s: auto grid without dagrt_kernel_autotune", k->name.c_str());
+    if (nargs != k->nparams || (nargs > 0 && !args)) return fail(c, DAGRT_ESIG, "kernel %s: argument count", k->name.c_str());
+    uint64_t key = 0xcbf29ce484222325ull ^ kh;
+    for (int i = 0; i < nargs; ++i)
+      if (!is_ptr(k->kind[i])) key = (key ^ (uint64_t)args[i].i64) * 0x100000001b3ull;
+    size_t r = 0;
+    while (r < c->tune.size() && !(c->tune[r].kernel == kh && c->tune[r].key == key)) ++r;
+    if (r == c->tune.size()) {
+      TuneRec tr;
+      tr.kernel = kh;
+      tr.key = key;
+      tr.ms.resize(k->cands.size());
+      c->tune.push_back(tr);
+    }
+    tune_collect(c);
+    TuneRec& tr = c->tune[r];
+    c->tune_last = (int64_t)r;
+    int32_t pick = tr.chosen;
+    if (pick < 0) {
+      if (c->be->active()) {  // graph cache on: no exploration (timing events are not replayable)
+        pick = 0;
+      } else {
+        // next candidate still short of samples (launched or pending)
+        const int32_t nc = (int32_t)k->cands.size();
+        for (int32_t tries = 0; tries < nc; ++tries) {
+          const int32_t cand = (tr.next + tries) % nc;
+          int32_t have = (int32_t)tr.ms[cand].size();
+          for (const TunePending& tp : c->tune_pending) have += tp.rec == r && tp.cand == cand;
+          if (have < k->trials) { pick = cand; break; }
+        }
+        if (pick < 0) pick = tr.next % nc;  // all sampled, awaiting collection
+        tr.next = (pick + 1) % nc;
+        c->tune_req_rec = (int64_t)r;
+        c->tune_req_cand = pick;
+      }
+    }
+    const dagrt_launch_config& cf = k->cands[pick];
+    grid = cf.grid;
+    block = cf.block;
+    smem = cf.smem;
+  }
   uint64_t vals[kMaxArgs + 1];
   void* argv[kMaxArgs + 1];
   ArrayRec* arrs[kMaxArgs];
   if (dagrt_status s = marshal(c, *k, args, nargs, vals, argv, arrs, dim3(grid.x, grid.y, grid.z),
                                dim3(block.x, block.y, block.z), smem))
     return s;
-  return launch_vertex(c, k, kh, grid, block, smem, argv, arrs, k->kind, nargs, nullptr, nullptr, t0);
+  const dagrt_status st = launch_vertex(c, k, kh, grid, block, smem, argv, arrs, k->kind, nargs, nullptr, nullptr, t0);
+  c->tune_req_rec = -1;
+  return st;
+}
+
+dagrt_status dagrt_kernel_autotune(dagrt_ctx c, dagrt_kernel kh, const dagrt_launch_config* cands, int32_t n,
+                                   int32_t trials) {
+  GUARD(c);
+  KernelRec* k;
+  if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  if (n < 1 || n > 16 || !cands || trials < 1) return fail(c, DAGRT_EINVAL, "autotune: 1..16 candidates, trials >= 1");
+  k->cands.assign(cands, cands + n);
+  k->trials = trials;
+  for (size_t i = 0; i < c->tune.size(); ++i)  // a new candidate list restarts this kernel's history
+    if (c->tune[i].kernel == kh) {
+      c->tune[i].ms.assign((size_t)n, {});
+      c->tune[i].chosen = -1;
+      c->tune[i].next = 0;
+    }
+  std::vector<TunePending> keep;
+  for (const TunePending& t : c->tune_pending)
+    if (c->tune[t.rec].kernel != kh) keep.push_back(t);
+  c->tune_pending.swap(keep);
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_autotune_state(dagrt_ctx c, dagrt_kernel kh, int32_t* chosen, double* ms, int32_t* n) {
+  GUARD(c);
+  if (!chosen || !n) return fail(c, DAGRT_EINVAL, "null out");
+  tune_collect(c);
+  int64_t r = -1;
+  for (size_t i = 0; i < c->tune.size(); ++i)
+    if (c->tune[i].kernel == kh && (r < 0 || (int64_t)i == c->tune_last)) r = (int64_t)i;
+  if (r < 0) return fail(c, DAGRT_ENOTFOUND, "no auto launch of kernel %u yet", kh);
+  const TuneRec& tr = c->tune[r];
+  *chosen = tr.chosen;
+  const int32_t cap = *n;
+  *n = (int32_t)tr.ms.size();
+  if (ms) {
+    if (cap < *n) return fail(c, DAGRT_EINVAL, "capacity");
+    for (int32_t i = 0; i < *n; ++i) ms[i] = tr.ms[i].empty() ? -1.0 : (double)median_of(tr.ms[i]);
+  }
+  return DAGRT_OK;
 }
 
 dagrt_status dagrt_launch_library(dagrt_ctx c, dagrt_library_fn fn, void* user, const char* name,
@@ -1764,6 +1924,7 @@ dagrt_status dagrt_sync(dagrt_ctx c) {
   c->st.host_syncs++;
   retire_all(c);
   recycle(c);
+  tune_collect(c);
   for (size_t i = 1; i < c->arrays.size(); ++i) c->arrays[i].h2d_pending = false;
   return DAGRT_OK;
 }

@@ -40,6 +40,10 @@ class Dim3(C.Structure):
     _fields_ = [("x", C.c_uint32), ("y", C.c_uint32), ("z", C.c_uint32)]
 
 
+class LaunchConfig(C.Structure):
+    _fields_ = [("grid", Dim3), ("block", Dim3), ("smem", C.c_uint32)]
+
+
 class Arg(C.Union):
     _fields_ = [("array", C.c_uint64), ("i32", C.c_int32), ("i64", C.c_int64),
                 ("f32", C.c_float), ("f64", C.c_double)]
@@ -177,6 +181,8 @@ def builtins():
 
 
 def dim3(v):
+    if isinstance(v, str) and v == "auto":  # history-driven launch configuration (dagrt_kernel_autotune)
+        return Dim3(0, 0, 0)
     if isinstance(v, int):
         return Dim3(v, 1, 1)
     v = tuple(v) + (1, 1)
@@ -419,6 +425,31 @@ class Context:
 
     def launch(self, kernel, grid, block, *args, smem=0):
         self.prepare(kernel, grid, block, args, smem)()
+
+    def autotune(self, kernel, candidates, trials=3):
+        """Candidate (grid, block, smem) configurations for launches of
+        `kernel` with grid "auto" (dagrt_kernel_autotune)."""
+        k = self.kernel(kernel) if isinstance(kernel, str) else kernel
+        arr = (LaunchConfig * len(candidates))()
+        for i, cand in enumerate(candidates):
+            g, b = cand[0], cand[1]
+            sm = cand[2] if len(cand) > 2 else 0
+            arr[i] = LaunchConfig(dim3(g), dim3(b), sm)
+        L = lib()
+        L.dagrt_kernel_autotune.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_int32, C.c_int32]
+        L.dagrt_kernel_autotune.restype = C.c_int32
+        self._check(L.dagrt_kernel_autotune(self._c, k.handle, C.addressof(arr), len(candidates), trials))
+
+    def autotune_state(self, kernel):
+        """(chosen candidate or -1, [median ms per candidate or -1])."""
+        k = self.kernel(kernel) if isinstance(kernel, str) else kernel
+        L = lib()
+        L.dagrt_autotune_state.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dagrt_autotune_state.restype = C.c_int32
+        ch, n = C.c_int32(), C.c_int32(16)
+        ms = (C.c_double * 16)()
+        self._check(L.dagrt_autotune_state(self._c, k.handle, C.byref(ch), ms, C.byref(n)))
+        return ch.value, list(ms[:n.value])
 
     LIBFN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p)
 

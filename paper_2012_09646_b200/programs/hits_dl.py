@@ -22,21 +22,33 @@ CONV2_TMAR_SMEM = 1024 + 12 * 3 * 4096 + 2 * 9 * 4096 + 2 * 9 * 512 + 256
 CONV2_TMAR_THREADS = 288
 # product "conv2" = conv2_tman3x1 (TMA-gathered A, three consumer groups with one
 # TMA stage each, 3xTF32 in two MMA chains); csrc/kernels_conv_tc.cu tmang_smem<3, 1>
-CONV2_GRID, CONV2_THREADS = 148, 384
-CONV2_SMEM = 1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64
+CONV2_TMAN_THREADS = 384  # round-1 product, now the variant "conv2_tman3x1"
+CONV2_TMAN_SMEM = 1024 + 3 * 9 * 4096 + 3 * 9 * 4096 + 2 * 9 * 512 + 64
 G2TC = 2 * 148                                    # persistent tcgen05 CTAs (2 per SM)
 # warp-specialised conv2 (csrc/kernels_conv2.cu c2ws::Cfg<S, NB, SW>): S TMA
 # stages, NB TMEM buffers, SW split warps -> (threads, dynamic shared memory)
 CONV2_WS_CFG = {"conv2_ws": (4, 2, 4), "conv2_ws6": (6, 2, 4), "conv2_ws6s8": (6, 2, 8),
                 "conv2_ws6b3": (6, 3, 4), "conv2_ws5s8b3": (5, 3, 8)}
+# row-staged conv2 (c2rows::Cfg<R, NB, SW>): R input-row slots of 8704 B
+CONV2_ROWS_CFG = {"conv2_rows": (12, 2, 8), "conv2_rows_s4": (12, 2, 4), "conv2_rows_r20": (20, 2, 8)}
+# one-MMA-per-tap fp16-split conv2 (c2h::Cfg<R, NB, SW>): B is 9 x 1 KB as in c2ws
+CONV2_H_CFG = {"conv2_h": (12, 3, 4), "conv2_h_s8": (12, 3, 8), "conv2_h_b4": (16, 4, 4), "conv2_h_s12": (12, 3, 12),
+               "conv2_h_s8b2": (12, 2, 8), "conv2_h_s8r16": (16, 3, 8)}
 
 
 def conv2_ws_launch(name):
+    if name in CONV2_ROWS_CFG or name in CONV2_H_CFG:
+        r, nb, sw = CONV2_ROWS_CFG.get(name) or CONV2_H_CFG[name]
+        return 32 * (6 + sw), 1024 + r * 8704 + 9 * 1024 + 8 * (2 * r + 3 * nb) + 16
     s, nb, sw = CONV2_WS_CFG[name]
     return 32 * (6 + sw), 1024 + s * 9 * 4096 + 9 * 1024 + 8 * (2 * s + 3 * nb) + 16
 
 
 CONV2_WS_THREADS, CONV2_WS_SMEM = conv2_ws_launch("conv2_ws")
+# product "conv2" = k_conv2_h<12, 3, 12> (csrc/kernels_conv2.cu): 148 persistent CTAs
+CONV2_H_CFG["conv2"] = (12, 3, 12)
+CONV2_GRID = 148
+CONV2_THREADS, CONV2_SMEM = conv2_ws_launch("conv2")
 CONV2_TC5_SMEM = 2 * 9 * 512 + 3 * 3 * 4 * 129 * 16 + 2 * 2 * 9 * 4096 + 64  # kC3Smem (conv2_tc5, 384 thr, 148 CTAs)
 HITS_ITERS = 10          # reading; parity unpinned (constant)
 SPMV_TILE = 32 * 8       # merge items per warp tile (csrc/kernels_hits.cu)
@@ -330,7 +342,8 @@ class DeepLearning(Program):
         self.alloc("wd", max(1, nz), torch.float32)
         for b in ("x", "y"):
             self.alloc(f"c1{b}", max(1, h1 * w1 * 8), torch.float32)
-            self.alloc(f"p{b}", max(1, h2 * w2 * 8), torch.float32)
+            # + 8 floats: a row-staged conv2 reads one pixel past the last row when W2 is odd
+            self.alloc(f"p{b}", h2 * w2 * 8 + 8, torch.float32)
             self.alloc(f"c2{b}", max(1, h3 * w3 * 16), torch.float32)
         self.alloc("z", max(1, nz), torch.float32)
         self.alloc_red("r")

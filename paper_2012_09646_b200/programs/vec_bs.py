@@ -65,23 +65,38 @@ class BlackScholes(Program):
     """10 independent pricing kernels (L865-870); host reads each price vector."""
     name = "bs"
 
-    def __init__(self, ctx, n=10_000_000, nvec=synth.BS_NVEC, **kw):
+    def __init__(self, ctx, n=10_000_000, nvec=synth.BS_NVEC, dtype="f64", **kw):
         super().__init__(ctx, **kw)
-        self.n, self.nvec = n, nvec
+        self.n, self.nvec, self.dtype = n, nvec, dtype
         stream = self.mode == "stream"
+        tdt = torch.float64 if dtype == "f64" else torch.float32
         for i in range(nvec):
-            self.alloc(f"s{i}", n, torch.float64, mirror=stream)
-            self.alloc(f"c{i}", n, torch.float64, mirror=stream)
+            self.alloc(f"s{i}", n, tdt, mirror=stream)
+            self.alloc(f"c{i}", n, tdt, mirror=stream)
         self.inputs = [f"s{i}" for i in range(nvec)]
         self.sinks = [f"c{i}" for i in range(nvec)]
-        g = grid_1d(n, 256, 8, waves=2)  # one wave of the 2 resident CTAs/SM
-        self.L = [ctx.prepare("bs", g, 256, [self.a[f"s{i}"], self.a[f"c{i}"], n,
-                                              BS_R, BS_V, BS_T, BS_K]) for i in range(nvec)]
+        if dtype == "f64":
+            g = grid_1d(n, 256, 8, waves=2)  # one wave of the 2 resident CTAs/SM
+            kname = "bs"
+        else:  # f4: fp32 storage and arithmetic (HBM-bound)
+            g = grid_1d(n, 256, 4, waves=8)
+            kname = "bs_f32"
+        self.L = [ctx.prepare(kname, g, 256, [self.a[f"s{i}"], self.a[f"c{i}"], n,
+                                               BS_R, BS_V, BS_T, BS_K]) for i in range(nvec)]
 
     def _inputs(self, set_index=0):
         spec = synth.spec_bs(self.n, self.nvec)
         for i in range(self.nvec):
-            self.fill(f"s{i}", spec[f"s{i}"], set_index)
+            if self.dtype == "f64":
+                self.fill(f"s{i}", spec[f"s{i}"], set_index)
+            elif not self.record:  # the same draws, rounded to fp32 (the oracle prices the rounded values)
+                sp = (spec[f"s{i}"][0], spec[f"s{i}"][1], spec[f"s{i}"][2])
+                tmp = torch.empty(self.n, dtype=torch.float64, device=self.device)
+                import synth.gpu as sg
+                sg.fill_tensor(tmp, self.seed + set_index, f"s{i}", sp)
+                self.t[f"s{i}"].copy_(tmp)
+                if f"s{i}" in self.mirror:
+                    self.mirror[f"s{i}"].copy_(self.t[f"s{i}"])
 
     def graph(self):
         g = self.ctx.graph()
@@ -93,4 +108,5 @@ class BlackScholes(Program):
         return g
 
     def kernel_bytes(self):
-        return {f"bs{i}": 16 * self.n for i in range(self.nvec)}
+        per = 16 if self.dtype == "f64" else 8
+        return {f"bs{i}": per * self.n for i in range(self.nvec)}

@@ -29,6 +29,7 @@ pytestmark = pytest.mark.gpu
 SMALL = {
     "vec": lambda c, m: Vec(c, n=100_003, mode=m),
     "bs": lambda c, m: BlackScholes(c, n=40_009, mode=m),
+    "bs_f32": lambda c, m: BlackScholes(c, n=40_009, mode=m, dtype="f32"),
     "img": lambda c, m: Images(c, h=300, w=517, mode=m),
     "ml": lambda c, m: MLEnsemble(c, n=20_011, mode=m),
     "hits": lambda c, m: Hits(c, n=50_000, e=150_000, iters=3, mode=m),
@@ -121,7 +122,9 @@ def test_dl_4096_elementwise():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("kernel", ["conv2_ws", "conv2_ws6", "conv2_ws6s8", "conv2_ws6b3", "conv2_ws5s8b3"])
+@pytest.mark.parametrize("kernel", ["conv2_ws", "conv2_ws6", "conv2_ws6s8", "conv2_ws6b3", "conv2_ws5s8b3",
+                                    "conv2_rows", "conv2_rows_s4", "conv2_rows_r20", "conv2_h", "conv2_h_s8",
+                                    "conv2_h_b4"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517), (1030, 2050), (4096, 4096)])
 def test_conv2_ws_matches_oracle(h, w, kernel):
     """The warp-specialised conv2 (A_lo in TMEM; csrc/kernels_conv2.cu) against
@@ -302,4 +305,24 @@ def test_library_call_vertex_on_the_gpu():
     verts, edges = c.dag()
     assert [v[2] for v in verts[:3]] == ["square", "matmul", "square"]
     assert {(p, ch) for p, ch, _ in edges} == {(0, 1), (1, 2), (2, 3)}
+    c.close()
+
+
+# ------------------------------------------------------------------ f3: history-driven launch configuration
+def test_autotune_picks_the_faster_configuration():
+    """Auto-configured B&S launches explore a 2-CTA and a full-GPU grid, then
+    keep the faster (the full one, ~100x); prices equal the oracle's under
+    every configuration tried."""
+    n = 2_000_003
+    c = D.Context(device=0)
+    p = BlackScholes(c, n=n, nvec=1)
+    p.load_inputs(0)
+    c.autotune("bs", [(2, 256), (296, 256)], trials=2)
+    for _ in range(6):
+        c.launch("bs", "auto", 0, p.a["s0"], p.a["c0"], n, obs.R, obs.V, obs.T, obs.K)
+        c.sync()
+    chosen, ms = c.autotune_state("bs")
+    assert chosen == 1 and ms[0] > 5 * ms[1], (chosen, ms)
+    from oracle_checks import check_bs
+    check_bs(p, p.seed)
     c.close()

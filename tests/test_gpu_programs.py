@@ -399,8 +399,8 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
         ctx.launch(variant, 2 * 148, 128, p.a["px"], p.a["w2"], o_arr, h2, w2s,
                    smem=2 * 9 * 512 + 2 * 9 * 4096 + 64)
     elif variant == "conv2_tman3x1":
-        from paper_2012_09646_b200.programs.hits_dl import CONV2_SMEM
-        ctx.launch(variant, 148, 384, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_SMEM)
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAN_SMEM
+        ctx.launch(variant, 148, 384, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TMAN_SMEM)
     elif variant == "conv2_tmar":
         from paper_2012_09646_b200.programs.hits_dl import CONV2_TMAR_SMEM, CONV2_TMAR_THREADS
         ctx.launch(variant, 148, CONV2_TMAR_THREADS, p.a["px"], p.a["w2"], o_arr, h2, w2s, smem=CONV2_TMAR_SMEM)

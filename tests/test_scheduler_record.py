@@ -455,3 +455,27 @@ def test_library_call_errors():
     ctx.launch_library(lambda s: None, "f", [a], [D.RW])
     with pytest.raises(D.DagrtError):  # a library-call name is not a launchable kernel
         ctx.launch("f", 1, 32)
+
+
+def test_history_driven_launch_configuration_record():
+    """f3: auto-configured launches cycle
+    through the candidates `trials` times each, then settle on the fastest
+    (ties -> the first: the recorder times everything as 0); histories are
+    per scalar-argument key; the DAG is the one of fixed-config launches."""
+    ctx = D.Context(backend="record", record_dag=True)
+    a = _reg(ctx, "a", 4096)
+    b = _reg(ctx, "b", 4096)
+    ctx.autotune("square", [(1, 256), (2, 128), (4, 64)], trials=2)
+    for _ in range(8):
+        ctx.launch("square", "auto", 0, a, b, 1000)
+        ctx.sync()
+    chosen, ms = ctx.autotune_state("square")
+    assert chosen == 0 and ms == [0.0, 0.0, 0.0]
+    trace = [t for t in ctx.trace() if t[0] == "launch"]
+    assert len(trace) == 8
+    ctx.launch("square", "auto", 0, a, b, 500)  # another size: a fresh history
+    assert ctx.autotune_state("square")[0] == -1
+    verts, edges = ctx.dag()
+    assert [v[2] for v in verts] == ["square"] * 9 and edges == set()
+    with pytest.raises(D.DagrtError):
+        ctx.launch("reduce_diff", "auto", 0, a, a, b, 10)  # no candidates registered

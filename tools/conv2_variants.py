@@ -85,7 +85,7 @@ def main():
             L = ctx.prepare(v, 148, 384, args, smem=CONV2_TC5_SMEM)
         elif v == "conv2_tc4":
             L = ctx.prepare(v, G2TC, 128, args, smem=2 * 9 * 512 + 4 * 3 * 4 * 129 * 16 + 2 * 9 * 4096 + 64)
-        elif v.startswith("conv2_ws"):
+        elif v.startswith("conv2_ws") or v.startswith("conv2_rows") or v.startswith("conv2_h"):
             from paper_2012_09646_b200.programs.hits_dl import conv2_ws_launch
             th, sm = conv2_ws_launch(v)
             L = ctx.prepare(v, 148, th, args, smem=sm)

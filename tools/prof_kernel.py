@@ -48,12 +48,13 @@ def main():
         p.load_inputs(0)
         p.run()
         ctx.sync()
-        from paper_2012_09646_b200.programs.hits_dl import CONV2_WS_SMEM, CONV2_WS_THREADS
+        from paper_2012_09646_b200.programs.hits_dl import CONV2_ROWS_CFG, CONV2_WS_CFG, conv2_ws_launch
         a = p.a
         (_, _), (h2, w2), _ = p.shapes
-        Ls = {"conv2": p.L[4],
-              "conv2_ws": ctx.prepare("conv2_ws", 148, CONV2_WS_THREADS, [a["px"], a["w2"], a["c2x"], h2, w2],
-                                      smem=CONV2_WS_SMEM)}
+        Ls = {"conv2": p.L[4]}
+        for v in list(CONV2_WS_CFG) + list(CONV2_ROWS_CFG):
+            th, sm = conv2_ws_launch(v)
+            Ls[v] = ctx.prepare(v, 148, th, [a["px"], a["w2"], a["c2x"], h2, w2], smem=sm)
     else:
         raise SystemExit(f"unknown {what}")
     for k in (names or list(Ls)):

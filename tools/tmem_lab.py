@@ -31,6 +31,14 @@ def main():
         if err > 1e-5:
             # which permutation of rows/cols would match?
             print("  D[0,:4]", d[0, :4], "ref", ref[0, :4])
+    A16 = rng.standard_normal((128, 64)).astype(np.float16)
+    B16 = rng.standard_normal((16, 64)).astype(np.float16)
+    ref16 = A16.astype(np.float64) @ B16.astype(np.float64).T
+    dA16, dB16 = torch.from_numpy(A16).cuda(), torch.from_numpy(B16).cuda()
+    D = torch.zeros(128 * 16, device="cuda")
+    rc = L.tmem_lab_f16(C.c_void_p(dA16.data_ptr()), C.c_void_p(dB16.data_ptr()), C.c_void_p(D.data_ptr()))
+    d = D.cpu().numpy().reshape(128, 16).astype(np.float64)
+    print(f"kind::f16 A tmem (2 fp16 per column): rc={rc} max rel err {np.abs(d - ref16).max() / np.abs(ref16).max():.3e}")
 
 
 if __name__ == "__main__":
