@@ -398,8 +398,10 @@ def _reg(ctx, name, nbytes, base=[0x10_0000_0000]):
     ("softmax", 10, 256, 0, lambda c: [_reg(c, "x", 4 * 100 * 20), 100, 20], "C <= 16"),
     ("spmv", 10, 256, 0, lambda c: [_reg(c, "rp", 4 * 11), _reg(c, "ci", 40), _reg(c, "pl", 64), _reg(c, "x", 40),
                                     _reg(c, "y", 40), 10], "y needs"),
-    ("conv2", 148, 384, 0, lambda c: [_reg(c, "p", 32 * 64 * 64), _reg(c, "w", 4608), _reg(c, "o", 64 * 32 * 32),
+    ("conv2", 148, 576, 0, lambda c: [_reg(c, "p", 32 * 64 * 64), _reg(c, "w", 4608), _reg(c, "o", 64 * 32 * 32),
                                       64, 64], "shared memory"),
+    ("conv2", 148, 384, 200000, lambda c: [_reg(c, "p", 32 * 64 * 64), _reg(c, "w", 4608), _reg(c, "o", 64 * 32 * 32),
+                                           64, 64], "block size"),
     ("square", 10, 2048, 0, lambda c: [_reg(c, "a", 400), _reg(c, "b", 400), 100], "block of 2048"),
 ], ids=lambda x: x if isinstance(x, str) else None)
 def test_builtin_launch_contracts_reject_bad_launches(case):
