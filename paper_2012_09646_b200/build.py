@@ -1,6 +1,8 @@
 """Build the in-tree native libraries (no JIT cache, no site-packages):
 
-* paper_2012_09646_b200/libdagrt.so  -- scheduler core + sm_100a kernels
+* paper_2012_09646_b200/libdagrt.so  -- scheduler core + sm_100a product kernels
+* paper_2012_09646_b200/libdagrt_exp.so -- experimental kernel variants
+  (csrc/exp/), loaded only on request (dagrt.load_experimental())
 * synth/libsynth.so                  -- GPU twin of the seeded input generator
 
 Every CUDA file is compiled with ``-gencode arch=compute_100a,code=sm_100a
@@ -46,7 +48,7 @@ def _compile(src, obj, includes, extra=()):
     return r.stderr
 
 
-def _lib(name, srcs, headers, includes, out, verbose=False):
+def _lib(name, srcs, headers, includes, out, verbose=False, link=()):
     os.makedirs(BUILD, exist_ok=True)
     objs, jobs = [], []
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
@@ -60,8 +62,9 @@ def _lib(name, srcs, headers, includes, out, verbose=False):
             if verbose and msg.strip():
                 print(msg, file=sys.stderr)
     if _needs(out, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs + \
-              ["-lpthread", "-ldl", "-lrt"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-Xlinker",
+                                 "-soname=" + os.path.basename(out), "-o", out] + objs + \
+              list(link) + ["-lpthread", "-ldl", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed for {out}:\n{r.stderr}")
@@ -74,6 +77,12 @@ def build(verbose=False):
     headers.append(os.path.join(ROOT, "include", "dagrt.h"))
     lib = _lib("dagrt", srcs, headers, [CSRC, os.path.join(ROOT, "include")],
                os.path.join(HERE, "libdagrt.so"), verbose)
+    # experimental variants: their own library over libdagrt.so's registry
+    edir = os.path.join(CSRC, "exp")
+    esrcs = sorted(os.path.join(edir, f) for f in os.listdir(edir) if f.endswith(".cu"))
+    eheaders = headers + [os.path.join(edir, f) for f in os.listdir(edir) if f.endswith(".cuh")]
+    _lib("dagrt_exp", esrcs, eheaders, [CSRC, edir], os.path.join(HERE, "libdagrt_exp.so"), verbose,
+         link=["-L" + HERE, "-ldagrt", "-Xlinker", "-rpath=$ORIGIN"])
     sdir = os.path.join(ROOT, "synth", "csrc")
     ssrcs = [os.path.join(sdir, f) for f in sorted(os.listdir(sdir)) if f.endswith(".cu")]
     slib = _lib("synth", ssrcs, [], [sdir], os.path.join(ROOT, "synth", "libsynth.so"), verbose)

@@ -58,6 +58,16 @@ int register_builtins(const Builtin* table, int n);  // returns n
 int builtin_count();
 const Builtin* builtin_at(int i);
 
+// Built-ins compiled into ANOTHER shared library (the experimental variants,
+// libdagrt_exp.so) live in that library's own (static) CUDA runtime: the
+// scheduler cannot resolve their host stubs itself.  Such a library registers
+// its table with its own resolver, which returns the CUfunction of a stub of
+// that library (cudaGetFuncBySymbol there); the scheduler launches it with
+// cuLaunchKernel and applies the dynamic shared memory opt-in with the driver.
+typedef int (*ResolveFn)(const void* stub, void** cufunc);
+int register_builtins_ext(const Builtin* table, int n, ResolveFn resolve);
+ResolveFn builtin_resolver(const void* stub);  // nullptr: a stub of libdagrt.so itself
+
 // Scheduler-internal kernel (kernels_runtime.cu): small host reads through
 // mapped pinned memory; args (src, dst_mapped_dev, n, flag_dev, seq).
 const void* read_mapped_kernel();

@@ -1,3 +1,7 @@
+// Experimental (libdagrt_exp.so; exp_common.cuh): the round-1 tensor-core
+// conv2 kernels (271-285 us per branch), kept as tested alternatives to the
+// round-2 product (kernels_conv2.cu).  Their notes as written in round 1:
+//
 // DL second convolution on the 5th-generation tensor cores (tcgen05, TMEM).
 //
 // conv2 (§V-B, Fig. 6; reading R-DL) is a real
@@ -29,7 +33,8 @@
 #include <mutex>
 #include <vector>
 
-#include "kcommon.cuh"
+#include "../kcommon.cuh"
+#include "exp_common.cuh"
 
 namespace dagrt {
 
@@ -1940,6 +1945,6 @@ static const Builtin kConvTc[] = {
     {"conv2_tc1", (const void*)k_conv2_tc, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE,
      kTcSmem},
 };
-DAGRT_REGISTER_BUILTINS(kConvTc);
+DAGRT_REGISTER_EXP(kConvTc);
 
 }  // namespace dagrt

@@ -42,9 +42,25 @@ static std::vector<Builtin>& registry() {
   static std::vector<Builtin> r;
   return r;
 }
+static std::vector<std::pair<const void*, ResolveFn>>& resolvers() {
+  static std::vector<std::pair<const void*, ResolveFn>> r;
+  return r;
+}
 int register_builtins(const Builtin* t, int n) {
   for (int i = 0; i < n; ++i) registry().push_back(t[i]);
   return n;
+}
+int register_builtins_ext(const Builtin* t, int n, ResolveFn resolve) {
+  for (int i = 0; i < n; ++i) {
+    registry().push_back(t[i]);
+    resolvers().push_back({t[i].fn, resolve});
+  }
+  return n;
+}
+ResolveFn builtin_resolver(const void* stub) {
+  for (auto& r : resolvers())
+    if (r.first == stub) return r.second;
+  return nullptr;
 }
 int builtin_count() { return (int)registry().size(); }
 const Builtin* builtin_at(int i) {
@@ -98,20 +114,46 @@ struct CudaBackend final : Backend {
   LaunchFn cu_launch = nullptr;
   bool cu_tried = false;
   std::vector<std::pair<const void*, void*>> funcs;  // host stub -> CUfunction
+  typedef int (*FuncAttrFn)(void* f, int attrib, int value);
+  FuncAttrFn cu_func_attr = nullptr;
   void* cufunc(const void* fn) {
     for (auto& p : funcs)
       if (p.first == fn) return p.second;
-    cudaFunction_t f = nullptr;
-    if (cudaGetFuncBySymbol(&f, fn) != cudaSuccess) {
-      cudaGetLastError();
-      f = nullptr;
+    void* f = nullptr;
+    if (ResolveFn rs = builtin_resolver(fn)) {
+      // a stub of another library's CUDA runtime (libdagrt_exp.so): its own
+      // lookup, then the shared memory opt-in through the driver
+      if (rs(fn, &f) != 0) f = nullptr;
+      if (f) {
+        if (!cu_func_attr) {
+          void* p = nullptr;
+          cudaDriverEntryPointQueryResult q;
+          if (cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+              q == cudaDriverEntryPointSuccess)
+            cu_func_attr = (FuncAttrFn)p;
+          cudaGetLastError();
+        }
+        for (int i = 0; i < builtin_count(); ++i)
+          if (builtin_at(i)->fn == fn && builtin_at(i)->smem_max > 0 && cu_func_attr)
+            cu_func_attr(f, 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */, builtin_at(i)->smem_max);
+      }
+    } else {
+      cudaFunction_t cf = nullptr;
+      if (cudaGetFuncBySymbol(&cf, fn) != cudaSuccess) {
+        cudaGetLastError();
+        cf = nullptr;
+      }
+      f = (void*)cf;
     }
-    funcs.push_back({fn, (void*)f});
-    return (void*)f;
+    funcs.push_back({fn, f});
+    return f;
   }
   cudaError_t launch(const void* fn, dim3 g, dim3 b, void** args, size_t smem, void* s,
                      bool coop, int) override {
-    if (coop) return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
+    if (coop) {  // cooperative kernels are product kernels (launched by their own runtime's stub)
+      if (builtin_resolver(fn)) return cudaErrorNotSupported;
+      return cudaLaunchCooperativeKernel(fn, g, b, args, smem, (cudaStream_t)s);
+    }
     if (!cu_tried) {
       cu_tried = true;
       void* p = nullptr;
@@ -123,6 +165,7 @@ struct CudaBackend final : Backend {
         cudaGetLastError();
     }
     void* f = cu_launch ? cufunc(fn) : nullptr;
+    if (!f && builtin_resolver(fn)) return cudaErrorInvalidDeviceFunction;  // not ours to launch by stub
     if (!f) return cudaLaunchKernel(fn, g, b, args, smem, (cudaStream_t)s);
     int r = cu_launch(f, g.x, g.y, g.z, b.x, b.y, b.z, (unsigned)smem, s, args, nullptr);
     // CUresult and cudaError_t share their numeric codes for launch failures
@@ -1278,6 +1321,22 @@ dagrt_status lookup_kernel(dagrt_ctx c, dagrt_kernel k, KernelRec** out) {
 }  // namespace
 
 // =================================================================== C ABI
+// A context's record of built-in b (handles 0..n-1 at creation; built-ins a
+// library registers later -- libdagrt_exp.so -- are appended on lookup).
+static dagrt_status add_builtin(dagrt_ctx c, const Builtin* b) {
+  KernelRec k;
+  k.name = b->name;
+  k.fn = b->fn;
+  k.coop = (b->flags & KF_COOPERATIVE) != 0;
+  k.pre = b->prelaunch;
+  k.validate = b->validate;
+  if (b->smem_max > 0 && c->be->real() && b->fn && !builtin_resolver(b->fn))
+    cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
+  if (parse_signature(b->signature, &k) != DAGRT_OK) return DAGRT_ESIG;
+  c->kernels.push_back(k);
+  return DAGRT_OK;
+}
+
 extern "C" {
 
 dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
@@ -1302,21 +1361,11 @@ dagrt_status dagrt_create(int device, const dagrt_config* cfg, dagrt_ctx* out) {
   c->arrays.resize(1);
   // built-in kernels are pre-registered (handles 0..n-1)
   for (int i = 0; i < builtin_count(); ++i) {
-    const Builtin* b = builtin_at(i);
-    KernelRec k;
-    k.name = b->name;
-    k.fn = b->fn;
-    k.coop = (b->flags & KF_COOPERATIVE) != 0;
-    k.pre = b->prelaunch;
-    k.validate = b->validate;
-    if (b->smem_max > 0 && c->be->real() && b->fn)
-      cudaFuncSetAttribute(b->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b->smem_max);
-    if (parse_signature(b->signature, &k) != DAGRT_OK) {
+    if (add_builtin(c, builtin_at(i)) != DAGRT_OK) {
       delete c->be;
       delete c;
       return DAGRT_ESIG;
     }
-    c->kernels.push_back(k);
   }
   if (ensure_streams(c) != DAGRT_OK) {
     delete c->be;
@@ -1449,6 +1498,12 @@ dagrt_status dagrt_kernel_lookup(dagrt_ctx c, const char* name, dagrt_kernel* ou
   for (size_t i = c->kernels.size(); i-- > 0;)
     if (c->kernels[i].name == name) {
       *out = (dagrt_kernel)i;
+      return DAGRT_OK;
+    }
+  for (int i = 0; i < builtin_count(); ++i)  // registered after the context was created
+    if (std::strcmp(builtin_at(i)->name, name) == 0) {
+      if (dagrt_status s = add_builtin(c, builtin_at(i))) return fail(c, s, "bad signature of '%s'", name);
+      *out = (dagrt_kernel)(c->kernels.size() - 1);
       return DAGRT_OK;
     }
   return fail(c, DAGRT_ENOTFOUND, "no kernel named '%s'", name);
@@ -2136,6 +2191,8 @@ dagrt_status dagrt_graph_add_kernel(dagrt_ctx c, dagrt_graph g, dagrt_kernel kh,
   if (!g || !node) return fail(c, DAGRT_EINVAL, "null graph/node");
   KernelRec* k;
   if (dagrt_status s = lookup_kernel(c, kh, &k)) return s;
+  if (builtin_resolver(k->fn))
+    return fail(c, DAGRT_EINVAL, "experimental built-ins (libdagrt_exp.so) are not graph nodes");
   uint64_t vals[kMaxArgs + 1];
   void* argv[kMaxArgs + 1];
   ArrayRec* arrs[kMaxArgs];

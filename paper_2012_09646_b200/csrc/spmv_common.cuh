@@ -1,0 +1,155 @@
+// SpMV building blocks shared by the product kernel (kernels_hits.cu) and
+// its experimental variants (exp/spmv_variants.cu): the cross-warp
+// workspace and deposit protocols that make rows spanning several warps
+// bit-reproducible, and the streamed column loads of the non-zero split.
+#pragma once
+#include "kcommon.cuh"
+
+namespace dagrt {
+
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvWarps = kSpmvThreads / 32;
+constexpr int kSpmvItems = 8;                 // merge items per lane
+constexpr int kSpmvTile = 32 * kSpmvItems;    // merge items per warp tile
+
+// Cross-warp workspace, one slot per participant (global warp of the grid).
+struct SpmvWs {
+  float* part;    // [G] share of the row crossing the warp range's end
+  float* head;    // [G] share of the row crossing the range's start (its end part)
+  unsigned* cnt;  // [G] arrival counters, indexed by the row's first participant
+};
+
+__device__ __forceinline__ SpmvWs spmv_ws(float* y, long long n, long long ncta) {
+  uintptr_t base = (uintptr_t)(y + n);
+  base = (base + 15) & ~(uintptr_t)15;
+  SpmvWs w;
+  w.part = reinterpret_cast<float*>(base);
+  w.head = w.part + ncta;
+  w.cnt = reinterpret_cast<unsigned*>(w.head + ncta);
+  return w;
+}
+
+// Merge-path coordinate of diagonal d: rows consumed i (row-end items) and
+// non-zeros consumed j = d - i.  Row-end i precedes nnz j iff row_ptr[i+1] <= j.
+// Executed by one full warp; 32-ary search.
+__device__ __forceinline__ long long warp_merge_search(const int* __restrict__ row_ptr, long long N,
+                                                       long long E, long long d) {
+  const int lane = threadIdx.x & 31;
+  long long lo = d - E > 0 ? d - E : 0;
+  long long hi = d < N ? d : N;
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long p = lo + lane * step;
+    bool pred = false;
+    if (p < hi) pred = (long long)__ldg(row_ptr + p + 1) <= d - p - 1;
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    const int cnt = __popc(b);  // predicate holds on a prefix of the probes
+    const long long nlo = cnt > 0 ? lo + (long long)(cnt - 1) * step + 1 : lo;
+    const long long nhi = min(hi, lo + (long long)cnt * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  const long long p = lo + lane;
+  bool pred = false;
+  if (p < hi) pred = (long long)__ldg(row_ptr + p + 1) <= d - p - 1;
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  return lo + __popc(b);
+}
+
+// Sum v[first..last] (fixed order: lane-strided partial sums, fixed tree) by one warp.
+__device__ __forceinline__ float warp_ordered_sum(const volatile float* v, long long first,
+                                                  long long last) {
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  for (long long k = first + lane; k <= last; k += 32) s += v[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// Deposit `val` for row r (spanning CTAs cs..ce) and finish the row if last.
+// Executed by one whole warp.  `is_head` = this participant holds the row's end (ce).
+__device__ __forceinline__ void spmv_deposit(const SpmvWs& ws, float* y, long long r, long long cs,
+                                             long long ce, long long c, float val, bool is_head) {
+  const int lane = threadIdx.x & 31;
+  unsigned old = 0;
+  if (lane == 0) {
+    if (is_head) ws.head[c] = val;
+    else ws.part[c] = val;
+    __threadfence();
+    old = atomicAdd(ws.cnt + cs, 1u);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == (unsigned)(ce - cs)) {  // last of the (ce - cs + 1) participants
+    __threadfence();
+    float s = warp_ordered_sum(ws.part, cs, ce - 1);
+    if (lane == 0) {
+      s += ((volatile float*)ws.head)[ce];
+      y[r] = s;
+      ws.cnt[cs] = 0;  // reusable by the next launch
+    }
+  }
+}
+
+// Single-thread deposit protocol (spmv_nz): participant c puts its share of
+// a row spanning warps cs..ce (the end participant into head[], the others
+// into part[]); the last to arrive at cnt[cs] adds them in warp order.
+__device__ __forceinline__ void spmv_ws_put(const SpmvWs& ws, long long c, float val, bool is_end) {
+  if (is_end) ws.head[c] = val;
+  else ws.part[c] = val;
+}
+__device__ __forceinline__ bool spmv_ws_arrive(const SpmvWs& ws, long long cs, long long ce) {
+  __threadfence();
+  const unsigned old = atomicAdd(ws.cnt + cs, 1u);
+  if (old != (unsigned)(ce - cs)) return false;
+  __threadfence();
+  ws.cnt[cs] = 0;  // reusable by the next launch
+  return true;
+}
+__device__ __forceinline__ float spmv_ws_sum(const SpmvWs& ws, long long cs, long long ce) {
+  float s = 0.f;
+  const volatile float* p = ws.part;
+  for (long long c = cs; c < ce; ++c) s += p[c];
+  return s + ((volatile float*)ws.head)[ce];
+}
+
+constexpr int kNzChunk = 128;  // non-zeros per warp chunk (4 per lane)
+constexpr int kNzHeader = 16;  // plan header ints
+
+__device__ __forceinline__ int4 ld_cols_stream(const int* p, uint64_t pol) {
+  int4 c;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(p), "l"(pol));
+  return c;
+}
+
+// One chunk's streamed inputs for one lane: its 4 column indices, and the
+// chunk's 4 row-start flag words (the same 16 bytes for every lane: one
+// broadcast load).  The flag words are used only when the chunk is reduced,
+// so their latency is covered by the pipeline like the columns'.
+struct NzIn {
+  int c[4];
+  uint4 fw;
+};
+
+__device__ __forceinline__ void nz_gather(const NzIn& in, const float* __restrict__ x, float (&v)[4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = in.c[u] >= 0 ? __ldg(x + in.c[u]) : 0.f;
+}
+
+// launch contract of the plan-driven kernels (builtin.h LaunchCheck)
+static inline const char* v_spmv_plan_kernel(const LaunchCheck& L) {  // row_ptr, col, plan, x, y, N
+  const int64_t N = L.i(5);
+  if (N < 0 || N >= (1ll << 31)) return "need 0 <= N < 2^31";
+  if (!fits(L, 0, 4ull * (N + 1))) return "row_ptr needs 4 (N + 1) bytes";
+  if (!fits(L, 2, 4ull * kNzHeader)) return "plan smaller than its header";
+  if (!fits(L, 3, 4ull * N)) return "x needs 4 N bytes";
+  if (L.block[0] % 32 || L.block[1] != 1 || L.block[2] != 1 || L.grid[1] != 1 || L.grid[2] != 1)
+    return "1-D launch, block a multiple of 32";
+  // y carries the cross-warp workspace: 16-byte aligned after N floats, 3 words per warp
+  if (!fits(L, 4, 4ull * N + 16 + 12ull * (L.block[0] / 32) * L.grid[0]))
+    return "y needs 4 N + 16 + 12 (warps of the grid) bytes";
+  return nullptr;
+}
+
+}  // namespace dagrt

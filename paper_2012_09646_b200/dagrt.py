@@ -174,6 +174,24 @@ def lib():
     return L
 
 
+EXP_LIBPATH = os.path.join(HERE, "libdagrt_exp.so")
+_exp = None
+
+
+def load_experimental():
+    """Load libdagrt_exp.so (csrc/exp/): the measured-but-not-shipped kernel
+    variants (round-1 kernels, tuning shapes) register into the built-in
+    registry; contexts find them by name (dagrt_kernel_lookup).  Tests and
+    tools only -- the product path never loads it."""
+    global _exp
+    if _exp is None:
+        lib()  # the registry lives in libdagrt.so, the exp library's dependency
+        if not os.path.exists(EXP_LIBPATH):
+            raise ImportError(f"{EXP_LIBPATH} not built: run `python -m paper_2012_09646_b200.build`")
+        _exp = C.CDLL(EXP_LIBPATH)
+    return _exp
+
+
 def builtins():
     L = lib()
     return [(L.dagrt_builtin_name(i).decode(), L.dagrt_builtin_signature(i).decode())

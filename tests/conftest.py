@@ -28,3 +28,11 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture
+def exp():
+    """The experimental kernel variants (csrc/exp/ -> libdagrt_exp.so): loaded
+    only by the tests that compare them with the product kernels."""
+    from paper_2012_09646_b200 import dagrt as D
+    return D.load_experimental()

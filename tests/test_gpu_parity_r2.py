@@ -126,7 +126,7 @@ def test_dl_4096_elementwise():
                                     "conv2_rows", "conv2_rows_s4", "conv2_rows_r20", "conv2_h", "conv2_h_s8",
                                     "conv2_h_b4"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517), (1030, 2050), (4096, 4096)])
-def test_conv2_ws_matches_oracle(h, w, kernel):
+def test_conv2_ws_matches_oracle(exp, h, w, kernel):
     """The warp-specialised conv2 (A_lo in TMEM; csrc/kernels_conv2.cu) against
     the oracle's conv on the pooled input, from one tile to ~14 tiles per CTA
     (every stage / TMEM buffer / barrier phase reused many times), ragged
@@ -223,7 +223,7 @@ def test_bs_limits(svals):
 
 
 @pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2", "bs2t_o4s4b2", "bs2t_o6s3b2"])
-def test_bs_kernels_limits_and_range(kernel):
+def test_bs_kernels_limits_and_range(exp, kernel):
     """Every B&S pricing kernel on the limit values plus a dense S sweep over
     [1e-3, 1e4] (log-spaced): deep out of / in the money, d ~ 0, the exp's
     underflow clamp; 1e-10 relative + 1e-12 absolute."""

@@ -382,7 +382,7 @@ def test_dl_full_size_sampled(ctx):
                                      "conv2_tc5", "conv2_tma0", "conv2_tma1", "conv2_tmag0", "conv2_tmag1",
                                      "conv2_tman1", "conv2_tmanr1", "conv2_tmar", "conv2_tman3x1"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
-def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
+def test_dl_conv2_variants_match_oracle(ctx, exp, h, w, variant):
     """The other conv2 kernels (CUDA-core FFMA; the tcgen05 versions with a
     cp.async ring) against the oracle too."""
     p = DeepLearning(ctx, h=h, w=w)
@@ -435,7 +435,7 @@ def test_dl_conv2_variants_match_oracle(ctx, h, w, variant):
 @pytest.mark.parametrize("variant", ["conv1_b1", "conv1_b3", "conv1_b4", "conv1_b4cs", "conv1_r2b3cs",
                                      "conv1_r2b2"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517)])
-def test_dl_conv1_variants_bitwise(ctx, h, w, variant):
+def test_dl_conv1_variants_bitwise(ctx, exp, h, w, variant):
     """Every conv1 variant (one or two output rows per iteration, store
     policies, register caps) gives the product kernel's output bit for bit
     (same arithmetic in the same order) -- the product is checked against the
@@ -457,7 +457,7 @@ def test_dl_conv1_variants_bitwise(ctx, h, w, variant):
 
 
 @pytest.mark.parametrize("h,w", [(515, 517)])
-def test_tensor_core_truncates_fp32_to_tf32(ctx, h, w):
+def test_tensor_core_truncates_fp32_to_tf32(ctx, exp, h, w):
     """Pins the hardware behaviour the product conv2 relies on: kind::tf32
     MMAs read an fp32 operand by TRUNCATING it to tf32.  conv2_tma1 (raw TMA
     box as A_hi, lo = x - trunc(x)) matches the oracle (test above) while
@@ -483,7 +483,7 @@ def test_tensor_core_truncates_fp32_to_tf32(ctx, h, w):
 
 
 @pytest.mark.parametrize("variant", ["spmv_sync", "spmv_as1", "spmv_x0s1", "spmv_x1s1"])
-def test_spmv_merge_variants_bitwise(ctx, variant):
+def test_spmv_merge_variants_bitwise(ctx, exp, variant):
     """The merge-path SpMV (previous default) and its variants (gathers in
     registers instead of cp.async; other L2 policies) give bit-identical y,
     and match the oracle."""
@@ -511,7 +511,7 @@ def test_spmv_merge_variants_bitwise(ctx, variant):
 
 @pytest.mark.parametrize("n,e,seed", [(1, 0, 1), (1000, 0, 2), (5000, 200_000, 3), (300_000, 900_000, 11),
                                       (50_000, 2_000_000, 5)])
-def test_spmv_plan_classes(ctx, n, e, seed):
+def test_spmv_plan_classes(ctx, exp, n, e, seed):
     """Row-class SpMV (alternative kernel) on graphs whose rows fall in every
     class (short, medium, long, multi-chunk hubs), run twice (the arrival
     counters must reset): matches the oracle and is bit-reproducible."""

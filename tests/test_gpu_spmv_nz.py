@@ -72,7 +72,7 @@ def run_nz(ctx, rp, ci, x, grid, tag, kernel="spmv"):
 @pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("grid", [1, 7, 148 * 6])
-def test_spmv_nz_edge_shapes(ctx, case, grid, kernel):
+def test_spmv_nz_edge_shapes(ctx, exp, case, grid, kernel):
     deg, ncols = CASES[case]
     rp, ci = csr_from_degrees(deg, ncols, 1)
     n = len(deg)
@@ -86,7 +86,7 @@ def test_spmv_nz_edge_shapes(ctx, case, grid, kernel):
 
 @pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
 @pytest.mark.parametrize("n,e,seed", [(10, 30, 1), (5000, 15000, 3), (300_000, 900_000, 11)])
-def test_spmv_nz_powerlaw(ctx, n, e, seed, kernel):
+def test_spmv_nz_powerlaw(ctx, exp, n, e, seed, kernel):
     rp, ci, _, _ = synth.powerlaw_graph(seed, n, e, device="auto")
     x = np.random.default_rng(seed).random(n).astype(np.float32)
     for grid in (3, 148 * 6):

@@ -187,7 +187,7 @@ def test_graph_cache_replays_identical_results(mode):
                                      "bs2_p1w2b4", "bs2t_o4s4b2", "bs2t_o4s3b3", "bs2t_o2s4b4", "bs2t_o6s3b2"])
 # 227_333: an odd number of full groups for the lean 4-pair loop (ping-pong tail)
 @pytest.mark.parametrize("n", [3, 200_001, 227_333])
-def test_bs_variants_match_oracle(ctx, variant, n):
+def test_bs_variants_match_oracle(ctx, exp, variant, n):
     """Every B&S tuning variant (register or cp.async prefetch depths) prices
     like the oracle on ragged sizes, in a grid that strides several times."""
     s = torch.empty(n, dtype=torch.float64, device="cuda")

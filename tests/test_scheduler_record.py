@@ -6,6 +6,8 @@ import ctypes as C
 import itertools
 import random
 
+import os
+
 import pytest
 
 from golden_io import all_cases
@@ -241,6 +243,36 @@ def test_all_symbols_exported():
     missing = [n for n in sorted(names) if not hasattr(L, n)]
     assert not missing, missing
     assert len(names) >= 30
+
+
+PRODUCT_BUILTINS = {
+    "square", "reduce_diff", "bs", "bs_f32",                                          # VEC, B&S
+    "blur", "sobel", "maximum", "minimum", "extend", "unsharpen", "combine",          # IMG
+    "norm", "nb_mmul", "rr_mmul", "rowmax", "lse", "exp_sub", "addv", "softmax", "argmax",  # ML
+    "spmv", "l2norm", "divide",                                                       # HITS
+    "conv1", "pool", "conv2", "concat", "dot",                                        # DL
+    "axpb", "peak_dfma", "peak_ffma",                                                 # runtime tests, peaks
+}
+
+
+def test_product_library_holds_only_product_kernels():
+    """libdagrt.so registers exactly the product kernels; the measured variants
+    come only with libdagrt_exp.so, which adds names without shadowing any
+    product kernel, and a context created before it was loaded finds them."""
+    import subprocess
+    import sys
+    code = ("from paper_2012_09646_b200 import dagrt as D\n"
+            "p = [n for n, _ in D.builtins()]\n"
+            "ctx = D.Context(backend='record')\n"
+            "D.load_experimental()\n"
+            "e = [n for n, _ in D.builtins()][len(p):]\n"
+            "ctx.kernel('bs2t_o4s4b2'); ctx.kernel('spmv_merge'); ctx.kernel('conv2_ws')\n"
+            "print(repr((p, e)))\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    prod, extra = eval(out.stdout.strip().splitlines()[-1])
+    assert set(prod) == PRODUCT_BUILTINS and len(prod) == len(PRODUCT_BUILTINS)
+    assert extra and not (set(extra) & PRODUCT_BUILTINS) and len(set(extra)) == len(extra)
 
 
 @pytest.mark.parametrize("idx", range(0, len(CASES), max(1, len(CASES) // 6)))

@@ -11,6 +11,7 @@ def main():
     import synth
     import synth.gpu as sg
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     n = 10_000_000
     ctx = D.Context(device=0)
     s = torch.empty(n, dtype=torch.float64, device="cuda")

@@ -1,15 +1,16 @@
 // Pipeline trace of the warp-specialised conv2 (tools only): compiles the
-// product kernel file with its trace points on and records the SM clock of
+// experimental kernel file with its trace points on and records the SM clock of
 // CTA 0 at every hand-off of its first 64 tiles.
 #include <cstdint>
 __device__ long long g_c2trace[10 * 64];
 #define C2_TRACE_ON 1
 #include "../paper_2012_09646_b200/csrc/kernels_conv2.cu"
-namespace dagrt {
-int register_builtins(const Builtin*, int n) { return n; }  // standalone: no registry
-int conv2_tma_prelaunch(const uint64_t* vals, int nargs, void** extra);
+#include "../paper_2012_09646_b200/csrc/exp/conv2_variants.cu"
+namespace dagrt {  // standalone: no registry
+int register_builtins(const Builtin*, int n) { return n; }
+int register_builtins_ext(const Builtin*, int n, ResolveFn) { return n; }
 }
-#include "../paper_2012_09646_b200/csrc/kernels_conv_tc.cu"
+#include "../paper_2012_09646_b200/csrc/exp/conv2_tc_variants.cu"
 
 extern "C" int conv2_trace(const float* in, const float* w, float* out, int H2, int W2, long long* host_trace) {
   using namespace dagrt;

@@ -20,6 +20,7 @@ def main():
     a = ap.parse_args()
     import torch
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     from paper_2012_09646_b200.programs import DeepLearning
     from paper_2012_09646_b200.programs.hits_dl import CONV2_TC5_SMEM, CONV2_TC_SMEM, CONV2_TC_THREADS, G2TC
     ctx = D.Context(device=0)

@@ -14,6 +14,8 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 from oracle import dl as odl  # noqa: E402
 from paper_2012_09646_b200 import dagrt as D  # noqa: E402
+
+D.load_experimental()  # conv1/conv2 variants live in libdagrt_exp.so
 from paper_2012_09646_b200.programs import DeepLearning  # noqa: E402
 from paper_2012_09646_b200.programs.hits_dl import G2TC  # noqa: E402
 

@@ -14,6 +14,7 @@ def main():
     import synth
     import synth.gpu as sg
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     what = sys.argv[1]
     names = sys.argv[2:]
     ctx = D.Context(device=0)

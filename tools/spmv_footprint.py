@@ -19,6 +19,7 @@ def main():
     import torch
     import synth
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     from paper_2012_09646_b200.programs.hits_dl import spmv_out_bytes, spmv_plan
     n, e = 20_000_000, 60_000_000
     rp, ci, _, _ = synth.powerlaw_graph(synth.BASE_SEED, n, e)

@@ -84,6 +84,7 @@ def main():
                                                          out.data_ptr(), E, gg, 10)
     # the SpMV kernels on the same graph, through the C ABI
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     from paper_2012_09646_b200.programs.hits_dl import spmv_nz_grid, spmv_nz_plan, spmv_out_bytes, spmv_pad_plan
     ctx = D.Context(device=0)
     ob, grid = spmv_out_bytes(n, E)

@@ -14,6 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     import torch
     from paper_2012_09646_b200 import dagrt as D
+    D.load_experimental()  # the variants live in libdagrt_exp.so
     from paper_2012_09646_b200.programs import Hits
     ctx = D.Context(device=0)
     p = Hits(ctx)
