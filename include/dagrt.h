@@ -143,6 +143,9 @@ dagrt_status dagrt_kernel_lookup(dagrt_ctx ctx, const char* name, dagrt_kernel* 
  * 3 mutable ptr (prefetched), 4 out ptr, 5 float, 6 double.
  * *n: capacity in, count out. */
 dagrt_status dagrt_kernel_signature(dagrt_ctx ctx, dagrt_kernel k, int32_t* kinds, int32_t* n);
+/* Name of kernel handle k (built-in, registered or library-call pseudo-kernel);
+ * NULL if k is not a handle of ctx.  Owned by the context. */
+const char* dagrt_kernel_name(dagrt_ctx ctx, dagrt_kernel k);
 int32_t dagrt_builtin_count(void);
 const char* dagrt_builtin_name(int32_t i);
 const char* dagrt_builtin_signature(int32_t i);
@@ -389,6 +392,89 @@ dagrt_status dagrt_graph_instantiate(dagrt_ctx ctx, dagrt_graph g);
 /* Launch the instantiated graph on the context's graph stream and wait for it. */
 dagrt_status dagrt_graph_run(dagrt_ctx ctx, dagrt_graph g, int32_t wait);
 dagrt_status dagrt_graph_destroy(dagrt_ctx ctx, dagrt_graph g);
+
+/* ---------------------------------------------------------------- multi-GPU placement (f2)
+ *
+ * The paper's future work (L1499-1502: "compute data location and migration
+ * costs at run time" to use several GPUs).  A multi-context drives one
+ * dagrt_ctx per SLOT (a CUDA device; the same device may back several slots,
+ * which is how a one-GPU box exercises the cross-slot path) from ONE host
+ * thread.  Every launch is a vertex of the DAG of the slot it is PLACED on;
+ * the per-slot schedulers infer dependencies, streams and events as for a
+ * single GPU.  Arrays are multi-arrays: a home copy (caller-owned), replicas
+ * on other slots (allocated by the library on first use, freed by
+ * dagrt_multi_destroy) and an optional pinned host mirror, with a validity
+ * set over {slots, host}.  A launch on slot d whose read arguments are not
+ * valid on d first migrates them, as library-call vertices (dagrt_launch_library):
+ *   slot -> slot: "migrate_pre" on d (mode W: waits d's users of the old
+ *     replica, records an event), "migrate_out" on the source slot (mode R:
+ *     after the last writer there, waits that event, cudaMemcpyPeerAsync over
+ *     NVLink / NVSwitch, records a second event) and "migrate_in" on d (mode W:
+ *     waits it) -- so later writers on the source wait for the copy, and
+ *     readers on d for its completion: a cross-device edge is a peer copy
+ *     plus cross-device events, no collective;
+ *   host -> slot: "upload" on d (mode W: cudaMemcpyAsync from the mirror).
+ * A kernel's writes leave only the replica it wrote valid.
+ *
+ * Placement: DAGRT_PLACE_DATA (default) estimates for every slot the time
+ * the vertex would finish -- the slot's estimated busy time, plus the bytes
+ * of read arguments not valid there over the link bandwidth they would
+ * cross (host 50 GB/s, peer 700 GB/s, same device 3000 GB/s), plus the
+ * vertex's own argument bytes over HBM bandwidth (6500 GB/s) -- and takes the
+ * earliest (ties: the lower slot); the busy estimates reset at
+ * dagrt_multi_sync.  DAGRT_PLACE_ROUND_ROBIN cycles over the slots.  A launch
+ * may also force a slot (slot >= 0).  Not thread-safe, like dagrt_ctx. */
+typedef struct dagrt_multi_s* dagrt_multi;
+/* Multi-array handle {index:32 | generation:32}; 0 is never valid. */
+typedef uint64_t dagrt_marray;
+enum { DAGRT_PLACE_DATA = 0, DAGRT_PLACE_ROUND_ROBIN = 1 };
+typedef struct {
+  uint64_t launches;          /* kernels launched through dagrt_multi_launch */
+  uint64_t migrations_peer;   /* slot -> slot array copies */
+  uint64_t bytes_peer;
+  uint64_t migrations_host;   /* host mirror -> slot copies */
+  uint64_t bytes_host;
+  uint64_t replicas;          /* replicas allocated by the library */
+  uint64_t bytes_replicas;
+  uint64_t per_slot[16];      /* launches placed on each slot */
+} dagrt_multi_stats_t;
+/* Create a multi-context over n (1..16) slots; devices[i] is slot i's CUDA
+ * device (ignored by the RECORD backend); cfg as for dagrt_create (applied
+ * to every slot); placement = DAGRT_PLACE_*.  Peer access is enabled between
+ * the distinct devices where the hardware allows it. */
+dagrt_status dagrt_multi_create(const int32_t* devices, int32_t n, const dagrt_config* cfg, int32_t placement,
+                                dagrt_multi* out);
+/* Waits for all work, frees the replicas, destroys the slot contexts. */
+dagrt_status dagrt_multi_destroy(dagrt_multi m);
+const char* dagrt_multi_last_error(dagrt_multi m);
+/* The slot's own context (for introspection: dagrt_dag_export, stats). */
+dagrt_status dagrt_multi_slot_ctx(dagrt_multi m, int32_t slot, dagrt_ctx* out);
+/* Register caller-owned memory as a multi-array: `dev` on slot `home` (NULL:
+ * the library allocates the home copy too), optional pinned host mirror.
+ * The array starts valid on its home slot if `dev` was given, else on the
+ * host if a mirror was given (else it is undefined until written). */
+dagrt_status dagrt_multi_array_register(dagrt_multi m, int32_t home, void* dev, void* host_pinned, size_t bytes,
+                                        dagrt_marray* out);
+/* Device pointer of the array's copy on a slot (NULL if none yet). */
+dagrt_status dagrt_multi_array_ptr(dagrt_multi m, dagrt_marray a, int32_t slot, void** dev);
+/* Launch built-in or registered kernel `name` (looked up in every slot's
+ * context): pointer arguments are dagrt_marray handles.  slot < 0: placed by
+ * the policy; *placed (nullable) receives the slot. */
+dagrt_status dagrt_multi_launch(dagrt_multi m, const char* name, dagrt_dim3 grid, dagrt_dim3 block, uint32_t smem,
+                                const dagrt_arg* args, int32_t nargs, int32_t slot, int32_t* placed);
+/* Host read of [off, off+bytes): from the mirror if the host copy is valid,
+ * else through the context of a slot holding a valid copy (dagrt_host_read:
+ * waits exactly for that copy's writer). */
+dagrt_status dagrt_multi_host_read(dagrt_multi m, dagrt_marray a, size_t off, size_t bytes, void* dst);
+/* Host write of [off, off+bytes) from src.  With a mirror: waits for uploads
+ * still reading it, makes it current first if the write is partial, copies
+ * src into it (src may be the mirror itself: the caller wrote it in place)
+ * and leaves only the host copy valid.  Without a mirror: written into the
+ * home copy through the home slot's context (dagrt_host_write). */
+dagrt_status dagrt_multi_host_write(dagrt_multi m, dagrt_marray a, size_t off, size_t bytes, const void* src);
+/* Barrier over every slot (dagrt_sync each); resets the busy estimates. */
+dagrt_status dagrt_multi_sync(dagrt_multi m);
+dagrt_status dagrt_multi_stats(dagrt_multi m, dagrt_multi_stats_t* out);
 
 #ifdef __cplusplus
 }

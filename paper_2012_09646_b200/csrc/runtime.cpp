@@ -1522,6 +1522,11 @@ dagrt_status dagrt_kernel_signature(dagrt_ctx c, dagrt_kernel k, int32_t* kinds,
   return DAGRT_OK;
 }
 
+const char* dagrt_kernel_name(dagrt_ctx c, dagrt_kernel k) {
+  if (!c || k >= c->kernels.size()) return nullptr;
+  return c->kernels[k].name.c_str();
+}
+
 int32_t dagrt_builtin_count(void) { return builtin_count(); }
 const char* dagrt_builtin_name(int32_t i) {
   const Builtin* b = builtin_at(i);

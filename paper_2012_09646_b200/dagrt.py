@@ -379,11 +379,21 @@ class Context:
         if s:
             self._raise(s)
 
+    @classmethod
+    def _borrow(cls, handle, policy="parallel", backend="cuda"):
+        """A view of a context owned elsewhere (a multi-context's slot)."""
+        self = cls.__new__(cls)
+        self._c = C.c_void_p(handle)
+        self.policy, self.backend = policy, backend
+        self.arrays, self._kernels, self._kname = {}, {}, {}
+        self._borrowed = True
+        return self
+
     def close(self):
-        if self._c:
+        if self._c and not getattr(self, "_borrowed", False):
             lib().dagrt_destroy(self._c)
-            self._c = None
-            self.arrays.clear()
+        self._c = None
+        self.arrays.clear()
 
     def __enter__(self):
         return self
@@ -560,7 +570,14 @@ class Context:
         V = (VertexInfo * max(1, nv.value))()
         E = (EdgeInfo * max(1, ne.value))()
         self._check(L.dagrt_dag_export(self._c, V, C.byref(nv), E, C.byref(ne)))
-        names = self._kname
+        names = dict(self._kname)
+        L.dagrt_kernel_name.argtypes = [C.c_void_p, C.c_uint32]
+        L.dagrt_kernel_name.restype = C.c_char_p
+        for v in V[:nv.value]:
+            if v.kind == 0 and v.kernel not in names:
+                nm = L.dagrt_kernel_name(self._c, v.kernel)
+                if nm:
+                    names[v.kernel] = nm.decode()
         arr = {h: a.name for h, a in self.arrays.items()}
         verts = []
         for v in V[:nv.value]:
@@ -642,3 +659,163 @@ def _timeline_export(self):
 
 Context.timeline = _timeline_enable
 Context.timeline_export = _timeline_export
+
+
+# ---------------------------------------------------------------- multi-GPU placement (f2)
+
+class MultiStats(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("migrations_peer", C.c_uint64), ("bytes_peer", C.c_uint64),
+                ("migrations_host", C.c_uint64), ("bytes_host", C.c_uint64), ("replicas", C.c_uint64),
+                ("bytes_replicas", C.c_uint64), ("per_slot", C.c_uint64 * 16)]
+
+
+class MultiArray:
+    """A multi-array (dagrt_marray): home copy, library-owned replicas, optional mirror."""
+    __slots__ = ("multi", "handle", "name", "nbytes", "host_ptr", "_keep")
+
+    def __init__(self, multi, handle, name, nbytes, host_ptr, keep):
+        self.multi, self.handle, self.name, self.nbytes = multi, handle, name, nbytes
+        self.host_ptr, self._keep = host_ptr, keep
+
+    def __repr__(self):
+        return f"MultiArray({self.name}, {self.nbytes} B)"
+
+
+PLACEMENTS = {"data": 0, "round_robin": 1}
+
+
+def _multi_lib():
+    L = lib()
+    if getattr(L, "_multi_ready", False):
+        return L
+    vp, st = C.c_void_p, C.c_int32
+    L.dagrt_multi_create.argtypes = [C.POINTER(C.c_int32), C.c_int32, C.POINTER(Config), C.c_int32, C.POINTER(vp)]
+    L.dagrt_multi_destroy.argtypes = [vp]
+    L.dagrt_multi_last_error.argtypes = [vp]
+    L.dagrt_multi_last_error.restype = C.c_char_p
+    L.dagrt_multi_slot_ctx.argtypes = [vp, C.c_int32, C.POINTER(vp)]
+    L.dagrt_multi_array_register.argtypes = [vp, C.c_int32, vp, vp, C.c_size_t, C.POINTER(C.c_uint64)]
+    L.dagrt_multi_array_ptr.argtypes = [vp, C.c_uint64, C.c_int32, C.POINTER(vp)]
+    L.dagrt_multi_launch.argtypes = [vp, C.c_char_p, Dim3, Dim3, C.c_uint32, C.POINTER(Arg), C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_int32)]
+    L.dagrt_multi_host_read.argtypes = [vp, C.c_uint64, C.c_size_t, C.c_size_t, vp]
+    L.dagrt_multi_host_write.argtypes = [vp, C.c_uint64, C.c_size_t, C.c_size_t, vp]
+    L.dagrt_multi_sync.argtypes = [vp]
+    L.dagrt_multi_stats.argtypes = [vp, C.POINTER(MultiStats)]
+    for fn in ("dagrt_multi_create", "dagrt_multi_destroy", "dagrt_multi_slot_ctx", "dagrt_multi_array_register",
+               "dagrt_multi_array_ptr", "dagrt_multi_launch", "dagrt_multi_host_read", "dagrt_multi_host_write",
+               "dagrt_multi_sync", "dagrt_multi_stats"):
+        getattr(L, fn).restype = st
+    L._multi_ready = True
+    return L
+
+
+class Multi:
+    """Multi-GPU DAG placement (include/dagrt.h "multi-GPU placement", SURVEY
+    f2): one scheduler context per slot, launches placed
+    by data location and estimated migration cost, cross-slot edges as peer
+    copies plus cross-device events.  `devices` lists each slot's CUDA device
+    (repeat a device to exercise the cross-slot path on one GPU)."""
+
+    def __init__(self, devices=(0,), placement="data", policy="parallel", prefetch=True, max_streams=0,
+                 record_dag=False, backend="cuda", graph_cache=False):
+        L = _multi_lib()
+        n = len(devices)
+        devs = (C.c_int32 * n)(*devices)
+        cfg = Config(POLICIES[policy], 1 if prefetch else 0, max_streams, 1 if record_dag else 0,
+                     BACKEND_CUDA if backend == "cuda" else BACKEND_RECORD, 1 if graph_cache else 0)
+        h = C.c_void_p()
+        s = L.dagrt_multi_create(devs, n, C.byref(cfg), PLACEMENTS[placement], C.byref(h))
+        if s:
+            raise DagrtError(s, "dagrt_multi_create failed")
+        self._m, self.devices, self.backend, self.policy = h, list(devices), backend, policy
+        self.arrays = {}
+        self._kinds = {}
+
+    def _check(self, s):
+        if s:
+            raise DagrtError(s, _multi_lib().dagrt_multi_last_error(self._m).decode())
+
+    def close(self):
+        if self._m:
+            _multi_lib().dagrt_multi_destroy(self._m)
+            self._m = None
+            self.arrays.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def register(self, name, nbytes, home=0, dev_ptr=None, host_ptr=None, keep=()):
+        h = C.c_uint64()
+        self._check(_multi_lib().dagrt_multi_array_register(self._m, home, C.c_void_p(dev_ptr) if dev_ptr else None,
+                                                             C.c_void_p(host_ptr) if host_ptr else None, nbytes,
+                                                             C.byref(h)))
+        a = MultiArray(self, h.value, name, nbytes, host_ptr, keep)
+        self.arrays[a.handle] = a
+        return a
+
+    def register_tensor(self, name, t=None, home=0, mirror=None):
+        """Device tensor t on slot `home` (None: the library allocates the home
+        copy) and/or a pinned host mirror tensor."""
+        ref = t if t is not None else mirror
+        nbytes = ref.numel() * ref.element_size()
+        return self.register(name, nbytes, home, t.data_ptr() if t is not None else None,
+                             mirror.data_ptr() if mirror is not None else None, keep=(t, mirror))
+
+    def ptr(self, a, slot):
+        p = C.c_void_p()
+        self._check(_multi_lib().dagrt_multi_array_ptr(self._m, a.handle, slot, C.byref(p)))
+        return p.value
+
+    def slot_context(self, slot):
+        """The slot's own scheduler context (borrowed: DAG export, stats)."""
+        p = C.c_void_p()
+        self._check(_multi_lib().dagrt_multi_slot_ctx(self._m, slot, C.byref(p)))
+        return Context._borrow(p.value, self.policy, self.backend)
+
+    def _signature(self, name):
+        k = self._kinds.get(name)
+        if k is None:
+            ctx = self.slot_context(0)
+            k = ctx.kernel(name).kinds
+            self._kinds[name] = k
+        return k
+
+    def launch(self, name, grid, block, *args, smem=0, slot=-1):
+        """Launch `name`; returns the slot it was placed on."""
+        kinds = self._signature(name)
+        if len(args) != len(kinds):
+            raise DagrtError(ESIG, f"{name}: {len(args)} args, signature has {len(kinds)}")
+        A = (Arg * max(1, len(args)))()
+        for i, (k, v) in enumerate(zip(kinds, args)):
+            if K_CONST <= k <= K_OUT:
+                if not isinstance(v, MultiArray):
+                    raise TypeError(f"pointer parameter needs a MultiArray, got {type(v)}")
+                A[i].array = v.handle
+            else:
+                _set_arg(A[i], k, v)
+        placed = C.c_int32(-1)
+        self._check(_multi_lib().dagrt_multi_launch(self._m, name.encode(), dim3(grid), dim3(block), smem, A,
+                                                     len(args), slot, C.byref(placed)))
+        return placed.value
+
+    def read(self, a, dst_ptr, off=0, nbytes=None):
+        n = a.nbytes - off if nbytes is None else nbytes
+        self._check(_multi_lib().dagrt_multi_host_read(self._m, a.handle, off, n, C.c_void_p(dst_ptr)))
+
+    def write(self, a, src_ptr, off=0, nbytes=None):
+        n = a.nbytes - off if nbytes is None else nbytes
+        self._check(_multi_lib().dagrt_multi_host_write(self._m, a.handle, off, n, C.c_void_p(src_ptr)))
+
+    def sync(self):
+        self._check(_multi_lib().dagrt_multi_sync(self._m))
+
+    def stats(self):
+        s = MultiStats()
+        self._check(_multi_lib().dagrt_multi_stats(self._m, C.byref(s)))
+        d = {f: getattr(s, f) for f, _ in MultiStats._fields_ if f != "per_slot"}
+        d["per_slot"] = list(s.per_slot[:len(self.devices)])
+        return d
