@@ -222,7 +222,7 @@ def time_steps(fn, steps, warmup, dist, prep=None):
 def needs_prep(prog):
     """True if the program prepares its inputs on the host before a run (HITS)."""
     from paper_2012_09646_b200.programs.base import Program
-    return type(prog).restart is not Program.restart
+    return type(prog).restart is not Program.restart or getattr(prog, "um", False)
 
 
 def cpu_oracle_rate(name, budget_s=10.0):
@@ -481,6 +481,20 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
             p2 = make_program(name, c2, "stream", share=eprog)
             res[f"{label}_stream_ms"] = time_steps(p2.run, K, W, dist, prep and p2.restart) / K
             c2.close()
+        # UM mode (§V-C): the stream workload on
+        # managed arrays -- runtime prefetch vs GPU page faults, and the serial
+        # page-fault baseline; pages go back to the host before every step
+        # (restart(), outside the timed region)
+        Ku = min(K, 5)
+        for label, kw in (("um_parallel_prefetch", dict()), ("um_parallel_fault", dict(prefetch=False)),
+                          ("um_serial_fault", dict(policy="serial", prefetch=False))):
+            c2 = D.Context(device=local, **kw)
+            p2 = make_program(name, c2, "um")
+            p2.load_inputs(0)
+            res[f"{label}_ms"] = time_steps(p2.run, Ku, W, dist, p2.restart) / Ku
+            del p2
+            c2.close()
+            torch.cuda.empty_cache()
         # Fig. 9 in stream mode: serial kernel + H2D times, D2H on the host vertices
         sverts, sedges, s_arr = dag_of(D, name, eprog, local, "stream")
         skms, shms = serial_vertex_times(D, name, eprog, local, "stream")

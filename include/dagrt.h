@@ -121,6 +121,25 @@ dagrt_status dagrt_array_register(dagrt_ctx ctx, void* dev, void* host_pinned, s
 /* Wait for the array's in-flight users, then forget it (the caller frees the
  * memory afterwards).  The handle becomes stale (DAGRT_ENOTFOUND). */
 dagrt_status dagrt_array_unregister(dagrt_ctx ctx, dagrt_array a);
+/* Register UNIFIED (managed) memory, cudaMallocManaged by the caller, as an
+ * array: one pointer valid on host and device.  The UM mode of the paper's
+ * GrCUDA (§V-C): with cfg.prefetch = 1 a host-newer array read by a
+ * kernel is moved with cudaMemPrefetchAsync (on the copy stream, like an
+ * H2D prefetch); with prefetch = 0 nothing is issued and the kernel's page
+ * faults migrate the pages ("disabling automatic prefetching ... turns the
+ * page fault controller into the main bottleneck", L904-907).  Host reads and
+ * writes wait on the DAG exactly as with a mirror, then access the memory
+ * directly (no copy).  Registering a managed array turns the graph cache of
+ * the context off (prefetches are not graph nodes). */
+dagrt_status dagrt_array_register_managed(dagrt_ctx ctx, void* ptr, size_t bytes, dagrt_array* out);
+/* Conveniences for callers without a CUDA binding of their own (the only
+ * memory functions of the library; not used on the product path):
+ * cudaMallocManaged / cudaFree, and moving the pages of [p, p+bytes) to the
+ * host (cudaMemPrefetchAsync to the CPU + synchronize) so that the next GPU
+ * access must migrate them again. */
+dagrt_status dagrt_managed_alloc(size_t bytes, void** p);
+dagrt_status dagrt_managed_free(void* p);
+dagrt_status dagrt_managed_to_host(void* p, size_t bytes);
 /* Device pointer of a registered array (for the caller's own bookkeeping). */
 dagrt_status dagrt_array_device_ptr(dagrt_ctx ctx, dagrt_array a, void** dev);
 
@@ -321,6 +340,8 @@ typedef struct {
   uint64_t table_vertices;     /* vertex records held now */
   uint64_t epoch_base;         /* global id of the first record held */
   uint64_t max_readers;        /* longest reader list of any live array now */
+  uint64_t um_prefetch_bytes;  /* managed arrays: bytes moved by cudaMemPrefetchAsync */
+  uint64_t um_fault_bytes;     /* managed arrays: host-newer bytes left to GPU page faults */
 } dagrt_stats_t;
 /* Copy min(size, sizeof(dagrt_stats_t)) bytes of the counters to out. */
 dagrt_status dagrt_stats(dagrt_ctx ctx, void* out, size_t size);

@@ -86,6 +86,7 @@ struct Backend {
   virtual cudaError_t stream_sync(void* s) = 0;
   virtual cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k,
                                  void* s) = 0;
+  virtual cudaError_t prefetch(void* p, size_t n, int dev, void* s) = 0;  // managed memory
   virtual bool real() const = 0;
 };
 
@@ -184,6 +185,9 @@ struct CudaBackend final : Backend {
                          void* s) override {
     return cudaMemcpyAsync(dst, src, n, k, (cudaStream_t)s);
   }
+  cudaError_t prefetch(void* p, size_t n, int dev, void* s) override {
+    return cudaMemPrefetchAsync(p, n, dev, (cudaStream_t)s);
+  }
   bool real() const override { return true; }
 };
 
@@ -205,6 +209,7 @@ struct RecordBackend final : Backend {
   cudaError_t copy_async(void*, const void*, size_t, cudaMemcpyKind, void*) override {
     return cudaSuccess;
   }
+  cudaError_t prefetch(void*, size_t, int, void*) override { return cudaSuccess; }
   bool real() const override { return false; }
 };
 
@@ -405,6 +410,11 @@ struct DeferBackend final : Backend {
     o.s = s;
     ops.push_back(o);
     return cudaSuccess;
+  }
+  cudaError_t prefetch(void* p, size_t n, int dev, void* s) override {  // never deferred
+    if (cudaError_t e = flush()) return e;
+    if (cudaError_t e = pre_eager(s)) return e;
+    return in->prefetch(p, n, dev, s);
   }
   cudaError_t event_sync(void* e) override {
     if (cudaError_t r = flush()) return r;
@@ -717,6 +727,7 @@ struct ArrayRec {
   uint32_t gen = 0;
   bool live = false;
   bool mapped = false;
+  bool managed = false;             // unified memory: dev == host, no copies (dagrt_array_register_managed)
   int64_t last_writer = -1;         // GLOBAL vertex id of the last kernel writer, -1 = none/host
   std::vector<int64_t> readers;     // global ids of the readers since the last writer (pruned lazily)
   uint8_t coh = COH_DEVICE;
@@ -1177,6 +1188,10 @@ dagrt_status d2h_mapped(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* ds
 
 dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   if (n == 0) return DAGRT_OK;
+  if (a->managed) {  // the host reads unified memory in place (page faults move it)
+    if (c->be->real() && dst != a->dev + off) memcpy(dst, a->dev + off, n);
+    return DAGRT_OK;
+  }
   trace_op(c, DAGRT_OP_D2H, -1, array_index(c, a), (int64_t)off, n);
   c->st.d2h_bytes += n;
   c->st.d2h_copies++;
@@ -1441,6 +1456,38 @@ dagrt_status dagrt_array_register(dagrt_ctx c, void* dev, void* host, size_t byt
   a.live = true;
   *out = array_handle(c, &a);
   return DAGRT_OK;
+}
+
+dagrt_status dagrt_array_register_managed(dagrt_ctx c, void* ptr, size_t bytes, dagrt_array* out) {
+  GUARD(c);
+  if (!out) return fail(c, DAGRT_EINVAL, "null out");
+  if (c->be->real() && ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type != cudaMemoryTypeManaged) {
+      cudaGetLastError();
+      return fail(c, DAGRT_EINVAL, "%p is not managed memory (cudaMallocManaged)", ptr);
+    }
+  }
+  if (dagrt_status s = dagrt_array_register(c, ptr, ptr, bytes, out)) return s;
+  ArrayRec* a = get_array(c, *out);
+  a->managed = true;
+  a->coh = COH_BOTH;
+  if (c->be->enabled) {  // prefetches are issued eagerly: no graph cache in UM mode
+    CK(c->be->flush(), "graph cache flush");
+    c->be->enabled = false;
+  }
+  return DAGRT_OK;
+}
+
+dagrt_status dagrt_managed_alloc(size_t bytes, void** p) {
+  if (!p) return DAGRT_EINVAL;
+  return cudaMallocManaged(p, bytes ? bytes : 1, cudaMemAttachGlobal) == cudaSuccess ? DAGRT_OK : DAGRT_ECUDA;
+}
+dagrt_status dagrt_managed_free(void* p) { return cudaFree(p) == cudaSuccess ? DAGRT_OK : DAGRT_ECUDA; }
+dagrt_status dagrt_managed_to_host(void* p, size_t bytes) {
+  if (!p) return DAGRT_EINVAL;
+  if (cudaMemPrefetchAsync(p, bytes, cudaCpuDeviceId, 0) != cudaSuccess) return DAGRT_ECUDA;
+  return cudaStreamSynchronize(0) == cudaSuccess ? DAGRT_OK : DAGRT_ECUDA;
 }
 
 dagrt_status dagrt_array_unregister(dagrt_ctx c, dagrt_array h) {
@@ -1735,13 +1782,22 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
     for (int j = 0; j < nacc; ++j) {
       ArrayRec* a = acc[j];
       if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
+        if (a->managed && !c->cfg.prefetch) {  // UM without prefetch: the kernel faults the pages in
+          c->st.um_fault_bytes += a->bytes;
+          a->coh = COH_BOTH;
+          continue;
+        }
         trace_op(c, DAGRT_OP_H2D, -3, array_index(c, a), 0, a->bytes);
         c->st.h2d_bytes += a->bytes;
         c->st.h2d_copies++;
+        if (a->managed) c->st.um_prefetch_bytes += a->bytes;
         if (c->be->real()) {
           void* t0;
           if (dagrt_status st_ = tl_begin(c, s, &t0)) return st_;
-          CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
+          if (a->managed)
+            CK(c->be->prefetch(a->dev, a->bytes, c->device, s), "cudaMemPrefetchAsync");
+          else
+            CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
           if (dagrt_status st_ = tl_end(c, s, t0, 1, -3, gvid, array_index(c, a), a->bytes)) return st_;
           CK(c->be->stream_sync(s), "cudaStreamSynchronize");
           c->st.host_syncs++;
@@ -1788,13 +1844,22 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
     ArrayRec* a = acc[j];
     if (a->h2d_pending && !is_active(c, a->h2d_consumer)) a->h2d_pending = false;
     if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
+      if (a->managed && !c->cfg.prefetch) {  // UM without prefetch: the kernel faults the pages in
+        c->st.um_fault_bytes += a->bytes;
+        a->coh = COH_BOTH;
+        continue;
+      }
       void* cs = c->cfg.prefetch ? c->copy_stream : s;
       trace_op(c, DAGRT_OP_H2D, c->cfg.prefetch ? -2 : sid, array_index(c, a), 0, a->bytes);
       c->st.h2d_bytes += a->bytes;
       c->st.h2d_copies++;
+      if (a->managed) c->st.um_prefetch_bytes += a->bytes;
       void* t0;
       if (dagrt_status st_ = tl_begin(c, cs, &t0)) return st_;
-      CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, cs), "cudaMemcpyAsync H2D");
+      if (a->managed)
+        CK(c->be->prefetch(a->dev, a->bytes, c->device, cs), "cudaMemPrefetchAsync");
+      else
+        CK(c->be->copy_async(a->dev, a->host, a->bytes, cudaMemcpyHostToDevice, cs), "cudaMemcpyAsync H2D");
       if (dagrt_status st_ = tl_end(c, cs, t0, 1, c->cfg.prefetch ? -2 : sid, gvid, array_index(c, a),
                                     a->bytes))
         return st_;
@@ -1881,7 +1946,7 @@ dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t byte
   if (bytes && !dst) return fail(c, DAGRT_EINVAL, "null dst");
   // a read that needs a copy orders the copy after its producers on the D2H
   // stream (one host round trip); otherwise the host waits on the events
-  const bool copy = bytes && (!a->host || a->coh == COH_DEVICE) && c->be->real();
+  const bool copy = bytes && (!a->host || a->coh == COH_DEVICE) && c->be->real() && !a->managed;
   if (c->cfg.policy != DAGRT_SERIAL_SYNC)
     if (dagrt_status s = host_sync_parents(c, a, false, copy ? c->d2h_stream : nullptr)) return s;
   if (!a->host) return d2h(c, a, off, bytes, dst);
@@ -1951,7 +2016,7 @@ dagrt_status dagrt_host_map(dagrt_ctx c, dagrt_array h, int32_t access, void** h
     a->readers.clear();
     a->coh = COH_HOST;
   } else {
-    const bool copy = a->bytes && a->coh == COH_DEVICE && c->be->real();
+    const bool copy = a->bytes && a->coh == COH_DEVICE && c->be->real() && !a->managed;
     if (c->cfg.policy != DAGRT_SERIAL_SYNC)
       if (dagrt_status s = host_sync_parents(c, a, false, copy ? c->d2h_stream : nullptr)) return s;
     if (a->coh == COH_DEVICE) {

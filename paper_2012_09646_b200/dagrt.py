@@ -73,7 +73,7 @@ STAT_FIELDS = ["launches", "vertices", "host_vertices", "edges", "cross_stream_w
                "copy_waits", "streams", "events_created", "h2d_bytes", "d2h_bytes",
                "h2d_copies", "d2h_copies", "host_syncs", "sched_ns", "graph_replays",
                "graph_captures", "eager_batches", "launch_ns", "record_ns", "wait_ns",
-               "table_vertices", "epoch_base", "max_readers"]
+               "table_vertices", "epoch_base", "max_readers", "um_prefetch_bytes", "um_fault_bytes"]
 
 
 class Stats(C.Structure):
@@ -190,6 +190,34 @@ def load_experimental():
             raise ImportError(f"{EXP_LIBPATH} not built: run `python -m paper_2012_09646_b200.build`")
         _exp = C.CDLL(EXP_LIBPATH)
     return _exp
+
+
+def managed_alloc(nbytes):
+    """cudaMallocManaged through the library (dagrt_managed_alloc)."""
+    L = lib()
+    L.dagrt_managed_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p)]
+    L.dagrt_managed_alloc.restype = C.c_int32
+    p = C.c_void_p()
+    s = L.dagrt_managed_alloc(nbytes, C.byref(p))
+    if s:
+        raise DagrtError(s, f"cudaMallocManaged({nbytes}) failed")
+    return p.value
+
+
+def managed_free(ptr):
+    L = lib()
+    L.dagrt_managed_free.argtypes = [C.c_void_p]
+    L.dagrt_managed_free(C.c_void_p(ptr))
+
+
+def managed_to_host(ptr, nbytes):
+    """Move the pages of a managed range to the host (dagrt_managed_to_host)."""
+    L = lib()
+    L.dagrt_managed_to_host.argtypes = [C.c_void_p, C.c_size_t]
+    L.dagrt_managed_to_host.restype = C.c_int32
+    s = L.dagrt_managed_to_host(C.c_void_p(ptr), nbytes)
+    if s:
+        raise DagrtError(s, "managed prefetch to host failed")
 
 
 def builtins():
@@ -408,6 +436,17 @@ class Context:
                                                C.c_void_p(host_ptr) if host_ptr else None,
                                                nbytes, C.byref(h)))
         a = Array(self, h.value, name, nbytes, dev_ptr, host_ptr, keep)
+        self.arrays[a.handle] = a
+        return a
+
+    def register_managed(self, name, ptr, nbytes, keep=()):
+        """Unified-memory array (dagrt_array_register_managed: the UM mode)."""
+        L = lib()
+        L.dagrt_array_register_managed.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
+        L.dagrt_array_register_managed.restype = C.c_int32
+        h = C.c_uint64()
+        self._check(L.dagrt_array_register_managed(self._c, C.c_void_p(ptr), nbytes, C.byref(h)))
+        a = Array(self, h.value, name, nbytes, ptr, ptr, keep)
         self.arrays[a.handle] = a
         return a
 

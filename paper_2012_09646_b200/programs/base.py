@@ -14,10 +14,17 @@ Modes:
 * ``stream``   -- inputs are rewritten by the host before every run (host
   newer => H2D inside the run, overlapped by the prefetcher, L356-366) and the
   host reads whole sink arrays (D2H inside the run).
+* ``um``       -- the stream workload on UNIFIED memory (GrCUDA's managed
+  arrays, §V-C): every array is cudaMallocManaged, the
+  inputs' pages are moved to the host before each run (restart(), outside
+  the timed region: the host rewrote them), the run either prefetches them
+  (context prefetch on: cudaMemPrefetchAsync) or leaves them to GPU page
+  faults (prefetch off), and the host reads whole sinks in place.
 """
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import torch
 
@@ -53,6 +60,8 @@ class Program:
         self.sinks = []    # arrays the host reads at the end of every run
         self._scalar = (C.c_char * 8)()
         self.red = set()   # scalar-reduction outputs (the host reads only the result)
+        self.um = mode == "um"
+        self.streaming = mode in ("stream", "um")  # host-newer inputs, whole-sink reads
 
     # ---------------------------------------------------------- allocation
     def alloc(self, name, numel, dtype, mirror=False, zero=False, nbytes=None):
@@ -67,6 +76,8 @@ class Program:
             self.t[name] = t
             self.a[name] = self.ctx.register_tensor(name, t, m)
             return t
+        if self.um and not self.record:
+            return self._alloc_managed(name, numel, dtype, zero, nbytes)
         if nbytes is not None:
             t = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         elif zero:
@@ -81,10 +92,31 @@ class Program:
         self.a[name] = self.ctx.register_tensor(name, t, m)
         return t
 
+    _TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8",
+                torch.uint8: "|u1"}
+
+    def _alloc_managed(self, name, numel, dtype, zero, nbytes):
+        """UM mode: cudaMallocManaged memory viewed as a CUDA tensor (no copy)."""
+        if nbytes is not None:
+            numel, dtype, zero = nbytes, torch.uint8, True
+        size = max(1, numel) * torch.empty(0, dtype=dtype).element_size()
+        ptr = D.managed_alloc(size)
+        weakref.finalize(self, D.managed_free, ptr)
+
+        class _View:  # __cuda_array_interface__: torch.as_tensor shares the memory
+            __cuda_array_interface__ = {"shape": (numel,), "typestr": self._TYPESTR[dtype],
+                                        "data": (ptr, False), "version": 2, "strides": None}
+        t = torch.as_tensor(_View(), device="cuda")
+        if zero:
+            t.zero_()
+        self.t[name] = t
+        self.a[name] = self.ctx.register_managed(name, ptr, numel * t.element_size(), keep=(t,))
+        return t
+
     def alloc_red(self, name):
         """Scalar-reduction output: RedOut layout (see csrc/kcommon.cuh)."""
         self.red.add(name)
-        return self.alloc(name, 0, None, mirror=self.mode == "stream", nbytes=self.red_bytes)
+        return self.alloc(name, 0, None, mirror=self.streaming, nbytes=self.red_bytes)
 
     def fill(self, name, spec, set_index=0):
         """Seeded input (synth) into the device tensor; stream mode: and its mirror."""
@@ -121,18 +153,32 @@ class Program:
     def restart(self):
         """Host-side preparation of a fresh run, outside the timed region
         (the paper writes the inputs before each run, L862-864): a no-op
-        except for programs whose inputs are also their outputs (HITS)."""
+        except for programs whose inputs are also their outputs (HITS), and
+        in UM mode, where the inputs' pages go back to the host (as if the
+        host had rewritten them) so that the run must migrate them again."""
+        if self.um and not self.record:
+            torch.cuda.synchronize()
+            for n in self.inputs:
+                D.managed_to_host(self.t[n].data_ptr(), self.t[n].numel() * self.t[n].element_size())
 
     def begin_run(self):
         """Stream mode: the host writes fresh inputs (host copy becomes newer)."""
-        if self.mode == "stream":
+        if self.streaming:
             for n in self.inputs:
                 self.ctx.host_map(self.a[n], D.W)
                 self.ctx.host_unmap(self.a[n])
 
     def end_run(self):
         """Host reads of the sinks: one element (resident) or whole arrays (stream)."""
-        if self.mode != "stream":
+        if self.um:  # the host reads the managed sinks in place (into host buffers)
+            if getattr(self, "_um_out", None) is None:
+                self._um_out = {n: torch.empty(self.a[n].nbytes, dtype=torch.uint8, pin_memory=not self.record)
+                                for n in self.sinks}
+            for n in self.sinks:
+                nb = min(4, self.a[n].nbytes) if n in self.red else self.a[n].nbytes
+                self.ctx.host_read(self.a[n], self._um_out[n].data_ptr(), 0, nb)
+            return
+        if not self.streaming:
             if getattr(self, "_reads", None) is None:  # arguments converted once
                 self._reads = [self.ctx.prepare_read(self.a[n], C.addressof(self._scalar), 0,
                                                      min(4, self.a[n].nbytes)) for n in self.sinks]
@@ -148,7 +194,7 @@ class Program:
                 self.ctx.host_read(arr, C.addressof(self._scalar), 0, min(4, arr.nbytes))
 
     def run(self):
-        if self.mode != "stream":  # resident: one batch call + the prepared sink reads
+        if not self.streaming:  # resident: one batch call + the prepared sink reads
             key = (id(getattr(self, "L", None)), id(getattr(self, "it", None)))
             steps = getattr(self, "_steps", None)
             if steps is None or self._steps_key != key:
@@ -208,6 +254,8 @@ class Program:
 
     def graph_io(self, g):
         """Stream mode: H2D nodes for inputs; returns {input name: node}."""
+        if self.um:
+            raise NotImplementedError("hand-written graphs take device or mirrored arrays, not UM")
         if self.mode != "stream":
             return {}
         return {n: g.copy(self.a[n], "h2d") for n in self.inputs}
@@ -240,4 +288,4 @@ class Program:
         h2d = sum(self.t[n].numel() * self.t[n].element_size() for n in self.inputs)
         d2h = sum(4 if n in self.red else self.t[n].numel() * self.t[n].element_size()
                   for n in self.sinks)
-        return (h2d, d2h) if self.mode == "stream" else (0, 4 * len(self.sinks))
+        return (h2d, d2h) if self.streaming else (0, 4 * len(self.sinks))

@@ -219,7 +219,7 @@ class Hits(Program):
         self.csr = graph
         rp, ci, rpt, cit = graph
         self.e = int(rp[-1])
-        stream = self.mode == "stream"
+        stream = self.streaming
         for name, arr in (("rp", rp), ("ci", ci), ("rpt", rpt), ("cit", cit)):
             self.alloc(name, max(1, arr.size), torch.int32)
             if arr.size:
@@ -272,6 +272,7 @@ class Hits(Program):
         v = 1.0 / math.sqrt(self.n) if self.n else 0.0
         if self.record:
             return
+        super().restart()  # UM mode: the inputs' pages back to the host
         if self.mode == "stream":
             for name in ("a1", "h1"):
                 self.mirror[name].fill_(v)
@@ -333,7 +334,7 @@ class DeepLearning(Program):
         self.h, self.w = h, w
         (h1, w1), (h2, w2), (h3, w3) = dl_shapes(h, w)
         self.shapes = ((h1, w1), (h2, w2), (h3, w3))
-        stream = self.mode == "stream"
+        stream = self.streaming
         nz = 2 * h3 * w3 * 16
         self.alloc("x", h * w, torch.float32, mirror=stream)
         self.alloc("y", h * w, torch.float32, mirror=stream)

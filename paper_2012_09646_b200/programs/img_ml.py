@@ -25,7 +25,7 @@ class Images(Program):
         self.h, self.w = h, w
         n = h * w
         self.n = n
-        stream = self.mode == "stream"
+        stream = self.streaming
         self.alloc("img", n, torch.float32, mirror=stream)
         for name in ("bs", "bl", "bu", "ms", "ml", "iu", "i2"):
             self.alloc(name, n, torch.float32)
@@ -106,7 +106,7 @@ class MLEnsemble(Program):
     def __init__(self, ctx, n=10_000_000, f=ML_F, c=ML_C, **kw):
         super().__init__(ctx, **kw)
         self.n, self.f, self.c = n, f, c
-        stream = self.mode == "stream"
+        stream = self.streaming
         self.alloc("X", n * f, torch.int32, mirror=stream)
         self.alloc("Z", n * f, torch.float32)
         self.alloc("stats", 0, None, nbytes=norm_stats_bytes(f))

@@ -23,7 +23,7 @@ class Vec(Program):
     def __init__(self, ctx, n=1_000_000, **kw):
         super().__init__(ctx, **kw)
         self.n = n
-        stream = self.mode == "stream"
+        stream = self.streaming
         self.alloc("x", n, torch.float32, mirror=stream)
         self.alloc("y", n, torch.float32, mirror=stream)
         self.alloc("x1", n, torch.float32)
@@ -68,7 +68,7 @@ class BlackScholes(Program):
     def __init__(self, ctx, n=10_000_000, nvec=synth.BS_NVEC, dtype="f64", **kw):
         super().__init__(ctx, **kw)
         self.n, self.nvec, self.dtype = n, nvec, dtype
-        stream = self.mode == "stream"
+        stream = self.streaming
         tdt = torch.float64 if dtype == "f64" else torch.float32
         for i in range(nvec):
             self.alloc(f"s{i}", n, tdt, mirror=stream)

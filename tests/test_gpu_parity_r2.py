@@ -62,6 +62,33 @@ def test_policy_outputs_match_oracle(bench, mode, policy):
 
 
 @pytest.mark.parametrize("bench", list(SMALL))
+@pytest.mark.parametrize("policy,prefetch", [("parallel", True), ("parallel", False), ("serial", False)])
+def test_unified_memory_mode_matches_oracle(bench, policy, prefetch):
+    """UM mode (managed arrays, §V-C): inputs'
+    pages moved to the host before each run, then prefetched by the runtime
+    (cudaMemPrefetchAsync) or faulted in by the kernels; the host reads the
+    sinks in place.  Three runs, the oracle's results each time."""
+    c = D.Context(device=0, policy=policy, prefetch=prefetch)
+    p = SMALL[bench](c, "um")
+    p.load_inputs(3)
+    c.stats_reset()
+    for _ in range(3):
+        p.restart()
+        p.run()
+        c.sync()
+        check(p, 3)
+    st = c.stats()
+    if prefetch:
+        assert st["um_prefetch_bytes"] > 0 and st["um_fault_bytes"] == 0, st
+    else:
+        assert st["um_fault_bytes"] > 0 and st["um_prefetch_bytes"] == 0, st
+    assert st["d2h_copies"] == 0, st  # the host reads managed memory in place
+    del p
+    c.close()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("bench", list(SMALL))
 @pytest.mark.parametrize("mode", ["resident", "stream"])
 def test_hand_written_graph_matches_oracle(bench, mode):
     c = D.Context(device=0)

@@ -513,3 +513,35 @@ def test_history_driven_launch_configuration_record():
     assert [v[2] for v in verts] == ["square"] * 9 and edges == set()
     with pytest.raises(D.DagrtError):
         ctx.launch("reduce_diff", "auto", 0, a, a, b, 10)  # no candidates registered
+
+
+@pytest.mark.parametrize("prefetch", [True, False])
+def test_unified_memory_arrays(prefetch):
+    """Managed arrays (dagrt_array_register_managed, the UM mode of PAPER.md
+    §V-C): the DAG is the same as with mirrors; a host-newer input is
+    prefetched on the copy stream (an H2D op in the trace, counted in
+    um_prefetch_bytes) or left to page faults (no transfer op at all,
+    um_fault_bytes); host reads never copy."""
+    ctx = D.Context(backend="record", record_dag=True, prefetch=prefetch)
+    bufs = [(C.c_char * 256)() for _ in range(2)]  # the recorder never touches them
+    x = ctx.register_managed("x", C.addressof(bufs[0]), 256)
+    y = ctx.register_managed("y", C.addressof(bufs[1]), 256)
+    k = ctx.register_kernel(None, "k", "const ptr, out ptr")
+    src = (C.c_char * 256)()
+    ctx.host_write(x, C.addressof(src), 0, 256)  # host newer
+    ctx.prepare(k, 1, 32, [x, y])()
+    ctx.host_read(y, C.addressof(src), 0, 256)
+    ops = [t[0] for t in ctx.trace()]
+    st = ctx.stats()
+    if prefetch:
+        assert ops.count("h2d") == 1 and st["um_prefetch_bytes"] == 256 and st["um_fault_bytes"] == 0
+    else:
+        assert "h2d" not in ops and st["um_fault_bytes"] == 256 and st["um_prefetch_bytes"] == 0
+    assert "d2h" not in ops and st["d2h_copies"] == 0
+    v, e = ctx.dag()
+    assert [t[1] for t in v] == ["kernel", "host"] and len(e) == 1
+    # a second launch reading x finds it current: nothing moves
+    ctx.prepare(k, 1, 32, [x, y])()
+    st2 = ctx.stats()
+    assert st2["um_prefetch_bytes"] + st2["um_fault_bytes"] == 256
+    ctx.close()
