@@ -307,6 +307,102 @@ __device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, doubl
     c[i] = o[0];
   }
 }
+// Warp-specialised form: warp 8 of a 288-thread CTA is a producer that keeps
+// a deeper ring (STAGES chunks of 256 * OPT options) filled with bulk copies;
+// the 8 consumer warps wait only on the stage they need (full barrier) and
+// release it with one arrival per warp (empty barrier, count 8) as soon as
+// their options are in registers -- no CTA-wide barrier per chunk, so warps
+// drift apart and the FP64 pipe is fed while others wait on memory (the
+// bs2t form lost ~40% of the pipe to chunk-synchronous waits: ncu fp64 pipe
+// 60%, barrier + long-scoreboard stalls, profiles/r2_ncu_*).
+__device__ __forceinline__ void bs_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <int OPT, int STAGES>
+__device__ __forceinline__ void bs3_ws_body(const double* __restrict__ s, double* __restrict__ c, long long n,
+                                            double r, double v, double t, double k) {
+  constexpr int kCons = 256;            // consumer threads (warps 0-7); warp 8 produces
+  constexpr int kChunk = kCons * OPT;   // options per chunk
+  __shared__ BsTables T;
+  extern __shared__ __align__(128) unsigned char bs3_dyn[];  // the ring: STAGES * kChunk * 8 bytes (dynamic)
+  double(*ring)[kChunk] = reinterpret_cast<double(*)[kChunk]>(bs3_dyn);
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  bs_tables_init(T);
+  BsConst C;
+  const double vst = v * sqrt(t);
+  C.vst = vst;
+  C.inv_vst = 1.0 / vst;
+  C.mu_s = (r + 0.5 * v * v) * t / vst;
+  C.inv_k = 1.0 / k;
+  C.c2 = exp(r * t) / k;
+  C.kexp = k * exp(-r * t);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  if (!(aligned16(s) && aligned16(c)) || blockDim.x != kCons + 32 || dyn < STAGES * kChunk * 8u) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < n; i += (long long)gridDim.x * blockDim.x) {
+      double a[2] = {s[i], 1.0}, o[2];
+      bs_price_w<2>(a, o, C, T);
+      c[i] = o[0];
+    }
+    return;
+  }
+  const long long nfullc = n / kChunk;
+  const long long G = gridDim.x;
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      bs_mbar_init(&full[q], 1);
+      bs_mbar_init(&empty[q], kCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kCons / 32) {  // producer (one lane)
+    if ((tid & 31) == 0) {
+      int it = 0;
+      for (long long ch = blockIdx.x; ch < nfullc; ch += G, ++it) {
+        const int st = it % STAGES;
+        if (it >= STAGES) bs_mbar_wait(&empty[st], (unsigned)((it / STAGES - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bs_bulk_g2s(ring[st], s + ch * kChunk, kChunk * 8, &full[st]);
+      }
+    }
+    return;  // no CTA-wide barrier below this point
+  }
+  int it = 0;
+  for (long long ch = blockIdx.x; ch < nfullc; ch += G, ++it) {
+    const int st = it % STAGES;
+    bs_mbar_wait(&full[st], (unsigned)((it / STAGES) & 1));
+    double a[OPT], o[OPT];
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) {
+      const double2 x = reinterpret_cast<const double2*>(ring[st])[tid + kCons * q];
+      a[2 * q] = x.x;
+      a[2 * q + 1] = x.y;
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) bs_mbar_arrive(&empty[st]);
+    bs_price_w<OPT>(a, o, C, T);
+    double2* dst = reinterpret_cast<double2*>(c + ch * kChunk);
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) dst[tid + kCons * q] = make_double2(o[2 * q], o[2 * q + 1]);
+  }
+  for (long long i = nfullc * kChunk + (long long)blockIdx.x * kCons + tid; i < n; i += G * kCons) {
+    double a[2] = {s[i], 1.0}, o[2];
+    bs_price_w<2>(a, o, C, T);
+    c[i] = o[0];
+  }
+}
+// dynamic shared memory of a bs3 instance (its ring)
+#define BS3_SMEM(OPT, STAGES) ((STAGES) * 256 * (OPT) * 8)
+#define BS3_VARIANT(NAME, OPT, STAGES, MINB)                                                      \
+  __global__ void __launch_bounds__(288, MINB) NAME(const double* __restrict__ s,                \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs3_ws_body<OPT, STAGES>(s, c, n, r, v, t, k);                                                 \
+  }
+
 #define BS2T_VARIANT(NAME, OPT, STAGES, MINB)                                                      \
   __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
                                                     double* __restrict__ c, long long n, double r, \

@@ -16,56 +16,7 @@
 
 namespace dagrt {
 
-// ---------------------------------------------------------------------------
-// "spmv" (product, round 2): the non-zero split of spmv_nz (exp/spmv_variants.cu,
-// whose notes describe the chunk pipeline, the segmented warp scan and the
-// cross-warp deposits this kernel shares) with EVERY row padded
-// to at least one item -- each empty row gets one column index -1 (value 0)
-// when the graph is registered (spmv_pad_plan(), programs/hits_dl.py).  Then
-// ordinals ARE row ids: completed rows are written to consecutive addresses
-// with no row-id loads and no zero-filling of skipped rows (the profile of
-// spmv_nz put its top stalls on exactly those: the row-id loads and the
-// divergent gap loops), at the cost of 9M more 4-byte column indices on the
-// HBM-cheap coalesced stream.  Plan (int32): [header(16) | rp2(N+1) |
-// rbase(nc+1) | flags(4 nc + 4 words) | ci2(E2)], rp2 the padded row
-// pointers (used only for rows crossing warp ranges), E2 = E + #empty rows.
-constexpr int kPadMagic = 0x50414430;  // "PAD0"
-
-struct PadPlan {
-  int nc, n, e2;
-  const int* rp2;
-  const int* rbase;
-  const unsigned* flags;
-  const int* ci2;
-};
-
-__device__ __forceinline__ PadPlan pad_plan(const int* plan) {
-  if (__ldg(plan) != kPadMagic || __ldg(plan + 3) != kNzChunk) __trap();  // built for another kernel
-  PadPlan P;
-  P.nc = __ldg(plan + 1);
-  P.n = __ldg(plan + 2);
-  P.rp2 = plan + __ldg(plan + 4);
-  P.rbase = plan + __ldg(plan + 5);
-  P.flags = reinterpret_cast<const unsigned*>(plan + __ldg(plan + 6));
-  P.ci2 = plan + __ldg(plan + 7);
-  P.e2 = __ldg(plan + 8);
-  return P;
-}
-
-__device__ __forceinline__ NzIn pad_load(const PadPlan& P, int chunk, int lane, uint64_t pol) {
-  NzIn in;
-  const int k = chunk * kNzChunk + 4 * lane;
-  if (k + 3 < P.e2) {
-    const int4 q = ld_cols_stream(P.ci2 + k, pol);
-    in.c[0] = q.x; in.c[1] = q.y; in.c[2] = q.z; in.c[3] = q.w;
-  } else {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) in.c[u] = k + u < P.e2 ? __ldg(P.ci2 + k + u) : -1;
-  }
-  in.fw = __ldg(reinterpret_cast<const uint4*>(P.flags) + chunk);
-  return in;
-}
-
+// "spmv" (product, round 2): the padded non-zero split (PadPlan, spmv_common.cuh).
 __global__ void __launch_bounds__(256, 4) k_spmv_pad(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                      const int* __restrict__ plan, const float* __restrict__ x,
                                                      float* __restrict__ y, long long N_) {

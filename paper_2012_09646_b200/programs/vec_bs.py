@@ -12,6 +12,17 @@ from .base import Program, grid_1d
 BS_R, BS_V, BS_T, BS_K = 0.08, 0.30, 1.0, 60.0
 
 
+def bs_launch(name):
+    """(block, dynamic shared memory) of a B&S pricing kernel: 256 threads,
+    or for the warp-specialised bs3 forms (csrc/bs_math.cuh bs3_ws_body,
+    named bs3_o<OPT>s<STAGES>b<CTAs/SM>) 8 consumer warps + 1 producer warp
+    and a ring of STAGES chunks of 256 * OPT options in dynamic smem."""
+    if name.startswith("bs3_"):
+        opt, stages = int(name[5]), int(name[7])
+        return 288, stages * 256 * opt * 8
+    return 256, 0
+
+
 # reduce_diff CTAs (deterministic last-block finish over this many partials)
 VEC_RED_CTAS = int(os.environ.get("DAGRT_VEC_RED_CTAS", "1024"))
 

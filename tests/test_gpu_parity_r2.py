@@ -249,7 +249,8 @@ def test_bs_limits(svals):
     c.close()
 
 
-@pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2", "bs2t_o4s4b2", "bs2t_o6s3b2"])
+@pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2", "bs2t_o4s4b2", "bs2t_o6s3b2", "bs3_o6s4b2",
+                                    "bs3_o4s8b2"])
 def test_bs_kernels_limits_and_range(exp, kernel):
     """Every B&S pricing kernel on the limit values plus a dense S sweep over
     [1e-3, 1e4] (log-spaced): deep out of / in the money, d ~ 0, the exp's
@@ -263,7 +264,9 @@ def test_bs_kernels_limits_and_range(exp, kernel):
     torch.cuda.synchronize()
     S = c.register_tensor("s", ts)
     Cc = c.register_tensor("c", tc)
-    c.launch(kernel, 37, 256, S, Cc, n, obs.R, obs.V, obs.T, obs.K)
+    from paper_2012_09646_b200.programs.vec_bs import bs_launch
+    block, smem = bs_launch(kernel)
+    c.launch(kernel, 37, block, S, Cc, n, obs.R, obs.V, obs.T, obs.K, smem=smem)
     c.sync()
     ref = obs.call(s)
     out = tc.cpu().numpy()

@@ -37,6 +37,10 @@ CASES = {
     "one_nonzero": ([0] * 500 + [1] + [0] * 499, 1000),
     "ragged_short": ([1, 2, 3, 0, 4] * 1001 + [5], 7000),
     "exact_chunks": ([4] * 32 * 40, 5000),
+    # every 4-item lane holds a row start, rows spanning two lanes (spmv_pad2's
+    # one-shuffle path) / some lanes inside a row (the full scan)
+    "short_rows": ([1, 2, 2, 1, 3] * 3000, 9000),
+    "lane_spanning": ([5, 1, 6, 2] * 2000, 8000),
 }
 
 
@@ -49,7 +53,7 @@ def ctx():
 
 def run_nz(ctx, rp, ci, x, grid, tag, kernel="spmv"):
     n = len(rp) - 1
-    plan = spmv_pad_plan(rp, ci) if kernel == "spmv" else spmv_nz_plan(rp)
+    plan = spmv_nz_plan(rp) if kernel == "spmv_nz" else spmv_pad_plan(rp, ci)
     ob = 4 * n + 16 + 12 * SPMV_WARPS * grid
     if kernel == "spmv":  # padded items: 4 * N more than E at most
         pass
@@ -69,7 +73,7 @@ def run_nz(ctx, rp, ci, x, grid, tag, kernel="spmv"):
     return outs
 
 
-@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3"])
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("grid", [1, 7, 148 * 6])
 def test_spmv_nz_edge_shapes(ctx, exp, case, grid, kernel):
@@ -84,7 +88,7 @@ def test_spmv_nz_edge_shapes(ctx, exp, case, grid, kernel):
     assert_close(y1.cpu().numpy(), ref, case)
 
 
-@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz"])
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3"])
 @pytest.mark.parametrize("n,e,seed", [(10, 30, 1), (5000, 15000, 3), (300_000, 900_000, 11)])
 def test_spmv_nz_powerlaw(ctx, exp, n, e, seed, kernel):
     rp, ci, _, _ = synth.powerlaw_graph(seed, n, e, device="auto")

@@ -180,11 +180,19 @@ def test_graph_cache_replays_identical_results(mode):
     gctx.close()
 
 
+def bs_launch(name):
+    """(block, dynamic smem) of a B&S kernel: the warp-specialised bs3 forms
+    take 8 consumer warps + a producer and their ring in dynamic smem."""
+    from paper_2012_09646_b200.programs.vec_bs import bs_launch as bl
+    return bl(name)
+
+
 @pytest.mark.parametrize("variant", ["bs_a3b4", "bs_a5b4", "bs_a7b4", "bs_a5b3", "bs_p2b3",
                                      "bs_p1b4", "bs_p2b4", "bs_p1b6", "bs_p4b2", "bs_p4",
                                      "bs_l4b2", "bs_l2b3", "bs_l2b4", "bs_l1b4", "bs_l3b2", "bs_l3b3",
                                      "bs_l8b1", "bs2_p3w2b2", "bs2_p2w2b3", "bs2_p2w4b2", "bs2_p4w2b2",
-                                     "bs2_p1w2b4", "bs2t_o4s4b2", "bs2t_o4s3b3", "bs2t_o2s4b4", "bs2t_o6s3b2"])
+                                     "bs2_p1w2b4", "bs2t_o4s4b2", "bs2t_o4s3b3", "bs2t_o2s4b4", "bs2t_o6s3b2",
+                                     "bs3_o6s4b2", "bs3_o6s6b2", "bs3_o4s8b2", "bs3_o4s6b3", "bs3_o2s8b4"])
 # 227_333: an odd number of full groups for the lean 4-pair loop (ping-pong tail)
 @pytest.mark.parametrize("n", [3, 200_001, 227_333])
 def test_bs_variants_match_oracle(ctx, exp, variant, n):
@@ -198,7 +206,8 @@ def test_bs_variants_match_oracle(ctx, exp, variant, n):
     torch.cuda.synchronize()
     S = ctx.register_tensor(f"bsv_s_{variant}_{n}", s)
     C = ctx.register_tensor(f"bsv_c_{variant}_{n}", c)
-    ctx.launch(variant, 37, 256, S, C, n, obs.R, obs.V, obs.T, obs.K)
+    block, smem = bs_launch(variant)
+    ctx.launch(variant, 37, block, S, C, n, obs.R, obs.V, obs.T, obs.K, smem=smem)
     ctx.sync()
     ref = obs.call(synth.draw(77, "s0", sp["s0"]))
     out = c.cpu().numpy()

@@ -29,12 +29,15 @@ def main():
                         ("bs_l3b2", 2), ("bs_l3b3", 3), ("bs_l8b1", 1),
                         ("bs2_p3w2b2", 2), ("bs2_p2w2b3", 3), ("bs2_p2w4b2", 2), ("bs2_p4w2b2", 2),
                         ("bs2_p1w2b4", 4), ("bs2t_o4s4b2", 2), ("bs2t_o4s3b3", 3), ("bs2t_o2s4b4", 4),
-                        ("bs2t_o6s3b2", 2)):
+                        ("bs2t_o6s3b2", 2), ("bs3_o6s4b2", 2), ("bs3_o6s6b2", 2), ("bs3_o4s8b2", 2),
+                        ("bs3_o4s6b3", 3), ("bs3_o2s8b4", 4)):
         if sel and name not in sel:
             continue
+        from paper_2012_09646_b200.programs.vec_bs import bs_launch
+        block, smem = bs_launch(name)
         for grid_mult in (1, 2, 4):
             grid = 148 * waves * grid_mult
-            L = ctx.prepare(name, grid, 256, [S, Cc, n, 0.08, 0.30, 1.0, 60.0])
+            L = ctx.prepare(name, grid, block, [S, Cc, n, 0.08, 0.30, 1.0, 60.0], smem=smem)
             for _ in range(3):
                 L.raw(st.cuda_stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

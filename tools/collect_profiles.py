@@ -17,7 +17,10 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 
-def main(tag):
+def main(tag, src=None):
+    global OUT
+    if src:
+        OUT = os.path.abspath(src)
     import ncu_summary
     os.makedirs(PROF, exist_ok=True)
     lines = [f"# GPU round {tag}: benchmarks, ncu launch lists, schedule overlap\n"]
@@ -84,6 +87,29 @@ def main(tag):
                                  f"{m['CC']:.2f} | {m['TOT']:.2f} | {m['span_ms']:.3f} |")
             shutil.copy(p, os.path.join(PROF, f"{tag}_{os.path.basename(p)}"))
         lines.append("")
+    ovk = sorted(glob.glob(os.path.join(OUT, "ovk_*.json")))
+    if ovk:
+        lines.append("## Schedule overlap from a CUPTI (kineto) trace (PAPER.md §V-F L1272-1283)\n")
+        lines.append("| bench | mode | policy | CT | TC | CC | TOT | span ms/DAG |")
+        lines.append("|---|---|---|---|---|---|---|---|")
+        for p in ovk:
+            d = json.load(open(p))
+            for pol in ("parallel", "serial"):
+                m = d.get(pol)
+                if m:
+                    lines.append(f"| {d.get('bench')} | {d.get('mode')} | {pol} | {m['CT']:.2f} | {m['TC']:.2f} | "
+                                 f"{m['CC']:.2f} | {m['TOT']:.2f} | {m.get('span_ms', float('nan')):.3f} |")
+            shutil.copy(p, os.path.join(PROF, f"{tag}_{os.path.basename(p)}"))
+        lines.append("")
+    san = sorted(glob.glob(os.path.join(OUT, "sanitize_*.log")))
+    if san:
+        lines.append("## compute-sanitizer (small parity tests of every benchmark)\n")
+        lines.append("```")
+        for p in san:
+            tail = [l for l in open(p).read().splitlines() if "SUMMARY" in l or "passed" in l or l.startswith("rc=")]
+            lines.append(f"{os.path.basename(p)}: " + " | ".join(tail))
+            shutil.copy(p, os.path.join(PROF, f"{tag}_{os.path.basename(p)}"))
+        lines.append("```\n")
     for rep in sorted(glob.glob(os.path.join(OUT, "prof_*.ncu-rep"))):
         import ncu_brief
         buf = io.StringIO()
@@ -118,4 +144,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r1")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1", sys.argv[2] if len(sys.argv) > 2 else None)
