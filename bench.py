@@ -503,7 +503,8 @@ def bench_one(name, args, dist, local, world, peaks, full_report):
     e2e_per = e2e_ms / K
 
     # --- dominant-kernel roofline
-    per_launch = sum(v for k, v in kb.items() if k.startswith(dom)) / max(1, sum(1 for k in kb if k.startswith(dom)))
+    kpre = "bs" if dom == "bs_f32" else dom  # kernel_bytes() labels of the fp32 B&S are bs0..bs9
+    per_launch = sum(v for k, v in kb.items() if k.startswith(kpre)) / max(1, sum(1 for k in kb if k.startswith(kpre)))
     avg_alone = sum_alone / max(1, n_alone)
     if name == "bs":
         # B&S is bound by whichever floor is higher: HBM (16 B/option) or the
@@ -668,7 +669,7 @@ def main():
         "clocks": h["clocks"],
     }
     for k in ("scheduler", "baselines", "speedup_vs_serial_resident", "vs_graph_resident",
-              "speedup_vs_serial_stream", "vs_graph_stream", "contention_free"):
+              "speedup_vs_serial_stream", "vs_graph_stream", "contention_free", "kernel_rooflines"):
         if k in h:
             out[k] = h[k]
     if len(names) > 1:
@@ -680,6 +681,7 @@ def main():
             "vs_graph_resident": geomean([r.get("vs_graph_resident") for r in results.values()]),
             "vs_graph_stream": geomean([r.get("vs_graph_stream") for r in results.values()]),
             "dag_roofline_frac_cp": geomean([r["dag_roofline"]["frac_cp"] for r in results.values()]),
+            "dag_roofline_frac_work": geomean([r["dag_roofline"]["frac_work"] for r in results.values()]),
         }
     print(json.dumps(out))
 

@@ -85,21 +85,45 @@ BS2T_VARIANT(k_bs2t_o6s3b2, 6, 3, 2)
 // FP64-bound").  Accuracy is fp32's (checked against the fp64 oracle with the
 // north_star's fp32 criterion, 1e-4 |o| + 1e-4 rms(o)).  4 options per thread
 // with 128-bit loads/stores, grid-stride.
-__device__ __forceinline__ float bs_price_f32(float s, float r, float v, float t, float k) {
-  const float vst = v * sqrtf(t);
-  const float d1 = (logf(s / k) + (r + 0.5f * v * v) * t) / vst;
-  const float d2 = d1 - vst;
-  auto cnd = [](float d) {
-    const float kk = 1.f / fmaf(0.2316419f, fabsf(d), 1.f);
-    const float p = 0.39894228040143268f * expf(-0.5f * d * d) * kk *
-                    fmaf(kk, fmaf(kk, fmaf(kk, fmaf(kk, 1.330274429f, -1.821255978f), 1.781477937f), -0.356563782f),
-                         0.31938153f);
-    return d > 0.f ? 1.f - p : p;
-  };
-  return s * cnd(d1) - k * expf(-r * t) * cnd(d2);
+// Same algebra as the fp64 pricer: one exponential per option (phi(d2) =
+// phi(d1) S e^{RT}/K), the hardware approximations (MUFU lg2 / ex2 / rcp,
+// ~2^-21 relative) that fp32's criterion allows, constants hoisted per CTA:
+// ~35 instructions per option, so the kernel is HBM-bound (the first fp32
+// version with IEEE divisions and the accurate logf/expf issued ~150 per
+// option and ran at 0.25 of HBM).
+struct BsF32C {
+  float inv_k, inv_vst, mu_s, vst, kexp, c2;
+};
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+__device__ __forceinline__ float bs_price_f32(float s, const BsF32C& C) {
+  const float A = 0.2316419f, R2PI = 0.39894228040143268f;
+  const float d1 = fmaf(__logf(s * C.inv_k), C.inv_vst, C.mu_s);
+  const float d2 = d1 - C.vst;
+  const float phi1 = R2PI * __expf(-0.5f * d1 * d1);
+  const float phi2 = phi1 * (s * C.c2);
+  const float k1 = rcp_approx(fmaf(A, fabsf(d1), 1.f)), k2 = rcp_approx(fmaf(A, fabsf(d2), 1.f));
+  const float q1 = k1 * fmaf(k1, fmaf(k1, fmaf(k1, fmaf(k1, 1.330274429f, -1.821255978f), 1.781477937f), -0.356563782f),
+                             0.31938153f);
+  const float q2 = k2 * fmaf(k2, fmaf(k2, fmaf(k2, fmaf(k2, 1.330274429f, -1.821255978f), 1.781477937f), -0.356563782f),
+                             0.31938153f);
+  const float p1 = phi1 * q1, p2 = phi2 * q2;
+  const float c1 = d1 > 0.f ? 1.f - p1 : p1, cc2 = d2 > 0.f ? 1.f - p2 : p2;
+  return fmaf(s, c1, -C.kexp * cc2);
+}
+
 __global__ void __launch_bounds__(256) k_bs_f32(const float* __restrict__ s, float* __restrict__ c, long long n,
                                                 float r, float v, float t, float k) {
+  BsF32C C;
+  C.vst = v * sqrtf(t);
+  C.inv_vst = 1.f / C.vst;
+  C.mu_s = (r + 0.5f * v * v) * t / C.vst;
+  C.inv_k = 1.f / k;
+  C.kexp = k * expf(-r * t);
+  C.c2 = expf(r * t) / k;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   long long done = 0;
@@ -107,12 +131,12 @@ __global__ void __launch_bounds__(256) k_bs_f32(const float* __restrict__ s, flo
     const long long n4 = n >> 2;
     for (long long i = tid; i < n4; i += nth) {
       const float4 x = ldg_stream(reinterpret_cast<const float4*>(s) + i);
-      reinterpret_cast<float4*>(c)[i] = make_float4(bs_price_f32(x.x, r, v, t, k), bs_price_f32(x.y, r, v, t, k),
-                                                    bs_price_f32(x.z, r, v, t, k), bs_price_f32(x.w, r, v, t, k));
+      reinterpret_cast<float4*>(c)[i] =
+          make_float4(bs_price_f32(x.x, C), bs_price_f32(x.y, C), bs_price_f32(x.z, C), bs_price_f32(x.w, C));
     }
     done = n4 << 2;
   }
-  for (long long i = done + tid; i < n; i += nth) c[i] = bs_price_f32(s[i], r, v, t, k);
+  for (long long i = done + tid; i < n; i += nth) c[i] = bs_price_f32(s[i], C);
 }
 
 // launch contracts (dagrt_launch validates them; builtin.h LaunchCheck)

@@ -728,6 +728,7 @@ struct ArrayRec {
   bool live = false;
   bool mapped = false;
   bool managed = false;             // unified memory: dev == host, no copies (dagrt_array_register_managed)
+  bool host_touched = false;        // managed: the host accessed it since the last device prefetch
   int64_t last_writer = -1;         // GLOBAL vertex id of the last kernel writer, -1 = none/host
   std::vector<int64_t> readers;     // global ids of the readers since the last writer (pruned lazily)
   uint8_t coh = COH_DEVICE;
@@ -1188,7 +1189,14 @@ dagrt_status d2h_mapped(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* ds
 
 dagrt_status d2h(dagrt_ctx c, ArrayRec* a, size_t off, size_t n, void* dst) {
   if (n == 0) return DAGRT_OK;
-  if (a->managed) {  // the host reads unified memory in place (page faults move it)
+  if (a->managed) {  // the host reads unified memory in place
+    a->host_touched = true;
+    if (c->cfg.prefetch) {  // move the range to the host first (DMA) instead of CPU page faults
+      c->st.um_prefetch_bytes += n;
+      CK(c->be->prefetch(a->dev + off, n, cudaCpuDeviceId, c->d2h_stream), "cudaMemPrefetchAsync to host");
+      CK(c->be->stream_sync(c->d2h_stream), "cudaStreamSynchronize D2H");
+      c->st.host_syncs++;
+    }
     if (c->be->real() && dst != a->dev + off) memcpy(dst, a->dev + off, n);
     return DAGRT_OK;
   }
@@ -1471,6 +1479,7 @@ dagrt_status dagrt_array_register_managed(dagrt_ctx c, void* ptr, size_t bytes, 
   if (dagrt_status s = dagrt_array_register(c, ptr, ptr, bytes, out)) return s;
   ArrayRec* a = get_array(c, *out);
   a->managed = true;
+  a->host_touched = true;  // where its pages are is unknown
   a->coh = COH_BOTH;
   if (c->be->enabled) {  // prefetches are issued eagerly: no graph cache in UM mode
     CK(c->be->flush(), "graph cache flush");
@@ -1751,6 +1760,23 @@ dagrt_status enqueue(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dim3 g, dim3 b,
   return DAGRT_OK;
 }
 
+// Does argument a of a vertex need a transfer before the vertex runs?  A
+// mirrored array: it is read (need) and the host copy is newer.  A managed
+// array (UM mode, D13): with prefetch on, whenever the host touched it since
+// the last prefetch -- reads AND writes, since pages left on the host would
+// otherwise be faulted in by the kernel; with prefetch off never (the faults
+// are the mode), counting the host-newer bytes the kernel will fault in.
+static bool transfer_needed(dagrt_ctx c, ArrayRec* a, bool need) {
+  if (!a->bytes || !a->host) return false;
+  if (!a->managed) return need && a->coh == COH_HOST;
+  if (c->cfg.prefetch) return a->host_touched;
+  if (need && a->coh == COH_HOST) {
+    c->st.um_fault_bytes += a->bytes;
+    a->coh = COH_BOTH;
+  }
+  return false;
+}
+
 dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
                            uint32_t smem, void** argv, ArrayRec* const* arrs, const uint8_t* kinds, int32_t nargs,
                            dagrt_library_fn lib, void* user, std::chrono::steady_clock::time_point t0) {
@@ -1781,12 +1807,7 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
     void* s = c->serial_stream;
     for (int j = 0; j < nacc; ++j) {
       ArrayRec* a = acc[j];
-      if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
-        if (a->managed && !c->cfg.prefetch) {  // UM without prefetch: the kernel faults the pages in
-          c->st.um_fault_bytes += a->bytes;
-          a->coh = COH_BOTH;
-          continue;
-        }
+      if (transfer_needed(c, a, need[j])) {
         trace_op(c, DAGRT_OP_H2D, -3, array_index(c, a), 0, a->bytes);
         c->st.h2d_bytes += a->bytes;
         c->st.h2d_copies++;
@@ -1802,7 +1823,8 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
           CK(c->be->stream_sync(s), "cudaStreamSynchronize");
           c->st.host_syncs++;
         }
-        a->coh = COH_BOTH;
+        if (need[j]) a->coh = COH_BOTH;
+        a->host_touched = false;
       }
     }
     trace_op(c, DAGRT_OP_LAUNCH, -3, gvid, kh, 0);
@@ -1843,12 +1865,7 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
   for (int j = 0; j < nacc; ++j) {
     ArrayRec* a = acc[j];
     if (a->h2d_pending && !is_active(c, a->h2d_consumer)) a->h2d_pending = false;
-    if (need[j] && a->host && a->coh == COH_HOST && a->bytes) {
-      if (a->managed && !c->cfg.prefetch) {  // UM without prefetch: the kernel faults the pages in
-        c->st.um_fault_bytes += a->bytes;
-        a->coh = COH_BOTH;
-        continue;
-      }
+    if (transfer_needed(c, a, need[j])) {
       void* cs = c->cfg.prefetch ? c->copy_stream : s;
       trace_op(c, DAGRT_OP_H2D, c->cfg.prefetch ? -2 : sid, array_index(c, a), 0, a->bytes);
       c->st.h2d_bytes += a->bytes;
@@ -1863,7 +1880,8 @@ dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim
       if (dagrt_status st_ = tl_end(c, cs, t0, 1, c->cfg.prefetch ? -2 : sid, gvid, array_index(c, a),
                                     a->bytes))
         return st_;
-      a->coh = COH_BOTH;
+      if (need[j]) a->coh = COH_BOTH;
+      a->host_touched = false;
       // the copy's event orders every later reader on another stream after
       // it (with prefetch off the copy runs on this consumer's own stream, so
       // only those other readers wait)
@@ -1950,6 +1968,7 @@ dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t byte
   if (c->cfg.policy != DAGRT_SERIAL_SYNC)
     if (dagrt_status s = host_sync_parents(c, a, false, copy ? c->d2h_stream : nullptr)) return s;
   if (!a->host) return d2h(c, a, off, bytes, dst);
+  if (a->managed) a->host_touched = true;
   if (a->coh == COH_DEVICE) {
     if (dagrt_status s = d2h(c, a, off, bytes, a->host + off)) return s;
     if (off == 0 && bytes == a->bytes) a->coh = COH_BOTH;
@@ -1962,6 +1981,7 @@ static dagrt_status host_write_prepare(dagrt_ctx c, ArrayRec* a, bool whole) {
   if (c->cfg.policy != DAGRT_SERIAL_SYNC) {
     if (dagrt_status s = host_sync_parents(c, a, true)) return s;
   }
+  if (a->managed) a->host_touched = true;
   if (a->h2d_pending) {  // the copy engine may still read the mirror
     CK(c->be->event_sync(a->h2d_ev), "cudaEventSynchronize copy");
     a->h2d_pending = false;
@@ -2025,6 +2045,7 @@ dagrt_status dagrt_host_map(dagrt_ctx c, dagrt_array h, int32_t access, void** h
     }
   }
   a->mapped = true;
+  if (a->managed) a->host_touched = true;
   *host_ptr = a->host;
   return DAGRT_OK;
 }

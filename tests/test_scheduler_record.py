@@ -518,10 +518,13 @@ def test_history_driven_launch_configuration_record():
 @pytest.mark.parametrize("prefetch", [True, False])
 def test_unified_memory_arrays(prefetch):
     """Managed arrays (dagrt_array_register_managed, the UM mode of PAPER.md
-    §V-C): the DAG is the same as with mirrors; a host-newer input is
-    prefetched on the copy stream (an H2D op in the trace, counted in
-    um_prefetch_bytes) or left to page faults (no transfer op at all,
-    um_fault_bytes); host reads never copy."""
+    §V-C, reading D13): the DAG is the same as with mirrors.  With
+    prefetch, every managed argument the host touched since its last prefetch
+    -- reads and writes, pages on the host would be faulted in -- is moved by a
+    prefetch on the copy stream (an h2d op in the trace), and a host read of
+    device-newer data is prefetched to the host first; without prefetch no
+    transfer is issued (um_fault_bytes counts the host-newer bytes left to
+    page faults).  Host reads never copy (no d2h op)."""
     ctx = D.Context(backend="record", record_dag=True, prefetch=prefetch)
     bufs = [(C.c_char * 256)() for _ in range(2)]  # the recorder never touches them
     x = ctx.register_managed("x", C.addressof(bufs[0]), 256)
@@ -530,18 +533,24 @@ def test_unified_memory_arrays(prefetch):
     src = (C.c_char * 256)()
     ctx.host_write(x, C.addressof(src), 0, 256)  # host newer
     ctx.prepare(k, 1, 32, [x, y])()
-    ctx.host_read(y, C.addressof(src), 0, 256)
-    ops = [t[0] for t in ctx.trace()]
     st = ctx.stats()
-    if prefetch:
-        assert ops.count("h2d") == 1 and st["um_prefetch_bytes"] == 256 and st["um_fault_bytes"] == 0
+    if prefetch:  # x (host-written) and y (never prefetched since registration)
+        assert [t[0] for t in ctx.trace()].count("h2d") == 2 and st["um_prefetch_bytes"] == 512
+        assert st["um_fault_bytes"] == 0
     else:
-        assert "h2d" not in ops and st["um_fault_bytes"] == 256 and st["um_prefetch_bytes"] == 0
-    assert "d2h" not in ops and st["d2h_copies"] == 0
+        assert "h2d" not in [t[0] for t in ctx.trace()]
+        assert st["um_fault_bytes"] == 256 and st["um_prefetch_bytes"] == 0
+    ctx.host_read(y, C.addressof(src), 0, 256)  # device newer: prefetched to the host first (prefetch on)
+    st = ctx.stats()
+    assert st["um_prefetch_bytes"] == (768 if prefetch else 0)
+    assert "d2h" not in [t[0] for t in ctx.trace()] and st["d2h_copies"] == 0
     v, e = ctx.dag()
     assert [t[1] for t in v] == ["kernel", "host"] and len(e) == 1
-    # a second launch reading x finds it current: nothing moves
+    # again: x is current on the device; y was touched by the host read
     ctx.prepare(k, 1, 32, [x, y])()
     st2 = ctx.stats()
-    assert st2["um_prefetch_bytes"] + st2["um_fault_bytes"] == 256
+    if prefetch:
+        assert st2["um_prefetch_bytes"] == 1024
+    else:
+        assert st2["um_fault_bytes"] == 256
     ctx.close()
