@@ -1005,7 +1005,185 @@ __global__ void __launch_bounds__(256, 3) k_spmv_pad2b3(const int* __restrict__,
   spmv_pad2_body<3>(plan, x, y, N_);
 }
 
+// ---------------------------------------------------------------------------
+// spmv_ws: the padded non-zero split with the gathers and the row logic on
+// DIFFERENT warps.  ncu on the product (profiles/r2_*): the gathers are
+// bounded by the L1/L2 request rate (lab floor 177 us for the 57M gathers +
+// the column stream), and each warp's chunk carries a long dependent chain
+// (flags -> popc -> ballot -> 5-step shuffle scan -> stores) that leaves the
+// request pipe idle when all warps of a scheduler sit in their chains.  Here
+// a CTA holds 4 producer warps that only load columns and gather x into a
+// per-pair shared ring (TWO chunks per step: 8 gathers in flight per lane),
+// and 4 consumer warps that reduce the staged values exactly like the
+// product (same rows, same deposits, same summation order: bit-identical).
+// Producer p serves consumer p over the consumer's chunk range; each ring
+// slot has a full and an empty mbarrier (32 arrivals each: every lane
+// arrives after its own shared-memory accesses).
+constexpr int kWsPairs = 4;     // producer/consumer warp pairs per CTA
+constexpr int kWsSlots = 8;     // ring slots per pair (one chunk each)
+struct WsSlot {
+  float4 v[32];   // the chunk's 128 gathered values, lane-major
+  uint4 fw;       // its 4 flag words
+};
+__device__ __forceinline__ void ws_mbar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(n));
+}
+__device__ __forceinline__ void ws_mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void ws_mbar_wait(uint64_t* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 4) k_spmv_ws(const int* __restrict__, const int* __restrict__,
+                                                    const int* __restrict__ plan, const float* __restrict__ x,
+                                                    float* __restrict__ y, long long N_) {
+  __shared__ WsSlot ring[kWsPairs][kWsSlots];
+  __shared__ uint64_t full[kWsPairs][kWsSlots], empty[kWsPairs][kWsSlots];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pair = warp & (kWsPairs - 1);
+  const bool producer = warp >= kWsPairs;
+  if (threadIdx.x < kWsPairs * kWsSlots) {
+    ws_mbar_init(&full[0][0] + threadIdx.x, 32);
+    ws_mbar_init(&empty[0][0] + threadIdx.x, 32);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const PadPlan P = pad_plan(plan);
+  if ((long long)P.n != N_ || P.n == 0 || blockDim.x != 2 * 32 * kWsPairs) return;
+  const int G = (int)gridDim.x * kWsPairs;  // consumer warps of the grid
+  const int g = (int)blockIdx.x * kWsPairs + pair;
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;  // both warps of the pair leave together; no CTA barrier below
+  WsSlot* R = ring[pair];
+  if (producer) {
+    const uint64_t pol = l2_policy_evict_first();
+    int it = 0;
+    for (int c = cb; c < ce; c += 2, it += 2) {
+      const bool two = c + 1 < ce;
+      NzIn a = pad_load(P, c, lane, pol), b = a;
+      if (two) b = pad_load(P, c + 1, lane, pol);
+      float va[4], vb[4];
+      nz_gather(a, x, va);
+      if (two) nz_gather(b, x, vb);
+      const int s0 = it % kWsSlots, s1 = (it + 1) % kWsSlots;
+      if (it >= kWsSlots) ws_mbar_wait(&empty[pair][s0], (unsigned)((it / kWsSlots - 1) & 1));
+      R[s0].v[lane] = make_float4(va[0], va[1], va[2], va[3]);
+      if (lane == 0) R[s0].fw = a.fw;
+      ws_mbar_arrive(&full[pair][s0]);
+      if (two) {
+        if (it + 1 >= kWsSlots) ws_mbar_wait(&empty[pair][s1], (unsigned)(((it + 1) / kWsSlots - 1) & 1));
+        R[s1].v[lane] = make_float4(vb[0], vb[1], vb[2], vb[3]);
+        if (lane == 0) R[s1].fw = b.fw;
+        ws_mbar_arrive(&full[pair][s1]);
+      }
+    }
+    return;
+  }
+  // consumer: the product's per-chunk reduction on staged values
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  auto warp_of_item = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);
+  bool head_pending = !start0;
+  float carry = 0.f;
+  int it = 0;
+  for (int c = cb; c < ce; ++c, ++it) {
+    const int sl = it % kWsSlots;
+    ws_mbar_wait(&full[pair][sl], (unsigned)((it / kWsSlots) & 1));
+    const float4 q = R[sl].v[lane];
+    uint4 fw = R[sl].fw;
+    ws_mbar_arrive(&empty[pair][sl]);
+    float v[4] = {q.x, q.y, q.z, q.w};
+    if (c == cb) fw.x &= ~1u;
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
+    const int nst = __popc(fl);
+    const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                       (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+    const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+    const int o = R0 + before;
+    float run = 0.f, head = 0.f;
+    bool seen = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((fl >> u) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.f;
+      }
+      run += v[u];
+    }
+    if (!seen) head = run;
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
+    float sv = nst ? run : head;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+      const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+      if (win == 0u) sv += tv;
+    }
+    float cin = __shfl_up_sync(0xffffffffu, sv, 1);
+    if (lane == 0) cin = 0.f;
+    if ((m & lanes_below) == 0u) cin += carry;
+    if (nst) {
+      const float val = cin + head;
+      if (head_pending && before == 0) {
+        const int cs = warp_of_item(__ldg(P.rp2 + o));
+        spmv_ws_put(ws, g, val, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[o] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[o] = val;
+      }
+      int j = 1;
+      float r2 = 0.f;
+      bool in = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (in) y[o + j++] = r2;
+          in = true;
+          r2 = 0.f;
+        }
+        r2 += v[u];
+      }
+    }
+    const float tail_all = __shfl_sync(0xffffffffu, sv, 31);
+    carry = m ? tail_all : carry + tail_all;
+    if (m) head_pending = false;
+    R0 += total;
+  }
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= P.e2 || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    if (ends_here) {
+      if (head_pending) {
+        const int cs = warp_of_item(__ldg(P.rp2 + R0));
+        spmv_ws_put(ws, g, carry, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[R0] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[R0] = carry;
+      }
+    } else {
+      const int cs = warp_of_item(__ldg(P.rp2 + R0));
+      const int cend = warp_of_item(__ldg(P.rp2 + R0 + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      if (spmv_ws_arrive(ws, cs, cend)) y[R0] = spmv_ws_sum(ws, cs, cend);
+    }
+  }
+}
+
 static const Builtin kHitsExp[] = {
+    {"spmv_ws", (const void*)k_spmv_ws, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2", (const void*)k_spmv_pad2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2b3", (const void*)k_spmv_pad2b3, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_nz", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},

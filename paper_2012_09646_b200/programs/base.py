@@ -19,7 +19,8 @@ Modes:
   inputs' pages are moved to the host before each run (restart(), outside
   the timed region: the host rewrote them), the run either prefetches them
   (context prefetch on: cudaMemPrefetchAsync) or leaves them to GPU page
-  faults (prefetch off), and the host reads whole sinks in place.
+  faults (prefetch off), and the host maps whole sinks in place (with
+  prefetch on, the runtime moves them to the host first).
 """
 from __future__ import annotations
 
@@ -170,14 +171,6 @@ class Program:
 
     def end_run(self):
         """Host reads of the sinks: one element (resident) or whole arrays (stream)."""
-        if self.um:  # the host reads the managed sinks in place (into host buffers)
-            if getattr(self, "_um_out", None) is None:
-                self._um_out = {n: torch.empty(self.a[n].nbytes, dtype=torch.uint8, pin_memory=not self.record)
-                                for n in self.sinks}
-            for n in self.sinks:
-                nb = min(4, self.a[n].nbytes) if n in self.red else self.a[n].nbytes
-                self.ctx.host_read(self.a[n], self._um_out[n].data_ptr(), 0, nb)
-            return
         if not self.streaming:
             if getattr(self, "_reads", None) is None:  # arguments converted once
                 self._reads = [self.ctx.prepare_read(self.a[n], C.addressof(self._scalar), 0,
