@@ -35,7 +35,31 @@
 #include "../../include/dagrt.h"
 #include "builtin.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace dagrt {
+
+// NVTX ranges (domain "dagrt") around launches, host accesses, barriers and
+// graph-cache flushes: a profiler (nsys / ncu --nvtx) shows the scheduler's
+// host timeline next to the GPU work.  Header-only NVTX3: without a tool
+// attached every call is a null-pointer check.
+static nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("dagrt");
+  return d;
+}
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t a{};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(nvtx_domain(), &a);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ------------------------------------------------------------ builtin registry
 static std::vector<Builtin>& registry() {
@@ -599,6 +623,7 @@ struct DeferBackend final : Backend {
   }
 
   cudaError_t flush() {
+    NvtxRange nvtx_("dagrt_graph_cache_flush");
     if (ops.empty()) return cudaSuccess;
     if (!origin)
       if (cudaError_t e = in->stream_create(&origin)) return e;
@@ -1780,6 +1805,7 @@ static bool transfer_needed(dagrt_ctx c, ArrayRec* a, bool need) {
 dagrt_status launch_vertex(dagrt_ctx c, KernelRec* k, dagrt_kernel kh, dagrt_dim3 grid, dagrt_dim3 block,
                            uint32_t smem, void** argv, ArrayRec* const* arrs, const uint8_t* kinds, int32_t nargs,
                            dagrt_library_fn lib, void* user, std::chrono::steady_clock::time_point t0) {
+  NvtxRange nvtx_(k->name.c_str());
 
   // merged access per distinct array (D3): write if any use writes,
   // needs data if any use reads (const / inout)
@@ -1957,6 +1983,7 @@ dagrt_status dagrt_launch_batch(dagrt_ctx c, const dagrt_launch_desc* d, int32_t
 }
 
 dagrt_status dagrt_host_read(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes, void* dst) {
+  NvtxRange nvtx_("dagrt_host_read");
   GUARD(c);
   ArrayRec* a = get_array(c, h);
   if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
@@ -1993,6 +2020,7 @@ static dagrt_status host_write_prepare(dagrt_ctx c, ArrayRec* a, bool whole) {
 
 dagrt_status dagrt_host_write(dagrt_ctx c, dagrt_array h, size_t off, size_t bytes,
                               const void* src) {
+  NvtxRange nvtx_("dagrt_host_write");
   GUARD(c);
   ArrayRec* a = get_array(c, h);
   if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
@@ -2021,6 +2049,7 @@ dagrt_status dagrt_host_write(dagrt_ctx c, dagrt_array h, size_t off, size_t byt
 }
 
 dagrt_status dagrt_host_map(dagrt_ctx c, dagrt_array h, int32_t access, void** host_ptr) {
+  NvtxRange nvtx_("dagrt_host_map");
   GUARD(c);
   ArrayRec* a = get_array(c, h);
   if (!a) return fail(c, DAGRT_ENOTFOUND, "array handle");
@@ -2060,6 +2089,7 @@ dagrt_status dagrt_host_unmap(dagrt_ctx c, dagrt_array h) {
 }
 
 dagrt_status dagrt_sync(dagrt_ctx c) {
+  NvtxRange nvtx_("dagrt_sync");
   GUARD(c);
   for (size_t s = 0; s < c->streams.size(); ++s) {
     trace_op(c, DAGRT_OP_STREAM_SYNC, (int32_t)s, 0, 0, 0);
@@ -2360,6 +2390,7 @@ dagrt_status dagrt_graph_instantiate(dagrt_ctx c, dagrt_graph g) {
 }
 
 dagrt_status dagrt_graph_run(dagrt_ctx c, dagrt_graph g, int32_t wait) {
+  NvtxRange nvtx_("dagrt_graph_run");
   GUARD(c);
   if (!g || !g->r.exec) return fail(c, DAGRT_ESTATE, "graph not instantiated");
   CK(cudaGraphLaunch(g->r.exec, (cudaStream_t)c->graph_stream), "cudaGraphLaunch");
