@@ -1182,7 +1182,14 @@ __global__ void __launch_bounds__(256, 4) k_spmv_ws(const int* __restrict__, con
   }
 }
 
+__global__ void __launch_bounds__(256, 4) k_spmv_pad_l2(const int* __restrict__, const int* __restrict__,
+                                                        const int* __restrict__ plan, const float* __restrict__ x,
+                                                        float* __restrict__ y, long long N_) {
+  spmv_pad_body<true>(plan, x, y, N_);
+}
+
 static const Builtin kHitsExp[] = {
+    {"spmv_pad_l2", (const void*)k_spmv_pad_l2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_ws", (const void*)k_spmv_ws, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2", (const void*)k_spmv_pad2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2b3", (const void*)k_spmv_pad2b3, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},

@@ -187,6 +187,144 @@ __device__ __forceinline__ NzIn pad_load(const PadPlan& P, int chunk, int lane, 
   return in;
 }
 
+template <bool HINTS>
+__device__ __forceinline__ void nz_gather_h(const NzIn& in, const float* __restrict__ x, float (&v)[4], uint64_t keep) {
+  if (!HINTS) {
+    nz_gather(in, x, v);
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = in.c[u] >= 0 ? ldg_hint(x + in.c[u], keep) : 0.f;
+}
+
+// The padded non-zero split (k_spmv_pad, kernels_hits.cu).  HINTS: the
+// gathers carry an L2 evict_last policy and the y stores evict_first, so the
+// streamed output does not push the gathered vector out of L2 (an
+// experimental form, exp/spmv_variants.cu).
+template <bool HINTS>
+__device__ __forceinline__ void spmv_pad_body(const int* __restrict__ plan, const float* __restrict__ x,
+                                              float* __restrict__ y, long long N_) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PadPlan P = pad_plan(plan);
+  if ((long long)P.n != N_ || P.n == 0) return;
+  const int G = (int)gridDim.x * (blockDim.x >> 5);
+  const int g = (int)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;  // warp-uniform; the kernel has no CTA barriers
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  const uint64_t pol = l2_policy_evict_first();
+  const uint64_t keep = HINTS ? l2_policy_evict_last() : 0;
+  auto store = [&](int i, float v) {
+    if (HINTS)
+      asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(y + i), "f"(v), "l"(pol) : "memory");
+    else
+      y[i] = v;
+  };
+  auto warp_of_item = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
+
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);  // row open at the current chunk's start
+  bool head_pending = !start0;   // ... which began in an earlier warp's range
+  float carry = 0.f;
+
+  NzIn cur = pad_load(P, cb, lane, pol);
+  NzIn nxt = cur;
+  if (cb + 1 < ce) nxt = pad_load(P, cb + 1, lane, pol);
+  float v[4];
+  nz_gather_h<HINTS>(cur, x, v, keep);
+  for (int c = cb; c < ce; ++c) {
+    uint4 fw = cur.fw;
+    if (c == cb) fw.x &= ~1u;  // the range's first item: handled by start0/head_pending
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
+    const int nst = __popc(fl);
+    const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                       (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+    const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+    const int o = R0 + before;  // row open entering the lane; ends at its first start
+    float vn[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c + 1 < ce) {
+      nz_gather_h<HINTS>(nxt, x, vn, keep);
+      cur = nxt;
+      if (c + 2 < ce) nxt = pad_load(P, c + 2, lane, pol);
+    }
+    float run = 0.f, head = 0.f;
+    bool seen = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((fl >> u) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.f;
+      }
+      run += v[u];
+    }
+    if (!seen) head = run;
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
+    float sv = nst ? run : head;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+      const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+      if (win == 0u) sv += tv;
+    }
+    float cin = __shfl_up_sync(0xffffffffu, sv, 1);
+    if (lane == 0) cin = 0.f;
+    if ((m & lanes_below) == 0u) cin += carry;
+    if (nst) {
+      const float val = cin + head;
+      if (head_pending && before == 0) {
+        const int cs = warp_of_item(__ldg(P.rp2 + o));
+        spmv_ws_put(ws, g, val, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[o] = spmv_ws_sum(ws, cs, g);
+      } else {
+        store(o, val);
+      }
+      int j = 1;
+      float r2 = 0.f;
+      bool in = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (in) store(o + j++, r2);
+          in = true;
+          r2 = 0.f;
+        }
+        r2 += v[u];
+      }
+    }
+    const float tail_all = __shfl_sync(0xffffffffu, sv, 31);
+    carry = m ? tail_all : carry + tail_all;
+    if (m) head_pending = false;
+    R0 += total;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = vn[u];
+  }
+  // the row open at the range end
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= P.e2 || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    if (ends_here) {
+      if (head_pending) {  // spans the whole range, ends at its end
+        const int cs = warp_of_item(__ldg(P.rp2 + R0));
+        spmv_ws_put(ws, g, carry, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[R0] = spmv_ws_sum(ws, cs, g);
+      } else {
+        store(R0, carry);
+      }
+    } else {
+      const int cs = warp_of_item(__ldg(P.rp2 + R0));
+      const int cend = warp_of_item(__ldg(P.rp2 + R0 + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      if (spmv_ws_arrive(ws, cs, cend)) y[R0] = spmv_ws_sum(ws, cs, cend);
+    }
+  }
+}
+
 // launch contract of the plan-driven kernels (builtin.h LaunchCheck)
 static inline const char* v_spmv_plan_kernel(const LaunchCheck& L) {  // row_ptr, col, plan, x, y, N
   const int64_t N = L.i(5);
