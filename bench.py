@@ -71,7 +71,7 @@ FULL = {
 DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1",
             "bs_f32": "bs_f32"}
 # device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
-KSYM = {"square": "k_square", "bs": "k_bs2t_o6s3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv_pad",
+KSYM = {"square": "k_square", "bs": "k_bs2l_o6s3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv_pad",
         "conv1": "k_conv1_r2b3", "conv2": "k_conv2_h", "bs_f32": "k_bs_f32"}
 DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32", "bs_f32": "f32"}
 WORKLOAD = {
@@ -89,7 +89,7 @@ SMS = 148
 # dynamic instruction counts, profiles/) and the FP64 pipe's peak per SM per
 # clock (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained;
 # confirmed by the DFMA probe: 63.3 ops/clk/SM, profiles/r1_box_peaks.json).
-BS_FP64_OPS_PER_OPTION = 39  # k_bs2t_o6s3b2 main loop: 234 DFMA+DMUL+DADD per 6 options (cuobjdump)
+BS_FP64_OPS_PER_OPTION = 37.5  # k_bs2l_o6s3b2: 39.5 DFMA+DMUL+DADD per option in ncu for the bs2t pricer, minus the two series terms the lean tables drop
 FP64_OPS_PER_SM_CLK = 64
 
 

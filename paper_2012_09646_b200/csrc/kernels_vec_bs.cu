@@ -72,11 +72,13 @@ __global__ void __launch_bounds__(256) k_reduce_diff(const float* __restrict__ x
 namespace dagrt {
 
 // ---------------------------------------------------------------- B&S product
-// 38-39 FP64 ops per option (bs_price_w), inputs streamed by cp.async.bulk
-// into a 3-stage shared-memory ring, 6 options per thread in lockstep, 2
-// CTAs/SM one wave (bs2_tma_body, bs_math.cuh).  The round-1 kernels and the
-// other tuning variants are in exp/bs_variants.cu (libdagrt_exp.so).
-BS2T_VARIANT(k_bs2t_o6s3b2, 6, 3, 2)
+// 37.5 FP64 ops per option (the lean pricer bs_price_l: 512-entry log and
+// 128-entry exp tables), inputs streamed by cp.async.bulk into a 3-stage
+// shared-memory ring, 6 options per thread in lockstep, 2 CTAs/SM one wave
+// (bs2_tma_body, bs_math.cuh): 40.3 us per 10M options vs 41.6 for the same
+// body with the round-2 pricer (bs2t_o6s3b2), tools/bs_variants.py.  The
+// round-1 kernels and the other tuning variants are in exp/bs_variants.cu.
+BS2L_VARIANT(k_bs2l_o6s3b2, 6, 3, 2)
 
 // ---------------------------------------------------------------- B&S in fp32 (f4)
 // The same pricing (A&S 26.2.17 CND) in fp32 storage and
@@ -174,11 +176,11 @@ static const Builtin kVecBs[] = {
     // product: lean loop, 3 pairs per thread, 2 CTAs/SM, one wave (44.8 us per
     // 10M options vs 46.2 for 4 pairs (k_bs_l4b2) in three back-to-back runs,
     // 49.5 for k_bs, tools/bs_variants.py); k_bs kept as "bs_p4"
-    // product (round 2): 38-39 FP64 ops per option (algebraic pricer), inputs
-    // streamed by cp.async.bulk into a 3-stage ring, 6 options per thread in
-    // lockstep, 2 CTAs/SM one wave: 40.5 us per 10M options vs 45.8 for the
-    // round-1 product (bs_l3b2) in the same run (tools/bs_variants.py)
-    {"bs", (const void*)k_bs2t_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, 0,
+    // product (round 2): 37.5 FP64 ops per option (lean algebraic pricer),
+    // inputs streamed by cp.async.bulk into a 3-stage ring, 6 options per
+    // thread in lockstep, 2 CTAs/SM one wave: 40.3 us per 10M options vs 45.8
+    // for the round-1 product (bs_l3b2), tools/bs_variants.py
+    {"bs", (const void*)k_bs2l_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, 0,
      nullptr, v_bs},
     // f4: the same pricing in fp32 (HBM-bound)
     {"bs_f32", (const void*)k_bs_f32, "const ptr, out ptr, sint64, float, float, float, float", KF_NONE, 0, nullptr,
