@@ -93,6 +93,8 @@ struct BsConst {
   double inv_k;    // 1 / K
   double c2;       // e^{RT} / K
   double kexp;     // K e^{-RT}
+  double mu_lnk;   // mu_s - ln(K) / (V sqrt T): d1 from ln S directly (lean pricer)
+  double nkexp;    // -K e^{-RT}
 };
 
 __device__ __forceinline__ double bs_price(double s, const BsConst& C, const BsTables& T) {
@@ -220,8 +222,12 @@ __device__ __forceinline__ void bs_price_w(const double (&s)[W], double (&out)[W
 // Lean pricer: the same formulas with larger tables so that both series
 // lose a term: a 512-entry log table (|r| <= 2^-10: ln(1+r) to r^3, the
 // dropped r^4/4 is < 2.3e-13 absolute) and a 128-entry exp table (|r2/2| <=
-// ln2/256: e^{-r2/2} to r2^3, the dropped term < 2.2e-12 relative) -- 37.5
-// instead of 39.5 FP64 instructions per option.  Tables: 9 KB of shared memory.
+// ln2/256: e^{-r2/2} to r2^3, the dropped term < 2.2e-12 relative); ln S
+// instead of ln(S/K) (ln K folded into the constant term of d1) and
+// C = S (e1 m + u1) - K e^{-RT} u2 with the indicators as selected constants
+// and the CND signs applied to k before one DFMA sums the two terms -- 34
+// instead of 39 FP64 instructions per option in the main loop.  Tables: 9 KB of
+// shared memory.
 struct BsTabsL {
   double inv[512];
   double lninv[512];
@@ -260,7 +266,7 @@ __device__ __forceinline__ void bs_price_l(const double (&s)[W], double (&out)[W
   double d1[W], d2[W], h[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) {
-    d1[w] = fma(bs_log_l(s[w] * C.inv_k, T), C.inv_vst, C.mu_s);
+    d1[w] = fma(bs_log_l(s[w], T), C.inv_vst, C.mu_lnk);  // ln(S/K) = ln S - ln K, folded into mu
     d2[w] = d1[w] - C.vst;
     h[w] = d1[w] * d1[w];
   }
@@ -299,14 +305,16 @@ __device__ __forceinline__ void bs_price_l(const double (&s)[W], double (&out)[W
     q2 = fma(k2[w], q2, B2);
     q1 = fma(k1[w], q1, B1);
     q2 = fma(k2[w], q2, B1);
-    const double w1 = q1 * k1[w], w2 = q2 * k2[w];
     const bool u1 = __double2hiint(d1[w]) > 0, u2 = __double2hiint(d2[w]) > 0;
-    const double a1 = __hiloint2double(__double2hiint(w1) ^ (u1 ? 0x80000000 : 0), __double2loint(w1));
-    const double a2 = __hiloint2double(__double2hiint(w2) ^ (u2 ? 0 : 0x80000000), __double2loint(w2));
-    const double m = a1 + a2;
-    const double sk = s[w] - C.kexp;
-    const double base = u2 ? sk : (u1 ? s[w] : 0.0);
-    out[w] = fma(s[w] * e1[w], m, base);
+    // m = sigma1 q1 k1 - sigma2 q2 k2 with the signs on k (integer pipe) and
+    // one DFMA for the sum: two FP64 instructions instead of three
+    const double k1s = __hiloint2double(__double2hiint(k1[w]) ^ (u1 ? 0x80000000 : 0), __double2loint(k1[w]));
+    const double k2s = __hiloint2double(__double2hiint(k2[w]) ^ (u2 ? 0 : 0x80000000), __double2loint(k2[w]));
+    const double m = fma(q1, k1s, q2 * k2s);
+    // C = S (e1 m + u1) - K e^{-RT} u2: the indicators as selected constants
+    const double u1d = __hiloint2double(u1 ? 0x3FF00000 : 0, 0);
+    const double nk = __hiloint2double(u2 ? __double2hiint(C.nkexp) : 0, u2 ? __double2loint(C.nkexp) : 0);
+    out[w] = fma(s[w], fma(e1[w], m, u1d), nk);
   }
 }
 
@@ -372,6 +380,8 @@ __device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, doubl
   C.inv_k = 1.0 / k;
   C.c2 = exp(r * t) / k;
   C.kexp = k * exp(-r * t);
+  C.mu_lnk = C.mu_s - log(k) * C.inv_vst;
+  C.nkexp = -C.kexp;
   const int tid = threadIdx.x;
   if (!(aligned16(s) && aligned16(c)) || blockDim.x != 256) {
     for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < n; i += (long long)gridDim.x * blockDim.x) {
