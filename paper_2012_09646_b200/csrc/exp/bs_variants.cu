@@ -102,6 +102,9 @@ BS2T_VARIANT(k_bs2t_o2s4b4, 2, 4, 4)
 BS2T_VARIANT(k_bs2t_o6s3b2, 6, 3, 2)  // the product shape, for side-by-side runs
 BS2L_VARIANT(k_bs2l_o6s3b2, 6, 3, 2)
 BS2L_VARIANT(k_bs2l_o4s3b3, 4, 3, 3)
+BS2L_VARIANT(k_bs2l_o6s3b3, 6, 3, 3)
+BS2L_VARIANT(k_bs2l_o6s2b3, 6, 2, 3)
+BS2L_VARIANT(k_bs2l_o8s2b2, 8, 2, 2)
 BS3_VARIANT(k_bs3_o6s4b2, 6, 4, 2)
 BS3_VARIANT(k_bs3_o6s6b2, 6, 6, 2)
 BS3_VARIANT(k_bs3_o4s8b2, 4, 8, 2)
@@ -365,6 +368,9 @@ static const Builtin kBsExp[] = {
     // lean pricer (larger tables, one series term fewer each)
     {"bs2l_o6s3b2", (const void*)k_bs2l_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o4s3b3", (const void*)k_bs2l_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2l_o6s3b3", (const void*)k_bs2l_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2l_o6s2b3", (const void*)k_bs2l_o6s2b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2l_o8s2b2", (const void*)k_bs2l_o8s2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     // warp-specialised (288 threads: 8 consumer warps + 1 producer warp)
     {"bs3_o6s4b2", (const void*)k_bs3_o6s4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(6, 4)},
     {"bs3_o6s6b2", (const void*)k_bs3_o6s6b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(6, 6)},

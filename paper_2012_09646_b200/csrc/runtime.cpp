@@ -623,8 +623,8 @@ struct DeferBackend final : Backend {
   }
 
   cudaError_t flush() {
-    NvtxRange nvtx_("dagrt_graph_cache_flush");
     if (ops.empty()) return cudaSuccess;
+    NvtxRange nvtx_("dagrt_graph_cache_flush");
     if (!origin)
       if (cudaError_t e = in->stream_create(&origin)) return e;
     build_key();

@@ -193,7 +193,7 @@ def bs_launch(name):
                                      "bs_l8b1", "bs2_p3w2b2", "bs2_p2w2b3", "bs2_p2w4b2", "bs2_p4w2b2",
                                      "bs2_p1w2b4", "bs2t_o4s4b2", "bs2t_o4s3b3", "bs2t_o2s4b4", "bs2t_o6s3b2",
                                      "bs3_o6s4b2", "bs3_o6s6b2", "bs3_o4s8b2", "bs3_o4s6b3", "bs3_o2s8b4",
-                                     "bs2l_o6s3b2", "bs2l_o4s3b3"])
+                                     "bs2l_o6s3b2", "bs2l_o4s3b3", "bs2l_o6s3b3", "bs2l_o6s2b3", "bs2l_o8s2b2"])
 # 227_333: an odd number of full groups for the lean 4-pair loop (ping-pong tail)
 @pytest.mark.parametrize("n", [3, 200_001, 227_333])
 def test_bs_variants_match_oracle(ctx, exp, variant, n):
