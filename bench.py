@@ -71,7 +71,7 @@ FULL = {
 DOMINANT = {"vec": "square", "bs": "bs", "img": "blur", "ml": "norm", "hits": "spmv", "dl": "conv1",
             "bs_f32": "bs_f32"}
 # device symbol of each dominant kernel (ncu names, profiles/*_traffic.json keys)
-KSYM = {"square": "k_square", "bs": "k_bs2l_o6s3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv_pad",
+KSYM = {"square": "k_square", "bs": "k_bs2l_o6s3b2", "blur": "k_blur", "norm": "k_norm", "spmv": "k_spmv_split",
         "conv1": "k_conv1_r2b3", "conv2": "k_conv2_h", "bs_f32": "k_bs_f32"}
 DTYPE = {"vec": "f32", "bs": "f64", "img": "f32", "ml": "f32/i32", "hits": "f32/i32", "dl": "f32", "bs_f32": "f32"}
 WORKLOAD = {

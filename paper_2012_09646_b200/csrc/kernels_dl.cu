@@ -72,13 +72,22 @@ __global__ void __launch_bounds__(256) k_dot(const float* __restrict__ z,
     const long long n4 = n >> 2;
     const float4* Z = reinterpret_cast<const float4*>(z);
     const float4* Wd = reinterpret_cast<const float4*>(wd);
-    for (long long i = tid; i < n4; i += nth) {
-      float4 a = ldg_stream(Z + i), b = ldg_stream(Wd + i);
-      acc = fma((double)a.x, (double)b.x, acc);
-      acc = fma((double)a.y, (double)b.y, acc);
-      acc = fma((double)a.z, (double)b.z, acc);
-      acc = fma((double)a.w, (double)b.w, acc);
+    auto dp = [](float4 a, float4 b, double t) {
+      t = fma((double)a.x, (double)b.x, t);
+      t = fma((double)a.y, (double)b.y, t);
+      t = fma((double)a.z, (double)b.z, t);
+      return fma((double)a.w, (double)b.w, t);
+    };
+    double acc1 = 0.0;
+    long long i = tid;
+    for (; i + nth < n4; i += 2 * nth) {  // four 16-byte loads in flight, two chains
+      const float4 a = ldg_stream(Z + i), b = ldg_stream(Wd + i), c = ldg_stream(Z + i + nth),
+                   d = ldg_stream(Wd + i + nth);
+      acc = dp(a, b, acc);
+      acc1 = dp(c, d, acc1);
     }
+    for (; i < n4; i += nth) acc = dp(ldg_stream(Z + i), ldg_stream(Wd + i), acc);
+    acc += acc1;
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) acc = fma((double)z[i], (double)wd[i], acc);

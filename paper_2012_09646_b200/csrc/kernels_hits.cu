@@ -16,11 +16,15 @@
 
 namespace dagrt {
 
-// "spmv" (product, round 2): the padded non-zero split (PadPlan, spmv_common.cuh).
-__global__ void __launch_bounds__(256, 4) k_spmv_pad(const int* __restrict__, const int* __restrict__,
-                                                     const int* __restrict__ plan, const float* __restrict__ x,
-                                                     float* __restrict__ y, long long N_) {
-  spmv_pad_body<false>(plan, x, y, N_);  // the plan carries the (padded) graph
+// "spmv" (product): the padded non-zero split (PadPlan, spmv_common.cuh)
+// with the segmented warp scan taken only where rows cross lanes
+// (spmv_pad2_body): 255 vs 259 us per launch and 1.7% off the HITS DAG
+// against the plain scan (spmv_pad_body, exp "spmv_pad"), tools/spmv_variants.py
+// and tools/hits_variants.py.
+__global__ void __launch_bounds__(256, 4) k_spmv_split(const int* __restrict__, const int* __restrict__,
+                                                 const int* __restrict__ plan, const float* __restrict__ x,
+                                                 float* __restrict__ y, long long N_) {
+  spmv_pad2_body<4>(plan, x, y, N_);  // the plan carries the (padded) graph
 }
 
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
@@ -34,10 +38,22 @@ __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, Red
   if (aligned16(v)) {
     const long long n4 = n >> 2;
     const float4* v4 = reinterpret_cast<const float4*>(v);
-    for (long long i = tid; i < n4; i += nth) {
-      float4 a = ldg_stream(v4 + i);
-      acc += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
+    // four independent 16-byte loads in flight per thread, two accumulators
+    // (one load per iteration was latency-bound at ~0.53 of HBM)
+    auto sq = [](float4 a) {
+      return fma((double)a.x, (double)a.x, fma((double)a.y, (double)a.y,
+                                               fma((double)a.z, (double)a.z, (double)a.w * a.w)));
+    };
+    double acc1 = 0.0;
+    long long i = tid;
+    for (; i + 3 * nth < n4; i += 4 * nth) {
+      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth), c = ldg_stream(v4 + i + 2 * nth),
+                   d = ldg_stream(v4 + i + 3 * nth);
+      acc += sq(a) + sq(b);
+      acc1 += sq(c) + sq(d);
     }
+    for (; i < n4; i += nth) acc += sq(ldg_stream(v4 + i));
+    acc += acc1;
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];
@@ -58,11 +74,19 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
   long long done = 0;
   if (aligned16(v) && aligned16(out)) {
     const long long n4 = n >> 2;
-    for (long long i = tid; i < n4; i += nth) {
-      float4 a = ldg_stream(reinterpret_cast<const float4*>(v) + i);
-      a.x *= is; a.y *= is; a.z *= is; a.w *= is;
-      reinterpret_cast<float4*>(out)[i] = a;
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    auto sc = [&](float4 a) { return make_float4(a.x * is, a.y * is, a.z * is, a.w * is); };
+    long long i = tid;
+    for (; i + 3 * nth < n4; i += 4 * nth) {  // four loads in flight before the stores
+      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth), c = ldg_stream(v4 + i + 2 * nth),
+                   d = ldg_stream(v4 + i + 3 * nth);
+      o4[i] = sc(a);
+      o4[i + nth] = sc(b);
+      o4[i + 2 * nth] = sc(c);
+      o4[i + 3 * nth] = sc(d);
     }
+    for (; i < n4; i += nth) o4[i] = sc(ldg_stream(v4 + i));
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) out[i] = v[i] * is;
@@ -80,7 +104,7 @@ static const char* v_divide(const LaunchCheck& L) {
 }
 
 static const Builtin kHits[] = {
-    {"spmv", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
+    {"spmv", (const void*)k_spmv_split, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"l2norm", (const void*)k_l2norm, "const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_l2norm},
     {"divide", (const void*)k_divide, "const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_divide},
 };

@@ -325,6 +325,163 @@ __device__ __forceinline__ void spmv_pad_body(const int* __restrict__ plan, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// spmv_pad2 (the product "spmv" since round 2's end): the padded non-zero split with the segmented warp scan
+// taken only where it is needed.  ncu on the product (profiles/r2_ncu_*): the
+// top stall is short_scoreboard (shuffle latency of the 5-step scan run on
+// every 128-item chunk).  Per chunk, m = lanes holding a row start:
+//   m == 0   (the chunk lies inside one row -- the hubs hold half of the
+//            non-zeros): each lane adds its 4 items to a per-lane partial;
+//            no shuffle at all; the partials are reduced (xor tree) once,
+//            when the row ends;
+//   m == all (every lane starts a row: rows span at most two lanes): a lane's
+//            first row is the previous lane's tail plus its head -- one
+//            shuffle up, one broadcast for the carry;
+//   else     the segmented scan as in the product.
+// Same rows, same deposits; fp32 sums in a different (fixed) order.
+template <int MINB>
+__device__ __forceinline__ void spmv_pad2_body(const int* __restrict__ plan, const float* __restrict__ x,
+                                               float* __restrict__ y, long long N_) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PadPlan P = pad_plan(plan);
+  if ((long long)P.n != N_ || P.n == 0) return;
+  const int G = (int)gridDim.x * (blockDim.x >> 5);
+  const int g = (int)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  const uint64_t pol = l2_policy_evict_first();
+  auto warp_of_item = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
+
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);
+  bool head_pending = !start0;
+  float carry = 0.f;       // warp-uniform part of the open row's partial sum
+  float carry_lane = 0.f;  // per-lane part, from chunks without a row start
+  bool dist = false;       // carry_lane is non-empty somewhere (warp-uniform)
+
+  NzIn cur = pad_load(P, cb, lane, pol);
+  NzIn nxt = cur;
+  if (cb + 1 < ce) nxt = pad_load(P, cb + 1, lane, pol);
+  float v[4];
+  nz_gather(cur, x, v);
+  for (int c = cb; c < ce; ++c) {
+    uint4 fw = cur.fw;
+    if (c == cb) fw.x &= ~1u;
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
+    const int nst = __popc(fl);
+    float vn[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c + 1 < ce) {
+      nz_gather(nxt, x, vn);
+      cur = nxt;
+      if (c + 2 < ce) nxt = pad_load(P, c + 2, lane, pol);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
+    if (m == 0u) {  // inside one row
+      carry_lane += (v[0] + v[1]) + (v[2] + v[3]);
+      dist = true;
+    } else {
+      if (dist) {
+        float t = carry_lane;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        carry += t;
+        carry_lane = 0.f;
+        dist = false;
+      }
+      const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                         (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+      const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+      const int o = R0 + before;
+      float run = 0.f, head = 0.f;
+      bool seen = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (!seen) head = run;
+          seen = true;
+          run = 0.f;
+        }
+        run += v[u];
+      }
+      if (!seen) head = run;
+      float cin, tail_all;
+      if (m == 0xffffffffu) {  // rows span at most two lanes
+        cin = __shfl_up_sync(0xffffffffu, run, 1);
+        if (lane == 0) cin = carry;
+        tail_all = __shfl_sync(0xffffffffu, run, 31);
+      } else {
+        float sv = nst ? run : head;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+          const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+          if (win == 0u) sv += tv;
+        }
+        cin = __shfl_up_sync(0xffffffffu, sv, 1);
+        if (lane == 0) cin = 0.f;
+        if ((m & lanes_below) == 0u) cin += carry;
+        tail_all = __shfl_sync(0xffffffffu, sv, 31);
+      }
+      if (nst) {
+        const float val = cin + head;
+        if (head_pending && before == 0) {
+          const int cs = warp_of_item(__ldg(P.rp2 + o));
+          spmv_ws_put(ws, g, val, true);
+          if (spmv_ws_arrive(ws, cs, g)) y[o] = spmv_ws_sum(ws, cs, g);
+        } else {
+          y[o] = val;
+        }
+        int j = 1;
+        float r2 = 0.f;
+        bool in = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if ((fl >> u) & 1u) {
+            if (in) y[o + j++] = r2;
+            in = true;
+            r2 = 0.f;
+          }
+          r2 += v[u];
+        }
+      }
+      carry = tail_all;
+      head_pending = false;
+      R0 += total;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = vn[u];
+  }
+  if (dist) {
+    float t = carry_lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    carry += t;
+  }
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= P.e2 || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    if (ends_here) {
+      if (head_pending) {
+        const int cs = warp_of_item(__ldg(P.rp2 + R0));
+        spmv_ws_put(ws, g, carry, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[R0] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[R0] = carry;
+      }
+    } else {
+      const int cs = warp_of_item(__ldg(P.rp2 + R0));
+      const int cend = warp_of_item(__ldg(P.rp2 + R0 + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      if (spmv_ws_arrive(ws, cs, cend)) y[R0] = spmv_ws_sum(ws, cs, cend);
+    }
+  }
+}
 // launch contract of the plan-driven kernels (builtin.h LaunchCheck)
 static inline const char* v_spmv_plan_kernel(const LaunchCheck& L) {  // row_ptr, col, plan, x, y, N
   const int64_t N = L.i(5);
