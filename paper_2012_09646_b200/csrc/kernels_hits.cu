@@ -38,22 +38,10 @@ __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, Red
   if (aligned16(v)) {
     const long long n4 = n >> 2;
     const float4* v4 = reinterpret_cast<const float4*>(v);
-    // four independent 16-byte loads in flight per thread, two accumulators
-    // (one load per iteration was latency-bound at ~0.53 of HBM)
-    auto sq = [](float4 a) {
-      return fma((double)a.x, (double)a.x, fma((double)a.y, (double)a.y,
-                                               fma((double)a.z, (double)a.z, (double)a.w * a.w)));
-    };
-    double acc1 = 0.0;
-    long long i = tid;
-    for (; i + 3 * nth < n4; i += 4 * nth) {
-      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth), c = ldg_stream(v4 + i + 2 * nth),
-                   d = ldg_stream(v4 + i + 3 * nth);
-      acc += sq(a) + sq(b);
-      acc1 += sq(c) + sq(d);
+    for (long long i = tid; i < n4; i += nth) {
+      float4 a = ldg_stream(v4 + i);
+      acc += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
     }
-    for (; i < n4; i += nth) acc += sq(ldg_stream(v4 + i));
-    acc += acc1;
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];
@@ -74,19 +62,11 @@ __global__ void __launch_bounds__(256) k_divide(const float* __restrict__ v,
   long long done = 0;
   if (aligned16(v) && aligned16(out)) {
     const long long n4 = n >> 2;
-    const float4* v4 = reinterpret_cast<const float4*>(v);
-    float4* o4 = reinterpret_cast<float4*>(out);
-    auto sc = [&](float4 a) { return make_float4(a.x * is, a.y * is, a.z * is, a.w * is); };
-    long long i = tid;
-    for (; i + 3 * nth < n4; i += 4 * nth) {  // four loads in flight before the stores
-      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth), c = ldg_stream(v4 + i + 2 * nth),
-                   d = ldg_stream(v4 + i + 3 * nth);
-      o4[i] = sc(a);
-      o4[i + nth] = sc(b);
-      o4[i + 2 * nth] = sc(c);
-      o4[i + 3 * nth] = sc(d);
+    for (long long i = tid; i < n4; i += nth) {
+      float4 a = ldg_stream(reinterpret_cast<const float4*>(v) + i);
+      a.x *= is; a.y *= is; a.z *= is; a.w *= is;
+      reinterpret_cast<float4*>(out)[i] = a;
     }
-    for (; i < n4; i += nth) o4[i] = sc(ldg_stream(v4 + i));
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) out[i] = v[i] * is;
