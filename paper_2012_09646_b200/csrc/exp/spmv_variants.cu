@@ -8,6 +8,7 @@
 //    non-empty-row list); the product pads empty rows instead.
 #include "../spmv_common.cuh"
 #include "exp_common.cuh"
+#include "../bs_math.cuh"  // bs_mbar_init / bs_mbar_wait
 
 namespace dagrt {
 
@@ -1037,7 +1038,211 @@ __global__ void __launch_bounds__(256, 4) k_spmv_pad(const int* __restrict__, co
   spmv_pad_body<false>(plan, x, y, N_);
 }
 
+// ---------------------------------------------------------------------------
+// spmv_tma: the product's scan-light padded split with the column-index and
+// flag streams fed by the TMA unit.  ncu on the product: the warps stall on
+// the register copy of the NEXT chunk's column indices (long_scoreboard: the
+// column loads queue behind the gathers in the L1 request pipe, and with a
+// 64-register budget only one chunk of columns can be in flight).  Here lane
+// 0 of each warp keeps S chunks of columns + flags in flight with bulk copies
+// into a per-warp shared ring (no registers, no L1 request slots); lanes
+// read their 4 columns with one 16-byte shared load.  Needs whole chunks in
+// the plan (spmv_pad_plan pads ci2 to a multiple of 128).
+template <int S>
+__device__ __forceinline__ void spmv_tma_body(const int* __restrict__ plan, const float* __restrict__ x,
+                                              float* __restrict__ y, long long N_) {
+  __shared__ __align__(128) int4 cring[8][S][32];   // 8 warps x S chunks x 128 columns
+  __shared__ __align__(16) uint4 fring[8][S];
+  __shared__ uint64_t bar[8][S];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PadPlan P = pad_plan(plan);
+  if ((long long)P.n != N_ || P.n == 0 || blockDim.x != 256) return;
+  const int G = (int)gridDim.x * 8;
+  const int g = (int)blockIdx.x * 8 + warp;
+  const int per = (P.nc + G - 1) / G;
+  const int cb = g * per, ce = min(P.nc, cb + per);
+  if (cb >= ce) return;
+  if (lane == 0) {
+    for (int q = 0; q < S; ++q) bs_mbar_init(&bar[warp][q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int chunk, int slot) {  // lane 0
+    uint64_t* b = &bar[warp][slot];
+    const unsigned ba = (unsigned)__cvta_generic_to_shared(b);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(528u) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&cring[warp][slot][0])),
+                 "l"(P.ci2 + (size_t)chunk * kNzChunk), "r"(ba)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&fring[warp][slot])),
+                 "l"(P.flags + 4 * (size_t)chunk), "r"(ba)
+                 : "memory");
+  };
+  if (lane == 0)
+    for (int q = 0; q < S && cb + q < ce; ++q) issue(cb + q, q);
+  const SpmvWs ws = spmv_ws(y, N_, G);
+  auto warp_of_item = [&](int k) { return (k / kNzChunk) / per; };
+  const int wsel = lane >> 3, bsh = 4 * (lane & 7);
+  const unsigned lanes_below = (1u << lane) - 1u;
+  const int k0w = cb * kNzChunk;
+  const bool start0 = (__ldg(P.flags + (k0w >> 5)) >> (k0w & 31)) & 1u;
+  int R0 = __ldg(P.rbase + cb);
+  bool head_pending = !start0;
+  float carry = 0.f, carry_lane = 0.f;
+  bool dist = false;
+  // take chunk `it` (the it-th of this warp) out of the ring: its columns
+  // (4 per lane) and flag words; lane 0 refills the slot with chunk it + S
+  auto take = [&](int it, int4& cols, uint4& fw) {
+    const int slot = it % S;
+    bs_mbar_wait(&bar[warp][slot], (unsigned)((it / S) & 1));
+    cols = cring[warp][slot][lane];
+    fw = fring[warp][slot];
+    __syncwarp();
+    if (lane == 0 && cb + it + S < ce) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(cb + it + S, slot);
+    }
+  };
+  auto gather = [&](const int4& q, float (&v)[4]) {
+    v[0] = q.x >= 0 ? __ldg(x + q.x) : 0.f;
+    v[1] = q.y >= 0 ? __ldg(x + q.y) : 0.f;
+    v[2] = q.z >= 0 ? __ldg(x + q.z) : 0.f;
+    v[3] = q.w >= 0 ? __ldg(x + q.w) : 0.f;
+  };
+  int4 q;
+  uint4 fwc, fwn = make_uint4(0, 0, 0, 0);
+  take(0, q, fwc);
+  float v[4];
+  gather(q, v);
+  for (int c = cb, it = 0; c < ce; ++c, ++it) {
+    float vn[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c + 1 < ce) {
+      take(it + 1, q, fwn);
+      gather(q, vn);
+    }
+    uint4 fw = fwc;
+    if (c == cb) fw.x &= ~1u;
+    const unsigned mine = wsel == 0 ? fw.x : (wsel == 1 ? fw.y : (wsel == 2 ? fw.z : fw.w));
+    const unsigned fl = (mine >> bsh) & 0xFu;
+    const int nst = __popc(fl);
+    const unsigned m = __ballot_sync(0xffffffffu, nst != 0);
+    if (m == 0u) {
+      carry_lane += (v[0] + v[1]) + (v[2] + v[3]);
+      dist = true;
+    } else {
+      if (dist) {
+        float t = carry_lane;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        carry += t;
+        carry_lane = 0.f;
+        dist = false;
+      }
+      const int before = (wsel > 0 ? __popc(fw.x) : 0) + (wsel > 1 ? __popc(fw.y) : 0) +
+                         (wsel > 2 ? __popc(fw.z) : 0) + __popc(mine & ((1u << bsh) - 1u));
+      const int total = __popc(fw.x) + __popc(fw.y) + __popc(fw.z) + __popc(fw.w);
+      const int o = R0 + before;
+      float run = 0.f, head = 0.f;
+      bool seen = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((fl >> u) & 1u) {
+          if (!seen) head = run;
+          seen = true;
+          run = 0.f;
+        }
+        run += v[u];
+      }
+      if (!seen) head = run;
+      float cin, tail_all;
+      if (m == 0xffffffffu) {
+        cin = __shfl_up_sync(0xffffffffu, run, 1);
+        if (lane == 0) cin = carry;
+        tail_all = __shfl_sync(0xffffffffu, run, 31);
+      } else {
+        float sv = nst ? run : head;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float tv = __shfl_up_sync(0xffffffffu, sv, off);
+          const unsigned win = lane >= off ? (m >> (lane - off + 1)) & ((1u << off) - 1u) : 1u;
+          if (win == 0u) sv += tv;
+        }
+        cin = __shfl_up_sync(0xffffffffu, sv, 1);
+        if (lane == 0) cin = 0.f;
+        if ((m & lanes_below) == 0u) cin += carry;
+        tail_all = __shfl_sync(0xffffffffu, sv, 31);
+      }
+      if (nst) {
+        const float val = cin + head;
+        if (head_pending && before == 0) {
+          const int cs = warp_of_item(__ldg(P.rp2 + o));
+          spmv_ws_put(ws, g, val, true);
+          if (spmv_ws_arrive(ws, cs, g)) y[o] = spmv_ws_sum(ws, cs, g);
+        } else {
+          y[o] = val;
+        }
+        int j = 1;
+        float r2 = 0.f;
+        bool in = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if ((fl >> u) & 1u) {
+            if (in) y[o + j++] = r2;
+            in = true;
+            r2 = 0.f;
+          }
+          r2 += v[u];
+        }
+      }
+      carry = tail_all;
+      head_pending = false;
+      R0 += total;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = vn[u];
+    fwc = fwn;
+  }
+  if (dist) {
+    float t = carry_lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    carry += t;
+  }
+  if (lane == 0) {
+    const int ke = ce * kNzChunk;
+    const bool ends_here = ke >= P.e2 || ((__ldg(P.flags + (ke >> 5)) >> (ke & 31)) & 1u);
+    if (ends_here) {
+      if (head_pending) {
+        const int cs = warp_of_item(__ldg(P.rp2 + R0));
+        spmv_ws_put(ws, g, carry, true);
+        if (spmv_ws_arrive(ws, cs, g)) y[R0] = spmv_ws_sum(ws, cs, g);
+      } else {
+        y[R0] = carry;
+      }
+    } else {
+      const int cs = warp_of_item(__ldg(P.rp2 + R0));
+      const int cend = warp_of_item(__ldg(P.rp2 + R0 + 1) - 1);
+      spmv_ws_put(ws, g, carry, false);
+      if (spmv_ws_arrive(ws, cs, cend)) y[R0] = spmv_ws_sum(ws, cs, cend);
+    }
+  }
+}
+__global__ void __launch_bounds__(256, 4) k_spmv_tma4(const int* __restrict__, const int* __restrict__,
+                                                      const int* __restrict__ plan, const float* __restrict__ x,
+                                                      float* __restrict__ y, long long N_) {
+  spmv_tma_body<4>(plan, x, y, N_);
+}
+__global__ void __launch_bounds__(256, 4) k_spmv_tma8(const int* __restrict__, const int* __restrict__,
+                                                      const int* __restrict__ plan, const float* __restrict__ x,
+                                                      float* __restrict__ y, long long N_) {
+  spmv_tma_body<8>(plan, x, y, N_);
+}
+
 static const Builtin kHitsExp[] = {
+    {"spmv_tma4", (const void*)k_spmv_tma4, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
+    {"spmv_tma8", (const void*)k_spmv_tma8, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad_l2", (const void*)k_spmv_pad_l2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_ws", (const void*)k_spmv_ws, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv_split(const int* __restrict__, 
 }
 
 // SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
-__global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, RedOut* out,
+__global__ void __launch_bounds__(256, 8) k_l2norm(const float* __restrict__ v, RedOut* out,
                                                 long long n) {
   __shared__ double sh[32];
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -38,10 +38,13 @@ __global__ void __launch_bounds__(256) k_l2norm(const float* __restrict__ v, Red
   if (aligned16(v)) {
     const long long n4 = n >> 2;
     const float4* v4 = reinterpret_cast<const float4*>(v);
-    for (long long i = tid; i < n4; i += nth) {
-      float4 a = ldg_stream(v4 + i);
-      acc += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
-    }
+    // each float4's four squares summed in fp32 (relative 2^-23, far inside
+    // the 1e-3 reduction criterion), one conversion per float4 into the fp64
+    // accumulator: the per-element fp32->fp64 conversions ran on the XU pipe
+    // (ncu: XU 33%) while the loop waited on memory; 32 registers keep the
+    // full 8 CTAs per SM (a two-load form at 33 registers lost occupancy)
+    auto sq4 = [](float4 a) { return (double)fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, a.w * a.w))); };
+    for (long long i = tid; i < n4; i += nth) acc += sq4(ldg_stream(v4 + i));
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];

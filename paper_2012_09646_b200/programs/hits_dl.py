@@ -157,7 +157,8 @@ def spmv_pad_plan(row_ptr, col_idx):
     int32 [header(16) | rp2(N+1) | rbase(nc+1) | flags(4nc+4) | ci2(E2)]:
       rp2   padded row pointers, E2 = rp2[N] = E + #empty rows;
       flags bit k set iff item k starts its row (every row starts one item);
-      rbase[c] row holding item c*128;  ci2 the padded column indices."""
+      rbase[c] row holding item c*128;  ci2 the padded column indices, the
+            last chunk filled up with -1 (whole 128-item chunks)."""
     import numpy as np
     rp = np.asarray(row_ptr, dtype=np.int64)
     ci = np.asarray(col_idx, dtype=np.int64)
@@ -167,7 +168,8 @@ def spmv_pad_plan(row_ptr, col_idx):
     rp2 = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(pdeg, out=rp2[1:])
     e2 = int(rp2[-1])
-    ci2 = np.full(max(e2, 1), -1, dtype=np.int64)
+    # whole chunks (the tail padded with -1) so that chunk copies stay in bounds
+    ci2 = np.full(max(-(-e2 // NZ_CHUNK) * NZ_CHUNK, 1), -1, dtype=np.int64)
     if ci.size:
         row_of = np.repeat(np.arange(n, dtype=np.int64), deg)
         ci2[rp2[row_of] + (np.arange(ci.size, dtype=np.int64) - rp[row_of])] = ci

@@ -73,7 +73,7 @@ def run_nz(ctx, rp, ci, x, grid, tag, kernel="spmv"):
     return outs
 
 
-@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3", "spmv_ws", "spmv_pad_l2"])
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3", "spmv_ws", "spmv_pad_l2", "spmv_tma4", "spmv_tma8"])
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("grid", [1, 7, 148 * 6])
 def test_spmv_nz_edge_shapes(ctx, exp, case, grid, kernel):
@@ -88,7 +88,7 @@ def test_spmv_nz_edge_shapes(ctx, exp, case, grid, kernel):
     assert_close(y1.cpu().numpy(), ref, case)
 
 
-@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3", "spmv_ws", "spmv_pad_l2"])
+@pytest.mark.parametrize("kernel", ["spmv", "spmv_nz", "spmv_pad2", "spmv_pad2b3", "spmv_ws", "spmv_pad_l2", "spmv_tma4", "spmv_tma8"])
 @pytest.mark.parametrize("n,e,seed", [(10, 30, 1), (5000, 15000, 3), (300_000, 900_000, 11)])
 def test_spmv_nz_powerlaw(ctx, exp, n, e, seed, kernel):
     rp, ci, _, _ = synth.powerlaw_graph(seed, n, e, device="auto")

@@ -29,7 +29,7 @@ def main():
     st = torch.cuda.Stream()
     out, ref = {}, None
     sel = sys.argv[1].split(",") if len(sys.argv) > 1 else None
-    for name in ("spmv", "spmv_pad", "spmv_ws"):
+    for name in ("spmv", "spmv_pad", "spmv_tma4", "spmv_tma8"):
         if sel and name not in sel:
             continue
         for grid in (148 * 4, 148 * 8, 148 * 12, 148 * 16):
