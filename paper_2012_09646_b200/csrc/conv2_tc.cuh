@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
         for (int a = chained ? 1 : 0; a < 3; ++a, ++rseq) {
           const int slot = rseq % R;
           mbar_wait(empty + slot, (uint32_t)(((rseq / R) & 1) ^ 1));
+          if (a == 2) C2T(0, i);
           const uint32_t bar = su32(full + slot);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
           const int y = 2 * p + a - 1;
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
               "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
               ::"r"(su32(dst + kPlaneStride)), "l"(tmap), "r"(0), "r"(1), "r"(q0 - 1), "r"(y), "r"(bar) : "memory");
         }
+        C2T(1, i);
         if (++p == H3) { p = 0; ++qb; }
       }
     }
@@ -315,7 +317,9 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
         const int b = i % NB;
         const uint32_t pb = (uint32_t)((i / NB) & 1);
         mbar_wait(loready + b, pb);
+        C2T(2, i);
         mbar_wait(accempty + b, pb ^ 1);
+        C2T(3, i);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + b * 32, a = tmem + kABase + b * kACols;
 #pragma unroll
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
                        "l"(bd), "r"(kId), "r"((uint32_t)(tap > 0)));
         }
         commit(mmadone + b);
+        C2T(4, i);
       }
     }
   } else if (warp < 2 + SW) {
@@ -341,6 +346,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
       const int s0 = chained ? rseq - 1 : rseq;
       const int b = i % NB;
       mbar_wait(mmadone + b, (uint32_t)(((i / NB) & 1) ^ 1));
+      if (warp == 2 && lane == 0) C2T(6, i);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t abuf = tmem + lane_off + kABase + b * kACols;
       const bool edge = 2 * (qb * 128 + r) + 1 >= W2;
@@ -349,6 +355,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
         const int rs = s0 + a;
         const int slot = rs % R;
         mbar_wait(full + slot, (uint32_t)((rs / R) & 1));
+        if (a == 2 && warp == 2 && lane == 0) C2T(5, i);
         const unsigned char* ev = rows + slot * kSlot;
         const unsigned char* od = ev + kPlaneStride;
 #pragma unroll
@@ -374,6 +381,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
+      if (warp == 2 && lane == 0) C2T(7, i);
       if (lane == 0) {
         mbar_arrive(loready + b);
         mbar_arrive(empty + (s0 % R));
@@ -390,6 +398,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
     for (int i = 0; i < nmine; ++i) {
       const int b = i % NB;
       mbar_wait(mmadone + b, (uint32_t)((i / NB) & 1));
+      if (warp == 2 + SW && lane == 0) C2T(8, i);
       asm volatile("tcgen05.fence::after_thread_sync;");
       uint32_t h[16], l[16];
       const uint32_t d = tmem + lane_off + b * 32;
@@ -410,6 +419,7 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
           dst[k] = make_float4(v[0], v[1], v[2], v[3]);
         }
       }
+      if (warp == 2 + SW && lane == 0) C2T(9, i);
       if (++p == H3) { p = 0; ++qb; }
     }
   }
@@ -418,6 +428,246 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
+
+
+// conv2_hs: k_conv2_h with the A operand in SHARED memory (the canonical
+// K-major no-swizzle layout, one 4 KB block per tap) instead of TMEM.  The
+// pipeline trace of the product (tools/conv2h_trace.py) has the split stage
+// on the critical path at ~1200 cycles per tile and 9 MMAs taking ~800
+// cycles to issue (vs ~47 cycles each in tools/mma_lab.py) while more split
+// warps make it slower: split stores into TMEM and the MMAs' A reads from
+// TMEM contend.  Here the split writes A with two 16-byte shared stores per
+// tap and pixel and the MMAs read A and B from shared memory (SS).
+namespace c2hs {
+constexpr int kATap = 128 * 32;  // A per tap: 128 rows x 16 fp16
+template <int R, int NB, int SW>
+struct Cfg {
+  static constexpr int kThreads = 32 * (2 + SW + 4);
+  static constexpr size_t smem() {
+    return 1024 + (size_t)R * c2rows::kSlot + 9 * c2h::kBTap + (size_t)NB * 9 * kATap + 8 * (2 * R + 3 * NB) + 16;
+  }
+  static_assert(NB * 32 <= (int)c2h::kABase, "TMEM budget");
+  static_assert(SW % 4 == 0 && SW >= 4, "split warps per lane quarter");
+  static_assert(smem() <= 227 * 1024, "shared memory budget");
+};
+}  // namespace c2hs
+
+template <int R, int NB, int SW>
+__global__ void __launch_bounds__(c2hs::Cfg<R, NB, SW>::kThreads, 1)
+    k_conv2_hs(const CUtensorMap* __restrict__ tmap, const float* __restrict__ in, const float* __restrict__ w,
+              float* __restrict__ out, int H2, int W2) {
+  using namespace c2ws;
+  using c2rows::kPlane;
+  using c2rows::kPlaneStride;
+  using c2rows::kSlot;
+  using c2rows::Tile;
+  using c2rows::tile_at;
+  constexpr int kThreads = c2hs::Cfg<R, NB, SW>::kThreads;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* rows = sm;
+  unsigned char* bt = rows + R * kSlot;                  // [9][32 rows x 32 B] fp16, interleaved
+  unsigned char* as = bt + 9 * c2h::kBTap;               // A: [NB][9 taps][128 rows x 32 B] fp16, interleaved
+  uint64_t* full = reinterpret_cast<uint64_t*>(as + NB * 9 * c2hs::kATap);
+  uint64_t* empty = full + R;
+  uint64_t* loready = empty + R;
+  uint64_t* mmadone = loready + NB;
+  uint64_t* accempty = mmadone + NB;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accempty + NB);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  (void)in;
+
+  // ---- B: per tap, row n < 16 = [w_hi | w_hi], row 16 + n = [w_lo | 0] (fp16, K-major)
+  for (int i = t; i < 16 * 72; i += kThreads) {
+    const int n = i / 72, r = i % 72, tap = r / 8, c = r % 8;
+    const float x = w[i];
+    const __half hi = __float2half_rn(x), lo = __float2half_rn(x - __half2float(hi));
+    auto at = [&](int row, int k) -> __half* {  // element k (0..15) of B row `row`
+      return reinterpret_cast<__half*>(bt + tap * c2h::kBTap + (row & 7) * 16 + (row >> 3) * 256 + (k >> 3) * 128 +
+                                       (k & 7) * 2);
+    };
+    *at(n, c) = hi;
+    *at(n, 8 + c) = hi;
+    *at(16 + n, c) = lo;
+    *at(16 + n, 8 + c) = __float2half_rn(0.f);
+  }
+  if (t == 0) {
+    for (int q = 0; q < R; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, SW);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(loready + b, SW);
+      mbar_init(mmadone + b, 1);
+      mbar_init(accempty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tslot;
+
+  const int H3 = (H2 + 1) / 2, W3 = (W2 + 1) / 2;
+  const int nqb = (W3 + 127) / 128;
+  const long long ntiles = (long long)H3 * nqb;
+  const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const long long tb = (long long)blockIdx.x * per, te = min(ntiles, tb + per);
+  const int nmine = te > tb ? (int)(te - tb) : 0;
+  // (qb, p) of the CTA's first tile; later tiles advance p, wrapping to the next column block
+  const int qb0 = (int)(tb / H3), p0 = (int)(tb % H3);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t tx = 2u * kPlane;
+      int rseq = 0, qb = qb0, p = p0;
+      for (int i = 0; i < nmine; ++i) {
+        const bool chained = i > 0 && p > 0;
+        const int q0 = qb * 128;
+        for (int a = chained ? 1 : 0; a < 3; ++a, ++rseq) {
+          const int slot = rseq % R;
+          mbar_wait(empty + slot, (uint32_t)(((rseq / R) & 1) ^ 1));
+          if (a == 2) C2T(0, i);
+          const uint32_t bar = su32(full + slot);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+          const int y = 2 * p + a - 1;
+          unsigned char* dst = rows + slot * kSlot;
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+              ::"r"(su32(dst)), "l"(tmap), "r"(0), "r"(0), "r"(q0), "r"(y), "r"(bar) : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+              ::"r"(su32(dst + kPlaneStride)), "l"(tmap), "r"(0), "r"(1), "r"(q0 - 1), "r"(y), "r"(bar) : "memory");
+        }
+        C2T(1, i);
+        if (++p == H3) { p = 0; ++qb; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kId = (1u << 4) | (0u << 7) | (0u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < nmine; ++i) {
+        const int b = i % NB;
+        const uint32_t pb = (uint32_t)((i / NB) & 1);
+        mbar_wait(loready + b, pb);
+        C2T(2, i);
+        mbar_wait(accempty + b, pb ^ 1);
+        C2T(3, i);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + b * 32;
+        const uint32_t a = su32(as + b * 9 * c2hs::kATap);
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) {
+          const uint64_t bd = desc_plain(su32(bt + tap * c2h::kBTap));
+          const uint64_t ad = desc_plain(a + tap * c2hs::kATap);
+          asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d), "l"(ad),
+                       "l"(bd), "r"(kId), "r"((uint32_t)(tap > 0)));
+        }
+        commit(mmadone + b);
+        C2T(4, i);
+      }
+    }
+  } else if (warp < 2 + SW) {
+    const int quarter = warp & 3, r = quarter * 32 + lane;
+    const int part = (warp - 2) / 4;
+    constexpr int kShares = SW / 4;
+    int rseq = 0, qb = qb0, p = p0;
+    for (int i = 0; i < nmine; ++i) {
+      const bool chained = i > 0 && p > 0;
+      const int nq = p + 1 == H3 ? 0 : p + 1;  // the next tile chains unless it wraps or is not ours
+      const bool next_chained = i + 1 < nmine && nq > 0;
+      const int s0 = chained ? rseq - 1 : rseq;
+      const int b = i % NB;
+      mbar_wait(mmadone + b, (uint32_t)(((i / NB) & 1) ^ 1));
+      if (warp == 2 && lane == 0) C2T(6, i);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      unsigned char* abuf = as + b * 9 * c2hs::kATap + (r & 7) * 16 + (r >> 3) * 256;  // this pixel's A row
+      const bool edge = 2 * (qb * 128 + r) + 1 >= W2;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int rs = s0 + a;
+        const int slot = rs % R;
+        mbar_wait(full + slot, (uint32_t)((rs / R) & 1));
+        if (a == 2 && warp == 2 && lane == 0) C2T(5, i);
+        const unsigned char* ev = rows + slot * kSlot;
+        const unsigned char* od = ev + kPlaneStride;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          const int tap = a * 3 + bb;
+          if ((tap * kShares) / 9 != part) continue;
+          const int row = bb == 2 ? r + 1 : r;
+          const unsigned char* pl = (bb == 1 ? ev : od) + 32 * row;
+          const int sw = (row >> 2) & 1;
+          float4 x0 = *reinterpret_cast<const float4*>(pl + 16 * sw);
+          float4 x1 = *reinterpret_cast<const float4*>(pl + 16 * (sw ^ 1));
+          if (bb == 2 && edge) x0 = x1 = make_float4(0.f, 0.f, 0.f, 0.f);
+          uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+          c2h::split_h2(x0.x, x0.y, h0, l0);
+          c2h::split_h2(x0.z, x0.w, h1, l1);
+          c2h::split_h2(x1.x, x1.y, h2, l2);
+          c2h::split_h2(x1.z, x1.w, h3, l3);
+          *reinterpret_cast<uint4*>(abuf + tap * c2hs::kATap) = make_uint4(h0, h1, h2, h3);        // k 0..7: hi
+          *reinterpret_cast<uint4*>(abuf + tap * c2hs::kATap + 128) = make_uint4(l0, l1, l2, l3);  // k 8..15: lo
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy A writes -> the MMA
+      __syncwarp();
+      if (warp == 2 && lane == 0) C2T(7, i);
+      if (lane == 0) {
+        mbar_arrive(loready + b);
+        mbar_arrive(empty + (s0 % R));
+        mbar_arrive(empty + ((s0 + 1) % R));
+        if (!next_chained) mbar_arrive(empty + ((s0 + 2) % R));
+      }
+      rseq += chained ? 2 : 3;
+      if (++p == H3) { p = 0; ++qb; }
+    }
+  } else {
+    const int quarter = warp & 3, r = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int qb = qb0, p = p0;
+    for (int i = 0; i < nmine; ++i) {
+      const int b = i % NB;
+      mbar_wait(mmadone + b, (uint32_t)((i / NB) & 1));
+      if (warp == 2 + SW && lane == 0) C2T(8, i);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t h[16], l[16];
+      const uint32_t d = tmem + lane_off + b * 32;
+      ld16(d, h);
+      ld16(d + 16, l);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty + b);
+      const int q = qb * 128 + r;
+      if (q < W3) {
+        float4* dst = reinterpret_cast<float4*>(out + ((size_t)p * W3 + q) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = fmaxf(__uint_as_float(h[4 * k + j]) + __uint_as_float(l[4 * k + j]), 0.f);
+          dst[k] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+      if (warp == 2 + SW && lane == 0) C2T(9, i);
+      if (++p == H3) { p = 0; ++qb; }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
 
 // Pre-launch hook of the row-staged kernels (kernels_conv2.cu): the 4-D
 // pair-plane tensor map of the input, cached per (device, pointer, shape).
@@ -442,6 +692,16 @@ static const char* v_conv2_h(const LaunchCheck& L) {
   if ((L.i32(4) & 1) && !fits(L, 0, 32ull * L.i32(3) * L.i32(4) + 32)) return "odd W2 needs 32 bytes of input slack";
   return nullptr;
 }
+template <int R, int NB, int SW>
+static const char* v_conv2_hs(const LaunchCheck& L) {
+  using C = c2hs::Cfg<R, NB, SW>;
+  if (const char* e = v_conv2_launch(L, C::kThreads, (unsigned)C::smem())) return e;
+  if ((L.i32(4) & 1) && !fits(L, 0, 32ull * L.i32(3) * L.i32(4) + 32)) return "odd W2 needs 32 bytes of input slack";
+  return nullptr;
+}
+#define C2HS(NAME, R, NB, SW)                                                                            \
+  {NAME, (const void*)k_conv2_hs<R, NB, SW>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, \
+   (int)c2hs::Cfg<R, NB, SW>::smem(), conv2_rows_prelaunch, v_conv2_hs<R, NB, SW>}
 #define C2H(NAME, R, NB, SW)                                                                            \
   {NAME, (const void*)k_conv2_h<R, NB, SW>, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, \
    (int)c2h::Cfg<R, NB, SW>::smem(), conv2_rows_prelaunch, v_conv2_h<R, NB, SW>}

@@ -456,6 +456,17 @@ static const Builtin kConv2Exp[] = {
     C2H("conv2_h_s12", 12, 3, 12),
     C2H("conv2_h_s8b2", 12, 2, 8),
     C2H("conv2_h_s8r16", 16, 3, 8),
+    // more split warps / a fourth TMEM buffer (the pipeline trace of the
+    // product, tools/conv2h_trace.py, puts the split stage on the critical path)
+    C2H("conv2_h_s16", 12, 3, 16),
+    C2H("conv2_h_s24", 12, 3, 24),
+    C2H("conv2_h_s12b4", 12, 4, 12),
+    C2H("conv2_h_s24b4", 12, 4, 24),
+    // A in shared memory (SS MMAs): R row slots, NB A/accumulator buffers, SW split warps
+    C2HS("conv2_hs", 8, 3, 12),
+    C2HS("conv2_hs_r12", 12, 3, 12),
+    C2HS("conv2_hs_s8", 8, 3, 8),
+    C2HS("conv2_hs_s16", 8, 3, 16),
 };
 DAGRT_REGISTER_EXP(kConv2Exp);
 

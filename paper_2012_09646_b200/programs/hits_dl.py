@@ -33,10 +33,18 @@ CONV2_WS_CFG = {"conv2_ws": (4, 2, 4), "conv2_ws6": (6, 2, 4), "conv2_ws6s8": (6
 CONV2_ROWS_CFG = {"conv2_rows": (12, 2, 8), "conv2_rows_s4": (12, 2, 4), "conv2_rows_r20": (20, 2, 8)}
 # one-MMA-per-tap fp16-split conv2 (c2h::Cfg<R, NB, SW>): B is 9 x 1 KB as in c2ws
 CONV2_H_CFG = {"conv2_h": (12, 3, 4), "conv2_h_s8": (12, 3, 8), "conv2_h_b4": (16, 4, 4), "conv2_h_s12": (12, 3, 12),
-               "conv2_h_s8b2": (12, 2, 8), "conv2_h_s8r16": (16, 3, 8)}
+               "conv2_h_s8b2": (12, 2, 8), "conv2_h_s8r16": (16, 3, 8), "conv2_h_s16": (12, 3, 16),
+               "conv2_h_s24": (12, 3, 24), "conv2_h_s12b4": (12, 4, 12), "conv2_h_s24b4": (12, 4, 24)}
+
+
+CONV2_HS_CFG = {"conv2_hs": (8, 3, 12), "conv2_hs_r12": (12, 3, 12), "conv2_hs_s8": (8, 3, 8),
+                "conv2_hs_s16": (8, 3, 16)}
 
 
 def conv2_ws_launch(name):
+    if name in CONV2_HS_CFG:  # A in shared memory: + NB x 9 taps x 4 KB
+        r, nb, sw = CONV2_HS_CFG[name]
+        return 32 * (6 + sw), 1024 + r * 8704 + 9 * 1024 + nb * 9 * 4096 + 8 * (2 * r + 3 * nb) + 16
     if name in CONV2_ROWS_CFG or name in CONV2_H_CFG:
         r, nb, sw = CONV2_ROWS_CFG.get(name) or CONV2_H_CFG[name]
         return 32 * (6 + sw), 1024 + r * 8704 + 9 * 1024 + 8 * (2 * r + 3 * nb) + 16
