@@ -215,17 +215,80 @@ def spmv_out_bytes(n, e):
     return 4 * n + 16 + 12 * SPMV_WARPS * grid, grid
 
 
+def degree_order(graph, device="auto"):
+    """The graph relabelled by descending total degree (hubs first): returns
+    (row_ptr, col_idx, row_ptr_t, col_idx_t) of P A P^T and new_id (old vertex
+    id -> new id).  Rows keep sorted columns.  A registration-time re-encoding
+    like the SpMV plans (outside the timed region): the DAG is unchanged, the
+    hub and authority vectors live in the new order (the scores of vertex v
+    are at new_id[v]).  On the HITS graph the gathers of the SpMVs then hit a
+    compact hot region of x: SpMV 218 vs 252 us, HITS DAG 4.90 vs 5.78 ms
+    (tools/spmv_relabel_lab.py)."""
+    import numpy as np
+    rp, ci, rpt, cit = graph
+    n = rp.size - 1
+    use_torch = False
+    if device == "auto":
+        try:
+            use_torch = torch.cuda.is_available()
+        except Exception:
+            use_torch = False
+    if use_torch:
+        dev = torch.device("cuda")
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(dev)  # noqa: E731
+        drp, drpt = torch.diff(t(rp)), torch.diff(t(rpt))
+        order = torch.sort(-(drp + drpt), stable=True).indices
+        new = torch.empty(n, dtype=torch.int64, device=dev)
+        new[order] = torch.arange(n, device=dev)
+
+        def perm(rp_, ci_):
+            d = torch.diff(t(rp_))
+            rows = torch.repeat_interleave(torch.arange(n, device=dev), d)
+            key = new[rows] * n + new[t(ci_)]
+            key = torch.sort(key).values
+            r2, c2 = key // n, key % n
+            rpn = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+            rpn[1:] = torch.cumsum(torch.bincount(r2, minlength=n), 0)
+            return rpn.to(torch.int32).cpu().numpy(), c2.to(torch.int32).cpu().numpy()
+        a, b = perm(rp, ci), perm(rpt, cit)
+        return (a[0], a[1], b[0], b[1]), new.cpu().numpy()
+    deg = np.diff(rp.astype(np.int64)) + np.diff(rpt.astype(np.int64))
+    order = np.argsort(-deg, kind="stable")
+    new = np.empty(n, np.int64)
+    new[order] = np.arange(n)
+
+    def perm_np(rp_, ci_):
+        d = np.diff(rp_.astype(np.int64))
+        rows = np.repeat(np.arange(n, dtype=np.int64), d)
+        key = np.sort(new[rows] * n + new[ci_.astype(np.int64)])
+        r2, c2 = key // n, key % n
+        rpn = np.zeros(n + 1, np.int64)
+        np.cumsum(np.bincount(r2, minlength=n), out=rpn[1:])
+        return rpn.astype(np.int32), c2.astype(np.int32)
+    a, b = perm_np(rp, ci), perm_np(rpt, cit)
+    return (a[0], a[1], b[0], b[1]), new
+
+
 class Hits(Program):
-    """HITS hub/authority iteration with two SpMV branches per iteration (L882-886)."""
+    """HITS hub/authority iteration with two SpMV branches per iteration (L882-886).
+
+    ``vertex_order``: "degree" (default) registers the graph relabelled by
+    descending degree (degree_order(); ``self.new_id`` maps the given ids to
+    the registered ones, ``self.csr`` is the registered graph), "given" keeps
+    the given ids (``self.new_id`` = None)."""
     name = "hits"
 
-    def __init__(self, ctx, n=20_000_000, e=60_000_000, iters=HITS_ITERS, graph=None, **kw):
+    def __init__(self, ctx, n=20_000_000, e=60_000_000, iters=HITS_ITERS, graph=None, vertex_order="degree", **kw):
         super().__init__(ctx, **kw)
         self.n, self.iters = n, iters
-        if graph is None:
-            src = self.share.csr if self.share is not None else None
-            graph = src if src is not None else synth.powerlaw_graph(
-                self.seed, n, e, device=None if ctx.backend == "record" else "auto")
+        if self.share is not None and graph is None:  # the registered graph of the program shared
+            graph, self.new_id = self.share.csr, self.share.new_id
+        else:
+            if graph is None:
+                graph = synth.powerlaw_graph(self.seed, n, e, device=None if ctx.backend == "record" else "auto")
+            self.new_id = None
+            if vertex_order == "degree":
+                graph, self.new_id = degree_order(graph, device=None if ctx.backend == "record" else "auto")
         self.csr = graph
         rp, ci, rpt, cit = graph
         self.e = int(rp[-1])

@@ -263,7 +263,7 @@ def test_hits_parity(ctx, n, e):
     p.load_inputs(0)
     p.run()
     ctx.sync()
-    _hits_check(p, graph, 3)
+    _hits_check(p, p.csr, 3)  # the registered (degree-ordered) graph
 
 
 def test_hits_star_and_chain():
@@ -280,11 +280,36 @@ def test_hits_star_and_chain():
     At.sort_indices()
     graph = (A.indptr.astype(np.int32), A.indices.astype(np.int32),
              At.indptr.astype(np.int32), At.indices.astype(np.int32))
-    p = Hits(c, n=n, iters=2, graph=graph)
+    for order in ("degree", "given"):
+        p = Hits(c, n=n, iters=2, graph=graph, vertex_order=order)
+        p.load_inputs(0)
+        p.run()
+        c.sync()
+        _hits_check(p, p.csr, 2)
+        if order == "given":
+            assert p.csr is graph and p.new_id is None
+    c.close()
+
+
+def test_hits_degree_order_is_a_relabelling():
+    """The registered degree-ordered graph is P A P^T: the GPU scores in the
+    registered order, mapped back through new_id, are the oracle's scores on
+    the GIVEN graph (L882-886)."""
+    n, e = 200_000, 600_000
+    graph = synth.powerlaw_graph(9, n, e)
+    c = D.Context(device=0)
+    p = Hits(c, n=n, e=e, iters=3, graph=graph)
+    assert p.new_id is not None and np.array_equal(np.sort(p.new_id), np.arange(n))
     p.load_inputs(0)
     p.run()
     c.sync()
-    _hits_check(p, graph, 2)
+    o = ohits.hits(*graph, iterations=3)
+    for name in ("a1", "h1"):
+        got = p.t[name].cpu().numpy()[p.new_id]  # back to the given ids
+        ok, info = close(got, o[name])
+        assert ok, (name, info)
+    deg = np.diff(p.csr[0]) + np.diff(p.csr[2])
+    assert np.all(np.diff(deg) <= 0)  # hubs first
     c.close()
 
 
