@@ -44,7 +44,12 @@ __global__ void __launch_bounds__(256, 8) k_l2norm(const float* __restrict__ v, 
     // (ncu: XU 33%) while the loop waited on memory; 32 registers keep the
     // full 8 CTAs per SM (a two-load form at 33 registers lost occupancy)
     auto sq4 = [](float4 a) { return (double)fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, a.w * a.w))); };
-    for (long long i = tid; i < n4; i += nth) acc += sq4(ldg_stream(v4 + i));
+    long long i = tid;
+    for (; i + nth < n4; i += 2 * nth) {  // two 16-byte loads in flight (latency-bound at one)
+      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth);
+      acc += sq4(a) + sq4(b);
+    }
+    if (i < n4) acc += sq4(ldg_stream(v4 + i));
     done = n4 << 2;
   }
   for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];
