@@ -31,7 +31,7 @@ def main(path):
               f"{f(dr.get('frac_cp'))} | {f(dr.get('frac_work'))} | {f(cf.get('resident_ms'))} | "
               f"{rf.get('kernel')} | {f(rf.get('frac'))} |")
     g = d.get("suite_geomean", {})
-    print("\nGeomeans over the six: " + ", ".join(f"{k} {v:.3f}" for k, v in g.items() if v is not None))
+    print("\nGeomeans over the six: " + ", ".join(f"{k} {v:.3f}" for k, v in g.items() if isinstance(v, float)))
     sch = d.get("scheduler", {})
     if sch:
         print(f"\nHost cost per launch (B&S DAG): {sch.get('sched_us_per_launch'):.2f} us = "
