@@ -77,12 +77,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = su32(b);
-  uint32_t done = 0;
-  long long spins = 0;
-  while (!done) {
+  uint32_t done;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  if (done) return;  // the common case: one probe, no guard bookkeeping
+  for (uint32_t spins = 0; !done; ++spins) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    if (++spins > (1ll << 30)) __trap();  // never hang the GPU on a protocol bug
+    if (spins > (1u << 30)) __trap();  // never hang the GPU on a protocol bug
   }
 }
 __device__ __forceinline__ void tma3d(uint32_t dst, const void* tmap, int c0, int c1, int c2, uint32_t bar) {
@@ -352,6 +354,11 @@ __global__ void __launch_bounds__(c2h::Cfg<R, NB, SW>::kThreads, 1)
       const bool edge = 2 * (qb * 128 + r) + 1 >= W2;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
+        // only the rows holding one of this part's taps are waited for and
+        // read (each try_wait costs ~100+ cycles even when the row is ready:
+        // ncu put a quarter of the split warps' samples on these waits)
+        if ((3 * a * kShares) / 9 != part && ((3 * a + 1) * kShares) / 9 != part && ((3 * a + 2) * kShares) / 9 != part)
+          continue;
         const int rs = s0 + a;
         const int slot = rs % R;
         mbar_wait(full + slot, (uint32_t)((rs / R) & 1));
