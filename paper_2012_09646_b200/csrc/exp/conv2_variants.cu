@@ -462,6 +462,10 @@ static const Builtin kConv2Exp[] = {
     C2H("conv2_h_s24", 12, 3, 24),
     C2H("conv2_h_s12b4", 12, 4, 12),
     C2H("conv2_h_s24b4", 12, 4, 24),
+    // deeper row rings (the producer waits for row slots the split still holds)
+    C2H("conv2_h_r16", 16, 3, 12),
+    C2H("conv2_h_r20", 20, 3, 12),
+    C2H("conv2_h_r24", 24, 3, 12),
     // A in shared memory (SS MMAs): R row slots, NB A/accumulator buffers, SW split warps
     C2HS("conv2_hs", 8, 3, 12),
     C2HS("conv2_hs_r12", 12, 3, 12),

@@ -34,7 +34,8 @@ CONV2_ROWS_CFG = {"conv2_rows": (12, 2, 8), "conv2_rows_s4": (12, 2, 4), "conv2_
 # one-MMA-per-tap fp16-split conv2 (c2h::Cfg<R, NB, SW>): B is 9 x 1 KB as in c2ws
 CONV2_H_CFG = {"conv2_h": (12, 3, 4), "conv2_h_s8": (12, 3, 8), "conv2_h_b4": (16, 4, 4), "conv2_h_s12": (12, 3, 12),
                "conv2_h_s8b2": (12, 2, 8), "conv2_h_s8r16": (16, 3, 8), "conv2_h_s16": (12, 3, 16),
-               "conv2_h_s24": (12, 3, 24), "conv2_h_s12b4": (12, 4, 12), "conv2_h_s24b4": (12, 4, 24)}
+               "conv2_h_s24": (12, 3, 24), "conv2_h_s12b4": (12, 4, 12), "conv2_h_s24b4": (12, 4, 24),
+               "conv2_h_r16": (16, 3, 12), "conv2_h_r20": (20, 3, 12), "conv2_h_r24": (24, 3, 12)}
 
 
 CONV2_HS_CFG = {"conv2_hs": (8, 3, 12), "conv2_hs_r12": (12, 3, 12), "conv2_hs_s8": (8, 3, 8),

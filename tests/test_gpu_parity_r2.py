@@ -152,7 +152,8 @@ def test_dl_4096_elementwise():
 @pytest.mark.parametrize("kernel", ["conv2_ws", "conv2_ws6", "conv2_ws6s8", "conv2_ws6b3", "conv2_ws5s8b3",
                                     "conv2_rows", "conv2_rows_s4", "conv2_rows_r20", "conv2_h", "conv2_h_s8",
                                     "conv2_h_b4", "conv2_h_s16", "conv2_h_s24", "conv2_h_s12b4", "conv2_h_s24b4",
-                                    "conv2_hs", "conv2_hs_r12", "conv2_hs_s8", "conv2_hs_s16"])
+                                    "conv2_hs", "conv2_hs_r12", "conv2_hs_s8", "conv2_hs_s16", "conv2_h_r16",
+                                    "conv2_h_r20", "conv2_h_r24"])
 @pytest.mark.parametrize("h,w", [(19, 23), (515, 517), (1030, 2050), (4096, 4096)])
 def test_conv2_ws_matches_oracle(exp, h, w, kernel):
     """The warp-specialised conv2 (A_lo in TMEM; csrc/kernels_conv2.cu) against
