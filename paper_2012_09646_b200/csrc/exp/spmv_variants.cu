@@ -849,6 +849,25 @@ __global__ void __launch_bounds__(256, 3) k_spmv_pad2b3(const int* __restrict__,
   spmv_pad2_body<3>(plan, x, y, N_);
 }
 
+// spmv_hub*: the product body with the hub head of x staged in shared memory
+// (spmv_common.cuh HUB); H = dynamic shared memory / 4 per launch; 256 x 4,
+// 512 x 2 and 1024 x 1 threads per SM (the same 64-register budget).
+__global__ void __launch_bounds__(256, 4) k_spmv_hub4(const int* __restrict__, const int* __restrict__,
+                                                      const int* __restrict__ plan, const float* __restrict__ x,
+                                                      float* __restrict__ y, long long N_) {
+  spmv_pad2_body<4, true>(plan, x, y, N_);
+}
+__global__ void __launch_bounds__(512, 2) k_spmv_hub2(const int* __restrict__, const int* __restrict__,
+                                                      const int* __restrict__ plan, const float* __restrict__ x,
+                                                      float* __restrict__ y, long long N_) {
+  spmv_pad2_body<2, true>(plan, x, y, N_);
+}
+__global__ void __launch_bounds__(1024, 1) k_spmv_hub1(const int* __restrict__, const int* __restrict__,
+                                                       const int* __restrict__ plan, const float* __restrict__ x,
+                                                       float* __restrict__ y, long long N_) {
+  spmv_pad2_body<1, true>(plan, x, y, N_);
+}
+
 // ---------------------------------------------------------------------------
 // spmv_ws: the padded non-zero split with the gathers and the row logic on
 // DIFFERENT warps.  ncu on the product (profiles/r2_*): the gathers are
@@ -1246,6 +1265,9 @@ static const Builtin kHitsExp[] = {
     {"spmv_pad", (const void*)k_spmv_pad, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad_l2", (const void*)k_spmv_pad_l2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_ws", (const void*)k_spmv_ws, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
+    {"spmv_hub4", (const void*)k_spmv_hub4, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 56 * 1024, nullptr, v_spmv_plan_kernel},
+    {"spmv_hub2", (const void*)k_spmv_hub2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 112 * 1024, nullptr, v_spmv_plan_kernel},
+    {"spmv_hub1", (const void*)k_spmv_hub1, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 226 * 1024, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2", (const void*)k_spmv_pad2, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_pad2b3", (const void*)k_spmv_pad2b3, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},
     {"spmv_nz", (const void*)k_spmv_nz, "const ptr, const ptr, const ptr, const ptr, out ptr, sint64", KF_NONE, 0, nullptr, v_spmv_plan_kernel},

@@ -339,12 +339,47 @@ __device__ __forceinline__ void spmv_pad_body(const int* __restrict__ plan, cons
 //            shuffle up, one broadcast for the carry;
 //   else     the segmented scan as in the product.
 // Same rows, same deposits; fp32 sums in a different (fixed) order.
-template <int MINB>
+//
+// HUB: the gathers of the hot head of x come from shared memory.  On the
+// degree-ordered HITS graph (vertices relabelled by descending degree when the
+// graph is registered, programs/hits_dl.py degree_order) the first H entries
+// of x are the hubs that most non-zeros point at; each CTA stages x[0, H) once
+// (H = dynamic shared memory / 4, a launch parameter) and every gather with a
+// column below H is a shared-memory load instead of an L1/L2 request -- the
+// request rate of the random gathers is this kernel's bound (tools/spmv_lab.py).
+// The values are the same, so the sums are bit-identical to HUB = false.
+__device__ __forceinline__ int hub_stage(const float* __restrict__ x, int n, float* hub) {
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  int H = min((int)(dyn >> 2), n) & ~3;
+  if (!aligned16(x)) H = 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* h4 = reinterpret_cast<float4*>(hub);
+  for (int i = threadIdx.x; i < (H >> 2); i += blockDim.x) h4[i] = __ldg(x4 + i);
+  __syncthreads();
+  return H;
+}
+__device__ __forceinline__ void nz_gather_hub(const NzIn& in, const float* __restrict__ x, const float* hub,
+                                              int H, float (&v)[4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = in.c[u];
+    v[u] = (unsigned)c < (unsigned)H ? hub[c] : (c >= 0 ? __ldg(x + c) : 0.f);
+  }
+}
+
+template <int MINB, bool HUB = false>
 __device__ __forceinline__ void spmv_pad2_body(const int* __restrict__ plan, const float* __restrict__ x,
                                                float* __restrict__ y, long long N_) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const PadPlan P = pad_plan(plan);
   if ((long long)P.n != N_ || P.n == 0) return;
+  extern __shared__ __align__(16) float hub_sm[];
+  const int H = HUB ? hub_stage(x, P.n, hub_sm) : 0;
+  auto gather = [&](const NzIn& in, float (&vv)[4]) {
+    if (HUB) nz_gather_hub(in, x, hub_sm, H, vv);
+    else nz_gather(in, x, vv);
+  };
   const int G = (int)gridDim.x * (blockDim.x >> 5);
   const int g = (int)blockIdx.x * (blockDim.x >> 5) + warp;
   const int per = (P.nc + G - 1) / G;
@@ -368,7 +403,7 @@ __device__ __forceinline__ void spmv_pad2_body(const int* __restrict__ plan, con
   NzIn nxt = cur;
   if (cb + 1 < ce) nxt = pad_load(P, cb + 1, lane, pol);
   float v[4];
-  nz_gather(cur, x, v);
+  gather(cur, v);
   for (int c = cb; c < ce; ++c) {
     uint4 fw = cur.fw;
     if (c == cb) fw.x &= ~1u;
@@ -377,7 +412,7 @@ __device__ __forceinline__ void spmv_pad2_body(const int* __restrict__ plan, con
     const int nst = __popc(fl);
     float vn[4] = {0.f, 0.f, 0.f, 0.f};
     if (c + 1 < ce) {
-      nz_gather(nxt, x, vn);
+      gather(nxt, vn);
       cur = nxt;
       if (c + 2 < ce) nxt = pad_load(P, c + 2, lane, pol);
     }
