@@ -27,6 +27,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -308,7 +309,57 @@ struct DeferBackend final : Backend {
   void* fork_ev = nullptr;
   uint64_t replays = 0, captures = 0, eager = 0;
 
-  explicit DeferBackend(Backend* inner) : in(inner) {}
+  // Event-record nodes of a captured batch.  A vertex's event is needed
+  // outside its batch only if later work or a host access waits on it (a
+  // later batch, a host read of an earlier sink); every other record would
+  // be an external event node that the graph executes for nothing (measured:
+  // VEC 29.1 -> 27.7 us per DAG without them, tools/f1_lab.py).  So the
+  // first, eager issue of a batch LEARNS which of its records escape (an
+  // outside wait or sync on the event before it is recorded again), and the
+  // capture gives only those their own event node; the others stand for
+  // their stream's tail event in the graph -- later than the vertex on the
+  // same stream, so a wait on it is still correct, only possibly longer.
+  // DAGRT_F1_EVENTS=vertex (a node per vertex) / tail (none) for the labs.
+  enum { EV_LEARN, EV_VERTEX, EV_TAIL } ev_mode = EV_LEARN;
+  struct Pending { void* e; uint64_t h; uint32_t ord; };
+  std::vector<Pending> pend;                                   // records of eager batches
+  std::vector<std::pair<uint64_t, std::vector<uint32_t>>> esc;  // batch hash -> escaped record ordinals
+  void note_escape(void* e) {
+    for (size_t i = 0; i < pend.size(); ++i)
+      if (pend[i].e == e) {
+        std::vector<uint32_t>* v = nullptr;
+        for (auto& x : esc)
+          if (x.first == pend[i].h) v = &x.second;
+        if (!v) {
+          if (esc.size() >= 64) esc.erase(esc.begin());
+          esc.push_back({pend[i].h, {}});
+          v = &esc.back().second;
+        }
+        if (std::find(v->begin(), v->end(), pend[i].ord) == v->end()) v->push_back(pend[i].ord);
+        pend[i] = pend.back();
+        pend.pop_back();
+        return;
+      }
+  }
+  void forget_pending(void* e) {
+    for (size_t i = 0; i < pend.size(); ++i)
+      if (pend[i].e == e) {
+        pend[i] = pend.back();
+        pend.pop_back();
+        return;
+      }
+  }
+  bool escaped(uint64_t h, uint32_t ord) const {
+    for (auto& x : esc)
+      if (x.first == h) return std::find(x.second.begin(), x.second.end(), ord) != x.second.end();
+    return false;
+  }
+  explicit DeferBackend(Backend* inner) : in(inner) {
+    if (const char* t = getenv("DAGRT_F1_EVENTS")) {
+      if (!strcmp(t, "vertex")) ev_mode = EV_VERTEX;
+      if (!strcmp(t, "tail")) ev_mode = EV_TAIL;
+    }
+  }
   ~DeferBackend() override {
     for (auto& e : cache)
       if (e.exec) cudaGraphExecDestroy(e.exec);
@@ -382,6 +433,7 @@ struct DeferBackend final : Backend {
   }
   cudaError_t record(void* e, void* s) override {
     unalias(e);
+    forget_pending(e);
     if (!enabled) {
       if (cudaError_t r = pre_eager(s)) return r;
       return in->record(e, s);
@@ -394,6 +446,7 @@ struct DeferBackend final : Backend {
     return cudaSuccess;
   }
   cudaError_t wait(void* s, void* e) override {
+    note_escape(e);
     e = resolve(e);
     if (!enabled) {
       if (cudaError_t r = pre_eager(s)) return r;
@@ -441,6 +494,7 @@ struct DeferBackend final : Backend {
     return in->prefetch(p, n, dev, s);
   }
   cudaError_t event_sync(void* e) override {
+    note_escape(e);
     if (cudaError_t r = flush()) return r;
     return in->event_sync(resolve(e));
   }
@@ -572,21 +626,30 @@ struct DeferBackend final : Backend {
     return cudaSuccess;
   }
 
-  cudaError_t capture(Entry* en) {
+  cudaError_t capture(Entry* en, uint64_t h) {
     std::vector<void*> streams = batch_streams();
     if (!fork_ev)
       if (cudaError_t r = in->event_create(&fork_ev)) return r;
-    for (const Op& o : ops)
-      if (o.kind == OP_RECORD) {
-        void* e;
-        if (cudaError_t r = owned_event(&e)) return r;
-        en->rec_ev.push_back(e);
-      }
     std::vector<void*> join(streams.size());
     for (size_t i = 0; i < streams.size(); ++i) {
       if (cudaError_t r = owned_event(&join[i])) return r;
       en->tail_ev.push_back({streams[i], join[i]});
     }
+    std::vector<bool> node;  // per record: its own external event node?
+    for (const Op& o : ops)
+      if (o.kind == OP_RECORD) {
+        const uint32_t ord = (uint32_t)node.size();
+        const bool own = ev_mode == EV_VERTEX || (ev_mode == EV_LEARN && escaped(h, ord));
+        node.push_back(own);
+        void* e = nullptr;
+        if (!own) {  // the vertex's event stands for its stream's tail in the graph
+          for (size_t i = 0; i < streams.size(); ++i)
+            if (streams[i] == o.s) e = join[i];
+        } else if (cudaError_t r = owned_event(&e)) {
+          return r;
+        }
+        en->rec_ev.push_back(e);
+      }
     cudaStream_t org = (cudaStream_t)origin;
     if (cudaError_t r = cudaStreamBeginCapture(org, cudaStreamCaptureModeRelaxed)) return r;
     cudaError_t err = in->record(fork_ev, origin);
@@ -598,8 +661,8 @@ struct DeferBackend final : Backend {
         if (!external_wait(i)) err = in->wait(ops[i].s, ops[i].e);
       } else {
         err = issue(ops[i], true);
-        if (!err && ops[i].kind == OP_RECORD)
-          err = cudaEventRecordWithFlags((cudaEvent_t)en->rec_ev[r++], (cudaStream_t)ops[i].s,
+        if (!err && ops[i].kind == OP_RECORD && node[r++])
+          err = cudaEventRecordWithFlags((cudaEvent_t)en->rec_ev[r - 1], (cudaStream_t)ops[i].s,
                                          cudaEventRecordExternal);
       }
     }
@@ -648,7 +711,7 @@ struct DeferBackend final : Backend {
         std::find(seen.begin(), seen.end(), h) != seen.end()) {
       Entry en;
       en.key = key;
-      cudaError_t ce = capture(&en);
+      cudaError_t ce = capture(&en, h);
       if (!ce) {
         if (cache.size() >= 16) {
           cudaGraphExecDestroy(cache.front().exec);
@@ -668,10 +731,17 @@ struct DeferBackend final : Backend {
         nocap.push_back(h);
       }
     }
-    if (!done) {  // first sighting: issue eagerly, remember the batch
+    if (!done) {  // first sighting: issue eagerly, remember the batch and its records
       err = cudaSuccess;
-      for (const Op& o : ops)
+      uint32_t ord = 0;
+      for (const Op& o : ops) {
         if (!err) err = issue(o, false);
+        if (o.kind == OP_RECORD) {
+          forget_pending(o.e);
+          if (pend.size() < 4096) pend.push_back(Pending{o.e, h, ord});
+          ++ord;
+        }
+      }
       if (seen.size() >= 64) seen.erase(seen.begin());
       seen.push_back(h);
       ++eager;
@@ -683,6 +753,7 @@ struct DeferBackend final : Backend {
   // A stream wait issued right away (after flushing the batch): used to
   // order a D2H copy after its producers without blocking the host.
   cudaError_t wait_now(void* s, void* e) {
+    note_escape(e);
     if (cudaError_t r = flush()) return r;
     if (cudaError_t r = pre_eager(s)) return r;
     return in->wait(s, resolve(e));

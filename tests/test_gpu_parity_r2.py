@@ -306,6 +306,39 @@ def test_graph_cache_orders_same_stream_work_across_flush():
     c.close()
 
 
+@pytest.mark.parametrize("events", ["learn", "vertex", "tail"])
+def test_graph_cache_host_reads_of_mid_stream_vertices(events, monkeypatch):
+    """f1 event-record nodes (DAGRT_F1_EVENTS): per run K1 A += 1, K2 C = A^2
+    (K2 follows K1 on its stream, so K1 is not the stream's tail), K3 B += 1
+    on another stream; the host reads B (flushes the batch), then A (waits
+    on K1's event from OUTSIDE the batch: an escaped record, given its own
+    node in "learn" mode after the eager first issue), then C.  Every read
+    sees run r's values in all three modes."""
+    monkeypatch.setenv("DAGRT_F1_EVENTS", events)
+    c = D.Context(device=0, graph_cache=True)
+    n = 1 << 20
+    A = torch.zeros(n, device="cuda")
+    B = torch.zeros(n, device="cuda")
+    Cc = torch.zeros(n, device="cuda")
+    torch.cuda.synchronize()
+    a, b, cc = (c.register_tensor(k, t) for k, t in (("A", A), ("B", B), ("C", Cc)))
+    import ctypes as C
+    buf = (C.c_float * 4)()
+    for r in range(1, 9):
+        c.launch("axpb", 148, 256, a, n, 1.0, 1.0)
+        c.launch("square", 148, 256, a, cc, n)
+        c.launch("axpb", 148, 256, b, n, 1.0, 1.0)
+        c.host_read(b, C.addressof(buf), 4 * (n - 4), 16)
+        assert list(buf) == [r] * 4
+        c.host_read(a, C.addressof(buf), 0, 16)
+        assert list(buf) == [r] * 4
+        c.host_read(cc, C.addressof(buf), 4 * (n // 2), 16)
+        assert list(buf) == [r * r] * 4
+    c.sync()
+    assert c.stats()["graph_replays"] >= 4
+    c.close()
+
+
 # ------------------------------------------------------------------ library-call vertices
 def test_library_call_vertex_on_the_gpu():
     """A library call (torch.matmul on the stream the scheduler picked,
