@@ -105,6 +105,12 @@ BS2L_VARIANT(k_bs2l_o4s3b3, 4, 3, 3)
 BS2L_VARIANT(k_bs2l_o6s3b3, 6, 3, 3)
 BS2L_VARIANT(k_bs2l_o6s2b3, 6, 2, 3)
 BS2L_VARIANT(k_bs2l_o8s2b2, 8, 2, 2)
+// round-2b pricer (bs_price_m: 32 FP64 per option, constant tables, ring issued before the setup)
+BS2M_VARIANT(k_bs2m_o6s3b2, 6, 3, 2)
+BS2M_VARIANT(k_bs2m_o4s3b3, 4, 3, 3)
+BS2M_VARIANT(k_bs2m_o6s3b3, 6, 3, 3)
+BS2M_VARIANT(k_bs2m_o8s2b2, 8, 2, 2)
+BS2M_VARIANT(k_bs2m_o4s4b2, 4, 4, 2)
 BS3_VARIANT(k_bs3_o6s4b2, 6, 4, 2)
 BS3_VARIANT(k_bs3_o6s6b2, 6, 6, 2)
 BS3_VARIANT(k_bs3_o4s8b2, 4, 8, 2)
@@ -366,6 +372,11 @@ static const Builtin kBsExp[] = {
     {"bs2t_o2s4b4", (const void*)k_bs2t_o2s4b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2t_o6s3b2", (const void*)k_bs2t_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     // lean pricer (larger tables, one series term fewer each)
+    {"bs2m_o6s3b2", (const void*)k_bs2m_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2m_o4s3b3", (const void*)k_bs2m_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2m_o6s3b3", (const void*)k_bs2m_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2m_o8s2b2", (const void*)k_bs2m_o8s2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2m_o4s4b2", (const void*)k_bs2m_o4s4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o6s3b2", (const void*)k_bs2l_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o4s3b3", (const void*)k_bs2l_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o6s3b3", (const void*)k_bs2l_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
