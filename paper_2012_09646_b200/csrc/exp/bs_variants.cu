@@ -105,6 +105,22 @@ BS2L_VARIANT(k_bs2l_o4s3b3, 4, 3, 3)
 BS2L_VARIANT(k_bs2l_o6s3b3, 6, 3, 3)
 BS2L_VARIANT(k_bs2l_o6s2b3, 6, 2, 3)
 BS2L_VARIANT(k_bs2l_o8s2b2, 8, 2, 2)
+// Memory-path floor of the TMA-staged body: the same ring, loads, stores and
+// table setup with the pricing replaced by one DMUL (tools/bs_variants.py).
+struct BsPricerCopy {
+  using Tables = BsTabsL;
+  static __device__ __forceinline__ void init(Tables& T) { bs_tabsl_init(T); }
+  template <int W>
+  static __device__ __forceinline__ void price(const double (&s)[W], double (&o)[W], const BsConst& C,
+                                               const Tables&) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) o[w] = s[w] * C.inv_k;
+  }
+};
+__global__ void __launch_bounds__(256, 2) k_bs2c_o6s3b2(const double* __restrict__ s, double* __restrict__ c,
+                                                        long long n, double r, double v, double t, double k) {
+  bs2_tma_body<6, 3, BsPricerCopy>(s, c, n, r, v, t, k);
+}
 // round-2b pricer (bs_price_m: 32 FP64 per option, constant tables, ring issued before the setup)
 BS2M_VARIANT(k_bs2m_o6s3b2, 6, 3, 2)
 BS2M_VARIANT(k_bs2m_o4s3b3, 4, 3, 3)
@@ -377,6 +393,7 @@ static const Builtin kBsExp[] = {
     {"bs2m_o6s3b3", (const void*)k_bs2m_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2m_o8s2b2", (const void*)k_bs2m_o8s2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2m_o4s4b2", (const void*)k_bs2m_o4s4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2c_o6s3b2", (const void*)k_bs2c_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o6s3b2", (const void*)k_bs2l_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o4s3b3", (const void*)k_bs2l_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o6s3b3", (const void*)k_bs2l_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
