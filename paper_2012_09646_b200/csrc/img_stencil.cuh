@@ -173,4 +173,123 @@ __device__ __forceinline__ void stencil_body(const float* __restrict__ src, floa
   }
 }
 
+
+// The same stencil with the row staging done by cp.async (LDGSTS): every
+// thread copies its 16 bytes (and the halo threads 4) of input row y + PF
+// straight into a ring of PF + 1 shared-memory rows, so PF rows of loads are
+// in flight per thread without holding them in registers (the register
+// prefetch of stencil_body<PF > 1> cost occupancy).  Zero padding through the
+// copies' source size (0 bytes read = 16 / 4 zero bytes written).  Row slot
+// layout: index j holds column x0 - 4 + j (the 4-float left pad keeps every
+// 16-byte destination aligned).  One CTA barrier per row, as before.
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+constexpr int kImgRowLen = kImgCols + 8;  // ring row: 4-float pads on both sides (R <= 4)
+// ring_s: (PF + 1) x kImgRowLen floats of shared memory, 16-byte aligned (declared
+// by the kernel, so that the instantiations for several R share it)
+template <int R, typename F, int PF>
+__device__ __forceinline__ void stencil_body_async(const float* __restrict__ src, float* __restrict__ dst,
+                                                   int H, int W, const F& f, float (*ring_s)[kImgRowLen]) {
+  constexpr int D = 2 * R + 1;
+  constexpr int NS = PF + 1;            // ring slots
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * kImgCols;
+  const int rows = (H + (int)gridDim.y - 1) / (int)gridDim.y;
+  const int y0 = blockIdx.y * rows;
+  const int y1 = min(H, y0 + rows);
+  const int cx = x0 + 4 * t;
+  const bool vec = ((W & 3) == 0) && aligned16(src) && aligned16(dst);
+
+  float ring[D][F::NCH][4];
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int c = 0; c < F::NCH; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ring[k][c][q] = 0.f;
+
+  // issue the copies of input row y (zeros outside the image) into slot sl
+  auto issue_row = [&](int y, int sl) {
+    float* r = ring_s[sl];
+    const bool in = y >= 0 && y < H;
+    const float* s = src + (size_t)(in ? y : 0) * W;
+    if (vec) {
+      cp_async16(r + 4 + 4 * t, in && cx + 3 < W ? s + cx : src, in && cx + 3 < W ? 16 : 0);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        cp_async4(r + 4 + 4 * t + q, in && cx + q < W ? s + cx + q : src, in && cx + q < W ? 4 : 0);
+    }
+    if (t < R) {
+      const int xl = x0 - R + t;
+      cp_async4(r + 4 - R + t, in && xl >= 0 ? s + xl : src, in && xl >= 0 ? 4 : 0);
+    } else if (t >= kImgThreads - R) {
+      const int k = t - (kImgThreads - R);
+      const int xr = x0 + kImgCols + k;
+      cp_async4(r + 4 + kImgCols + k, in && xr < W ? s + xr : src, in && xr < W ? 4 : 0);
+    }
+  };
+
+  const int ybeg = y0 - R, yend = y1 + R;  // input rows [ybeg, yend)
+#pragma unroll
+  for (int p = 0; p < PF; ++p) {
+    if (ybeg + p < yend) issue_row(ybeg + p, p);
+    cp_async_commit();  // one group per row (possibly empty): wait_group counts stay uniform
+  }
+  int sl = 0;
+  for (int y = ybeg; y < yend; ++y) {
+    cp_async_wait<PF - 1>();  // this thread's copies of row y have landed
+    __syncthreads();          // ... everyone's; and everyone is done with row y - 1's slot
+    const int ns = sl == 0 ? NS - 1 : sl - 1;  // slot of row y - 1 = slot of row y + PF
+    if (y + PF < yend) issue_row(y + PF, ns);
+    cp_async_commit();
+    float win[4 + 2 * R];
+#pragma unroll
+    for (int j = 0; j < 4 + 2 * R; ++j) win[j] = ring_s[sl][4 - R + 4 * t + j];
+    float h[F::NCH][4];
+    f.horiz(win, h);
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k)
+#pragma unroll
+      for (int c = 0; c < F::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ring[k][c][q] = ring[k + 1][c][q];
+#pragma unroll
+    for (int c = 0; c < F::NCH; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ring[D - 1][c][q] = h[c][q];
+    const int yo = y - R;
+    if (yo >= y0 && cx < W) {
+      float4 o;
+      o.x = f.vert(ring, 0);
+      o.y = f.vert(ring, 1);
+      o.z = f.vert(ring, 2);
+      o.w = f.vert(ring, 3);
+      float* d = dst + (size_t)yo * W;
+      if (vec && cx + 3 < W) {
+        *reinterpret_cast<float4*>(d + cx) = o;
+      } else {
+        d[cx] = o.x;
+        if (cx + 1 < W) d[cx + 1] = o.y;
+        if (cx + 2 < W) d[cx + 2] = o.z;
+        if (cx + 3 < W) d[cx + 3] = o.w;
+      }
+    }
+    sl = sl == NS - 1 ? 0 : sl + 1;
+  }
+  cp_async_wait<0>();
+}
+
 }  // namespace dagrt

@@ -6,8 +6,9 @@
 // pixel and be shared-memory bound at ~1/3 of the HBM roofline, so both are
 // computed SEPARABLY with a column-streaming scheme:
 //   * a CTA owns 512 columns (128 threads x 4 columns) and a strip of rows;
-//   * per input row it stages the row segment + halo in shared memory
-//     (128-bit coalesced loads, double-buffered: one barrier per row),
+//   * per input row it stages the row segment + halo in shared memory with
+//     cp.async (16-byte copies, zero-filled outside the image) into a ring
+//     of PF + 1 rows, PF rows ahead (one barrier per row),
 //   * each thread applies the horizontal 1-D filter to its 4 columns from
 //     smem (two 128-bit LDS), pushes the result into a register ring of the
 //     last 2R+1 rows, and applies the vertical 1-D filter -> 4 outputs
@@ -21,29 +22,36 @@
 namespace dagrt {
 
 // BLUR (Fig. 6): normalised Gaussian, diameter d in {3, 5}.
+// Row staging by cp.async into a ring of kBlurPF + 1 rows (img_stencil.cuh
+// stencil_body_async): 358 vs 431 us per 16384^2 launch with the round-1
+// register-staged rows (0.92 vs 0.76 of HBM, bitwise-identical outputs,
+// tools/img_variants.py, profiles/r2_img_stencil_variants.json).
+constexpr int kBlurPF = 4, kSobelPF = 6;
 __global__ void __launch_bounds__(kImgThreads) k_blur(const float* __restrict__ src,
                                                       float* __restrict__ dst, int H, int W,
                                                       int diameter, float sigma2) {
+  __shared__ __align__(16) float ring_s[kBlurPF + 1][kImgRowLen];
   if (diameter == 3) {
     GaussFilter<1> f;
     f.init(sigma2);
-    stencil_body<1>(src, dst, H, W, f);
+    stencil_body_async<1, GaussFilter<1>, kBlurPF>(src, dst, H, W, f, ring_s);
   } else if (diameter == 5) {
     GaussFilter<2> f;
     f.init(sigma2);
-    stencil_body<2>(src, dst, H, W, f);
+    stencil_body_async<2, GaussFilter<2>, kBlurPF>(src, dst, H, W, f, ring_s);
   } else if (diameter == 1) {
     GaussFilter<0> f;
     f.init(sigma2);
-    stencil_body<0>(src, dst, H, W, f);
+    stencil_body_async<0, GaussFilter<0>, kBlurPF>(src, dst, H, W, f, ring_s);
   }
 }
 
-// SOBEL (Fig. 6): |grad| with the 3x3 Sobel taps.
+// SOBEL (Fig. 6): |grad| with the 3x3 Sobel taps (367 vs 453 us, 0.90 of HBM).
 __global__ void __launch_bounds__(kImgThreads) k_sobel(const float* __restrict__ src,
                                                        float* __restrict__ dst, int H, int W) {
+  __shared__ __align__(16) float ring_s[kSobelPF + 1][kImgRowLen];
   SobelFilter f;
-  stencil_body<1>(src, dst, H, W, f);
+  stencil_body_async<1, SobelFilter, kSobelPF>(src, dst, H, W, f, ring_s);
 }
 
 // MAX / MIN (Fig. 6): global extrema of the sobel mask (two sibling
