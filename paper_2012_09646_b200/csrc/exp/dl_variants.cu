@@ -7,6 +7,7 @@
 
 namespace dagrt {
 
+// the round-1/2 product conv1 (direct 64-byte-strided stores), for comparison
 __global__ void __launch_bounds__(256, 3) k_conv1_r2b3(const float* __restrict__ x, const float* __restrict__ w,
                                                        float* __restrict__ out, int H, int W) {
   conv1_body2<false>(x, w, out, H, W);
@@ -19,6 +20,33 @@ __global__ void __launch_bounds__(256, 2) k_conv1_r2b2(const float* __restrict__
                                                        float* __restrict__ out, int H, int W) {
   conv1_body2<false>(x, w, out, H, W);
 }
+
+// cp.async-staged, banded conv1 (conv1_body3): ring of 4 PFP + 5 input rows
+// in dynamic shared memory (NSR x kConv1RowLen floats)
+#define CONV1_CA(NAME, PFP, MINB, CS)                                                                  \
+  __global__ void __launch_bounds__(256, MINB) NAME(const float* __restrict__ x, const float* __restrict__ w, \
+                                                    float* __restrict__ out, int H, int W) {             \
+    extern __shared__ __align__(16) float c1ring[];                                                    \
+    conv1_body3<PFP, CS>(x, w, out, H, W, c1ring);                                                     \
+  }
+// conv1_body2 with warp-transposed (512-byte contiguous) stores
+__global__ void __launch_bounds__(256, 3) k_conv1_r2b3st(const float* __restrict__ x, const float* __restrict__ w,
+                                                         float* __restrict__ out, int H, int W) {
+  conv1_body2<false, true>(x, w, out, H, W);
+}
+__global__ void __launch_bounds__(256, 3) k_conv1_r2b3stcs(const float* __restrict__ x, const float* __restrict__ w,
+                                                           float* __restrict__ out, int H, int W) {
+  conv1_body2<true, true>(x, w, out, H, W);
+}
+__global__ void __launch_bounds__(256, 4) k_conv1_r2b4st(const float* __restrict__ x, const float* __restrict__ w,
+                                                         float* __restrict__ out, int H, int W) {
+  conv1_body2<false, true>(x, w, out, H, W);
+}
+CONV1_CA(k_conv1_ca1b4, 1, 4, false)
+CONV1_CA(k_conv1_ca1b3, 1, 3, false)
+CONV1_CA(k_conv1_ca2b3, 2, 3, false)
+CONV1_CA(k_conv1_ca2b4, 2, 4, false)
+CONV1_CA(k_conv1_ca2b4cs, 2, 4, true)
 
 __global__ void __launch_bounds__(256) k_conv1(const float* __restrict__ x, const float* __restrict__ w,
                                                float* __restrict__ out, int H, int W) {
@@ -112,6 +140,14 @@ __global__ void __launch_bounds__(256, 3) k_conv2(const float* __restrict__ in,
 }
 
 static const Builtin kDlExp[] = {
+    {"conv1_r2b3st", (const void*)k_conv1_r2b3st, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_r2b3stcs", (const void*)k_conv1_r2b3stcs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_r2b4st", (const void*)k_conv1_r2b4st, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
+    {"conv1_ca1b4", (const void*)k_conv1_ca1b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 9 * 4112},
+    {"conv1_ca1b3", (const void*)k_conv1_ca1b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 9 * 4112},
+    {"conv1_ca2b3", (const void*)k_conv1_ca2b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 13 * 4112},
+    {"conv1_ca2b4", (const void*)k_conv1_ca2b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 13 * 4112},
+    {"conv1_ca2b4cs", (const void*)k_conv1_ca2b4cs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE, 13 * 4112},
     {"conv1_b3", (const void*)k_conv1_b3, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4", (const void*)k_conv1_b4, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},
     {"conv1_b4cs", (const void*)k_conv1_b4cs, "const ptr, const ptr, out ptr, sint32, sint32", KF_NONE},

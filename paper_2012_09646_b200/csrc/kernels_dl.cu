@@ -12,10 +12,13 @@ namespace dagrt {
 
 // product conv1: two output rows per iteration, 3 CTAs/SM; grid.y walks row
 // PAIRS (633 us vs 690 us for one row per iteration, tools/conv2_variants.py);
-// the other shapes are in exp/dl_variants.cu
+// outputs transposed per warp through shared memory so that each 128-bit
+// store covers 512 contiguous bytes, with the evict-first policy (598 vs
+// 630 us, 0.82 vs 0.78 of HBM, bitwise-identical: tools/conv1_variants.py,
+// profiles/r2_conv1_variants.json); the other shapes are in exp/dl_variants.cu
 __global__ void __launch_bounds__(256, 3) k_conv1_r2b3(const float* __restrict__ x, const float* __restrict__ w,
                                                        float* __restrict__ out, int H, int W) {
-  conv1_body2<false>(x, w, out, H, W);
+  conv1_body2<true, true>(x, w, out, H, W);
 }
 
 // POOL: 2x2 mean, stride 2, 8 channels (two float4 per pixel).

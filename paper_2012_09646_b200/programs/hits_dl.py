@@ -428,8 +428,8 @@ class DeepLearning(Program):
         P = ctx.prepare
         # conv grids: x = column pairs / 256, y = output rows (<= 65535, kernels loop)
         x1b = max(1, -(-((w1 + 1) // 2) // 256))
-        # blocks loop over output row PAIRS ("conv1" = k_conv1_r2b3), ~16 blocks per SM
-        g1 = (x1b, max(1, min((h1 + 1) // 2, -(-16 * SMS // x1b))))
+        # blocks loop over output row PAIRS ("conv1" = k_conv1_r2b3), ~32 blocks per SM
+        g1 = (x1b, max(1, min((h1 + 1) // 2, -(-32 * SMS // x1b))))
         gp = grid_1d(h2 * w2 * 2, 256)
         x2b = max(1, -(-((w3 + 1) // 2) // 256))
         g2 = (x2b, max(1, min(h3, -(-8 * SMS // x2b))))
