@@ -12,6 +12,36 @@ namespace dagrt {
 
 constexpr int kMaxClasses = 16;
 
+// mbarrier / bulk-copy helpers (NORM ring, MMUL tiles)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- NORM
 // Z = (X - mu_f) / sd_f with population statistics, computed in ONE vertex:
 // pass 1 exact integer column sums S = sum x (int64) and Q = sum x^2
@@ -59,7 +89,7 @@ __device__ __forceinline__ double u128_to_double(u128 v) {
 
 __global__ void __launch_bounds__(512, 2) k_norm(const int* __restrict__ X, float* __restrict__ Z,
                                               unsigned char* stats, long long N, int F) {
-  extern __shared__ unsigned long long sh_u[];  // [RL][3F]: S, Qlo, Qhi per column
+  extern __shared__ __align__(128) unsigned long long sh_u[];  // [RL][3F]: S, Qlo, Qhi per column (aliases the ring)
   NormHdr* hdr = reinterpret_cast<NormHdr*>(stats);
   double* mean = reinterpret_cast<double*>(stats + 16);
   double* inv = mean + F;
@@ -75,10 +105,70 @@ __global__ void __launch_bounds__(512, 2) k_norm(const int* __restrict__ X, floa
   const long long r0 = (long long)blockIdx.x * rows_per;
   const long long r1 = min(N, r0 + rows_per);
 
+  // Ring path (vec, and dynamic shared memory for >= 2 chunks of CH = 2 RL
+  // rows): the block's rows stream through shared memory by cp.async.bulk,
+  // NST chunks in flight (one elected thread issues, an mbarrier per slot),
+  // in pass 1 and again in pass 2 (whose first chunks are issued before the
+  // grid barriers, so the statistics step overlaps them).  The register path
+  // below had 4 x 16 B per thread in flight and was latency-bound (ncu:
+  // long-scoreboard stalls dominate).  The per-thread partials' shared area
+  // aliases the ring between the two passes.
+  __shared__ uint64_t rfull[8];
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const int CH = 2 * RL;
+  const unsigned slot_bytes = (unsigned)CH * (unsigned)F * 4u;
+  const int NST = vec ? min(8, (int)(dyn / slot_bytes)) : 0;
+  const bool ring = NST >= 2 && aligned16(X) && RL * G <= (int)blockDim.x;
+  const long long nch = ring ? (r1 > r0 ? (r1 - r0) / CH : 0) : 0;  // whole chunks; the tail directly
+  const int4* ringp = reinterpret_cast<const int4*>(sh_u);
+  auto issue = [&](long long c, int st) {
+    mbar_expect_tx(&rfull[st], slot_bytes);
+    tma_bulk_g2s(reinterpret_cast<char*>(sh_u) + (size_t)st * slot_bytes, X + (r0 + c * CH) * F, slot_bytes,
+                 &rfull[st]);
+  };
+  if (ring) {
+    if (t == 0) {
+      for (int st = 0; st < NST; ++st) mbar_init(&rfull[st], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int st = 0; st < NST && st < nch; ++st) issue(st, st);
+    }
+    __syncthreads();
+  }
+  unsigned it = 0;  // ring iterations (both passes): slot it % NST, parity (it / NST) & 1
+
   // ---- pass 1: exact column sums
   long long s[4] = {0, 0, 0, 0};
   u128 q[4] = {0, 0, 0, 0};
-  if (active) {
+  if (ring) {
+    for (long long c = 0; c < nch; ++c, ++it) {
+      const int st = (int)(it % NST);
+      mbar_wait(&rfull[st], (it / NST) & 1);
+      int4 v[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+      if (active) {
+        const int4* sl = ringp + (size_t)st * CH * G;
+        v[0] = sl[rl * G + g];
+        v[1] = sl[(rl + RL) * G + g];
+      }
+      __syncthreads();  // the slot is consumed: refill it
+      if (t == 0 && c + NST < nch) issue(c + NST, st);
+      if (active) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          acc_x(s[0], q[0], v[u].x); acc_x(s[1], q[1], v[u].y);
+          acc_x(s[2], q[2], v[u].z); acc_x(s[3], q[3], v[u].w);
+        }
+      }
+    }
+    if (active) {
+      const int4* X4 = reinterpret_cast<const int4*>(X);
+      for (long long r = r0 + nch * CH + rl; r < r1; r += RL) {
+        int4 v = ldg_stream(X4 + r * G + g);
+        acc_x(s[0], q[0], v.x); acc_x(s[1], q[1], v.y);
+        acc_x(s[2], q[2], v.z); acc_x(s[3], q[3], v.w);
+      }
+    }
+  } else if (active) {
     if (vec) {
       const int4* X4 = reinterpret_cast<const int4*>(X);
       long long r = r0 + rl;
@@ -123,6 +213,14 @@ __global__ void __launch_bounds__(512, 2) k_norm(const int* __restrict__ X, floa
     o[F + j] = (unsigned long long)b;
     o[2 * F + j] = (unsigned long long)(b >> 64);
   }
+  const unsigned it2 = it;  // pass 2 starts at this ring iteration
+  if (ring) {
+    __syncthreads();  // the partials' reads of the (aliased) ring are done
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before async-proxy writes
+      for (int k = 0; k < NST && k < nch; ++k) issue(k, (int)((it2 + k) % NST));
+    }
+  }
   grid_barrier(&hdr->bar, gridDim.x);
 
   // ---- statistics: column j reduced by block j (and j + grid, ...), warp 0
@@ -156,7 +254,52 @@ __global__ void __launch_bounds__(512, 2) k_norm(const int* __restrict__ X, floa
   grid_barrier(&hdr->bar, 2 * gridDim.x);
 
   // ---- pass 2: Z = (x - mu) * inv_sd
-  if (active) {
+  if (ring) {
+    float mu[4] = {0.f, 0.f, 0.f, 0.f}, is[4] = {0.f, 0.f, 0.f, 0.f};
+    if (active)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        mu[w] = (float)((volatile double*)mean)[4 * g + w];
+        is[w] = (float)((volatile double*)inv)[4 * g + w];
+      }
+    float4* Z4 = reinterpret_cast<float4*>(Z);
+    it = it2;
+    for (long long c = 0; c < nch; ++c, ++it) {
+      const int st = (int)(it % NST);
+      mbar_wait(&rfull[st], (it / NST) & 1);
+      int4 v[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+      if (active) {
+        const int4* sl = ringp + (size_t)st * CH * G;
+        v[0] = sl[rl * G + g];
+        v[1] = sl[(rl + RL) * G + g];
+      }
+      __syncthreads();
+      if (t == 0 && c + NST < nch) issue(c + NST, st);
+      if (active) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float4 z;
+          z.x = ((float)v[u].x - mu[0]) * is[0];
+          z.y = ((float)v[u].y - mu[1]) * is[1];
+          z.z = ((float)v[u].z - mu[2]) * is[2];
+          z.w = ((float)v[u].w - mu[3]) * is[3];
+          Z4[(r0 + c * CH + rl + u * RL) * G + g] = z;
+        }
+      }
+    }
+    if (active) {
+      const int4* X4 = reinterpret_cast<const int4*>(X);
+      for (long long r = r0 + nch * CH + rl; r < r1; r += RL) {
+        int4 v = ldg_stream(X4 + r * G + g);
+        float4 z;
+        z.x = ((float)v.x - mu[0]) * is[0];
+        z.y = ((float)v.y - mu[1]) * is[1];
+        z.z = ((float)v.z - mu[2]) * is[2];
+        z.w = ((float)v.w - mu[3]) * is[3];
+        Z4[r * G + g] = z;
+      }
+    }
+  } else if (active) {
     if (vec) {
       float mu[4], is[4];
 #pragma unroll
@@ -285,35 +428,6 @@ __device__ __forceinline__ void mmul_generic(const T* __restrict__ A, const floa
 // shuffle per class.  Per 4 features a warp issues 1 + 10 LDS.128 for 40 FFMA.
 constexpr int kMmThreads = 128;
 constexpr int kMmRows = kMmThreads / 2;  // rows per tile
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-               "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          (unsigned)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-      : "memory");
-}
 
 template <typename T>
 __device__ __forceinline__ float4 as_f4(const T* p);
