@@ -392,3 +392,31 @@ def test_autotune_picks_the_faster_configuration():
     from oracle_checks import check_bs
     check_bs(p, p.seed)
     c.close()
+
+
+# ------------------------------------------------------------------ L2 norm ring
+@pytest.mark.parametrize("n,offset,grid", [(5_000_003, 0, 592), (5_000_003, 1, 592), (20_000_000, 0, 592),
+                                           (1_000_000, 0, 592), (4099, 0, 17), (1, 0, 1), (0, 0, 3),
+                                           (3_000_001, 2, 1024)])
+def test_l2norm_ring_matches_oracle(n, offset, grid):
+    """The product l2norm (cp.async.bulk ring, l2norm_ring.cuh): whole chunks
+    through the ring, the per-CTA tail, the unaligned (scalar) path, tiny and
+    empty vectors, a grid beyond one wave; ||v|| vs the fp64 sum (SUM node of
+    the HITS DAG, reading R-HITS), 1e-6 relative (fp32 squares per float4)."""
+    c = D.Context(device=0)
+    base = torch.rand(n + offset + 4, device="cuda") * 2 - 1
+    v = base[offset:offset + n]
+    out = torch.zeros(8 + 8 * 1024, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    V = c.register_tensor("v", v)
+    O = c.register_tensor("o", out)
+    c.launch("l2norm", grid, 256, V, O, n)
+    c.sync()
+    got = float(out[:4].view(torch.float32)[0])
+    ref = float(np.sqrt(np.sum(v.double().cpu().numpy() ** 2)))
+    assert abs(got - ref) <= 1e-6 * max(ref, 1e-30), (got, ref)
+    # reusable: the arrival counter is reset by the last CTA
+    c.launch("l2norm", grid, 256, V, O, n)
+    c.sync()
+    assert float(out[:4].view(torch.float32)[0]) == got
+    c.close()
