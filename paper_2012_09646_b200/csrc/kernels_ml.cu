@@ -441,12 +441,16 @@ __device__ __forceinline__ float4 as_f4<float>(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
 
-template <typename T>
+// RPT = rows per thread: 1 (128 threads per 64-row tile, the round-2 form)
+// or 2 (64 threads; thread pair k takes rows k and k + 32, so every weight
+// load feeds 2 x 4 x 2 FMAs instead of 4 x 2 and the shared-memory wavefronts
+// per FMA -- the kernel's bound, ncu -- drop to 28 / 80 from 24 / 40).
+template <typename T, int RPT = 1>
 __device__ __forceinline__ void mmul_tma10(const T* __restrict__ A, const float* __restrict__ sW,
                                            unsigned char* smem_tiles, uint64_t* full,
                                            const float* __restrict__ bias, float* __restrict__ out,
                                            long long N, int F) {
-  const int t = threadIdx.x, h = t & 1, row = t >> 1;
+  const int t = threadIdx.x, h = t & 1, row = t >> 1;  // rows row, row + 32 (RPT 2)
   const int half = F / 2;                     // features per thread (multiple of 2)
   const size_t tile_bytes = (size_t)kMmRows * F * 4;
   auto buf = [&](int st) { return reinterpret_cast<T*>(smem_tiles + st * tile_bytes); };
@@ -476,36 +480,56 @@ __device__ __forceinline__ void mmul_tma10(const T* __restrict__ A, const float*
     mbar_wait(&full[stage], (k >> 1) & 1);
     const long long r0 = tile * kMmRows;
     const int nrows = (int)min((long long)kMmRows, N - r0);
-    float acc[10];
+    float acc[RPT][10];
 #pragma unroll
-    for (int c = 0; c < 10; ++c) acc[c] = h == 0 ? b[c] : 0.f;
-    if (row < nrows) {
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+      for (int c = 0; c < 10; ++c) acc[q][c] = h == 0 ? b[c] : 0.f;
+    if (row < nrows) {  // (RPT 2: row + 32 may be past the tile's end; it then reads stale data, never stored)
       const T* xr = buf(stage) + (size_t)row * F + h * half;
       const float* wr = sW + h * half;
 #pragma unroll 5
       for (int f = 0; f < half; f += 4) {
-        const float4 x = as_f4<T>(xr + f);
+        float4 x[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) x[q] = as_f4<T>(xr + (size_t)q * 32 * F + f);
 #pragma unroll
         for (int c = 0; c < 10; ++c) {
           const float4 w = *reinterpret_cast<const float4*>(wr + c * F + f);
-          acc[c] = fmaf(x.x, w.x, acc[c]);
-          acc[c] = fmaf(x.y, w.y, acc[c]);
-          acc[c] = fmaf(x.z, w.z, acc[c]);
-          acc[c] = fmaf(x.w, w.w, acc[c]);
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            acc[q][c] = fmaf(x[q].x, w.x, acc[q][c]);
+            acc[q][c] = fmaf(x[q].y, w.y, acc[q][c]);
+            acc[q][c] = fmaf(x[q].z, w.z, acc[q][c]);
+            acc[q][c] = fmaf(x[q].w, w.w, acc[q][c]);
+          }
         }
       }
     }
 #pragma unroll
-    for (int c = 0; c < 10; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-    if (row < nrows) {
-      float2* o = reinterpret_cast<float2*>(out + (r0 + row) * 10);
-      if (h == 0) {
-        o[0] = make_float2(acc[0], acc[1]);
-        o[1] = make_float2(acc[2], acc[3]);
-      } else {
-        o[2] = make_float2(acc[4], acc[5]);
-        o[3] = make_float2(acc[6], acc[7]);
-        o[4] = make_float2(acc[8], acc[9]);
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+      for (int c = 0; c < 10; ++c) acc[q][c] += __shfl_xor_sync(0xffffffffu, acc[q][c], 1);
+    if (RPT == 1) {
+      if (row < nrows) {
+        float2* o = reinterpret_cast<float2*>(out + (r0 + row) * 10);
+        if (h == 0) {
+          o[0] = make_float2(acc[0][0], acc[0][1]);
+          o[1] = make_float2(acc[0][2], acc[0][3]);
+        } else {
+          o[2] = make_float2(acc[0][4], acc[0][5]);
+          o[3] = make_float2(acc[0][6], acc[0][7]);
+          o[4] = make_float2(acc[0][8], acc[0][9]);
+        }
+      }
+    } else {  // lane h = 0 stores row `row`, lane h = 1 row `row + 32`
+      const int rr = row + 32 * h;
+      if (rr < nrows) {
+        float2* o = reinterpret_cast<float2*>(out + (r0 + rr) * 10);
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+          o[c] = h == 0 ? make_float2(acc[0][2 * c], acc[0][2 * c + 1])
+                        : make_float2(acc[RPT - 1][2 * c], acc[RPT - 1][2 * c + 1]);
       }
     }
     __syncthreads();  // every thread is done with buf[stage]
@@ -528,11 +552,13 @@ __device__ __forceinline__ void mmul_body(const T* A, const float* W, const floa
   for (int i = threadIdx.x; i < C * F; i += blockDim.x) sW[i] = W[i];
   __syncthreads();
   const bool tma = C == 10 && (F & 3) == 0 && F <= 200 && ((F / 2) & 3) == 0 &&
-                   blockDim.x == kMmThreads && aligned16(A) && (((uintptr_t)out) & 7) == 0;
+                   (blockDim.x == kMmThreads || blockDim.x == kMmThreads / 2) && aligned16(A) &&
+                   (((uintptr_t)out) & 7) == 0;
   if (tma) {
     uint64_t* full = reinterpret_cast<uint64_t*>(sW + 10 * F);   // 10F*4 is a multiple of 16
     unsigned char* tiles = reinterpret_cast<unsigned char*>(full + 2);
-    mmul_tma10<T>(A, sW, tiles, full, bias, out, N, F);
+    if (blockDim.x == kMmThreads) mmul_tma10<T, 1>(A, sW, tiles, full, bias, out, N, F);
+    else mmul_tma10<T, 2>(A, sW, tiles, full, bias, out, N, F);
   } else if (C == 10) {
     mmul_rows<T, 10>(A, sW, bias, out, N, F);
   } else {
@@ -782,7 +808,8 @@ static const char* v_mmul(const LaunchCheck& L) {  // A, W, [prior,] out, N, F, 
   if (NB && !fits(L, 2, 4ull * C)) return "prior needs 4 C bytes";
   if (L.nthreads() > 256 || L.block[1] != 1 || L.block[2] != 1) return "1-D block of <= 256 threads";
   if (L.smem < 4u * C * F) return "dynamic shared memory below 4 C F bytes";
-  const bool tma = C == 10 && F % 4 == 0 && F <= 200 && (F / 2) % 4 == 0 && L.block[0] == kMmThreads &&
+  const bool tma = C == 10 && F % 4 == 0 && F <= 200 && (F / 2) % 4 == 0 &&
+                   (L.block[0] == kMmThreads || L.block[0] == kMmThreads / 2) &&
                    L.vals[0] % 16 == 0 && L.vals[2 + o] % 8 == 0;
   if (tma && L.smem < mmul_tma_smem(F)) return "TMA path needs mmul_tma_smem(F) bytes of shared memory";
   return nullptr;

@@ -129,7 +129,11 @@ class MLEnsemble(Program):
             P("norm", NORM_GRID, NORM_THREADS, [a["X"], a["Z"], a["stats"], n, f], smem=norm_smem(f)),
             P("nb_mmul", gm, MM_THREADS, [a["X"], a["theta"], a["prior"], a["r1"], n, f, c],
               smem=mm_smem),
-            P("rr_mmul", gm, MM_THREADS, [a["Z"], a["W"], a["r2"], n, f, c], smem=mm_smem),
+            # rr_mmul (fp32 rows): 64 threads, two rows per thread (kernels_ml.cu
+            # mmul_tma10<float, 2>: 1.36 vs 1.54 ms); nb_mmul keeps one row per
+            # thread (its int->fp32 conversions run on the XU pipe: 2.34 vs 1.58 ms
+            # with two rows per thread, tools/mmul_lab.py)
+            P("rr_mmul", gm, MM_THREADS // 2, [a["Z"], a["W"], a["r2"], n, f, c], smem=mm_smem),
             P("rowmax", gr, 256, [a["r1"], a["amax"], n, c]),
             P("lse", gr, 256, [a["r1"], a["amax"], a["l"], n, c]),
             P("addv", gr, 256, [a["r2"], a["b"], n, c]),

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--variants", default="ws")
+    ap.add_argument("--variants", default="")
     args = ap.parse_args()
     import torch
     import bench
@@ -37,8 +37,10 @@ def main():
     for kind, L0 in base.items():
         outn = "r1" if kind == "nb_mmul" else "r2"
         ref = None
-        for name in [kind] + [f"{kind}_{v}" for v in args.variants.split(",") if v]:
-            L = ctx.prepare(name, L0.grid.x, L0.block.x, list(L0.args_in) if hasattr(L0, "args_in") else
+        confs = [(kind, L0.block.x, L0.grid.x)] + [(kind, 64, g) for g in (296, 444)] + \
+                [(f"{kind}_{v}", L0.block.x, L0.grid.x) for v in args.variants.split(",") if v]
+        for name, blk, grd in confs:
+            L = ctx.prepare(name, grd, blk, list(L0.args_in) if hasattr(L0, "args_in") else
                             [p.a["X"], p.a["theta"], p.a["prior"], p.a["r1"], p.n, p.f, p.c] if kind == "nb_mmul" else
                             [p.a["Z"], p.a["W"], p.a["r2"], p.n, p.f, p.c], L0.smem)
             L.raw(st.cuda_stream)
@@ -56,7 +58,8 @@ def main():
             byts = (4.0 * p.f + 4.0 * p.c) * p.n
             r = {"ms": round(ms, 4), "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / peak, 3),
                  "bitwise_same_as_product": bool(torch.equal(ref, y))}
-            res[name] = r
+            r.update({"block": blk, "grid": grd})
+            res[f"{name}_b{blk}_g{grd}"] = r
             print(name, json.dumps(r), flush=True)
     if args.out:
         with open(args.out, "w") as f:
