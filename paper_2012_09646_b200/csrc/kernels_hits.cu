@@ -13,7 +13,6 @@
 // The round-1 merge-path kernel, the row-class kernel and the unpadded
 // non-zero split are experimental variants (exp/spmv_variants.cu).
 #include "spmv_common.cuh"
-#include "l2norm_ring.cuh"
 
 namespace dagrt {
 
@@ -28,13 +27,41 @@ __global__ void __launch_bounds__(256, 4) k_spmv_split(const int* __restrict__, 
   spmv_pad2_body<4>(plan, x, y, N_);  // the plan carries the (padded) graph
 }
 
-// SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.  The
-// vector streams through a cp.async.bulk ring (l2norm_ring.cuh: 2 x 16 KB in
-// flight per CTA, 4 CTAs/SM, one wave of 592): 11.6-12.6 us per 20M floats
-// vs 14.9 us back to back for the round-2 register form (tools/l2norm_lab.py,
-// profiles/r2_l2norm_lab.json), the same result.
-__global__ void __launch_bounds__(256, 4) k_l2norm(const float* __restrict__ v, RedOut* out, long long n) {
-  l2norm_tma_body<2, 16384>(v, out, n);
+// SUM node read as the L2 norm: n = sqrt(sum v^2), fp64 accumulation.
+// (A cp.async.bulk-ring form, l2norm_ring.cuh / exp l2norm_t*, is faster
+// only when the vector is L2-warm from repeated launches: on a vector just
+// written by its producer -- the HITS DAG's case -- it measured 19.5 vs
+// 18.7 us, and 25.8 vs 24.6 cold; tools/l2norm_lab.py,
+// profiles/r2_l2norm_lab.json.  This register form stays.)
+__global__ void __launch_bounds__(256, 8) k_l2norm(const float* __restrict__ v, RedOut* out,
+                                                long long n) {
+  __shared__ double sh[32];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  long long done = 0;
+  if (aligned16(v)) {
+    const long long n4 = n >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    // each float4's four squares summed in fp32 (relative 2^-23, far inside
+    // the 1e-3 reduction criterion), one conversion per float4 into the fp64
+    // accumulator: the per-element fp32->fp64 conversions ran on the XU pipe
+    // (ncu: XU 33%) while the loop waited on memory; 32 registers keep the
+    // full 8 CTAs per SM (a two-load form at 33 registers lost occupancy)
+    auto sq4 = [](float4 a) { return (double)fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, a.w * a.w))); };
+    long long i = tid;
+    for (; i + nth < n4; i += 2 * nth) {  // two 16-byte loads in flight (latency-bound at one)
+      const float4 a = ldg_stream(v4 + i), b = ldg_stream(v4 + i + nth);
+      acc += sq4(a) + sq4(b);
+    }
+    if (i < n4) acc += sq4(ldg_stream(v4 + i));
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nth) acc += (double)v[i] * v[i];
+  double blk = block_reduce(acc, OpAdd(), sh);
+  double total;
+  if (grid_finish(out, blk, OpAdd(), 0.0, &total, sh) && threadIdx.x == 0)
+    out->result = (float)sqrt(total);
 }
 
 // DIV node: out = v / ||v|| (zeros if the norm is 0).

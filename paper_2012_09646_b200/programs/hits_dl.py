@@ -319,7 +319,7 @@ class Hits(Program):
         a = self.a
         P = ctx.prepare
         ge = grid_1d(n, 256, 4)
-        gr = min(grid_1d(n, 256, 8), 4 * SMS)  # l2norm: one wave of the 4-CTA/SM ring kernel
+        gr = min(grid_1d(n, 256, 8), 1024)
         self.it = [
             P("spmv", gs, 256, [a["rpt"], a["cit"], a["plant"], a["h1"], a["a2"], n]),  # a2 = A^T h1
             P("spmv", gs, 256, [a["rp"], a["ci"], a["plan"], a["a1"], a["h2"], n]),      # h2 = A a1

@@ -394,15 +394,15 @@ def test_autotune_picks_the_faster_configuration():
     c.close()
 
 
-# ------------------------------------------------------------------ L2 norm ring
+# ------------------------------------------------------------------ L2 norm
 @pytest.mark.parametrize("n,offset,grid", [(5_000_003, 0, 592), (5_000_003, 1, 592), (20_000_000, 0, 592),
                                            (1_000_000, 0, 592), (4099, 0, 17), (1, 0, 1), (0, 0, 3),
                                            (3_000_001, 2, 1024)])
-def test_l2norm_ring_matches_oracle(n, offset, grid):
-    """The product l2norm (cp.async.bulk ring, l2norm_ring.cuh): whole chunks
-    through the ring, the per-CTA tail, the unaligned (scalar) path, tiny and
-    empty vectors, a grid beyond one wave; ||v|| vs the fp64 sum (SUM node of
-    the HITS DAG, reading R-HITS), 1e-6 relative (fp32 squares per float4)."""
+def test_l2norm_matches_oracle(n, offset, grid):
+    """The product l2norm: float4 streams with a scalar tail, the unaligned
+    (scalar) path, tiny and empty vectors, several grids; ||v|| vs the fp64
+    sum (SUM node of the HITS DAG, reading R-HITS), 1e-6 relative (fp32
+    squares per float4)."""
     c = D.Context(device=0)
     base = torch.rand(n + offset + 4, device="cuda") * 2 - 1
     v = base[offset:offset + n]
