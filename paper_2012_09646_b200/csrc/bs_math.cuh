@@ -493,7 +493,10 @@ __device__ __forceinline__ void bs_bulk_g2s(void* dst, const void* src, unsigned
                : "memory");
 }
 
-template <int OPT, int STAGES, class PR = BsPricerR2>
+// MODE (labs only): 0 = the kernel; 1 = compute only (every bulk copy reads
+// the CTA's first chunk -- L2-resident -- and nothing is stored unless a
+// price is NaN); 2 = memory only is BsPricerCopy (exp)
+template <int OPT, int STAGES, class PR = BsPricerR2, int MODE = 0>
 __device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, double* __restrict__ c, long long n,
                                              double r, double v, double t, double k) {
   constexpr int kChunk = 256 * OPT;  // options per chunk (blockDim.x == 256)
@@ -530,7 +533,7 @@ __device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, doubl
   if (tid == 0)
     for (int q = 0; q < STAGES; ++q) {
       const long long ch = blockIdx.x + q * G;
-      if (ch < nfullc) bs_bulk_g2s(ring[q], s + ch * kChunk, kChunk * 8, &full[q]);
+      if (ch < nfullc) bs_bulk_g2s(ring[q], s + (MODE == 1 ? (long long)blockIdx.x : ch) * kChunk, kChunk * 8, &full[q]);
     }
   int it = 0;
   for (long long ch = blockIdx.x; ch < nfullc; ch += G, ++it) {
@@ -546,12 +549,14 @@ __device__ __forceinline__ void bs2_tma_body(const double* __restrict__ s, doubl
     __syncthreads();  // every thread has its options: the stage may be refilled
     if (tid == 0 && ch + STAGES * G < nfullc) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bs_bulk_g2s(ring[st], s + (ch + STAGES * G) * kChunk, kChunk * 8, &full[st]);
+      bs_bulk_g2s(ring[st], s + (MODE == 1 ? (long long)blockIdx.x : ch + STAGES * G) * kChunk, kChunk * 8, &full[st]);
     }
     PR::template price<OPT>(a, o, C, T);
     double2* dst = reinterpret_cast<double2*>(c + ch * kChunk);
 #pragma unroll
-    for (int q = 0; q < OPT / 2; ++q) dst[tid + 256 * q] = make_double2(o[2 * q], o[2 * q + 1]);
+    for (int q = 0; q < OPT / 2; ++q)
+      if (MODE == 0 || o[2 * q] != o[2 * q] || o[2 * q + 1] != o[2 * q + 1])
+        dst[tid + 256 * q] = make_double2(o[2 * q], o[2 * q + 1]);
   }
   for (long long i = nfullc * kChunk + (long long)blockIdx.x * blockDim.x + tid; i < n; i += G * blockDim.x) {
     double a[2] = {s[i], 1.0}, o[2];

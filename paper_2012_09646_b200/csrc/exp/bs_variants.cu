@@ -117,6 +117,11 @@ struct BsPricerCopy {
     for (int w = 0; w < W; ++w) o[w] = s[w] * C.inv_k;
   }
 };
+// compute-only form of the product (MODE 1: L2-resident input chunk, no stores)
+__global__ void __launch_bounds__(256, 2) k_bs2x_o6s3b2(const double* __restrict__ s, double* __restrict__ c,
+                                                        long long n, double r, double v, double t, double k) {
+  bs2_tma_body<6, 3, BsPricerLean, 1>(s, c, n, r, v, t, k);
+}
 __global__ void __launch_bounds__(256, 2) k_bs2c_o6s3b2(const double* __restrict__ s, double* __restrict__ c,
                                                         long long n, double r, double v, double t, double k) {
   bs2_tma_body<6, 3, BsPricerCopy>(s, c, n, r, v, t, k);
@@ -393,6 +398,7 @@ static const Builtin kBsExp[] = {
     {"bs2m_o6s3b3", (const void*)k_bs2m_o6s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2m_o8s2b2", (const void*)k_bs2m_o8s2b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2m_o4s4b2", (const void*)k_bs2m_o4s4b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
+    {"bs2x_o6s3b2", (const void*)k_bs2x_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2c_o6s3b2", (const void*)k_bs2c_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o6s3b2", (const void*)k_bs2l_o6s3b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},
     {"bs2l_o4s3b3", (const void*)k_bs2l_o4s3b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE},

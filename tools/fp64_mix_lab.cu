@@ -22,6 +22,13 @@ __global__ void __launch_bounds__(256, 2) k_mix(double* out, int iters, double m
       if (V == 3) a[i] = a[i] + c;
       if (V == 4) asm volatile("rcp.approx.ftz.f64 %0, %0;" : "+d"(a[i]));
       if (V == 5) a[i] = a[i] + (double)(it + i);
+      if (V == 6 || V == 7) a[i] = fma(a[i], m, c);
+    }
+    if (V == 6) asm volatile("rcp.approx.ftz.f64 %0, %0;" : "+d"(a[it & 7]));  // 8 DFMA + 1 RCP64H
+    if (V == 7) {  // 8 DFMA + 1 fp32 MUFU.RCP on a value built from the double's bits
+      float f = __int_as_float((__double2hiint(a[it & 7]) << 3) | 1);
+      asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(f));
+      a[it & 7] += (double)__float_as_int(f) * 1e-30;
     }
   }
   double s = 0;
@@ -45,6 +52,8 @@ extern "C" int fp64_mix_lab(int v, int iters, float* ms) {
       case 3: k_mix<3><<<296, 256>>>(d, iters, 0.999999, 1e-7); break;
       case 4: k_mix<4><<<296, 256>>>(d, iters, 0.999999, 1e-7); break;
       case 5: k_mix<5><<<296, 256>>>(d, iters, 0.999999, 1e-7); break;
+      case 6: k_mix<6><<<296, 256>>>(d, iters, 0.999999, 1e-7); break;
+      case 7: k_mix<7><<<296, 256>>>(d, iters, 0.999999, 1e-7); break;
     }
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);

@@ -7,7 +7,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-NAMES = ["dfma_reg", "dfma_cbank", "dmul", "dadd", "mufu_rcp64h", "i2f_f64_plus_dadd"]
+NAMES = ["dfma_reg", "dfma_cbank", "dmul", "dadd", "mufu_rcp64h", "i2f_f64_plus_dadd",
+         "8dfma_plus_1rcp64h", "8dfma_plus_1rcp_f32"]
 
 
 def main():
@@ -23,6 +24,8 @@ def main():
         warps_per_smsp = 296 * 8 / (148 * 4)
         instr = iters * 8 * warps_per_smsp
         out[name] = {"rc": rc, "ms": ms.value, "cycles_per_warp_instr": ms.value * 1e-3 * mhz * 1e6 / instr}
+        if v >= 6:  # per iteration: 8 DFMA + 1 extra; report cycles per 8-DFMA group
+            out[name]["cycles_per_8dfma_group"] = ms.value * 1e-3 * mhz * 1e6 / (iters * warps_per_smsp)
     print(json.dumps(out, indent=1))
 
 
