@@ -11,8 +11,9 @@ assignment, event wiring, prefetch), the sm_100a kernels, and the host
 reads of the sinks.  By default ALL SIX benchmarks are measured (the suite,
 BASELINE.json configs[0..4] at full size); the printed headline is B&S
 (configs[1], 10 x 10M fp64 options) and the other five ride along under
-"suite".  ``--bench X`` measures one benchmark only (its line is the
-headline).
+"suite" (short DAGs -- VEC, the fp32 B&S -- over more steps, each
+entry stating its own).  ``--bench X`` measures one benchmark only (its line
+is the headline).
 
 Printed JSON line (rank 0), headline benchmark:
   value      ms per DAG, job aggregate = max-over-ranks timed ms / DAGs done by
@@ -29,7 +30,8 @@ Printed JSON line (rank 0), headline benchmark:
   contention_free  Fig. 9 estimate (L1195-1201): serial per-vertex times
              summed along the DAG's longest path
   roofline   dominant kernel, event-timed live on its own launch stream while
-             it runs alone (serial-sync region) and inside the DAG
+             it runs alone (each launch of one DAG run repeated back to back on
+             one stream) and inside the DAG; kernel_rooflines: every kernel
   cpu_baseline  the fp64 oracle on ONE pinned host core, bounded sample
 Under torchrun each rank runs independent DAG instances on its own GPU (no
 collective on the data path; NCCL only for the barrier and the max of the
