@@ -420,3 +420,39 @@ def test_l2norm_matches_oracle(n, offset, grid):
     c.sync()
     assert float(out[:4].view(torch.float32)[0]) == got
     c.close()
+
+
+# ------------------------------------------------------------------ IMG stencils, edge shapes
+@pytest.mark.parametrize("h,w,offset", [(1, 1, 0), (2, 3, 1), (3, 5, 0), (7, 4099, 1), (130, 1030, 0),
+                                        (64, 1000, 0), (65, 513, 3), (5, 4096, 0)])
+def test_img_stencils_edge_shapes(h, w, offset):
+    """The product blur (d = 1, 3, 5) and sobel (cp.async row ring, PF rows
+    ahead; img_stencil.cuh) on images shorter than the ring, narrower than a
+    tile, with W % 4 != 0 and misaligned bases (the 4-byte copy path), and
+    a ragged last tile; against the fp64 oracle (zero padding), fp32 1e-4
+    relative + 1e-6 absolute (reading R-IMG)."""
+    from oracle import img as oimg
+    c = D.Context(device=0)
+    rng = np.random.default_rng(h * 7919 + w)
+    img = rng.random((h, w))
+    base = torch.zeros(h * w + 8, device="cuda")
+    x = base[offset:offset + h * w]
+    x.copy_(torch.from_numpy(img.astype(np.float32).ravel()))
+    y = torch.full((h * w,), -7.0, device="cuda")
+    torch.cuda.synchronize()
+    X = c.register_tensor("x", x)
+    Y = c.register_tensor("y", y)
+    grid = (max(1, -(-w // 512)), max(1, -(-h // 64)))
+    xf = img.astype(np.float32).astype(np.float64)
+    for d, s2 in ((1, 1.0), (3, 0.1), (5, 10.0)):
+        c.launch("blur", grid, 128, X, Y, h, w, d, s2)
+        c.sync()
+        ref = oimg.blur(xf, d, s2)
+        got = y.cpu().numpy().reshape(h, w).astype(np.float64)
+        assert np.all(np.abs(got - ref) <= 1e-4 * np.abs(ref) + 1e-6), ("blur", d, float(np.abs(got - ref).max()))
+    c.launch("sobel", grid, 128, X, Y, h, w)
+    c.sync()
+    ref = oimg.sobel(xf)
+    got = y.cpu().numpy().reshape(h, w).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 1e-4 * np.abs(ref) + 1e-5), ("sobel", float(np.abs(got - ref).max()))
+    c.close()
