@@ -456,3 +456,37 @@ def test_img_stencils_edge_shapes(h, w, offset):
     got = y.cpu().numpy().reshape(h, w).astype(np.float64)
     assert np.all(np.abs(got - ref) <= 1e-4 * np.abs(ref) + 1e-5), ("sobel", float(np.abs(got - ref).max()))
     c.close()
+
+
+# ------------------------------------------------------------------ conv1, edge shapes
+@pytest.mark.parametrize("h,w,offset", [(1, 1, 0), (3, 5, 1), (33, 35, 0), (7, 4100, 0), (64, 130, 2),
+                                        (517, 2051, 1), (2, 2048, 0), (9, 16386, 0)])
+def test_conv1_edge_shapes(h, w, offset):
+    """The product conv1 (two output rows per iteration, warp-transposed
+    stores through shared memory, conv1.cuh) where warps run past the last
+    column pair, W1 is odd (half-pixel stores masked), H1 is odd (the second
+    row of the last pair absent), W % 4 != 0 / misaligned bases (scalar
+    loads), and a CTA row block wider than one; against the fp64 oracle
+    (R-DL: 3x3 stride 2 pad 1, ReLU), fp32 1e-4 relative + 1e-5 absolute."""
+    c = D.Context(device=0)
+    rng = np.random.default_rng(h * 131 + w)
+    img = rng.random((h, w))
+    wt = rng.uniform(-1, 1, size=72) / 3.0
+    base = torch.zeros(h * w + 8, device="cuda")
+    x = base[offset:offset + h * w]
+    x.copy_(torch.from_numpy(img.astype(np.float32).ravel()))
+    W1 = torch.from_numpy(wt.astype(np.float32)).cuda()
+    h1, w1 = (h + 1) // 2, (w + 1) // 2
+    y = torch.full((h1 * w1 * 8,), -7.0, device="cuda")
+    torch.cuda.synchronize()
+    X, Wt, Y = (c.register_tensor(k, t) for k, t in (("x", x), ("w", W1), ("y", y)))
+    pairs = (w1 + 1) // 2
+    grid = (max(1, -(-pairs // 256)), max(1, min((h1 + 1) // 2, 64)))
+    c.launch("conv1", grid, 256, X, Wt, Y, h, w)
+    c.sync()
+    ref = odl.conv3x3s2(img.astype(np.float32).astype(np.float64),
+                        wt.astype(np.float32).astype(np.float64).reshape(8, 3, 3, 1))
+    got = y.cpu().numpy().reshape(h1, w1, 8).astype(np.float64)
+    err = np.abs(got - ref) - (1e-4 * np.abs(ref) + 1e-5)
+    assert np.all(err <= 0), float(err.max())
+    c.close()
