@@ -490,3 +490,31 @@ def test_conv1_edge_shapes(h, w, offset):
     err = np.abs(got - ref) - (1e-4 * np.abs(ref) + 1e-5)
     assert np.all(err <= 0), float(err.max())
     c.close()
+
+
+# ------------------------------------------------------------------ NORM, feature counts and ragged rows
+@pytest.mark.parametrize("n,f", [(5923, 12), (1_000_003, 4), (777, 7), (40_000, 4), (3, 200), (20_011, 200)])
+def test_norm_feature_counts(n, f):
+    """The product NORM (cooperative; bulk-copy row ring when F % 4 == 0 and
+    a block holds whole 2 RL-row chunks, the register path otherwise) for
+    several F (ring slot sizes, G = F/4 column groups, the non-vector path
+    at F = 7), ragged rows per block and ring tails; exact statistics and Z
+    against the fp64 oracle (R-ML)."""
+    from paper_2012_09646_b200.programs.img_ml import NORM_GRID, NORM_THREADS, norm_smem, norm_stats_bytes
+    c = D.Context(device=0)
+    rng = np.random.default_rng(n + f)
+    X = rng.integers(-50, 50, size=(n, f), endpoint=True).astype(np.int32)
+    tX = torch.from_numpy(X.ravel()).cuda()
+    tZ = torch.zeros(n * f, device="cuda")
+    st = torch.zeros(norm_stats_bytes(f), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    A, Z, S = (c.register_tensor(k, t) for k, t in (("X", tX), ("Z", tZ), ("s", st)))
+    for _ in range(2):  # the grid barrier and exit counter reset for the next launch
+        c.launch("norm", NORM_GRID, NORM_THREADS, A, Z, S, n, f, smem=norm_smem(f))
+        c.sync()
+    mu, sd = oml.norm_stats(X)
+    stats = st[16:16 + 16 * f].view(torch.float64).cpu().numpy()
+    assert np.allclose(stats[:f], mu, rtol=1e-12, atol=1e-12)
+    assert np.allclose(1.0 / stats[f:], sd, rtol=1e-12)
+    assert_close(tZ.cpu().numpy().reshape(n, f), oml.apply_norm(X, mu, sd), "Z")
+    c.close()
