@@ -681,11 +681,20 @@ def main():
         return run_reference(args, rank, world)
 
     import torch
+    # functional checks of the multi-rank path on a one-GPU box only (never a
+    # measurement): DAGRT_BENCH_GPU pins every rank to one device and
+    # DAGRT_DIST_BACKEND=gloo replaces NCCL (which refuses two ranks per GPU)
+    if os.environ.get("DAGRT_BENCH_GPU") is not None:
+        local = int(os.environ["DAGRT_BENCH_GPU"])
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("DAGRT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
 
     peaks, _ = load_peaks()
