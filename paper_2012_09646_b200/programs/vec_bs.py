@@ -42,7 +42,9 @@ class Vec(Program):
         self.alloc_red("z")
         self.inputs, self.sinks = ["x", "y"], ["z"]
         a = self.a
-        g = grid_1d(n, 256, 8, waves=8)
+        # one wave of 4 CTAs per SM (27.0 vs 28.1 us per VEC DAG with the
+        # 489-CTA grid of 8 elements per thread, tools/vec_lab.py)
+        g = grid_1d(n, 256, 4, waves=4)
         self.L = [
             ctx.prepare("square", g, 256, [a["x"], a["x1"], n]),
             ctx.prepare("square", g, 256, [a["y"], a["y1"], n]),
