@@ -8,6 +8,196 @@
 
 namespace dagrt {
 
+// ---------------------------------------------------------------- B&S, round 2b
+// The lean pricer with two FP64 instructions and ~4 integer instructions
+// fewer per option (32 FP64 in the loop), tables from constant memory images:
+//   * d1 is carried SCALED, ds = kappa d1 with kappa = sqrt(64 / ln 2), so
+//     that -d1^2/2 = -ds^2 ln2/128: the exp's range reduction is
+//     t = fma(-ds, ds, 1.5 2^52) (n = round(-ds^2) from the exact square),
+//     rho = fma(ds, ds, n) -- the square is never formed on its own (3 FP64
+//     instead of h, t, nd, r2); kappa is folded into every constant that
+//     touches d1 (the log polynomial, the per-CTA table, d2's offset, the
+//     A&S p);
+//   * ln S: r = fma(S, inv[j] 2^-e, -1) with the 2^-e applied to the table
+//     value's exponent field in place (no mantissa extraction, no register
+//     copy), the polynomial pre-multiplied by kappa / (V sqrt T), and the
+//     per-CTA table TL[j] = -ln(inv[j]) kappa / (V sqrt T) + kappa mu
+//     interleaved with inv[j] (one 16-byte shared load per option):
+//     ds = fma(e, kappa ln2 / (V sqrt T), fma(p, r, TL[j])) -- 5 FP64 from S to
+//     ds instead of 6;
+//   * inv / -ln inv / 2^(j/128) are exact hex images (bs_tables.inc,
+//     tools/gen_bs_tables.py) copied into shared memory: no libdevice log /
+//     exp2 per CTA (~2.5% of the kernel's FP64 work).
+// Same formulas (SURVEY §8(c2) B&S: A&S 26.2.17, fp64), same truncation
+// errors as the lean pricer (log series to r^3 with |r| <= 2^-10, exp series
+// to rho^3 with |rho ln2/128| <= ln2/256).
+#include "bs_tables.inc"
+
+struct BsTabsM {
+  double2 lt[512];  // {inv[j], TL[j]}
+  double exp2j[128];
+};
+struct BsConstM {
+  double c1, c2, c3;  // g, -g/2, g/3 with g = kappa / (V sqrt T): kappa x the log series
+  double ln2g;        // ln2 g
+  double vk;          // kappa V sqrt T (ds2 = ds1 - vk)
+  double as;          // A&S p / kappa
+  double nkexp;       // -K e^{-RT}
+};
+enum { kcMRound, kcMNegC3, kcMC2, kcMNegC, kcMCount };
+static __constant__ double kBsM[kcMCount] = {
+    6755399441055744.0,          // 1.5 2^52
+    -2.6466421444330967e-08,     // -(ln2/128)^3 / 6
+    1.4662262387640423e-05,      // (ln2/128)^2 / 2
+    -0.0054152123481245725};     // -ln2/128
+constexpr double kKappa = 9.608979270291599;  // sqrt(64 / ln 2)
+
+// Per-CTA: constants and tables (TL depends on the launch's V, T, K, R).
+__device__ __forceinline__ void bs_m_setup(BsTabsM& T, BsConstM& C, double r, double v, double t, double k) {
+  const double vst = v * sqrt(t);
+  const double ivst = 1.0 / vst;
+  const double g = kKappa * ivst;
+  const double mu_lnk = ((r + 0.5 * v * v) * t - log(k)) * ivst;  // d1 = ln S / (V sqrt T) + mu_lnk
+  const double muk = kKappa * mu_lnk;
+  C.c1 = g;
+  C.c2 = -0.5 * g;
+  C.c3 = g / 3.0;
+  C.ln2g = 0.6931471805599453 * g;
+  C.vk = kKappa * vst;
+  C.as = kBsK[kcA] / kKappa;
+  C.nkexp = -k * exp(-r * t);
+  for (int j = threadIdx.x; j < 512; j += blockDim.x) {
+    const double2 q = __ldg(reinterpret_cast<const double2*>(kBsLogTab) + j);  // {inv, -ln inv}
+    T.lt[j] = make_double2(q.x, fma(q.y, g, muk));
+    if (j < 128) T.exp2j[j] = __ldg(kBsExp2Tab + j);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void bs_price_m(const double (&s)[W], double (&out)[W], const BsConstM& C,
+                                           const BsTabsM& T) {
+  const double B1 = kBsK[kcB1], B2 = kBsK[kcB2], B3 = kBsK[kcB3], B4 = kBsK[kcB4], B5 = kBsK[kcB5];
+  double d1[W], d2[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int hi = __double2hiint(s[w]);
+    const int eb = hi >> 20;                      // biased exponent (S positive)
+    const double2 q = T.lt[(hi >> 11) & 511];     // {inv[j], TL[j]}
+    // inv[j] 2^-(eb - 1023): the table value's exponent field lowered in place
+    const double ie = __hiloint2double(__double2hiint(q.x) - ((eb - 1023) << 20), __double2loint(q.x));
+    const double r = fma(s[w], ie, -1.0);         // = m inv[j] - 1, |r| <= 2^-10
+    double p = fma(r, C.c3, C.c2);
+    p = fma(r, p, C.c1);                           // g (1 - r/2 + r^2/3)
+    d1[w] = fma((double)(eb - 1023), C.ln2g, fma(p, r, q.y));  // kappa d1
+    d2[w] = d1[w] - C.vk;
+  }
+  double e1[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    // |ds| clamped to ~359 (ds^2 ln2/128 <= ~700: exp(-700) ~ 1e-304 stands
+    // for 0 and the 2^(n/128) scaling stays in the normal range)
+    const double dc = __hiloint2double(min(__double2hiint(d1[w]) & 0x7fffffff, 0x40767000), __double2loint(d1[w]));
+    const double t = fma(-dc, dc, kBsM[kcMRound]);
+    const int n = __double2loint(t);               // round(-ds^2)
+    const double rho = fma(dc, dc, t - kBsM[kcMRound]);  // ds^2 + n, |rho| <= 1/2
+    double p = fma(rho, kBsM[kcMNegC3], kBsM[kcMC2]);
+    p = fma(rho, p, kBsM[kcMNegC]);
+    p = fma(rho, p, 1.0);                          // e^{-rho ln2/128}
+    const double sc = T.exp2j[n & 127] * p;
+    e1[w] = __hiloint2double(__double2hiint(sc) + ((n >> 7) << 20), __double2loint(sc));  // e^{-d1^2/2}
+  }
+  double k1[W], k2[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const double D1 = fma(C.as, fabs(d1[w]), 1.0), D2 = fma(C.as, fabs(d2[w]), 1.0);
+    const double P = D1 * D2;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(P));
+    const double er = fma(-P, y, 1.0);
+    y = fma(y, er, y);
+    k1[w] = D2 * y;
+    k2[w] = D1 * y;
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    double q1 = fma(k1[w], B5, B4), q2 = fma(k2[w], B5, B4);
+    q1 = fma(k1[w], q1, B3);
+    q2 = fma(k2[w], q2, B3);
+    q1 = fma(k1[w], q1, B2);
+    q2 = fma(k2[w], q2, B2);
+    q1 = fma(k1[w], q1, B1);
+    q2 = fma(k2[w], q2, B1);
+    const bool u1 = __double2hiint(d1[w]) > 0, u2 = __double2hiint(d2[w]) > 0;
+    const double k1s = __hiloint2double(__double2hiint(k1[w]) ^ (u1 ? 0x80000000 : 0), __double2loint(k1[w]));
+    const double k2s = __hiloint2double(__double2hiint(k2[w]) ^ (u2 ? 0 : 0x80000000), __double2loint(k2[w]));
+    const double m = fma(q1, k1s, q2 * k2s);
+    const double u1d = __hiloint2double(u1 ? 0x3FF00000 : 0, 0);
+    const double nk = __hiloint2double(u2 ? __double2hiint(C.nkexp) : 0, u2 ? __double2loint(C.nkexp) : 0);
+    out[w] = fma(s[w], fma(e1[w], m, u1d), nk);
+  }
+}
+
+// The TMA-staged body for the round-2b pricer: the ring's first bulk copies
+// are issued BEFORE the per-CTA table setup, so the setup overlaps them.
+template <int OPT, int STAGES>
+__device__ __forceinline__ void bs2m_tma_body(const double* __restrict__ s, double* __restrict__ c, long long n,
+                                              double r, double v, double t, double k) {
+  constexpr int kChunk = 256 * OPT;
+  __shared__ BsTabsM T;
+  __shared__ __align__(128) double ring[STAGES][kChunk];
+  __shared__ uint64_t full[STAGES];
+  BsConstM C;
+  const int tid = threadIdx.x;
+  const bool fast = aligned16(s) && aligned16(c) && blockDim.x == 256;
+  const long long nfullc = fast ? n / kChunk : 0;
+  const long long G = gridDim.x;
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) bs_mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < STAGES; ++q) {
+      const long long ch = blockIdx.x + q * G;
+      if (ch < nfullc) bs_bulk_g2s(ring[q], s + ch * kChunk, kChunk * 8, &full[q]);
+    }
+  }
+  bs_m_setup(T, C, r, v, t, k);
+  __syncthreads();  // tables and barrier initialisation visible
+  int it = 0;
+  for (long long ch = blockIdx.x; ch < nfullc; ch += G, ++it) {
+    const int st = it % STAGES;
+    bs_mbar_wait(&full[st], (unsigned)((it / STAGES) & 1));
+    double a[OPT], o[OPT];
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) {
+      const double2 x = reinterpret_cast<const double2*>(ring[st])[tid + 256 * q];
+      a[2 * q] = x.x;
+      a[2 * q + 1] = x.y;
+    }
+    __syncthreads();
+    if (tid == 0 && ch + STAGES * G < nfullc) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bs_bulk_g2s(ring[st], s + (ch + STAGES * G) * kChunk, kChunk * 8, &full[st]);
+    }
+    bs_price_m<OPT>(a, o, C, T);
+    double2* dst = reinterpret_cast<double2*>(c + ch * kChunk);
+#pragma unroll
+    for (int q = 0; q < OPT / 2; ++q) dst[tid + 256 * q] = make_double2(o[2 * q], o[2 * q + 1]);
+  }
+  const long long stride = G * blockDim.x;
+  for (long long i = nfullc * kChunk + (long long)blockIdx.x * blockDim.x + tid; i < n; i += stride) {
+    double a[1] = {s[i]}, o[1];
+    bs_price_m<1>(a, o, C, T);
+    c[i] = o[0];
+  }
+}
+
+#define BS2M_VARIANT(NAME, OPT, STAGES, MINB)                                                      \
+  __global__ void __launch_bounds__(256, MINB) NAME(const double* __restrict__ s,                 \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs2m_tma_body<OPT, STAGES>(s, c, n, r, v, t, k);                                               \
+  }
+
+
 // Lean loop of bs_body_lean with the lockstep pricer: PAIRS double2 per
 // thread per group, priced W options at a time.
 template <int PAIRS, int W>
