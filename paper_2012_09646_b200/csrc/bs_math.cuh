@@ -447,16 +447,16 @@ __device__ __forceinline__ void bs_mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
 }
 
-template <int OPT, int STAGES>
+template <int OPT, int STAGES, class PR = BsPricerR2>
 __device__ __forceinline__ void bs3_ws_body(const double* __restrict__ s, double* __restrict__ c, long long n,
                                             double r, double v, double t, double k) {
   constexpr int kCons = 256;            // consumer threads (warps 0-7); warp 8 produces
   constexpr int kChunk = kCons * OPT;   // options per chunk
-  __shared__ BsTables T;
+  __shared__ typename PR::Tables T;
   extern __shared__ __align__(128) unsigned char bs3_dyn[];  // the ring: STAGES * kChunk * 8 bytes (dynamic)
   double(*ring)[kChunk] = reinterpret_cast<double(*)[kChunk]>(bs3_dyn);
   __shared__ uint64_t full[STAGES], empty[STAGES];
-  bs_tables_init(T);
+  PR::init(T);
   BsConst C;
   const double vst = v * sqrt(t);
   C.vst = vst;
@@ -465,13 +465,15 @@ __device__ __forceinline__ void bs3_ws_body(const double* __restrict__ s, double
   C.inv_k = 1.0 / k;
   C.c2 = exp(r * t) / k;
   C.kexp = k * exp(-r * t);
+  C.mu_lnk = C.mu_s - log(k) * C.inv_vst;
+  C.nkexp = -C.kexp;
   const int tid = threadIdx.x, warp = tid >> 5;
   unsigned dyn;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
   if (!(aligned16(s) && aligned16(c)) || blockDim.x != kCons + 32 || dyn < STAGES * kChunk * 8u) {
     for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < n; i += (long long)gridDim.x * blockDim.x) {
       double a[2] = {s[i], 1.0}, o[2];
-      bs_price_w<2>(a, o, C, T);
+      PR::template price<2>(a, o, C, T);
       c[i] = o[0];
     }
     return;
@@ -511,19 +513,25 @@ __device__ __forceinline__ void bs3_ws_body(const double* __restrict__ s, double
     }
     __syncwarp();
     if ((tid & 31) == 0) bs_mbar_arrive(&empty[st]);
-    bs_price_w<OPT>(a, o, C, T);
+    PR::template price<OPT>(a, o, C, T);
     double2* dst = reinterpret_cast<double2*>(c + ch * kChunk);
 #pragma unroll
     for (int q = 0; q < OPT / 2; ++q) dst[tid + kCons * q] = make_double2(o[2 * q], o[2 * q + 1]);
   }
   for (long long i = nfullc * kChunk + (long long)blockIdx.x * kCons + tid; i < n; i += G * kCons) {
     double a[2] = {s[i], 1.0}, o[2];
-    bs_price_w<2>(a, o, C, T);
+    PR::template price<2>(a, o, C, T);
     c[i] = o[0];
   }
 }
 // dynamic shared memory of a bs3 instance (its ring)
 #define BS3_SMEM(OPT, STAGES) ((STAGES) * 256 * (OPT) * 8)
+#define BS3L_VARIANT(NAME, OPT, STAGES, MINB)                                                     \
+  __global__ void __launch_bounds__(288, MINB) NAME(const double* __restrict__ s,                \
+                                                    double* __restrict__ c, long long n, double r, \
+                                                    double v, double t, double k) {                \
+    bs3_ws_body<OPT, STAGES, BsPricerLean>(s, c, n, r, v, t, k);                                   \
+  }
 #define BS3_VARIANT(NAME, OPT, STAGES, MINB)                                                      \
   __global__ void __launch_bounds__(288, MINB) NAME(const double* __restrict__ s,                \
                                                     double* __restrict__ c, long long n, double r, \

@@ -327,6 +327,11 @@ BS3_VARIANT(k_bs3_o6s6b2, 6, 6, 2)
 BS3_VARIANT(k_bs3_o4s8b2, 4, 8, 2)
 BS3_VARIANT(k_bs3_o4s6b3, 4, 6, 3)
 BS3_VARIANT(k_bs3_o2s8b4, 2, 8, 4)
+// warp-specialised ring with the lean (product) pricer: no CTA barrier per chunk
+BS3L_VARIANT(k_bs3_o6s4b2l, 6, 4, 2)
+BS3L_VARIANT(k_bs3_o6s6b2l, 6, 6, 2)
+BS3L_VARIANT(k_bs3_o4s6b3l, 4, 6, 3)
+BS3L_VARIANT(k_bs3_o4s8b2l, 4, 8, 2)
 
 // K3: c[i] = BlackScholesCall(s[i]; K, R, V, T), 128-bit fp64 loads/stores.
 // PAIRS double2 per thread per iteration (independent chains for the FP64
@@ -600,6 +605,10 @@ static const Builtin kBsExp[] = {
     {"bs3_o6s6b2", (const void*)k_bs3_o6s6b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(6, 6)},
     {"bs3_o4s8b2", (const void*)k_bs3_o4s8b2, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(4, 8)},
     {"bs3_o4s6b3", (const void*)k_bs3_o4s6b3, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(4, 6)},
+    {"bs3_o6s4b2l", (const void*)k_bs3_o6s4b2l, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(6, 4)},
+    {"bs3_o6s6b2l", (const void*)k_bs3_o6s6b2l, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(6, 6)},
+    {"bs3_o4s6b3l", (const void*)k_bs3_o4s6b3l, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(4, 6)},
+    {"bs3_o4s8b2l", (const void*)k_bs3_o4s8b2l, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(4, 8)},
     {"bs3_o2s8b4", (const void*)k_bs3_o2s8b4, "const ptr, out ptr, sint64, double, double, double, double", KF_NONE, BS3_SMEM(2, 8)},
 };
 DAGRT_REGISTER_EXP(kBsExp);

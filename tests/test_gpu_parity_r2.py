@@ -253,7 +253,7 @@ def test_bs_limits(svals):
 
 @pytest.mark.parametrize("kernel", ["bs", "bs2_p3w2b2", "bs2_p2w4b2", "bs2t_o4s4b2", "bs2t_o6s3b2", "bs3_o6s4b2",
                                     "bs3_o4s8b2", "bs2l_o6s3b2", "bs2l_o4s3b3", "bs2m_o6s3b2", "bs2m_o4s3b3",
-                                    "bs2m_o6s3b3", "bs2m_o8s2b2", "bs2m_o4s4b2"])
+                                    "bs2m_o6s3b3", "bs2m_o8s2b2", "bs2m_o4s4b2", "bs3_o6s4b2l", "bs3_o4s6b3l"])
 def test_bs_kernels_limits_and_range(exp, kernel):
     """Every B&S pricing kernel on the limit values plus a dense S sweep over
     [1e-3, 1e4] (log-spaced): deep out of / in the money, d ~ 0, the exp's

@@ -33,7 +33,8 @@ def main():
                         ("bs3_o4s6b3", 3), ("bs3_o2s8b4", 4), ("bs2l_o6s3b2", 2), ("bs2l_o4s3b3", 3),
                         ("bs2l_o6s3b3", 3), ("bs2l_o6s2b3", 3), ("bs2l_o8s2b2", 2),
                         ("bs2m_o6s3b2", 2), ("bs2m_o4s3b3", 3), ("bs2m_o6s3b3", 3), ("bs2m_o8s2b2", 2),
-                        ("bs2m_o4s4b2", 2), ("bs2c_o6s3b2", 2), ("bs2x_o6s3b2", 2)):
+                        ("bs2m_o4s4b2", 2), ("bs2c_o6s3b2", 2), ("bs2x_o6s3b2", 2),
+                        ("bs3_o6s4b2l", 2), ("bs3_o6s6b2l", 2), ("bs3_o4s6b3l", 3), ("bs3_o4s8b2l", 2)):
         if sel and name not in sel:
             continue
         from paper_2012_09646_b200.programs.vec_bs import bs_launch
